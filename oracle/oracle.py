@@ -1,0 +1,300 @@
+"""ctypes bindings for the parity checkers -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` leg may import this module, and only as the checker or
+the CPU baseline.  The product package never imports it.
+
+Two checkers share one Python interface:
+
+* ``Oracle("port")``      -> oracle/liboracle.so, the plain-C restatement
+  (fppm_oracle.c) of the reference path;
+* ``Oracle("reference")`` -> oracle/_ref/libfppm_ref.so, the reference's own
+  proj/core sources compiled unmodified plus the extern "C" driver
+  oracle/ref_driver.cpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PORT = os.path.join(HERE, "liboracle.so")
+LIB_REF = os.path.join(HERE, "_ref", "libfppm_ref.so")
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_u32p = C.POINTER(C.c_uint32)
+_u64p = C.POINTER(C.c_uint64)
+_u8p = C.POINTER(C.c_uint8)
+_ip = C.POINTER(C.c_int)
+
+
+def _ptr(a, t):
+    if a is None:
+        return C.cast(None, t)
+    return a.ctypes.data_as(t)
+
+
+class Config(C.Structure):
+    """Mirror of orc_config / RefConfig."""
+
+    _fields_ = [
+        ("n_annuli", C.c_int), ("n_sectors", C.c_int), ("alpha_f", C.c_double),
+        ("channels", C.c_int), ("override_decision", C.c_int),
+        ("k", C.c_double), ("alpha", C.c_double), ("r_min_base", C.c_double),
+        ("initial_radius", C.c_double), ("samples_per_iteration", C.c_uint64),
+        ("max_depth", C.c_uint32), ("normal_guard_cos", C.c_double),
+        ("threads", C.c_int),
+    ]
+
+
+class IterOut(C.Structure):
+    _fields_ = [
+        ("radius", _dp), ("gather_r", _dp), ("t", _u64p), ("tested", _u8p),
+        ("rejected", _u8p), ("statistic", _dp), ("critical", _dp),
+        ("flux", _dp), ("radiance", _dp), ("accepted", _u64p),
+        ("stat_count", _u64p), ("stat_sum", _dp), ("stat_sum_sq", _dp),
+    ]
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+class InvalidArgument(OracleError, ValueError):
+    pass
+
+
+class DomainError(OracleError, ArithmeticError):
+    pass
+
+
+def _raise(code):
+    if code == 1:
+        raise InvalidArgument("invalid argument")
+    if code == 2:
+        raise DomainError("domain error")
+    if code:
+        raise OracleError(f"oracle error {code}")
+
+
+class Oracle:
+    """Uniform Python view over liboracle.so ('port') or _ref ('reference')."""
+
+    def __init__(self, kind: str = "port"):
+        self.kind = kind
+        path = LIB_PORT if kind == "port" else LIB_REF
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing; run `make -C oracle`")
+        self.lib = L = C.CDLL(path)
+        self.p = "orc_" if kind == "port" else "ref_"
+        p = self.p
+        def fn(name, res, args):
+            f = getattr(L, p + name)
+            f.restype = res
+            f.argtypes = args
+            return f
+        self._sector = fn("sector_index", C.c_int, [C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, _ip])
+        self._sched = fn("schedule_radius", C.c_double, [C.c_double, C.c_double, C.c_uint64])
+        self._fq = fn("f_quantile", C.c_double, [C.c_double, C.c_double, C.c_double, _ip])
+        self._cq = fn("chi2_quantile", C.c_double, [C.c_double, C.c_double, _ip])
+        self._fcdf = fn("f_cdf", C.c_double, [C.c_double, C.c_double, C.c_double, _ip])
+        self._ccdf = fn("chi2_cdf", C.c_double, [C.c_double, C.c_double, _ip])
+        self._ib = fn("reg_inc_beta", C.c_double, [C.c_double, C.c_double, C.c_double, _ip])
+        self._lg = fn("reg_lower_gamma", C.c_double, [C.c_double, C.c_double, _ip])
+        self._fs = fn("f_statistic", C.c_double, [_u64p, _dp, _dp, C.c_int, C.c_uint64, _ip])
+        self._c2s = fn("chi2_statistic", C.c_double, [_u64p, C.c_int, _ip])
+        self._frame = fn("build_frame", None, [_dp, _dp, _dp])
+        self._gb = fn("grid_build", C.c_void_p, [_dp, C.c_size_t, C.c_double, _ip])
+        self._gf = fn("grid_free", None, [C.c_void_p])
+        self._gc = fn("grid_cell_count", C.c_size_t, [C.c_void_p])
+        self._ge = fn("grid_export", None, [C.c_void_p, _u64p, _u32p, _u32p, _u32p])
+        self._gq = fn("grid_query_ball", C.c_size_t, [C.c_void_p, _dp, C.c_double, _u32p, C.c_size_t, _ip])
+        self._sc = fn("session_create", C.c_void_p, [C.POINTER(Config), C.c_size_t, _dp, _dp, _dp, _dp, _dp, _u32p, _u8p, _ip])
+        self._sf = fn("session_free", None, [C.c_void_p])
+        self._smr = fn("session_max_radius", C.c_double, [C.c_void_p])
+        if kind == "port":
+            self._si = fn("session_iterate", C.c_int, [C.c_void_p, C.c_uint64, _fp, _fp, _fp, _fp, _u32p, C.c_size_t, C.c_double, _u32p, C.c_size_t, C.POINTER(IterOut)])
+            self._gen = fn("gen_photons", None, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _fp, _fp, _fp, _fp, _u32p])
+            self._ghp = fn("gen_raster_hitpoints", None, [C.c_uint32, _dp, _dp, _dp, _dp, _dp, _u32p])
+            self._pcg = fn("pcg32_at", C.c_uint32, [C.c_uint64, C.c_uint64, C.c_uint64])
+            self._sincos = fn("dm_sincos2pi", None, [C.c_double, _dp, _dp])
+            self._log = fn("dm_log", C.c_double, [C.c_double])
+            self._exp = fn("dm_exp", C.c_double, [C.c_double])
+            self._fcrit = fn("f_critical", C.c_double, [C.c_int64, C.c_int64, C.c_double])
+        else:
+            self._si = fn("session_iterate", C.c_int, [C.c_void_p, C.c_uint64, _fp, _fp, _fp, _fp, _u32p, C.c_size_t, C.c_double, _u32p, C.c_size_t, C.POINTER(IterOut), _dp, _dp])
+            self._anova = fn("anova_f_test", None, [_u64p, _dp, _dp, C.c_int, C.c_uint64, C.c_double, _dp, _ip])
+            self._hw = fn("hardware_threads", C.c_uint, [])
+
+    # ---------------------------------------------------------- scalars
+    def _call(self, f, *a):
+        err = C.c_int(0)
+        v = f(*a, C.byref(err))
+        _raise(err.value)
+        return v
+
+    def sector_index(self, u, v, r, na, ns):
+        return self._call(self._sector, u, v, r, na, ns)
+
+    def schedule_radius(self, base, alpha, i):
+        return self._sched(base, alpha, i)
+
+    def f_quantile(self, p, d1, d2):
+        return self._call(self._fq, p, d1, d2)
+
+    def chi2_quantile(self, p, df):
+        return self._call(self._cq, p, df)
+
+    def f_cdf(self, x, d1, d2):
+        return self._call(self._fcdf, x, d1, d2)
+
+    def chi2_cdf(self, x, df):
+        return self._call(self._ccdf, x, df)
+
+    def reg_inc_beta(self, a, b, x):
+        return self._call(self._ib, a, b, x)
+
+    def reg_lower_gamma(self, a, x):
+        return self._call(self._lg, a, x)
+
+    def f_statistic(self, count, s, q, m):
+        s = np.ascontiguousarray(s, np.float64)
+        q = np.ascontiguousarray(q, np.float64)
+        c = np.ascontiguousarray(count if count is not None else np.zeros(len(s)), np.uint64)
+        return self._call(self._fs, _ptr(c, _u64p), _ptr(s, _dp), _ptr(q, _dp), len(s), m)
+
+    def chi2_statistic(self, counts):
+        c = np.ascontiguousarray(counts, np.uint64)
+        return self._call(self._c2s, _ptr(c, _u64p), len(c))
+
+    def build_frame(self, n):
+        n = np.ascontiguousarray(n, np.float64)
+        u = np.zeros(3); v = np.zeros(3)
+        self._frame(_ptr(n, _dp), _ptr(u, _dp), _ptr(v, _dp))
+        return u, v
+
+    # ---------------------------------------------------------- grid
+    def grid_build(self, pos, cell):
+        pos = np.ascontiguousarray(pos, np.float64).reshape(-1, 3)
+        err = C.c_int(0)
+        h = self._gb(_ptr(pos, _dp), len(pos), cell, C.byref(err))
+        _raise(err.value)
+        return _Grid(self, h, len(pos))
+
+    # ---------------------------------------------------------- session
+    def session(self, cfg: dict, hit):
+        return _Session(self, cfg, hit)
+
+    # ---------------------------------------------------------- generators (port only)
+    def gen_photons(self, workload, seed, iteration, begin, count):
+        pos = np.zeros((count, 3), np.float32); nrm = np.zeros((count, 3), np.float32)
+        wi = np.zeros((count, 3), np.float32); pw = np.zeros((count, 3), np.float32)
+        depth = np.zeros(count, np.uint32)
+        self._gen(workload, seed, iteration, begin, count, _ptr(pos, _fp), _ptr(nrm, _fp),
+                  _ptr(wi, _fp), _ptr(pw, _fp), _ptr(depth, _u32p))
+        return dict(pos=pos, nrm=nrm, wi=wi, pow=pw, depth=depth)
+
+    def gen_raster_hitpoints(self, W):
+        H = W * W
+        a = {k: np.zeros((H, 3), np.float64) for k in ("pos", "nrm", "wo", "thr", "alb")}
+        a["eye_depth"] = np.zeros(H, np.uint32)
+        self._ghp(W, *[_ptr(a[k], _dp) for k in ("pos", "nrm", "wo", "thr", "alb")],
+                  _ptr(a["eye_depth"], _u32p))
+        return a
+
+
+class _Grid:
+    def __init__(self, o, h, n):
+        self.o, self.h, self.n = o, h, n
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o._gf(self.h)
+            self.h = None
+
+    def export(self):
+        nc = self.o._gc(self.h)
+        keys = np.zeros(nc, np.uint64); b = np.zeros(nc, np.uint32)
+        e = np.zeros(nc, np.uint32); order = np.zeros(self.n, np.uint32)
+        self.o._ge(self.h, _ptr(keys, _u64p), _ptr(b, _u32p), _ptr(e, _u32p), _ptr(order, _u32p))
+        return keys, b, e, order
+
+    def query_ball(self, c, r):
+        c = np.ascontiguousarray(c, np.float64)
+        cap = max(self.n, 1)
+        out = np.zeros(cap, np.uint32)
+        err = C.c_int(0)
+        k = self.o._gq(self.h, _ptr(c, _dp), r, _ptr(out, _u32p), cap, C.byref(err))
+        _raise(err.value)
+        return out[:k].copy()
+
+
+OUT_FIELDS = ("radius", "gather_r", "t", "tested", "rejected", "statistic",
+              "critical", "flux", "radiance", "accepted", "stat_count",
+              "stat_sum", "stat_sum_sq")
+
+
+class _Session:
+    def __init__(self, o, cfg, hit):
+        self.o = o
+        c = Config()
+        defaults = dict(n_annuli=2, n_sectors=6, alpha_f=0.01, channels=1,
+                        override_decision=0, k=0.7, alpha=0.75, r_min_base=0.0,
+                        initial_radius=0.02, samples_per_iteration=1, max_depth=10,
+                        normal_guard_cos=0.86602540378443865, threads=1)
+        defaults.update(cfg)
+        for k_, v in defaults.items():
+            setattr(c, k_, v)
+        self.cfg = c
+        self.G = c.n_annuli * c.n_sectors
+        self.C = c.channels
+        self.H = len(hit["pos"])
+        self._keep = {k: np.ascontiguousarray(hit[k], np.float64) for k in ("pos", "nrm", "wo", "thr", "alb")}
+        self._keep["eye_depth"] = np.ascontiguousarray(hit["eye_depth"], np.uint32)
+        g = hit.get("gathered")
+        self._keep["gathered"] = None if g is None else np.ascontiguousarray(g, np.uint8)
+        err = C.c_int(0)
+        kp = self._keep
+        self.h = o._sc(C.byref(c), self.H, *[_ptr(kp[k], _dp) for k in ("pos", "nrm", "wo", "thr", "alb")],
+                       _ptr(kp["eye_depth"], _u32p), _ptr(kp["gathered"], _u8p), C.byref(err))
+        _raise(err.value)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o._sf(self.h)
+            self.h = None
+
+    def max_radius(self):
+        return self.o._smr(self.h)
+
+    def iterate(self, iteration, ph, cell=0.0, subset=None):
+        n = self.H if subset is None else len(subset)
+        CG = self.G * self.C
+        out = dict(radius=np.zeros(n), gather_r=np.zeros(n), t=np.zeros(n, np.uint64),
+                   tested=np.zeros(n, np.uint8), rejected=np.zeros(n, np.uint8),
+                   statistic=np.zeros(n), critical=np.zeros(n), flux=np.zeros((n, 3)),
+                   radiance=np.zeros((n, 3)), accepted=np.zeros(n, np.uint64),
+                   stat_count=np.zeros((n, CG), np.uint64), stat_sum=np.zeros((n, CG)),
+                   stat_sum_sq=np.zeros((n, CG)))
+        io = IterOut()
+        for k in OUT_FIELDS:
+            t = IterOut._fields_[[f[0] for f in IterOut._fields_].index(k)][1]
+            setattr(io, k, _ptr(out[k], t))
+        arrs = [np.ascontiguousarray(ph[k], np.float32) for k in ("pos", "nrm", "wi", "pow")]
+        depth = np.ascontiguousarray(ph["depth"], np.uint32)
+        sub = None if subset is None else np.ascontiguousarray(subset, np.uint32)
+        N = len(depth)
+        args = [self.h, iteration, *[_ptr(a, _fp) for a in arrs], _ptr(depth, _u32p), N,
+                float(cell), _ptr(sub, _u32p), 0 if sub is None else len(sub), C.byref(io)]
+        if self.o.kind == "port":
+            rc = self.o._si(*args)
+            times = None
+        else:
+            gs, ts = C.c_double(0), C.c_double(0)
+            rc = self.o._si(*args, C.byref(gs), C.byref(ts))
+            times = (gs.value, ts.value)
+        _raise(rc)
+        out["times"] = times
+        return out

@@ -1,0 +1,386 @@
+// ref_driver.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A thin extern "C" driver over the reference's OWN public C++ API
+// (fppm::PhotonGrid, fppm::GatherRegion, fppm::Bsdf, the stat/special
+// functions), compiled together with the unmodified reference sources from
+// /root/reference/proj/core/src into oracle/_ref/libfppm_ref.so by
+// oracle/Makefile.  It is the "reference" CPU arm of bench.py and the pin for
+// the C restatement in fppm_oracle.c.
+//
+// The only reference logic restated here is Renderer::gather_disk's filter
+// chain (proj/core/src/integrator.cpp:388-402) and the pixel_pm callback
+// (:445-451, :452-455, :476-489), which live in a private class of
+// integrator.cpp and cannot be called from outside.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+// Read-only access to PhotonGrid's private order_/keys_/cells_ so grid
+// parity can be checked on keys and permutation, not only on query results.
+#define private public
+#include "fppm/photon_map.hpp"
+#undef private
+#include "fppm/bsdf.hpp"
+#include "fppm/frame.hpp"
+#include "fppm/gather.hpp"
+#include "fppm/sampling.hpp"
+#include "fppm/special_functions.hpp"
+#include "fppm/stat_tests.hpp"
+
+using namespace fppm;
+
+namespace {
+constexpr double kNormalGuardCos = 0.86602540378443865; // integrator.cpp:47
+
+template <typename F>
+double guarded(int* err, F&& f) {
+  try {
+    return f();
+  } catch (const std::invalid_argument&) {
+    if (err) *err = 1;
+  } catch (const std::domain_error&) {
+    if (err) *err = 2;
+  } catch (...) {
+    if (err) *err = 9;
+  }
+  return 0.0;
+}
+
+// Same static split as parallel_ranges (integrator.cpp:55-70).
+template <typename F>
+void parallel_ranges(int threads, std::size_t count, F&& fn) {
+  const std::size_t t =
+      std::min<std::size_t>(std::max(threads, 1), std::max<std::size_t>(count, 1));
+  if (t <= 1) {
+    fn(std::size_t{0}, count);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (std::size_t w = 1; w < t; ++w)
+    pool.emplace_back([&fn, w, t, count] { fn(count * w / t, count * (w + 1) / t); });
+  fn(std::size_t{0}, count / t);
+  for (auto& th : pool) th.join();
+}
+} // namespace
+
+extern "C" {
+
+// ---------------------------------------------------------------- scalars
+int ref_sector_index(double u, double v, double r, int na, int ns, int* err) {
+  return static_cast<int>(guarded(err, [&] {
+    return static_cast<double>(sector_index(UnifiedPoint{u, v}, r, na, ns));
+  }));
+}
+double ref_schedule_radius(double base, double alpha, uint64_t i) {
+  return schedule_radius(base, alpha, i);
+}
+double ref_f_quantile(double p, double d1, double d2, int* err) {
+  return guarded(err, [&] { return f_quantile(p, d1, d2); });
+}
+double ref_chi2_quantile(double p, double df, int* err) {
+  return guarded(err, [&] { return chi2_quantile(p, df); });
+}
+double ref_f_cdf(double x, double d1, double d2, int* err) {
+  return guarded(err, [&] { return f_cdf(x, d1, d2); });
+}
+double ref_chi2_cdf(double x, double df, int* err) {
+  return guarded(err, [&] { return chi2_cdf(x, df); });
+}
+double ref_reg_inc_beta(double a, double b, double x, int* err) {
+  return guarded(err, [&] { return reg_inc_beta(a, b, x); });
+}
+double ref_reg_lower_gamma(double a, double x, int* err) {
+  return guarded(err, [&] { return reg_lower_gamma(a, x); });
+}
+static std::vector<SectorStats> make_stats(const uint64_t* c, const double* s,
+                                           const double* q, int n) {
+  std::vector<SectorStats> v(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) v[i] = SectorStats{c ? c[i] : 0, s[i], q[i]};
+  return v;
+}
+double ref_f_statistic(const uint64_t* c, const double* s, const double* q, int n,
+                       uint64_t m, int* err) {
+  return guarded(err, [&] { return f_statistic(make_stats(c, s, q, n), m); });
+}
+// out: [f, critical, reject, d1, d2]
+void ref_anova_f_test(const uint64_t* c, const double* s, const double* q, int n,
+                      uint64_t m, double alpha, double* out, int* err) {
+  guarded(err, [&] {
+    const FTestResult r = anova_f_test(make_stats(c, s, q, n), m, alpha);
+    out[0] = r.f;
+    out[1] = r.critical;
+    out[2] = r.reject ? 1.0 : 0.0;
+    out[3] = static_cast<double>(r.d1);
+    out[4] = static_cast<double>(r.d2);
+    return 0.0;
+  });
+}
+double ref_chi2_statistic(const uint64_t* c, int n, int* err) {
+  return guarded(err, [&] {
+    return chi2_statistic(std::span<const std::uint64_t>(c, static_cast<std::size_t>(n)));
+  });
+}
+void ref_build_frame(const double* n, double* u, double* v) {
+  const TangentFrame f = build_tangent_frame(Normal3{n[0], n[1], n[2]});
+  u[0] = f.u.x; u[1] = f.u.y; u[2] = f.u.z;
+  v[0] = f.v.x; v[1] = f.v.y; v[2] = f.v.z;
+}
+
+// ---------------------------------------------------------------- grid
+void* ref_grid_build(const double* pos, size_t n, double cell, int* err) {
+  try {
+    std::vector<LightVertex> vs(n);
+    for (size_t i = 0; i < n; ++i) {
+      vs[i].position = Point3{pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+      vs[i].path_index = static_cast<uint32_t>(i);
+    }
+    return new PhotonGrid(std::move(vs), cell);
+  } catch (const std::invalid_argument&) {
+    if (err) *err = 1;
+  }
+  return nullptr;
+}
+void ref_grid_free(void* g) { delete static_cast<PhotonGrid*>(g); }
+size_t ref_grid_cell_count(void* g) { return static_cast<PhotonGrid*>(g)->keys_.size(); }
+void ref_grid_export(void* gp, uint64_t* keys, uint32_t* begin, uint32_t* end,
+                     uint32_t* order) {
+  const PhotonGrid* g = static_cast<PhotonGrid*>(gp);
+  for (size_t i = 0; i < g->keys_.size(); ++i) {
+    if (keys) keys[i] = g->keys_[i];
+    if (begin) begin[i] = g->cells_[i].begin;
+    if (end) end[i] = g->cells_[i].end;
+  }
+  if (order) std::memcpy(order, g->order_.data(), sizeof(uint32_t) * g->order_.size());
+}
+size_t ref_grid_query_ball(void* gp, const double* c, double r, uint32_t* out,
+                           size_t cap, int* err) {
+  std::vector<uint32_t> found;
+  try {
+    static_cast<PhotonGrid*>(gp)->query_ball(Point3{c[0], c[1], c[2]}, r, found);
+  } catch (const std::invalid_argument&) {
+    if (err) *err = 1;
+    return 0;
+  }
+  for (size_t i = 0; i < found.size() && i < cap; ++i) out[i] = found[i];
+  return found.size();
+}
+
+// ---------------------------------------------------------------- session
+struct RefConfig { // identical layout to orc_config (fppm_oracle.h)
+  int n_annuli, n_sectors;
+  double alpha_f;
+  int channels;
+  int override_decision;
+  double k, alpha, r_min_base;
+  double initial_radius;
+  uint64_t samples_per_iteration;
+  uint32_t max_depth;
+  double normal_guard_cos;
+  int threads;
+};
+
+struct RefIterOut { // identical layout to orc_iter_out
+  double* radius;
+  double* gather_r;
+  uint64_t* t;
+  uint8_t* tested;
+  uint8_t* rejected;
+  double* statistic;
+  double* critical;
+  double* flux;
+  double* radiance;
+  uint64_t* accepted;
+  uint64_t* stat_count;
+  double* stat_sum;
+  double* stat_sum_sq;
+};
+
+struct RefSession {
+  RefConfig cfg;
+  std::vector<GatherRegion> regions;
+  std::vector<Point3> pos;
+  std::vector<Normal3> nrm;
+  std::vector<Vec3> wo;
+  std::vector<Rgb> thr;
+  std::vector<Material> mat;
+  std::vector<uint32_t> eye_depth;
+  std::vector<uint8_t> gathered;
+};
+
+void* ref_session_create(const RefConfig* cfg, size_t H, const double* pos,
+                         const double* nrm, const double* wo, const double* thr,
+                         const double* alb, const uint32_t* eye_depth,
+                         const uint8_t* gathered, int* err) {
+  try {
+    auto* s = new RefSession;
+    s->cfg = *cfg;
+    TestConfig test;
+    test.n_annuli = cfg->n_annuli;
+    test.n_sectors = cfg->n_sectors;
+    test.alpha_f = cfg->alpha_f;
+    test.channels = cfg->channels == 3 ? TestChannels::rgb : TestChannels::luminance;
+    test.override_decision = cfg->override_decision == 1   ? TestOverride::always_reject
+                             : cfg->override_decision == 2 ? TestOverride::never_reject
+                                                           : TestOverride::none;
+    const RadiusSchedule sched{cfg->k, cfg->alpha, cfg->r_min_base};
+    s->regions.assign(H, GatherRegion(test, sched, cfg->initial_radius));
+    for (size_t h = 0; h < H; ++h) {
+      s->pos.push_back({pos[3 * h], pos[3 * h + 1], pos[3 * h + 2]});
+      s->nrm.push_back({nrm[3 * h], nrm[3 * h + 1], nrm[3 * h + 2]});
+      s->wo.push_back({wo[3 * h], wo[3 * h + 1], wo[3 * h + 2]});
+      s->thr.push_back({thr[3 * h], thr[3 * h + 1], thr[3 * h + 2]});
+      Material m;
+      m.kind = MaterialKind::lambertian;
+      m.albedo = Rgb{alb[3 * h], alb[3 * h + 1], alb[3 * h + 2]};
+      s->mat.push_back(m);
+      s->eye_depth.push_back(eye_depth[h]);
+      s->gathered.push_back(gathered ? gathered[h] : 1);
+    }
+    return s;
+  } catch (const std::invalid_argument&) {
+    if (err) *err = 1;
+  }
+  return nullptr;
+}
+
+void ref_session_free(void* s) { delete static_cast<RefSession*>(s); }
+
+double ref_session_max_radius(void* sp) {
+  auto* s = static_cast<RefSession*>(sp);
+  double r = 0.0;
+  for (const GatherRegion& g : s->regions) r = std::max(r, g.radius());
+  return r;
+}
+
+// Builds the reference PhotonGrid from canonical fp32 photons widened to
+// double, then gathers + tests every selected hit point exactly as
+// Renderer::pixel_pm does (integrator.cpp:407-490) for a first-hit diffuse
+// gather point.  grid_seconds / gather_seconds receive steady-clock timings.
+int ref_session_iterate(void* sp, uint64_t iteration, const float* ppos,
+                        const float* pnrm, const float* pwi, const float* ppow,
+                        const uint32_t* pdepth, size_t N, double cell_size,
+                        const uint32_t* subset, size_t nsub, RefIterOut* out,
+                        double* grid_seconds, double* gather_seconds) {
+  auto* s = static_cast<RefSession*>(sp);
+  const RefConfig& cfg = s->cfg;
+  double cell = cell_size;
+  if (!(cell > 0)) cell = ref_session_max_radius(sp); // integrator.cpp:159-161
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<LightVertex> flat(N);
+  for (size_t i = 0; i < N; ++i) {
+    LightVertex& v = flat[i];
+    v.position = {ppos[3 * i], ppos[3 * i + 1], ppos[3 * i + 2]};
+    v.shading_normal = {pnrm[3 * i], pnrm[3 * i + 1], pnrm[3 * i + 2]};
+    v.geom_normal = v.shading_normal;
+    v.wi = {pwi[3 * i], pwi[3 * i + 1], pwi[3 * i + 2]};
+    v.throughput = {ppow[3 * i], ppow[3 * i + 1], ppow[3 * i + 2]};
+    v.path_index = static_cast<uint32_t>(i);
+    v.depth = pdepth[i];
+  }
+  PhotonGrid grid;
+  try {
+    grid = PhotonGrid(std::move(flat), cell); // integrator.cpp:262-264
+  } catch (const std::invalid_argument&) {
+    return 1;
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  const std::vector<LightVertex>& photons = grid.vertices();
+  const size_t count = subset ? nsub : s->regions.size();
+  const int CG = cfg.n_annuli * cfg.n_sectors * (cfg.channels == 3 ? 3 : 1);
+  int failure = 0;
+
+  parallel_ranges(cfg.threads, count, [&](size_t begin, size_t end) {
+    std::vector<uint32_t> query;
+    for (size_t slot = begin; slot < end; ++slot) {
+      const size_t h = subset ? subset[slot] : slot;
+      GatherRegion* region = &s->regions[h];
+      const double r = region->radius(); // :411
+      if (out && out->gather_r) out->gather_r[slot] = r;
+      Rgb sum;
+      uint64_t accepted = 0;
+      const bool gathered = s->gathered[h] != 0;
+      try {
+        if (gathered) {
+          const Point3& center = s->pos[h];
+          const Normal3& normal = s->nrm[h];
+          region->move_to(center, normal); // :438
+          const TangentFrame frame = region->frame();
+          const Bsdf bsdf(s->mat[h], normal, s->wo[h], true);
+          const Rgb throughput = s->thr[h];
+          // gather_disk (:388-402)
+          grid.query_ball(center, r, query);
+          const double r2 = r * r;
+          for (const uint32_t id : query) {
+            const LightVertex& p = photons[id];
+            if (s->eye_depth[h] + p.depth > cfg.max_depth) continue;
+            if (dot(p.shading_normal, normal) < cfg.normal_guard_cos) continue;
+            const UnifiedPoint y = map_to_unified(center, p.position, frame);
+            if (y.u * y.u + y.v * y.v > r2) continue;
+            // callback (:445-451)
+            double pf = 0, pr = 0;
+            const Rgb f = bsdf.eval(p.wi, pf, pr);
+            const Rgb val = throughput * f * p.throughput;
+            sum += val;
+            region->accumulate({y, val});
+            ++accepted;
+          }
+        }
+      } catch (...) {
+        failure = 2;
+        return;
+      }
+      if (out && out->flux) {
+        out->flux[3 * slot] = sum.r; out->flux[3 * slot + 1] = sum.g; out->flux[3 * slot + 2] = sum.b;
+      }
+      if (out && out->radiance) {
+        const Rgb c = gathered ? sum / (kPi * r * r * static_cast<double>(cfg.samples_per_iteration))
+                               : Rgb{};
+        out->radiance[3 * slot] = c.r; out->radiance[3 * slot + 1] = c.g; out->radiance[3 * slot + 2] = c.b;
+      }
+      if (out && out->accepted) out->accepted[slot] = accepted;
+      if (out && (out->stat_count || out->stat_sum || out->stat_sum_sq)) {
+        for (int c = 0; c < region->channel_count(); ++c) {
+          const auto st = region->sector_stats(c);
+          for (size_t g = 0; g < st.size(); ++g) {
+            const size_t o = static_cast<size_t>(CG) * slot + static_cast<size_t>(c) * st.size() + g;
+            if (out->stat_count) out->stat_count[o] = st[g].count;
+            if (out->stat_sum) out->stat_sum[o] = st[g].sum;
+            if (out->stat_sum_sq) out->stat_sum_sq[o] = st[g].sum_sq;
+          }
+        }
+      }
+      RadiusUpdate up;
+      if (gathered) {
+        up = region->end_iteration(iteration, cfg.samples_per_iteration); // :480
+      } else {
+        up.radius = region->radius(); // :486
+      }
+      if (out && out->radius) out->radius[slot] = up.radius;
+      if (out && out->t) out->t[slot] = region->held_iterations();
+      if (out && out->tested) out->tested[slot] = up.tested ? 1 : 0;
+      if (out && out->rejected) out->rejected[slot] = up.rejected ? 1 : 0;
+      if (out && out->statistic) out->statistic[slot] = up.statistic;
+      if (out && out->critical) out->critical[slot] = up.critical;
+    }
+  });
+  const auto t2 = std::chrono::steady_clock::now();
+  if (grid_seconds) *grid_seconds = std::chrono::duration<double>(t1 - t0).count();
+  if (gather_seconds) *gather_seconds = std::chrono::duration<double>(t2 - t1).count();
+  return failure;
+}
+
+unsigned ref_hardware_threads() { return std::thread::hardware_concurrency(); }
+
+} // extern "C"
