@@ -1,0 +1,487 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 gather + F-test hot path (BASELINE.json metric).
+
+A step is one FPPM iteration of the workload (default: BASELINE configs[1],
+"c2"): the max-live-radius reduction, the photon hash-grid build (cell keys,
+radix sort, cell table, record permute), the warp-per-hit-point gather with
+fp64 sector moments, and the fused end-of-iteration F-test/radius update.
+
+Arms
+  default            this repo's CUDA path (libfppm_gpu.so) on N GPUs
+  --impl reference   the reference's own CPU code (oracle/_ref, compiled
+                     unmodified from proj/core) on the host cores, bounded
+                     samples of the same workload
+
+Output: one JSON line on rank 0 (contract in the task statement).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("hit-point×photon kernel queries/sec (gather+F-test), photons traced/sec, "
+          "% HBM roofline")
+UNIT = "queries/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-stride", type=int, default=0,
+                   help="hit-point stride of the CPU sample (0 = auto)")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per gather launch from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "gather_ncu.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("workload")
+    except (OSError, ValueError):
+        return None, None
+
+
+def raster_rows(W, rank, world):
+    r0 = W * rank // world
+    r1 = W * (rank + 1) // world
+    return r0, r1
+
+
+def hitpoints_for_rows(W, r0, r1):
+    import numpy as np
+    j, i = np.meshgrid(np.arange(r0, r1), np.arange(W), indexing="ij")
+    pos = np.zeros(((r1 - r0) * W, 3))
+    pos[:, 0] = ((i.ravel() + 0.5) / W).astype(np.float32)
+    pos[:, 1] = ((j.ravel() + 0.5) / W).astype(np.float32)
+    nrm = np.tile([0.0, 0.0, 1.0], (len(pos), 1))
+    return pos, nrm
+
+
+def emit(line):
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference_run(wl, steps, warmup, stride, threads, first_iteration=1):
+    """Reference CPU path (oracle/_ref) on a hit-point sample; per step the
+    full photon grid is built and every `stride`-th hit point is gathered and
+    tested.  Returns per-step extrapolated (queries, seconds)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle
+    ref, port = Oracle("reference"), Oracle("port")
+    hp = port.gen_raster_hitpoints(wl.raster)
+    sub = np.arange(0, wl.hitpoints, stride, dtype=np.uint32)
+    hp_s = {k: v[sub] for k, v in hp.items()}
+    sess = ref.session(dict(n_annuli=wl.n_annuli, n_sectors=wl.n_sectors, alpha_f=wl.alpha_f,
+                            initial_radius=wl.initial_radius, r_min_base=0.001 * wl.initial_radius,
+                            samples_per_iteration=wl.photons, k=wl.k, alpha=wl.alpha,
+                            threads=threads), hp_s)
+    scale = wl.hitpoints / len(sub)
+    out = []
+    for s in range(warmup + steps):
+        it = first_iteration + s
+        ph = port.gen_photons(wl.generator, wl.seed, it, 0, wl.photons)
+        r = sess.iterate(it, ph)
+        grid_s, gather_s = r["times"]
+        if s >= warmup:
+            out.append((float(r["accepted"].sum()) * scale, grid_s + gather_s * scale,
+                        grid_s, gather_s))
+    return out, len(sub)
+
+
+def run_reference_arm(args, wl, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    stride = args.cpu_stride or (64 if wl.name.startswith("c2") else 16)
+    steps = run = None
+    try:
+        run, nsub = cpu_reference_run(wl, max(args.steps, 1), max(args.warmup, 0), stride, threads)
+    except Exception as e:  # the reference arm must still print a line
+        emit({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"})
+        return
+    q = sum(x[0] for x in run)
+    t = sum(x[1] for x in run)
+    v = q / t
+    sample = (f"{wl.name}: per step the full {wl.photons}-photon grid build (serial std::sort, "
+              f"photon_map.cpp:26-51) + gather/F-test of every {stride}th hit point "
+              f"({nsub} of {wl.hitpoints}) on {threads} threads, queries and gather time "
+              f"extrapolated x{wl.hitpoints / nsub:g} to the full frame")
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(run),
+          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+          "data": "synthetic (canonical PCG32 inputs, DESIGN.md §3)",
+          "config": workload_config(wl),
+          "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                           "sample": sample},
+          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+def workload_config(wl, **extra):
+    cfg = {"workload": f"{wl.name} (BASELINE configs[{0 if wl.name.startswith('c1') else 1}])",
+           "hitpoints": wl.hitpoints, "photons_per_iteration": wl.photons,
+           "groups": f"{wl.n_annuli}x{wl.n_sectors}", "alpha_f": wl.alpha_f,
+           "initial_radius": wl.initial_radius}
+    cfg.update(extra)
+    return cfg
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_gpu_arm(args, wl, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2504_04411_b200 import FppmContext
+    from paper_2504_04411_b200 import _native as N
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    W = wl.raster
+    r0, r1 = raster_rows(W, rank, world)
+    H = (r1 - r0) * W
+    n_local = wl.photons * (rank + 1) // world - wl.photons * rank // world
+    begin = wl.photons * rank // world
+    ctx = FppmContext(**wl.context_kwargs(max_hitpoints=H, max_photons=wl.photons,
+                                          device=local_rank))
+    pos, nrm = hitpoints_for_rows(W, r0, r1)
+    ctx.set_hitpoints(pos, nrm)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    total_steps = args.warmup + args.steps
+
+    # ---- per-iteration photon shares, resident in HBM before timing
+    def gen_batch(it):
+        out = {}
+        for key, dt, width in (("photon_pos", torch.float32, 3), ("photon_normal", torch.float32, 3),
+                               ("photon_wi", torch.float32, 3), ("photon_power", torch.float32, 3),
+                               ("photon_depth", torch.int32, 1)):
+            out[key] = torch.empty((n_local, width) if width > 1 else (n_local,), dtype=dt,
+                                   device=dev)
+        ph = N.Photons(*[out[k].data_ptr() for k in ("photon_pos", "photon_normal", "photon_wi",
+                                                      "photon_power", "photon_depth")])
+        torch.cuda.synchronize()
+        N.check(ctx._lib.fppm_gpu_generate_photons_to(ctx._h, wl.generator, wl.seed, it, begin,
+                                                      n_local, ph), ctx._h)
+        ctx.synchronize()
+        return out
+
+    batches = [gen_batch(it) for it in range(1, total_steps + 1)]
+    full = None
+    if world > 1:
+        full = {k: torch.empty((wl.photons,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+                for k, t in batches[0].items()}
+    torch.cuda.synchronize()
+
+    gather_ms = []
+
+    def step(it, b, timed):
+        src = b
+        if world > 1:
+            with torch.cuda.stream(stream):
+                for k in full:
+                    dist.all_gather_into_tensor(full[k], b[k])
+            src = full
+        ph = N.Photons(*[src[k].data_ptr() for k in ("photon_pos", "photon_normal", "photon_wi",
+                                                      "photon_power", "photon_depth")])
+        N.check(ctx._lib.fppm_gpu_set_photons_device(ctx._h, ph, wl.photons), ctx._h)
+        if world > 1:
+            rl = torch.tensor([ctx.max_radius()], dtype=torch.float64, device=dev)
+            dist.all_reduce(rl, op=dist.ReduceOp.MAX)
+            cell = float(rl.item())  # integrator.cpp:159-161 over all ranks
+        else:
+            cell = 0.0  # device-side max live radius
+        ctx.build_grid(cell)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.gather_test(it, outputs=False, summary=False)
+        e1.record(stream)
+        if timed:
+            gather_ms.append((e0, e1))
+
+    for s in range(args.warmup):
+        step(s + 1, batches[s], False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    c0 = ctx.counters()
+    l0 = FppmContext.kernel_launches()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for s in range(args.warmup, total_steps):
+        step(s + 1, batches[s], True)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = FppmContext.kernel_launches() - l0
+    c1 = ctx.counters()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    g_ms = [a.elapsed_time(b) for a, b in gather_ms]
+    q_local = c1["accepted"] - c0["accepted"]
+    stats = torch.tensor([elapsed_ms, float(q_local), float(launches)], dtype=torch.float64, device=dev)
+    if world > 1:
+        t_max = stats[:1].clone()
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        q_sum = stats[1:2].clone()
+        dist.all_reduce(q_sum, op=dist.ReduceOp.SUM)
+        elapsed_ms, q_total = float(t_max.item()), float(q_sum.item())
+    else:
+        q_total = float(q_local)
+    value = q_total / (elapsed_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (k_gather_test), rank 0
+    G, C = wl.groups, 1
+    gather_avg_s = statistics.mean(g_ms) / 1e3
+    alg_bytes = 16.0 * q_local / args.steps + (64 + 48 * G * C) * H
+    peak, peak_src = peaks()
+    achieved = alg_bytes / gather_avg_s / 1e9
+    traffic, traffic_wl = ncu_traffic()
+
+    # ---- end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(ctx, wl, batches, args, world, rank, dev, stream, H)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            stride = args.cpu_stride or (64 if wl.name.startswith("c2") else 16)
+            threads = os.cpu_count() or 1
+            run, nsub = cpu_reference_run(wl, 1, 0, stride, threads)
+            q, t = run[0][0], run[0][1]
+            cpu = {"value": q / t, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": (f"iteration 1 of {wl.name}: full {wl.photons}-photon grid build "
+                              f"(reference PhotonGrid, serial sort) {run[0][2]:.2f} s + gather/F-test "
+                              f"of every {stride}th hit point ({nsub} of {wl.hitpoints}) "
+                              f"{run[0][3]:.2f} s on {threads} threads, extrapolated to the frame")}
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (canonical PCG32 inputs generated on device, DESIGN.md §3)",
+            "config": workload_config(
+                wl, parallelism=f"hit points sharded by raster rows over {world} GPU(s); photon "
+                                "shares all-gathered (NCCL) each step" if world > 1 else "1 GPU",
+                l2=f"inputs larger than L2: fresh {wl.photons * 52 / 1e6:.0f} MB photon batch "
+                   "per step (+256 MB sorted records)" if wl.photons * 52 > 126e6 else
+                   "photon batch smaller than L2 (not flushed)",
+                iterations_timed=f"{args.warmup + 1}..{args.warmup + args.steps}"),
+            "photons_per_s": wl.photons * args.steps / (elapsed_ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_gather_test (gather + fused F-test)",
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "bytes_formula": "16*Q + (64 + 48*G*C)*H (SURVEY.md 8d)",
+                         "avg_launch_ms": gather_avg_s * 1e3,
+                         "share_of_step": gather_avg_s * 1e3 / (elapsed_ms / args.steps),
+                         "peak_source": peak_src, "traffic_source": traffic_wl},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "counters": {"accepted": q_total, "candidates": c1["candidates"] - c0["candidates"],
+                         "exact_path_pairs": c1["exact"] - c0["exact"],
+                         "ambiguous_pairs": c1["ambiguous"] - c0["ambiguous"]},
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        emit(line)
+    ctx.close()
+
+
+def run_e2e(ctx, wl, batches, args, world, rank, dev, stream, H):
+    """Same metric through the C-ABI host path: per step the photon share is
+    copied from pinned host memory (fppm_gpu_set_photons) and the per-hit-point
+    radius, radiance and decision are read back (fppm_gpu_gather_test out)."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2504_04411_b200 import _native as N
+
+    pinned = []
+    for b in batches:
+        hb = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for k, t in b.items()}
+        for k in b:
+            hb[k].copy_(b[k])
+        pinned.append(hb)
+    if world > 1:
+        # each rank uploads its share; the exchange stays on the device (NCCL)
+        full = {k: torch.empty((wl.photons,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+                for k, t in batches[0].items()}
+        local = {k: torch.empty_like(t) for k, t in batches[0].items()}
+    out_r = torch.empty(H, dtype=torch.float64, pin_memory=True)
+    out_rad = torch.empty((H, 3), dtype=torch.float32, pin_memory=True)
+    out_rej = torch.empty(H, dtype=torch.uint8, pin_memory=True)
+    io = N.IterOut()
+    io.radius = out_r.data_ptr()
+    io.radiance = out_rad.data_ptr()
+    io.rejected = out_rej.data_ptr()
+    torch.cuda.synchronize()
+    ctx.reset_regions()
+    n_local = next(iter(pinned[0].values())).shape[0]
+    h2d = sum(t.numel() * t.element_size() for t in pinned[0].values())
+    d2h = H * (8 + 12 + 1)
+
+    def one(it, hb):
+        if world == 1:
+            ph = N.Photons(*[hb[k].data_ptr() for k in ("photon_pos", "photon_normal", "photon_wi",
+                                                         "photon_power", "photon_depth")])
+            N.check(ctx._lib.fppm_gpu_set_photons(ctx._h, ph, n_local), ctx._h)
+            N.check(ctx._lib.fppm_gpu_iterate(ctx._h, it, C.byref(io), None), ctx._h)
+        else:
+            with torch.cuda.stream(stream):
+                for k in local:
+                    local[k].copy_(hb[k], non_blocking=True)
+                    dist.all_gather_into_tensor(full[k], local[k])
+            ph = N.Photons(*[full[k].data_ptr() for k in ("photon_pos", "photon_normal",
+                                                           "photon_wi", "photon_power",
+                                                           "photon_depth")])
+            N.check(ctx._lib.fppm_gpu_set_photons_device(ctx._h, ph, wl.photons), ctx._h)
+            rl = torch.tensor([ctx.max_radius()], dtype=torch.float64, device=dev)
+            dist.all_reduce(rl, op=dist.ReduceOp.MAX)
+            ctx.build_grid(float(rl.item()))
+            N.check(ctx._lib.fppm_gpu_gather_test(ctx._h, it, C.byref(io), None), ctx._h)
+
+    for s in range(args.warmup):
+        one(s + 1, pinned[s])
+    c0 = ctx.counters()["accepted"]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(args.warmup, args.warmup + args.steps):
+        one(s + 1, pinned[s])
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    q = float(ctx.counters()["accepted"] - c0)
+    el = torch.tensor([t1 - t0, q], dtype=torch.float64, device=dev)
+    if world > 1:
+        tm = el[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        qs = el[1:].clone()
+        dist.all_reduce(qs, op=dist.ReduceOp.SUM)
+        secs, q = float(tm.item()), float(qs.item())
+    else:
+        secs = t1 - t0
+    return {"value": q / secs, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * secs / args.steps,
+            "path": "fppm_gpu_set_photons (pinned host) + fppm_gpu_iterate with host outputs"}
+
+
+def main():
+    args = parse()
+    from paper_2504_04411_b200.workloads import WORKLOADS
+    wl = WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, wl, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu_arm(args, wl, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

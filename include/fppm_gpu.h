@@ -1,0 +1,242 @@
+/*
+ * fppm_gpu.h -- C ABI of the B200-native gather + F-test hot path.
+ *
+ * This is the drop-in boundary for the reference's in-process C++ interface
+ * of the hot path (reference proj/core, installed headers fppm/*.hpp):
+ *
+ *   fppm::PhotonGrid(std::vector<LightVertex>, double cell)   photon_map.hpp:18
+ *   fppm::PhotonGrid::query_ball(center, r, out)              photon_map.hpp:26-27
+ *   fppm::GatherRegion(TestConfig, RadiusSchedule, r0)        gather.hpp:71-72
+ *   fppm::GatherRegion::move_to / accumulate / end_iteration  gather.hpp:75-81
+ *   fppm::GatherRegion::chi2_end_iteration / schedule_end_iteration  :84-87
+ *   Renderer::gather_disk + pixel_pm gather block   integrator.cpp:388-402, :435-489
+ *
+ * The reference drives one GatherRegion per pixel from a host thread pool;
+ * here one context owns all regions ("hit points") of a frame on one B200
+ * and every call is a batched, stream-ordered operation over all of them.
+ *
+ * Conventions:
+ *   - every entry point returns fppm_status (0 = ok); no exception crosses;
+ *     the C++ wrapper fppm_gpu.hpp rethrows std::invalid_argument /
+ *     std::domain_error for FPPM_ERR_INVALID_ARGUMENT / FPPM_ERR_DOMAIN;
+ *   - the caller owns host buffers, the context owns device buffers;
+ *   - calls are ordered on the context's CUDA stream and are not re-entrant
+ *     (one host thread per context);
+ *   - photons are canonical fp32 records (position, shading normal, incident
+ *     direction wi, power/throughput RGB, depth); hit points are fp64 like the
+ *     reference Point3/Normal3; accumulators and radii are fp64.
+ */
+#ifndef FPPM_GPU_H
+#define FPPM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPPM_GPU_ABI_VERSION 1
+
+typedef enum fppm_status {
+  FPPM_OK = 0,
+  FPPM_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  FPPM_ERR_DOMAIN = 2,           /* reference: std::domain_error */
+  FPPM_ERR_CUDA = 3,             /* CUDA runtime failure (message in last_error) */
+  FPPM_ERR_CAPACITY = 4,         /* a buffer bound in fppm_gpu_config exceeded */
+  FPPM_ERR_STATE = 5,            /* call order violated (e.g. gather before grid) */
+  FPPM_ERR_NO_DEVICE = 6         /* no sm_100 device: there is no CPU fallback */
+} fppm_status;
+
+/* gather.hpp:29 TestChannels (auto_detect is resolved by the caller) */
+#define FPPM_CHANNELS_LUMINANCE 1
+#define FPPM_CHANNELS_RGB 3
+/* gather.hpp:32 TestOverride */
+#define FPPM_OVERRIDE_NONE 0
+#define FPPM_OVERRIDE_ALWAYS_REJECT 1
+#define FPPM_OVERRIDE_NEVER_REJECT 2
+/* end-of-iteration policy: gather.cpp:90 / :114 / :138 */
+#define FPPM_POLICY_FTEST 0
+#define FPPM_POLICY_CHI2 1
+#define FPPM_POLICY_SCHEDULE 2
+/* canonical synthetic workloads */
+#define FPPM_WORKLOAD_C1 1
+#define FPPM_WORKLOAD_C2 2
+
+typedef struct fppm_gpu_config {
+  /* TestConfig (gather.hpp:34-41) */
+  int32_t n_annuli;
+  int32_t n_sectors;
+  double alpha_f;
+  double alpha_chi2;
+  int32_t channels;          /* FPPM_CHANNELS_* */
+  int32_t override_decision; /* FPPM_OVERRIDE_* */
+  int32_t policy;            /* FPPM_POLICY_* */
+  /* RadiusSchedule (gather.hpp:16-20) */
+  double k;
+  double alpha;
+  double r_min_base;
+  /* r_1 of every region (GatherRegion ctor, gather.cpp:35-52) */
+  double initial_radius;
+  /* J: nominal samples per iteration (end_iteration arg, integrator.cpp:480) */
+  uint64_t samples_per_iteration;
+  /* integrator.cpp:396-397 filters */
+  uint32_t max_depth;
+  double normal_guard_cos; /* 0.86602540378443865 in the reference */
+  /* capacities (device buffers are sized once) */
+  uint32_t max_hitpoints;
+  uint32_t max_photons;
+  uint32_t max_cells; /* 0 -> 1<<28 dense cells */
+  int32_t device;     /* CUDA ordinal */
+  void *stream;       /* cudaStream_t to order work on; NULL -> own stream */
+} fppm_gpu_config;
+
+typedef struct fppm_gpu_ctx fppm_gpu_ctx;
+
+/* Hit points (the GatherRegion centers of one iteration); all [n][3] fp64
+ * except eye_depth (u32) and gathered (u8, NULL = every hit point gathers). */
+typedef struct fppm_hitpoints {
+  const double *pos;        /* gather point x (move_to center) */
+  const double *normal;     /* shading normal (move_to normal, Bsdf frame) */
+  const double *wo;         /* direction toward the eye (Bsdf cos_o) */
+  const double *throughput; /* eye-path throughput (integrator.cpp:448) */
+  const double *albedo;     /* Lambertian albedo (bsdf.cpp:63) */
+  const uint32_t *eye_depth;/* depth of the gather vertex (integrator.cpp:444) */
+  const uint8_t *gathered;  /* integrator.cpp:476-488 */
+} fppm_hitpoints;
+
+/* Photons = light vertices (LightVertex, path.hpp:76-89), canonical fp32. */
+typedef struct fppm_photons {
+  const float *pos;     /* [n][3] */
+  const float *normal;  /* [n][3] shading normal at the deposit */
+  const float *wi;      /* [n][3] unit, toward where the energy came from */
+  const float *power;   /* [n][3] throughput RGB */
+  const uint32_t *depth;/* [n] */
+} fppm_photons;
+
+/* Per-hit-point outputs of one iteration (host pointers; NULL skips).
+ * Field meanings follow RadiusUpdate (gather.hpp:55-61) and pixel_pm. */
+typedef struct fppm_gpu_iter_out {
+  double *radius;        /* after the update */
+  double *gather_radius; /* radius the gather used */
+  uint64_t *t;           /* held_iterations() after the update */
+  uint8_t *tested;
+  uint8_t *rejected;
+  double *statistic;
+  double *critical;
+  double *flux;          /* [n][3] sum of photon values (integrator.cpp:449) */
+  float *radiance;       /* [n][3] flux / (pi r^2 J) (integrator.cpp:452-455) */
+  uint32_t *accepted;    /* accepted photons this iteration */
+  uint64_t *stat_count;  /* [n][C*G] pooled stats BEFORE end_iteration */
+  double *stat_sum;
+  double *stat_sum_sq;
+} fppm_gpu_iter_out;
+
+/* Whole-frame summary of one iteration (host). */
+typedef struct fppm_gpu_summary {
+  uint64_t accepted;       /* Q: accepted (hit point, photon) pairs */
+  uint64_t candidates;     /* pairs ball-tested (27-cell neighbourhoods) */
+  uint64_t exact_pairs;    /* pairs resolved on the fp64 exact path */
+  uint64_t ambiguous_pairs;/* sector assignments within 1 ulp of a bin edge */
+  uint32_t tested;
+  uint32_t rejected;
+  double cell_size;        /* grid cell (= max live radius before the update) */
+  double r_max_next;       /* max radius after the update */
+  uint64_t cells;          /* dense cells in the grid bounding box */
+} fppm_gpu_summary;
+
+/* Device pointers owned by the context (for zero-copy producers such as an
+ * NCCL all-gather into the photon staging buffers). */
+typedef struct fppm_gpu_device_view {
+  float *photon_pos, *photon_normal, *photon_wi, *photon_power;
+  uint32_t *photon_depth;
+  double *radius;
+  uint64_t *counters; /* [0]=accepted [1]=candidates [2]=exact [3]=ambiguous, cumulative */
+} fppm_gpu_device_view;
+
+int fppm_gpu_abi_version(void);
+const char *fppm_gpu_status_string(int status);
+
+int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out);
+int fppm_gpu_destroy(fppm_gpu_ctx *ctx);
+const char *fppm_gpu_last_error(const fppm_gpu_ctx *ctx);
+int fppm_gpu_synchronize(fppm_gpu_ctx *ctx);
+void *fppm_gpu_stream(fppm_gpu_ctx *ctx);
+int fppm_gpu_device_view_get(fppm_gpu_ctx *ctx, fppm_gpu_device_view *view);
+
+/* ---- hit points / regions (GatherRegion state) ---- */
+int fppm_gpu_set_hitpoints(fppm_gpu_ctx *ctx, const fppm_hitpoints *host, uint32_t n);
+int fppm_gpu_set_hitpoints_device(fppm_gpu_ctx *ctx, const fppm_hitpoints *dev, uint32_t n);
+/* Canonical raster hit points ((i+1/2)/W, (j+1/2)/W, 0), n=+z. */
+int fppm_gpu_generate_raster_hitpoints(fppm_gpu_ctx *ctx, uint32_t W);
+/* Reset every region to r_1, t = 1, zero stats (GatherRegion ctor). */
+int fppm_gpu_reset_regions(fppm_gpu_ctx *ctx);
+/* Region state readback/overwrite (host arrays, NULL skips). */
+int fppm_gpu_get_regions(fppm_gpu_ctx *ctx, double *radius, uint64_t *t,
+                         uint64_t *stat_count, double *stat_sum, double *stat_sum_sq);
+int fppm_gpu_set_regions(fppm_gpu_ctx *ctx, const double *radius, const uint64_t *t,
+                         const uint64_t *stat_count, const double *stat_sum,
+                         const double *stat_sum_sq);
+int fppm_gpu_max_radius(fppm_gpu_ctx *ctx, double *r_max);
+
+/* ---- photons + grid (PhotonGrid) ---- */
+int fppm_gpu_set_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n);
+int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint32_t n);
+/* Canonical synthetic photons [begin, begin+n) of (seed, iteration). */
+int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed,
+                              uint64_t iteration, uint64_t begin, uint32_t n);
+/* Same generator writing into caller-owned device arrays (no staging). */
+int fppm_gpu_generate_photons_to(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed,
+                                 uint64_t iteration, uint64_t begin, uint32_t n,
+                                 const fppm_photons *dev_dst);
+/* Copy the staged photons back to host arrays (NULL skips). */
+int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi, float *power,
+                         uint32_t *depth);
+/* Build the uniform hash grid; cell_size <= 0 uses the max live radius
+ * (integrator.cpp:159-161).  Throws invalid_argument when cell <= 0. */
+int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size);
+/* Reference-layout export (PhotonGrid keys_/cells_/order_, photon_map.cpp:26-51).
+ * Pass NULL arrays to query *ncells first. */
+int fppm_gpu_export_grid(fppm_gpu_ctx *ctx, uint64_t *keys, uint32_t *begin,
+                         uint32_t *end, uint32_t *order, uint64_t *ncells);
+/* Batched query_ball (photon_map.cpp:53-78): indices of stored photons with
+ * |pos - c|^2 <= r^2 in reference visit order.  offsets has nq+1 entries;
+ * indices holds cap entries; *total receives the full count. */
+int fppm_gpu_query_ball(fppm_gpu_ctx *ctx, const double *centers, const double *radii,
+                        uint32_t nq, uint64_t *offsets, uint32_t *indices,
+                        uint64_t cap, uint64_t *total);
+
+/* ---- the hot path ---- */
+/* Gather + accumulate + end-of-iteration policy for every hit point against
+ * the grid built last (pixel_pm, integrator.cpp:435-489).  out/summary may be
+ * NULL (then the call is fully asynchronous). */
+int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration,
+                         fppm_gpu_iter_out *out, fppm_gpu_summary *summary);
+/* One FPPM iteration: build_grid(max live radius) + gather_test. */
+int fppm_gpu_iterate(fppm_gpu_ctx *ctx, uint64_t iteration,
+                     fppm_gpu_iter_out *out, fppm_gpu_summary *summary);
+
+/* ---- GatherRegion primitives on explicit samples (gather.cpp:59-67, 90-144) ---- */
+/* Adds samples (region index, plane coords y, RGB value) to pooled stats. */
+int fppm_gpu_accumulate(fppm_gpu_ctx *ctx, const uint32_t *region, const double *y,
+                        const double *value, uint32_t n);
+/* J passed to end_iteration (gather.hpp:81 samples_per_iteration). */
+int fppm_gpu_set_samples_per_iteration(fppm_gpu_ctx *ctx, uint64_t samples_per_iteration);
+/* Runs the configured end-of-iteration policy on every region without a gather. */
+int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration,
+                           fppm_gpu_iter_out *out);
+
+/* Cumulative counters of this context: [accepted, candidates, exact, ambiguous]. */
+int fppm_gpu_counters(fppm_gpu_ctx *ctx, uint64_t out[4]);
+/* Kernel launches issued by this library since load (all contexts). */
+uint64_t fppm_gpu_kernel_launches(void);
+
+/* ---- free functions (host-side numerics shared with the device tables) ---- */
+double fppm_gpu_schedule_radius(double base, double alpha, uint64_t i);
+double fppm_gpu_f_quantile(double p, double d1, double d2, int *status);
+double fppm_gpu_chi2_quantile(double p, double df, int *status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPPM_GPU_H */

@@ -1,0 +1,905 @@
+// context.cu -- the C ABI (include/fppm_gpu.h): device buffers, the per-iteration
+// orchestration and host<->device plumbing around the kernels in grid.cu,
+// gather.cu and generate.cu.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gather.cuh"
+
+struct fppm_gpu_ctx {
+  fppm_gpu_config cfg{};
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int G = 0, C = 1;
+
+  // regions
+  uint32_t H = 0;
+  double3 *d_pos = nullptr, *d_nrm = nullptr, *d_wo = nullptr, *d_thr = nullptr,
+          *d_alb = nullptr, *d_K = nullptr;
+  uint32_t *d_eye = nullptr;
+  uint8_t *d_gathered = nullptr;
+  double *d_radius = nullptr;
+  uint32_t *d_t = nullptr;
+  unsigned long long *d_st_cnt = nullptr;
+  double *d_st_sum = nullptr, *d_st_sq = nullptr;
+
+  // photon staging (canonical [n][3] fp32)
+  uint32_t N = 0;
+  float *d_ppos = nullptr, *d_pnrm = nullptr, *d_pwi = nullptr, *d_ppow = nullptr;
+  uint32_t *d_pdepth = nullptr;
+  // photons the next grid build reads: the staging buffers, or caller-owned
+  // device buffers registered by fppm_gpu_set_photons_device (zero copy)
+  const float *in_pos = nullptr, *in_nrm = nullptr, *in_wi = nullptr, *in_pow = nullptr;
+  const uint32_t *in_depth = nullptr;
+
+  // grid
+  fppm_b200::PhotonRecs recs{};
+  fppm_b200::SortScratch sort{};
+  uint32_t *d_skeys = nullptr, *d_order = nullptr;  // alias into sort buffers
+  uint32_t *d_cell_start = nullptr;
+  unsigned long long cell_cap = 0;
+  fppm_b200::GridHeader *d_hdr = nullptr, *h_hdr = nullptr;
+  long long *d_bounds = nullptr, *h_bounds_init = nullptr;
+  double *d_cell = nullptr, *h_cell = nullptr;
+  bool grid_valid = false;
+
+  // outputs
+  double *o_gather_r = nullptr, *o_stat = nullptr, *o_crit = nullptr, *o_flux = nullptr;
+  uint8_t *o_flags = nullptr;
+  float *o_rad = nullptr;
+  uint32_t *o_acc = nullptr;
+  unsigned long long *snap_cnt = nullptr;
+  double *snap_sum = nullptr, *snap_sq = nullptr;
+
+  // counters
+  unsigned long long *d_counters = nullptr, *h_counters = nullptr;
+  unsigned long long last_counters[4] = {0, 0, 0, 0};
+  unsigned int *d_iter_tr = nullptr, *d_work = nullptr;
+  unsigned long long *d_rmax_bits = nullptr;
+
+  // critical-value table by t
+  std::vector<double> crit;
+  double *d_crit = nullptr;
+  uint32_t crit_cap = 0;
+  uint64_t end_calls = 0;
+  double chi2_crit = 0.0;
+
+  // scratch for explicit-sample / query APIs
+  void *d_scratch = nullptr;
+  size_t scratch_bytes = 0;
+};
+
+namespace fppm_b200 {
+
+int cuda_fail(fppm_gpu_ctx *ctx, cudaError_t e, const char *what) {
+  if (ctx) {
+    ctx->err = std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what;
+  }
+  return FPPM_ERR_CUDA;
+}
+
+static int fail(fppm_gpu_ctx *ctx, int code, const std::string &msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename T>
+static cudaError_t dalloc(T **p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void **>(p), sizeof(T) * count);
+}
+
+static cudaError_t ensure_scratch(fppm_gpu_ctx *ctx, size_t bytes) {
+  if (bytes <= ctx->scratch_bytes) return cudaSuccess;
+  if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+  ctx->scratch_bytes = 0;
+  cudaError_t e = cudaMalloc(&ctx->d_scratch, bytes);
+  if (e == cudaSuccess) ctx->scratch_bytes = bytes;
+  return e;
+}
+
+__global__ void k_max_radius(const double *__restrict__ radius, uint32_t H,
+                             double *__restrict__ out) {
+  __shared__ unsigned long long s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  double m = 0.0;
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x)
+    m = fmax(m, radius[h]);
+  atomicMax(&s, (unsigned long long)__double_as_longlong(m));
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long *>(out), s);
+}
+
+__global__ void k_fill_regions(double *radius, uint32_t *t, uint32_t H, double r0) {
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
+    radius[h] = r0;
+    t[h] = 1;
+  }
+}
+
+// grow the F critical table so that every t <= need is covered
+static int ensure_crit(fppm_gpu_ctx *ctx, uint64_t need) {
+  const fppm_gpu_config &c = ctx->cfg;
+  if (c.policy != FPPM_POLICY_FTEST || c.override_decision != FPPM_OVERRIDE_NONE) {
+    if (ctx->crit.empty()) ctx->crit.assign(2, 0.0);
+  }
+  if (ctx->crit.empty()) ctx->crit.push_back(0.0);  // t = 0 unused
+  const size_t old = ctx->crit.size();
+  if (ctx->crit.size() <= need && c.policy == FPPM_POLICY_FTEST &&
+      c.override_decision == FPPM_OVERRIDE_NONE) {
+    const long long d1 = (long long)ctx->G - 1;
+    while (ctx->crit.size() <= need) {
+      const uint64_t t = ctx->crit.size();
+      const uint64_t m = t * c.samples_per_iteration;
+      double v = 0.0;
+      if (m >= 2) {
+        const long long d2 = (long long)ctx->G * (long long)(m - 1);
+        // chi-squared limit is constant in d2 (special_functions.cpp:157)
+        if ((double)d2 > 2e7 && ctx->crit.size() > 1 &&
+            (double)((long long)ctx->G * (long long)((t - 1) * c.samples_per_iteration - 1)) > 2e7) {
+          v = ctx->crit.back();
+        } else {
+          int st = 0;
+          v = fppm_b200::host_f_quantile(1.0 - c.alpha_f, (double)d1, (double)d2, &st);
+        }
+      }
+      ctx->crit.push_back(v);
+    }
+  }
+  if (ctx->crit.size() > ctx->crit_cap) {
+    uint32_t cap = std::max<uint32_t>(64, ctx->crit_cap * 2);
+    while (cap < ctx->crit.size()) cap *= 2;
+    double *p = nullptr;
+    FPPM_CUDA_OK(cudaMalloc(&p, sizeof(double) * cap));
+    if (ctx->d_crit) {
+      FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+      cudaFree(ctx->d_crit);
+    }
+    ctx->d_crit = p;
+    ctx->crit_cap = cap;
+    FPPM_CUDA_OK(cudaMemcpyAsync(p, ctx->crit.data(), sizeof(double) * ctx->crit.size(),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  } else if (ctx->crit.size() > old) {
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_crit + old, ctx->crit.data() + old,
+                                 sizeof(double) * (ctx->crit.size() - old),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  }
+  return FPPM_OK;
+}
+
+static EndParams end_params(fppm_gpu_ctx *ctx, uint64_t iteration) {
+  const fppm_gpu_config &c = ctx->cfg;
+  EndParams P;
+  P.policy = c.policy;
+  P.override_decision = c.override_decision;
+  P.J = c.samples_per_iteration;
+  P.k = c.k;
+  P.floor_next = host_schedule_radius(c.r_min_base, c.alpha, iteration + 1);
+  P.sched_next = host_schedule_radius(c.initial_radius, c.alpha, iteration + 1);
+  P.crit = ctx->d_crit;
+  P.crit_len = (uint32_t)ctx->crit.size();
+  P.chi2_crit = ctx->chi2_crit;
+  return P;
+}
+
+static int copy_out(fppm_gpu_ctx *ctx, void *dst, const void *src, size_t bytes) {
+  if (!dst || bytes == 0) return FPPM_OK;
+  FPPM_CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return FPPM_OK;
+}
+
+static int copy_iter_out(fppm_gpu_ctx *ctx, fppm_gpu_iter_out *out, bool with_gather) {
+  if (!out) return FPPM_OK;
+  const size_t H = ctx->H, CG = (size_t)ctx->G * ctx->C;
+  int rc;
+  if ((rc = copy_out(ctx, out->radius, ctx->d_radius, sizeof(double) * H))) return rc;
+  if ((rc = copy_out(ctx, out->gather_radius, ctx->o_gather_r, sizeof(double) * H))) return rc;
+  if ((rc = copy_out(ctx, out->tested, ctx->o_flags, H))) return rc;
+  if ((rc = copy_out(ctx, out->statistic, ctx->o_stat, sizeof(double) * H))) return rc;
+  if ((rc = copy_out(ctx, out->critical, ctx->o_crit, sizeof(double) * H))) return rc;
+  if (with_gather) {
+    if ((rc = copy_out(ctx, out->flux, ctx->o_flux, sizeof(double) * 3 * H))) return rc;
+    if ((rc = copy_out(ctx, out->radiance, ctx->o_rad, sizeof(float) * 3 * H))) return rc;
+    if ((rc = copy_out(ctx, out->accepted, ctx->o_acc, sizeof(uint32_t) * H))) return rc;
+  }
+  if ((rc = copy_out(ctx, out->stat_count, ctx->snap_cnt, sizeof(unsigned long long) * CG * H))) return rc;
+  if ((rc = copy_out(ctx, out->stat_sum, ctx->snap_sum, sizeof(double) * CG * H))) return rc;
+  if ((rc = copy_out(ctx, out->stat_sum_sq, ctx->snap_sq, sizeof(double) * CG * H))) return rc;
+  std::vector<uint32_t> t32;
+  if (out->t) {
+    t32.resize(H);
+    if ((rc = copy_out(ctx, t32.data(), ctx->d_t, sizeof(uint32_t) * H))) return rc;
+  }
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  if (out->t)
+    for (size_t h = 0; h < H; ++h) out->t[h] = t32[h];
+  if (out->tested || out->rejected) {
+    // o_flags was copied into `tested`; split bits (bit0 tested, bit1 rejected)
+    std::vector<uint8_t> flags(H);
+    if (out->tested) {
+      std::memcpy(flags.data(), out->tested, H);
+    } else {
+      FPPM_CUDA_OK(cudaMemcpy(flags.data(), ctx->o_flags, H, cudaMemcpyDeviceToHost));
+    }
+    for (size_t h = 0; h < H; ++h) {
+      if (out->tested) out->tested[h] = flags[h] & 1;
+      if (out->rejected) out->rejected[h] = (flags[h] >> 1) & 1;
+    }
+  }
+  return FPPM_OK;
+}
+
+}  // namespace fppm_b200
+
+using namespace fppm_b200;
+
+extern "C" {
+
+int fppm_gpu_abi_version(void) { return FPPM_GPU_ABI_VERSION; }
+
+const char *fppm_gpu_status_string(int status) {
+  switch (status) {
+    case FPPM_OK: return "ok";
+    case FPPM_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case FPPM_ERR_DOMAIN: return "domain error";
+    case FPPM_ERR_CUDA: return "CUDA error";
+    case FPPM_ERR_CAPACITY: return "capacity exceeded";
+    case FPPM_ERR_STATE: return "invalid call order";
+    case FPPM_ERR_NO_DEVICE: return "no sm_100 device";
+  }
+  return "unknown status";
+}
+
+const char *fppm_gpu_last_error(const fppm_gpu_ctx *ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
+  if (!config || !out) return FPPM_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  const fppm_gpu_config &c = *config;
+  // GatherRegion ctor validation (gather.cpp:41-50)
+  if (!(c.initial_radius > 0)) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!(c.k > 0 && c.k < 1)) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!(c.alpha >= 0.5 && c.alpha < 1)) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!(c.r_min_base > 0 && c.r_min_base <= c.initial_radius)) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.n_annuli < 1 || c.n_sectors < 1 || c.n_annuli * c.n_sectors < 2) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.n_annuli * c.n_sectors > 32) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.channels != FPPM_CHANNELS_LUMINANCE && c.channels != FPPM_CHANNELS_RGB) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.policy < FPPM_POLICY_FTEST || c.policy > FPPM_POLICY_SCHEDULE) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.policy == FPPM_POLICY_FTEST && c.override_decision == FPPM_OVERRIDE_NONE &&
+      !(c.alpha_f > 0.0 && c.alpha_f < 1.0)) return FPPM_ERR_INVALID_ARGUMENT;  // stat_tests.cpp:88
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return FPPM_ERR_NO_DEVICE;
+  if (c.device < 0 || c.device >= ndev) return FPPM_ERR_NO_DEVICE;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c.device) != cudaSuccess || prop.major != 10) return FPPM_ERR_NO_DEVICE;
+  if (cudaSetDevice(c.device) != cudaSuccess) return FPPM_ERR_NO_DEVICE;
+
+  auto *ctx = new (std::nothrow) fppm_gpu_ctx;
+  if (!ctx) return FPPM_ERR_CAPACITY;
+  ctx->cfg = c;
+  if (ctx->cfg.max_cells == 0) ctx->cfg.max_cells = 1u << 28;
+  ctx->sms = prop.multiProcessorCount;
+  ctx->G = c.n_annuli * c.n_sectors;
+  ctx->C = c.channels;
+  if (c.stream) {
+    ctx->stream = static_cast<cudaStream_t>(c.stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return FPPM_ERR_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  const size_t Hc = std::max<uint32_t>(c.max_hitpoints, 1);
+  const size_t Nc = std::max<uint32_t>(c.max_photons, 1);
+  const size_t CG = (size_t)ctx->G * ctx->C;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  A(dalloc(&ctx->d_pos, Hc)); A(dalloc(&ctx->d_nrm, Hc)); A(dalloc(&ctx->d_wo, Hc));
+  A(dalloc(&ctx->d_thr, Hc)); A(dalloc(&ctx->d_alb, Hc)); A(dalloc(&ctx->d_K, Hc));
+  A(dalloc(&ctx->d_eye, Hc)); A(dalloc(&ctx->d_gathered, Hc));
+  A(dalloc(&ctx->d_radius, Hc)); A(dalloc(&ctx->d_t, Hc));
+  A(dalloc(&ctx->d_st_cnt, Hc * CG)); A(dalloc(&ctx->d_st_sum, Hc * CG)); A(dalloc(&ctx->d_st_sq, Hc * CG));
+  A(dalloc(&ctx->d_ppos, Nc * 3)); A(dalloc(&ctx->d_pnrm, Nc * 3)); A(dalloc(&ctx->d_pwi, Nc * 3));
+  A(dalloc(&ctx->d_ppow, Nc * 3)); A(dalloc(&ctx->d_pdepth, Nc));
+  A(dalloc(&ctx->recs.rec0, Nc)); A(dalloc(&ctx->recs.rec1, Nc));
+  A(dalloc(&ctx->recs.rec2, Nc)); A(dalloc(&ctx->recs.rec3, Nc));
+  A(dalloc(&ctx->sort.keys_a, Nc)); A(dalloc(&ctx->sort.vals_a, Nc));
+  A(dalloc(&ctx->sort.keys_b, Nc)); A(dalloc(&ctx->sort.vals_b, Nc));
+  A(dalloc(&ctx->sort.hist, radix_hist_entries((uint32_t)Nc)));
+  A(dalloc(&ctx->d_hdr, 1)); A(dalloc(&ctx->d_bounds, 6)); A(dalloc(&ctx->d_cell, 1));
+  A(cudaMallocHost(&ctx->h_hdr, sizeof(GridHeader)));
+  A(cudaMallocHost(&ctx->h_bounds_init, sizeof(long long) * 6));
+  A(cudaMallocHost(&ctx->h_cell, sizeof(double)));
+  A(cudaMallocHost(&ctx->h_counters, sizeof(unsigned long long) * 8));
+  A(dalloc(&ctx->o_gather_r, Hc)); A(dalloc(&ctx->o_stat, Hc)); A(dalloc(&ctx->o_crit, Hc));
+  A(dalloc(&ctx->o_flux, Hc * 3)); A(dalloc(&ctx->o_flags, Hc)); A(dalloc(&ctx->o_rad, Hc * 3));
+  A(dalloc(&ctx->o_acc, Hc));
+  A(dalloc(&ctx->d_counters, 4)); A(dalloc(&ctx->d_iter_tr, 2)); A(dalloc(&ctx->d_work, 1));
+  A(dalloc(&ctx->d_rmax_bits, 1));
+  if (e != cudaSuccess) {
+    int rc = cuda_fail(ctx, e, "fppm_gpu_create allocation");
+    fppm_gpu_destroy(ctx);
+    return rc == FPPM_ERR_CUDA ? FPPM_ERR_CAPACITY : rc;
+  }
+  for (int a = 0; a < 3; ++a) {
+    ctx->h_bounds_init[a] = LLONG_MAX;
+    ctx->h_bounds_init[3 + a] = LLONG_MIN;
+  }
+  cudaMemsetAsync(ctx->d_counters, 0, sizeof(unsigned long long) * 4, ctx->stream);
+  if (c.policy == FPPM_POLICY_CHI2) {
+    int st = 0;
+    ctx->chi2_crit = host_chi2_quantile(1.0 - c.alpha_chi2, (double)(ctx->G - 1), &st);
+    if (st) {
+      fppm_gpu_destroy(ctx);
+      return FPPM_ERR_INVALID_ARGUMENT;
+    }
+  }
+  int rc = ensure_crit(ctx, std::max<uint64_t>(64, 2));
+  if (rc) {
+    fppm_gpu_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return FPPM_OK;
+}
+
+int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
+  if (!ctx) return FPPM_OK;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  void *dev[] = {ctx->d_pos, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb, ctx->d_K, ctx->d_eye,
+                 ctx->d_gathered, ctx->d_radius, ctx->d_t, ctx->d_st_cnt, ctx->d_st_sum,
+                 ctx->d_st_sq, ctx->d_ppos, ctx->d_pnrm, ctx->d_pwi, ctx->d_ppow, ctx->d_pdepth,
+                 ctx->recs.rec0, ctx->recs.rec1, ctx->recs.rec2, ctx->recs.rec3, ctx->sort.keys_a,
+                 ctx->sort.vals_a, ctx->sort.keys_b, ctx->sort.vals_b, ctx->sort.hist,
+                 ctx->d_cell_start, ctx->d_hdr, ctx->d_bounds, ctx->d_cell,
+                 ctx->o_gather_r, ctx->o_stat, ctx->o_crit, ctx->o_flux, ctx->o_flags, ctx->o_rad,
+                 ctx->o_acc, ctx->snap_cnt, ctx->snap_sum, ctx->snap_sq, ctx->d_counters,
+                 ctx->d_iter_tr, ctx->d_work, ctx->d_rmax_bits, ctx->d_crit, ctx->d_scratch};
+  for (void *p : dev)
+    if (p) cudaFree(p);
+  if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
+  if (ctx->h_bounds_init) cudaFreeHost(ctx->h_bounds_init);
+  if (ctx->h_cell) cudaFreeHost(ctx->h_cell);
+  if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return FPPM_OK;
+}
+
+int fppm_gpu_synchronize(fppm_gpu_ctx *ctx) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  return FPPM_OK;
+}
+
+void *fppm_gpu_stream(fppm_gpu_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int fppm_gpu_device_view_get(fppm_gpu_ctx *ctx, fppm_gpu_device_view *v) {
+  if (!ctx || !v) return FPPM_ERR_INVALID_ARGUMENT;
+  v->photon_pos = ctx->d_ppos;
+  v->photon_normal = ctx->d_pnrm;
+  v->photon_wi = ctx->d_pwi;
+  v->photon_power = ctx->d_ppow;
+  v->photon_depth = ctx->d_pdepth;
+  v->radius = ctx->d_radius;
+  v->counters = reinterpret_cast<uint64_t *>(ctx->d_counters);
+  return FPPM_OK;
+}
+
+// ------------------------------------------------------------------ regions
+static int finish_hitpoints(fppm_gpu_ctx *ctx, uint32_t n, bool has_gathered) {
+  if (!has_gathered) FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_gathered, 1, std::max<uint32_t>(n, 1), ctx->stream));
+  FPPM_CUDA_OK(launch_hit_weights(ctx->stream, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb, n, ctx->d_K));
+  const bool reset = n != ctx->H;
+  ctx->H = n;
+  if (reset) return fppm_gpu_reset_regions(ctx);
+  return FPPM_OK;
+}
+
+static int set_hitpoints(fppm_gpu_ctx *ctx, const fppm_hitpoints *hp, uint32_t n, cudaMemcpyKind kind) {
+  if (!ctx || !hp) return FPPM_ERR_INVALID_ARGUMENT;
+  if (n > ctx->cfg.max_hitpoints) return fail(ctx, FPPM_ERR_CAPACITY, "hit points exceed max_hitpoints");
+  if (n && (!hp->pos || !hp->normal || !hp->wo || !hp->throughput || !hp->albedo || !hp->eye_depth))
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null hit point array");
+  const size_t b3 = sizeof(double3) * n;
+  cudaStream_t s = ctx->stream;
+  if (n) {
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_pos, hp->pos, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_nrm, hp->normal, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_wo, hp->wo, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_thr, hp->throughput, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_alb, hp->albedo, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_eye, hp->eye_depth, sizeof(uint32_t) * n, kind, s));
+    if (hp->gathered) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_gathered, hp->gathered, n, kind, s));
+  }
+  return finish_hitpoints(ctx, n, hp->gathered != nullptr);
+}
+
+int fppm_gpu_set_hitpoints(fppm_gpu_ctx *ctx, const fppm_hitpoints *host, uint32_t n) {
+  return set_hitpoints(ctx, host, n, cudaMemcpyHostToDevice);
+}
+
+int fppm_gpu_set_hitpoints_device(fppm_gpu_ctx *ctx, const fppm_hitpoints *dev, uint32_t n) {
+  return set_hitpoints(ctx, dev, n, cudaMemcpyDeviceToDevice);
+}
+
+int fppm_gpu_generate_raster_hitpoints(fppm_gpu_ctx *ctx, uint32_t W) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  const uint64_t n = (uint64_t)W * W;
+  if (n > ctx->cfg.max_hitpoints) return fail(ctx, FPPM_ERR_CAPACITY, "raster exceeds max_hitpoints");
+  launch_raster_hitpoints(ctx->stream, W, ctx->d_pos, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb,
+                          ctx->d_eye, ctx->d_gathered, ctx->sms);
+  FPPM_CUDA_OK(cudaGetLastError());
+  return finish_hitpoints(ctx, (uint32_t)n, true);
+}
+
+int fppm_gpu_reset_regions(fppm_gpu_ctx *ctx) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  const size_t H = std::max<uint32_t>(ctx->H, 1), CG = (size_t)ctx->G * ctx->C;
+  k_fill_regions<<<(unsigned)((H + 255) / 256), 256, 0, ctx->stream>>>(ctx->d_radius, ctx->d_t, ctx->H,
+                                                                     ctx->cfg.initial_radius);
+  note_launches(1);
+  FPPM_CUDA_OK(cudaGetLastError());
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_st_cnt, 0, sizeof(unsigned long long) * H * CG, ctx->stream));
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_st_sum, 0, sizeof(double) * H * CG, ctx->stream));
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_st_sq, 0, sizeof(double) * H * CG, ctx->stream));
+  ctx->end_calls = 0;
+  return FPPM_OK;
+}
+
+int fppm_gpu_get_regions(fppm_gpu_ctx *ctx, double *radius, uint64_t *t, uint64_t *stat_count,
+                         double *stat_sum, double *stat_sum_sq) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  const size_t H = ctx->H, CG = (size_t)ctx->G * ctx->C;
+  int rc;
+  if ((rc = copy_out(ctx, radius, ctx->d_radius, sizeof(double) * H))) return rc;
+  if ((rc = copy_out(ctx, stat_count, ctx->d_st_cnt, sizeof(unsigned long long) * H * CG))) return rc;
+  if ((rc = copy_out(ctx, stat_sum, ctx->d_st_sum, sizeof(double) * H * CG))) return rc;
+  if ((rc = copy_out(ctx, stat_sum_sq, ctx->d_st_sq, sizeof(double) * H * CG))) return rc;
+  std::vector<uint32_t> t32(t ? H : 0);
+  if (t && (rc = copy_out(ctx, t32.data(), ctx->d_t, sizeof(uint32_t) * H))) return rc;
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  for (size_t h = 0; t && h < H; ++h) t[h] = t32[h];
+  return FPPM_OK;
+}
+
+int fppm_gpu_set_regions(fppm_gpu_ctx *ctx, const double *radius, const uint64_t *t,
+                         const uint64_t *stat_count, const double *stat_sum,
+                         const double *stat_sum_sq) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  const size_t H = ctx->H, CG = (size_t)ctx->G * ctx->C;
+  cudaStream_t s = ctx->stream;
+  if (radius) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_radius, radius, sizeof(double) * H, cudaMemcpyHostToDevice, s));
+  if (stat_count) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_st_cnt, stat_count, 8 * H * CG, cudaMemcpyHostToDevice, s));
+  if (stat_sum) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_st_sum, stat_sum, 8 * H * CG, cudaMemcpyHostToDevice, s));
+  if (stat_sum_sq) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_st_sq, stat_sum_sq, 8 * H * CG, cudaMemcpyHostToDevice, s));
+  if (t) {
+    std::vector<uint32_t> t32(H);
+    uint64_t tmax = 0;
+    for (size_t h = 0; h < H; ++h) {
+      if (t[h] < 1 || t[h] > 0xffffffffull) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "t out of range");
+      t32[h] = (uint32_t)t[h];
+      tmax = std::max<uint64_t>(tmax, t[h]);
+    }
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_t, t32.data(), sizeof(uint32_t) * H, cudaMemcpyHostToDevice, s));
+    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    if (tmax > ctx->end_calls + 1) ctx->end_calls = tmax - 1;
+  }
+  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  return FPPM_OK;
+}
+
+static int device_max_radius(fppm_gpu_ctx *ctx, double *dst) {
+  FPPM_CUDA_OK(cudaMemsetAsync(dst, 0, sizeof(double), ctx->stream));
+  if (ctx->H) {
+    unsigned blocks = (ctx->H + 255) / 256;
+    blocks = std::min<unsigned>(blocks, (unsigned)ctx->sms * 4);
+    k_max_radius<<<blocks, 256, 0, ctx->stream>>>(ctx->d_radius, ctx->H, dst);
+    note_launches(1);
+    FPPM_CUDA_OK(cudaGetLastError());
+  }
+  return FPPM_OK;
+}
+
+int fppm_gpu_max_radius(fppm_gpu_ctx *ctx, double *r_max) {
+  if (!ctx || !r_max) return FPPM_ERR_INVALID_ARGUMENT;
+  int rc = device_max_radius(ctx, ctx->d_cell);
+  if (rc) return rc;
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_cell, ctx->d_cell, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  *r_max = *ctx->h_cell;
+  return FPPM_OK;
+}
+
+// ------------------------------------------------------------------ photons + grid
+static void use_staging(fppm_gpu_ctx *ctx) {
+  ctx->in_pos = ctx->d_ppos;
+  ctx->in_nrm = ctx->d_pnrm;
+  ctx->in_wi = ctx->d_pwi;
+  ctx->in_pow = ctx->d_ppow;
+  ctx->in_depth = ctx->d_pdepth;
+}
+
+static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cudaMemcpyKind kind) {
+  if (!ctx || !p) return FPPM_ERR_INVALID_ARGUMENT;
+  if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
+  if (n && (!p->pos || !p->normal || !p->wi || !p->power || !p->depth))
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
+  cudaStream_t s = ctx->stream;
+  const size_t b3 = sizeof(float) * 3 * n;
+  if (n) {
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_ppos, p->pos, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_pnrm, p->normal, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_pwi, p->wi, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_ppow, p->power, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_pdepth, p->depth, sizeof(uint32_t) * n, kind, s));
+  }
+  ctx->N = n;
+  ctx->grid_valid = false;
+  use_staging(ctx);
+  return FPPM_OK;
+}
+
+int fppm_gpu_set_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n) {
+  return set_photons(ctx, host, n, cudaMemcpyHostToDevice);
+}
+
+// Zero copy: the grid build reads the caller's device arrays directly; they
+// must stay valid and unchanged until the next build_grid has been issued.
+int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint32_t n) {
+  if (!ctx || !dev) return FPPM_ERR_INVALID_ARGUMENT;
+  if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
+  if (n && (!dev->pos || !dev->normal || !dev->wi || !dev->power || !dev->depth))
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
+  ctx->in_pos = dev->pos;
+  ctx->in_nrm = dev->normal;
+  ctx->in_wi = dev->wi;
+  ctx->in_pow = dev->power;
+  ctx->in_depth = dev->depth;
+  ctx->N = n;
+  ctx->grid_valid = false;
+  return FPPM_OK;
+}
+
+int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed, uint64_t iteration,
+                              uint64_t begin, uint32_t n) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2)
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
+  if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
+  launch_generate_photons(ctx->stream, workload, seed, iteration, begin, n, ctx->d_ppos, ctx->d_pnrm,
+                          ctx->d_pwi, ctx->d_ppow, ctx->d_pdepth, ctx->sms);
+  FPPM_CUDA_OK(cudaGetLastError());
+  ctx->N = n;
+  ctx->grid_valid = false;
+  use_staging(ctx);
+  return FPPM_OK;
+}
+
+int fppm_gpu_generate_photons_to(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed,
+                                 uint64_t iteration, uint64_t begin, uint32_t n,
+                                 const fppm_photons *d) {
+  if (!ctx || !d) return FPPM_ERR_INVALID_ARGUMENT;
+  if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2)
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
+  if (n && (!d->pos || !d->normal || !d->wi || !d->power || !d->depth))
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
+  launch_generate_photons(ctx->stream, workload, seed, iteration, begin, n,
+                          const_cast<float *>(d->pos), const_cast<float *>(d->normal),
+                          const_cast<float *>(d->wi), const_cast<float *>(d->power),
+                          const_cast<uint32_t *>(d->depth), ctx->sms);
+  FPPM_CUDA_OK(cudaGetLastError());
+  return FPPM_OK;
+}
+
+int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi, float *power,
+                         uint32_t *depth) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->in_pos) use_staging(ctx);
+  const size_t b3 = sizeof(float) * 3 * ctx->N;
+  int rc;
+  if ((rc = copy_out(ctx, pos, ctx->in_pos, b3))) return rc;
+  if ((rc = copy_out(ctx, normal, ctx->in_nrm, b3))) return rc;
+  if ((rc = copy_out(ctx, wi, ctx->in_wi, b3))) return rc;
+  if ((rc = copy_out(ctx, power, ctx->in_pow, b3))) return rc;
+  if ((rc = copy_out(ctx, depth, ctx->in_depth, sizeof(uint32_t) * ctx->N))) return rc;
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  return FPPM_OK;
+}
+
+int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = ctx->stream;
+  ctx->grid_valid = false;
+  if (cell_size > 0.0) {
+    *ctx->h_cell = cell_size;
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_cell, ctx->h_cell, sizeof(double), cudaMemcpyHostToDevice, s));
+  } else {
+    int rc = device_max_radius(ctx, ctx->d_cell);  // integrator.cpp:159-161
+    if (rc) return rc;
+  }
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_bounds, ctx->h_bounds_init, sizeof(long long) * 6,
+                               cudaMemcpyHostToDevice, s));
+  if (!ctx->in_pos) use_staging(ctx);
+  launch_cell_bounds(s, ctx->in_pos, ctx->N, ctx->d_cell, ctx->d_bounds, ctx->sms);
+  launch_grid_header(s, ctx->d_bounds, ctx->d_cell, ctx->N, ctx->cfg.max_cells, ctx->d_hdr);
+  FPPM_CUDA_OK(cudaGetLastError());
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_hdr, ctx->d_hdr, sizeof(GridHeader), cudaMemcpyDeviceToHost, s));
+  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  const GridHeader g = *ctx->h_hdr;
+  if (!(g.cell > 0.0)) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "PhotonGrid: cell size must be positive");
+  if (!g.ok) return fail(ctx, FPPM_ERR_CAPACITY, "grid bounding box exceeds max_cells dense cells");
+  if (g.ncells + 1 > ctx->cell_cap) {
+    if (ctx->d_cell_start) cudaFree(ctx->d_cell_start);
+    ctx->d_cell_start = nullptr;
+    ctx->cell_cap = 0;
+    const unsigned long long cap = std::max<unsigned long long>(g.ncells + 1, 1024);
+    FPPM_CUDA_OK(cudaMalloc(&ctx->d_cell_start, sizeof(uint32_t) * cap));
+    ctx->cell_cap = cap;
+  }
+  launch_dense_keys(s, ctx->in_pos, ctx->N, ctx->d_hdr, ctx->sort.keys_a, ctx->sort.vals_a, ctx->sms);
+  FPPM_CUDA_OK(radix_sort_pairs(s, ctx->sort, ctx->N, g.key_bits, &ctx->d_skeys, &ctx->d_order));
+  launch_cell_start(s, ctx->d_skeys, ctx->N, ctx->d_hdr, ctx->d_cell_start, g.ncells, ctx->sms);
+  launch_permute(s, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,
+                 ctx->in_depth, ctx->recs, ctx->sms);
+  FPPM_CUDA_OK(cudaGetLastError());
+  ctx->grid_valid = true;
+  return FPPM_OK;
+}
+
+int fppm_gpu_export_grid(fppm_gpu_ctx *ctx, uint64_t *keys, uint32_t *begin, uint32_t *end,
+                         uint32_t *order, uint64_t *ncells) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "grid not built");
+  const uint32_t n = ctx->N;
+  std::vector<uint32_t> sk(n), ord(n);
+  if (n) {
+    FPPM_CUDA_OK(cudaMemcpyAsync(sk.data(), ctx->d_skeys, 4ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ord.data(), ctx->d_order, 4ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  const GridHeader g = *ctx->h_hdr;
+  uint64_t nc = 0;
+  const uint64_t bias = 1ull << 20;  // photon_map.cpp:11
+  for (uint32_t i = 0; i < n; ++i) {
+    if (i == 0 || sk[i] != sk[i - 1]) {
+      const unsigned long long k = sk[i];
+      const long long X = (long long)(k / ((unsigned long long)g.ny * g.nz));
+      const long long Y = (long long)((k / (unsigned long long)g.nz) % (unsigned long long)g.ny);
+      const long long Z = (long long)(k % (unsigned long long)g.nz);
+      const uint64_t ix = (uint64_t)(X + g.ix0), iy = (uint64_t)(Y + g.iy0), iz = (uint64_t)(Z + g.iz0);
+      if (keys) keys[nc] = ((ix + bias) << 42) | ((iy + bias) << 21) | (iz + bias);
+      if (begin) begin[nc] = i;
+      ++nc;
+    }
+    if (end) end[nc - 1] = i + 1;
+  }
+  if (order && n) std::memcpy(order, ord.data(), 4ull * n);
+  if (ncells) *ncells = nc;
+  return FPPM_OK;
+}
+
+int fppm_gpu_query_ball(fppm_gpu_ctx *ctx, const double *centers, const double *radii, uint32_t nq,
+                        uint64_t *offsets, uint32_t *indices, uint64_t cap, uint64_t *total) {
+  if (!ctx || (nq && (!centers || !radii || !offsets))) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "grid not built");
+  const GridHeader g = *ctx->h_hdr;
+  if (ctx->N > 0)
+    for (uint32_t q = 0; q < nq; ++q)
+      if (radii[q] > g.cell)  // photon_map.cpp:57-58
+        return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "PhotonGrid: query radius exceeds cell size");
+  const size_t need = sizeof(double) * 4 * nq + sizeof(unsigned long long) * 2 * (nq + 1) +
+                      sizeof(uint32_t) * (cap + 1) + 256;
+  FPPM_CUDA_OK(ensure_scratch(ctx, need));
+  char *p = static_cast<char *>(ctx->d_scratch);
+  double *d_c = reinterpret_cast<double *>(p);
+  double *d_r = d_c + 3 * (size_t)nq;
+  unsigned long long *d_cnt = reinterpret_cast<unsigned long long *>(d_r + nq);
+  unsigned long long *d_off = d_cnt + nq + 1;
+  uint32_t *d_out = reinterpret_cast<uint32_t *>(d_off + nq + 1);
+  cudaStream_t s = ctx->stream;
+  if (nq) {
+    FPPM_CUDA_OK(cudaMemcpyAsync(d_c, centers, sizeof(double) * 3 * nq, cudaMemcpyHostToDevice, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(d_r, radii, sizeof(double) * nq, cudaMemcpyHostToDevice, s));
+  }
+  launch_query_ball(s, d_c, d_r, nq, ctx->d_hdr, ctx->d_cell_start, ctx->recs.rec0, ctx->d_order,
+                    d_cnt, nullptr, nullptr, 0);
+  FPPM_CUDA_OK(cudaGetLastError());
+  std::vector<unsigned long long> cnt(nq);
+  if (nq) FPPM_CUDA_OK(cudaMemcpyAsync(cnt.data(), d_cnt, 8ull * nq, cudaMemcpyDeviceToHost, s));
+  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  uint64_t run = 0;
+  for (uint32_t q = 0; q < nq; ++q) {
+    offsets[q] = run;
+    run += cnt[q];
+  }
+  offsets[nq] = run;
+  if (total) *total = run;
+  if (run <= cap && indices && run) {
+    FPPM_CUDA_OK(cudaMemcpyAsync(d_off, offsets, 8ull * (nq + 1), cudaMemcpyHostToDevice, s));
+    launch_query_ball(s, d_c, d_r, nq, ctx->d_hdr, ctx->d_cell_start, ctx->recs.rec0, ctx->d_order,
+                      nullptr, d_off, d_out, 1);
+    FPPM_CUDA_OK(cudaGetLastError());
+    FPPM_CUDA_OK(cudaMemcpyAsync(indices, d_out, 4ull * run, cudaMemcpyDeviceToHost, s));
+    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  } else if (run > cap && indices) {
+    return fail(ctx, FPPM_ERR_CAPACITY, "query result exceeds cap");
+  }
+  return FPPM_OK;
+}
+
+// ------------------------------------------------------------------ hot path
+static int ensure_snapshots(fppm_gpu_ctx *ctx) {
+  if (ctx->snap_cnt) return FPPM_OK;
+  const size_t n = (size_t)std::max<uint32_t>(ctx->cfg.max_hitpoints, 1) * ctx->G * ctx->C;
+  FPPM_CUDA_OK(dalloc(&ctx->snap_cnt, n));
+  FPPM_CUDA_OK(dalloc(&ctx->snap_sum, n));
+  FPPM_CUDA_OK(dalloc(&ctx->snap_sq, n));
+  return FPPM_OK;
+}
+
+static int fill_summary(fppm_gpu_ctx *ctx, fppm_gpu_summary *sm) {
+  cudaStream_t s = ctx->stream;
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 32, cudaMemcpyDeviceToHost, s));
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_counters + 4, ctx->d_iter_tr, 8, cudaMemcpyDeviceToHost, s));
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_counters + 5, ctx->d_rmax_bits, 8, cudaMemcpyDeviceToHost, s));
+  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  const unsigned long long *c = ctx->h_counters;
+  sm->accepted = c[0] - ctx->last_counters[0];
+  sm->candidates = c[1] - ctx->last_counters[1];
+  sm->exact_pairs = c[2] - ctx->last_counters[2];
+  sm->ambiguous_pairs = c[3] - ctx->last_counters[3];
+  for (int i = 0; i < 4; ++i) ctx->last_counters[i] = c[i];
+  const unsigned int *tr = reinterpret_cast<const unsigned int *>(c + 4);
+  sm->tested = tr[0];
+  sm->rejected = tr[1];
+  double rmax;
+  std::memcpy(&rmax, c + 5, 8);
+  sm->r_max_next = rmax;
+  sm->cell_size = ctx->h_hdr->cell;
+  sm->cells = ctx->h_hdr->ncells;
+  return FPPM_OK;
+}
+
+int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *out,
+                         fppm_gpu_summary *summary) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "gather before build_grid");
+  int rc = ensure_crit(ctx, ctx->end_calls + 2);
+  if (rc) return rc;
+  const bool snap = out && (out->stat_count || out->stat_sum || out->stat_sum_sq);
+  if (snap && (rc = ensure_snapshots(ctx))) return rc;
+  cudaStream_t s = ctx->stream;
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned int), s));
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_iter_tr, 0, 2 * sizeof(unsigned int), s));
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_rmax_bits, 0, sizeof(unsigned long long), s));
+  GatherArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.pos = ctx->d_pos; A.nrm = ctx->d_nrm; A.K = ctx->d_K;
+  A.eye_depth = ctx->d_eye; A.gathered = ctx->d_gathered;
+  A.radius = ctx->d_radius; A.t = ctx->d_t;
+  A.st_cnt = ctx->d_st_cnt; A.st_sum = ctx->d_st_sum; A.st_sq = ctx->d_st_sq;
+  A.H = ctx->H;
+  A.rec0 = ctx->recs.rec0; A.rec1 = ctx->recs.rec1; A.rec2 = ctx->recs.rec2; A.rec3 = ctx->recs.rec3;
+  A.cell_start = ctx->d_cell_start; A.grid = ctx->d_hdr;
+  A.na = ctx->cfg.n_annuli; A.ns = ctx->cfg.n_sectors;
+  A.max_depth = ctx->cfg.max_depth; A.guard = ctx->cfg.normal_guard_cos;
+  A.end = end_params(ctx, iteration);
+  A.o_gather_r = ctx->o_gather_r; A.o_stat = ctx->o_stat; A.o_crit = ctx->o_crit;
+  A.o_flux = ctx->o_flux; A.o_flags = ctx->o_flags; A.o_radiance = ctx->o_rad;
+  A.o_accepted = ctx->o_acc;
+  if (snap) { A.snap_cnt = ctx->snap_cnt; A.snap_sum = ctx->snap_sum; A.snap_sq = ctx->snap_sq; }
+  A.counters = ctx->d_counters; A.iter_tr = ctx->d_iter_tr; A.work = ctx->d_work;
+  A.rmax_bits = ctx->d_rmax_bits;
+  if (ctx->H) FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
+  ctx->end_calls++;
+  if (out && (rc = copy_iter_out(ctx, out, true))) return rc;
+  if (summary && (rc = fill_summary(ctx, summary))) return rc;
+  return FPPM_OK;
+}
+
+int fppm_gpu_iterate(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *out,
+                     fppm_gpu_summary *summary) {
+  int rc = fppm_gpu_build_grid(ctx, 0.0);
+  if (rc) return rc;
+  return fppm_gpu_gather_test(ctx, iteration, out, summary);
+}
+
+int fppm_gpu_accumulate(fppm_gpu_ctx *ctx, const uint32_t *region, const double *y,
+                        const double *value, uint32_t n) {
+  if (!ctx || (n && (!region || !y || !value))) return FPPM_ERR_INVALID_ARGUMENT;
+  if (n == 0) return FPPM_OK;
+  const size_t need = (4 + 16 + 24 + 4) * (size_t)n + 64;
+  FPPM_CUDA_OK(ensure_scratch(ctx, need));
+  char *p = static_cast<char *>(ctx->d_scratch);
+  double2 *d_y = reinterpret_cast<double2 *>(p);
+  double *d_v = reinterpret_cast<double *>(d_y + n);
+  uint32_t *d_reg = reinterpret_cast<uint32_t *>(d_v + 3 * (size_t)n);
+  int *d_sec = reinterpret_cast<int *>(d_reg + n);
+  int *d_err = d_sec + n;
+  cudaStream_t s = ctx->stream;
+  FPPM_CUDA_OK(cudaMemcpyAsync(d_y, y, 16ull * n, cudaMemcpyHostToDevice, s));
+  FPPM_CUDA_OK(cudaMemcpyAsync(d_v, value, 24ull * n, cudaMemcpyHostToDevice, s));
+  FPPM_CUDA_OK(cudaMemcpyAsync(d_reg, region, 4ull * n, cudaMemcpyHostToDevice, s));
+  FPPM_CUDA_OK(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+  FPPM_CUDA_OK(launch_samples(s, d_reg, d_y, d_v, n, ctx->d_radius, ctx->H, ctx->cfg.n_annuli,
+                              ctx->cfg.n_sectors, ctx->C, d_sec, d_err, nullptr, nullptr, nullptr, 0));
+  int herr = 0;
+  FPPM_CUDA_OK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  if (herr == FPPM_ERR_DOMAIN) return fail(ctx, FPPM_ERR_DOMAIN, "sector_index: point outside the kernel disk");
+  if (herr) return fail(ctx, herr, "region index out of range");
+  FPPM_CUDA_OK(launch_samples(s, d_reg, d_y, d_v, n, ctx->d_radius, ctx->H, ctx->cfg.n_annuli,
+                              ctx->cfg.n_sectors, ctx->C, d_sec, d_err, ctx->d_st_cnt, ctx->d_st_sum,
+                              ctx->d_st_sq, 1));
+  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  return FPPM_OK;
+}
+
+int fppm_gpu_set_samples_per_iteration(fppm_gpu_ctx *ctx, uint64_t samples_per_iteration) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (samples_per_iteration == ctx->cfg.samples_per_iteration) return FPPM_OK;
+  ctx->cfg.samples_per_iteration = samples_per_iteration;
+  ctx->crit.clear();  // F_c depends on m = t * J
+  return ensure_crit(ctx, ctx->end_calls + 2);
+}
+
+int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *out) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  int rc = ensure_crit(ctx, ctx->end_calls + 2);
+  if (rc) return rc;
+  const bool snap = out && (out->stat_count || out->stat_sum || out->stat_sum_sq);
+  if (snap && (rc = ensure_snapshots(ctx))) return rc;
+  EndArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.radius = ctx->d_radius; A.t = ctx->d_t;
+  A.st_cnt = ctx->d_st_cnt; A.st_sum = ctx->d_st_sum; A.st_sq = ctx->d_st_sq;
+  A.H = ctx->H; A.G = ctx->G; A.C = ctx->C;
+  A.end = end_params(ctx, iteration);
+  A.o_gather_r = ctx->o_gather_r; A.o_stat = ctx->o_stat; A.o_crit = ctx->o_crit;
+  A.o_flags = ctx->o_flags;
+  if (snap) { A.snap_cnt = ctx->snap_cnt; A.snap_sum = ctx->snap_sum; A.snap_sq = ctx->snap_sq; }
+  FPPM_CUDA_OK(launch_end_iteration(ctx->stream, A));
+  ctx->end_calls++;
+  if (out) return copy_iter_out(ctx, out, false);
+  return FPPM_OK;
+}
+
+uint64_t fppm_gpu_kernel_launches(void) { return g_kernel_launches.load(); }
+
+int fppm_gpu_counters(fppm_gpu_ctx *ctx, uint64_t out[4]) {
+  if (!ctx || !out) return FPPM_ERR_INVALID_ARGUMENT;
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 32, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < 4; ++i) out[i] = ctx->h_counters[i];
+  return FPPM_OK;
+}
+
+double fppm_gpu_schedule_radius(double base, double alpha, uint64_t i) {
+  return host_schedule_radius(base, alpha, i);
+}
+
+double fppm_gpu_f_quantile(double p, double d1, double d2, int *status) {
+  if (status) *status = FPPM_OK;
+  return host_f_quantile(p, d1, d2, status);
+}
+
+double fppm_gpu_chi2_quantile(double p, double df, int *status) {
+  if (status) *status = FPPM_OK;
+  return host_chi2_quantile(p, df, status);
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// gather.cuh -- kernel argument blocks shared by gather.cu and context.cu.
+#pragma once
+#include <atomic>
+
+#include "common.cuh"
+
+namespace fppm_b200 {
+
+// every kernel launch issued by this library (reported as gpu_launches)
+extern std::atomic<unsigned long long> g_kernel_launches;
+inline void note_launches(int n) { g_kernel_launches.fetch_add((unsigned long long)n); }
+
+constexpr int kGatherThreads = 256;
+constexpr int kMaxCG = 96;  // n_a * n_s <= 32, times up to 3 channels
+
+// end-of-iteration policy parameters (gather.cpp:74-144)
+struct EndParams {
+  int policy;
+  int override_decision;
+  unsigned long long J;      // samples per iteration
+  double k;                  // RadiusSchedule::k
+  double floor_next;         // schedule_radius(r_min_base, alpha, i + 1)
+  double sched_next;         // schedule_radius(r_1, alpha, i + 1)
+  const double *crit;        // F_c by t (host-computed f_quantile table)
+  uint32_t crit_len;
+  double chi2_crit;
+};
+
+struct GatherArgs {
+  // regions
+  const double3 *pos, *nrm, *K;
+  const uint32_t *eye_depth;
+  const uint8_t *gathered;
+  double *radius;
+  uint32_t *t;
+  unsigned long long *st_cnt;
+  double *st_sum, *st_sq;
+  uint32_t H;
+  // grid
+  const float4 *rec0, *rec1, *rec2, *rec3;
+  const uint32_t *cell_start;
+  const GridHeader *grid;
+  // config
+  int na, ns;
+  uint32_t max_depth;
+  double guard;
+  EndParams end;
+  // outputs (device, nullable)
+  double *o_gather_r, *o_stat, *o_crit, *o_flux;
+  uint8_t *o_flags;
+  float *o_radiance;
+  uint32_t *o_accepted;
+  unsigned long long *snap_cnt;
+  double *snap_sum, *snap_sq;
+  // counters
+  unsigned long long *counters;  // cumulative [accepted, candidates, exact, ambiguous]
+  unsigned int *iter_tr;         // this launch [tested, rejected]
+  unsigned int *work;
+  unsigned long long *rmax_bits;
+};
+
+struct EndArgs {
+  double *radius;
+  uint32_t *t;
+  unsigned long long *st_cnt;
+  double *st_sum, *st_sq;
+  uint32_t H;
+  int G, C;
+  EndParams end;
+  double *o_gather_r, *o_stat, *o_crit;
+  uint8_t *o_flags;
+  unsigned long long *snap_cnt;
+  double *snap_sum, *snap_sq;
+};
+
+cudaError_t launch_gather_test(cudaStream_t s, const GatherArgs &A, int C, int sms);
+cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2 *y,
+                           const double *value, uint32_t n, const double *radius, uint32_t H,
+                           int na, int ns, int C, int *sectors, int *err,
+                           unsigned long long *st_cnt, double *st_sum, double *st_sq, int phase);
+cudaError_t launch_end_iteration(cudaStream_t s, const EndArgs &A);
+cudaError_t launch_hit_weights(cudaStream_t s, const double3 *nrm, const double3 *wo,
+                               const double3 *thr, const double3 *alb, uint32_t H, double3 *K);
+
+// grid.cu
+struct SortScratch {
+  uint32_t *keys_a, *vals_a, *keys_b, *vals_b;
+  uint32_t *hist;  // [digit][tile] + digit totals
+};
+size_t radix_hist_entries(uint32_t n);
+cudaError_t radix_sort_pairs(cudaStream_t s, SortScratch &sc, uint32_t n, uint32_t bits,
+                             uint32_t **keys_sorted, uint32_t **vals_sorted);
+void launch_cell_bounds(cudaStream_t s, const float *pos, uint32_t n, const double *cell,
+                        long long *bounds, int sms);
+void launch_grid_header(cudaStream_t s, const long long *bounds, const double *cell, uint32_t n,
+                        unsigned long long max_cells, GridHeader *hdr);
+void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridHeader *hdr,
+                       uint32_t *keys, uint32_t *vals, int sms);
+void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const GridHeader *hdr,
+                       uint32_t *start, unsigned long long ncells, int sms);
+void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const float *pos,
+                    const float *nrm, const float *wi, const float *pw, const uint32_t *depth,
+                    const PhotonRecs &r, int sms);
+void launch_query_ball(cudaStream_t s, const double *centers, const double *radii, uint32_t nq,
+                       const GridHeader *hdr, const uint32_t *start, const float4 *rec0,
+                       const uint32_t *order, unsigned long long *counts,
+                       const unsigned long long *offsets, uint32_t *out, int fill);
+
+// generate.cu
+void launch_generate_photons(cudaStream_t s, int workload, uint64_t seed, uint64_t iteration,
+                             uint64_t begin, uint32_t n, float *pos, float *nrm, float *wi,
+                             float *pw, uint32_t *depth, int sms);
+void launch_raster_hitpoints(cudaStream_t s, uint32_t W, double3 *pos, double3 *nrm,
+                             double3 *wo, double3 *thr, double3 *alb, uint32_t *eye_depth,
+                             uint8_t *gathered, int sms);
+
+// host_stats.cpp
+double host_f_quantile(double p, double d1, double d2, int *status);
+double host_chi2_quantile(double p, double df, int *status);
+double host_schedule_radius(double base, double alpha, uint64_t i);
+
+}  // namespace fppm_b200

@@ -1,0 +1,462 @@
+// grid.cu -- uniform hash-grid build on the device (PhotonGrid, photon_map.cpp:26-51).
+//
+//  1. k_cell_bounds: per-photon fp64 cell coordinates floor(x * (1/cell))
+//     (photon_map.cpp:13-15), block-reduced min/max -> grid bounding box.
+//  2. k_grid_header: dense dims; dense id = ((x*ny + y)*nz + z) preserves the
+//     reference key order (x major, z minor; photon_map.cpp:19-24).
+//  3. k_dense_keys + hand-written LSD radix sort of (dense id, photon index)
+//     pairs.  Stable, so ties keep insertion order exactly like std::sort on
+//     (key, index) pairs (photon_map.cpp:39-40).  Per pass: tile digit
+//     histograms, a two-kernel digit-major scan, and a stable scatter whose
+//     tile is staged in shared memory in sorted order and streamed out
+//     coalesced.
+//  4. k_cell_start: start offset per dense cell (the cells_ ranges).
+//  5. k_permute: 64-B photon records written in sorted order as four
+//     coalesced float4 SoA streams (the gather reads rec0 per candidate).
+#include "common.cuh"
+#include "gather.cuh"
+
+namespace fppm_b200 {
+
+std::atomic<unsigned long long> g_kernel_launches{0};
+
+// ------------------------------------------------------------------ block helpers
+template <typename T, typename Op>
+__device__ __forceinline__ T warp_reduce(T v, Op op) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// exclusive scan of one value per thread over a 256-thread block; returns the
+// block total through *total.
+__device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_t *s_warp,
+                                                             uint32_t *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < 8 ? s_warp[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < 8) s_warp[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  const uint32_t before = warp == 0 ? 0u : s_warp[warp - 1];
+  *total = s_warp[7];
+  __syncthreads();
+  return before + x - v;
+}
+
+// ------------------------------------------------------------------ bounds
+__global__ void __launch_bounds__(256)
+    k_cell_bounds(const float *__restrict__ pos, uint32_t n, const double *__restrict__ cell_ptr,
+                  long long *__restrict__ bounds /* [6]: min xyz, max xyz */) {
+  const double inv = dd(1.0, *cell_ptr);
+  long long mn[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+  long long mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const long long c = (long long)floor(dm((double)pos[3 * (size_t)i + a], inv));
+      mn[a] = min(mn[a], c);
+      mx[a] = max(mx[a], c);
+    }
+  }
+  __shared__ long long s[6][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const long long wmin = warp_reduce(mn[a], [](long long x, long long y) { return min(x, y); });
+    const long long wmax = warp_reduce(mx[a], [](long long x, long long y) { return max(x, y); });
+    if (lane == 0) {
+      s[a][warp] = wmin;
+      s[3 + a][warp] = wmax;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int a = threadIdx.x;
+    long long bmin = LLONG_MAX, bmax = LLONG_MIN;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      bmin = min(bmin, s[a][w]);
+      bmax = max(bmax, s[3 + a][w]);
+    }
+    atomicMin(&bounds[a], bmin);
+    atomicMax(&bounds[3 + a], bmax);
+  }
+}
+
+__global__ void k_grid_header(const long long *__restrict__ bounds, const double *__restrict__ cell_ptr,
+                              uint32_t n, unsigned long long max_cells,
+                              GridHeader *__restrict__ hdr) {
+  GridHeader g;
+  g.cell = *cell_ptr;
+  g.inv = dd(1.0, g.cell);
+  g.n = n;
+  g.pad = 0;
+  if (n == 0) {
+    g.ix0 = g.iy0 = g.iz0 = 0;
+    g.nx = g.ny = g.nz = 1;
+    g.ncells = 1;
+    g.key_bits = 1;
+    g.ok = 1;
+  } else {
+    g.ix0 = bounds[0];
+    g.iy0 = bounds[1];
+    g.iz0 = bounds[2];
+    g.nx = bounds[3] - bounds[0] + 1;
+    g.ny = bounds[4] - bounds[1] + 1;
+    g.nz = bounds[5] - bounds[2] + 1;
+    const double dcells = (double)g.nx * (double)g.ny * (double)g.nz;
+    g.ok = (g.nx > 0 && g.ny > 0 && g.nz > 0 && dcells <= (double)max_cells) ? 1u : 0u;
+    g.ncells = g.ok ? (unsigned long long)g.nx * (unsigned long long)g.ny * (unsigned long long)g.nz : 0;
+    uint32_t bits = 1;
+    while (bits < 32 && (1ull << bits) < g.ncells) ++bits;
+    g.key_bits = bits;
+  }
+  *hdr = g;
+}
+
+__global__ void __launch_bounds__(256)
+    k_dense_keys(const float *__restrict__ pos, uint32_t n, const GridHeader *__restrict__ hdr,
+                 uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+  const GridHeader g = *hdr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const size_t o = 3 * (size_t)i;
+    const long long x = (long long)floor(dm((double)pos[o], g.inv)) - g.ix0;
+    const long long y = (long long)floor(dm((double)pos[o + 1], g.inv)) - g.iy0;
+    const long long z = (long long)floor(dm((double)pos[o + 2], g.inv)) - g.iz0;
+    keys[i] = (uint32_t)((x * g.ny + y) * g.nz + z);
+    vals[i] = i;
+  }
+}
+
+// ------------------------------------------------------------------ radix sort
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kTile = kSortThreads * kSortItems;  // 4096 keys per tile
+constexpr int kRadixMax = 256;
+
+__global__ void __launch_bounds__(kSortThreads)
+    k_radix_upsweep(const uint32_t *__restrict__ keys, uint32_t n, int shift, uint32_t mask,
+                    uint32_t *__restrict__ hist /* [digit][tile] */, uint32_t tiles) {
+  __shared__ uint32_t s_h[kRadixMax];
+  for (int d = threadIdx.x; d < kRadixMax; d += blockDim.x) s_h[d] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * kTile;
+#pragma unroll 4
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint32_t i = base + it * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&s_h[(keys[i] >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d <= mask; d += blockDim.x) hist[d * tiles + blockIdx.x] = s_h[d];
+}
+
+// block d: total of digit d over all tiles
+__global__ void __launch_bounds__(256)
+    k_digit_totals(const uint32_t *__restrict__ hist, uint32_t tiles, uint32_t *__restrict__ totals) {
+  const uint32_t *row = hist + (size_t)blockIdx.x * tiles;
+  uint32_t s = 0;
+  for (uint32_t i = threadIdx.x; i < tiles; i += blockDim.x) s += row[i];
+  s = warp_reduce(s, [](uint32_t x, uint32_t y) { return x + y; });
+  __shared__ uint32_t sw[8];
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; ++w) t += sw[w];
+    totals[blockIdx.x] = t;
+  }
+}
+
+// block d: hist[d][*] <- exclusive digit-major prefix (all tiles of digits < d
+// first, then tiles of digit d in order).
+__global__ void __launch_bounds__(256)
+    k_hist_scan(uint32_t *__restrict__ hist, uint32_t tiles, const uint32_t *__restrict__ totals) {
+  __shared__ uint32_t s_warp[8];
+  uint32_t part = 0;
+  for (uint32_t d = threadIdx.x; d < blockIdx.x; d += blockDim.x) part += totals[d];
+  uint32_t base_total;
+  (void)block_exclusive_scan_256(part, s_warp, &base_total);
+  uint32_t carry = base_total;
+  uint32_t *row = hist + (size_t)blockIdx.x * tiles;
+  for (uint32_t c = 0; c < tiles; c += blockDim.x) {
+    const uint32_t i = c + threadIdx.x;
+    const uint32_t v = i < tiles ? row[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan_256(v, s_warp, &tot);
+    if (i < tiles) row[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+// Stable tile ranking: warp w owns tile elements [w*32*ITEMS, (w+1)*32*ITEMS)
+// in rounds of 32 consecutive keys; __match_any_sync groups equal digits, so
+// rank = per-warp running count + earlier peers in the round.  Per-digit
+// prefixes over warps keep warp order (= index order).
+__global__ void __launch_bounds__(kSortThreads)
+    k_radix_downsweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+                      uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
+                      uint32_t n, int shift, uint32_t mask,
+                      const uint32_t *__restrict__ hist_scan, uint32_t tiles) {
+  constexpr int kWarps = kSortThreads / kWarp;
+  __shared__ uint32_t s_wcnt[kWarps][kRadixMax];
+  __shared__ uint32_t s_dstart[kRadixMax];
+  __shared__ uint32_t s_gbase[kRadixMax];
+  __shared__ uint32_t s_keys[kTile];
+  __shared__ uint32_t s_vals[kTile];
+  __shared__ uint32_t s_warp[8];
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  for (int i = threadIdx.x; i < kWarps * kRadixMax; i += blockDim.x) (&s_wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile_base = blockIdx.x * kTile;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t k[kSortItems], v[kSortItems], rank[kSortItems];
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint32_t i = tile_base + (warp * kSortItems + it) * kWarp + lane;
+    const bool valid = i < n;
+    k[it] = valid ? keys_in[i] : 0u;
+    v[it] = valid ? vals_in[i] : 0u;
+    const uint32_t d = valid ? ((k[it] >> shift) & mask) : (uint32_t)kRadixMax;
+    const uint32_t peers = __match_any_sync(kFull, d);
+    const uint32_t before = valid ? s_wcnt[warp][d] : 0u;
+    __syncwarp();
+    if (valid && (__ffs(peers) - 1) == lane) s_wcnt[warp][d] = before + __popc(peers);
+    __syncwarp();
+    rank[it] = before + __popc(peers & lt_mask);
+  }
+  __syncthreads();
+  uint32_t total = 0;
+  if (threadIdx.x < kRadixMax) {
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s_wcnt[w][threadIdx.x];
+      s_wcnt[w][threadIdx.x] = total;
+      total += c;
+    }
+    s_gbase[threadIdx.x] = threadIdx.x <= mask ? hist_scan[threadIdx.x * tiles + blockIdx.x] : 0u;
+  }
+  uint32_t tile_total;
+  const uint32_t start = block_exclusive_scan_256(threadIdx.x < kRadixMax ? total : 0u, s_warp,
+                                                  &tile_total);
+  if (threadIdx.x < kRadixMax) s_dstart[threadIdx.x] = start;
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint32_t i = tile_base + (warp * kSortItems + it) * kWarp + lane;
+    if (i < n) {
+      const uint32_t d = (k[it] >> shift) & mask;
+      const uint32_t lp = s_dstart[d] + s_wcnt[warp][d] + rank[it];
+      s_keys[lp] = k[it];
+      s_vals[lp] = v[it];
+    }
+  }
+  __syncthreads();
+  const uint32_t valid_n = min((uint32_t)kTile, n - tile_base);
+  for (uint32_t i = threadIdx.x; i < valid_n; i += blockDim.x) {
+    const uint32_t key = s_keys[i];
+    const uint32_t d = (key >> shift) & mask;
+    const uint32_t o = s_gbase[d] + (i - s_dstart[d]);
+    keys_out[o] = key;
+    vals_out[o] = s_vals[i];
+  }
+}
+
+// ------------------------------------------------------------------ cell table
+// start[c] = first sorted position with dense id >= c, c in [0, ncells].
+__global__ void k_cell_start(const uint32_t *__restrict__ skeys, uint32_t n,
+                             const GridHeader *__restrict__ hdr, uint32_t *__restrict__ start) {
+  const unsigned long long nc = hdr->ncells;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long k = skeys[i];
+    const unsigned long long prev = i == 0 ? 0ull : (unsigned long long)skeys[i - 1] + 1ull;
+    for (unsigned long long c = prev; c <= k; ++c) start[c] = i;
+    if (i == n - 1)
+      for (unsigned long long c = k + 1; c <= nc; ++c) start[c] = n;
+  }
+}
+
+// Sparse bounding boxes (ncells >> n): one thread per cell, lower_bound.
+__global__ void k_cell_start_bsearch(const uint32_t *__restrict__ skeys, uint32_t n,
+                                     unsigned long long ncells, uint32_t *__restrict__ start) {
+  for (unsigned long long c = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       c <= ncells; c += (unsigned long long)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      if ((unsigned long long)skeys[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    start[c] = lo;
+  }
+}
+
+__global__ void k_cell_start_empty(uint32_t *__restrict__ start, unsigned long long ncells) {
+  for (unsigned long long c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncells;
+       c += gridDim.x * blockDim.x)
+    start[c] = 0;
+}
+
+// ------------------------------------------------------------------ permute
+__global__ void __launch_bounds__(256)
+    k_permute(const uint32_t *__restrict__ order, uint32_t n, const float *__restrict__ pos,
+              const float *__restrict__ nrm, const float *__restrict__ wi,
+              const float *__restrict__ pw, const uint32_t *__restrict__ depth,
+              float4 *__restrict__ rec0, float4 *__restrict__ rec1, float4 *__restrict__ rec2,
+              float4 *__restrict__ rec3) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const size_t j = order[i];
+    const size_t o = 3 * j;
+    rec0[i] = make_float4(pos[o], pos[o + 1], pos[o + 2], __uint_as_float(depth[j]));
+    rec1[i] = make_float4(nrm[o], nrm[o + 1], nrm[o + 2], wi[o]);
+    rec2[i] = make_float4(wi[o + 1], wi[o + 2], pw[o], pw[o + 1]);
+    rec3[i] = make_float4(pw[o + 2], 0.f, 0.f, 0.f);
+  }
+}
+
+// ------------------------------------------------------------------ query_ball
+// photon_map.cpp:53-78: 27 cells in (dx, dy, dz) nested order, each cell in
+// sorted (= insertion) order, closed fp64 ball test.  pass 0 counts, pass 1 fills.
+__global__ void k_query_ball(const double *__restrict__ centers, const double *__restrict__ radii,
+                             uint32_t nq, const GridHeader *__restrict__ hdr,
+                             const uint32_t *__restrict__ start, const float4 *__restrict__ rec0,
+                             const uint32_t *__restrict__ order,
+                             unsigned long long *__restrict__ counts,
+                             const unsigned long long *__restrict__ offsets,
+                             uint32_t *__restrict__ out, int fill) {
+  const GridHeader g = *hdr;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    const double cx = centers[3 * (size_t)q], cy = centers[3 * (size_t)q + 1],
+                 cz = centers[3 * (size_t)q + 2];
+    const double r = radii[q];
+    const double r2 = dm(r, r);
+    const long long ix = (long long)floor(dm(cx, g.inv)) - g.ix0;
+    const long long iy = (long long)floor(dm(cy, g.inv)) - g.iy0;
+    const long long iz = (long long)floor(dm(cz, g.inv)) - g.iz0;
+    unsigned long long cnt = 0;
+    const unsigned long long o = fill ? offsets[q] : 0ull;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          const long long X = ix + dx, Y = iy + dy, Z = iz + dz;
+          if (g.n == 0 || X < 0 || Y < 0 || Z < 0 || X >= g.nx || Y >= g.ny || Z >= g.nz) continue;
+          const unsigned long long c = (unsigned long long)((X * g.ny + Y) * g.nz + Z);
+          for (uint32_t i = start[c]; i < start[c + 1]; ++i) {
+            const float4 p = rec0[i];
+            const double ddx = ds((double)p.x, cx), ddy = ds((double)p.y, cy),
+                         ddz = ds((double)p.z, cz);
+            if (edot(ddx, ddy, ddz, ddx, ddy, ddz) <= r2) {
+              if (fill) out[o + cnt] = order[i];
+              ++cnt;
+            }
+          }
+        }
+    if (!fill) counts[q] = cnt;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static inline int cap_blocks(unsigned long long work, int threads, int sms, int per_sm) {
+  unsigned long long b = (work + threads - 1) / threads;
+  const unsigned long long cap = (unsigned long long)sms * per_sm;
+  if (b > cap) b = cap;
+  return (int)(b ? b : 1);
+}
+
+size_t radix_hist_entries(uint32_t n) {
+  const uint32_t tiles = (n + kTile - 1) / kTile;
+  return (size_t)kRadixMax * (tiles ? tiles : 1) + kRadixMax;  // + digit totals
+}
+
+// Sorts (keys_a, vals_a) by the low `bits` bits; returns the buffers holding
+// the result (a or b) through the out pointers.
+cudaError_t radix_sort_pairs(cudaStream_t s, SortScratch &sc, uint32_t n, uint32_t bits,
+                             uint32_t **keys_sorted, uint32_t **vals_sorted) {
+  uint32_t *ki = sc.keys_a, *vi = sc.vals_a, *ko = sc.keys_b, *vo = sc.vals_b;
+  if (n > 1) {
+    const uint32_t tiles = (n + kTile - 1) / kTile;
+    const uint32_t passes = (bits + 7) / 8;
+    const uint32_t width = (bits + passes - 1) / passes;
+    uint32_t *totals = sc.hist + (size_t)kRadixMax * tiles;
+    for (uint32_t p = 0; p < passes; ++p) {
+      const int shift = (int)(p * width);
+      const uint32_t w = min(width, bits - p * width);
+      const uint32_t mask = (1u << w) - 1u;
+      k_radix_upsweep<<<tiles, kSortThreads, 0, s>>>(ki, n, shift, mask, sc.hist, tiles);
+      k_digit_totals<<<mask + 1, 256, 0, s>>>(sc.hist, tiles, totals);
+      k_hist_scan<<<mask + 1, 256, 0, s>>>(sc.hist, tiles, totals);
+      k_radix_downsweep<<<tiles, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, shift, mask, sc.hist,
+                                                       tiles);
+      note_launches(4);
+      uint32_t *t;
+      t = ki; ki = ko; ko = t;
+      t = vi; vi = vo; vo = t;
+    }
+  }
+  *keys_sorted = ki;
+  *vals_sorted = vi;
+  return cudaGetLastError();
+}
+
+void launch_cell_bounds(cudaStream_t s, const float *pos, uint32_t n, const double *cell,
+                        long long *bounds, int sms) {
+  if (n == 0) return;
+  k_cell_bounds<<<cap_blocks(n, 256, sms, 8), 256, 0, s>>>(pos, n, cell, bounds);
+  note_launches(1);
+}
+
+void launch_grid_header(cudaStream_t s, const long long *bounds, const double *cell, uint32_t n,
+                        unsigned long long max_cells, GridHeader *hdr) {
+  k_grid_header<<<1, 1, 0, s>>>(bounds, cell, n, max_cells, hdr);
+  note_launches(1);
+}
+
+void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridHeader *hdr,
+                       uint32_t *keys, uint32_t *vals, int sms) {
+  if (n == 0) return;
+  k_dense_keys<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(pos, n, hdr, keys, vals);
+  note_launches(1);
+}
+
+void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const GridHeader *hdr,
+                       uint32_t *start, unsigned long long ncells, int sms) {
+  if (n == 0) {
+    k_cell_start_empty<<<1, 32, 0, s>>>(start, ncells);
+  } else if (ncells > 4ull * n) {
+    k_cell_start_bsearch<<<cap_blocks(ncells + 1, 256, sms, 16), 256, 0, s>>>(skeys, n, ncells, start);
+  } else {
+    k_cell_start<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(skeys, n, hdr, start);
+  }
+  note_launches(1);
+}
+
+void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const float *pos,
+                    const float *nrm, const float *wi, const float *pw, const uint32_t *depth,
+                    const PhotonRecs &r, int sms) {
+  if (n == 0) return;
+  k_permute<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
+                                                         r.rec0, r.rec1, r.rec2, r.rec3);
+  note_launches(1);
+}
+
+void launch_query_ball(cudaStream_t s, const double *centers, const double *radii, uint32_t nq,
+                       const GridHeader *hdr, const uint32_t *start, const float4 *rec0,
+                       const uint32_t *order, unsigned long long *counts,
+                       const unsigned long long *offsets, uint32_t *out, int fill) {
+  if (nq == 0) return;
+  k_query_ball<<<(int)((nq + 127) / 128), 128, 0, s>>>(centers, radii, nq, hdr, start, rec0, order,
+                                                       counts, offsets, out, fill);
+  note_launches(1);
+}
+
+}  // namespace fppm_b200
