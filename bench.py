@@ -40,6 +40,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    p.add_argument("--kernel", default="tile", choices=["tile", "warp"],
+                   help="gather kernel variant (A/B)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-stride", type=int, default=0,
@@ -220,7 +222,7 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
     n_local = wl.photons * (rank + 1) // world - wl.photons * rank // world
     begin = wl.photons * rank // world
     ctx = FppmContext(**wl.context_kwargs(max_hitpoints=H, max_photons=wl.photons,
-                                          device=local_rank))
+                                          device=local_rank, gather_kernel=args.kernel))
     pos, nrm = hitpoints_for_rows(W, r0, r1)
     ctx.set_hitpoints(pos, nrm)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfppm_gpu.so")
+LIB_PATH = os.environ.get("FPPM_GPU_LIB") or os.path.join(HERE, "libfppm_gpu.so")
 
 FPPM_OK = 0
 FPPM_ERR_INVALID_ARGUMENT = 1
@@ -81,7 +81,7 @@ class Config(C.Structure):
         ("initial_radius", C.c_double), ("samples_per_iteration", C.c_uint64),
         ("max_depth", C.c_uint32), ("normal_guard_cos", C.c_double),
         ("max_hitpoints", C.c_uint32), ("max_photons", C.c_uint32), ("max_cells", C.c_uint32),
-        ("device", C.c_int32), ("stream", C.c_void_p),
+        ("device", C.c_int32), ("stream", C.c_void_p), ("gather_kernel", C.c_int32),
     ]
 
 

@@ -74,6 +74,10 @@ struct fppm_gpu_ctx {
   // scratch for explicit-sample / query APIs
   void *d_scratch = nullptr;
   size_t scratch_bytes = 0;
+
+  // tiled-gather schedule (home-cell items)
+  fppm_b200::TileSched tile{};
+  uint32_t *h_total = nullptr;
 };
 
 namespace fppm_b200 {
@@ -328,6 +332,10 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->o_acc, Hc));
   A(dalloc(&ctx->d_counters, 4)); A(dalloc(&ctx->d_iter_tr, 2)); A(dalloc(&ctx->d_work, 1));
   A(dalloc(&ctx->d_rmax_bits, 1));
+  A(dalloc(&ctx->tile.sort.keys_a, Hc)); A(dalloc(&ctx->tile.sort.vals_a, Hc));
+  A(dalloc(&ctx->tile.sort.keys_b, Hc)); A(dalloc(&ctx->tile.sort.vals_b, Hc));
+  A(dalloc(&ctx->tile.sort.hist, radix_hist_entries((uint32_t)Hc)));
+  A(cudaMallocHost(&ctx->h_total, sizeof(uint32_t)));
   if (e != cudaSuccess) {
     int rc = cuda_fail(ctx, e, "fppm_gpu_create allocation");
     fppm_gpu_destroy(ctx);
@@ -369,6 +377,12 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
                  ctx->d_iter_tr, ctx->d_work, ctx->d_rmax_bits, ctx->d_crit, ctx->d_scratch};
   for (void *p : dev)
     if (p) cudaFree(p);
+  const TileSched &T = ctx->tile;
+  void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
+                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.partials, T.done};
+  for (void *p : tdev)
+    if (p) cudaFree(p);
+  if (ctx->h_total) cudaFreeHost(ctx->h_total);
   if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
   if (ctx->h_bounds_init) cudaFreeHost(ctx->h_bounds_init);
   if (ctx->h_cell) cudaFreeHost(ctx->h_cell);
@@ -803,7 +817,56 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
   if (snap) { A.snap_cnt = ctx->snap_cnt; A.snap_sum = ctx->snap_sum; A.snap_sq = ctx->snap_sq; }
   A.counters = ctx->d_counters; A.iter_tr = ctx->d_iter_tr; A.work = ctx->d_work;
   A.rmax_bits = ctx->d_rmax_bits;
-  if (ctx->H) FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
+  if (ctx->H && ctx->cfg.gather_kernel == 1) {
+    FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
+  } else if (ctx->H) {
+    // ---- tiled path: bin hit points by home cell, build items, run
+    TileSched &S = ctx->tile;
+    const GridHeader g = *ctx->h_hdr;
+    const unsigned long long n_ext =
+        (unsigned long long)(g.nx + 2) * (unsigned long long)(g.ny + 2) * (unsigned long long)(g.nz + 2);
+    if (n_ext + 2 > S.bucket_cap) {
+      FPPM_CUDA_OK(cudaStreamSynchronize(s));
+      void *old[] = {S.hp_start, S.items, S.chunks, S.item_base, S.scan_tmp};
+      for (void *p : old)
+        if (p) cudaFree(p);
+      const unsigned long long cap = std::max<unsigned long long>(n_ext + 2, 4096);
+      FPPM_CUDA_OK(dalloc(&S.hp_start, cap + 1));
+      FPPM_CUDA_OK(dalloc(&S.items, cap + 1));
+      FPPM_CUDA_OK(dalloc(&S.chunks, cap + 1));
+      FPPM_CUDA_OK(dalloc(&S.item_base, cap + 1));
+      FPPM_CUDA_OK(dalloc(&S.scan_tmp, cap / 4096 + 8));
+      S.bucket_cap = cap;
+    }
+    uint32_t nb = 0;
+    FPPM_CUDA_OK(tile_schedule_bins(s, A, S, g, ctx->sms, &nb));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
+                                 cudaMemcpyDeviceToHost, s));
+    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    const uint32_t total = *ctx->h_total;
+    if (total > S.item_cap) {
+      if (S.desc) cudaFree(S.desc);
+      if (S.partials) cudaFree(S.partials);
+      if (S.done) cudaFree(S.done);
+      S.desc = nullptr;
+      S.partials = nullptr;
+      S.done = nullptr;
+      const unsigned long long cap = std::max<unsigned long long>(total + total / 4, 1024);
+      FPPM_CUDA_OK(dalloc(&S.desc, cap));
+      FPPM_CUDA_OK(dalloc(&S.partials, cap * tile_partial_doubles(ctx->G, ctx->C)));
+      FPPM_CUDA_OK(dalloc(&S.done, cap));
+      S.item_cap = cap;
+    }
+    FPPM_CUDA_OK(cudaMemsetAsync(S.done, 0, sizeof(uint32_t) * std::max<uint32_t>(total, 1), s));
+    FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms));
+    TileArgs T;
+    T.desc = S.desc;
+    T.hp_order = S.hp_order;
+    T.partials = S.partials;
+    T.done = S.done;
+    T.total_items = S.item_base + nb;
+    FPPM_CUDA_OK(launch_gather_tiles(s, A, T, ctx->C, ctx->sms));
+  }
   ctx->end_calls++;
   if (out && (rc = copy_iter_out(ctx, out, true))) return rc;
   if (summary && (rc = fill_summary(ctx, summary))) return rc;

@@ -73,6 +73,52 @@ struct EndArgs {
   double *snap_sum, *snap_sq;
 };
 
+// ---- tiled gather (gather_tile.cu)
+constexpr int kChunk = 1536;  // candidates staged per item (64 B each: 96 KB of smem)
+
+struct ItemDesc {  // 112 B, one per (home cell, hit-point wave, candidate chunk)
+  uint32_t hp_lo, hp_n;      // range in the cell-sorted hit points
+  uint32_t first, nchunks;   // first item of this wave, chunks per wave
+  uint32_t ncand, chunk, npieces, pad;
+  uint32_t src[9], len[9];   // contiguous pieces of the sorted photon records
+  uint32_t pad2[2];
+};
+
+struct TileArgs {
+  const ItemDesc *desc;
+  const uint32_t *hp_order;     // cell-sorted hit point indices
+  double *partials;             // [item][32][partial_size]
+  uint32_t *done;               // per first-item-of-wave completion counters
+  const uint32_t *total_items;  // device scalar
+};
+
+struct SortScratch {
+  uint32_t *keys_a, *vals_a, *keys_b, *vals_b;
+  uint32_t *hist;  // [digit][tile] + digit totals
+};
+
+struct TileSched {
+  SortScratch sort;     // hit-point keys (capacity H)
+  uint32_t *hp_order;   // alias of the sorted values
+  uint32_t *hp_start;   // [nb + 1]
+  uint32_t *items, *chunks, *item_base;  // [nb + 1]
+  uint32_t *scan_tmp;
+  ItemDesc *desc;
+  double *partials;
+  uint32_t *done;
+  unsigned long long bucket_cap, item_cap;
+};
+
+__host__ __device__ constexpr int partial_size(int gmax, int ch) { return gmax + 2 * ch * gmax + 3; }
+
+cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S,
+                               const GridHeader &g, int sms, uint32_t *nb_out);
+cudaError_t tile_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb,
+                                int sms);
+cudaError_t launch_gather_tiles(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
+                                int sms);
+size_t tile_partial_doubles(int G, int C);
+
 cudaError_t launch_gather_test(cudaStream_t s, const GatherArgs &A, int C, int sms);
 cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2 *y,
                            const double *value, uint32_t n, const double *radius, uint32_t H,
@@ -83,10 +129,6 @@ cudaError_t launch_hit_weights(cudaStream_t s, const double3 *nrm, const double3
                                const double3 *thr, const double3 *alb, uint32_t H, double3 *K);
 
 // grid.cu
-struct SortScratch {
-  uint32_t *keys_a, *vals_a, *keys_b, *vals_b;
-  uint32_t *hist;  // [digit][tile] + digit totals
-};
 size_t radix_hist_entries(uint32_t n);
 cudaError_t radix_sort_pairs(cudaStream_t s, SortScratch &sc, uint32_t n, uint32_t bits,
                              uint32_t **keys_sorted, uint32_t **vals_sorted);

@@ -28,35 +28,6 @@ __device__ __forceinline__ T warp_reduce(T v, Op op) {
   return v;
 }
 
-// exclusive scan of one value per thread over a 256-thread block; returns the
-// block total through *total.
-__device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_t *s_warp,
-                                                             uint32_t *total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_warp[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = lane < 8 ? s_warp[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < 8) s_warp[lane] = w;  // inclusive warp totals
-  }
-  __syncthreads();
-  const uint32_t before = warp == 0 ? 0u : s_warp[warp - 1];
-  *total = s_warp[7];
-  __syncthreads();
-  return before + x - v;
-}
-
 // ------------------------------------------------------------------ bounds
 __global__ void __launch_bounds__(256)
     k_cell_bounds(const float *__restrict__ pos, uint32_t n, const double *__restrict__ cell_ptr,
@@ -320,7 +291,11 @@ __global__ void __launch_bounds__(256)
     rec0[i] = make_float4(pos[o], pos[o + 1], pos[o + 2], __uint_as_float(depth[j]));
     rec1[i] = make_float4(nrm[o], nrm[o + 1], nrm[o + 2], wi[o]);
     rec2[i] = make_float4(wi[o + 1], wi[o + 2], pw[o], pw[o + 1]);
-    rec3[i] = make_float4(pw[o + 2], 0.f, 0.f, 0.f);
+    // luminance of the photon power in fp64 (vec.hpp:79-81), for gray hit-point weights
+    const double L = elum((double)pw[o], (double)pw[o + 1], (double)pw[o + 2]);
+    const unsigned long long Lb = (unsigned long long)__double_as_longlong(L);
+    rec3[i] = make_float4(pw[o + 2], 0.f, __uint_as_float((uint32_t)Lb),
+                          __uint_as_float((uint32_t)(Lb >> 32)));
   }
 }
 

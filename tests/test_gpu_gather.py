@@ -23,13 +23,15 @@ def test_generator_bitexact(port, wl_name):
         assert np.array_equal(got[k].view(np.uint32), want[k].view(np.uint32)), k
 
 
+@pytest.mark.parametrize("kernel", ["tile", "warp"])
 @pytest.mark.parametrize("wl_name,raster,photons,iters", [
     ("c1", 64, 1 << 16, 4),
     ("c2", 64, 1 << 17, 4),
+    ("c2", 128, 1 << 19, 3),
 ])
-def test_iterations_match_oracle(port, wl_name, raster, photons, iters):
+def test_iterations_match_oracle(port, wl_name, raster, photons, iters, kernel):
     wl = WORKLOADS[wl_name].scaled(raster=raster, photons=photons)
-    ctx = gpu_context(wl)
+    ctx = gpu_context(wl, gather_kernel=kernel)
     sess = port.session(oracle_cfg(wl), port.gen_raster_hitpoints(wl.raster))
     for it in range(1, iters + 1):
         ctx.generate_photons(wl.generator, wl.seed, it, wl.photons)
