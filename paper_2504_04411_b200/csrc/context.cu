@@ -335,6 +335,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->tile.sort.keys_a, Hc)); A(dalloc(&ctx->tile.sort.vals_a, Hc));
   A(dalloc(&ctx->tile.sort.keys_b, Hc)); A(dalloc(&ctx->tile.sort.vals_b, Hc));
   A(dalloc(&ctx->tile.sort.hist, radix_hist_entries((uint32_t)Hc)));
+  A(dalloc(&ctx->tile.hp_map, 3 * Hc));
   A(cudaMallocHost(&ctx->h_total, sizeof(uint32_t)));
   if (e != cudaSuccess) {
     int rc = cuda_fail(ctx, e, "fppm_gpu_create allocation");
@@ -379,7 +380,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
-                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.partials, T.done};
+                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.partials, T.hp_map};
   for (void *p : tdev)
     if (p) cudaFree(p);
   if (ctx->h_total) cudaFreeHost(ctx->h_total);
@@ -847,25 +848,22 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
     if (total > S.item_cap) {
       if (S.desc) cudaFree(S.desc);
       if (S.partials) cudaFree(S.partials);
-      if (S.done) cudaFree(S.done);
       S.desc = nullptr;
       S.partials = nullptr;
-      S.done = nullptr;
       const unsigned long long cap = std::max<unsigned long long>(total + total / 4, 1024);
       FPPM_CUDA_OK(dalloc(&S.desc, cap));
       FPPM_CUDA_OK(dalloc(&S.partials, cap * tile_partial_doubles(ctx->G, ctx->C)));
-      FPPM_CUDA_OK(dalloc(&S.done, cap));
       S.item_cap = cap;
     }
-    FPPM_CUDA_OK(cudaMemsetAsync(S.done, 0, sizeof(uint32_t) * std::max<uint32_t>(total, 1), s));
     FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms));
     TileArgs T;
     T.desc = S.desc;
     T.hp_order = S.hp_order;
     T.partials = S.partials;
-    T.done = S.done;
+    T.hp_map = S.hp_map;
     T.total_items = S.item_base + nb;
     FPPM_CUDA_OK(launch_gather_tiles(s, A, T, ctx->C, ctx->sms));
+    FPPM_CUDA_OK(launch_tile_finalize(s, A, T, ctx->C, ctx->sms));
   }
   ctx->end_calls++;
   if (out && (rc = copy_iter_out(ctx, out, true))) return rc;

@@ -74,7 +74,9 @@ struct EndArgs {
 };
 
 // ---- tiled gather (gather_tile.cu)
-constexpr int kChunk = 1536;  // candidates staged per item (64 B each: 96 KB of smem)
+// candidates staged per item (64 B each: 88 KB of smem, so that two CTAs of
+// the tiled kernel with their queues and fragment partials fit one SM)
+constexpr int kChunk = 1376;
 
 struct ItemDesc {  // 112 B, one per (home cell, hit-point wave, candidate chunk)
   uint32_t hp_lo, hp_n;      // range in the cell-sorted hit points
@@ -87,8 +89,8 @@ struct ItemDesc {  // 112 B, one per (home cell, hit-point wave, candidate chunk
 struct TileArgs {
   const ItemDesc *desc;
   const uint32_t *hp_order;     // cell-sorted hit point indices
-  double *partials;             // [item][32][partial_size]
-  uint32_t *done;               // per first-item-of-wave completion counters
+  double *partials;             // [item][32][partial_size] per-item results
+  const uint32_t *hp_map;       // per hit point: first item, chunks, wave slot
   const uint32_t *total_items;  // device scalar
 };
 
@@ -105,7 +107,7 @@ struct TileSched {
   uint32_t *scan_tmp;
   ItemDesc *desc;
   double *partials;
-  uint32_t *done;
+  uint32_t *hp_map;     // [3 H]
   unsigned long long bucket_cap, item_cap;
 };
 
@@ -117,6 +119,8 @@ cudaError_t tile_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &
                                 int sms);
 cudaError_t launch_gather_tiles(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
                                 int sms);
+cudaError_t launch_tile_finalize(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
+                                 int sms);
 size_t tile_partial_doubles(int G, int C);
 
 cudaError_t launch_gather_test(cudaStream_t s, const GatherArgs &A, int C, int sms);

@@ -58,6 +58,7 @@ struct Hit {
   float chx, chy, chz, clx, cly, clz;  // center as float hi + lo
   float nfx, nfy, nfz, ufx, ufy, ufz, vfx, vfy, vfz;
   float r2f, lim_hi, lim_lo, band_y, guard_f;
+  float guard_ceil;  // smallest float f with (double)f >= guard
   float qa_scale;  // n_a / r2 (fp32)
   uint32_t h, eye;
   bool fast, gray;
@@ -67,7 +68,7 @@ struct Hit {
 struct HitF {
   float chx, chy, chz, clx, cly, clz;
   float nfx, nfy, nfz, ufx, ufy, ufz, vfx, vfy, vfz;
-  float lim_hi, lim_lo, band_y, guard_f, qa_scale, r;
+  float lim_hi, lim_lo, band_y, guard_f, qa_scale, r, guard_ceil;
   uint32_t eye;
   int na, ns;
   bool fast;
@@ -97,6 +98,7 @@ static __device__ __forceinline__ void make_hit(const GatherArgs &A, uint32_t h,
   H.r2f = (float)H.r2;
   H.band_y = 1e-5f * (float)r;
   H.guard_f = (float)A.guard;
+  H.guard_ceil = __double2float_ru(A.guard);
   H.qa_scale = (float)A.na / H.r2f;
   const double cmax = fmax(fabs(c.x), fmax(fabs(c.y), fabs(c.z)));
   const double nn = edot(n.x, n.y, n.z, n.x, n.y, n.z);
@@ -113,7 +115,7 @@ static __device__ __forceinline__ HitF hitf(const Hit &H, int na, int ns) {
   F.ufx = H.ufx; F.ufy = H.ufy; F.ufz = H.ufz;
   F.vfx = H.vfx; F.vfy = H.vfy; F.vfz = H.vfz;
   F.lim_hi = H.lim_hi; F.lim_lo = H.lim_lo; F.band_y = H.band_y; F.guard_f = H.guard_f;
-  F.qa_scale = H.qa_scale; F.r = (float)H.r;
+  F.qa_scale = H.qa_scale; F.r = (float)H.r; F.guard_ceil = H.guard_ceil;
   F.eye = H.eye; F.na = na; F.ns = ns; F.fast = H.fast;
   return F;
 }

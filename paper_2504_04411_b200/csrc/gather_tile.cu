@@ -17,12 +17,14 @@
 //   flush  whenever 32 survivors are queued, all 32 lanes take one each:
 //          guard, cos_i, sector in fp32 with bands (fp64 exact path otherwise),
 //          then fp64 accumulation into per-lane sector registers
-//   reduce fixed-order warp shuffles; lane 0 pools the moments with the
-//          region state and runs end_iteration (fused), or, for cells split
-//          over several chunks, writes partials that the last chunk's CTA
-//          combines in chunk order (deterministic).
+//   reduce fixed-order warp shuffles; fragments of one hit point (the
+//          (hit point x candidate) space is split evenly over the warps)
+//          are combined in warp order and written as the item's partial.
 //
 // Items are scheduled by a persistent grid through a global work counter.
+// Every item writes one partial per hit point of its wave; k_tile_finalize
+// (one thread per hit point) sums a wave's chunk partials in chunk order and
+// runs the fused end_iteration, so no CTA waits on the serial epilogue.
 #include "common.cuh"
 #include "gather.cuh"
 #include "gather_dev.cuh"
@@ -32,7 +34,9 @@ namespace fppm_b200 {
 constexpr int kTileWarps = 8;
 constexpr int kTileThreads = kTileWarps * kWarp;
 constexpr int kWave = 32;  // hit points per item
-constexpr int kQueue = 64;
+constexpr int kUnroll = 4;                  // candidates per lane per test round
+constexpr int kQueue = 256;               // survivor ring per warp (holds <= 31 + 128)
+constexpr int kMaxFrag = kWave + kTileWarps;
 
 
 // ------------------------------------------------------------------ scheduling
@@ -190,7 +194,8 @@ __global__ void k_item_desc(const uint32_t *__restrict__ hp_start, uint32_t nb,
                             const GridHeader *__restrict__ hdr,
                             const uint32_t *__restrict__ cell_start,
                             const uint32_t *__restrict__ items, const uint32_t *__restrict__ chunks,
-                            const uint32_t *__restrict__ item_base, ItemDesc *__restrict__ desc) {
+                            const uint32_t *__restrict__ item_base, const uint32_t *__restrict__ hp_order,
+                            ItemDesc *__restrict__ desc, uint32_t *__restrict__ hp_map) {
   const GridHeader g = *hdr;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
     if (items[b] == 0) continue;
@@ -208,6 +213,12 @@ __global__ void k_item_desc(const uint32_t *__restrict__ hp_start, uint32_t nb,
     uint32_t item = item_base[b];
     for (uint32_t w = 0; w < waves; ++w) {
       const uint32_t first = item;
+      for (uint32_t j = w * kWave; j < min(nhp, (w + 1) * kWave); ++j) {
+        const uint32_t h = hp_order[h0 + j];
+        hp_map[3 * (size_t)h] = first;
+        hp_map[3 * (size_t)h + 1] = nch;
+        hp_map[3 * (size_t)h + 2] = j - w * kWave;
+      }
       for (uint32_t ch = 0; ch < nch; ++ch, ++item) {
         ItemDesc d;
         d.hp_lo = h0 + w * kWave;
@@ -274,43 +285,64 @@ __device__ __forceinline__ bool fast_sector(const HitF &F, float yu, float yv, f
 }
 
 
-__host__ __device__ constexpr size_t tile_dyn_smem_bytes() { return (size_t)kChunk * 64; }
+template <int GMAX, int CH>
+__host__ __device__ constexpr size_t tile_dyn_smem_bytes() {
+  return (size_t)kChunk * 64 + (size_t)kMaxFrag * partial_size(GMAX, CH) * sizeof(double);
+}
 
 constexpr uint32_t kNoEntry = 0xffffffffu;
 constexpr uint32_t kExactCode = 0xffu;
 
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// Test phase: ball and depth only (photon_map.cpp:76, integrator.cpp:396).
+// False only when the reference certainly rejects the pair; disk, sector and
+// the remaining filters are decided in the flush, where every lane holds a
+// survivor.
+__device__ __forceinline__ bool ball_pass(const HitF &F, bool lo_zero, float4 a, uint32_t max_depth) {
+  float dx = a.x - F.chx, dy = a.y - F.chy, dz = a.z - F.chz;
+  if (!lo_zero) {
+    dx -= F.clx;
+    dy -= F.cly;
+    dz -= F.clz;
+  }
+  const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  return d2 <= F.lim_hi && F.eye + __float_as_uint(a.w) <= max_depth;
+}
+
 template <int GMAX, int CH>
 __global__ void __launch_bounds__(kTileThreads, FPPM_TILE_MINB) k_gather_tiles(const GatherArgs A,
                                                                               const TileArgs T) {
+  constexpr int PS = partial_size(GMAX, CH);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float4 *s_rec0 = reinterpret_cast<float4 *>(smem_raw);
-  float4 *s_rec1 = s_rec0 + kChunk;
-  float4 *s_rec2 = s_rec1 + kChunk;
-  float4 *s_rec3 = s_rec2 + kChunk;
+  double *s_frag = reinterpret_cast<double *>(smem_raw + (size_t)kChunk * 64);
   __shared__ Hit s_hit[kWave];
-  __shared__ uint32_t s_q[kTileWarps][kQueue];  // survivor = index | (sector or exact) << 16
+  __shared__ uint32_t s_q[kTileWarps][kQueue];  // ring: survivor = index | (sector or exact) << 16
+  __shared__ uint32_t s_frag_hp[kMaxFrag];
   __shared__ ItemDesc s_desc;
   __shared__ __align__(8) uint64_t s_bar;
-  __shared__ uint32_t s_item, s_last;
-  __shared__ unsigned long long s_c[4], s_rmax;
-  __shared__ unsigned int s_tr[2];
+  __shared__ uint32_t s_item;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t *q = s_q[warp];
+  const uint32_t r0 = smem_u32(smem_raw);       // rec0 .. rec3 in 16-B strides
+  const uint32_t r1 = r0 + kChunk * 16u, r2 = r1 + kChunk * 16u, r3 = r2 + kChunk * 16u;
   const uint32_t total_items = *T.total_items;
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
-    s_c[0] = s_c[1] = s_c[2] = s_c[3] = 0;
-    s_rmax = 0;
-    s_tr[0] = s_tr[1] = 0;
   }
   __syncthreads();
   uint32_t phase = 0;
   uint32_t my_cand = 0, my_exact = 0, my_amb = 0, my_acc = 0;
-  double my_rmax = 0.0;
-  uint32_t my_tested = 0, my_rejected = 0;
 
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(A.work, 1u);
@@ -320,6 +352,7 @@ __global__ void __launch_bounds__(kTileThreads, FPPM_TILE_MINB) k_gather_tiles(c
     if (threadIdx.x < sizeof(ItemDesc) / 4)
       reinterpret_cast<uint32_t *>(&s_desc)[threadIdx.x] =
           reinterpret_cast<const uint32_t *>(T.desc + item)[threadIdx.x];
+    if (threadIdx.x < kMaxFrag) s_frag_hp[threadIdx.x] = kNoEntry;
     __syncthreads();
     const uint32_t ncand = s_desc.ncand, hp_n = s_desc.hp_n;
     if (threadIdx.x == 0 && ncand) {
@@ -329,9 +362,9 @@ __global__ void __launch_bounds__(kTileThreads, FPPM_TILE_MINB) k_gather_tiles(c
       for (uint32_t p = 0; p < s_desc.npieces; ++p) {
         const uint32_t src = s_desc.src[p], n = s_desc.len[p];
         bulk_g2s(s_rec0 + off, A.rec0 + src, n * 16u, &s_bar);
-        bulk_g2s(s_rec1 + off, A.rec1 + src, n * 16u, &s_bar);
-        bulk_g2s(s_rec2 + off, A.rec2 + src, n * 16u, &s_bar);
-        bulk_g2s(s_rec3 + off, A.rec3 + src, n * 16u, &s_bar);
+        bulk_g2s(s_rec0 + kChunk + off, A.rec1 + src, n * 16u, &s_bar);
+        bulk_g2s(s_rec0 + 2 * kChunk + off, A.rec2 + src, n * 16u, &s_bar);
+        bulk_g2s(s_rec0 + 3 * kChunk + off, A.rec3 + src, n * 16u, &s_bar);
         off += n;
       }
     }
@@ -341,14 +374,22 @@ __global__ void __launch_bounds__(kTileThreads, FPPM_TILE_MINB) k_gather_tiles(c
       mbar_wait(&s_bar, phase);
       phase ^= 1u;
     }
-    const bool multi = s_desc.nchunks > 1;
 
-    for (uint32_t k = warp; k < hp_n; k += kTileWarps) {
+    // ---- balanced split of the (hit point x candidate) space over warps:
+    // warp w owns flattened positions [w*W/8, (w+1)*W/8), i.e. a few
+    // contiguous (hit point, candidate range) fragments.
+    const uint32_t W = hp_n * ncand;
+    const uint32_t f0 = (uint32_t)(((unsigned long long)W * warp) / kTileWarps);
+    const uint32_t f1 = (uint32_t)(((unsigned long long)W * (warp + 1)) / kTileWarps);
+    for (uint32_t f = f0; f < f1;) {
+      const uint32_t k = f / ncand;
+      const uint32_t ib = f - k * ncand;
+      const uint32_t ie = min(ncand, f1 - k * ncand);
+      f = k * ncand + ie;
       const Hit &Hs = s_hit[k];
       const HitF F = hitf(Hs, A.na, A.ns);
-      // uniform specialisations: n = +z gives u = (1,-0,-0), v = (-0,1,-0), so
-      // the fp32 plane coordinates are exactly (dx, dy); an fp32-exact center
-      // has a zero low part.
+      // n = +z gives u = (1,-0,-0), v = (-0,1,-0): the fp32 plane coordinates
+      // are exactly (dx, dy); an fp32-exact center has a zero low part.
       const bool planar = F.fast && Hs.nx == 0.0 && Hs.ny == 0.0 && Hs.nz == 1.0;
       const bool lo_zero = F.clx == 0.0f && F.cly == 0.0f && F.clz == 0.0f;
       uint32_t cnt[GMAX];
@@ -360,86 +401,95 @@ __global__ void __launch_bounds__(kTileThreads, FPPM_TILE_MINB) k_gather_tiles(c
         for (int c = 0; c < CH; ++c) { sm[c][g] = 0.0; sq[c][g] = 0.0; }
       }
       double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-      uint32_t qn = 0, base = 0;
+      uint32_t qh = 0, qt = 0, base = ib;  // ring head / tail (warp-uniform)
 
-      // One loop, one flush site: test rounds append survivors to the warp
-      // queue; every 32 survivors are flushed with all lanes busy.
+      // One loop, one flush site: test rounds (kUnroll candidates per lane)
+      // append survivors to the warp queue while fewer than 32 are pending;
+      // otherwise 32 survivors are flushed with all lanes busy.
       for (;;) {
-        if (base < ncand) {
-          const uint32_t i = base + lane;
-          base += 32;
-          uint32_t ent = kNoEntry;
-          if (i < ncand) {
-            ++my_cand;
-            const float4 a = s_rec0[i];
-            float dx = a.x - F.chx, dy = a.y - F.chy, dz = a.z - F.chz;
-            if (!lo_zero) {
-              dx -= F.clx;
-              dy -= F.cly;
-              dz -= F.clz;
-            }
-            const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            if (d2 <= F.lim_hi && F.eye + __float_as_uint(a.w) <= A.max_depth) {
-              float yu, yv;
-              if (planar) {
-                yu = dx;
-                yv = dy;
-              } else {
-                yu = fmaf(dx, F.ufx, fmaf(dy, F.ufy, dz * F.ufz));
-                yv = fmaf(dx, F.vfx, fmaf(dy, F.vfy, dz * F.vfz));
-              }
-              const float yy = fmaf(yu, yu, yv * yv);
-              if (yy <= F.lim_hi) {
-                int sec;
-                const bool sure = fast_sector(F, yu, yv, yy, sec) && F.fast && d2 < F.lim_lo &&
-                                  yy < F.lim_lo;
-                ent = i | ((sure ? (uint32_t)sec : kExactCode) << 16);
-              }
-            }
+        if (qt - qh < 32 && base < ie) {
+          uint32_t ent[kUnroll];
+          float4 a[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t i = base + u * 32 + lane;
+            a[u] = lds128(r0 + (i < ie ? i : ib) * 16u);
           }
-          const uint32_t m = __ballot_sync(kFull, ent != kNoEntry);
-          if (ent != kNoEntry) q[qn + __popc(m & lt)] = ent;
-          qn += __popc(m);
-          if (qn < 32) continue;
-        } else if (qn == 0) {
-          break;
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t i = base + u * 32 + lane;
+            ent[u] = i < ie && ball_pass(F, lo_zero, a[u], A.max_depth) ? i : kNoEntry;
+            my_cand += i < ie ? 1u : 0u;
+          }
+          base += 32 * kUnroll;
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t m = __ballot_sync(kFull, ent[u] != kNoEntry);
+            if (ent[u] != kNoEntry) q[(qt + __popc(m & lt)) & (kQueue - 1)] = ent[u];
+            qt += __popc(m);
+          }
+          continue;
         }
+        if (qt == qh) break;
         // ---- flush min(qn, 32) survivors, one per lane
         __syncwarp();
-        const uint32_t n = qn < 32 ? qn : 32u;
+        const uint32_t n = qt - qh < 32 ? qt - qh : 32u;
         bool acc = false, cos_pos = false;
         int sector = 0;
         float4 c2 = make_float4(0.f, 0.f, 0.f, 0.f), c3 = c2;
         if ((uint32_t)lane < n) {
-          const uint32_t ent = q[lane];
-          const uint32_t i = ent & 0xffffu, code = ent >> 16;
-          const float4 b = s_rec1[i];
-          c2 = s_rec2[i];
-          c3 = s_rec3[i];
-          bool ex = code == kExactCode;
+          const uint32_t i = q[(qh + lane) & (kQueue - 1)];
+          const float4 a = lds128(r0 + i * 16u);
+          const float4 b = lds128(r1 + i * 16u);
+          c2 = lds128(r2 + i * 16u);
+          c3 = lds128(r3 + i * 16u);
+          float dx = a.x - F.chx, dy = a.y - F.chy, dz = a.z - F.chz;
+          if (!lo_zero) {
+            dx -= F.clx;
+            dy -= F.cly;
+            dz -= F.clz;
+          }
+          const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+          float yu = dx, yv = dy;
+          if (!planar) {
+            yu = fmaf(dx, F.ufx, fmaf(dy, F.ufy, dz * F.ufz));
+            yv = fmaf(dx, F.vfx, fmaf(dy, F.vfy, dz * F.vfz));
+          }
+          const float yy = fmaf(yu, yu, yv * yv);
+          // disk (integrator.cpp:399): certain reject above the band
+          const bool keep = yy <= F.lim_hi;
+          bool ex = !(F.fast && d2 < F.lim_lo && yy < F.lim_lo);
+          ex = !fast_sector(F, yu, yv, yy, sector) || ex;
           bool guard_ok = true;
-          if (!ex) {
+          if (planar) {
+            // n = +z: dot(p.n, n) = p.n.z and dot(wi, n) = wi.z exactly in fp64
+            // when the x, y components are finite (integrator.cpp:397, bsdf.cpp:56)
+            ex = ex || !(fabsf(b.x) < INFINITY && fabsf(b.y) < INFINITY && fabsf(b.w) < INFINITY &&
+                         fabsf(c2.x) < INFINITY);
+            guard_ok = !(b.z < F.guard_ceil);
+            cos_pos = !(c2.y <= 0.0f);
+          } else {
             const float gd = fmaf(b.x, F.nfx, fmaf(b.y, F.nfy, b.z * F.nfz));
             const float gb =
                 2e-6f * (fabsf(b.x * F.nfx) + fabsf(b.y * F.nfy) + fabsf(b.z * F.nfz)) + 1e-30f;
             guard_ok = !(gd < F.guard_f - gb);
-            ex = guard_ok && !(gd >= F.guard_f + gb);
+            ex = ex || (guard_ok && !(gd >= F.guard_f + gb));
             const float ci = fmaf(b.w, F.nfx, fmaf(c2.x, F.nfy, c2.y * F.nfz));
             const float cb =
                 2e-6f * (fabsf(b.w * F.nfx) + fabsf(c2.x * F.nfy) + fabsf(c2.y * F.nfz)) + 1e-30f;
             ex = ex || !(fabsf(ci) > cb);
             cos_pos = ci > 0.0f;
-            sector = (int)code;
           }
+          ex = ex && keep;  // a certain disk reject needs no exact check
           if (ex) {
             ++my_exact;
-            const uint32_t f = exact_pair_packed(Hs, s_rec0[i], b, c2, F.na, F.ns, A.guard);
-            acc = (f & 1u) != 0;
-            cos_pos = (f & 2u) != 0;
-            my_amb += (f >> 2) & 1u;
-            sector = (int)(f >> 8);
+            const uint32_t fl = exact_pair_packed(Hs, a, b, c2, F.na, F.ns, A.guard);
+            acc = (fl & 1u) != 0;
+            cos_pos = (fl & 2u) != 0;
+            my_amb += (fl >> 2) & 1u;
+            sector = (int)(fl >> 8);
           } else {
-            acc = guard_ok;
+            acc = keep && guard_ok;
           }
         }
         if (acc) {
@@ -468,16 +518,11 @@ __global__ void __launch_bounds__(kTileThreads, FPPM_TILE_MINB) k_gather_tiles(c
 #pragma unroll
           for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
         }
-        __syncwarp();
-        const uint32_t rest = qn - n;
-        const uint32_t keep = (uint32_t)lane < rest ? q[32 + lane] : 0u;
-        __syncwarp();
-        if ((uint32_t)lane < rest) q[lane] = keep;
-        qn = rest;
+        qh += n;
         __syncwarp();
       }
 
-      // ---- fixed-order warp reduction
+      // ---- fragment partial: fixed-order warp reduction into smem slot k + warp
 #pragma unroll
       for (int g = 0; g < GMAX; ++g) {
         cnt[g] = warp_sum(cnt[g]);
@@ -491,90 +536,103 @@ __global__ void __launch_bounds__(kTileThreads, FPPM_TILE_MINB) k_gather_tiles(c
       p1 = warp_sum(p1);
       p2 = warp_sum(p2);
       if (lane == 0) {
-        if (!multi) {
-          finalize_hit<GMAX, CH>(A, Hs.h, cnt, sm, sq, p0, p1, p2, my_tested, my_rejected, my_rmax);
-        } else {
-          double *pp = T.partials + ((size_t)item * kWave + k) * partial_size(GMAX, CH);
+        const uint32_t slot = k + warp;
+        double *pp = s_frag + (size_t)slot * PS;
 #pragma unroll
-          for (int g = 0; g < GMAX; ++g) pp[g] = (double)cnt[g];
+        for (int g = 0; g < GMAX; ++g) pp[g] = (double)cnt[g];
 #pragma unroll
-          for (int c = 0; c < CH; ++c)
+        for (int c = 0; c < CH; ++c)
 #pragma unroll
-            for (int g = 0; g < GMAX; ++g) {
-              pp[GMAX + c * GMAX + g] = sm[c][g];
-              pp[GMAX + CH * GMAX + c * GMAX + g] = sq[c][g];
-            }
-          pp[GMAX + 2 * CH * GMAX] = p0;
-          pp[GMAX + 2 * CH * GMAX + 1] = p1;
-          pp[GMAX + 2 * CH * GMAX + 2] = p2;
-        }
+          for (int g = 0; g < GMAX; ++g) {
+            pp[GMAX + c * GMAX + g] = sm[c][g];
+            pp[GMAX + CH * GMAX + c * GMAX + g] = sq[c][g];
+          }
+        pp[GMAX + 2 * CH * GMAX] = p0;
+        pp[GMAX + 2 * CH * GMAX + 1] = p1;
+        pp[GMAX + 2 * CH * GMAX + 2] = p2;
+        s_frag_hp[slot] = k;
       }
       __syncwarp();
     }
+    __syncthreads();
 
-    if (multi) {
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const uint32_t old = atomicAdd(&T.done[s_desc.first], 1u);
-        s_last = old == s_desc.nchunks - 1 ? 1u : 0u;
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        // combine the wave's chunk partials in chunk order, then finalize
-        for (uint32_t k = warp; k < hp_n; k += kTileWarps) {
-          if (lane == 0) {
-            uint32_t cnt[GMAX];
-            double sm[CH][GMAX], sq[CH][GMAX];
-            double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-#pragma unroll
-            for (int g = 0; g < GMAX; ++g) {
-              cnt[g] = 0;
-#pragma unroll
-              for (int c = 0; c < CH; ++c) sm[c][g] = sq[c][g] = 0.0;
-            }
-            for (uint32_t ch = 0; ch < s_desc.nchunks; ++ch) {
-              const double *pp =
-                  T.partials + ((size_t)(s_desc.first + ch) * kWave + k) * partial_size(GMAX, CH);
-#pragma unroll
-              for (int g = 0; g < GMAX; ++g) cnt[g] += (uint32_t)__ldcg(pp + g);
-#pragma unroll
-              for (int c = 0; c < CH; ++c)
-#pragma unroll
-                for (int g = 0; g < GMAX; ++g) {
-                  sm[c][g] += __ldcg(pp + GMAX + c * GMAX + g);
-                  sq[c][g] += __ldcg(pp + GMAX + CH * GMAX + c * GMAX + g);
-                }
-              p0 += __ldcg(pp + GMAX + 2 * CH * GMAX);
-              p1 += __ldcg(pp + GMAX + 2 * CH * GMAX + 1);
-              p2 += __ldcg(pp + GMAX + 2 * CH * GMAX + 2);
-            }
-            finalize_hit<GMAX, CH>(A, s_hit[k].h, cnt, sm, sq, p0, p1, p2, my_tested, my_rejected,
-                                   my_rmax);
-          }
-        }
+    // ---- combine fragments per hit point (slots k .. k+7, warp order) into
+    // this item's partial; k_tile_finalize sums the wave's chunks in order.
+    if (threadIdx.x < hp_n) {
+      const uint32_t k = threadIdx.x;
+      double *out = T.partials + ((size_t)item * kWave + k) * PS;
+      for (int j = 0; j < PS; ++j) {
+        double x = 0.0;
+        for (int w = 0; w < kTileWarps; ++w)
+          if (s_frag_hp[k + w] == k) x += s_frag[(size_t)(k + w) * PS + j];
+        out[j] = x;
       }
     }
     __syncthreads();  // smem (records, hit points, descriptor) reused by the next item
   }
 
   // ------------------------------------------------------ block totals
+  __shared__ unsigned long long s_c[4];
+  if (threadIdx.x == 0) s_c[0] = s_c[1] = s_c[2] = s_c[3] = 0;
+  __syncthreads();
   atomicAdd(&s_c[0], (unsigned long long)my_acc);
   atomicAdd(&s_c[1], (unsigned long long)my_cand);
   atomicAdd(&s_c[2], (unsigned long long)my_exact);
   atomicAdd(&s_c[3], (unsigned long long)my_amb);
-  if (lane == 0) {
-    atomicAdd(&s_tr[0], my_tested);
-    atomicAdd(&s_tr[1], my_rejected);
-    atomicMax(&s_rmax, (unsigned long long)__double_as_longlong(my_rmax));
-  }
   __syncthreads();
   if (threadIdx.x == 0) {
     atomicAdd(&A.counters[0], s_c[0]);
     atomicAdd(&A.counters[1], s_c[1]);
     atomicAdd(&A.counters[2], s_c[2]);
     atomicAdd(&A.counters[3], s_c[3]);
+  }
+}
+
+// One thread per hit point: sum the wave's chunk partials in chunk order
+// (deterministic), pool with the region state and run end_iteration.
+template <int GMAX, int CH>
+__global__ void __launch_bounds__(128) k_tile_finalize(const GatherArgs A, const TileArgs T) {
+  constexpr int PS = partial_size(GMAX, CH);
+  double my_rmax = 0.0;
+  uint32_t my_tested = 0, my_rejected = 0;
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < A.H; h += gridDim.x * blockDim.x) {
+    const uint32_t first = T.hp_map[3 * (size_t)h], nch = T.hp_map[3 * (size_t)h + 1],
+                   slot = T.hp_map[3 * (size_t)h + 2];
+    uint32_t cnt[GMAX];
+    double sm[CH][GMAX], sq[CH][GMAX];
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      cnt[g] = 0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) sm[c][g] = sq[c][g] = 0.0;
+    }
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+      const double *pp = T.partials + ((size_t)(first + ch) * kWave + slot) * PS;
+#pragma unroll
+      for (int g = 0; g < GMAX; ++g) cnt[g] += (uint32_t)pp[g];
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int g = 0; g < GMAX; ++g) {
+          sm[c][g] += pp[GMAX + c * GMAX + g];
+          sq[c][g] += pp[GMAX + CH * GMAX + c * GMAX + g];
+        }
+      p0 += pp[GMAX + 2 * CH * GMAX];
+      p1 += pp[GMAX + 2 * CH * GMAX + 1];
+      p2 += pp[GMAX + 2 * CH * GMAX + 2];
+    }
+    finalize_hit<GMAX, CH>(A, h, cnt, sm, sq, p0, p1, p2, my_tested, my_rejected, my_rmax);
+  }
+  __shared__ unsigned int s_tr[2];
+  __shared__ unsigned long long s_rmax;
+  if (threadIdx.x == 0) { s_tr[0] = s_tr[1] = 0; s_rmax = 0; }
+  __syncthreads();
+  atomicAdd(&s_tr[0], my_tested);
+  atomicAdd(&s_tr[1], my_rejected);
+  atomicMax(&s_rmax, (unsigned long long)__double_as_longlong(my_rmax));
+  __syncthreads();
+  if (threadIdx.x == 0) {
     atomicAdd(A.iter_tr, s_tr[0]);
     atomicAdd(A.iter_tr + 1, s_tr[1]);
     atomicMax(A.rmax_bits, s_rmax);
@@ -622,14 +680,15 @@ cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
 cudaError_t tile_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb,
                                 int sms) {
   k_item_desc<<<blocks_for(nb, 128, sms, 16), 128, 0, s>>>(S.hp_start, nb, A.grid, A.cell_start,
-                                                           S.items, S.chunks, S.item_base, S.desc);
+                                                           S.items, S.chunks, S.item_base,
+                                                           S.hp_order, S.desc, S.hp_map);
   note_launches(1);
   return cudaGetLastError();
 }
 
 template <int GMAX, int CH>
 static cudaError_t launch_tiles(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int sms) {
-  const size_t smem = tile_dyn_smem_bytes();
+  const size_t smem = tile_dyn_smem_bytes<GMAX, CH>();
   cudaError_t e = cudaFuncSetAttribute(k_gather_tiles<GMAX, CH>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -657,6 +716,30 @@ cudaError_t launch_gather_tiles(cudaStream_t s, const GatherArgs &A, const TileA
   if (G <= 8) return launch_tiles<8, 3>(s, A, T, sms);
   if (G <= 12) return launch_tiles<12, 3>(s, A, T, sms);
   return launch_tiles<32, 3>(s, A, T, sms);
+}
+
+template <int GMAX, int CH>
+static cudaError_t launch_fin(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int sms) {
+  if (A.H == 0) return cudaSuccess;
+  k_tile_finalize<GMAX, CH><<<blocks_for(A.H, 128, sms, 8), 128, 0, s>>>(A, T);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_finalize(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
+                                 int sms) {
+  const int G = A.na * A.ns;
+  if (C == 1) {
+    if (G <= 4) return launch_fin<4, 1>(s, A, T, sms);
+    if (G <= 8) return launch_fin<8, 1>(s, A, T, sms);
+    if (G <= 12) return launch_fin<12, 1>(s, A, T, sms);
+    if (G <= 16) return launch_fin<16, 1>(s, A, T, sms);
+    return launch_fin<32, 1>(s, A, T, sms);
+  }
+  if (G <= 4) return launch_fin<4, 3>(s, A, T, sms);
+  if (G <= 8) return launch_fin<8, 3>(s, A, T, sms);
+  if (G <= 12) return launch_fin<12, 3>(s, A, T, sms);
+  return launch_fin<32, 3>(s, A, T, sms);
 }
 
 size_t tile_partial_doubles(int G, int C) {
