@@ -93,7 +93,7 @@ class FppmContext:
                  k: float = 0.7, alpha: float = 0.75, r_min_base: Optional[float] = None,
                  max_depth: int = 10, normal_guard_cos: float = NORMAL_GUARD_COS,
                  max_hitpoints: int = 1, max_photons: int = 1, max_cells: int = 0,
-                 device: int = 0, stream: Optional[int] = None, gather_kernel: str = "tile"):
+                 device: int = 0, stream: Optional[int] = None, gather_kernel: str = "auto"):
         self._lib = N.lib()
         cfg = N.Config()
         cfg.n_annuli, cfg.n_sectors = n_annuli, n_sectors
@@ -110,7 +110,7 @@ class FppmContext:
         cfg.max_hitpoints, cfg.max_photons, cfg.max_cells = max_hitpoints, max_photons, max_cells
         cfg.device = device
         cfg.stream = stream
-        cfg.gather_kernel = {"tile": 0, "warp": 1}[gather_kernel]
+        cfg.gather_kernel = {"auto": 0, "warp": 1, "tile": 2, "lanes": 3}[gather_kernel]
         self.config = cfg
         self.G = n_annuli * n_sectors
         self.C = cfg.channels

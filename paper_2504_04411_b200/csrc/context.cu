@@ -336,6 +336,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->tile.sort.keys_b, Hc)); A(dalloc(&ctx->tile.sort.vals_b, Hc));
   A(dalloc(&ctx->tile.sort.hist, radix_hist_entries((uint32_t)Hc)));
   A(dalloc(&ctx->tile.hp_map, 3 * Hc));
+  A(dalloc(&ctx->tile.nonempty, 1));
   A(cudaMallocHost(&ctx->h_total, sizeof(uint32_t)));
   if (e != cudaSuccess) {
     int rc = cuda_fail(ctx, e, "fppm_gpu_create allocation");
@@ -380,7 +381,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
-                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.partials, T.hp_map};
+                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.partials, T.hp_map, T.nonempty};
   for (void *p : tdev)
     if (p) cudaFree(p);
   if (ctx->h_total) cudaFreeHost(ctx->h_total);
@@ -840,7 +841,12 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
       S.bucket_cap = cap;
     }
     uint32_t nb = 0;
-    FPPM_CUDA_OK(tile_schedule_bins(s, A, S, g, ctx->sms, &nb));
+    // kernel choice: the tiled kernel (candidates per lane) is the default;
+    // the lanes kernel (lanes = hit points) is selectable for A/B runs
+    const int variant = ctx->cfg.gather_kernel == 0 ? 2 : ctx->cfg.gather_kernel;
+    const uint32_t chunk = variant == 3 ? (uint32_t)kLaneChunk : (uint32_t)kChunk;
+    FPPM_CUDA_OK(cudaMemsetAsync(S.nonempty, 0, sizeof(uint32_t), s));
+    FPPM_CUDA_OK(tile_schedule_bins(s, A, S, g, ctx->sms, chunk, &nb));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
                                  cudaMemcpyDeviceToHost, s));
     FPPM_CUDA_OK(cudaStreamSynchronize(s));
@@ -855,14 +861,17 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
       FPPM_CUDA_OK(dalloc(&S.partials, cap * tile_partial_doubles(ctx->G, ctx->C)));
       S.item_cap = cap;
     }
-    FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms));
+    FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms, chunk));
     TileArgs T;
     T.desc = S.desc;
     T.hp_order = S.hp_order;
     T.partials = S.partials;
     T.hp_map = S.hp_map;
     T.total_items = S.item_base + nb;
-    FPPM_CUDA_OK(launch_gather_tiles(s, A, T, ctx->C, ctx->sms));
+    if (variant == 3)
+      FPPM_CUDA_OK(launch_gather_lanes(s, A, T, ctx->C, ctx->sms));
+    else
+      FPPM_CUDA_OK(launch_gather_tiles(s, A, T, ctx->C, ctx->sms));
     FPPM_CUDA_OK(launch_tile_finalize(s, A, T, ctx->C, ctx->sms));
   }
   ctx->end_calls++;

@@ -108,14 +108,19 @@ struct TileSched {
   ItemDesc *desc;
   double *partials;
   uint32_t *hp_map;     // [3 H]
+  uint32_t *nonempty;   // device counter: buckets holding hit points
   unsigned long long bucket_cap, item_cap;
 };
 
 __host__ __device__ constexpr int partial_size(int gmax, int ch) { return gmax + 2 * ch * gmax + 3; }
 
 cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S,
-                               const GridHeader &g, int sms, uint32_t *nb_out);
+                               const GridHeader &g, int sms, uint32_t chunk, uint32_t *nb_out);
 cudaError_t tile_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb,
+                                int sms, uint32_t chunk);
+// lanes kernel (gather_lanes.cu): lanes = hit points of one home cell
+constexpr int kLaneChunk = 2048;  // candidates per item
+cudaError_t launch_gather_lanes(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
                                 int sms);
 cudaError_t launch_gather_tiles(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
                                 int sms);

@@ -218,6 +218,51 @@ static __device__ __forceinline__ bool flush_pair(const HitF &F, const Hit &Hs, 
   return true;
 }
 
+// Fast-path sector of a surviving candidate; false when any band is hit.
+static __device__ __forceinline__ bool fast_sector(const HitF &F, float yu, float yv, float yy, int &sector) {
+  bool ok;
+  int s_ang;
+  if (F.ns == 4) {
+    ok = fabsf(yu) > F.band_y && fabsf(yv) > F.band_y;
+    s_ang = yu > 0.0f ? (yv > 0.0f ? 0 : 3) : (yv > 0.0f ? 1 : 2);
+  } else {
+    ok = fmaxf(fabsf(yu), fabsf(yv)) > 1e-3f * F.r;
+    float th = atan2f(yv, yu);
+    if (th < 0.0f) th += 6.2831853f;
+    const float tt = (float)F.ns * th * 0.15915494f;
+    const float kk = rintf(tt);
+    ok = ok && !(kk >= 1.0f && kk <= (float)(F.ns - 1) && fabsf(tt - kk) < 4e-3f);
+    s_ang = min((int)tt, F.ns - 1);
+  }
+  int a_ring = 0;
+  if (F.na > 1) {
+    const float qa = yy * F.qa_scale;
+    const float kq = rintf(qa);
+    ok = ok && !(kq >= 1.0f && kq <= (float)(F.na - 1) && fabsf(qa - kq) < 1e-4f * (float)F.na);
+    a_ring = min((int)qa, F.na - 1);
+  }
+  sector = a_ring * F.ns + s_ang;
+  return ok;
+}
+
+
+
+// Test phase: ball and depth only (photon_map.cpp:76, integrator.cpp:396).
+// False only when the reference certainly rejects the pair; disk, sector and
+// the remaining filters are decided in the flush, where every lane holds a
+// survivor.
+static __device__ __forceinline__ bool ball_pass(const HitF &F, bool lo_zero, float4 a, uint32_t max_depth) {
+  float dx = a.x - F.chx, dy = a.y - F.chy, dz = a.z - F.chz;
+  if (!lo_zero) {
+    dx -= F.clx;
+    dy -= F.cly;
+    dz -= F.clz;
+  }
+  const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  return d2 <= F.lim_hi && F.eye + __float_as_uint(a.w) <= max_depth;
+}
+
+
 // ---------------------------------------------------------------- accumulators
 // Per-lane fp64 sector accumulators must stay in registers.  Written as
 // "if (sector == k) acc[k] += v" the optimiser proves that exactly one k

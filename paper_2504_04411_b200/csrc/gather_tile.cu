@@ -125,12 +125,14 @@ __device__ __forceinline__ void bucket_cell(const GridHeader &g, uint32_t b, lon
 __global__ void k_bucket_items(const uint32_t *__restrict__ hp_start, uint32_t nb,
                                const GridHeader *__restrict__ hdr,
                                const uint32_t *__restrict__ cell_start,
-                               uint32_t *__restrict__ items, uint32_t *__restrict__ chunks) {
+                               uint32_t *__restrict__ items, uint32_t *__restrict__ chunks,
+                               uint32_t chunk, uint32_t *__restrict__ nonempty) {
   const GridHeader g = *hdr;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
     const uint32_t nhp = b < nb ? hp_start[b + 1] - hp_start[b] : 0u;
     uint32_t ch = 0, it = 0;
     if (nhp) {
+      atomicAdd(nonempty, 1u);
       uint32_t T = 0;
       if (b + 1 < nb) {  // bucket nb-1 is the "no candidates" bucket
         long long ix, iy, iz;
@@ -138,7 +140,7 @@ __global__ void k_bucket_items(const uint32_t *__restrict__ hp_start, uint32_t n
         uint32_t beg[9], len[9];
         T = column_ranges(g, cell_start, ix, iy, iz, beg, len);
       }
-      ch = T == 0 ? 1u : (T + kChunk - 1) / kChunk;
+      ch = T == 0 ? 1u : (T + chunk - 1) / chunk;
       it = ch * ((nhp + kWave - 1) / kWave);
     }
     items[b] = it;
@@ -195,7 +197,8 @@ __global__ void k_item_desc(const uint32_t *__restrict__ hp_start, uint32_t nb,
                             const uint32_t *__restrict__ cell_start,
                             const uint32_t *__restrict__ items, const uint32_t *__restrict__ chunks,
                             const uint32_t *__restrict__ item_base, const uint32_t *__restrict__ hp_order,
-                            ItemDesc *__restrict__ desc, uint32_t *__restrict__ hp_map) {
+                            ItemDesc *__restrict__ desc, uint32_t *__restrict__ hp_map,
+                            uint32_t kChunk) {
   const GridHeader g = *hdr;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
     if (items[b] == 0) continue;
@@ -257,34 +260,6 @@ __global__ void k_item_desc(const uint32_t *__restrict__ hp_start, uint32_t nb,
 #endif
 
 
-// Fast-path sector of a surviving candidate; false when any band is hit.
-__device__ __forceinline__ bool fast_sector(const HitF &F, float yu, float yv, float yy, int &sector) {
-  bool ok;
-  int s_ang;
-  if (F.ns == 4) {
-    ok = fabsf(yu) > F.band_y && fabsf(yv) > F.band_y;
-    s_ang = yu > 0.0f ? (yv > 0.0f ? 0 : 3) : (yv > 0.0f ? 1 : 2);
-  } else {
-    ok = fmaxf(fabsf(yu), fabsf(yv)) > 1e-3f * F.r;
-    float th = atan2f(yv, yu);
-    if (th < 0.0f) th += 6.2831853f;
-    const float tt = (float)F.ns * th * 0.15915494f;
-    const float kk = rintf(tt);
-    ok = ok && !(kk >= 1.0f && kk <= (float)(F.ns - 1) && fabsf(tt - kk) < 4e-3f);
-    s_ang = min((int)tt, F.ns - 1);
-  }
-  int a_ring = 0;
-  if (F.na > 1) {
-    const float qa = yy * F.qa_scale;
-    const float kq = rintf(qa);
-    ok = ok && !(kq >= 1.0f && kq <= (float)(F.na - 1) && fabsf(qa - kq) < 1e-4f * (float)F.na);
-    a_ring = min((int)qa, F.na - 1);
-  }
-  sector = a_ring * F.ns + s_ang;
-  return ok;
-}
-
-
 template <int GMAX, int CH>
 __host__ __device__ constexpr size_t tile_dyn_smem_bytes() {
   return (size_t)kChunk * 64 + (size_t)kMaxFrag * partial_size(GMAX, CH) * sizeof(double);
@@ -299,21 +274,6 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(addr));
   return v;
-}
-
-// Test phase: ball and depth only (photon_map.cpp:76, integrator.cpp:396).
-// False only when the reference certainly rejects the pair; disk, sector and
-// the remaining filters are decided in the flush, where every lane holds a
-// survivor.
-__device__ __forceinline__ bool ball_pass(const HitF &F, bool lo_zero, float4 a, uint32_t max_depth) {
-  float dx = a.x - F.chx, dy = a.y - F.chy, dz = a.z - F.chz;
-  if (!lo_zero) {
-    dx -= F.clx;
-    dy -= F.cly;
-    dz -= F.clz;
-  }
-  const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  return d2 <= F.lim_hi && F.eye + __float_as_uint(a.w) <= max_depth;
 }
 
 template <int GMAX, int CH>
@@ -648,7 +608,7 @@ static inline unsigned blocks_for(unsigned long long n, int threads, int sms, in
 }
 
 cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S,
-                               const GridHeader &g, int sms, uint32_t *nb_out) {
+                               const GridHeader &g, int sms, uint32_t chunk, uint32_t *nb_out) {
   const unsigned long long n_ext =
       (unsigned long long)(g.nx + 2) * (unsigned long long)(g.ny + 2) * (unsigned long long)(g.nz + 2);
   if (n_ext + 1 >= 0xffffffffull) return cudaErrorInvalidValue;
@@ -667,8 +627,8 @@ cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
     k_bucket_start_bsearch<<<blocks_for(nb + 1, 256, sms, 16), 256, 0, s>>>(skeys, A.H, nb, S.hp_start);
   else
     k_bucket_start<<<blocks_for(A.H, 256, sms, 16), 256, 0, s>>>(skeys, A.H, nb, S.hp_start);
-  k_bucket_items<<<blocks_for(nb + 1, 256, sms, 16), 256, 0, s>>>(S.hp_start, nb, A.grid,
-                                                                  A.cell_start, S.items, S.chunks);
+  k_bucket_items<<<blocks_for(nb + 1, 256, sms, 16), 256, 0, s>>>(
+      S.hp_start, nb, A.grid, A.cell_start, S.items, S.chunks, chunk, S.nonempty);
   const uint32_t nt = (nb + 1 + kScanTile - 1) / kScanTile;
   k_scan_tiles<<<nt, 256, 0, s>>>(S.items, nb + 1, S.scan_tmp);
   k_scan_top<<<1, 256, 0, s>>>(S.scan_tmp, nt);
@@ -678,10 +638,10 @@ cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
 }
 
 cudaError_t tile_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb,
-                                int sms) {
+                                int sms, uint32_t chunk) {
   k_item_desc<<<blocks_for(nb, 128, sms, 16), 128, 0, s>>>(S.hp_start, nb, A.grid, A.cell_start,
                                                            S.items, S.chunks, S.item_base,
-                                                           S.hp_order, S.desc, S.hp_map);
+                                                           S.hp_order, S.desc, S.hp_map, chunk);
   note_launches(1);
   return cudaGetLastError();
 }
