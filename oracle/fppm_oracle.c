@@ -608,10 +608,27 @@ static void process_hit(worker_t *w, size_t slot) {
    * without observation (integrator.cpp:483-488). */
   int tested = 0, rejected = 0;
   double stat = 0, critical = 0;
-  if (gathered) {
+  if (gathered && cfg->policy == 2) {
+    /* schedule_end_iteration (gather.cpp:138-144): fixed SPPM schedule */
+    reg->radius = orc_schedule_radius(reg->initial_radius, cfg->alpha, w->iteration + 1);
+    ++reg->t;
+  } else if (gathered) {
     int decide = 0;
     if (cfg->override_decision != 0) {
       rejected = cfg->override_decision == 1;
+      decide = 1;
+    } else if (cfg->policy == 1) {
+      /* chi2_end_iteration (gather.cpp:114-136): channel-0 counts only */
+      uint64_t total = 0;
+      for (int g = 0; g < s->G; ++g) total += reg->count[g];
+      if (total == 0) {
+        rejected = 0;
+      } else {
+        critical = orc_chi2_quantile(1.0 - cfg->alpha_chi2, (double)(s->G - 1), NULL);
+        stat = orc_chi2_statistic(reg->count, s->G, NULL);
+        rejected = stat > critical;
+        tested = 1;
+      }
       decide = 1;
     } else {
       const uint64_t m = reg->t * cfg->samples_per_iteration;

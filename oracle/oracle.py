@@ -45,7 +45,7 @@ class Config(C.Structure):
         ("k", C.c_double), ("alpha", C.c_double), ("r_min_base", C.c_double),
         ("initial_radius", C.c_double), ("samples_per_iteration", C.c_uint64),
         ("max_depth", C.c_uint32), ("normal_guard_cos", C.c_double),
-        ("threads", C.c_int),
+        ("threads", C.c_int), ("alpha_chi2", C.c_double), ("policy", C.c_int),
     ]
 
 
@@ -243,7 +243,8 @@ class _Session:
         defaults = dict(n_annuli=2, n_sectors=6, alpha_f=0.01, channels=1,
                         override_decision=0, k=0.7, alpha=0.75, r_min_base=0.0,
                         initial_radius=0.02, samples_per_iteration=1, max_depth=10,
-                        normal_guard_cos=0.86602540378443865, threads=1)
+                        normal_guard_cos=0.86602540378443865, threads=1, alpha_chi2=0.01,
+                        policy=0)
         defaults.update(cfg)
         for k_, v in defaults.items():
             setattr(c, k_, v)

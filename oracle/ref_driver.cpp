@@ -189,6 +189,8 @@ struct RefConfig { // identical layout to orc_config (fppm_oracle.h)
   uint32_t max_depth;
   double normal_guard_cos;
   int threads;
+  double alpha_chi2;
+  int policy;  // 0 end_iteration, 1 chi2_end_iteration, 2 schedule_end_iteration
 };
 
 struct RefIterOut { // identical layout to orc_iter_out
@@ -230,6 +232,7 @@ void* ref_session_create(const RefConfig* cfg, size_t H, const double* pos,
     test.n_annuli = cfg->n_annuli;
     test.n_sectors = cfg->n_sectors;
     test.alpha_f = cfg->alpha_f;
+    test.alpha_chi2 = cfg->alpha_chi2;
     test.channels = cfg->channels == 3 ? TestChannels::rgb : TestChannels::luminance;
     test.override_decision = cfg->override_decision == 1   ? TestOverride::always_reject
                              : cfg->override_decision == 2 ? TestOverride::never_reject
@@ -363,7 +366,10 @@ int ref_session_iterate(void* sp, uint64_t iteration, const float* ppos,
       }
       RadiusUpdate up;
       if (gathered) {
-        up = region->end_iteration(iteration, cfg.samples_per_iteration); // :480
+        // :478-480 (CPPM uses chi2_end_iteration); schedule policy: gather.cpp:138
+        up = cfg.policy == 1   ? region->chi2_end_iteration(iteration, cfg.samples_per_iteration)
+             : cfg.policy == 2 ? region->schedule_end_iteration(iteration)
+                               : region->end_iteration(iteration, cfg.samples_per_iteration);
       } else {
         up.radius = region->radius(); // :486
       }

@@ -1,0 +1,90 @@
+"""CPU, world_size 2 over gloo: the multi-GPU decomposition reproduces the
+single-process result exactly.
+
+Each rank generates its photon share, the shares are all-gathered in rank
+order, the cell size is all-reduced (max), and each rank gathers + tests its
+own band of raster rows.  The oracle stands in for the per-rank device work
+(the decomposition logic, not the kernels, is under test here); the per-rank
+results, stitched by rows, must equal one single-process run bit for bit.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+W, N, ITERS = 24, 1 << 13, 3
+CFG = dict(n_annuli=2, n_sectors=4, alpha_f=0.01, initial_radius=0.05, r_min_base=5e-5,
+           samples_per_iteration=N, threads=2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    from oracle import Oracle
+    from paper_2504_04411_b200.distributed import (allgather_photons, global_cell_size,
+                                                   photon_share, row_band)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle("port")
+    hp = orc.gen_raster_hitpoints(W)
+    r0, r1 = row_band(W, rank, world)
+    mine = {k: v[r0 * W:r1 * W] for k, v in hp.items()}
+    sess = orc.session(CFG, mine)
+    results = []
+    for it in range(1, ITERS + 1):
+        b, n = photon_share(N, rank, world)
+        part = orc.gen_photons(2, 0x5EED, it, b, n)
+        local = {"pos": torch.from_numpy(part["pos"]), "normal": torch.from_numpy(part["nrm"]),
+                 "wi": torch.from_numpy(part["wi"]), "power": torch.from_numpy(part["pow"]),
+                 "depth": torch.from_numpy(part["depth"].view(np.int32))}
+        full = allgather_photons(local, N)
+        ph = {"pos": full["pos"].numpy(), "nrm": full["normal"].numpy(), "wi": full["wi"].numpy(),
+              "pow": full["power"].numpy(), "depth": full["depth"].numpy().view(np.uint32)}
+        cell = global_cell_size(sess.max_radius())
+        out = sess.iterate(it, ph, cell=cell)
+        results.append({k: v for k, v in out.items() if k != "times"})
+    np.save(os.path.join(outdir, f"rank{rank}.npy"), results, allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_decomposition_matches_single_process(port, tmp_path):
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    per_rank = [np.load(tmp_path / f"rank{r}.npy", allow_pickle=True) for r in range(world)]
+    hp = port.gen_raster_hitpoints(W)
+    sess = port.session(CFG, hp)
+    for it in range(1, ITERS + 1):
+        want = sess.iterate(it, port.gen_photons(2, 0x5EED, it, 0, N))
+        for k in want:
+            if k == "times":
+                continue
+            got = np.concatenate([per_rank[r][it - 1][k] for r in range(world)], axis=0)
+            assert np.array_equal(got, want[k]), (it, k)
+
+
+def test_partitions_cover_exactly():
+    from paper_2504_04411_b200.distributed import photon_share, row_band
+    for world in (1, 2, 3, 4, 8):
+        rows = [row_band(512, r, world) for r in range(world)]
+        assert rows[0][0] == 0 and rows[-1][1] == 512
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+        shares = [photon_share(1 << 22, r, world) for r in range(world)]
+        assert sum(c for _, c in shares) == 1 << 22
+        assert all(s[0] + s[1] == t[0] for s, t in zip(shares, shares[1:]))

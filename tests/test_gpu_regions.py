@@ -1,0 +1,309 @@
+"""GPU mirror of the reference's GatherRegion unit tests (proj/tests/test_gather.cpp)
+plus bit-level parity of the device sector binning / statistics / decisions.
+
+GatherRegionBatch holds `count` fppm::GatherRegion objects in HBM; accumulate
+and end_iteration run as CUDA kernels through the C ABI.  Random draws come
+from numpy (the reference's RngStream sequences are not needed: these are
+property tests, and the parity cases compare against the oracle on the same
+inputs)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2504_04411_b200 import InvalidArgument, DomainError
+from paper_2504_04411_b200.api import (GatherRegionBatch, RadiusSchedule, TestConfig,
+                                       chi2_quantile, f_quantile, schedule_radius)
+
+pytestmark = pytest.mark.gpu
+
+
+def schedule(r_min, k=0.7, alpha=0.75):
+    return RadiusSchedule(k=k, alpha=alpha, r_min_base=r_min)
+
+
+def lum(v):
+    v = np.asarray(v, np.float64)
+    return 0.2126 * v[..., 0] + 0.7152 * v[..., 1] + 0.0722 * v[..., 2]
+
+
+def acc1(b, y, v, region=0):
+    b.accumulate(np.array([region], np.uint32), np.array([y], np.float64),
+                 np.array([[v, v, v]] if np.isscalar(v) else [v], np.float64))
+
+
+def test_sector_index_layout():
+    # test_gather.cpp:26-36 on the device: one region per sample
+    pts = [((0.999, 0.0), 6), ((0.0, 0.4), 1), ((0.0, -0.4), 4), ((1.0, 0.0), 6), ((0.0, 0.0), 0)]
+    b = GatherRegionBatch(TestConfig(), schedule(0.001), 1.0, count=len(pts))
+    b.accumulate(np.arange(len(pts), dtype=np.uint32), np.array([p for p, _ in pts]),
+                 np.ones((len(pts), 3)))
+    for i, (_, want) in enumerate(pts):
+        cnt, _, _ = b.sector_stats(i)
+        assert int(np.argmax(cnt)) == want and cnt.sum() == 1
+    with pytest.raises(DomainError):
+        acc1(b, (1.1, 0.0), 1.0)
+
+
+@pytest.mark.parametrize("na,ns", [(2, 6), (1, 4), (3, 5), (1, 2), (4, 8)])
+def test_sector_index_bitexact_vs_oracle(port, na, ns):
+    rng = np.random.default_rng(na * 100 + ns)
+    n = 4000
+    r = 0.37
+    rr = r * np.sqrt(rng.random(n))
+    phi = 2 * np.pi * rng.random(n)
+    y = np.stack([rr * np.cos(phi), rr * np.sin(phi)], 1)
+    # boundary cases: axes, annulus edges, the rim, sector edges, the centre
+    edges = [(r, 0.0), (0.0, r), (-r, 0.0), (0.0, -r), (0.0, 0.0), (r * math.sqrt(0.5), 0.0),
+             (r * math.sqrt(1 / na), 0.0), (-1e-300, 0.0), (0.0, -0.0), (-0.0, -1e-17)]
+    for s in range(ns):
+        a = 2 * math.pi * s / ns
+        edges.append((0.5 * r * math.cos(a), 0.5 * r * math.sin(a)))
+    y = np.concatenate([y, np.array(edges)])
+    b = GatherRegionBatch(TestConfig(n_annuli=na, n_sectors=ns), schedule(0.001), r, count=len(y))
+    b.accumulate(np.arange(len(y), dtype=np.uint32), y, np.ones((len(y), 3)))
+    cnt = b._ctx.regions()["stat_count"]
+    got = np.argmax(cnt, axis=1)
+    want = np.array([port.sector_index(u, v, r, na, ns) for u, v in y])
+    assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+
+
+def test_hold_keeps_stats_reject_clears_them():
+    # test_gather.cpp:66-96
+    holder = GatherRegionBatch(TestConfig(override_decision="never_reject"), schedule(0.001), 1.0,
+                               samples_per_iteration=10)
+    acc1(holder, (0.1, 0.2), 2.0)
+    up = holder.end_iteration(1, 10)
+    assert up["rejected"][0] == 0 and up["radius"][0] == 1.0
+    assert holder.held_iterations()[0] == 2
+    cnt, s, _ = holder.sector_stats(0)
+    assert s[1] == pytest.approx(lum([2.0, 2.0, 2.0]))  # sector of (0.1, 0.2) in 2x6
+
+    shrinker = GatherRegionBatch(TestConfig(override_decision="always_reject"), schedule(0.001),
+                                 1.0, samples_per_iteration=10)
+    acc1(shrinker, (0.1, 0.2), 2.0)
+    up = shrinker.end_iteration(1, 10)
+    assert up["rejected"][0] == 1 and up["radius"][0] == pytest.approx(0.7)
+    assert shrinker.held_iterations()[0] == 1
+    cnt, s, q = shrinker.sector_stats(0)
+    assert not cnt.any() and not s.any() and not q.any()
+
+
+def test_shrink_respects_power_law_floor():
+    # test_gather.cpp:98-106
+    b = GatherRegionBatch(TestConfig(override_decision="always_reject"), schedule(1.0, 0.5, 0.75),
+                          1.0, samples_per_iteration=10)
+    up = b.end_iteration(3, 10)
+    assert up["radius"][0] == pytest.approx(4.0 ** -0.125, rel=1e-12)
+
+
+def test_forced_rejection_reproduces_fixed_schedule():
+    # test_gather.cpp:108-121: bitwise equal trajectories
+    forced = GatherRegionBatch(TestConfig(override_decision="always_reject"),
+                               schedule(0.5, 0.7, 0.75), 0.5, samples_per_iteration=10)
+    fixed = GatherRegionBatch(TestConfig(), schedule(0.5, 0.7, 0.75), 0.5,
+                              samples_per_iteration=10, policy="schedule")
+    for i in range(1, 201):
+        a = forced.end_iteration(i, 10)["radius"][0]
+        b = fixed.end_iteration(i, 10)["radius"][0]
+        assert a == b == schedule_radius(0.5, 0.75, i + 1)
+
+
+def test_radius_monotone_and_bounded():
+    # test_gather.cpp:123-152, 16 independent regions at once
+    R = 16
+    rng = np.random.default_rng(17)
+    b = GatherRegionBatch(TestConfig(), schedule(0.001), 1.0, count=R, samples_per_iteration=40)
+    prev = b.radius().copy()
+    shrinks = 0
+    for i in range(1, 401):
+        burst = i % 60 == 0
+        rad = b.radius()
+        reg = np.repeat(np.arange(R, dtype=np.uint32), 40)
+        rr_ = np.repeat(rad, 40)
+        if burst:
+            y = np.stack([0.2 * rr_, 0.01 * rr_ * rng.random(len(reg))], 1)
+        else:
+            rr = rr_ * np.sqrt(rng.random(len(reg)))
+            phi = 2 * np.pi * rng.random(len(reg))
+            y = np.stack([rr * np.cos(phi), rr * np.sin(phi)], 1)
+        b.accumulate(reg, y, np.ones((len(reg), 3)))
+        up = b.end_iteration(i, 40)
+        shrinks += int(up["rejected"].sum())
+        assert np.all(up["radius"] <= prev + 1e-15)
+        assert np.all(up["radius"] >= schedule_radius(0.001, 0.75, i + 1) - 1e-12)
+        prev = up["radius"].copy()
+    assert shrinks > 0
+
+
+def test_t_counts_iterations_at_current_radius():
+    b = GatherRegionBatch(TestConfig(override_decision="never_reject"), schedule(0.001), 1.0,
+                          samples_per_iteration=10)
+    assert b.held_iterations()[0] == 1
+    b.end_iteration(1, 10)
+    b.end_iteration(2, 10)
+    assert b.held_iterations()[0] == 3
+
+
+def test_hot_sector_triggers_f_rejection():
+    rng = np.random.default_rng(23)
+    b = GatherRegionBatch(TestConfig(), schedule(0.001), 1.0, samples_per_iteration=60)
+    shrank = False
+    for i in range(1, 4):
+        y = np.stack([np.full(60, 0.2), 0.05 * rng.random(60)], 1)
+        b.accumulate(np.zeros(60, np.uint32), y, np.full((60, 3), 5.0))
+        shrank = bool(b.end_iteration(i, 60)["rejected"][0])
+        if shrank:
+            break
+    assert shrank
+
+
+def test_null_data_rarely_shrinks():
+    # 64 regions x 200 iterations of null data: the per-region rejection rate
+    # must stay near alpha_f = 1% (reference bound: <= 10 of 200)
+    R = 64
+    rng = np.random.default_rng(29)
+    b = GatherRegionBatch(TestConfig(), schedule(0.001), 1.0, count=R, samples_per_iteration=24)
+    rejects = np.zeros(R, int)
+    for i in range(1, 201):
+        rad = np.repeat(b.radius(), 24)
+        rr = rad * np.sqrt(rng.random(len(rad)))
+        phi = 2 * np.pi * rng.random(len(rad))
+        v = np.repeat((1.0 + 0.2 * rng.random(len(rad)))[:, None], 3, 1)
+        b.accumulate(np.repeat(np.arange(R, dtype=np.uint32), 24),
+                     np.stack([rr * np.cos(phi), rr * np.sin(phi)], 1), v)
+        rejects += b.end_iteration(i, 24)["rejected"]
+    assert rejects.max() <= 10
+    assert rejects.mean() <= 5
+
+
+def test_rgb_mode_catches_compensating_channel_shifts():
+    red = 0.5
+    green = -red * 0.2126 / 0.7152
+    lum_b = GatherRegionBatch(TestConfig(), schedule(0.001), 1.0, samples_per_iteration=200)
+    rgb_b = GatherRegionBatch(TestConfig(channels="rgb"), schedule(0.001), 1.0,
+                              samples_per_iteration=200)
+    rng = np.random.default_rng(41)
+    for i in range(1, 5):
+        rr = np.sqrt(rng.random(200))
+        phi = 2 * np.pi * rng.random(200)
+        unit = np.stack([rr * np.cos(phi), rr * np.sin(phi)], 1)
+        # sector 0 of the 2x6 layout on the unit disk
+        th = np.mod(np.arctan2(unit[:, 1], unit[:, 0]), 2 * np.pi)
+        s0 = (rr * rr < 0.5) & (th < 2 * np.pi / 6)
+        v = np.ones((200, 3))
+        v[s0, 0] += red
+        v[s0, 1] += green
+        z = np.zeros(200, np.uint32)
+        lum_b.accumulate(z, unit * lum_b.radius()[0], v)
+        rgb_b.accumulate(z, unit * rgb_b.radius()[0], v)
+        lum_b.end_iteration(i, 200)
+        rgb_b.end_iteration(i, 200)
+    assert lum_b.radius()[0] == 1.0
+    assert rgb_b.radius()[0] < 1.0
+
+
+def test_chi2_policy_reacts_to_concentrated_counts_only():
+    rng = np.random.default_rng(59)
+    uni = GatherRegionBatch(TestConfig(), schedule(0.001), 1.0, samples_per_iteration=120,
+                            policy="chi2")
+    skw = GatherRegionBatch(TestConfig(), schedule(0.001), 1.0, samples_per_iteration=120,
+                            policy="chi2")
+    z = np.zeros(120, np.uint32)
+    for i in range(1, 6):
+        rr = np.sqrt(rng.random(120)) * uni.radius()[0]
+        phi = 2 * np.pi * rng.random(120)
+        uni.accumulate(z, np.stack([rr * np.cos(phi), rr * np.sin(phi)], 1), np.ones((120, 3)))
+        sr = skw.radius()[0]
+        skw.accumulate(z, np.stack([np.full(120, 0.2 * sr), 0.01 * sr * rng.random(120)], 1),
+                       np.ones((120, 3)))
+        uni.end_iteration(i, 120)
+        skw.end_iteration(i, 120)
+    assert uni.radius()[0] == 1.0
+    assert skw.radius()[0] < 1.0
+    empty = GatherRegionBatch(TestConfig(), schedule(0.001), 1.0, samples_per_iteration=120,
+                              policy="chi2")
+    up = empty.end_iteration(1, 120)
+    assert up["tested"][0] == 0 and up["radius"][0] == 1.0
+
+
+def test_constructor_validation():
+    with pytest.raises(InvalidArgument):
+        GatherRegionBatch(TestConfig(), schedule(2.0), 1.0)
+    with pytest.raises(InvalidArgument):
+        GatherRegionBatch(TestConfig(), schedule(0.001, 1.5), 1.0)
+    with pytest.raises(InvalidArgument):
+        GatherRegionBatch(TestConfig(), schedule(0.001, 0.7, 0.3), 1.0)
+    with pytest.raises(InvalidArgument):
+        GatherRegionBatch(TestConfig(), schedule(0.001), 0.0)
+    with pytest.raises(InvalidArgument):
+        GatherRegionBatch(TestConfig(n_annuli=1, n_sectors=1), schedule(0.001), 1.0)
+
+
+@pytest.mark.parametrize("channels", ["luminance", "rgb"])
+@pytest.mark.parametrize("policy", ["ftest", "chi2"])
+def test_statistics_and_decisions_match_oracle(port, channels, policy):
+    """Streaming sector stats, statistic, critical value and decision of 256
+    regions over 6 iterations vs the oracle's f_statistic / chi2_statistic and
+    quantiles on the same samples (sums in the same sample order)."""
+    R, J, na, ns = 256, 48, 2, 4
+    G, Cn = na * ns, (3 if channels == "rgb" else 1)
+    rng = np.random.default_rng(7 + len(channels) + len(policy))
+    test = TestConfig(n_annuli=na, n_sectors=ns, alpha_f=0.05, alpha_chi2=0.05, channels=channels)
+    b = GatherRegionBatch(test, schedule(0.001), 1.0, count=R, samples_per_iteration=J,
+                          policy=policy)
+    radius = np.ones(R)
+    t = np.ones(R, np.uint64)
+    cnt = np.zeros((R, Cn * G), np.uint64)
+    s = np.zeros((R, Cn * G))
+    q = np.zeros((R, Cn * G))
+    for it in range(1, 7):
+        # a hot sector in some regions, uniform elsewhere
+        reg = np.repeat(np.arange(R, dtype=np.uint32), J)
+        rr = np.sqrt(rng.random(R * J)) * radius[reg]
+        phi = 2 * np.pi * rng.random(R * J)
+        hot = (reg % 5 == 0) & (rng.random(R * J) < 0.3)
+        phi[hot] = 0.3
+        y = np.stack([rr * np.cos(phi), rr * np.sin(phi)], 1)
+        v = rng.random((R * J, 3)) + 0.5
+        b.accumulate(reg, y, v)
+        for k in range(R * J):  # host restatement of accumulate (gather.cpp:59-67)
+            h = reg[k]
+            sec = port.sector_index(y[k, 0], y[k, 1], radius[h], na, ns)
+            vals = [lum(v[k])] if Cn == 1 else list(v[k])
+            for c, x in enumerate(vals):
+                cnt[h, c * G + sec] += 1
+                s[h, c * G + sec] += x
+                q[h, c * G + sec] += x * x
+        st = b._ctx.regions()
+        assert np.array_equal(st["stat_count"], cnt)
+        np.testing.assert_allclose(st["stat_sum"], s, rtol=1e-13)
+        np.testing.assert_allclose(st["stat_sum_sq"], q, rtol=1e-13)
+        up = b.end_iteration(it, J)
+        for h in range(R):
+            if policy == "ftest":
+                m = int(t[h]) * J
+                crit = f_quantile(1 - 0.05, G - 1, G * (m - 1))
+                fs = [port.f_statistic(cnt[h, c * G:(c + 1) * G], s[h, c * G:(c + 1) * G],
+                                       q[h, c * G:(c + 1) * G], m) for c in range(Cn)]
+                stat, rej = max(fs), any(f > crit for f in fs)
+            else:
+                crit = chi2_quantile(1 - 0.05, G - 1)
+                stat = port.chi2_statistic(cnt[h, :G])
+                rej = stat > crit
+            assert up["tested"][h] == 1
+            assert up["critical"][h] == crit
+            assert up["statistic"][h] == pytest.approx(stat, rel=1e-9)
+            if abs(stat - crit) > 1e-6 * crit:
+                assert bool(up["rejected"][h]) == rej, (it, h, stat, crit)
+            rej = bool(up["rejected"][h])
+            if rej:
+                radius[h] = max(0.7 * radius[h], schedule_radius(0.001, 0.75, it + 1))
+                t[h] = 1
+                cnt[h] = 0
+                s[h] = 0
+                q[h] = 0
+            else:
+                t[h] += 1
+        assert np.array_equal(up["radius"], radius)
+        assert np.array_equal(b.held_iterations(), t)
