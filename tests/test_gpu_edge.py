@@ -145,12 +145,23 @@ def test_closed_ball_rim_and_coincident_photons(port):
     assert int(want["accepted"][0]) >= 6
 
 
-def test_photons_outside_guard_or_depth_are_ignored(port):
+def test_normal_guard_and_depth_filters(port):
+    """Flipped photon normals fail the 30-degree guard against their own hit
+    point (only stray cross-region pairs survive); max_depth 2 keeps only
+    depth-1 photons of eye-depth-1 hit points."""
     hit, ph = scene3d(8, H=200, N=8000)
-    ph["nrm"] = -ph["nrm"]  # every photon fails the 30-degree normal guard
     ctx, sess = make_pair(port, hit, BASE)
     ctx.set_photons(ph["pos"], ph["nrm"], ph["wi"], ph["pow"], ph["depth"])
+    base, _ = ctx.iterate(1, stats=True)
+    flipped = dict(ph, nrm=-ph["nrm"])
+    ctx, sess = make_pair(port, hit, BASE)
+    ctx.set_photons(flipped["pos"], flipped["nrm"], flipped["wi"], flipped["pow"], flipped["depth"])
     got, _ = ctx.iterate(1, stats=True)
-    want = sess.iterate(1, ph)
-    compare_iteration(got, want)
-    assert int(got["accepted"].sum()) == 0
+    compare_iteration(got, sess.iterate(1, flipped))
+    assert got["accepted"].sum() * 20 < base["accepted"].sum()
+    shallow = dict(BASE, max_depth=2)
+    ctx, sess = make_pair(port, hit, shallow)
+    ctx.set_photons(ph["pos"], ph["nrm"], ph["wi"], ph["pow"], ph["depth"])
+    got, _ = ctx.iterate(1, stats=True)
+    compare_iteration(got, sess.iterate(1, ph))
+    assert np.all(got["accepted"][hit["eye_depth"] > 1] == 0)
