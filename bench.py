@@ -40,7 +40,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--workload", default="c2", choices=["c1", "c2"])
-    p.add_argument("--kernel", default="auto", choices=["auto", "tile", "warp", "lanes"],
+    p.add_argument("--kernel", default="auto", choices=["auto", "fine", "tile", "warp", "lanes"],
                    help="gather kernel variant (A/B)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")

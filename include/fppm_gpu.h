@@ -89,7 +89,8 @@ typedef struct fppm_gpu_config {
   uint32_t max_cells; /* 0 -> 1<<28 dense cells */
   int32_t device;     /* CUDA ordinal */
   void *stream;       /* cudaStream_t to order work on; NULL -> own stream */
-  int32_t gather_kernel; /* 0 auto; 1 warp per hit point; 2 tiled (candidates per lane); 3 lanes = hit points */
+  int32_t gather_kernel; /* 0 auto (= 4); 1 warp per hit point; 2 tiled; 3 lanes = hit points;
+                            4 fine-cell tiled (default) */
 } fppm_gpu_config;
 
 typedef struct fppm_gpu_ctx fppm_gpu_ctx;

@@ -110,7 +110,7 @@ class FppmContext:
         cfg.max_hitpoints, cfg.max_photons, cfg.max_cells = max_hitpoints, max_photons, max_cells
         cfg.device = device
         cfg.stream = stream
-        cfg.gather_kernel = {"auto": 0, "warp": 1, "tile": 2, "lanes": 3}[gather_kernel]
+        cfg.gather_kernel = {"auto": 0, "warp": 1, "tile": 2, "lanes": 3, "fine": 4}[gather_kernel]
         self.config = cfg
         self.G = n_annuli * n_sectors
         self.C = cfg.channels

@@ -59,10 +59,22 @@ struct GridHeader {
   uint32_t key_bits;
   uint32_t n;      // photons in the grid
   uint32_t ok;     // 1 when dims fit the dense table
+  uint32_t S;      // fine cells per reference cell and axis (power of two; 1 = reference cells)
+  uint32_t shift;  // log2(S)
   uint32_t pad;
 };
+// With S > 1 the dense table indexes FINE cells of size cell / S ("slab"
+// layout, used when the photons span few reference cells along z): inv is
+// S / cell and ix0.. / nx.. are fine-cell coordinates.  Because S is a power
+// of two, floor(x * (S / cell)) = S * floor-part of x * (1 / cell) exactly, so
+// the reference cell of a fine cell is its coordinate >> shift.
 
-// Sorted photon record, 4 x 16 B vectors (SoA of float4):
+// Sorted photon record, 4 x 16 B vectors (SoA of float4).
+// Layout used by the fine gather (gather_fine.cu):
+//   rec0 = (x, y, z, depth bits), rec1 = (n.z, wi.z, lum(pow) as fp64 lo/hi),
+//   rec2 = (pow.r, pow.g, pow.b, flags), rec3 = (n.x, n.y, wi.x, wi.y)
+//   flags bit0: n.x, n.y, wi.x, wi.y all finite (planar-shortcut exactness)
+// Layout used by the tile / warp / lanes kernels:
 //   rec0 = (x, y, z, depth bits)     -- the only vector read per candidate
 //   rec1 = (nx, ny, nz, wi.x)
 //   rec2 = (wi.y, wi.z, pow.r, pow.g)

@@ -280,6 +280,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   if (c.n_annuli * c.n_sectors > 32) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.channels != FPPM_CHANNELS_LUMINANCE && c.channels != FPPM_CHANNELS_RGB) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy < FPPM_POLICY_FTEST || c.policy > FPPM_POLICY_SCHEDULE) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.gather_kernel < 0 || c.gather_kernel > 4) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy == FPPM_POLICY_FTEST && c.override_decision == FPPM_OVERRIDE_NONE &&
       !(c.alpha_f > 0.0 && c.alpha_f < 1.0)) return FPPM_ERR_INVALID_ARGUMENT;  // stat_tests.cpp:88
   int ndev = 0;
@@ -381,7 +382,8 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
-                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.partials, T.hp_map, T.nonempty};
+                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.fdesc, T.partials,
+                  T.hp_map, T.nonempty};
   for (void *p : tdev)
     if (p) cudaFree(p);
   if (ctx->h_total) cudaFreeHost(ctx->h_total);
@@ -635,7 +637,14 @@ int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi
   return FPPM_OK;
 }
 
-int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size) {
+// gather kernel variant: 1 warp per hit point, 2 tiled, 3 lanes, 4 fine (default)
+static int gather_variant(const fppm_gpu_ctx *ctx) {
+  if (ctx->cfg.gather_kernel == 0) return fine_supported(ctx->G, ctx->C) ? 4 : 2;
+  return ctx->cfg.gather_kernel;
+}
+
+// S_req > 1 asks for the fine (slab) table when the photon set allows it.
+static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   cudaStream_t s = ctx->stream;
   ctx->grid_valid = false;
@@ -649,8 +658,8 @@ int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size) {
   FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_bounds, ctx->h_bounds_init, sizeof(long long) * 6,
                                cudaMemcpyHostToDevice, s));
   if (!ctx->in_pos) use_staging(ctx);
-  launch_cell_bounds(s, ctx->in_pos, ctx->N, ctx->d_cell, ctx->d_bounds, ctx->sms);
-  launch_grid_header(s, ctx->d_bounds, ctx->d_cell, ctx->N, ctx->cfg.max_cells, ctx->d_hdr);
+  launch_cell_bounds(s, ctx->in_pos, ctx->N, ctx->d_cell, S_req, ctx->d_bounds, ctx->sms);
+  launch_grid_header(s, ctx->d_bounds, ctx->d_cell, ctx->N, ctx->cfg.max_cells, S_req, ctx->d_hdr);
   FPPM_CUDA_OK(cudaGetLastError());
   FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_hdr, ctx->d_hdr, sizeof(GridHeader), cudaMemcpyDeviceToHost, s));
   FPPM_CUDA_OK(cudaStreamSynchronize(s));
@@ -669,16 +678,30 @@ int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size) {
   FPPM_CUDA_OK(radix_sort_pairs(s, ctx->sort, ctx->N, g.key_bits, &ctx->d_skeys, &ctx->d_order));
   launch_cell_start(s, ctx->d_skeys, ctx->N, ctx->d_hdr, ctx->d_cell_start, g.ncells, ctx->sms);
   launch_permute(s, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,
-                 ctx->in_depth, ctx->recs, ctx->sms);
+                 ctx->in_depth, ctx->recs, gather_variant(ctx) == 4, ctx->sms);
   FPPM_CUDA_OK(cudaGetLastError());
   ctx->grid_valid = true;
   return FPPM_OK;
+}
+
+// The fine gather uses the fine (slab) table; query_ball / export_grid switch
+// back to reference cells on demand (ensure_reference_cells).
+int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  return build_grid_impl(ctx, cell_size, gather_variant(ctx) == 4 ? kFineS : 1u);
+}
+
+// query_ball / export need the reference-cell table
+static int ensure_reference_cells(fppm_gpu_ctx *ctx) {
+  if (!ctx->grid_valid || ctx->h_hdr->S == 1) return FPPM_OK;
+  return build_grid_impl(ctx, ctx->h_hdr->cell, 1);
 }
 
 int fppm_gpu_export_grid(fppm_gpu_ctx *ctx, uint64_t *keys, uint32_t *begin, uint32_t *end,
                          uint32_t *order, uint64_t *ncells) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "grid not built");
+  if (int rc = ensure_reference_cells(ctx)) return rc;
   const uint32_t n = ctx->N;
   std::vector<uint32_t> sk(n), ord(n);
   if (n) {
@@ -711,6 +734,7 @@ int fppm_gpu_query_ball(fppm_gpu_ctx *ctx, const double *centers, const double *
                         uint64_t *offsets, uint32_t *indices, uint64_t cap, uint64_t *total) {
   if (!ctx || (nq && (!centers || !radii || !offsets))) return FPPM_ERR_INVALID_ARGUMENT;
   if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "grid not built");
+  if (int rc = ensure_reference_cells(ctx)) return rc;
   const GridHeader g = *ctx->h_hdr;
   if (ctx->N > 0)
     for (uint32_t q = 0; q < nq; ++q)
@@ -841,37 +865,63 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
       S.bucket_cap = cap;
     }
     uint32_t nb = 0;
-    // kernel choice: the tiled kernel (candidates per lane) is the default;
-    // the lanes kernel (lanes = hit points) is selectable for A/B runs
-    const int variant = ctx->cfg.gather_kernel == 0 ? 2 : ctx->cfg.gather_kernel;
-    const uint32_t chunk = variant == 3 ? (uint32_t)kLaneChunk : (uint32_t)kChunk;
+    // kernel choice: the fine-cell tiled kernel is the default (it needs the
+    // fine record layout and supports G*C <= 24); the tiled, lanes and warp
+    // kernels are selectable for A/B runs and as parity cross-checks
+    int variant = gather_variant(ctx);
+    if (variant == 4 && !fine_supported(ctx->G, ctx->C))
+      return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "fine gather supports n_a*n_s*channels <= 24; "
+                                                  "select gather_kernel 1-3");
+    const uint32_t chunk = variant == 4   ? fine_chunk(ctx->G, ctx->C)
+                           : variant == 3 ? (uint32_t)kLaneChunk
+                                          : (uint32_t)kChunk;
     FPPM_CUDA_OK(cudaMemsetAsync(S.nonempty, 0, sizeof(uint32_t), s));
-    FPPM_CUDA_OK(tile_schedule_bins(s, A, S, g, ctx->sms, chunk, &nb));
+    if (variant == 4)
+      FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, chunk, &nb));
+    else
+      FPPM_CUDA_OK(tile_schedule_bins(s, A, S, g, ctx->sms, chunk, &nb));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
                                  cudaMemcpyDeviceToHost, s));
     FPPM_CUDA_OK(cudaStreamSynchronize(s));
     const uint32_t total = *ctx->h_total;
     if (total > S.item_cap) {
       if (S.desc) cudaFree(S.desc);
+      if (S.fdesc) cudaFree(S.fdesc);
       if (S.partials) cudaFree(S.partials);
       S.desc = nullptr;
+      S.fdesc = nullptr;
       S.partials = nullptr;
       const unsigned long long cap = std::max<unsigned long long>(total + total / 4, 1024);
-      FPPM_CUDA_OK(dalloc(&S.desc, cap));
+      if (variant == 4)
+        FPPM_CUDA_OK(dalloc(&S.fdesc, cap));
+      else
+        FPPM_CUDA_OK(dalloc(&S.desc, cap));
       FPPM_CUDA_OK(dalloc(&S.partials, cap * tile_partial_doubles(ctx->G, ctx->C)));
       S.item_cap = cap;
     }
-    FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms, chunk));
     TileArgs T;
-    T.desc = S.desc;
     T.hp_order = S.hp_order;
     T.partials = S.partials;
     T.hp_map = S.hp_map;
     T.total_items = S.item_base + nb;
-    if (variant == 3)
-      FPPM_CUDA_OK(launch_gather_lanes(s, A, T, ctx->C, ctx->sms));
-    else
-      FPPM_CUDA_OK(launch_gather_tiles(s, A, T, ctx->C, ctx->sms));
+    if (variant == 4) {
+      FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, chunk));
+      FineArgs F;
+      F.desc = S.fdesc;
+      F.hp_order = S.hp_order;
+      F.partials = S.partials;
+      F.hp_map = S.hp_map;
+      F.total_items = S.item_base + nb;
+      T.desc = nullptr;
+      FPPM_CUDA_OK(launch_gather_fine(s, A, F, ctx->C, ctx->sms));
+    } else {
+      FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms, chunk));
+      T.desc = S.desc;
+      if (variant == 3)
+        FPPM_CUDA_OK(launch_gather_lanes(s, A, T, ctx->C, ctx->sms));
+      else
+        FPPM_CUDA_OK(launch_gather_tiles(s, A, T, ctx->C, ctx->sms));
+    }
     FPPM_CUDA_OK(launch_tile_finalize(s, A, T, ctx->C, ctx->sms));
   }
   ctx->end_calls++;

@@ -99,7 +99,30 @@ struct SortScratch {
   uint32_t *hist;  // [digit][tile] + digit totals
 };
 
+// ---- fine-cell tiled gather (gather_fine.cu)
+constexpr int kFMaxPieces = 12;
+constexpr uint32_t kFineS = 4;  // fine cells per reference cell and axis (slab layout)
+struct FineDesc {  // 160 B, one per (home cell, wave, window of the staged union)
+  uint32_t hp_lo, hp_n, first, nchunks;
+  uint32_t lo, hi, npieces, chunk;  // window [lo, hi) of the union's flattened pieces
+  int32_t ux0, ux1, uy0, uy1, uz0, uz1;  // union of the wave's fine boxes
+  uint32_t src[kFMaxPieces];        // first sorted record of piece p
+  uint32_t pre[kFMaxPieces + 1];    // flattened offset of piece p
+  uint32_t pad[1];
+};
+static_assert(sizeof(FineDesc) == 160, "FineDesc layout");
+
+struct FineArgs {
+  const FineDesc *desc;
+  const uint32_t *hp_order;
+  double *partials;
+  const uint32_t *hp_map;
+  const uint32_t *total_items;
+};
+
 struct TileSched {
+  FineDesc *fdesc = nullptr;
+  unsigned long long fdesc_cap = 0;
   SortScratch sort;     // hit-point keys (capacity H)
   uint32_t *hp_order;   // alias of the sorted values
   uint32_t *hp_start;   // [nb + 1]
@@ -128,6 +151,18 @@ cudaError_t launch_tile_finalize(cudaStream_t s, const GatherArgs &A, const Tile
                                  int sms);
 size_t tile_partial_doubles(int G, int C);
 
+cudaError_t launch_bucket_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, uint32_t nb,
+                                uint32_t *start, int sms);
+cudaError_t launch_exclusive_scan(cudaStream_t s, const uint32_t *in, uint32_t n, uint32_t *tmp,
+                                  uint32_t *out);
+bool fine_supported(int G, int C);
+uint32_t fine_chunk(int G, int C);
+cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
+                               int sms, uint32_t chunk, uint32_t *nb_out);
+cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
+                                uint32_t chunk);
+cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms);
+
 cudaError_t launch_gather_test(cudaStream_t s, const GatherArgs &A, int C, int sms);
 cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2 *y,
                            const double *value, uint32_t n, const double *radius, uint32_t H,
@@ -142,16 +177,16 @@ size_t radix_hist_entries(uint32_t n);
 cudaError_t radix_sort_pairs(cudaStream_t s, SortScratch &sc, uint32_t n, uint32_t bits,
                              uint32_t **keys_sorted, uint32_t **vals_sorted);
 void launch_cell_bounds(cudaStream_t s, const float *pos, uint32_t n, const double *cell,
-                        long long *bounds, int sms);
+                        uint32_t S, long long *bounds, int sms);
 void launch_grid_header(cudaStream_t s, const long long *bounds, const double *cell, uint32_t n,
-                        unsigned long long max_cells, GridHeader *hdr);
+                        unsigned long long max_cells, uint32_t S, GridHeader *hdr);
 void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridHeader *hdr,
                        uint32_t *keys, uint32_t *vals, int sms);
 void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const GridHeader *hdr,
                        uint32_t *start, unsigned long long ncells, int sms);
 void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const float *pos,
                     const float *nrm, const float *wi, const float *pw, const uint32_t *depth,
-                    const PhotonRecs &r, int sms);
+                    const PhotonRecs &r, int fine_layout, int sms);
 void launch_query_ball(cudaStream_t s, const double *centers, const double *radii, uint32_t nq,
                        const GridHeader *hdr, const uint32_t *start, const float4 *rec0,
                        const uint32_t *order, unsigned long long *counts,

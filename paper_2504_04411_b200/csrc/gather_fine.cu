@@ -1,0 +1,852 @@
+// gather_fine.cu -- fine-cell tiled gather + F-test (the default kernel).
+//
+// Same work decomposition as gather_tile.cu -- item = (home reference cell,
+// wave of <= 32 hit points, window of the wave's staged candidates) -- with
+// three changes that cut the instruction count per accepted pair:
+//
+//  * fine culling.  The photon table is built on fine cells of size
+//    cell / S (S = 4 when the photons span <= 3 reference cells in z, the
+//    "slab" layout; grid.cu).  Every hit point tests only the fine cells of
+//    its own bounding box [c - r, c + r] clipped to the reference
+//    27-neighbourhood of its home cell (photon_map.cpp:65-77): the candidate
+//    area follows the hit point's own radius instead of 9 r_max^2.  The wave
+//    stages the union of its members' boxes (one contiguous piece per fine
+//    row) with TMA bulk copies; each hit point walks its own runs inside it.
+//  * specialised flush.  Hit points with n = +z, an fp32-exact center and
+//    n_s = 4 (every canonical workload) take a flush that needs no frame
+//    projection: plane coordinates are (dx, dy), guard and cos_i are p.n.z and
+//    wi.z (exact when the other components are finite, precomputed flag), and
+//    the photon luminance comes precomputed in fp64 from the record.
+//  * shared-memory accumulators.  Each lane adds its pair's value into its own
+//    (sector, lane) slot {sum, sum_sq} in shared memory (one LDS.128 + two
+//    DADD + one STS.128 per pair instead of G predicated adds); per-sector
+//    counts come from one ballot per sector per flush.  Slots are reduced in
+//    a fixed order at the end of each fragment, so results are deterministic.
+//
+// Pairs whose fp32 predicates fall inside an error band are deferred to a
+// per-warp list and decided on the exact fp64 path (exact_pair, gather_dev.cuh)
+// outside the hot loop.  Partials and k_tile_finalize are shared with the
+// tiled kernel.
+#include "common.cuh"
+#include "gather.cuh"
+#include "gather_dev.cuh"
+
+namespace fppm_b200 {
+
+constexpr int kFWarps = 8;
+constexpr int kFThreads = kFWarps * kWarp;
+constexpr int kFWave = 32;      // hit points per wave (= kWave of the partial layout)
+constexpr int kFQueue = 128;    // survivor ring per warp (<= 31 + 64 pending)
+constexpr int kFExact = 64;     // deferred exact pairs per warp (<= 31 + 32 pending)
+constexpr int kFMaxFrag = kFWave + kFWarps;
+constexpr uint32_t kFNone = 0xffffffffu;
+
+__device__ __forceinline__ float4 lds128_f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// ------------------------------------------------------------------ geometry
+struct FBox {
+  int x0, x1, y0, y1, z0, z1;
+};
+
+// fine-cell range of one axis: the box [c - m, c + m] intersected with the
+// reference 27-neighbourhood of the home cell and the table.
+static __device__ __forceinline__ bool fine_axis(const GridHeader &g, double c, double m,
+                                                 long long o, long long n, int &lo, int &hi) {
+  const double hc = dm(c, g.inv);
+  if (!(fabs(hc) < 4.0e15)) return false;
+  const long long h = (long long)floor(hc);
+  const long long H = h >> g.shift;  // reference cell (floor division by S)
+  long long a = (H - 1) * (long long)g.S, b = (H + 2) * (long long)g.S - 1;
+  const long long a2 = (long long)floor(dm(ds(c, m), g.inv));
+  const long long b2 = (long long)floor(dm(da(c, m), g.inv));
+  a = (a > a2 ? a : a2) - o;
+  b = (b < b2 ? b : b2) - o;
+  if (a < 0) a = 0;
+  if (b > n - 1) b = n - 1;
+  lo = (int)a;
+  hi = (int)b;
+  return a <= b;
+}
+
+// Fine cells that can hold an accepted photon of the ball (c, r): the margin
+// covers the rounding of the fp64 ball test (|p - c| <= r (1 + 2^-50)) and of
+// c +- m.
+static __device__ __forceinline__ bool fine_box(const GridHeader &g, double cx, double cy, double cz,
+                                                double r, FBox &b) {
+  if (g.n == 0) return false;
+  const double cm = fmax(fabs(cx), fmax(fabs(cy), fabs(cz)));
+  const double m = da(da(r, dm(r, 1e-9)), dm(cm, 4e-16));
+  return fine_axis(g, cx, m, g.ix0, g.nx, b.x0, b.x1) && fine_axis(g, cy, m, g.iy0, g.ny, b.y0, b.y1) &&
+         fine_axis(g, cz, m, g.iz0, g.nz, b.z0, b.z1);
+}
+
+static __device__ __forceinline__ unsigned long long fid(const GridHeader &g, long long x, long long y,
+                                                         long long z) {
+  return (unsigned long long)((x * g.ny + y) * g.nz + z);
+}
+
+// Key range of piece p of a union box (slab: one fine row over the union's y
+// range and every z; otherwise one (x, y) column over the union's z range).
+static __device__ __forceinline__ void piece_keys(const GridHeader &g, const FBox &u, int p,
+                                                  unsigned long long &k0, unsigned long long &k1) {
+  if (g.S > 1) {
+    const long long x = u.x0 + p;
+    k0 = fid(g, x, u.y0, 0);
+    k1 = fid(g, x, u.y1, g.nz - 1);
+  } else {
+    const int nyu = u.y1 - u.y0 + 1;
+    const long long x = u.x0 + p / nyu, y = u.y0 + p % nyu;
+    k0 = fid(g, x, y, u.z0);
+    k1 = fid(g, x, y, u.z1);
+  }
+}
+static __device__ __forceinline__ int piece_count(const GridHeader &g, const FBox &u) {
+  return g.S > 1 ? u.x1 - u.x0 + 1 : (u.x1 - u.x0 + 1) * (u.y1 - u.y0 + 1);
+}
+// Run j of hit-point box b inside union u: key range and the piece holding it.
+static __device__ __forceinline__ int run_keys(const GridHeader &g, const FBox &u, const FBox &b, int j,
+                                               unsigned long long &k0, unsigned long long &k1) {
+  if (g.S > 1) {
+    const long long x = b.x0 + j;
+    k0 = fid(g, x, b.y0, 0);
+    k1 = fid(g, x, b.y1, g.nz - 1);
+    return (int)(x - u.x0);
+  }
+  const int nyb = b.y1 - b.y0 + 1, nyu = u.y1 - u.y0 + 1;
+  const long long x = b.x0 + j / nyb, y = b.y0 + j % nyb;
+  k0 = fid(g, x, y, b.z0);
+  k1 = fid(g, x, y, b.z1);
+  return (int)((x - u.x0) * nyu + (y - u.y0));
+}
+static __device__ __forceinline__ int run_count(const GridHeader &g, const FBox &b) {
+  return g.S > 1 ? b.x1 - b.x0 + 1 : (b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1);
+}
+
+// ------------------------------------------------------------------ scheduling
+// bucket = home reference cell in the table's reference box extended by one
+// cell on every side; key n_ext = "no candidates" (outside / not gathered /
+// empty photon set).
+struct RefBox {
+  long long x0, y0, z0, ex, ey, ez;
+};
+static __device__ __forceinline__ RefBox ref_box(const GridHeader &g) {
+  RefBox b;
+  b.x0 = g.ix0 >> g.shift;
+  b.y0 = g.iy0 >> g.shift;
+  b.z0 = g.iz0 >> g.shift;
+  b.ex = ((g.ix0 + g.nx - 1) >> g.shift) - b.x0 + 3;
+  b.ey = ((g.iy0 + g.ny - 1) >> g.shift) - b.y0 + 3;
+  b.ez = ((g.iz0 + g.nz - 1) >> g.shift) - b.z0 + 3;
+  return b;
+}
+
+__global__ void k_fine_bin(const double3 *__restrict__ pos, const uint8_t *__restrict__ gathered,
+                           uint32_t H, const GridHeader *__restrict__ hdr,
+                           uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+  const GridHeader g = *hdr;
+  const RefBox rb = ref_box(g);
+  const uint32_t n_ext = (uint32_t)(rb.ex * rb.ey * rb.ez);
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
+    uint32_t key = n_ext;
+    const double3 c = pos[h];
+    if (g.n > 0 && (gathered == nullptr || gathered[h])) {
+      const double hx = dm(c.x, g.inv), hy = dm(c.y, g.inv), hz = dm(c.z, g.inv);
+      if (fabs(hx) < 4.0e15 && fabs(hy) < 4.0e15 && fabs(hz) < 4.0e15) {
+        const long long X = ((long long)floor(hx) >> g.shift) - rb.x0 + 1;
+        const long long Y = ((long long)floor(hy) >> g.shift) - rb.y0 + 1;
+        const long long Z = ((long long)floor(hz) >> g.shift) - rb.z0 + 1;
+        if (X >= 0 && Y >= 0 && Z >= 0 && X < rb.ex && Y < rb.ey && Z < rb.ez)
+          key = (uint32_t)((X * rb.ey + Y) * rb.ez + Z);
+      }
+    }
+    keys[h] = key;
+    vals[h] = h;
+  }
+}
+
+// Union box of one wave (false when no member has candidates).
+static __device__ bool wave_union(const GatherArgs &A, const GridHeader &g, const uint32_t *hp_order,
+                                  uint32_t b0, uint32_t n, FBox &u) {
+  bool any = false;
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t h = hp_order[b0 + j];
+    const double3 c = A.pos[h];
+    FBox b;
+    if (!fine_box(g, c.x, c.y, c.z, A.radius[h], b)) continue;
+    if (!any) {
+      u = b;
+      any = true;
+    } else {
+      u.x0 = min(u.x0, b.x0); u.x1 = max(u.x1, b.x1);
+      u.y0 = min(u.y0, b.y0); u.y1 = max(u.y1, b.y1);
+      u.z0 = min(u.z0, b.z0); u.z1 = max(u.z1, b.z1);
+    }
+  }
+  return any;
+}
+
+// items per bucket: sum over its waves of ceil(staged union / chunk)
+__global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
+                             const uint32_t *__restrict__ hp_order, uint32_t *__restrict__ items,
+                             uint32_t chunk, uint32_t *__restrict__ nonempty) {
+  const GridHeader g = *A.grid;
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+    const uint32_t h0 = b < nb ? hp_start[b] : 0u;
+    const uint32_t nhp = b < nb ? hp_start[b + 1] - h0 : 0u;
+    uint32_t it = 0;
+    if (nhp) atomicAdd(nonempty, 1u);
+    for (uint32_t w = 0; w * kFWave < nhp; ++w) {
+      const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
+      FBox u;
+      uint32_t T = 0;
+      if (b + 1 < nb && wave_union(A, g, hp_order, h0 + w * kFWave, n, u)) {
+        const int np = piece_count(g, u);
+        for (int p = 0; p < np; ++p) {
+          unsigned long long k0, k1;
+          piece_keys(g, u, p, k0, k1);
+          T += A.cell_start[k1 + 1] - A.cell_start[k0];
+        }
+      }
+      it += T == 0 ? 1u : (T + chunk - 1) / chunk;
+    }
+    items[b] = it;
+  }
+}
+
+__global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
+                            const uint32_t *__restrict__ hp_order, const uint32_t *__restrict__ item_base,
+                            FineDesc *__restrict__ desc, uint32_t *__restrict__ hp_map, uint32_t chunk) {
+  const GridHeader g = *A.grid;
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    const uint32_t h0 = hp_start[b], nhp = hp_start[b + 1] - h0;
+    uint32_t item = item_base[b];
+    for (uint32_t w = 0; w * kFWave < nhp; ++w) {
+      const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
+      FineDesc d;
+      d.hp_lo = h0 + w * kFWave;
+      d.hp_n = n;
+      FBox u = {0, -1, 0, -1, 0, -1};
+      uint32_t T = 0;
+      int np = 0;
+      if (b + 1 < nb && wave_union(A, g, hp_order, d.hp_lo, n, u)) {
+        np = piece_count(g, u);
+        for (int p = 0; p < np; ++p) {
+          unsigned long long k0, k1;
+          piece_keys(g, u, p, k0, k1);
+          d.src[p] = A.cell_start[k0];
+          d.pre[p] = T;
+          T += A.cell_start[k1 + 1] - d.src[p];
+        }
+      }
+      for (int p = np; p < kFMaxPieces; ++p) {
+        d.src[p] = 0;
+        d.pre[p] = T;
+      }
+      d.pre[kFMaxPieces] = T;
+      d.npieces = (uint32_t)np;
+      d.ux0 = u.x0; d.ux1 = u.x1; d.uy0 = u.y0; d.uy1 = u.y1; d.uz0 = u.z0; d.uz1 = u.z1;
+      const uint32_t nch = T == 0 ? 1u : (T + chunk - 1) / chunk;
+      d.first = item;
+      d.nchunks = nch;
+      for (uint32_t j = 0; j < n; ++j) {
+        const uint32_t h = hp_order[d.hp_lo + j];
+        hp_map[3 * (size_t)h] = item;
+        hp_map[3 * (size_t)h + 1] = nch;
+        hp_map[3 * (size_t)h + 2] = j;
+      }
+      for (uint32_t ch = 0; ch < nch; ++ch, ++item) {
+        d.chunk = ch;
+        d.lo = ch * chunk;
+        d.hi = min(T, d.lo + chunk);
+        if (d.hi < d.lo) d.hi = d.lo;
+        desc[item] = d;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+template <int GMAX, int CH>
+struct FineLayout {
+  static constexpr int NC = GMAX * CH;                  // accumulator columns
+  static constexpr int NQ = 32 / NC;                    // lane groups in the slot reduction
+  static constexpr int PS = partial_size(GMAX, CH);
+  static constexpr size_t kSlotBytes = (size_t)kFWarps * NC * 32 * 16;
+  static constexpr size_t kFragBytes = (size_t)kFMaxFrag * PS * sizeof(double);
+  static constexpr int kMinBlocks = NC <= 8 ? 2 : 1;
+  // dynamic shared memory: records (64 B per candidate) + slots + fragments
+  // (2 CTAs per SM: 228 KB - 2 x (1 KB reserved + ~18 KB static) per CTA)
+  static constexpr size_t kBudget = NC <= 8 ? (size_t)94 * 1024 : (size_t)200 * 1024;
+  static constexpr uint32_t kChunk =
+      (uint32_t)(((kBudget - kSlotBytes - kFragBytes) / 64) & ~(size_t)31);
+  static constexpr size_t kDynBytes = (size_t)kChunk * 64 + kSlotBytes + kFragBytes;
+};
+
+struct FineState {
+  uint32_t qh, qt, eh, et;  // survivor ring and exact ring (warp-uniform)
+  uint32_t n_cand, n_exact, n_amb, n_acc;
+};
+
+// Per-hit-point weights held in registers for the fragment.
+struct HitV {
+  double K0, K1, K2;
+  bool gray;
+};
+
+// Per-sector pair counts of one lane, packed as bytes (a lane adds at most
+// one pair per flush or exact batch: <= 2 * chunk / 32 < 256 per fragment).
+template <int GMAX>
+struct PackedCounts {
+  static constexpr int NP = (GMAX + 3) / 4;
+  uint32_t w[NP];
+};
+#define FPPM_PK_CASE(r)                                                          \
+  if constexpr ((r) < PackedCounts<GMAX>::NP) {                                  \
+    if ((sector >> 2) == (r)) asm("add.u32 %0, %0, %1; // pk " #r : "+r"(c.w[r]) : "r"(inc)); \
+  }
+template <int GMAX>
+static __device__ __forceinline__ void pk_add(PackedCounts<GMAX> &c, int sector) {
+  const uint32_t inc = 1u << ((sector & 3) * 8);
+  FPPM_PK_CASE(0) FPPM_PK_CASE(1) FPPM_PK_CASE(2) FPPM_PK_CASE(3)
+}
+#undef FPPM_PK_CASE
+
+static __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+static __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+static __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+static __device__ __forceinline__ void sts_f64x2(uint32_t addr, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Value of an accepted pair (integrator.cpp:445-451, gather.cpp:59-67) added
+// to the lane's (sector, lane) slot; flux sums; packed sector counts.
+// slots = shared address of this warp's [C][GMAX][32] {sum, sum_sq} slots.
+template <int GMAX, int CH>
+static __device__ __forceinline__ void fine_accumulate(const HitV &K, bool acc, bool cos_pos, int sector,
+                                                       float4 pw, double L, uint32_t slots, int lane,
+                                                       PackedCounts<GMAX> &cnt, double &p0, double &p1,
+                                                       double &p2) {
+  if (!acc) return;
+  const double pr = cos_pos ? (double)pw.x : 0.0, pg = cos_pos ? (double)pw.y : 0.0,
+               pb = cos_pos ? (double)pw.z : 0.0;
+  p0 += pr;
+  p1 += pg;
+  p2 += pb;
+  pk_add<GMAX>(cnt, sector);
+  if constexpr (CH == 1) {
+    const double v = K.gray ? (cos_pos ? dm(K.K0, L) : 0.0)
+                            : elum(dm(K.K0, pr), dm(K.K1, pg), dm(K.K2, pb));
+    const uint32_t a = slots + (uint32_t)(sector * 32 + lane) * 16u;
+    double2 o = lds_f64x2(a);
+    o.x += v;
+    o.y += v * v;
+    sts_f64x2(a, o);
+  } else {
+    const double v[3] = {dm(K.K0, pr), dm(K.K1, pg), dm(K.K2, pb)};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const uint32_t a = slots + (uint32_t)((c * GMAX + sector) * 32 + lane) * 16u;
+      double2 o = lds_f64x2(a);
+      o.x += v[c];
+      o.y += v[c] * v[c];
+      sts_f64x2(a, o);
+    }
+  }
+}
+
+// One fp64-exact evaluation of a deferred pair (fine record layout -> the
+// tile layout expected by exact_pair).
+static __device__ __forceinline__ uint32_t fine_exact(const Hit &Hs, uint32_t r0, uint32_t r1, uint32_t r2,
+                                                      uint32_t r3, uint32_t i, int na, int ns,
+                                                      double guard, float4 &pw, double &L) {
+  const float4 a = lds128_f(r0 + i * 16u), B = lds128_f(r1 + i * 16u), Cc = lds128_f(r2 + i * 16u),
+               D = lds128_f(r3 + i * 16u);
+  pw = Cc;
+  L = __longlong_as_double(((long long)__float_as_uint(B.w) << 32) | __float_as_uint(B.z));
+  const float4 b_old = make_float4(D.x, D.y, B.x, D.z);
+  const float4 c2_old = make_float4(D.w, B.y, Cc.x, Cc.y);
+  return exact_pair_packed(Hs, a, b_old, c2_old, na, ns, guard);
+}
+
+// Decide up to 32 queued survivors (lane < n holds one), defer banded pairs to
+// the exact ring, accumulate the rest.
+template <int GMAX, int CH, bool PLANAR>
+static __device__ __forceinline__ void fine_flush(const GatherArgs &A, const HitV &K, const HitF &F,
+                                                  bool lo_zero, uint32_t n, uint32_t q, uint32_t ex,
+                                                  uint32_t slots, PackedCounts<GMAX> &cnt, double &p0,
+                                                  double &p1, double &p2, uint32_t r0, uint32_t r1,
+                                                  uint32_t r2, uint32_t r3, FineState &st) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  __syncwarp();
+  const bool have = (uint32_t)lane < n;
+  const uint32_t i = have ? lds_u32(q + ((st.qh + lane) & (kFQueue - 1)) * 4u) : 0u;
+  st.qh += n;
+  bool acc = false, cos_pos = false, need = false;
+  int sector = 0;
+  float4 pw = make_float4(0.f, 0.f, 0.f, 0.f);
+  double L = 0.0;
+  if (have) {
+    const float4 p = lds128_f(r0 + i * 16u);
+    const float4 B = lds128_f(r1 + i * 16u);
+    pw = lds128_f(r2 + i * 16u);
+    L = __longlong_as_double(((long long)__float_as_uint(B.w) << 32) | __float_as_uint(B.z));
+    if constexpr (PLANAR) {
+      // n = +z: y = (dx, dy) exactly; guard = p.n.z, cos_i = wi.z (finite flag)
+      const float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
+      const float yy = fmaf(dx, dx, dy * dy);
+      const float d2 = fmaf(dz, dz, yy);
+      need = !(d2 < F.lim_lo) || !(fabsf(dx) > F.band_y) || !(fabsf(dy) > F.band_y) ||
+             (__float_as_uint(pw.w) & 1u) == 0u;
+      const int quad = dx > 0.0f ? (dy > 0.0f ? 0 : 3) : (dy > 0.0f ? 1 : 2);
+      int ring = 0;
+      if (F.na > 1) {
+        const float qa = yy * F.qa_scale;
+        const float kq = rintf(qa);
+        need = need || (kq >= 1.0f && kq <= (float)(F.na - 1) && fabsf(qa - kq) < 1e-4f * (float)F.na);
+        ring = min((int)qa, F.na - 1);
+      }
+      sector = ring * 4 + quad;
+      cos_pos = !(B.y <= 0.0f);              // bsdf.cpp:56-58
+      acc = !need && !(B.x < F.guard_ceil);  // integrator.cpp:397
+    } else {
+      const float4 D = lds128_f(r3 + i * 16u);
+      float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
+      if (!lo_zero) {
+        dx -= F.clx;
+        dy -= F.cly;
+        dz -= F.clz;
+      }
+      const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      const float yu = fmaf(dx, F.ufx, fmaf(dy, F.ufy, dz * F.ufz));
+      const float yv = fmaf(dx, F.vfx, fmaf(dy, F.vfy, dz * F.vfz));
+      const float yy = fmaf(yu, yu, yv * yv);
+      const bool keep = yy <= F.lim_hi;  // disk (integrator.cpp:399): certain reject above
+      need = !(F.fast && d2 < F.lim_lo && yy < F.lim_lo);
+      need = !fast_sector(F, yu, yv, yy, sector) || need;
+      const float gd = fmaf(D.x, F.nfx, fmaf(D.y, F.nfy, B.x * F.nfz));
+      const float gb = 2e-6f * (fabsf(D.x * F.nfx) + fabsf(D.y * F.nfy) + fabsf(B.x * F.nfz)) + 1e-30f;
+      const bool guard_ok = !(gd < F.guard_f - gb);
+      need = need || (guard_ok && !(gd >= F.guard_f + gb));
+      const float ci = fmaf(D.z, F.nfx, fmaf(D.w, F.nfy, B.y * F.nfz));
+      const float cb = 2e-6f * (fabsf(D.z * F.nfx) + fabsf(D.w * F.nfy) + fabsf(B.y * F.nfz)) + 1e-30f;
+      need = (need || !(fabsf(ci) > cb)) && keep;
+      cos_pos = ci > 0.0f;
+      acc = !need && keep && guard_ok;
+    }
+  }
+  const uint32_t me = __ballot_sync(kFull, need);
+  if (me) {  // rare: banded pairs go to the exact ring
+    if (need) sts_u32(ex + ((st.et + __popc(me & lt)) & (kFExact - 1)) * 4u, i);
+    st.et += __popc(me);
+  }
+  st.n_acc += acc ? 1u : 0u;
+  fine_accumulate<GMAX, CH>(K, acc, cos_pos, sector, pw, L, slots, lane, cnt, p0, p1, p2);
+}
+
+// Exact (fp64) decision of up to 32 deferred pairs.
+template <int GMAX, int CH>
+static __device__ __forceinline__ void fine_exact_batch(const GatherArgs &A, const Hit &Hs, const HitV &K,
+                                                     uint32_t n, uint32_t ex, uint32_t slots,
+                                                     PackedCounts<GMAX> &cnt, double &p0, double &p1,
+                                                     double &p2, uint32_t r0, uint32_t r1, uint32_t r2,
+                                                     uint32_t r3, FineState &st) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const bool have = (uint32_t)lane < n;
+  const uint32_t i = have ? lds_u32(ex + ((st.eh + lane) & (kFExact - 1)) * 4u) : 0u;
+  st.eh += n;
+  float4 pw = make_float4(0.f, 0.f, 0.f, 0.f);
+  double L = 0.0;
+  uint32_t fl = 0;
+  if (have) {
+    fl = fine_exact(Hs, r0, r1, r2, r3, i, A.na, A.ns, A.guard, pw, L);
+    st.n_exact += 1;
+    st.n_amb += (fl >> 2) & 1u;
+    st.n_acc += fl & 1u;
+  }
+  fine_accumulate<GMAX, CH>(K, (fl & 1u) != 0, (fl & 2u) != 0, (int)(fl >> 8), pw, L, slots, lane, cnt, p0,
+                            p1, p2);
+  __syncwarp();
+}
+
+template <int GMAX, int CH, bool PLANAR>
+static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const Hit &Hs, uint32_t ib,
+                                                     uint32_t ie, const uint2 *runs, int nruns,
+                                                     uint32_t q, uint32_t ex, uint32_t slots,
+                                                     PackedCounts<GMAX> &cnt, double &p0, double &p1,
+                                                     double &p2, uint32_t r0, uint32_t r1, uint32_t r2,
+                                                     uint32_t r3, FineState &st) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const HitF F = hitf(Hs, A.na, A.ns);
+  HitV K;
+  K.K0 = Hs.K0;
+  K.K1 = Hs.K1;
+  K.K2 = Hs.K2;
+  K.gray = Hs.gray;
+  const uint32_t max_depth = A.max_depth;
+  const bool lo_zero = PLANAR || (F.clx == 0.0f && F.cly == 0.0f && F.clz == 0.0f);
+  uint32_t vp = 0;
+  for (int j = 0; j < nruns && vp < ie; ++j) {
+    const uint2 R = runs[j];
+    const uint32_t a = max(vp, ib), b = min(vp + R.y, ie);
+    const uint32_t rb = vp;
+    vp += R.y;
+    if (b <= a) continue;
+    const uint32_t s1 = R.x + (b - rb);
+    for (uint32_t base = R.x + (a - rb); base < s1; base += 64) {
+      // ---- test: ball + depth (photon_map.cpp:76, integrator.cpp:396)
+      const uint32_t i0 = base + lane, i1 = i0 + 32;
+      const bool v0 = i0 < s1, v1 = i1 < s1;
+      const float4 a0 = lds128_f(r0 + (v0 ? i0 : base) * 16u);
+      const float4 a1 = lds128_f(r0 + (v1 ? i1 : base) * 16u);
+      const bool t0 = v0 && ball_pass(F, lo_zero, a0, max_depth);
+      const bool t1 = v1 && ball_pass(F, lo_zero, a1, max_depth);
+      st.n_cand += (v0 ? 1u : 0u) + (v1 ? 1u : 0u);
+      const uint32_t m0 = __ballot_sync(kFull, t0);
+      if (t0) sts_u32(q + ((st.qt + __popc(m0 & lt)) & (kFQueue - 1)) * 4u, i0);
+      st.qt += __popc(m0);
+      const uint32_t m1 = __ballot_sync(kFull, t1);
+      if (t1) sts_u32(q + ((st.qt + __popc(m1 & lt)) & (kFQueue - 1)) * 4u, i1);
+      st.qt += __popc(m1);
+      // ---- flush 32 survivors with every lane busy
+      while (st.qt - st.qh >= 32) {
+        fine_flush<GMAX, CH, PLANAR>(A, K, F, lo_zero, 32u, q, ex, slots, cnt, p0, p1, p2, r0, r1, r2,
+                                     r3, st);
+        if (st.et - st.eh >= 32)
+          fine_exact_batch<GMAX, CH>(A, Hs, K, 32u, ex, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
+      }
+    }
+  }
+  // ---- drain the survivors (< 32) and the exact ring
+  if (st.qt != st.qh)
+    fine_flush<GMAX, CH, PLANAR>(A, K, F, lo_zero, st.qt - st.qh, q, ex, slots, cnt, p0, p1, p2, r0, r1,
+                                 r2, r3, st);
+  while (st.et != st.eh)
+    fine_exact_batch<GMAX, CH>(A, Hs, K, min(32u, st.et - st.eh), ex, slots, cnt, p0, p1, p2, r0, r1, r2,
+                               r3, st);
+  __syncwarp();
+}
+
+template <int GMAX, int CH>
+__global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
+    k_gather_fine(const GatherArgs A, const FineArgs T) {
+  using Lay = FineLayout<GMAX, CH>;
+  constexpr int NC = Lay::NC, NQ = Lay::NQ, PS = Lay::PS;
+  constexpr uint32_t CHUNK = Lay::kChunk;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double *s_slots = reinterpret_cast<double *>(smem_raw + (size_t)CHUNK * 64);
+  double *s_frag = reinterpret_cast<double *>(smem_raw + (size_t)CHUNK * 64 + Lay::kSlotBytes);
+  __shared__ Hit s_hit[kFWave];
+  __shared__ uint2 s_run[kFWave][kFMaxPieces];
+  __shared__ uint32_t s_nrun[kFWave], s_tot[kFWave];
+  __shared__ uint32_t s_q[kFWarps][kFQueue];
+  __shared__ uint32_t s_ex[kFWarps][kFExact];
+  __shared__ uint32_t s_frag_hp[kFMaxFrag];
+  __shared__ FineDesc s_desc;
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ uint32_t s_item;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t r0 = smem_u32(smem_raw);
+  const uint32_t r1 = r0 + CHUNK * 16u, r2 = r1 + CHUNK * 16u, r3 = r2 + CHUNK * 16u;
+  double *slots_p = s_slots + (size_t)warp * NC * 32 * 2;
+  for (int i = lane; i < NC * 32 * 2; i += 32) slots_p[i] = 0.0;
+  const uint32_t slots = smem_u32(slots_p);
+  const uint32_t qa = smem_u32(&s_q[warp][0]), exa = smem_u32(&s_ex[warp][0]);
+  const uint32_t total_items = *T.total_items;
+  const GridHeader g = *A.grid;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  FineState st = {0, 0, 0, 0, 0, 0, 0, 0};
+
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(A.work, 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    if (item >= total_items) break;
+    if (threadIdx.x < sizeof(FineDesc) / 4)
+      reinterpret_cast<uint32_t *>(&s_desc)[threadIdx.x] =
+          reinterpret_cast<const uint32_t *>(T.desc + item)[threadIdx.x];
+    if (threadIdx.x < kFMaxFrag) s_frag_hp[threadIdx.x] = kFNone;
+    __syncthreads();
+    const uint32_t lo = s_desc.lo, hi = s_desc.hi, hp_n = s_desc.hp_n;
+    const uint32_t ncand = hi - lo;
+    if (threadIdx.x == 0 && ncand) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&s_bar, ncand * 64u);
+      for (uint32_t p = 0; p < s_desc.npieces; ++p) {
+        const uint32_t a = max(s_desc.pre[p], lo), e = min(s_desc.pre[p + 1], hi);
+        if (e <= a) continue;
+        const uint32_t src = s_desc.src[p] + (a - s_desc.pre[p]), dst = a - lo, n = e - a;
+        bulk_g2s(smem_raw + (size_t)dst * 16, A.rec0 + src, n * 16u, &s_bar);
+        bulk_g2s(smem_raw + (size_t)(CHUNK + dst) * 16, A.rec1 + src, n * 16u, &s_bar);
+        bulk_g2s(smem_raw + (size_t)(2 * CHUNK + dst) * 16, A.rec2 + src, n * 16u, &s_bar);
+        bulk_g2s(smem_raw + (size_t)(3 * CHUNK + dst) * 16, A.rec3 + src, n * 16u, &s_bar);
+      }
+    }
+    if (threadIdx.x < hp_n) make_hit(A, T.hp_order[s_desc.hp_lo + threadIdx.x], s_hit[threadIdx.x]);
+    __syncthreads();
+
+    // ---- per hit point: its runs inside this window (lane = run)
+    FBox u;
+    u.x0 = s_desc.ux0; u.x1 = s_desc.ux1; u.y0 = s_desc.uy0; u.y1 = s_desc.uy1;
+    u.z0 = s_desc.uz0; u.z1 = s_desc.uz1;
+    for (uint32_t k = warp; k < hp_n; k += kFWarps) {
+      const Hit &H = s_hit[k];
+      FBox b;
+      const bool ok = ncand && fine_box(g, H.cx, H.cy, H.cz, H.r, b);
+      const int nr = ok ? run_count(g, b) : 0;
+      uint32_t rs = 0, rl = 0;
+      if (lane < nr) {
+        unsigned long long k0, k1;
+        const int p = run_keys(g, u, b, lane, k0, k1);
+        const uint32_t ga = A.cell_start[k0], gb = A.cell_start[k1 + 1];
+        const uint32_t fa = s_desc.pre[p] + (ga - s_desc.src[p]), fb = fa + (gb - ga);
+        const uint32_t ca = max(fa, lo), cb = min(fb, hi);
+        if (cb > ca) {
+          rs = ca - lo;
+          rl = cb - ca;
+        }
+      }
+      if (lane < kFMaxPieces) s_run[k][lane] = make_uint2(rs, rl);
+      const uint32_t tot = warp_sum(rl);
+      if (lane == 0) {
+        s_tot[k] = tot;
+        s_nrun[k] = (uint32_t)nr;
+      }
+    }
+    __syncthreads();
+
+    // ---- balanced split of the (hit point x candidate) space over the warps
+    const uint32_t tk = (uint32_t)lane < hp_n ? s_tot[lane] : 0u;
+    uint32_t incl = tk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - tk;
+    const uint32_t W = __shfl_sync(kFull, incl, 31);
+    const uint32_t f0 = (uint32_t)(((unsigned long long)W * warp) / kFWarps);
+    const uint32_t f1 = (uint32_t)(((unsigned long long)W * (warp + 1)) / kFWarps);
+    if (ncand) {
+      mbar_wait(&s_bar, phase);
+      phase ^= 1u;
+    }
+    for (uint32_t f = f0; f < f1;) {
+      const uint32_t m = __ballot_sync(kFull, (uint32_t)lane < hp_n && incl > f);
+      const int k = __ffs(m) - 1;
+      const uint32_t Pk = __shfl_sync(kFull, excl, k), Tk = __shfl_sync(kFull, tk, k);
+      const uint32_t ib = f - Pk, ie = min(Tk, f1 - Pk);
+      f = Pk + ie;
+      const Hit &Hs = s_hit[k];
+      PackedCounts<GMAX> cnt;
+#pragma unroll
+      for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+      const bool planar = Hs.fast && Hs.nx == 0.0 && Hs.ny == 0.0 && Hs.nz == 1.0 && A.ns == 4 &&
+                          Hs.clx == 0.0f && Hs.cly == 0.0f && Hs.clz == 0.0f;
+      if (planar)
+        fine_fragment<GMAX, CH, true>(A, Hs, ib, ie, s_run[k], (int)s_nrun[k], qa, exa, slots, cnt, p0, p1,
+                                      p2, r0, r1, r2, r3, st);
+      else
+        fine_fragment<GMAX, CH, false>(A, Hs, ib, ie, s_run[k], (int)s_nrun[k], qa, exa, slots, cnt, p0,
+                                       p1, p2, r0, r1, r2, r3, st);
+
+      // ---- fragment partial: fixed-order reduction of the lane slots
+      const int col = lane % NC, grp = lane / NC;
+      double sm = 0.0, sq = 0.0;
+      if (grp < NQ) {
+        // rows rotated by the column: the 16-B slots a warp touches per step
+        // fall in distinct bank groups (fixed order, so still deterministic)
+        constexpr int R = 32 / NQ;
+        const uint32_t base = slots + (uint32_t)(col * 32 + grp * R) * 16u;
+#pragma unroll 4
+        for (int i = 0; i < R; ++i) {
+          const uint32_t a = base + (uint32_t)((i + col) % R) * 16u;
+          const double2 v = lds_f64x2(a);
+          sm += v.x;
+          sq += v.y;
+          sts_f64x2(a, make_double2(0.0, 0.0));
+        }
+      }
+#pragma unroll
+      for (int o = (NQ / 2) * NC; o >= NC && o > 0; o >>= 1) {
+        sm += __shfl_down_sync(kFull, sm, o);
+        sq += __shfl_down_sync(kFull, sq, o);
+      }
+      p0 = warp_sum(p0);
+      p1 = warp_sum(p1);
+      p2 = warp_sum(p2);
+      // packed byte counts -> 16-bit halves -> warp sums (<= 32 * 255 per half)
+      uint32_t csum[2 * PackedCounts<GMAX>::NP];
+#pragma unroll
+      for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) {
+        csum[2 * r] = __reduce_add_sync(kFull, cnt.w[r] & 0x00ff00ffu);
+        csum[2 * r + 1] = __reduce_add_sync(kFull, (cnt.w[r] >> 8) & 0x00ff00ffu);
+      }
+      const uint32_t slot = k + warp;
+      double *pp = s_frag + (size_t)slot * PS;
+      if (lane < NC) {
+        const int c = lane / GMAX, gg = lane % GMAX;
+        pp[GMAX + c * GMAX + gg] = sm;
+        pp[GMAX + CH * GMAX + c * GMAX + gg] = sq;
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int gg = 0; gg < GMAX; ++gg) {
+          const uint32_t wd = csum[2 * (gg >> 2) + (gg & 1)];
+          pp[gg] = (double)((gg & 2) ? (wd >> 16) : (wd & 0xffffu));
+        }
+        pp[GMAX + 2 * CH * GMAX] = p0;
+        pp[GMAX + 2 * CH * GMAX + 1] = p1;
+        pp[GMAX + 2 * CH * GMAX + 2] = p2;
+        s_frag_hp[slot] = (uint32_t)k;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+
+    // ---- combine fragments per hit point (warp order) into the item partial
+    if (threadIdx.x < hp_n) {
+      const uint32_t k = threadIdx.x;
+      double *out = T.partials + ((size_t)item * kFWave + k) * PS;
+      for (int j = 0; j < PS; ++j) {
+        double x = 0.0;
+        for (int w = 0; w < kFWarps; ++w)
+          if (s_frag_hp[k + w] == k) x += s_frag[(size_t)(k + w) * PS + j];
+        out[j] = x;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ------------------------------------------------------ block totals
+  __shared__ unsigned long long s_c[4];
+  if (threadIdx.x == 0) s_c[0] = s_c[1] = s_c[2] = s_c[3] = 0;
+  __syncthreads();
+  atomicAdd(&s_c[0], (unsigned long long)st.n_acc);
+  atomicAdd(&s_c[1], (unsigned long long)st.n_cand);
+  atomicAdd(&s_c[2], (unsigned long long)st.n_exact);
+  atomicAdd(&s_c[3], (unsigned long long)st.n_amb);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(&A.counters[0], s_c[0]);
+    atomicAdd(&A.counters[1], s_c[1]);
+    atomicAdd(&A.counters[2], s_c[2]);
+    atomicAdd(&A.counters[3], s_c[3]);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static inline unsigned fblocks(unsigned long long n, int threads, int sms, int per_sm) {
+  unsigned long long b = (n + threads - 1) / threads;
+  const unsigned long long cap = (unsigned long long)sms * per_sm;
+  if (b > cap) b = cap;
+  return (unsigned)(b ? b : 1);
+}
+
+bool fine_supported(int G, int C) {
+  const int gmax = G <= 4 ? 4 : G <= 8 ? 8 : G <= 12 ? 12 : G <= 16 ? 16 : 32;
+  return gmax * C <= 24;
+}
+
+uint32_t fine_chunk(int G, int C) {
+  if (C == 1) {
+    if (G <= 4) return FineLayout<4, 1>::kChunk;
+    if (G <= 8) return FineLayout<8, 1>::kChunk;
+    if (G <= 12) return FineLayout<12, 1>::kChunk;
+    return FineLayout<16, 1>::kChunk;
+  }
+  if (G <= 4) return FineLayout<4, 3>::kChunk;
+  return FineLayout<8, 3>::kChunk;
+}
+
+cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
+                               int sms, uint32_t chunk, uint32_t *nb_out) {
+  const long long x0 = g.ix0 >> g.shift, y0 = g.iy0 >> g.shift, z0 = g.iz0 >> g.shift;
+  const unsigned long long ex = (unsigned long long)(((g.ix0 + g.nx - 1) >> g.shift) - x0 + 3);
+  const unsigned long long ey = (unsigned long long)(((g.iy0 + g.ny - 1) >> g.shift) - y0 + 3);
+  const unsigned long long ez = (unsigned long long)(((g.iz0 + g.nz - 1) >> g.shift) - z0 + 3);
+  const unsigned long long n_ext = ex * ey * ez;
+  if (n_ext + 1 >= 0xffffffffull) return cudaErrorInvalidValue;
+  const uint32_t nb = (uint32_t)n_ext + 1;
+  *nb_out = nb;
+  k_fine_bin<<<fblocks(A.H, 256, sms, 16), 256, 0, s>>>(A.pos, A.gathered, A.H, A.grid,
+                                                        S.sort.keys_a, S.sort.vals_a);
+  note_launches(1);
+  uint32_t bits = 1;
+  while (bits < 32 && (1ull << bits) < (unsigned long long)nb) ++bits;
+  uint32_t *skeys, *svals;
+  cudaError_t e = radix_sort_pairs(s, S.sort, A.H, bits, &skeys, &svals);
+  if (e != cudaSuccess) return e;
+  S.hp_order = svals;
+  e = launch_bucket_start(s, skeys, A.H, nb, S.hp_start, sms);
+  if (e != cudaSuccess) return e;
+  k_fine_items<<<fblocks(nb + 1, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order, S.items,
+                                                             chunk, S.nonempty);
+  note_launches(1);
+  return launch_exclusive_scan(s, S.items, nb + 1, S.scan_tmp, S.item_base);
+}
+
+cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
+                                uint32_t chunk) {
+  k_fine_desc<<<fblocks(nb, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order, S.item_base,
+                                                        S.fdesc, S.hp_map, chunk);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+template <int GMAX, int CH>
+static cudaError_t launch_fine_t(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int sms) {
+  using Lay = FineLayout<GMAX, CH>;
+  const size_t smem = Lay::kDynBytes;
+  cudaError_t e = cudaFuncSetAttribute(k_gather_fine<GMAX, CH>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_fine<GMAX, CH>, kFThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  k_gather_fine<GMAX, CH><<<sms * per_sm, kFThreads, smem, s>>>(A, T);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms) {
+  const int G = A.na * A.ns;
+  if (C == 1) {
+    if (G <= 4) return launch_fine_t<4, 1>(s, A, T, sms);
+    if (G <= 8) return launch_fine_t<8, 1>(s, A, T, sms);
+    if (G <= 12) return launch_fine_t<12, 1>(s, A, T, sms);
+    if (G <= 16) return launch_fine_t<16, 1>(s, A, T, sms);
+    return cudaErrorInvalidValue;
+  }
+  if (G <= 4) return launch_fine_t<4, 3>(s, A, T, sms);
+  if (G <= 8) return launch_fine_t<8, 3>(s, A, T, sms);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fppm_b200

@@ -637,6 +637,26 @@ cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   return cudaGetLastError();
 }
 
+cudaError_t launch_bucket_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, uint32_t nb,
+                                uint32_t *start, int sms) {
+  if ((unsigned long long)nb > 4ull * n)
+    k_bucket_start_bsearch<<<blocks_for(nb + 1, 256, sms, 16), 256, 0, s>>>(skeys, n, nb, start);
+  else
+    k_bucket_start<<<blocks_for(n, 256, sms, 16), 256, 0, s>>>(skeys, n, nb, start);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exclusive_scan(cudaStream_t s, const uint32_t *in, uint32_t n, uint32_t *tmp,
+                                  uint32_t *out) {
+  const uint32_t nt = (n + kScanTile - 1) / kScanTile;
+  k_scan_tiles<<<nt, 256, 0, s>>>(in, n, tmp);
+  k_scan_top<<<1, 256, 0, s>>>(tmp, nt);
+  k_scan_apply<<<nt, 256, 0, s>>>(in, n, tmp, out);
+  note_launches(3);
+  return cudaGetLastError();
+}
+
 cudaError_t tile_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb,
                                 int sms, uint32_t chunk) {
   k_item_desc<<<blocks_for(nb, 128, sms, 16), 128, 0, s>>>(S.hp_start, nb, A.grid, A.cell_start,

@@ -31,8 +31,8 @@ __device__ __forceinline__ T warp_reduce(T v, Op op) {
 // ------------------------------------------------------------------ bounds
 __global__ void __launch_bounds__(256)
     k_cell_bounds(const float *__restrict__ pos, uint32_t n, const double *__restrict__ cell_ptr,
-                  long long *__restrict__ bounds /* [6]: min xyz, max xyz */) {
-  const double inv = dd(1.0, *cell_ptr);
+                  uint32_t S, long long *__restrict__ bounds /* [6]: min xyz, max xyz */) {
+  const double inv = dm(dd(1.0, *cell_ptr), (double)S);  // photon_map.cpp:29, x S exactly
   long long mn[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
   long long mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -67,14 +67,33 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// bounds are in cells of size cell / S_req.  The fine (slab) layout is kept
+// when the z extent is at most 3 reference cells and the dense table fits;
+// otherwise the bounds are folded back to reference cells (>> shift, exact).
 __global__ void k_grid_header(const long long *__restrict__ bounds, const double *__restrict__ cell_ptr,
-                              uint32_t n, unsigned long long max_cells,
+                              uint32_t n, unsigned long long max_cells, uint32_t S_req,
                               GridHeader *__restrict__ hdr) {
   GridHeader g;
   g.cell = *cell_ptr;
-  g.inv = dd(1.0, g.cell);
   g.n = n;
   g.pad = 0;
+  uint32_t shift = 0;
+  while ((1u << shift) < S_req) ++shift;
+  long long b[6];
+  for (int i = 0; i < 6; ++i) b[i] = bounds[i];
+  if (n > 0 && S_req > 1) {
+    const double fx = (double)(b[3] - b[0] + 1), fy = (double)(b[4] - b[1] + 1),
+                 fz = (double)(b[5] - b[2] + 1);
+    if (!(fz <= 3.0 * S_req && fx * fy * fz <= (double)max_cells)) {
+      for (int i = 0; i < 6; ++i) b[i] >>= shift;  // floor division by S
+      shift = 0;
+    }
+  } else {
+    shift = 0;
+  }
+  g.S = 1u << shift;
+  g.shift = shift;
+  g.inv = dm(dd(1.0, g.cell), (double)g.S);
   if (n == 0) {
     g.ix0 = g.iy0 = g.iz0 = 0;
     g.nx = g.ny = g.nz = 1;
@@ -82,12 +101,12 @@ __global__ void k_grid_header(const long long *__restrict__ bounds, const double
     g.key_bits = 1;
     g.ok = 1;
   } else {
-    g.ix0 = bounds[0];
-    g.iy0 = bounds[1];
-    g.iz0 = bounds[2];
-    g.nx = bounds[3] - bounds[0] + 1;
-    g.ny = bounds[4] - bounds[1] + 1;
-    g.nz = bounds[5] - bounds[2] + 1;
+    g.ix0 = b[0];
+    g.iy0 = b[1];
+    g.iz0 = b[2];
+    g.nx = b[3] - b[0] + 1;
+    g.ny = b[4] - b[1] + 1;
+    g.nz = b[5] - b[2] + 1;
     const double dcells = (double)g.nx * (double)g.ny * (double)g.nz;
     g.ok = (g.nx > 0 && g.ny > 0 && g.nz > 0 && dcells <= (double)max_cells) ? 1u : 0u;
     g.ncells = g.ok ? (unsigned long long)g.nx * (unsigned long long)g.ny * (unsigned long long)g.nz : 0;
@@ -299,6 +318,30 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// fine-gather layout (common.cuh): the planar fast path reads rec0..rec2 only
+__global__ void __launch_bounds__(256)
+    k_permute_fine(const uint32_t *__restrict__ order, uint32_t n, const float *__restrict__ pos,
+                   const float *__restrict__ nrm, const float *__restrict__ wi,
+                   const float *__restrict__ pw, const uint32_t *__restrict__ depth,
+                   float4 *__restrict__ rec0, float4 *__restrict__ rec1, float4 *__restrict__ rec2,
+                   float4 *__restrict__ rec3) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const size_t j = order[i];
+    const size_t o = 3 * j;
+    const float nx = nrm[o], ny = nrm[o + 1], wx = wi[o], wy = wi[o + 1];
+    const double L = elum((double)pw[o], (double)pw[o + 1], (double)pw[o + 2]);
+    const unsigned long long Lb = (unsigned long long)__double_as_longlong(L);
+    const uint32_t flags =
+        (fabsf(nx) < INFINITY && fabsf(ny) < INFINITY && fabsf(wx) < INFINITY && fabsf(wy) < INFINITY)
+            ? 1u : 0u;
+    rec0[i] = make_float4(pos[o], pos[o + 1], pos[o + 2], __uint_as_float(depth[j]));
+    rec1[i] = make_float4(nrm[o + 2], wi[o + 2], __uint_as_float((uint32_t)Lb),
+                          __uint_as_float((uint32_t)(Lb >> 32)));
+    rec2[i] = make_float4(pw[o], pw[o + 1], pw[o + 2], __uint_as_float(flags));
+    rec3[i] = make_float4(nx, ny, wx, wy);
+  }
+}
+
 // ------------------------------------------------------------------ query_ball
 // photon_map.cpp:53-78: 27 cells in (dx, dy, dz) nested order, each cell in
 // sorted (= insertion) order, closed fp64 ball test.  pass 0 counts, pass 1 fills.
@@ -384,15 +427,15 @@ cudaError_t radix_sort_pairs(cudaStream_t s, SortScratch &sc, uint32_t n, uint32
 }
 
 void launch_cell_bounds(cudaStream_t s, const float *pos, uint32_t n, const double *cell,
-                        long long *bounds, int sms) {
+                        uint32_t S, long long *bounds, int sms) {
   if (n == 0) return;
-  k_cell_bounds<<<cap_blocks(n, 256, sms, 8), 256, 0, s>>>(pos, n, cell, bounds);
+  k_cell_bounds<<<cap_blocks(n, 256, sms, 8), 256, 0, s>>>(pos, n, cell, S, bounds);
   note_launches(1);
 }
 
 void launch_grid_header(cudaStream_t s, const long long *bounds, const double *cell, uint32_t n,
-                        unsigned long long max_cells, GridHeader *hdr) {
-  k_grid_header<<<1, 1, 0, s>>>(bounds, cell, n, max_cells, hdr);
+                        unsigned long long max_cells, uint32_t S, GridHeader *hdr) {
+  k_grid_header<<<1, 1, 0, s>>>(bounds, cell, n, max_cells, S, hdr);
   note_launches(1);
 }
 
@@ -417,10 +460,14 @@ void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const 
 
 void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const float *pos,
                     const float *nrm, const float *wi, const float *pw, const uint32_t *depth,
-                    const PhotonRecs &r, int sms) {
+                    const PhotonRecs &r, int fine_layout, int sms) {
   if (n == 0) return;
-  k_permute<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
-                                                         r.rec0, r.rec1, r.rec2, r.rec3);
+  if (fine_layout)
+    k_permute_fine<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
+                                                                r.rec0, r.rec1, r.rec2, r.rec3);
+  else
+    k_permute<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
+                                                           r.rec0, r.rec1, r.rec2, r.rec3);
   note_launches(1);
 }
 
