@@ -365,7 +365,7 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
                          "kernel": "k_gather_test (gather + fused F-test)",
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "bytes_formula": "16*Q + (64 + 48*G*C)*H (SURVEY.md 8d)",
-                         "avg_launch_ms": gather_avg_s * 1e3,
+                         "avg_launch_ms": gather_avg_s * 1e3, "launch_ms": [round(x, 3) for x in g_ms],
                          "share_of_step": gather_avg_s * 1e3 / (elapsed_ms / args.steps),
                          "peak_source": peak_src, "traffic_source": traffic_wl},
             "gpu_launches": launches,

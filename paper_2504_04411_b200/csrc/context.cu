@@ -337,8 +337,9 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->tile.sort.keys_b, Hc)); A(dalloc(&ctx->tile.sort.vals_b, Hc));
   A(dalloc(&ctx->tile.sort.hist, radix_hist_entries((uint32_t)Hc)));
   A(dalloc(&ctx->tile.hp_map, 3 * Hc));
+  A(dalloc(reinterpret_cast<char **>(&ctx->tile.fprep), fine_prep_bytes() * Hc));
   A(dalloc(&ctx->tile.nonempty, 1));
-  A(cudaMallocHost(&ctx->h_total, sizeof(uint32_t)));
+  A(cudaMallocHost(&ctx->h_total, 2 * sizeof(uint32_t)));
   if (e != cudaSuccess) {
     int rc = cuda_fail(ctx, e, "fppm_gpu_create allocation");
     fppm_gpu_destroy(ctx);
@@ -382,7 +383,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
-                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.fdesc, T.partials,
+                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.fdesc, T.fprep, T.pbase, T.partials,
                   T.hp_map, T.nonempty};
   for (void *p : tdev)
     if (p) cudaFree(p);
@@ -853,7 +854,7 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
         (unsigned long long)(g.nx + 2) * (unsigned long long)(g.ny + 2) * (unsigned long long)(g.nz + 2);
     if (n_ext + 2 > S.bucket_cap) {
       FPPM_CUDA_OK(cudaStreamSynchronize(s));
-      void *old[] = {S.hp_start, S.items, S.chunks, S.item_base, S.scan_tmp};
+      void *old[] = {S.hp_start, S.items, S.chunks, S.item_base, S.scan_tmp, S.pbase};
       for (void *p : old)
         if (p) cudaFree(p);
       const unsigned long long cap = std::max<unsigned long long>(n_ext + 2, 4096);
@@ -861,6 +862,7 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
       FPPM_CUDA_OK(dalloc(&S.items, cap + 1));
       FPPM_CUDA_OK(dalloc(&S.chunks, cap + 1));
       FPPM_CUDA_OK(dalloc(&S.item_base, cap + 1));
+      FPPM_CUDA_OK(dalloc(&S.pbase, cap + 1));
       FPPM_CUDA_OK(dalloc(&S.scan_tmp, cap / 4096 + 8));
       S.bucket_cap = cap;
     }
@@ -882,22 +884,35 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
       FPPM_CUDA_OK(tile_schedule_bins(s, A, S, g, ctx->sms, chunk, &nb));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
                                  cudaMemcpyDeviceToHost, s));
+    if (variant == 4)
+      FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total + 1, S.pbase + nb, sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost, s));
     FPPM_CUDA_OK(cudaStreamSynchronize(s));
-    const uint32_t total = *ctx->h_total;
+    const uint32_t total = ctx->h_total[0];
+    // partial rows: fine = one per (hit point, item); tiled = 32 per item
+    const unsigned long long rows =
+        variant == 4 ? (unsigned long long)ctx->h_total[1] : (unsigned long long)total * 32ull;
     if (total > S.item_cap) {
       if (S.desc) cudaFree(S.desc);
       if (S.fdesc) cudaFree(S.fdesc);
-      if (S.partials) cudaFree(S.partials);
       S.desc = nullptr;
       S.fdesc = nullptr;
-      S.partials = nullptr;
-      const unsigned long long cap = std::max<unsigned long long>(total + total / 4, 1024);
+      // generous growth: reallocation inside a timed loop costs milliseconds
+      const unsigned long long cap =
+          std::max<unsigned long long>(2ull * total, (unsigned long long)ctx->H / 8 + 4096);
       if (variant == 4)
         FPPM_CUDA_OK(dalloc(&S.fdesc, cap));
       else
         FPPM_CUDA_OK(dalloc(&S.desc, cap));
-      FPPM_CUDA_OK(dalloc(&S.partials, cap * tile_partial_doubles(ctx->G, ctx->C)));
       S.item_cap = cap;
+    }
+    if (rows > S.row_cap) {
+      if (S.partials) cudaFree(S.partials);
+      S.partials = nullptr;
+      const unsigned long long cap =
+          std::max<unsigned long long>(2ull * rows, 4ull * ctx->H + 4096);
+      FPPM_CUDA_OK(dalloc(&S.partials, cap * (tile_partial_doubles(ctx->G, ctx->C) / 32)));
+      S.row_cap = cap;
     }
     TileArgs T;
     T.hp_order = S.hp_order;
@@ -906,8 +921,10 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
     T.total_items = S.item_base + nb;
     if (variant == 4) {
       FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, chunk));
+      FPPM_CUDA_OK(launch_fine_prep(s, A, S.hp_order, S.fprep, ctx->sms));
       FineArgs F;
       F.desc = S.fdesc;
+      F.prep = static_cast<const FinePrep *>(S.fprep);
       F.hp_order = S.hp_order;
       F.partials = S.partials;
       F.hp_map = S.hp_map;

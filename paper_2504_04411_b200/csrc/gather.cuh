@@ -102,18 +102,21 @@ struct SortScratch {
 // ---- fine-cell tiled gather (gather_fine.cu)
 constexpr int kFMaxPieces = 12;
 constexpr uint32_t kFineS = 4;  // fine cells per reference cell and axis (slab layout)
-struct FineDesc {  // 160 B, one per (home cell, wave, window of the staged union)
-  uint32_t hp_lo, hp_n, first, nchunks;
-  uint32_t lo, hi, npieces, chunk;  // window [lo, hi) of the union's flattened pieces
+constexpr uint32_t kFSub = 16;   // windows per item (one CTA walks them in order)
+struct FineDesc {  // 160 B, one per (home cell, wave, run of <= kFSub windows)
+  uint32_t hp_lo, hp_n, nwin, npieces;
+  uint32_t c0, c1, pbase, pad0;     // windows [c0, c1) of the union; partial rows pbase + k
   int32_t ux0, ux1, uy0, uy1, uz0, uz1;  // union of the wave's fine boxes
   uint32_t src[kFMaxPieces];        // first sorted record of piece p
-  uint32_t pre[kFMaxPieces + 1];    // flattened offset of piece p
+  uint32_t pre[kFMaxPieces + 1];    // flattened offset of piece p (pre[12] = union size)
   uint32_t pad[1];
 };
 static_assert(sizeof(FineDesc) == 160, "FineDesc layout");
 
+struct FinePrep;  // gather_fine.cu (per hit point state in wave order)
 struct FineArgs {
   const FineDesc *desc;
+  const FinePrep *prep;
   const uint32_t *hp_order;
   double *partials;
   const uint32_t *hp_map;
@@ -123,6 +126,8 @@ struct FineArgs {
 struct TileSched {
   FineDesc *fdesc = nullptr;
   unsigned long long fdesc_cap = 0;
+  void *fprep = nullptr;  // FinePrep[H]
+  uint32_t *pbase = nullptr;  // [nb + 1] partial rows per bucket, scanned
   SortScratch sort;     // hit-point keys (capacity H)
   uint32_t *hp_order;   // alias of the sorted values
   uint32_t *hp_start;   // [nb + 1]
@@ -133,6 +138,7 @@ struct TileSched {
   uint32_t *hp_map;     // [3 H]
   uint32_t *nonempty;   // device counter: buckets holding hit points
   unsigned long long bucket_cap, item_cap;
+  unsigned long long row_cap = 0;  // partial rows allocated
 };
 
 __host__ __device__ constexpr int partial_size(int gmax, int ch) { return gmax + 2 * ch * gmax + 3; }
@@ -161,7 +167,11 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
                                int sms, uint32_t chunk, uint32_t *nb_out);
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
                                 uint32_t chunk);
+size_t fine_acc_doubles(int G, int C);
 cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms);
+size_t fine_prep_bytes();
+cudaError_t launch_fine_prep(cudaStream_t s, const GatherArgs &A, const uint32_t *hp_order, void *prep,
+                             int sms);
 
 cudaError_t launch_gather_test(cudaStream_t s, const GatherArgs &A, int C, int sms);
 cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2 *y,

@@ -191,15 +191,17 @@ static __device__ bool wave_union(const GatherArgs &A, const GridHeader &g, cons
   return any;
 }
 
-// items per bucket: sum over its waves of ceil(staged union / chunk)
+// per bucket: items (runs of <= kFSub windows of ceil(union / chunk)) and
+// partial rows (items x wave size)
 __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
                              const uint32_t *__restrict__ hp_order, uint32_t *__restrict__ items,
-                             uint32_t chunk, uint32_t *__restrict__ nonempty) {
+                             uint32_t *__restrict__ prows, uint32_t chunk,
+                             uint32_t *__restrict__ nonempty) {
   const GridHeader g = *A.grid;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
     const uint32_t h0 = b < nb ? hp_start[b] : 0u;
     const uint32_t nhp = b < nb ? hp_start[b + 1] - h0 : 0u;
-    uint32_t it = 0;
+    uint32_t it = 0, pr = 0;
     if (nhp) atomicAdd(nonempty, 1u);
     for (uint32_t w = 0; w * kFWave < nhp; ++w) {
       const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
@@ -213,19 +215,24 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
           T += A.cell_start[k1 + 1] - A.cell_start[k0];
         }
       }
-      it += T == 0 ? 1u : (T + chunk - 1) / chunk;
+      const uint32_t nwin = T == 0 ? 1u : (T + chunk - 1) / chunk;
+      const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
+      it += nsub;
+      pr += nsub * n;
     }
     items[b] = it;
+    prows[b] = pr;
   }
 }
 
 __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
                             const uint32_t *__restrict__ hp_order, const uint32_t *__restrict__ item_base,
-                            FineDesc *__restrict__ desc, uint32_t *__restrict__ hp_map, uint32_t chunk) {
+                            const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
+                            uint32_t *__restrict__ hp_map, uint32_t chunk) {
   const GridHeader g = *A.grid;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
     const uint32_t h0 = hp_start[b], nhp = hp_start[b + 1] - h0;
-    uint32_t item = item_base[b];
+    uint32_t item = item_base[b], prow = prow_base[b];
     for (uint32_t w = 0; w * kFWave < nhp; ++w) {
       const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
       FineDesc d;
@@ -250,24 +257,64 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
       }
       d.pre[kFMaxPieces] = T;
       d.npieces = (uint32_t)np;
+      d.pad0 = 0;
+      d.pad[0] = 0;
       d.ux0 = u.x0; d.ux1 = u.x1; d.uy0 = u.y0; d.uy1 = u.y1; d.uz0 = u.z0; d.uz1 = u.z1;
-      const uint32_t nch = T == 0 ? 1u : (T + chunk - 1) / chunk;
-      d.first = item;
-      d.nchunks = nch;
+      const uint32_t nwin = T == 0 ? 1u : (T + chunk - 1) / chunk;
+      const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
+      d.nwin = nwin;
       for (uint32_t j = 0; j < n; ++j) {
         const uint32_t h = hp_order[d.hp_lo + j];
-        hp_map[3 * (size_t)h] = item;
-        hp_map[3 * (size_t)h + 1] = nch;
-        hp_map[3 * (size_t)h + 2] = j;
+        hp_map[3 * (size_t)h] = prow + j;  // finalize: rows prow + j + sub * n
+        hp_map[3 * (size_t)h + 1] = nsub;
+        hp_map[3 * (size_t)h + 2] = n;
       }
-      for (uint32_t ch = 0; ch < nch; ++ch, ++item) {
-        d.chunk = ch;
-        d.lo = ch * chunk;
-        d.hi = min(T, d.lo + chunk);
-        if (d.hi < d.lo) d.hi = d.lo;
+      for (uint32_t sb = 0; sb < nsub; ++sb, ++item) {
+        d.c0 = sb * kFSub;
+        d.c1 = min(nwin, d.c0 + kFSub);
+        d.pbase = prow + sb * n;
         desc[item] = d;
       }
+      prow += nsub * n;
     }
+  }
+}
+
+struct __align__(16) FinePrep {
+  Hit h;
+  int32_t bx0, bx1, by0, by1, bz0, bz1;  // fine box (fine_box)
+  uint32_t nruns, pad;
+  uint2 run[kFMaxPieces];  // sorted-record range [begin, end) of each run
+};
+static_assert(sizeof(FinePrep) % 16 == 0, "FinePrep must be a multiple of 16 B (TMA)");
+
+// Per hit point, once per gather, in wave order (position in hp_order): the
+// full Hit state, its fine box and the sorted-record range of each run.
+__global__ void k_fine_prep(const GatherArgs A, const uint32_t *__restrict__ hp_order,
+                            FinePrep *__restrict__ prep) {
+  const GridHeader g = *A.grid;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.H; i += gridDim.x * blockDim.x) {
+    const uint32_t h = hp_order[i];
+    FinePrep P;
+    make_hit(A, h, P.h);
+    FBox b = {0, -1, 0, -1, 0, -1};
+    const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
+    const bool ok = gathered && fine_box(g, P.h.cx, P.h.cy, P.h.cz, P.h.r, b);
+    const int nr = ok ? run_count(g, b) : 0;
+    P.bx0 = b.x0; P.bx1 = b.x1; P.by0 = b.y0; P.by1 = b.y1; P.bz0 = b.z0; P.bz1 = b.z1;
+    P.nruns = (uint32_t)nr;
+    P.pad = 0;
+    const FBox none = {0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < kFMaxPieces; ++j) {
+      uint2 r = make_uint2(0u, 0u);
+      if (j < nr) {
+        unsigned long long k0, k1;
+        (void)run_keys(g, none, b, j, k0, k1);
+        r = make_uint2(A.cell_start[k0], A.cell_start[k1 + 1]);
+      }
+      P.run[j] = r;
+    }
+    prep[i] = P;
   }
 }
 
@@ -278,14 +325,15 @@ struct FineLayout {
   static constexpr int NQ = 32 / NC;                    // lane groups in the slot reduction
   static constexpr int PS = partial_size(GMAX, CH);
   static constexpr size_t kSlotBytes = (size_t)kFWarps * NC * 32 * 16;
-  static constexpr size_t kFragBytes = (size_t)kFMaxFrag * PS * sizeof(double);
+  static constexpr size_t kPrepBytes = (size_t)kFWave * sizeof(FinePrep);
+  static constexpr size_t kAccBytes = (size_t)kFWave * PS * sizeof(double);  // per-hp sums over windows
   static constexpr int kMinBlocks = NC <= 8 ? 2 : 1;
   // dynamic shared memory: records (64 B per candidate) + slots + fragments
-  // (2 CTAs per SM: 228 KB - 2 x (1 KB reserved + ~18 KB static) per CTA)
-  static constexpr size_t kBudget = NC <= 8 ? (size_t)94 * 1024 : (size_t)200 * 1024;
+  // (2 CTAs per SM: 228 KB - 2 x (1 KB reserved + ~3 KB static) per CTA)
+  static constexpr size_t kBudget = NC <= 8 ? (size_t)106 * 1024 : (size_t)212 * 1024;
   static constexpr uint32_t kChunk =
-      (uint32_t)(((kBudget - kSlotBytes - kFragBytes) / 64) & ~(size_t)31);
-  static constexpr size_t kDynBytes = (size_t)kChunk * 64 + kSlotBytes + kFragBytes;
+      (uint32_t)(((kBudget - kSlotBytes - kPrepBytes - kAccBytes) / 64) & ~(size_t)31);
+  static constexpr size_t kDynBytes = (size_t)kChunk * 64 + kSlotBytes + kPrepBytes + kAccBytes;
 };
 
 struct FineState {
@@ -486,13 +534,14 @@ static __device__ __forceinline__ void fine_exact_batch(const GatherArgs &A, con
   __syncwarp();
 }
 
+// All candidates of one hit point inside the staged window: runs held by
+// lanes (lane j: smem start rs, length rl of run j).
 template <int GMAX, int CH, bool PLANAR>
-static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const Hit &Hs, uint32_t ib,
-                                                     uint32_t ie, const uint2 *runs, int nruns,
-                                                     uint32_t q, uint32_t ex, uint32_t slots,
-                                                     PackedCounts<GMAX> &cnt, double &p0, double &p1,
-                                                     double &p2, uint32_t r0, uint32_t r1, uint32_t r2,
-                                                     uint32_t r3, FineState &st) {
+static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const Hit &Hs, uint32_t rs,
+                                                     uint32_t rl, int nruns, uint32_t q, uint32_t ex,
+                                                     uint32_t slots, PackedCounts<GMAX> &cnt, double &p0,
+                                                     double &p1, double &p2, uint32_t r0, uint32_t r1,
+                                                     uint32_t r2, uint32_t r3, FineState &st) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
   const HitF F = hitf(Hs, A.na, A.ns);
@@ -503,15 +552,10 @@ static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const 
   K.gray = Hs.gray;
   const uint32_t max_depth = A.max_depth;
   const bool lo_zero = PLANAR || (F.clx == 0.0f && F.cly == 0.0f && F.clz == 0.0f);
-  uint32_t vp = 0;
-  for (int j = 0; j < nruns && vp < ie; ++j) {
-    const uint2 R = runs[j];
-    const uint32_t a = max(vp, ib), b = min(vp + R.y, ie);
-    const uint32_t rb = vp;
-    vp += R.y;
-    if (b <= a) continue;
-    const uint32_t s1 = R.x + (b - rb);
-    for (uint32_t base = R.x + (a - rb); base < s1; base += 64) {
+  for (int j = 0; j < nruns; ++j) {
+    const uint32_t s0 = __shfl_sync(kFull, rs, j), n = __shfl_sync(kFull, rl, j);
+    const uint32_t s1 = s0 + n;
+    for (uint32_t base = s0; base < s1; base += 64) {
       // ---- test: ball + depth (photon_map.cpp:76, integrator.cpp:396)
       const uint32_t i0 = base + lane, i1 = i0 + 32;
       const bool v0 = i0 < s1, v1 = i1 < s1;
@@ -553,16 +597,14 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
   constexpr uint32_t CHUNK = Lay::kChunk;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *s_slots = reinterpret_cast<double *>(smem_raw + (size_t)CHUNK * 64);
-  double *s_frag = reinterpret_cast<double *>(smem_raw + (size_t)CHUNK * 64 + Lay::kSlotBytes);
-  __shared__ Hit s_hit[kFWave];
-  __shared__ uint2 s_run[kFWave][kFMaxPieces];
-  __shared__ uint32_t s_nrun[kFWave], s_tot[kFWave];
+  FinePrep *s_prep = reinterpret_cast<FinePrep *>(smem_raw + (size_t)CHUNK * 64 + Lay::kSlotBytes);
+  double *s_acc =
+      reinterpret_cast<double *>(smem_raw + (size_t)CHUNK * 64 + Lay::kSlotBytes + Lay::kPrepBytes);
   __shared__ uint32_t s_q[kFWarps][kFQueue];
   __shared__ uint32_t s_ex[kFWarps][kFExact];
-  __shared__ uint32_t s_frag_hp[kFMaxFrag];
   __shared__ FineDesc s_desc;
   __shared__ __align__(8) uint64_t s_bar;
-  __shared__ uint32_t s_item;
+  __shared__ uint32_t s_item, s_next;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t r0 = smem_u32(smem_raw);
@@ -589,157 +631,133 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
     if (threadIdx.x < sizeof(FineDesc) / 4)
       reinterpret_cast<uint32_t *>(&s_desc)[threadIdx.x] =
           reinterpret_cast<const uint32_t *>(T.desc + item)[threadIdx.x];
-    if (threadIdx.x < kFMaxFrag) s_frag_hp[threadIdx.x] = kFNone;
     __syncthreads();
-    const uint32_t lo = s_desc.lo, hi = s_desc.hi, hp_n = s_desc.hp_n;
-    const uint32_t ncand = hi - lo;
-    if (threadIdx.x == 0 && ncand) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&s_bar, ncand * 64u);
-      for (uint32_t p = 0; p < s_desc.npieces; ++p) {
-        const uint32_t a = max(s_desc.pre[p], lo), e = min(s_desc.pre[p + 1], hi);
-        if (e <= a) continue;
-        const uint32_t src = s_desc.src[p] + (a - s_desc.pre[p]), dst = a - lo, n = e - a;
-        bulk_g2s(smem_raw + (size_t)dst * 16, A.rec0 + src, n * 16u, &s_bar);
-        bulk_g2s(smem_raw + (size_t)(CHUNK + dst) * 16, A.rec1 + src, n * 16u, &s_bar);
-        bulk_g2s(smem_raw + (size_t)(2 * CHUNK + dst) * 16, A.rec2 + src, n * 16u, &s_bar);
-        bulk_g2s(smem_raw + (size_t)(3 * CHUNK + dst) * 16, A.rec3 + src, n * 16u, &s_bar);
-      }
+    const uint32_t hp_n = s_desc.hp_n, Tu = s_desc.pre[kFMaxPieces];
+    double *out = T.partials + (size_t)s_desc.pbase * PS;
+    if (Tu == 0) {
+      // no candidates for this wave: zero partials
+      for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) out[i] = 0.0;
+      __syncthreads();
+      continue;
     }
-    if (threadIdx.x < hp_n) make_hit(A, T.hp_order[s_desc.hp_lo + threadIdx.x], s_hit[threadIdx.x]);
-    __syncthreads();
-
-    // ---- per hit point: its runs inside this window (lane = run)
-    FBox u;
-    u.x0 = s_desc.ux0; u.x1 = s_desc.ux1; u.y0 = s_desc.uy0; u.y1 = s_desc.uy1;
-    u.z0 = s_desc.uz0; u.z1 = s_desc.uz1;
-    for (uint32_t k = warp; k < hp_n; k += kFWarps) {
-      const Hit &H = s_hit[k];
-      FBox b;
-      const bool ok = ncand && fine_box(g, H.cx, H.cy, H.cz, H.r, b);
-      const int nr = ok ? run_count(g, b) : 0;
-      uint32_t rs = 0, rl = 0;
-      if (lane < nr) {
-        unsigned long long k0, k1;
-        const int p = run_keys(g, u, b, lane, k0, k1);
-        const uint32_t ga = A.cell_start[k0], gb = A.cell_start[k1 + 1];
-        const uint32_t fa = s_desc.pre[p] + (ga - s_desc.src[p]), fb = fa + (gb - ga);
-        const uint32_t ca = max(fa, lo), cb = min(fb, hi);
-        if (cb > ca) {
-          rs = ca - lo;
-          rl = cb - ca;
+    for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) s_acc[i] = 0.0;
+    // ---- the item's windows in order; per-hp sums accumulate in s_acc
+    for (uint32_t c = s_desc.c0; c < s_desc.c1; ++c) {
+      const uint32_t lo = c * CHUNK, hi = min(Tu, lo + CHUNK);
+      const uint32_t ncand = hi - lo;
+      if (threadIdx.x == 0) {
+        s_next = 0;
+        fence_proxy_async_smem();
+        const uint32_t prep_bytes = c == s_desc.c0 ? hp_n * (uint32_t)sizeof(FinePrep) : 0u;
+        mbar_arrive_expect_tx(&s_bar, ncand * 64u + prep_bytes);
+        if (prep_bytes) bulk_g2s(s_prep, T.prep + s_desc.hp_lo, prep_bytes, &s_bar);
+        for (uint32_t p = 0; p < s_desc.npieces; ++p) {
+          const uint32_t a = max(s_desc.pre[p], lo), e = min(s_desc.pre[p + 1], hi);
+          if (e <= a) continue;
+          const uint32_t src = s_desc.src[p] + (a - s_desc.pre[p]), dst = a - lo, n = e - a;
+          bulk_g2s(smem_raw + (size_t)dst * 16, A.rec0 + src, n * 16u, &s_bar);
+          bulk_g2s(smem_raw + (size_t)(CHUNK + dst) * 16, A.rec1 + src, n * 16u, &s_bar);
+          bulk_g2s(smem_raw + (size_t)(2 * CHUNK + dst) * 16, A.rec2 + src, n * 16u, &s_bar);
+          bulk_g2s(smem_raw + (size_t)(3 * CHUNK + dst) * 16, A.rec3 + src, n * 16u, &s_bar);
         }
       }
-      if (lane < kFMaxPieces) s_run[k][lane] = make_uint2(rs, rl);
-      const uint32_t tot = warp_sum(rl);
-      if (lane == 0) {
-        s_tot[k] = tot;
-        s_nrun[k] = (uint32_t)nr;
-      }
-    }
-    __syncthreads();
-
-    // ---- balanced split of the (hit point x candidate) space over the warps
-    const uint32_t tk = (uint32_t)lane < hp_n ? s_tot[lane] : 0u;
-    uint32_t incl = tk;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const uint32_t excl = incl - tk;
-    const uint32_t W = __shfl_sync(kFull, incl, 31);
-    const uint32_t f0 = (uint32_t)(((unsigned long long)W * warp) / kFWarps);
-    const uint32_t f1 = (uint32_t)(((unsigned long long)W * (warp + 1)) / kFWarps);
-    if (ncand) {
       mbar_wait(&s_bar, phase);
       phase ^= 1u;
-    }
-    for (uint32_t f = f0; f < f1;) {
-      const uint32_t m = __ballot_sync(kFull, (uint32_t)lane < hp_n && incl > f);
-      const int k = __ffs(m) - 1;
-      const uint32_t Pk = __shfl_sync(kFull, excl, k), Tk = __shfl_sync(kFull, tk, k);
-      const uint32_t ib = f - Pk, ie = min(Tk, f1 - Pk);
-      f = Pk + ie;
-      const Hit &Hs = s_hit[k];
-      PackedCounts<GMAX> cnt;
-#pragma unroll
-      for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
-      double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-      const bool planar = Hs.fast && Hs.nx == 0.0 && Hs.ny == 0.0 && Hs.nz == 1.0 && A.ns == 4 &&
-                          Hs.clx == 0.0f && Hs.cly == 0.0f && Hs.clz == 0.0f;
-      if (planar)
-        fine_fragment<GMAX, CH, true>(A, Hs, ib, ie, s_run[k], (int)s_nrun[k], qa, exa, slots, cnt, p0, p1,
-                                      p2, r0, r1, r2, r3, st);
-      else
-        fine_fragment<GMAX, CH, false>(A, Hs, ib, ie, s_run[k], (int)s_nrun[k], qa, exa, slots, cnt, p0,
-                                       p1, p2, r0, r1, r2, r3, st);
 
-      // ---- fragment partial: fixed-order reduction of the lane slots
-      const int col = lane % NC, grp = lane / NC;
-      double sm = 0.0, sq = 0.0;
-      if (grp < NQ) {
-        // rows rotated by the column: the 16-B slots a warp touches per step
-        // fall in distinct bank groups (fixed order, so still deterministic)
-        constexpr int R = 32 / NQ;
-        const uint32_t base = slots + (uint32_t)(col * 32 + grp * R) * 16u;
+      // ---- warps take whole hit points (one fragment per hit point and window)
+      for (;;) {
+        uint32_t k = 0;
+        if (lane == 0) k = atomicAdd(&s_next, 1u);
+        k = __shfl_sync(kFull, k, 0);
+        if (k >= hp_n) break;
+        const FinePrep &P = s_prep[k];
+        const Hit &Hs = P.h;
+        // runs of this hit point inside the window (lane j = run j)
+        const int nr = (int)P.nruns;
+        uint32_t rs = 0, rl = 0;
+        if (lane < nr) {
+          int pc;
+          if (g.S > 1) {
+            pc = P.bx0 + lane - s_desc.ux0;
+          } else {
+            const int nyb = P.by1 - P.by0 + 1, nyu = s_desc.uy1 - s_desc.uy0 + 1;
+            pc = (P.bx0 + lane / nyb - s_desc.ux0) * nyu + (P.by0 + lane % nyb - s_desc.uy0);
+          }
+          const uint2 R = P.run[lane];
+          const uint32_t fa = s_desc.pre[pc] + (R.x - s_desc.src[pc]), fb = fa + (R.y - R.x);
+          const uint32_t ca = max(fa, lo), cb = min(fb, hi);
+          if (cb > ca) {
+            rs = ca - lo;
+            rl = cb - ca;
+          }
+        }
+        if (!__any_sync(kFull, rl != 0)) continue;
+        PackedCounts<GMAX> cnt;
+#pragma unroll
+        for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+        const bool planar = Hs.fast && Hs.nx == 0.0 && Hs.ny == 0.0 && Hs.nz == 1.0 && A.ns == 4 &&
+                            Hs.clx == 0.0f && Hs.cly == 0.0f && Hs.clz == 0.0f;
+        if (planar)
+          fine_fragment<GMAX, CH, true>(A, Hs, rs, rl, nr, qa, exa, slots, cnt, p0, p1, p2, r0, r1, r2, r3,
+                                        st);
+        else
+          fine_fragment<GMAX, CH, false>(A, Hs, rs, rl, nr, qa, exa, slots, cnt, p0, p1, p2, r0, r1, r2,
+                                         r3, st);
+
+        // ---- fixed-order reduction of the lane slots, added to the hp's sums
+        const int col = lane % NC, grp = lane / NC;
+        double sm = 0.0, sq = 0.0;
+        if (grp < NQ) {
+          // rows rotated by the column: the 16-B slots a warp touches per step
+          // fall in distinct bank groups (fixed order, so still deterministic)
+          constexpr int R = 32 / NQ;
+          const uint32_t base = slots + (uint32_t)(col * 32 + grp * R) * 16u;
 #pragma unroll 4
-        for (int i = 0; i < R; ++i) {
-          const uint32_t a = base + (uint32_t)((i + col) % R) * 16u;
-          const double2 v = lds_f64x2(a);
-          sm += v.x;
-          sq += v.y;
-          sts_f64x2(a, make_double2(0.0, 0.0));
+          for (int i = 0; i < R; ++i) {
+            const uint32_t a = base + (uint32_t)((i + col) % R) * 16u;
+            const double2 v = lds_f64x2(a);
+            sm += v.x;
+            sq += v.y;
+            sts_f64x2(a, make_double2(0.0, 0.0));
+          }
         }
-      }
 #pragma unroll
-      for (int o = (NQ / 2) * NC; o >= NC && o > 0; o >>= 1) {
-        sm += __shfl_down_sync(kFull, sm, o);
-        sq += __shfl_down_sync(kFull, sq, o);
-      }
-      p0 = warp_sum(p0);
-      p1 = warp_sum(p1);
-      p2 = warp_sum(p2);
-      // packed byte counts -> 16-bit halves -> warp sums (<= 32 * 255 per half)
-      uint32_t csum[2 * PackedCounts<GMAX>::NP];
-#pragma unroll
-      for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) {
-        csum[2 * r] = __reduce_add_sync(kFull, cnt.w[r] & 0x00ff00ffu);
-        csum[2 * r + 1] = __reduce_add_sync(kFull, (cnt.w[r] >> 8) & 0x00ff00ffu);
-      }
-      const uint32_t slot = k + warp;
-      double *pp = s_frag + (size_t)slot * PS;
-      if (lane < NC) {
-        const int c = lane / GMAX, gg = lane % GMAX;
-        pp[GMAX + c * GMAX + gg] = sm;
-        pp[GMAX + CH * GMAX + c * GMAX + gg] = sq;
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int gg = 0; gg < GMAX; ++gg) {
-          const uint32_t wd = csum[2 * (gg >> 2) + (gg & 1)];
-          pp[gg] = (double)((gg & 2) ? (wd >> 16) : (wd & 0xffffu));
+        for (int o = (NQ / 2) * NC; o >= NC && o > 0; o >>= 1) {
+          sm += __shfl_down_sync(kFull, sm, o);
+          sq += __shfl_down_sync(kFull, sq, o);
         }
-        pp[GMAX + 2 * CH * GMAX] = p0;
-        pp[GMAX + 2 * CH * GMAX + 1] = p1;
-        pp[GMAX + 2 * CH * GMAX + 2] = p2;
-        s_frag_hp[slot] = (uint32_t)k;
+        p0 = warp_sum(p0);
+        p1 = warp_sum(p1);
+        p2 = warp_sum(p2);
+        // packed byte counts -> 16-bit halves -> warp sums (<= 32 * 255 per half)
+        uint32_t csum[2 * PackedCounts<GMAX>::NP];
+#pragma unroll
+        for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) {
+          csum[2 * r] = __reduce_add_sync(kFull, cnt.w[r] & 0x00ff00ffu);
+          csum[2 * r + 1] = __reduce_add_sync(kFull, (cnt.w[r] >> 8) & 0x00ff00ffu);
+        }
+        double *acc = s_acc + (size_t)k * PS;
+        if (lane < NC) {
+          const int cc = lane / GMAX, gg = lane % GMAX;
+          acc[GMAX + cc * GMAX + gg] += sm;
+          acc[GMAX + CH * GMAX + cc * GMAX + gg] += sq;
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int gg = 0; gg < GMAX; ++gg) {
+            const uint32_t wd = csum[2 * (gg >> 2) + (gg & 1)];
+            acc[gg] += (double)((gg & 2) ? (wd >> 16) : (wd & 0xffffu));
+          }
+          acc[GMAX + 2 * CH * GMAX] += p0;
+          acc[GMAX + 2 * CH * GMAX + 1] += p1;
+          acc[GMAX + 2 * CH * GMAX + 2] += p2;
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      __syncthreads();  // the window buffer and s_next are reused by the next window
     }
-    __syncthreads();
-
-    // ---- combine fragments per hit point (warp order) into the item partial
-    if (threadIdx.x < hp_n) {
-      const uint32_t k = threadIdx.x;
-      double *out = T.partials + ((size_t)item * kFWave + k) * PS;
-      for (int j = 0; j < PS; ++j) {
-        double x = 0.0;
-        for (int w = 0; w < kFWarps; ++w)
-          if (s_frag_hp[k + w] == k) x += s_frag[(size_t)(k + w) * PS + j];
-        out[j] = x;
-      }
-    }
+    for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) out[i] = s_acc[i];
     __syncthreads();
   }
 
@@ -806,15 +824,17 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   e = launch_bucket_start(s, skeys, A.H, nb, S.hp_start, sms);
   if (e != cudaSuccess) return e;
   k_fine_items<<<fblocks(nb + 1, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order, S.items,
-                                                             chunk, S.nonempty);
+                                                             S.chunks, chunk, S.nonempty);
   note_launches(1);
-  return launch_exclusive_scan(s, S.items, nb + 1, S.scan_tmp, S.item_base);
+  e = launch_exclusive_scan(s, S.items, nb + 1, S.scan_tmp, S.item_base);
+  if (e != cudaSuccess) return e;
+  return launch_exclusive_scan(s, S.chunks, nb + 1, S.scan_tmp, S.pbase);
 }
 
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
                                 uint32_t chunk) {
   k_fine_desc<<<fblocks(nb, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order, S.item_base,
-                                                        S.fdesc, S.hp_map, chunk);
+                                                        S.pbase, S.fdesc, S.hp_map, chunk);
   note_launches(1);
   return cudaGetLastError();
 }
@@ -831,6 +851,16 @@ static cudaError_t launch_fine_t(cudaStream_t s, const GatherArgs &A, const Fine
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   k_gather_fine<GMAX, CH><<<sms * per_sm, kFThreads, smem, s>>>(A, T);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+size_t fine_prep_bytes() { return sizeof(FinePrep); }
+
+cudaError_t launch_fine_prep(cudaStream_t s, const GatherArgs &A, const uint32_t *hp_order, void *prep,
+                             int sms) {
+  if (A.H == 0) return cudaSuccess;
+  k_fine_prep<<<fblocks(A.H, 128, sms, 8), 128, 0, s>>>(A, hp_order, static_cast<FinePrep *>(prep));
   note_launches(1);
   return cudaGetLastError();
 }

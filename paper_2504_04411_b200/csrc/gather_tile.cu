@@ -218,9 +218,10 @@ __global__ void k_item_desc(const uint32_t *__restrict__ hp_start, uint32_t nb,
       const uint32_t first = item;
       for (uint32_t j = w * kWave; j < min(nhp, (w + 1) * kWave); ++j) {
         const uint32_t h = hp_order[h0 + j];
-        hp_map[3 * (size_t)h] = first;
+        // finalize reads partials (base + ch * stride) for ch < nch
+        hp_map[3 * (size_t)h] = first * kWave + (j - w * kWave);
         hp_map[3 * (size_t)h + 1] = nch;
-        hp_map[3 * (size_t)h + 2] = j - w * kWave;
+        hp_map[3 * (size_t)h + 2] = kWave;
       }
       for (uint32_t ch = 0; ch < nch; ++ch, ++item) {
         ItemDesc d;
@@ -556,8 +557,8 @@ __global__ void __launch_bounds__(128) k_tile_finalize(const GatherArgs A, const
   double my_rmax = 0.0;
   uint32_t my_tested = 0, my_rejected = 0;
   for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < A.H; h += gridDim.x * blockDim.x) {
-    const uint32_t first = T.hp_map[3 * (size_t)h], nch = T.hp_map[3 * (size_t)h + 1],
-                   slot = T.hp_map[3 * (size_t)h + 2];
+    const uint32_t pbase = T.hp_map[3 * (size_t)h], nch = T.hp_map[3 * (size_t)h + 1],
+                   stride = T.hp_map[3 * (size_t)h + 2];
     uint32_t cnt[GMAX];
     double sm[CH][GMAX], sq[CH][GMAX];
     double p0 = 0.0, p1 = 0.0, p2 = 0.0;
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(128) k_tile_finalize(const GatherArgs A, const
       for (int c = 0; c < CH; ++c) sm[c][g] = sq[c][g] = 0.0;
     }
     for (uint32_t ch = 0; ch < nch; ++ch) {
-      const double *pp = T.partials + ((size_t)(first + ch) * kWave + slot) * PS;
+      const double *pp = T.partials + ((size_t)pbase + (size_t)ch * stride) * PS;
 #pragma unroll
       for (int g = 0; g < GMAX; ++g) cnt[g] += (uint32_t)pp[g];
 #pragma unroll
