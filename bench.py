@@ -17,6 +17,7 @@ Output: one JSON line on rank 0 (contract in the task statement).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -463,6 +464,10 @@ def run_e2e(ctx, wl, batches, args, world, rank, dev, stream, H):
 
 
 def main():
+    # no Python garbage-collection pauses inside timed regions (a gen-2 pass
+    # between two launches would be charged to the device timeline)
+    gc.collect()
+    gc.disable()
     args = parse()
     from paper_2504_04411_b200.workloads import WORKLOADS
     wl = WORKLOADS[args.workload]

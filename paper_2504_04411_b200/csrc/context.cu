@@ -2,6 +2,7 @@
 // orchestration and host<->device plumbing around the kernels in grid.cu,
 // gather.cu and generate.cu.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -671,7 +672,7 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
     if (ctx->d_cell_start) cudaFree(ctx->d_cell_start);
     ctx->d_cell_start = nullptr;
     ctx->cell_cap = 0;
-    const unsigned long long cap = std::max<unsigned long long>(g.ncells + 1, 1024);
+    const unsigned long long cap = std::max<unsigned long long>(2 * (g.ncells + 1), 1024);
     FPPM_CUDA_OK(cudaMalloc(&ctx->d_cell_start, sizeof(uint32_t) * cap));
     ctx->cell_cap = cap;
   }
@@ -818,8 +819,13 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
                          fppm_gpu_summary *summary) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "gather before build_grid");
+  const bool dbg = std::getenv("FPPM_DEBUG") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   int rc = ensure_crit(ctx, ctx->end_calls + 2);
   if (rc) return rc;
+  const auto t1 = now();
   const bool snap = out && (out->stat_count || out->stat_sum || out->stat_sum_sq);
   if (snap && (rc = ensure_snapshots(ctx))) return rc;
   cudaStream_t s = ctx->stream;
@@ -857,7 +863,7 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
       void *old[] = {S.hp_start, S.items, S.chunks, S.item_base, S.scan_tmp, S.pbase};
       for (void *p : old)
         if (p) cudaFree(p);
-      const unsigned long long cap = std::max<unsigned long long>(n_ext + 2, 4096);
+      const unsigned long long cap = std::max<unsigned long long>(2 * (n_ext + 2), 4096);
       FPPM_CUDA_OK(dalloc(&S.hp_start, cap + 1));
       FPPM_CUDA_OK(dalloc(&S.items, cap + 1));
       FPPM_CUDA_OK(dalloc(&S.chunks, cap + 1));
@@ -887,8 +893,14 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
     if (variant == 4)
       FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total + 1, S.pbase + nb, sizeof(uint32_t),
                                    cudaMemcpyDeviceToHost, s));
+    const auto t2 = now();
     FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    const auto t3 = now();
     const uint32_t total = ctx->h_total[0];
+    if (dbg)
+      std::fprintf(stderr, "[fppm] iteration %llu items %u rows %u (caps %llu %llu) crit %.3f sched-issue %.3f sync %.3f ms\n",
+                   (unsigned long long)iteration, total, variant == 4 ? ctx->h_total[1] : total * 32u,
+                   S.item_cap, S.row_cap, ms(t0, t1), ms(t1, t2), ms(t2, t3));
     // partial rows: fine = one per (hit point, item); tiled = 32 per item
     const unsigned long long rows =
         variant == 4 ? (unsigned long long)ctx->h_total[1] : (unsigned long long)total * 32ull;

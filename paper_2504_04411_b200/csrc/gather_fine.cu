@@ -36,8 +36,7 @@ namespace fppm_b200 {
 constexpr int kFWarps = 8;
 constexpr int kFThreads = kFWarps * kWarp;
 constexpr int kFWave = 32;      // hit points per wave (= kWave of the partial layout)
-constexpr int kFQueue = 128;    // survivor ring per warp (<= 31 + 64 pending)
-constexpr int kFExact = 64;     // deferred exact pairs per warp (<= 31 + 32 pending)
+constexpr int kFExact = 128;    // deferred exact pairs per warp (<= 31 + 64 pending)
 constexpr int kFMaxFrag = kFWave + kFWarps;
 constexpr uint32_t kFNone = 0xffffffffu;
 
@@ -329,15 +328,15 @@ struct FineLayout {
   static constexpr size_t kAccBytes = (size_t)kFWave * PS * sizeof(double);  // per-hp sums over windows
   static constexpr int kMinBlocks = NC <= 8 ? 2 : 1;
   // dynamic shared memory: records (64 B per candidate) + slots + fragments
-  // (2 CTAs per SM: 228 KB - 2 x (1 KB reserved + ~3 KB static) per CTA)
-  static constexpr size_t kBudget = NC <= 8 ? (size_t)106 * 1024 : (size_t)212 * 1024;
+  // (2 CTAs per SM: 228 KB - 2 x (1 KB reserved + ~2.3 KB static) per CTA)
+  static constexpr size_t kBudget = NC <= 8 ? (size_t)109 * 1024 : (size_t)218 * 1024;
   static constexpr uint32_t kChunk =
       (uint32_t)(((kBudget - kSlotBytes - kPrepBytes - kAccBytes) / 64) & ~(size_t)31);
   static constexpr size_t kDynBytes = (size_t)kChunk * 64 + kSlotBytes + kPrepBytes + kAccBytes;
 };
 
 struct FineState {
-  uint32_t qh, qt, eh, et;  // survivor ring and exact ring (warp-uniform)
+  uint32_t eh, et, pad0, pad1;  // exact ring (warp-uniform)
   uint32_t n_cand, n_exact, n_amb, n_acc;
 };
 
@@ -432,82 +431,6 @@ static __device__ __forceinline__ uint32_t fine_exact(const Hit &Hs, uint32_t r0
   return exact_pair_packed(Hs, a, b_old, c2_old, na, ns, guard);
 }
 
-// Decide up to 32 queued survivors (lane < n holds one), defer banded pairs to
-// the exact ring, accumulate the rest.
-template <int GMAX, int CH, bool PLANAR>
-static __device__ __forceinline__ void fine_flush(const GatherArgs &A, const HitV &K, const HitF &F,
-                                                  bool lo_zero, uint32_t n, uint32_t q, uint32_t ex,
-                                                  uint32_t slots, PackedCounts<GMAX> &cnt, double &p0,
-                                                  double &p1, double &p2, uint32_t r0, uint32_t r1,
-                                                  uint32_t r2, uint32_t r3, FineState &st) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t lt = (1u << lane) - 1u;
-  __syncwarp();
-  const bool have = (uint32_t)lane < n;
-  const uint32_t i = have ? lds_u32(q + ((st.qh + lane) & (kFQueue - 1)) * 4u) : 0u;
-  st.qh += n;
-  bool acc = false, cos_pos = false, need = false;
-  int sector = 0;
-  float4 pw = make_float4(0.f, 0.f, 0.f, 0.f);
-  double L = 0.0;
-  if (have) {
-    const float4 p = lds128_f(r0 + i * 16u);
-    const float4 B = lds128_f(r1 + i * 16u);
-    pw = lds128_f(r2 + i * 16u);
-    L = __longlong_as_double(((long long)__float_as_uint(B.w) << 32) | __float_as_uint(B.z));
-    if constexpr (PLANAR) {
-      // n = +z: y = (dx, dy) exactly; guard = p.n.z, cos_i = wi.z (finite flag)
-      const float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
-      const float yy = fmaf(dx, dx, dy * dy);
-      const float d2 = fmaf(dz, dz, yy);
-      need = !(d2 < F.lim_lo) || !(fabsf(dx) > F.band_y) || !(fabsf(dy) > F.band_y) ||
-             (__float_as_uint(pw.w) & 1u) == 0u;
-      const int quad = dx > 0.0f ? (dy > 0.0f ? 0 : 3) : (dy > 0.0f ? 1 : 2);
-      int ring = 0;
-      if (F.na > 1) {
-        const float qa = yy * F.qa_scale;
-        const float kq = rintf(qa);
-        need = need || (kq >= 1.0f && kq <= (float)(F.na - 1) && fabsf(qa - kq) < 1e-4f * (float)F.na);
-        ring = min((int)qa, F.na - 1);
-      }
-      sector = ring * 4 + quad;
-      cos_pos = !(B.y <= 0.0f);              // bsdf.cpp:56-58
-      acc = !need && !(B.x < F.guard_ceil);  // integrator.cpp:397
-    } else {
-      const float4 D = lds128_f(r3 + i * 16u);
-      float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
-      if (!lo_zero) {
-        dx -= F.clx;
-        dy -= F.cly;
-        dz -= F.clz;
-      }
-      const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      const float yu = fmaf(dx, F.ufx, fmaf(dy, F.ufy, dz * F.ufz));
-      const float yv = fmaf(dx, F.vfx, fmaf(dy, F.vfy, dz * F.vfz));
-      const float yy = fmaf(yu, yu, yv * yv);
-      const bool keep = yy <= F.lim_hi;  // disk (integrator.cpp:399): certain reject above
-      need = !(F.fast && d2 < F.lim_lo && yy < F.lim_lo);
-      need = !fast_sector(F, yu, yv, yy, sector) || need;
-      const float gd = fmaf(D.x, F.nfx, fmaf(D.y, F.nfy, B.x * F.nfz));
-      const float gb = 2e-6f * (fabsf(D.x * F.nfx) + fabsf(D.y * F.nfy) + fabsf(B.x * F.nfz)) + 1e-30f;
-      const bool guard_ok = !(gd < F.guard_f - gb);
-      need = need || (guard_ok && !(gd >= F.guard_f + gb));
-      const float ci = fmaf(D.z, F.nfx, fmaf(D.w, F.nfy, B.y * F.nfz));
-      const float cb = 2e-6f * (fabsf(D.z * F.nfx) + fabsf(D.w * F.nfy) + fabsf(B.y * F.nfz)) + 1e-30f;
-      need = (need || !(fabsf(ci) > cb)) && keep;
-      cos_pos = ci > 0.0f;
-      acc = !need && keep && guard_ok;
-    }
-  }
-  const uint32_t me = __ballot_sync(kFull, need);
-  if (me) {  // rare: banded pairs go to the exact ring
-    if (need) sts_u32(ex + ((st.et + __popc(me & lt)) & (kFExact - 1)) * 4u, i);
-    st.et += __popc(me);
-  }
-  st.n_acc += acc ? 1u : 0u;
-  fine_accumulate<GMAX, CH>(K, acc, cos_pos, sector, pw, L, slots, lane, cnt, p0, p1, p2);
-}
-
 // Exact (fp64) decision of up to 32 deferred pairs.
 template <int GMAX, int CH>
 static __device__ __forceinline__ void fine_exact_batch(const GatherArgs &A, const Hit &Hs, const HitV &K,
@@ -534,14 +457,77 @@ static __device__ __forceinline__ void fine_exact_batch(const GatherArgs &A, con
   __syncwarp();
 }
 
-// All candidates of one hit point inside the staged window: runs held by
-// lanes (lane j: smem start rs, length rl of run j).
+// Full fp32 evaluation of candidate i against the hit point (ball, depth,
+// guard, disk, sector, cos_i; integrator.cpp:394-401, gather.cpp:15-33).
+// acc: certainly accepted; need: inside an error band -> exact fp64 path.
+template <bool PLANAR>
+static __device__ __forceinline__ void fine_eval(const HitF &F, bool lo_zero, uint32_t max_depth, bool valid,
+                                                 uint32_t i, uint32_t r0, uint32_t r1, uint32_t r2,
+                                                 uint32_t r3, bool &acc, bool &need, bool &cos_pos,
+                                                 int &sector, float4 &pw, double &L) {
+  const float4 p = lds128_f(r0 + i * 16u);
+  const float4 B = lds128_f(r1 + i * 16u);
+  pw = lds128_f(r2 + i * 16u);
+  L = __longlong_as_double(((long long)__float_as_uint(B.w) << 32) | __float_as_uint(B.z));
+  const bool dep_ok = F.eye + __float_as_uint(p.w) <= max_depth;  // integrator.cpp:396
+  if constexpr (PLANAR) {
+    // n = +z: y = (dx, dy) exactly; guard = p.n.z, cos_i = wi.z (finite flag)
+    const float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
+    const float yy = fmaf(dx, dx, dy * dy);
+    const float d2 = fmaf(dz, dz, yy);
+    const bool maybe = valid && dep_ok && d2 <= F.lim_hi;  // photon_map.cpp:76 (certain reject above)
+    bool band = !(d2 < F.lim_lo) || !(fabsf(dx) > F.band_y) || !(fabsf(dy) > F.band_y) ||
+                (__float_as_uint(pw.w) & 1u) == 0u;
+    const int quad = dx > 0.0f ? (dy > 0.0f ? 0 : 3) : (dy > 0.0f ? 1 : 2);
+    int ring = 0;
+    if (F.na > 1) {
+      const float qa = yy * F.qa_scale;
+      const float kq = rintf(qa);
+      band = band || (kq >= 1.0f && kq <= (float)(F.na - 1) && fabsf(qa - kq) < 1e-4f * (float)F.na);
+      ring = min((int)qa, F.na - 1);
+    }
+    sector = ring * 4 + quad;
+    cos_pos = !(B.y <= 0.0f);                        // bsdf.cpp:56-58
+    need = maybe && band;
+    acc = maybe && !band && !(B.x < F.guard_ceil);   // integrator.cpp:397
+  } else {
+    const float4 D = lds128_f(r3 + i * 16u);
+    float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
+    if (!lo_zero) {
+      dx -= F.clx;
+      dy -= F.cly;
+      dz -= F.clz;
+    }
+    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float yu = fmaf(dx, F.ufx, fmaf(dy, F.ufy, dz * F.ufz));
+    const float yv = fmaf(dx, F.vfx, fmaf(dy, F.vfy, dz * F.vfz));
+    const float yy = fmaf(yu, yu, yv * yv);
+    const bool maybe = valid && dep_ok && d2 <= F.lim_hi && yy <= F.lim_hi;  // ball, disk
+    bool band = !(F.fast && d2 < F.lim_lo && yy < F.lim_lo);
+    band = !fast_sector(F, yu, yv, yy, sector) || band;
+    const float gd = fmaf(D.x, F.nfx, fmaf(D.y, F.nfy, B.x * F.nfz));
+    const float gb = 2e-6f * (fabsf(D.x * F.nfx) + fabsf(D.y * F.nfy) + fabsf(B.x * F.nfz)) + 1e-30f;
+    const bool guard_ok = !(gd < F.guard_f - gb);
+    band = band || (guard_ok && !(gd >= F.guard_f + gb));
+    const float ci = fmaf(D.z, F.nfx, fmaf(D.w, F.nfy, B.y * F.nfz));
+    const float cb = 2e-6f * (fabsf(D.z * F.nfx) + fabsf(D.w * F.nfy) + fabsf(B.y * F.nfz)) + 1e-30f;
+    band = band || !(fabsf(ci) > cb);
+    cos_pos = ci > 0.0f;
+    need = maybe && band;
+    acc = maybe && !band && guard_ok;
+  }
+}
+
+// All candidates of one hit point inside the staged window, one per lane per
+// step (no compaction: at the fine boxes' pass rates a survivor queue costs
+// more than the idle lanes).  Runs are held by lanes (lane j: smem start rs,
+// length rl of run j).
 template <int GMAX, int CH, bool PLANAR>
 static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const Hit &Hs, uint32_t rs,
-                                                     uint32_t rl, int nruns, uint32_t q, uint32_t ex,
-                                                     uint32_t slots, PackedCounts<GMAX> &cnt, double &p0,
-                                                     double &p1, double &p2, uint32_t r0, uint32_t r1,
-                                                     uint32_t r2, uint32_t r3, FineState &st) {
+                                                     uint32_t rl, int nruns, uint32_t ex, uint32_t slots,
+                                                     PackedCounts<GMAX> &cnt, double &p0, double &p1,
+                                                     double &p2, uint32_t r0, uint32_t r1, uint32_t r2,
+                                                     uint32_t r3, FineState &st) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
   const HitF F = hitf(Hs, A.na, A.ns);
@@ -556,33 +542,32 @@ static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const 
     const uint32_t s0 = __shfl_sync(kFull, rs, j), n = __shfl_sync(kFull, rl, j);
     const uint32_t s1 = s0 + n;
     for (uint32_t base = s0; base < s1; base += 64) {
-      // ---- test: ball + depth (photon_map.cpp:76, integrator.cpp:396)
       const uint32_t i0 = base + lane, i1 = i0 + 32;
       const bool v0 = i0 < s1, v1 = i1 < s1;
-      const float4 a0 = lds128_f(r0 + (v0 ? i0 : base) * 16u);
-      const float4 a1 = lds128_f(r0 + (v1 ? i1 : base) * 16u);
-      const bool t0 = v0 && ball_pass(F, lo_zero, a0, max_depth);
-      const bool t1 = v1 && ball_pass(F, lo_zero, a1, max_depth);
+      bool acc0, need0, cp0, acc1, need1, cp1;
+      int sec0, sec1;
+      float4 pw0, pw1;
+      double L0, L1;
+      fine_eval<PLANAR>(F, lo_zero, max_depth, v0, v0 ? i0 : s0, r0, r1, r2, r3, acc0, need0, cp0, sec0,
+                        pw0, L0);
+      fine_eval<PLANAR>(F, lo_zero, max_depth, v1, v1 ? i1 : s0, r0, r1, r2, r3, acc1, need1, cp1, sec1,
+                        pw1, L1);
       st.n_cand += (v0 ? 1u : 0u) + (v1 ? 1u : 0u);
-      const uint32_t m0 = __ballot_sync(kFull, t0);
-      if (t0) sts_u32(q + ((st.qt + __popc(m0 & lt)) & (kFQueue - 1)) * 4u, i0);
-      st.qt += __popc(m0);
-      const uint32_t m1 = __ballot_sync(kFull, t1);
-      if (t1) sts_u32(q + ((st.qt + __popc(m1 & lt)) & (kFQueue - 1)) * 4u, i1);
-      st.qt += __popc(m1);
-      // ---- flush 32 survivors with every lane busy
-      while (st.qt - st.qh >= 32) {
-        fine_flush<GMAX, CH, PLANAR>(A, K, F, lo_zero, 32u, q, ex, slots, cnt, p0, p1, p2, r0, r1, r2,
-                                     r3, st);
-        if (st.et - st.eh >= 32)
+      st.n_acc += (acc0 ? 1u : 0u) + (acc1 ? 1u : 0u);
+      fine_accumulate<GMAX, CH>(K, acc0, cp0, sec0, pw0, L0, slots, lane, cnt, p0, p1, p2);
+      fine_accumulate<GMAX, CH>(K, acc1, cp1, sec1, pw1, L1, slots, lane, cnt, p0, p1, p2);
+      // banded pairs (rare) go to the exact ring
+      const uint32_t m0 = __ballot_sync(kFull, need0), m1 = __ballot_sync(kFull, need1);
+      if (m0 | m1) {
+        if (need0) sts_u32(ex + ((st.et + __popc(m0 & lt)) & (kFExact - 1)) * 4u, i0);
+        st.et += __popc(m0);
+        if (need1) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
+        st.et += __popc(m1);
+        while (st.et - st.eh >= 32)
           fine_exact_batch<GMAX, CH>(A, Hs, K, 32u, ex, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
       }
     }
   }
-  // ---- drain the survivors (< 32) and the exact ring
-  if (st.qt != st.qh)
-    fine_flush<GMAX, CH, PLANAR>(A, K, F, lo_zero, st.qt - st.qh, q, ex, slots, cnt, p0, p1, p2, r0, r1,
-                                 r2, r3, st);
   while (st.et != st.eh)
     fine_exact_batch<GMAX, CH>(A, Hs, K, min(32u, st.et - st.eh), ex, slots, cnt, p0, p1, p2, r0, r1, r2,
                                r3, st);
@@ -600,7 +585,6 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
   FinePrep *s_prep = reinterpret_cast<FinePrep *>(smem_raw + (size_t)CHUNK * 64 + Lay::kSlotBytes);
   double *s_acc =
       reinterpret_cast<double *>(smem_raw + (size_t)CHUNK * 64 + Lay::kSlotBytes + Lay::kPrepBytes);
-  __shared__ uint32_t s_q[kFWarps][kFQueue];
   __shared__ uint32_t s_ex[kFWarps][kFExact];
   __shared__ FineDesc s_desc;
   __shared__ __align__(8) uint64_t s_bar;
@@ -612,7 +596,7 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
   double *slots_p = s_slots + (size_t)warp * NC * 32 * 2;
   for (int i = lane; i < NC * 32 * 2; i += 32) slots_p[i] = 0.0;
   const uint32_t slots = smem_u32(slots_p);
-  const uint32_t qa = smem_u32(&s_q[warp][0]), exa = smem_u32(&s_ex[warp][0]);
+  const uint32_t exa = smem_u32(&s_ex[warp][0]);
   const uint32_t total_items = *T.total_items;
   const GridHeader g = *A.grid;
   if (threadIdx.x == 0) {
@@ -699,11 +683,9 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
         const bool planar = Hs.fast && Hs.nx == 0.0 && Hs.ny == 0.0 && Hs.nz == 1.0 && A.ns == 4 &&
                             Hs.clx == 0.0f && Hs.cly == 0.0f && Hs.clz == 0.0f;
         if (planar)
-          fine_fragment<GMAX, CH, true>(A, Hs, rs, rl, nr, qa, exa, slots, cnt, p0, p1, p2, r0, r1, r2, r3,
-                                        st);
+          fine_fragment<GMAX, CH, true>(A, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
         else
-          fine_fragment<GMAX, CH, false>(A, Hs, rs, rl, nr, qa, exa, slots, cnt, p0, p1, p2, r0, r1, r2,
-                                         r3, st);
+          fine_fragment<GMAX, CH, false>(A, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
 
         // ---- fixed-order reduction of the lane slots, added to the hp's sums
         const int col = lane % NC, grp = lane / NC;

@@ -2,6 +2,8 @@
 import time, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+import gc
+if os.environ.get("NOGC"): gc.disable()
 from paper_2504_04411_b200 import FppmContext, WORKLOADS
 wl = WORKLOADS["c2"]
 kern = sys.argv[1] if len(sys.argv) > 1 else "auto"
