@@ -99,6 +99,11 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+KERNEL_NAMES = {"auto": "k_gather_fine (gather + accumulate; F-test fused in k_tile_finalize)",
+                "fine": "k_gather_fine (gather + accumulate; F-test fused in k_tile_finalize)",
+                "tile": "k_gather_tiles", "lanes": "k_gather_lanes", "warp": "k_gather_test"}
+
+
 # ---------------------------------------------------------------- helpers
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -282,6 +287,7 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
     for s in range(args.warmup):
         step(s + 1, batches[s], False)
     torch.cuda.synchronize()
+    ctx.gather_kernel_ms()  # drop the warm-up launches
     if world > 1:
         dist.barrier()
     c0 = ctx.counters()
@@ -304,7 +310,8 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
     launches = FppmContext.kernel_launches() - l0
     c1 = ctx.counters()
     elapsed_ms = t_start.elapsed_time(t_end)
-    g_ms = [a.elapsed_time(b) for a, b in gather_ms]
+    call_ms = [a.elapsed_time(b) for a, b in gather_ms]  # whole gather_test call
+    g_ms = ctx.gather_kernel_ms()  # the dominant kernel alone (events in the library)
     q_local = c1["accepted"] - c0["accepted"]
     stats = torch.tensor([elapsed_ms, float(q_local), float(launches)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -363,10 +370,13 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
             "photons_per_s": wl.photons * args.steps / (elapsed_ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_gather_test (gather + fused F-test)",
+                         "kernel": KERNEL_NAMES.get(args.kernel, args.kernel),
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "bytes_formula": "16*Q + (64 + 48*G*C)*H (SURVEY.md 8d)",
                          "avg_launch_ms": gather_avg_s * 1e3, "launch_ms": [round(x, 3) for x in g_ms],
+                         "timing": "CUDA events around the kernel launch on the context stream "
+                                   "(fppm_gpu_gather_kernel_ms)",
+                         "gather_call_ms": statistics.mean(call_ms),
                          "share_of_step": gather_avg_s * 1e3 / (elapsed_ms / args.steps),
                          "peak_source": peak_src, "traffic_source": traffic_wl},
             "gpu_launches": launches,

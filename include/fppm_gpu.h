@@ -230,6 +230,10 @@ int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration,
 
 /* Cumulative counters of this context: [accepted, candidates, exact, ambiguous]. */
 int fppm_gpu_counters(fppm_gpu_ctx *ctx, uint64_t out[4]);
+/* Durations (ms, CUDA events on the context stream) of the dominant gather
+ * kernel of the gathers issued since the previous call (at most the last 64);
+ * waits for them to finish. *n receives the count written to out. */
+int fppm_gpu_gather_kernel_ms(fppm_gpu_ctx *ctx, float *out, uint32_t max, uint32_t *n);
 /* Kernel launches issued by this library since load (all contexts). */
 uint64_t fppm_gpu_kernel_launches(void);
 

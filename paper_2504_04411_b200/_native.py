@@ -151,6 +151,7 @@ _SIGS = [
     ("fppm_gpu_set_samples_per_iteration", C.c_int, [C.c_void_p, C.c_uint64]),
     ("fppm_gpu_end_iteration", C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(IterOut)]),
     ("fppm_gpu_kernel_launches", C.c_uint64, []),
+    ("fppm_gpu_gather_kernel_ms", C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.POINTER(C.c_uint32)]),
     ("fppm_gpu_counters", C.c_int, [C.c_void_p, C.c_void_p]),
     ("fppm_gpu_schedule_radius", C.c_double, [C.c_double, C.c_double, C.c_uint64]),
     ("fppm_gpu_f_quantile", C.c_double, [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int)]),

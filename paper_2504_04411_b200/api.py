@@ -158,6 +158,14 @@ class FppmContext:
     def kernel_launches() -> int:
         return int(N.lib().fppm_gpu_kernel_launches())
 
+    def gather_kernel_ms(self) -> list:
+        """Durations (ms) of the dominant gather kernel of the gathers issued
+        since the previous call (CUDA events on the context stream)."""
+        buf = (C.c_float * 64)()
+        n = C.c_uint32(0)
+        self._check(self._lib.fppm_gpu_gather_kernel_ms(self._h, buf, 64, C.byref(n)))
+        return [float(buf[i]) for i in range(n.value)]
+
     def device_view(self) -> dict:
         v = N.DeviceView()
         self._check(self._lib.fppm_gpu_device_view_get(self._h, C.byref(v)))

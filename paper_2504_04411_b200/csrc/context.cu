@@ -78,6 +78,10 @@ struct fppm_gpu_ctx {
 
   // tiled-gather schedule (home-cell items)
   fppm_b200::TileSched tile{};
+  // CUDA events around the dominant gather kernel of recent gathers (ring)
+  static constexpr int kEvRing = 64;
+  cudaEvent_t ev_k[kEvRing][2] = {};
+  uint32_t ev_head = 0, ev_count = 0;
   uint32_t *h_total = nullptr;
 };
 
@@ -388,6 +392,9 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
                   T.hp_map, T.nonempty};
   for (void *p : tdev)
     if (p) cudaFree(p);
+  for (auto &pr : ctx->ev_k)
+    for (cudaEvent_t e : pr)
+      if (e) cudaEventDestroy(e);
   if (ctx->h_total) cudaFreeHost(ctx->h_total);
   if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
   if (ctx->h_bounds_init) cudaFreeHost(ctx->h_bounds_init);
@@ -815,6 +822,33 @@ static int fill_summary(fppm_gpu_ctx *ctx, fppm_gpu_summary *sm) {
   return FPPM_OK;
 }
 
+// Bracket the dominant gather kernel with events (timed on its own stream).
+static int kernel_event(fppm_gpu_ctx *ctx, int which) {
+  const uint32_t slot = ctx->ev_head % fppm_gpu_ctx::kEvRing;
+  cudaEvent_t &e = ctx->ev_k[slot][which];
+  if (!e) FPPM_CUDA_OK(cudaEventCreate(&e));
+  FPPM_CUDA_OK(cudaEventRecord(e, ctx->stream));
+  if (which == 1) {
+    ctx->ev_head++;
+    if (ctx->ev_count < (uint32_t)fppm_gpu_ctx::kEvRing) ctx->ev_count++;
+  }
+  return FPPM_OK;
+}
+
+int fppm_gpu_gather_kernel_ms(fppm_gpu_ctx *ctx, float *out, uint32_t max, uint32_t *n) {
+  if (!ctx || (max && !out)) return FPPM_ERR_INVALID_ARGUMENT;
+  const uint32_t cnt = std::min(ctx->ev_count, max);
+  for (uint32_t i = 0; i < cnt; ++i) {
+    const uint32_t slot =
+        (ctx->ev_head + fppm_gpu_ctx::kEvRing - ctx->ev_count + i) % fppm_gpu_ctx::kEvRing;
+    FPPM_CUDA_OK(cudaEventSynchronize(ctx->ev_k[slot][1]));
+    FPPM_CUDA_OK(cudaEventElapsedTime(&out[i], ctx->ev_k[slot][0], ctx->ev_k[slot][1]));
+  }
+  if (n) *n = cnt;
+  ctx->ev_count = 0;
+  return FPPM_OK;
+}
+
 int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *out,
                          fppm_gpu_summary *summary) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
@@ -851,7 +885,9 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
   A.counters = ctx->d_counters; A.iter_tr = ctx->d_iter_tr; A.work = ctx->d_work;
   A.rmax_bits = ctx->d_rmax_bits;
   if (ctx->H && ctx->cfg.gather_kernel == 1) {
+    if ((rc = kernel_event(ctx, 0))) return rc;
     FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
+    if ((rc = kernel_event(ctx, 1))) return rc;
   } else if (ctx->H) {
     // ---- tiled path: bin hit points by home cell, build items, run
     TileSched &S = ctx->tile;
@@ -942,14 +978,18 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
       F.hp_map = S.hp_map;
       F.total_items = S.item_base + nb;
       T.desc = nullptr;
+      if ((rc = kernel_event(ctx, 0))) return rc;
       FPPM_CUDA_OK(launch_gather_fine(s, A, F, ctx->C, ctx->sms));
+      if ((rc = kernel_event(ctx, 1))) return rc;
     } else {
       FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms, chunk));
       T.desc = S.desc;
+      if ((rc = kernel_event(ctx, 0))) return rc;
       if (variant == 3)
         FPPM_CUDA_OK(launch_gather_lanes(s, A, T, ctx->C, ctx->sms));
       else
         FPPM_CUDA_OK(launch_gather_tiles(s, A, T, ctx->C, ctx->sms));
+      if ((rc = kernel_event(ctx, 1))) return rc;
     }
     FPPM_CUDA_OK(launch_tile_finalize(s, A, T, ctx->C, ctx->sms));
   }
