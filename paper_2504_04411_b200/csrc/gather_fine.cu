@@ -328,8 +328,8 @@ struct FineLayout {
   static constexpr size_t kAccBytes = (size_t)kFWave * PS * sizeof(double);  // per-hp sums over windows
   static constexpr int kMinBlocks = NC <= 8 ? 2 : 1;
   // dynamic shared memory: records (64 B per candidate) + slots + fragments
-  // (2 CTAs per SM: 228 KB - 2 x (1 KB reserved + ~2.3 KB static) per CTA)
-  static constexpr size_t kBudget = NC <= 8 ? (size_t)109 * 1024 : (size_t)218 * 1024;
+  // (2 CTAs per SM: 228 KB - 2 x (1 KB reserved + ~4.3 KB static) per CTA)
+  static constexpr size_t kBudget = NC <= 8 ? (size_t)108 * 1024 : (size_t)216 * 1024;
   static constexpr uint32_t kChunk =
       (uint32_t)(((kBudget - kSlotBytes - kPrepBytes - kAccBytes) / 64) & ~(size_t)31);
   static constexpr size_t kDynBytes = (size_t)kChunk * 64 + kSlotBytes + kPrepBytes + kAccBytes;
@@ -450,7 +450,6 @@ static __device__ __forceinline__ void fine_exact_batch(const GatherArgs &A, con
     fl = fine_exact(Hs, r0, r1, r2, r3, i, A.na, A.ns, A.guard, pw, L);
     st.n_exact += 1;
     st.n_amb += (fl >> 2) & 1u;
-    st.n_acc += fl & 1u;
   }
   fine_accumulate<GMAX, CH>(K, (fl & 1u) != 0, (fl & 2u) != 0, (int)(fl >> 8), pw, L, slots, lane, cnt, p0,
                             p1, p2);
@@ -480,7 +479,11 @@ static __device__ __forceinline__ void fine_eval(const HitF &F, bool lo_zero, ui
                 (__float_as_uint(pw.w) & 1u) == 0u;
     const int quad = dx > 0.0f ? (dy > 0.0f ? 0 : 3) : (dy > 0.0f ? 1 : 2);
     int ring = 0;
-    if (F.na > 1) {
+    if (F.na == 2) {  // one annulus edge at d2 = r2 / 2
+      const float qa = yy * F.qa_scale;
+      band = band || fabsf(qa - 1.0f) < 2e-4f;
+      ring = qa >= 1.0f ? 1 : 0;
+    } else if (F.na > 2) {
       const float qa = yy * F.qa_scale;
       const float kq = rintf(qa);
       band = band || (kq >= 1.0f && kq <= (float)(F.na - 1) && fabsf(qa - kq) < 1e-4f * (float)F.na);
@@ -538,34 +541,49 @@ static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const 
   K.gray = Hs.gray;
   const uint32_t max_depth = A.max_depth;
   const bool lo_zero = PLANAR || (F.clx == 0.0f && F.cly == 0.0f && F.clz == 0.0f);
-  for (int j = 0; j < nruns; ++j) {
-    const uint32_t s0 = __shfl_sync(kFull, rs, j), n = __shfl_sync(kFull, rl, j);
-    const uint32_t s1 = s0 + n;
-    for (uint32_t base = s0; base < s1; base += 64) {
-      const uint32_t i0 = base + lane, i1 = i0 + 32;
-      const bool v0 = i0 < s1, v1 = i1 < s1;
-      bool acc0, need0, cp0, acc1, need1, cp1;
-      int sec0, sec1;
-      float4 pw0, pw1;
-      double L0, L1;
-      fine_eval<PLANAR>(F, lo_zero, max_depth, v0, v0 ? i0 : s0, r0, r1, r2, r3, acc0, need0, cp0, sec0,
-                        pw0, L0);
-      fine_eval<PLANAR>(F, lo_zero, max_depth, v1, v1 ? i1 : s0, r0, r1, r2, r3, acc1, need1, cp1, sec1,
-                        pw1, L1);
-      st.n_cand += (v0 ? 1u : 0u) + (v1 ? 1u : 0u);
-      st.n_acc += (acc0 ? 1u : 0u) + (acc1 ? 1u : 0u);
-      fine_accumulate<GMAX, CH>(K, acc0, cp0, sec0, pw0, L0, slots, lane, cnt, p0, p1, p2);
-      fine_accumulate<GMAX, CH>(K, acc1, cp1, sec1, pw1, L1, slots, lane, cnt, p0, p1, p2);
-      // banded pairs (rare) go to the exact ring
-      const uint32_t m0 = __ballot_sync(kFull, need0), m1 = __ballot_sync(kFull, need1);
-      if (m0 | m1) {
-        if (need0) sts_u32(ex + ((st.et + __popc(m0 & lt)) & (kFExact - 1)) * 4u, i0);
-        st.et += __popc(m0);
-        if (need1) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
-        st.et += __popc(m1);
-        while (st.et - st.eh >= 32)
-          fine_exact_batch<GMAX, CH>(A, Hs, K, 32u, ex, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
-      }
+  // Runs are concatenated into one virtual index space [0, total) walked 64
+  // slots per step with no per-run tails: lane j holds the inclusive end
+  // `incl` of run j and the offset smem index - virtual index of that run.
+  uint32_t incl = rl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t off = rs - (incl - rl);
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  if (lane == 0) st.n_cand += total;
+  int jlo = 0;  // first run ending after `base` (warp-uniform)
+  for (uint32_t base = 0; base < total; base += 64) {
+    while (__shfl_sync(kFull, incl, jlo) <= base) ++jlo;
+    const uint32_t v0 = base + lane, v1 = v0 + 32;
+    int j0 = jlo, j1 = jlo;
+    for (int k = jlo; k < nruns; ++k) {  // run ends inside this step
+      const uint32_t e = __shfl_sync(kFull, incl, k);
+      if (e >= base + 64) break;
+      j0 += e <= v0 ? 1 : 0;
+      j1 += e <= v1 ? 1 : 0;
+    }
+    const bool ok0 = v0 < total, ok1 = v1 < total;
+    const uint32_t o0 = __shfl_sync(kFull, off, j0 & 31), o1 = __shfl_sync(kFull, off, j1 & 31);
+    const uint32_t i0 = ok0 ? v0 + o0 : rs, i1 = ok1 ? v1 + o1 : rs;
+    bool acc0, need0, cp0, acc1, need1, cp1;
+    int sec0, sec1;
+    float4 pw0, pw1;
+    double L0, L1;
+    fine_eval<PLANAR>(F, lo_zero, max_depth, ok0, i0, r0, r1, r2, r3, acc0, need0, cp0, sec0, pw0, L0);
+    fine_eval<PLANAR>(F, lo_zero, max_depth, ok1, i1, r0, r1, r2, r3, acc1, need1, cp1, sec1, pw1, L1);
+    fine_accumulate<GMAX, CH>(K, acc0, cp0, sec0, pw0, L0, slots, lane, cnt, p0, p1, p2);
+    fine_accumulate<GMAX, CH>(K, acc1, cp1, sec1, pw1, L1, slots, lane, cnt, p0, p1, p2);
+    // banded pairs (rare) go to the exact ring
+    const uint32_t m0 = __ballot_sync(kFull, need0), m1 = __ballot_sync(kFull, need1);
+    if (m0 | m1) {
+      if (need0) sts_u32(ex + ((st.et + __popc(m0 & lt)) & (kFExact - 1)) * 4u, i0);
+      st.et += __popc(m0);
+      if (need1) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
+      st.et += __popc(m1);
+      while (st.et - st.eh >= 32)
+        fine_exact_batch<GMAX, CH>(A, Hs, K, 32u, ex, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
     }
   }
   while (st.et != st.eh)
@@ -718,6 +736,12 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
         for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) {
           csum[2 * r] = __reduce_add_sync(kFull, cnt.w[r] & 0x00ff00ffu);
           csum[2 * r + 1] = __reduce_add_sync(kFull, (cnt.w[r] >> 8) & 0x00ff00ffu);
+        }
+        if (lane == 0) {
+          uint32_t tot = 0;
+#pragma unroll
+          for (int r = 0; r < 2 * PackedCounts<GMAX>::NP; ++r) tot += (csum[r] & 0xffffu) + (csum[r] >> 16);
+          st.n_acc += tot;
         }
         double *acc = s_acc + (size_t)k * PS;
         if (lane < NC) {
