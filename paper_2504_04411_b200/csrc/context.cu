@@ -343,6 +343,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->tile.sort.hist, radix_hist_entries((uint32_t)Hc)));
   A(dalloc(&ctx->tile.hp_map, 3 * Hc));
   A(dalloc(reinterpret_cast<char **>(&ctx->tile.fprep), fine_prep_bytes() * Hc));
+  A(dalloc(reinterpret_cast<char **>(&ctx->tile.fhot), fine_hot_bytes() * Hc));
   A(dalloc(&ctx->tile.nonempty, 1));
   A(cudaMallocHost(&ctx->h_total, 2 * sizeof(uint32_t)));
   if (e != cudaSuccess) {
@@ -388,7 +389,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
-                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.fdesc, T.fprep, T.pbase, T.partials,
+                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.fdesc, T.fprep, T.fhot, T.pbase, T.partials,
                   T.hp_map, T.nonempty};
   for (void *p : tdev)
     if (p) cudaFree(p);
@@ -916,12 +917,12 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
     if (variant == 4 && !fine_supported(ctx->G, ctx->C))
       return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "fine gather supports n_a*n_s*channels <= 24; "
                                                   "select gather_kernel 1-3");
-    const uint32_t chunk = variant == 4   ? fine_chunk(ctx->G, ctx->C)
-                           : variant == 3 ? (uint32_t)kLaneChunk
-                                          : (uint32_t)kChunk;
+    uint32_t cap64 = 0, cap48 = 0;
+    if (variant == 4) fine_caps(ctx->G, ctx->C, &cap64, &cap48);
+    const uint32_t chunk = variant == 3 ? (uint32_t)kLaneChunk : (uint32_t)kChunk;
     FPPM_CUDA_OK(cudaMemsetAsync(S.nonempty, 0, sizeof(uint32_t), s));
     if (variant == 4)
-      FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, chunk, &nb));
+      FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, cap64, cap48, &nb));
     else
       FPPM_CUDA_OK(tile_schedule_bins(s, A, S, g, ctx->sms, chunk, &nb));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
@@ -968,11 +969,11 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
     T.hp_map = S.hp_map;
     T.total_items = S.item_base + nb;
     if (variant == 4) {
-      FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, chunk));
-      FPPM_CUDA_OK(launch_fine_prep(s, A, S.hp_order, S.fprep, ctx->sms));
+      FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48));
       FineArgs F;
       F.desc = S.fdesc;
       F.prep = static_cast<const FinePrep *>(S.fprep);
+      F.hot = static_cast<const FineHot *>(S.fhot);
       F.hp_order = S.hp_order;
       F.partials = S.partials;
       F.hp_map = S.hp_map;

@@ -100,23 +100,28 @@ struct SortScratch {
 };
 
 // ---- fine-cell tiled gather (gather_fine.cu)
-constexpr int kFMaxPieces = 12;
-constexpr uint32_t kFineS = 4;  // fine cells per reference cell and axis (slab layout)
+#ifndef FPPM_FINE_S
+#define FPPM_FINE_S 4
+#endif
+constexpr uint32_t kFineS = FPPM_FINE_S;  // fine cells per reference cell and axis (slab layout)
+constexpr int kFMaxPieces = 3 * (int)kFineS > 9 ? 3 * (int)kFineS : 9;  // slab rows / 3x3 columns
+static_assert(kFMaxPieces <= 32, "one lane per run");
 constexpr uint32_t kFSub = 16;   // windows per item (one CTA walks them in order)
-struct FineDesc {  // 160 B, one per (home cell, wave, run of <= kFSub windows)
+struct alignas(16) FineDesc {  // one per (home cell, wave, run of <= kFSub windows)
   uint32_t hp_lo, hp_n, nwin, npieces;
   uint32_t c0, c1, pbase, pad0;     // windows [c0, c1) of the union; partial rows pbase + k
   int32_t ux0, ux1, uy0, uy1, uz0, uz1;  // union of the wave's fine boxes
   uint32_t src[kFMaxPieces];        // first sorted record of piece p
-  uint32_t pre[kFMaxPieces + 1];    // flattened offset of piece p (pre[12] = union size)
-  uint32_t pad[1];
+  uint32_t pre[kFMaxPieces + 1];    // flattened offset of piece p (pre[max] = union size)
 };
-static_assert(sizeof(FineDesc) == 160, "FineDesc layout");
+static_assert(sizeof(FineDesc) % 16 == 0 && sizeof(FineDesc) / 4 <= 256, "FineDesc layout");
 
 struct FinePrep;  // gather_fine.cu (per hit point state in wave order)
+struct FineHot;   // compact per hit point state staged per item
 struct FineArgs {
   const FineDesc *desc;
   const FinePrep *prep;
+  const FineHot *hot;
   const uint32_t *hp_order;
   double *partials;
   const uint32_t *hp_map;
@@ -127,6 +132,7 @@ struct TileSched {
   FineDesc *fdesc = nullptr;
   unsigned long long fdesc_cap = 0;
   void *fprep = nullptr;  // FinePrep[H]
+  void *fhot = nullptr;   // FineHot[H]
   uint32_t *pbase = nullptr;  // [nb + 1] partial rows per bucket, scanned
   SortScratch sort;     // hit-point keys (capacity H)
   uint32_t *hp_order;   // alias of the sorted values
@@ -162,16 +168,15 @@ cudaError_t launch_bucket_start(cudaStream_t s, const uint32_t *skeys, uint32_t 
 cudaError_t launch_exclusive_scan(cudaStream_t s, const uint32_t *in, uint32_t n, uint32_t *tmp,
                                   uint32_t *out);
 bool fine_supported(int G, int C);
-uint32_t fine_chunk(int G, int C);
+void fine_caps(int G, int C, uint32_t *cap64, uint32_t *cap48);
 cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
-                               int sms, uint32_t chunk, uint32_t *nb_out);
+                               int sms, uint32_t cap64, uint32_t cap48, uint32_t *nb_out);
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
-                                uint32_t chunk);
+                                uint32_t cap64, uint32_t cap48);
 size_t fine_acc_doubles(int G, int C);
 cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms);
 size_t fine_prep_bytes();
-cudaError_t launch_fine_prep(cudaStream_t s, const GatherArgs &A, const uint32_t *hp_order, void *prep,
-                             int sms);
+size_t fine_hot_bytes();
 
 cudaError_t launch_gather_test(cudaStream_t s, const GatherArgs &A, int C, int sms);
 cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2 *y,

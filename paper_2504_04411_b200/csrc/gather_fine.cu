@@ -33,7 +33,13 @@
 
 namespace fppm_b200 {
 
-constexpr int kFWarps = 8;
+#ifndef FPPM_EXPERIMENT
+#define FPPM_EXPERIMENT 0
+#endif
+#ifndef FPPM_FINE_WARPS
+#define FPPM_FINE_WARPS 8
+#endif
+constexpr int kFWarps = FPPM_FINE_WARPS;
 constexpr int kFThreads = kFWarps * kWarp;
 constexpr int kFWave = 32;      // hit points per wave (= kWave of the partial layout)
 constexpr int kFExact = 128;    // deferred exact pairs per warp (<= 31 + 64 pending)
@@ -127,6 +133,71 @@ static __device__ __forceinline__ int run_count(const GridHeader &g, const FBox 
   return g.S > 1 ? b.x1 - b.x0 + 1 : (b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1);
 }
 
+struct __align__(16) FinePrep {
+  Hit h;
+  int32_t bx0, bx1, by0, by1, bz0, bz1;  // fine box (fine_box)
+  uint32_t nruns, pad;
+  uint2 run[kFMaxPieces];  // sorted-record range [begin, end) of each run
+};
+static_assert(sizeof(FinePrep) % 16 == 0, "FinePrep must be a multiple of 16 B (TMA)");
+
+// Compact per-hit-point state staged in shared memory per item (the full
+// Hit stays in global memory for the exact path).
+struct alignas(16) FineHot {
+  HitF F;
+  double K0, K1, K2;
+  uint32_t planar, gray;
+  int32_t bx0, by0, by1;
+  uint32_t nruns;
+  uint2 run[kFMaxPieces];
+};
+static_assert(sizeof(FineHot) % 16 == 0, "FineHot must be a multiple of 16 B (TMA)");
+
+// Per hit point, once per gather, in wave order (position in hp_order): the
+// full Hit state, its fine box and the sorted-record range of each run.
+__global__ void k_fine_prep(const GatherArgs A, const uint32_t *__restrict__ hp_order,
+                            FinePrep *__restrict__ prep, FineHot *__restrict__ hot) {
+  const GridHeader g = *A.grid;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.H; i += gridDim.x * blockDim.x) {
+    const uint32_t h = hp_order[i];
+    FinePrep P;
+    make_hit(A, h, P.h);
+    FBox b = {0, -1, 0, -1, 0, -1};
+    const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
+    const bool ok = gathered && fine_box(g, P.h.cx, P.h.cy, P.h.cz, P.h.r, b);
+    const int nr = ok ? run_count(g, b) : 0;
+    P.bx0 = b.x0; P.bx1 = b.x1; P.by0 = b.y0; P.by1 = b.y1; P.bz0 = b.z0; P.bz1 = b.z1;
+    P.nruns = (uint32_t)nr;
+    P.pad = 0;
+    const FBox none = {0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < kFMaxPieces; ++j) {
+      uint2 r = make_uint2(0u, 0u);
+      if (j < nr) {
+        unsigned long long k0, k1;
+        (void)run_keys(g, none, b, j, k0, k1);
+        r = make_uint2(A.cell_start[k0], A.cell_start[k1 + 1]);
+      }
+      P.run[j] = r;
+    }
+    prep[i] = P;
+    FineHot Q;
+    Q.F = hitf(P.h, A.na, A.ns);
+    Q.K0 = P.h.K0;
+    Q.K1 = P.h.K1;
+    Q.K2 = P.h.K2;
+    // n = +z, fp32-exact center, 4 bins: the planar fast path (gather_dev.cuh)
+    Q.planar = (P.h.fast && P.h.nx == 0.0 && P.h.ny == 0.0 && P.h.nz == 1.0 && A.ns == 4 &&
+                P.h.clx == 0.0f && P.h.cly == 0.0f && P.h.clz == 0.0f) ? 1u : 0u;
+    Q.gray = P.h.gray ? 1u : 0u;
+    Q.bx0 = b.x0;
+    Q.by0 = b.y0;
+    Q.by1 = b.y1;
+    Q.nruns = (uint32_t)nr;
+    for (int j = 0; j < kFMaxPieces; ++j) Q.run[j] = P.run[j];
+    hot[i] = Q;
+  }
+}
+
 // ------------------------------------------------------------------ scheduling
 // bucket = home reference cell in the table's reference box extended by one
 // cell on every side; key n_ext = "no candidates" (outside / not gathered /
@@ -192,10 +263,18 @@ static __device__ bool wave_union(const GatherArgs &A, const GridHeader &g, cons
 
 // per bucket: items (runs of <= kFSub windows of ceil(union / chunk)) and
 // partial rows (items x wave size)
+// window capacity of a wave: 48-B records when every member takes the planar
+// path (rec3 is then read from global memory on the exact path only)
+static __device__ __forceinline__ bool wave_planar(const FineHot *hot, uint32_t b0, uint32_t n) {
+  for (uint32_t j = 0; j < n; ++j)
+    if (!hot[b0 + j].planar) return false;
+  return true;
+}
+
 __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
-                             const uint32_t *__restrict__ hp_order, uint32_t *__restrict__ items,
-                             uint32_t *__restrict__ prows, uint32_t chunk,
-                             uint32_t *__restrict__ nonempty) {
+                             const uint32_t *__restrict__ hp_order, const FineHot *__restrict__ hot,
+                             uint32_t *__restrict__ items, uint32_t *__restrict__ prows, uint32_t cap64,
+                             uint32_t cap48, uint32_t *__restrict__ nonempty) {
   const GridHeader g = *A.grid;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
     const uint32_t h0 = b < nb ? hp_start[b] : 0u;
@@ -214,6 +293,7 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
           T += A.cell_start[k1 + 1] - A.cell_start[k0];
         }
       }
+      const uint32_t chunk = wave_planar(hot, h0 + w * kFWave, n) ? cap48 : cap64;
       const uint32_t nwin = T == 0 ? 1u : (T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
       it += nsub;
@@ -225,9 +305,10 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
 }
 
 __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
-                            const uint32_t *__restrict__ hp_order, const uint32_t *__restrict__ item_base,
+                            const uint32_t *__restrict__ hp_order, const FineHot *__restrict__ hot,
+                            const uint32_t *__restrict__ item_base,
                             const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
-                            uint32_t *__restrict__ hp_map, uint32_t chunk) {
+                            uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48) {
   const GridHeader g = *A.grid;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
     const uint32_t h0 = hp_start[b], nhp = hp_start[b + 1] - h0;
@@ -256,8 +337,9 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
       }
       d.pre[kFMaxPieces] = T;
       d.npieces = (uint32_t)np;
-      d.pad0 = 0;
-      d.pad[0] = 0;
+      const bool planar = wave_planar(hot, d.hp_lo, n);
+      const uint32_t chunk = planar ? cap48 : cap64;
+      d.pad0 = planar ? 1u : 0u;  // flags: bit0 = 48-B records (no rec3 staged)
       d.ux0 = u.x0; d.ux1 = u.x1; d.uy0 = u.y0; d.uy1 = u.y1; d.uz0 = u.z0; d.uz1 = u.z1;
       const uint32_t nwin = T == 0 ? 1u : (T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
@@ -279,44 +361,6 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
   }
 }
 
-struct __align__(16) FinePrep {
-  Hit h;
-  int32_t bx0, bx1, by0, by1, bz0, bz1;  // fine box (fine_box)
-  uint32_t nruns, pad;
-  uint2 run[kFMaxPieces];  // sorted-record range [begin, end) of each run
-};
-static_assert(sizeof(FinePrep) % 16 == 0, "FinePrep must be a multiple of 16 B (TMA)");
-
-// Per hit point, once per gather, in wave order (position in hp_order): the
-// full Hit state, its fine box and the sorted-record range of each run.
-__global__ void k_fine_prep(const GatherArgs A, const uint32_t *__restrict__ hp_order,
-                            FinePrep *__restrict__ prep) {
-  const GridHeader g = *A.grid;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.H; i += gridDim.x * blockDim.x) {
-    const uint32_t h = hp_order[i];
-    FinePrep P;
-    make_hit(A, h, P.h);
-    FBox b = {0, -1, 0, -1, 0, -1};
-    const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
-    const bool ok = gathered && fine_box(g, P.h.cx, P.h.cy, P.h.cz, P.h.r, b);
-    const int nr = ok ? run_count(g, b) : 0;
-    P.bx0 = b.x0; P.bx1 = b.x1; P.by0 = b.y0; P.by1 = b.y1; P.bz0 = b.z0; P.bz1 = b.z1;
-    P.nruns = (uint32_t)nr;
-    P.pad = 0;
-    const FBox none = {0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < kFMaxPieces; ++j) {
-      uint2 r = make_uint2(0u, 0u);
-      if (j < nr) {
-        unsigned long long k0, k1;
-        (void)run_keys(g, none, b, j, k0, k1);
-        r = make_uint2(A.cell_start[k0], A.cell_start[k1 + 1]);
-      }
-      P.run[j] = r;
-    }
-    prep[i] = P;
-  }
-}
-
 // ------------------------------------------------------------------ kernel
 template <int GMAX, int CH>
 struct FineLayout {
@@ -324,15 +368,18 @@ struct FineLayout {
   static constexpr int NQ = 32 / NC;                    // lane groups in the slot reduction
   static constexpr int PS = partial_size(GMAX, CH);
   static constexpr size_t kSlotBytes = (size_t)kFWarps * NC * 32 * 16;
-  static constexpr size_t kPrepBytes = (size_t)kFWave * sizeof(FinePrep);
-  static constexpr size_t kAccBytes = (size_t)kFWave * PS * sizeof(double);  // per-hp sums over windows
+  static constexpr size_t kHotBytes = (size_t)kFWave * sizeof(FineHot);
   static constexpr int kMinBlocks = NC <= 8 ? 2 : 1;
-  // dynamic shared memory: records (64 B per candidate) + slots + fragments
-  // (2 CTAs per SM: 228 KB - 2 x (1 KB reserved + ~4.3 KB static) per CTA)
-  static constexpr size_t kBudget = NC <= 8 ? (size_t)108 * 1024 : (size_t)216 * 1024;
-  static constexpr uint32_t kChunk =
-      (uint32_t)(((kBudget - kSlotBytes - kPrepBytes - kAccBytes) / 64) & ~(size_t)31);
-  static constexpr size_t kDynBytes = (size_t)kChunk * 64 + kSlotBytes + kPrepBytes + kAccBytes;
+  // dynamic shared memory: records + lane slots + staged hit points;
+  // kMinBlocks CTAs share the SM's 228 KB, each with 1 KB reserved and the
+  // static arrays of the kernel
+  static constexpr size_t kStatic = (size_t)kFWarps * kFExact * 4 + 2 * sizeof(FineDesc) + 64;
+  static constexpr size_t kBudget = (size_t)233472 / kMinBlocks - 1024 - kStatic - 256;
+  static constexpr size_t kRecBytes = kBudget - kSlotBytes - kHotBytes;
+  // window capacity: 64 B per candidate, or 48 B for planar waves (no rec3)
+  static constexpr uint32_t kCap64 = (uint32_t)((kRecBytes / 64) & ~(size_t)31);
+  static constexpr uint32_t kCap48 = (uint32_t)((kRecBytes / 48) & ~(size_t)31);
+  static constexpr size_t kDynBytes = kRecBytes + kSlotBytes + kHotBytes;
 };
 
 struct FineState {
@@ -343,6 +390,7 @@ struct FineState {
 // Per-hit-point weights held in registers for the fragment.
 struct HitV {
   double K0, K1, K2;
+  double Kz, Kz0, Kz1, Kz2;  // value of an accepted pair with cos_i <= 0 (K * 0: NaN for inf K)
   bool gray;
 };
 
@@ -383,29 +431,40 @@ static __device__ __forceinline__ void sts_f64x2(uint32_t addr, double2 v) {
 
 // Value of an accepted pair (integrator.cpp:445-451, gather.cpp:59-67) added
 // to the lane's (sector, lane) slot; flux sums; packed sector counts.
+// Branch-free: a lane without an accepted pair adds zeros to a valid slot.
 // slots = shared address of this warp's [C][GMAX][32] {sum, sum_sq} slots.
-template <int GMAX, int CH>
+// GRAY: K0 = K1 = K2, so lum(K * pow) is taken as K0 * lum(pow) with the
+// photon luminance precomputed in fp64 (same value to ~1 ulp).
+template <int GMAX, int CH, bool GRAY>
 static __device__ __forceinline__ void fine_accumulate(const HitV &K, bool acc, bool cos_pos, int sector,
                                                        float4 pw, double L, uint32_t slots, int lane,
                                                        PackedCounts<GMAX> &cnt, double &p0, double &p1,
                                                        double &p2) {
-  if (!acc) return;
-  const double pr = cos_pos ? (double)pw.x : 0.0, pg = cos_pos ? (double)pw.y : 0.0,
-               pb = cos_pos ? (double)pw.z : 0.0;
+  const bool on = acc && cos_pos;
+  const double pr = (double)(on ? pw.x : 0.0f), pg = (double)(on ? pw.y : 0.0f),
+               pb = (double)(on ? pw.z : 0.0f);
   p0 += pr;
   p1 += pg;
   p2 += pb;
-  pk_add<GMAX>(cnt, sector);
+  if (acc) pk_add<GMAX>(cnt, sector);
   if constexpr (CH == 1) {
-    const double v = K.gray ? (cos_pos ? dm(K.K0, L) : 0.0)
-                            : elum(dm(K.K0, pr), dm(K.K1, pg), dm(K.K2, pb));
+    double v;
+    if constexpr (GRAY) {
+      const double kv = cos_pos ? dm(K.K0, L) : K.Kz;  // bsdf.cpp:58: f = 0 when cos_i <= 0
+      v = acc ? kv : 0.0;
+    } else {
+      const double kv = cos_pos ? elum(dm(K.K0, pr), dm(K.K1, pg), dm(K.K2, pb)) : K.Kz;
+      v = acc ? kv : 0.0;
+    }
     const uint32_t a = slots + (uint32_t)(sector * 32 + lane) * 16u;
     double2 o = lds_f64x2(a);
     o.x += v;
     o.y += v * v;
     sts_f64x2(a, o);
   } else {
-    const double v[3] = {dm(K.K0, pr), dm(K.K1, pg), dm(K.K2, pb)};
+    const double v[3] = {acc ? (cos_pos ? dm(K.K0, pr) : K.Kz0) : 0.0,
+                         acc ? (cos_pos ? dm(K.K1, pg) : K.Kz1) : 0.0,
+                         acc ? (cos_pos ? dm(K.K2, pb) : K.Kz2) : 0.0};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const uint32_t a = slots + (uint32_t)((c * GMAX + sector) * 32 + lane) * 16u;
@@ -417,13 +476,29 @@ static __device__ __forceinline__ void fine_accumulate(const HitV &K, bool acc, 
   }
 }
 
+// Where the staged window lives: smem addresses of the record arrays and,
+// for 48-B windows, how to find rec3 of a candidate in global memory.
+struct FineWin {
+  uint32_t r0, r1, r2, r3;  // r3 = 0: rec3 not staged
+  uint32_t lo;               // window start in the union's flattened order
+  const FineDesc *d;
+  const float4 *grec3;
+};
+
 // One fp64-exact evaluation of a deferred pair (fine record layout -> the
 // tile layout expected by exact_pair).
-static __device__ __forceinline__ uint32_t fine_exact(const Hit &Hs, uint32_t r0, uint32_t r1, uint32_t r2,
-                                                      uint32_t r3, uint32_t i, int na, int ns,
-                                                      double guard, float4 &pw, double &L) {
-  const float4 a = lds128_f(r0 + i * 16u), B = lds128_f(r1 + i * 16u), Cc = lds128_f(r2 + i * 16u),
-               D = lds128_f(r3 + i * 16u);
+static __device__ __forceinline__ uint32_t fine_exact(const Hit &Hs, const FineWin &Wn, uint32_t i, int na,
+                                                      int ns, double guard, float4 &pw, double &L) {
+  const float4 a = lds128_f(Wn.r0 + i * 16u), B = lds128_f(Wn.r1 + i * 16u), Cc = lds128_f(Wn.r2 + i * 16u);
+  float4 D;
+  if (Wn.r3) {
+    D = lds128_f(Wn.r3 + i * 16u);
+  } else {  // flattened position -> piece -> sorted record
+    const uint32_t f = i + Wn.lo;
+    uint32_t p = 0;
+    while (p + 1 < Wn.d->npieces && Wn.d->pre[p + 1] <= f) ++p;
+    D = Wn.grec3[Wn.d->src[p] + (f - Wn.d->pre[p])];
+  }
   pw = Cc;
   L = __longlong_as_double(((long long)__float_as_uint(B.w) << 32) | __float_as_uint(B.z));
   const float4 b_old = make_float4(D.x, D.y, B.x, D.z);
@@ -431,13 +506,11 @@ static __device__ __forceinline__ uint32_t fine_exact(const Hit &Hs, uint32_t r0
   return exact_pair_packed(Hs, a, b_old, c2_old, na, ns, guard);
 }
 
-// Exact (fp64) decision of up to 32 deferred pairs.
-template <int GMAX, int CH>
+template <int GMAX, int CH, bool GRAY>
 static __device__ __forceinline__ void fine_exact_batch(const GatherArgs &A, const Hit &Hs, const HitV &K,
                                                      uint32_t n, uint32_t ex, uint32_t slots,
                                                      PackedCounts<GMAX> &cnt, double &p0, double &p1,
-                                                     double &p2, uint32_t r0, uint32_t r1, uint32_t r2,
-                                                     uint32_t r3, FineState &st) {
+                                                     double &p2, const FineWin &Wn, FineState &st) {
   const int lane = threadIdx.x & 31;
   __syncwarp();
   const bool have = (uint32_t)lane < n;
@@ -447,12 +520,12 @@ static __device__ __forceinline__ void fine_exact_batch(const GatherArgs &A, con
   double L = 0.0;
   uint32_t fl = 0;
   if (have) {
-    fl = fine_exact(Hs, r0, r1, r2, r3, i, A.na, A.ns, A.guard, pw, L);
+    fl = fine_exact(Hs, Wn, i, A.na, A.ns, A.guard, pw, L);
     st.n_exact += 1;
     st.n_amb += (fl >> 2) & 1u;
   }
-  fine_accumulate<GMAX, CH>(K, (fl & 1u) != 0, (fl & 2u) != 0, (int)(fl >> 8), pw, L, slots, lane, cnt, p0,
-                            p1, p2);
+  fine_accumulate<GMAX, CH, GRAY>(K, (fl & 1u) != 0, (fl & 2u) != 0, (int)(fl >> 8), pw, L, slots, lane, cnt,
+                                  p0, p1, p2);
   __syncwarp();
 }
 
@@ -525,20 +598,25 @@ static __device__ __forceinline__ void fine_eval(const HitF &F, bool lo_zero, ui
 // step (no compaction: at the fine boxes' pass rates a survivor queue costs
 // more than the idle lanes).  Runs are held by lanes (lane j: smem start rs,
 // length rl of run j).
-template <int GMAX, int CH, bool PLANAR>
-static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const Hit &Hs, uint32_t rs,
-                                                     uint32_t rl, int nruns, uint32_t ex, uint32_t slots,
-                                                     PackedCounts<GMAX> &cnt, double &p0, double &p1,
-                                                     double &p2, uint32_t r0, uint32_t r1, uint32_t r2,
-                                                     uint32_t r3, FineState &st) {
+template <int GMAX, int CH, bool PLANAR, bool GRAY>
+static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const FineHot &Hh, const Hit &Hs,
+                                                     uint32_t rs, uint32_t rl, int nruns, uint32_t ex,
+                                                     uint32_t slots, PackedCounts<GMAX> &cnt, double &p0,
+                                                     double &p1, double &p2, const FineWin &Wn,
+                                                     FineState &st) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  const HitF F = hitf(Hs, A.na, A.ns);
+  const HitF F = Hh.F;
+  const uint32_t r0 = Wn.r0, r1 = Wn.r1, r2 = Wn.r2, r3 = Wn.r3;
   HitV K;
-  K.K0 = Hs.K0;
-  K.K1 = Hs.K1;
-  K.K2 = Hs.K2;
-  K.gray = Hs.gray;
+  K.K0 = Hh.K0;
+  K.K1 = Hh.K1;
+  K.K2 = Hh.K2;
+  K.gray = GRAY;
+  K.Kz0 = dm(Hh.K0, 0.0);
+  K.Kz1 = dm(Hh.K1, 0.0);
+  K.Kz2 = dm(Hh.K2, 0.0);
+  K.Kz = elum(K.Kz0, K.Kz1, K.Kz2);
   const uint32_t max_depth = A.max_depth;
   const bool lo_zero = PLANAR || (F.clx == 0.0f && F.cly == 0.0f && F.clz == 0.0f);
   // Runs are concatenated into one virtual index space [0, total) walked 64
@@ -571,10 +649,24 @@ static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const 
     int sec0, sec1;
     float4 pw0, pw1;
     double L0, L1;
+#if FPPM_EXPERIMENT == 2  // timing experiment: loads only
+    {
+      const float4 q0 = lds128_f(r0 + i0 * 16u), q1 = lds128_f(r0 + i1 * 16u);
+      acc0 = ok0 && q0.x > F.chx; acc1 = ok1 && q1.x > F.chx;
+      need0 = need1 = false; cp0 = cp1 = true; sec0 = sec1 = 0;
+      pw0 = pw1 = make_float4(0.f, 0.f, 0.f, 0.f); L0 = L1 = 0.0;
+    }
+#else
     fine_eval<PLANAR>(F, lo_zero, max_depth, ok0, i0, r0, r1, r2, r3, acc0, need0, cp0, sec0, pw0, L0);
     fine_eval<PLANAR>(F, lo_zero, max_depth, ok1, i1, r0, r1, r2, r3, acc1, need1, cp1, sec1, pw1, L1);
-    fine_accumulate<GMAX, CH>(K, acc0, cp0, sec0, pw0, L0, slots, lane, cnt, p0, p1, p2);
-    fine_accumulate<GMAX, CH>(K, acc1, cp1, sec1, pw1, L1, slots, lane, cnt, p0, p1, p2);
+#endif
+#if FPPM_EXPERIMENT >= 1  // timing experiment: no accumulation
+    if (acc0) pk_add<GMAX>(cnt, sec0);
+    if (acc1) pk_add<GMAX>(cnt, sec1);
+#else
+    fine_accumulate<GMAX, CH, GRAY>(K, acc0, cp0, sec0, pw0, L0, slots, lane, cnt, p0, p1, p2);
+    fine_accumulate<GMAX, CH, GRAY>(K, acc1, cp1, sec1, pw1, L1, slots, lane, cnt, p0, p1, p2);
+#endif
     // banded pairs (rare) go to the exact ring
     const uint32_t m0 = __ballot_sync(kFull, need0), m1 = __ballot_sync(kFull, need1);
     if (m0 | m1) {
@@ -583,12 +675,11 @@ static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const 
       if (need1) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
       st.et += __popc(m1);
       while (st.et - st.eh >= 32)
-        fine_exact_batch<GMAX, CH>(A, Hs, K, 32u, ex, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
+        fine_exact_batch<GMAX, CH, GRAY>(A, Hs, K, 32u, ex, slots, cnt, p0, p1, p2, Wn, st);
     }
   }
   while (st.et != st.eh)
-    fine_exact_batch<GMAX, CH>(A, Hs, K, min(32u, st.et - st.eh), ex, slots, cnt, p0, p1, p2, r0, r1, r2,
-                               r3, st);
+    fine_exact_batch<GMAX, CH, GRAY>(A, Hs, K, min(32u, st.et - st.eh), ex, slots, cnt, p0, p1, p2, Wn, st);
   __syncwarp();
 }
 
@@ -597,173 +688,210 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
     k_gather_fine(const GatherArgs A, const FineArgs T) {
   using Lay = FineLayout<GMAX, CH>;
   constexpr int NC = Lay::NC, NQ = Lay::NQ, PS = Lay::PS;
-  constexpr uint32_t CHUNK = Lay::kChunk;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double *s_slots = reinterpret_cast<double *>(smem_raw + (size_t)CHUNK * 64);
-  FinePrep *s_prep = reinterpret_cast<FinePrep *>(smem_raw + (size_t)CHUNK * 64 + Lay::kSlotBytes);
-  double *s_acc =
-      reinterpret_cast<double *>(smem_raw + (size_t)CHUNK * 64 + Lay::kSlotBytes + Lay::kPrepBytes);
+  double *s_slots = reinterpret_cast<double *>(smem_raw + Lay::kRecBytes);
+  FineHot *s_hot = reinterpret_cast<FineHot *>(smem_raw + Lay::kRecBytes + Lay::kSlotBytes);
   __shared__ uint32_t s_ex[kFWarps][kFExact];
-  __shared__ FineDesc s_desc;
-  __shared__ __align__(8) uint64_t s_bar;
-  __shared__ uint32_t s_item, s_next;
+  __shared__ FineDesc s_descs[2];
+  __shared__ __align__(8) uint64_t s_bar, s_dbar[2];  // records; descriptor buffer 0 / 1
+  __shared__ uint32_t s_cur, s_next;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t r0 = smem_u32(smem_raw);
-  const uint32_t r1 = r0 + CHUNK * 16u, r2 = r1 + CHUNK * 16u, r3 = r2 + CHUNK * 16u;
   double *slots_p = s_slots + (size_t)warp * NC * 32 * 2;
   for (int i = lane; i < NC * 32 * 2; i += 32) slots_p[i] = 0.0;
   const uint32_t slots = smem_u32(slots_p);
   const uint32_t exa = smem_u32(&s_ex[warp][0]);
   const uint32_t total_items = *T.total_items;
   const GridHeader g = *A.grid;
+  // Items are claimed one ahead and their descriptors prefetched by TMA, so
+  // the work-counter atomic and the descriptor load overlap the current item.
+  uint32_t nxt = 0;
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
+    mbar_init(&s_dbar[0], 1);
+    mbar_init(&s_dbar[1], 1);
     fence_mbar_init();
+    const uint32_t first = atomicAdd(A.work, 1u);
+    if (first < total_items) {
+      mbar_arrive_expect_tx(&s_dbar[0], (uint32_t)sizeof(FineDesc));
+      bulk_g2s(&s_descs[0], T.desc + first, (uint32_t)sizeof(FineDesc), &s_dbar[0]);
+    }
+    s_cur = first;
+    nxt = atomicAdd(A.work, 1u);
   }
   __syncthreads();
-  uint32_t phase = 0;
+  uint32_t phase = 0, dphase = 0, b = 0;
   FineState st = {0, 0, 0, 0, 0, 0, 0, 0};
 
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(A.work, 1u);
-    __syncthreads();
-    const uint32_t item = s_item;
+    const uint32_t item = s_cur;
     if (item >= total_items) break;
-    if (threadIdx.x < sizeof(FineDesc) / 4)
-      reinterpret_cast<uint32_t *>(&s_desc)[threadIdx.x] =
-          reinterpret_cast<const uint32_t *>(T.desc + item)[threadIdx.x];
-    __syncthreads();
-    const uint32_t hp_n = s_desc.hp_n, Tu = s_desc.pre[kFMaxPieces];
-    double *out = T.partials + (size_t)s_desc.pbase * PS;
-    if (Tu == 0) {
-      // no candidates for this wave: zero partials
-      for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) out[i] = 0.0;
-      __syncthreads();
-      continue;
-    }
-    for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) s_acc[i] = 0.0;
-    // ---- the item's windows in order; per-hp sums accumulate in s_acc
-    for (uint32_t c = s_desc.c0; c < s_desc.c1; ++c) {
-      const uint32_t lo = c * CHUNK, hi = min(Tu, lo + CHUNK);
-      const uint32_t ncand = hi - lo;
-      if (threadIdx.x == 0) {
-        s_next = 0;
+    mbar_wait(&s_dbar[b], (dphase >> b) & 1u);
+    dphase ^= 1u << b;
+    const FineDesc &s_desc = s_descs[b];
+    uint32_t nxt2 = 0;
+    if (threadIdx.x == 0) {
+      if (nxt < total_items) {
         fence_proxy_async_smem();
-        const uint32_t prep_bytes = c == s_desc.c0 ? hp_n * (uint32_t)sizeof(FinePrep) : 0u;
-        mbar_arrive_expect_tx(&s_bar, ncand * 64u + prep_bytes);
-        if (prep_bytes) bulk_g2s(s_prep, T.prep + s_desc.hp_lo, prep_bytes, &s_bar);
-        for (uint32_t p = 0; p < s_desc.npieces; ++p) {
-          const uint32_t a = max(s_desc.pre[p], lo), e = min(s_desc.pre[p + 1], hi);
-          if (e <= a) continue;
-          const uint32_t src = s_desc.src[p] + (a - s_desc.pre[p]), dst = a - lo, n = e - a;
-          bulk_g2s(smem_raw + (size_t)dst * 16, A.rec0 + src, n * 16u, &s_bar);
-          bulk_g2s(smem_raw + (size_t)(CHUNK + dst) * 16, A.rec1 + src, n * 16u, &s_bar);
-          bulk_g2s(smem_raw + (size_t)(2 * CHUNK + dst) * 16, A.rec2 + src, n * 16u, &s_bar);
-          bulk_g2s(smem_raw + (size_t)(3 * CHUNK + dst) * 16, A.rec3 + src, n * 16u, &s_bar);
-        }
+        mbar_arrive_expect_tx(&s_dbar[b ^ 1u], (uint32_t)sizeof(FineDesc));
+        bulk_g2s(&s_descs[b ^ 1u], T.desc + nxt, (uint32_t)sizeof(FineDesc), &s_dbar[b ^ 1u]);
       }
-      mbar_wait(&s_bar, phase);
-      phase ^= 1u;
-
-      // ---- warps take whole hit points (one fragment per hit point and window)
-      for (;;) {
-        uint32_t k = 0;
-        if (lane == 0) k = atomicAdd(&s_next, 1u);
-        k = __shfl_sync(kFull, k, 0);
-        if (k >= hp_n) break;
-        const FinePrep &P = s_prep[k];
-        const Hit &Hs = P.h;
-        // runs of this hit point inside the window (lane j = run j)
-        const int nr = (int)P.nruns;
-        uint32_t rs = 0, rl = 0;
-        if (lane < nr) {
-          int pc;
-          if (g.S > 1) {
-            pc = P.bx0 + lane - s_desc.ux0;
-          } else {
-            const int nyb = P.by1 - P.by0 + 1, nyu = s_desc.uy1 - s_desc.uy0 + 1;
-            pc = (P.bx0 + lane / nyb - s_desc.ux0) * nyu + (P.by0 + lane % nyb - s_desc.uy0);
+      nxt2 = atomicAdd(A.work, 1u);  // consumed at the end of this item
+    }
+    const uint32_t hp_n = s_desc.hp_n, Tu = s_desc.pre[kFMaxPieces];
+    // per-hp sums over the item's windows accumulate in its partial rows
+    double *out = T.partials + (size_t)s_desc.pbase * PS;
+    for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) out[i] = 0.0;
+    __syncthreads();  // zeroed rows before any warp adds to them
+    if (Tu != 0) {
+      // window layout: 48-B records for planar waves (rec3 stays in HBM)
+      const bool r48 = (s_desc.pad0 & 1u) != 0;
+      const uint32_t cap = r48 ? Lay::kCap48 : Lay::kCap64;
+      FineWin Wn;
+      Wn.r0 = r0;
+      Wn.r1 = r0 + cap * 16u;
+      Wn.r2 = Wn.r1 + cap * 16u;
+      Wn.r3 = r48 ? 0u : Wn.r2 + cap * 16u;
+      Wn.d = &s_desc;
+      Wn.grec3 = A.rec3;
+      unsigned char *rec1 = smem_raw + (size_t)cap * 16, *rec2 = rec1 + (size_t)cap * 16,
+                    *rec3 = rec2 + (size_t)cap * 16;
+      // ---- the item's windows in order
+      for (uint32_t c = s_desc.c0; c < s_desc.c1; ++c) {
+        const uint32_t lo = c * cap, hi = min(Tu, lo + cap);
+        const uint32_t ncand = hi - lo;
+        Wn.lo = lo;
+        if (warp == 0) {
+          // lane 0 arms the barrier; lane p copies piece p, lane 31 the hit points
+          const uint32_t hot_bytes = c == s_desc.c0 ? hp_n * (uint32_t)sizeof(FineHot) : 0u;
+          if (lane == 0) {
+            s_next = 0;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&s_bar, ncand * (r48 ? 48u : 64u) + hot_bytes);
           }
-          const uint2 R = P.run[lane];
-          const uint32_t fa = s_desc.pre[pc] + (R.x - s_desc.src[pc]), fb = fa + (R.y - R.x);
-          const uint32_t ca = max(fa, lo), cb = min(fb, hi);
-          if (cb > ca) {
-            rs = ca - lo;
-            rl = cb - ca;
+          __syncwarp();
+          if (lane == 31 && hot_bytes) bulk_g2s(s_hot, T.hot + s_desc.hp_lo, hot_bytes, &s_bar);
+          if ((uint32_t)lane < s_desc.npieces) {
+            const uint32_t p = lane;
+            const uint32_t a = max(s_desc.pre[p], lo), e = min(s_desc.pre[p + 1], hi);
+            if (e > a) {
+              const uint32_t src = s_desc.src[p] + (a - s_desc.pre[p]), dst = a - lo, n = e - a;
+              bulk_g2s(smem_raw + (size_t)dst * 16, A.rec0 + src, n * 16u, &s_bar);
+              bulk_g2s(rec1 + (size_t)dst * 16, A.rec1 + src, n * 16u, &s_bar);
+              bulk_g2s(rec2 + (size_t)dst * 16, A.rec2 + src, n * 16u, &s_bar);
+              if (!r48) bulk_g2s(rec3 + (size_t)dst * 16, A.rec3 + src, n * 16u, &s_bar);
+            }
           }
         }
-        if (!__any_sync(kFull, rl != 0)) continue;
-        PackedCounts<GMAX> cnt;
-#pragma unroll
-        for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
-        double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-        const bool planar = Hs.fast && Hs.nx == 0.0 && Hs.ny == 0.0 && Hs.nz == 1.0 && A.ns == 4 &&
-                            Hs.clx == 0.0f && Hs.cly == 0.0f && Hs.clz == 0.0f;
-        if (planar)
-          fine_fragment<GMAX, CH, true>(A, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
-        else
-          fine_fragment<GMAX, CH, false>(A, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, r0, r1, r2, r3, st);
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
 
-        // ---- fixed-order reduction of the lane slots, added to the hp's sums
-        const int col = lane % NC, grp = lane / NC;
-        double sm = 0.0, sq = 0.0;
-        if (grp < NQ) {
-          // rows rotated by the column: the 16-B slots a warp touches per step
-          // fall in distinct bank groups (fixed order, so still deterministic)
-          constexpr int R = 32 / NQ;
-          const uint32_t base = slots + (uint32_t)(col * 32 + grp * R) * 16u;
+        // ---- warps take whole hit points (one fragment per hit point and window)
+        for (;;) {
+          uint32_t k = 0;
+          if (lane == 0) k = atomicAdd(&s_next, 1u);
+          k = __shfl_sync(kFull, k, 0);
+          if (k >= hp_n) break;
+          const FineHot &Hh = s_hot[k];
+          // runs of this hit point inside the window (lane j = run j)
+          const int nr = (int)Hh.nruns;
+          uint32_t rs = 0, rl = 0;
+          if (lane < nr) {
+            int pc;
+            if (g.S > 1) {
+              pc = Hh.bx0 + lane - s_desc.ux0;
+            } else {
+              const int nyb = Hh.by1 - Hh.by0 + 1, nyu = s_desc.uy1 - s_desc.uy0 + 1;
+              pc = (Hh.bx0 + lane / nyb - s_desc.ux0) * nyu + (Hh.by0 + lane % nyb - s_desc.uy0);
+            }
+            const uint2 R = Hh.run[lane];
+            const uint32_t fa = s_desc.pre[pc] + (R.x - s_desc.src[pc]), fb = fa + (R.y - R.x);
+            const uint32_t ca = max(fa, lo), cb = min(fb, hi);
+            if (cb > ca) {
+              rs = ca - lo;
+              rl = cb - ca;
+            }
+          }
+          if (!__any_sync(kFull, rl != 0)) continue;
+          const Hit &Hs = T.prep[s_desc.hp_lo + k].h;  // full state: exact path only
+          PackedCounts<GMAX> cnt;
+#pragma unroll
+          for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
+          double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+          if (Hh.planar && Hh.gray)
+            fine_fragment<GMAX, CH, true, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+          else if (Hh.planar)
+            fine_fragment<GMAX, CH, true, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+          else if (Hh.gray)
+            fine_fragment<GMAX, CH, false, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+          else
+            fine_fragment<GMAX, CH, false, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn,
+                                                  st);
+
+          // ---- fixed-order reduction of the lane slots, added to the hp's row
+          const int col = lane % NC, grp = lane / NC;
+          double sm = 0.0, sq = 0.0;
+          if (grp < NQ) {
+            // rows rotated by the column: the 16-B slots a warp touches per step
+            // fall in distinct bank groups (fixed order, so still deterministic)
+            constexpr int R = 32 / NQ;
+            const uint32_t base = slots + (uint32_t)(col * 32 + grp * R) * 16u;
 #pragma unroll 4
-          for (int i = 0; i < R; ++i) {
-            const uint32_t a = base + (uint32_t)((i + col) % R) * 16u;
-            const double2 v = lds_f64x2(a);
-            sm += v.x;
-            sq += v.y;
-            sts_f64x2(a, make_double2(0.0, 0.0));
+            for (int i = 0; i < R; ++i) {
+              const uint32_t a = base + (uint32_t)((i + col) % R) * 16u;
+              const double2 v = lds_f64x2(a);
+              sm += v.x;
+              sq += v.y;
+              sts_f64x2(a, make_double2(0.0, 0.0));
+            }
           }
-        }
 #pragma unroll
-        for (int o = (NQ / 2) * NC; o >= NC && o > 0; o >>= 1) {
-          sm += __shfl_down_sync(kFull, sm, o);
-          sq += __shfl_down_sync(kFull, sq, o);
-        }
-        p0 = warp_sum(p0);
-        p1 = warp_sum(p1);
-        p2 = warp_sum(p2);
-        // packed byte counts -> 16-bit halves -> warp sums (<= 32 * 255 per half)
-        uint32_t csum[2 * PackedCounts<GMAX>::NP];
+          for (int o = (NQ / 2) * NC; o >= NC && o > 0; o >>= 1) {
+            sm += __shfl_down_sync(kFull, sm, o);
+            sq += __shfl_down_sync(kFull, sq, o);
+          }
+          p0 = warp_sum(p0);
+          p1 = warp_sum(p1);
+          p2 = warp_sum(p2);
+          // packed byte counts -> 16-bit halves -> warp sums (<= 32 * 255 per half)
+          uint32_t csum[2 * PackedCounts<GMAX>::NP];
 #pragma unroll
-        for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) {
-          csum[2 * r] = __reduce_add_sync(kFull, cnt.w[r] & 0x00ff00ffu);
-          csum[2 * r + 1] = __reduce_add_sync(kFull, (cnt.w[r] >> 8) & 0x00ff00ffu);
-        }
-        if (lane == 0) {
-          uint32_t tot = 0;
+          for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) {
+            csum[2 * r] = __reduce_add_sync(kFull, cnt.w[r] & 0x00ff00ffu);
+            csum[2 * r + 1] = __reduce_add_sync(kFull, (cnt.w[r] >> 8) & 0x00ff00ffu);
+          }
+          if (lane == 0) {
+            uint32_t tot = 0;
 #pragma unroll
-          for (int r = 0; r < 2 * PackedCounts<GMAX>::NP; ++r) tot += (csum[r] & 0xffffu) + (csum[r] >> 16);
-          st.n_acc += tot;
-        }
-        double *acc = s_acc + (size_t)k * PS;
-        if (lane < NC) {
-          const int cc = lane / GMAX, gg = lane % GMAX;
-          acc[GMAX + cc * GMAX + gg] += sm;
-          acc[GMAX + CH * GMAX + cc * GMAX + gg] += sq;
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int gg = 0; gg < GMAX; ++gg) {
+            for (int r = 0; r < 2 * PackedCounts<GMAX>::NP; ++r) tot += (csum[r] & 0xffffu) + (csum[r] >> 16);
+            st.n_acc += tot;
+          }
+          double *acc = out + (size_t)k * PS;  // windows of an item run in order in one CTA
+          if (lane < NC) {
+            const int cc = lane / GMAX, gg = lane % GMAX;
+            acc[GMAX + cc * GMAX + gg] += sm;
+            acc[GMAX + CH * GMAX + cc * GMAX + gg] += sq;
+          } else if (lane >= 32 - GMAX) {
+            const int gg = lane - (32 - GMAX);
             const uint32_t wd = csum[2 * (gg >> 2) + (gg & 1)];
             acc[gg] += (double)((gg & 2) ? (wd >> 16) : (wd & 0xffffu));
           }
-          acc[GMAX + 2 * CH * GMAX] += p0;
-          acc[GMAX + 2 * CH * GMAX + 1] += p1;
-          acc[GMAX + 2 * CH * GMAX + 2] += p2;
+          if (lane == 0) {
+            acc[GMAX + 2 * CH * GMAX] += p0;
+            acc[GMAX + 2 * CH * GMAX + 1] += p1;
+            acc[GMAX + 2 * CH * GMAX + 2] += p2;
+          }
+          __syncwarp();
         }
-        __syncwarp();
+        __syncthreads();  // the window buffer and s_next are reused by the next window
       }
-      __syncthreads();  // the window buffer and s_next are reused by the next window
     }
-    for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) out[i] = s_acc[i];
+    if (threadIdx.x == 0) {
+      s_cur = nxt;
+      nxt = nxt2;
+    }
+    b ^= 1u;
     __syncthreads();
   }
 
@@ -797,19 +925,26 @@ bool fine_supported(int G, int C) {
   return gmax * C <= 24;
 }
 
-uint32_t fine_chunk(int G, int C) {
+void fine_caps(int G, int C, uint32_t *cap64, uint32_t *cap48) {
+#define FPPM_CAPS(gm, ch) \
+  do {                    \
+    *cap64 = FineLayout<gm, ch>::kCap64; \
+    *cap48 = FineLayout<gm, ch>::kCap48; \
+  } while (0)
   if (C == 1) {
-    if (G <= 4) return FineLayout<4, 1>::kChunk;
-    if (G <= 8) return FineLayout<8, 1>::kChunk;
-    if (G <= 12) return FineLayout<12, 1>::kChunk;
-    return FineLayout<16, 1>::kChunk;
+    if (G <= 4) FPPM_CAPS(4, 1);
+    else if (G <= 8) FPPM_CAPS(8, 1);
+    else if (G <= 12) FPPM_CAPS(12, 1);
+    else FPPM_CAPS(16, 1);
+  } else {
+    if (G <= 4) FPPM_CAPS(4, 3);
+    else FPPM_CAPS(8, 3);
   }
-  if (G <= 4) return FineLayout<4, 3>::kChunk;
-  return FineLayout<8, 3>::kChunk;
+#undef FPPM_CAPS
 }
 
 cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
-                               int sms, uint32_t chunk, uint32_t *nb_out) {
+                               int sms, uint32_t cap64, uint32_t cap48, uint32_t *nb_out) {
   const long long x0 = g.ix0 >> g.shift, y0 = g.iy0 >> g.shift, z0 = g.iz0 >> g.shift;
   const unsigned long long ex = (unsigned long long)(((g.ix0 + g.nx - 1) >> g.shift) - x0 + 3);
   const unsigned long long ey = (unsigned long long)(((g.iy0 + g.ny - 1) >> g.shift) - y0 + 3);
@@ -829,8 +964,13 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   S.hp_order = svals;
   e = launch_bucket_start(s, skeys, A.H, nb, S.hp_start, sms);
   if (e != cudaSuccess) return e;
-  k_fine_items<<<fblocks(nb + 1, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order, S.items,
-                                                             S.chunks, chunk, S.nonempty);
+  // per hit point state in wave order (needed by the window sizing below)
+  k_fine_prep<<<fblocks(A.H, 128, sms, 8), 128, 0, s>>>(A, S.hp_order, static_cast<FinePrep *>(S.fprep),
+                                                        static_cast<FineHot *>(S.fhot));
+  note_launches(1);
+  k_fine_items<<<fblocks(nb + 1, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order,
+                                                             static_cast<const FineHot *>(S.fhot), S.items,
+                                                             S.chunks, cap64, cap48, S.nonempty);
   note_launches(1);
   e = launch_exclusive_scan(s, S.items, nb + 1, S.scan_tmp, S.item_base);
   if (e != cudaSuccess) return e;
@@ -838,9 +978,10 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
 }
 
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
-                                uint32_t chunk) {
-  k_fine_desc<<<fblocks(nb, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order, S.item_base,
-                                                        S.pbase, S.fdesc, S.hp_map, chunk);
+                                uint32_t cap64, uint32_t cap48) {
+  k_fine_desc<<<fblocks(nb, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order,
+                                                        static_cast<const FineHot *>(S.fhot), S.item_base,
+                                                        S.pbase, S.fdesc, S.hp_map, cap64, cap48);
   note_launches(1);
   return cudaGetLastError();
 }
@@ -862,14 +1003,7 @@ static cudaError_t launch_fine_t(cudaStream_t s, const GatherArgs &A, const Fine
 }
 
 size_t fine_prep_bytes() { return sizeof(FinePrep); }
-
-cudaError_t launch_fine_prep(cudaStream_t s, const GatherArgs &A, const uint32_t *hp_order, void *prep,
-                             int sms) {
-  if (A.H == 0) return cudaSuccess;
-  k_fine_prep<<<fblocks(A.H, 128, sms, 8), 128, 0, s>>>(A, hp_order, static_cast<FinePrep *>(prep));
-  note_launches(1);
-  return cudaGetLastError();
-}
+size_t fine_hot_bytes() { return sizeof(FineHot); }
 
 cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms) {
   const int G = A.na * A.ns;
