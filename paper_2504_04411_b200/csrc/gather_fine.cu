@@ -407,8 +407,16 @@ struct PackedCounts {
   }
 template <int GMAX>
 static __device__ __forceinline__ void pk_add(PackedCounts<GMAX> &c, int sector) {
-  const uint32_t inc = 1u << ((sector & 3) * 8);
-  FPPM_PK_CASE(0) FPPM_PK_CASE(1) FPPM_PK_CASE(2) FPPM_PK_CASE(3)
+  if constexpr (GMAX == 8) {
+    // one 64-bit shift-add over the two words
+    unsigned long long wd = ((unsigned long long)c.w[1] << 32) | c.w[0];
+    wd += 1ull << (sector * 8);
+    c.w[0] = (uint32_t)wd;
+    c.w[1] = (uint32_t)(wd >> 32);
+  } else {
+    const uint32_t inc = 1u << ((sector & 3) * 8);
+    FPPM_PK_CASE(0) FPPM_PK_CASE(1) FPPM_PK_CASE(2) FPPM_PK_CASE(3)
+  }
 }
 #undef FPPM_PK_CASE
 
@@ -441,11 +449,12 @@ static __device__ __forceinline__ void fine_accumulate(const HitV &K, bool acc, 
                                                        PackedCounts<GMAX> &cnt, double &p0, double &p1,
                                                        double &p2) {
   const bool on = acc && cos_pos;
-  const double pr = (double)(on ? pw.x : 0.0f), pg = (double)(on ? pw.y : 0.0f),
-               pb = (double)(on ? pw.z : 0.0f);
-  p0 += pr;
-  p1 += pg;
-  p2 += pb;
+  const double pr = (double)pw.x, pg = (double)pw.y, pb = (double)pw.z;
+  if (on) {  // predicated: flux sums (integrator.cpp:449)
+    p0 += pr;
+    p1 += pg;
+    p2 += pb;
+  }
   if (acc) pk_add<GMAX>(cnt, sector);
   if constexpr (CH == 1) {
     double v;
@@ -453,7 +462,7 @@ static __device__ __forceinline__ void fine_accumulate(const HitV &K, bool acc, 
       const double kv = cos_pos ? dm(K.K0, L) : K.Kz;  // bsdf.cpp:58: f = 0 when cos_i <= 0
       v = acc ? kv : 0.0;
     } else {
-      const double kv = cos_pos ? elum(dm(K.K0, pr), dm(K.K1, pg), dm(K.K2, pb)) : K.Kz;
+      const double kv = cos_pos ? elum(dm(K.K0, pr), dm(K.K1, pg), dm(K.K2, pb)) : K.Kz;  // pr.. unselected: cos_pos
       v = acc ? kv : 0.0;
     }
     const uint32_t a = slots + (uint32_t)(sector * 32 + lane) * 16u;
