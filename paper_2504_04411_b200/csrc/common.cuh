@@ -81,6 +81,7 @@ struct GridHeader {
 //   rec3 = (pow.b, 0, lum(pow) as fp64 lo/hi words)
 struct PhotonRecs {
   float4 *rec0, *rec1, *rec2, *rec3;
+  float4 *pack;  // fine layout: 64-B records in input order (permutation source)
 };
 
 // exclusive scan of one value per thread over a 256-thread block; returns the

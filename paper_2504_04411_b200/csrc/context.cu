@@ -106,6 +106,12 @@ static cudaError_t dalloc(T **p, size_t count) {
   return cudaMalloc(reinterpret_cast<void **>(p), sizeof(T) * count);
 }
 
+// gather kernel variant: 1 warp per hit point, 2 tiled, 3 lanes, 4 fine (default)
+static int gather_variant(const fppm_gpu_ctx *ctx) {
+  if (ctx->cfg.gather_kernel == 0) return fine_supported(ctx->G, ctx->C) ? 4 : 2;
+  return ctx->cfg.gather_kernel;
+}
+
 static cudaError_t ensure_scratch(fppm_gpu_ctx *ctx, size_t bytes) {
   if (bytes <= ctx->scratch_bytes) return cudaSuccess;
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
@@ -325,6 +331,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->d_ppow, Nc * 3)); A(dalloc(&ctx->d_pdepth, Nc));
   A(dalloc(&ctx->recs.rec0, Nc)); A(dalloc(&ctx->recs.rec1, Nc));
   A(dalloc(&ctx->recs.rec2, Nc)); A(dalloc(&ctx->recs.rec3, Nc));
+  if (gather_variant(ctx) == 4) A(dalloc(&ctx->recs.pack, 4 * Nc));
   A(dalloc(&ctx->sort.keys_a, Nc)); A(dalloc(&ctx->sort.vals_a, Nc));
   A(dalloc(&ctx->sort.keys_b, Nc)); A(dalloc(&ctx->sort.vals_b, Nc));
   A(dalloc(&ctx->sort.hist, radix_hist_entries((uint32_t)Nc)));
@@ -379,7 +386,8 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   void *dev[] = {ctx->d_pos, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb, ctx->d_K, ctx->d_eye,
                  ctx->d_gathered, ctx->d_radius, ctx->d_t, ctx->d_st_cnt, ctx->d_st_sum,
                  ctx->d_st_sq, ctx->d_ppos, ctx->d_pnrm, ctx->d_pwi, ctx->d_ppow, ctx->d_pdepth,
-                 ctx->recs.rec0, ctx->recs.rec1, ctx->recs.rec2, ctx->recs.rec3, ctx->sort.keys_a,
+                 ctx->recs.rec0, ctx->recs.rec1, ctx->recs.rec2, ctx->recs.rec3, ctx->recs.pack,
+                 ctx->sort.keys_a,
                  ctx->sort.vals_a, ctx->sort.keys_b, ctx->sort.vals_b, ctx->sort.hist,
                  ctx->d_cell_start, ctx->d_hdr, ctx->d_bounds, ctx->d_cell,
                  ctx->o_gather_r, ctx->o_stat, ctx->o_crit, ctx->o_flux, ctx->o_flags, ctx->o_rad,
@@ -647,11 +655,6 @@ int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi
   return FPPM_OK;
 }
 
-// gather kernel variant: 1 warp per hit point, 2 tiled, 3 lanes, 4 fine (default)
-static int gather_variant(const fppm_gpu_ctx *ctx) {
-  if (ctx->cfg.gather_kernel == 0) return fine_supported(ctx->G, ctx->C) ? 4 : 2;
-  return ctx->cfg.gather_kernel;
-}
 
 // S_req > 1 asks for the fine (slab) table when the photon set allows it.
 static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) {
@@ -685,6 +688,9 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
     ctx->cell_cap = cap;
   }
   launch_dense_keys(s, ctx->in_pos, ctx->N, ctx->d_hdr, ctx->sort.keys_a, ctx->sort.vals_a, ctx->sms);
+  if (gather_variant(ctx) == 4 && ctx->recs.pack)
+    launch_pack_fine(s, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow, ctx->in_depth, ctx->N,
+                     ctx->recs.pack, ctx->sms);
   FPPM_CUDA_OK(radix_sort_pairs(s, ctx->sort, ctx->N, g.key_bits, &ctx->d_skeys, &ctx->d_order));
   launch_cell_start(s, ctx->d_skeys, ctx->N, ctx->d_hdr, ctx->d_cell_start, g.ncells, ctx->sms);
   launch_permute(s, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,

@@ -197,6 +197,8 @@ void launch_grid_header(cudaStream_t s, const long long *bounds, const double *c
                         unsigned long long max_cells, uint32_t S, GridHeader *hdr);
 void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridHeader *hdr,
                        uint32_t *keys, uint32_t *vals, int sms);
+void launch_pack_fine(cudaStream_t s, const float *pos, const float *nrm, const float *wi, const float *pw,
+                      const uint32_t *depth, uint32_t n, float4 *pack, int sms);
 void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const GridHeader *hdr,
                        uint32_t *start, unsigned long long ncells, int sms);
 void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const float *pos,

@@ -131,6 +131,54 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Fine-layout records packed in input order (coalesced reads of the SoA input
+// and 64-B contiguous writes); the permutation then moves whole 64-B records.
+__device__ __forceinline__ void fine_record(const float *__restrict__ pos, const float *__restrict__ nrm,
+                                            const float *__restrict__ wi, const float *__restrict__ pw,
+                                            const uint32_t *__restrict__ depth, size_t j, float4 &q0,
+                                            float4 &q1, float4 &q2, float4 &q3) {
+  const size_t o = 3 * j;
+  const float nx = nrm[o], ny = nrm[o + 1], wx = wi[o], wy = wi[o + 1];
+  const double L = elum((double)pw[o], (double)pw[o + 1], (double)pw[o + 2]);
+  const unsigned long long Lb = (unsigned long long)__double_as_longlong(L);
+  const uint32_t flags =
+      (fabsf(nx) < INFINITY && fabsf(ny) < INFINITY && fabsf(wx) < INFINITY && fabsf(wy) < INFINITY) ? 1u
+                                                                                                     : 0u;
+  q0 = make_float4(pos[o], pos[o + 1], pos[o + 2], __uint_as_float(depth[j]));
+  q1 = make_float4(nrm[o + 2], wi[o + 2], __uint_as_float((uint32_t)Lb), __uint_as_float((uint32_t)(Lb >> 32)));
+  q2 = make_float4(pw[o], pw[o + 1], pw[o + 2], __uint_as_float(flags));
+  q3 = make_float4(nx, ny, wx, wy);
+}
+
+__global__ void __launch_bounds__(256)
+    k_pack_fine(const float *__restrict__ pos, const float *__restrict__ nrm, const float *__restrict__ wi,
+                const float *__restrict__ pw, const uint32_t *__restrict__ depth, uint32_t n,
+                float4 *__restrict__ pack) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float4 q0, q1, q2, q3;
+    fine_record(pos, nrm, wi, pw, depth, i, q0, q1, q2, q3);
+    float4 *d = pack + 4 * (size_t)i;
+    d[0] = q0;
+    d[1] = q1;
+    d[2] = q2;
+    d[3] = q3;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_permute_packed(const uint32_t *__restrict__ order, uint32_t n, const float4 *__restrict__ pack,
+                     float4 *__restrict__ rec0, float4 *__restrict__ rec1, float4 *__restrict__ rec2,
+                     float4 *__restrict__ rec3) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float4 *src = pack + 4 * (size_t)order[i];
+    const float4 q0 = src[0], q1 = src[1], q2 = src[2], q3 = src[3];
+    rec0[i] = q0;
+    rec1[i] = q1;
+    rec2[i] = q2;
+    rec3[i] = q3;
+  }
+}
+
 // ------------------------------------------------------------------ radix sort
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;
@@ -439,6 +487,13 @@ void launch_grid_header(cudaStream_t s, const long long *bounds, const double *c
   note_launches(1);
 }
 
+void launch_pack_fine(cudaStream_t s, const float *pos, const float *nrm, const float *wi, const float *pw,
+                      const uint32_t *depth, uint32_t n, float4 *pack, int sms) {
+  if (n == 0) return;
+  k_pack_fine<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(pos, nrm, wi, pw, depth, n, pack);
+  note_launches(1);
+}
+
 void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridHeader *hdr,
                        uint32_t *keys, uint32_t *vals, int sms) {
   if (n == 0) return;
@@ -462,7 +517,10 @@ void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const flo
                     const float *nrm, const float *wi, const float *pw, const uint32_t *depth,
                     const PhotonRecs &r, int fine_layout, int sms) {
   if (n == 0) return;
-  if (fine_layout)
+  if (fine_layout && r.pack)
+    k_permute_packed<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, r.pack, r.rec0, r.rec1, r.rec2,
+                                                                  r.rec3);
+  else if (fine_layout)
     k_permute_fine<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
                                                                 r.rec0, r.rec1, r.rec2, r.rec3);
   else
