@@ -191,7 +191,9 @@ int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed
 int fppm_gpu_generate_photons_to(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed,
                                  uint64_t iteration, uint64_t begin, uint32_t n,
                                  const fppm_photons *dev_dst);
-/* Copy the staged photons back to host arrays (NULL skips). */
+/* Copy the staged photons back to host arrays (NULL skips).
+ * Host uploads (fppm_gpu_set_photons) alternate between two staging sets on a
+ * copy stream, so uploading iteration i+1 overlaps the gather of iteration i. */
 int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi, float *power,
                          uint32_t *depth);
 /* Build the uniform hash grid; cell_size <= 0 uses the max live radius
@@ -210,8 +212,10 @@ int fppm_gpu_query_ball(fppm_gpu_ctx *ctx, const double *centers, const double *
 
 /* ---- the hot path ---- */
 /* Gather + accumulate + end-of-iteration policy for every hit point against
- * the grid built last (pixel_pm, integrator.cpp:435-489).  out/summary may be
- * NULL (then the call is fully asynchronous). */
+ * the grid built last (pixel_pm, integrator.cpp:435-489).  `out` arrays are
+ * filled by asynchronous copies on the context stream: call
+ * fppm_gpu_synchronize() before reading them (use pinned host memory for a
+ * non-blocking call).  A non-NULL summary synchronizes. */
 int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration,
                          fppm_gpu_iter_out *out, fppm_gpu_summary *summary);
 /* One FPPM iteration: build_grid(max live radius) + gather_test. */
@@ -224,7 +228,8 @@ int fppm_gpu_accumulate(fppm_gpu_ctx *ctx, const uint32_t *region, const double 
                         const double *value, uint32_t n);
 /* J passed to end_iteration (gather.hpp:81 samples_per_iteration). */
 int fppm_gpu_set_samples_per_iteration(fppm_gpu_ctx *ctx, uint64_t samples_per_iteration);
-/* Runs the configured end-of-iteration policy on every region without a gather. */
+/* Runs the configured end-of-iteration policy on every region without a gather
+ * (outputs asynchronous as for fppm_gpu_gather_test). */
 int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration,
                            fppm_gpu_iter_out *out);
 

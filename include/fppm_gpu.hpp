@@ -68,6 +68,7 @@ class Context {
     ok(fppm_gpu_iterate(ctx_, i, out, &s));
     return s;
   }
+  // (summary != NULL synchronizes, so `out` is complete on return)
   fppm_gpu_summary gather_test(uint64_t i, fppm_gpu_iter_out *out = nullptr) {
     fppm_gpu_summary s{};
     ok(fppm_gpu_gather_test(ctx_, i, out, &s));
@@ -160,6 +161,7 @@ class GatherRegionBatch {
   void end_iteration(uint64_t i, uint64_t samples_per_iteration, fppm_gpu_iter_out *out = nullptr) {
     ctx_.ok(fppm_gpu_set_samples_per_iteration(ctx_.get(), samples_per_iteration));
     ctx_.ok(fppm_gpu_end_iteration(ctx_.get(), i, out));
+    if (out) ctx_.ok(fppm_gpu_synchronize(ctx_.get()));
   }
   std::vector<double> radius() const {
     std::vector<double> r(count_);

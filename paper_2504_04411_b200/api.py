@@ -318,6 +318,8 @@ class FppmContext:
         self._check(self._lib.fppm_gpu_gather_test(self._h, iteration,
                                                    C.byref(io) if io is not None else None,
                                                    C.byref(sm) if sm is not None else None))
+        if o is not None:
+            self.synchronize()  # outputs are written asynchronously
         return o, (sm.as_dict() if sm is not None else None)
 
     def iterate(self, iteration: int, outputs: bool = True, stats: bool = False,
@@ -328,6 +330,8 @@ class FppmContext:
         self._check(self._lib.fppm_gpu_iterate(self._h, iteration,
                                                C.byref(io) if io is not None else None,
                                                C.byref(sm) if sm is not None else None))
+        if o is not None:
+            self.synchronize()  # outputs are written asynchronously
         return o, (sm.as_dict() if sm is not None else None)
 
     def accumulate(self, region, y, value):
@@ -344,6 +348,8 @@ class FppmContext:
         o, io = self._out(outputs, stats, False)
         self._check(self._lib.fppm_gpu_end_iteration(self._h, iteration,
                                                      C.byref(io) if io is not None else None))
+        if o is not None:
+            self.synchronize()
         return o
 
 

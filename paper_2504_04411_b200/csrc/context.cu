@@ -35,6 +35,15 @@ struct fppm_gpu_ctx {
   uint32_t N = 0;
   float *d_ppos = nullptr, *d_pnrm = nullptr, *d_pwi = nullptr, *d_ppow = nullptr;
   uint32_t *d_pdepth = nullptr;
+  // second staging set: host uploads alternate between the two sets on a copy
+  // stream, so the upload of the next batch overlaps the current iteration
+  float *d_ppos2 = nullptr, *d_pnrm2 = nullptr, *d_pwi2 = nullptr, *d_ppow2 = nullptr;
+  uint32_t *d_pdepth2 = nullptr;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_copied[2] = {}, ev_free[2] = {};
+  int stage_cur = 0;       // staging set the current photons live in
+  int stage_pending = -1;  // set whose upload the next grid build must wait for
+  bool free_recorded[2] = {false, false};
   // photons the next grid build reads: the staging buffers, or caller-owned
   // device buffers registered by fppm_gpu_set_photons_device (zero copy)
   const float *in_pos = nullptr, *in_nrm = nullptr, *in_wi = nullptr, *in_pow = nullptr;
@@ -54,6 +63,8 @@ struct fppm_gpu_ctx {
   // outputs
   double *o_gather_r = nullptr, *o_stat = nullptr, *o_crit = nullptr, *o_flux = nullptr;
   uint8_t *o_flags = nullptr;
+  uint8_t *o_tested = nullptr, *o_rejected = nullptr;  // unpacked flags (async outputs)
+  unsigned long long *o_t64 = nullptr;
   float *o_rad = nullptr;
   uint32_t *o_acc = nullptr;
   unsigned long long *snap_cnt = nullptr;
@@ -214,13 +225,40 @@ static int copy_out(fppm_gpu_ctx *ctx, void *dst, const void *src, size_t bytes)
   return FPPM_OK;
 }
 
+// Split the decision flags and widen t on the device, so every output is a
+// plain asynchronous copy (the call does not block the host).
+__global__ void k_unpack_outputs(const uint8_t *__restrict__ flags, const uint32_t *__restrict__ t,
+                                 uint32_t n, uint8_t *__restrict__ tested, uint8_t *__restrict__ rejected,
+                                 unsigned long long *__restrict__ t64) {
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < n; h += gridDim.x * blockDim.x) {
+    const uint8_t f = flags[h];
+    tested[h] = f & 1u;
+    rejected[h] = (f >> 1) & 1u;
+    t64[h] = t[h];
+  }
+}
+
 static int copy_iter_out(fppm_gpu_ctx *ctx, fppm_gpu_iter_out *out, bool with_gather) {
   if (!out) return FPPM_OK;
   const size_t H = ctx->H, CG = (size_t)ctx->G * ctx->C;
   int rc;
+  if (!ctx->o_tested) {
+    const size_t Hc = std::max<uint32_t>(ctx->cfg.max_hitpoints, 1);
+    FPPM_CUDA_OK(dalloc(&ctx->o_tested, Hc));
+    FPPM_CUDA_OK(dalloc(&ctx->o_rejected, Hc));
+    FPPM_CUDA_OK(dalloc(&ctx->o_t64, Hc));
+  }
+  if (H && (out->tested || out->rejected || out->t)) {
+    k_unpack_outputs<<<(unsigned)std::min<size_t>((H + 255) / 256, 1024), 256, 0, ctx->stream>>>(
+        ctx->o_flags, ctx->d_t, (uint32_t)H, ctx->o_tested, ctx->o_rejected, ctx->o_t64);
+    fppm_b200::note_launches(1);
+    FPPM_CUDA_OK(cudaGetLastError());
+  }
   if ((rc = copy_out(ctx, out->radius, ctx->d_radius, sizeof(double) * H))) return rc;
   if ((rc = copy_out(ctx, out->gather_radius, ctx->o_gather_r, sizeof(double) * H))) return rc;
-  if ((rc = copy_out(ctx, out->tested, ctx->o_flags, H))) return rc;
+  if ((rc = copy_out(ctx, out->tested, ctx->o_tested, H))) return rc;
+  if ((rc = copy_out(ctx, out->rejected, ctx->o_rejected, H))) return rc;
+  if ((rc = copy_out(ctx, out->t, ctx->o_t64, sizeof(uint64_t) * H))) return rc;
   if ((rc = copy_out(ctx, out->statistic, ctx->o_stat, sizeof(double) * H))) return rc;
   if ((rc = copy_out(ctx, out->critical, ctx->o_crit, sizeof(double) * H))) return rc;
   if (with_gather) {
@@ -231,27 +269,6 @@ static int copy_iter_out(fppm_gpu_ctx *ctx, fppm_gpu_iter_out *out, bool with_ga
   if ((rc = copy_out(ctx, out->stat_count, ctx->snap_cnt, sizeof(unsigned long long) * CG * H))) return rc;
   if ((rc = copy_out(ctx, out->stat_sum, ctx->snap_sum, sizeof(double) * CG * H))) return rc;
   if ((rc = copy_out(ctx, out->stat_sum_sq, ctx->snap_sq, sizeof(double) * CG * H))) return rc;
-  std::vector<uint32_t> t32;
-  if (out->t) {
-    t32.resize(H);
-    if ((rc = copy_out(ctx, t32.data(), ctx->d_t, sizeof(uint32_t) * H))) return rc;
-  }
-  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
-  if (out->t)
-    for (size_t h = 0; h < H; ++h) out->t[h] = t32[h];
-  if (out->tested || out->rejected) {
-    // o_flags was copied into `tested`; split bits (bit0 tested, bit1 rejected)
-    std::vector<uint8_t> flags(H);
-    if (out->tested) {
-      std::memcpy(flags.data(), out->tested, H);
-    } else {
-      FPPM_CUDA_OK(cudaMemcpy(flags.data(), ctx->o_flags, H, cudaMemcpyDeviceToHost));
-    }
-    for (size_t h = 0; h < H; ++h) {
-      if (out->tested) out->tested[h] = flags[h] & 1;
-      if (out->rejected) out->rejected[h] = (flags[h] >> 1) & 1;
-    }
-  }
   return FPPM_OK;
 }
 
@@ -328,6 +345,8 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->d_radius, Hc)); A(dalloc(&ctx->d_t, Hc));
   A(dalloc(&ctx->d_st_cnt, Hc * CG)); A(dalloc(&ctx->d_st_sum, Hc * CG)); A(dalloc(&ctx->d_st_sq, Hc * CG));
   A(dalloc(&ctx->d_ppos, Nc * 3)); A(dalloc(&ctx->d_pnrm, Nc * 3)); A(dalloc(&ctx->d_pwi, Nc * 3));
+  A(dalloc(&ctx->d_ppos2, Nc * 3)); A(dalloc(&ctx->d_pnrm2, Nc * 3)); A(dalloc(&ctx->d_pwi2, Nc * 3));
+  A(dalloc(&ctx->d_ppow2, Nc * 3)); A(dalloc(&ctx->d_pdepth2, Nc));
   A(dalloc(&ctx->d_ppow, Nc * 3)); A(dalloc(&ctx->d_pdepth, Nc));
   A(dalloc(&ctx->recs.rec0, Nc)); A(dalloc(&ctx->recs.rec1, Nc));
   A(dalloc(&ctx->recs.rec2, Nc)); A(dalloc(&ctx->recs.rec3, Nc));
@@ -386,12 +405,14 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   void *dev[] = {ctx->d_pos, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb, ctx->d_K, ctx->d_eye,
                  ctx->d_gathered, ctx->d_radius, ctx->d_t, ctx->d_st_cnt, ctx->d_st_sum,
                  ctx->d_st_sq, ctx->d_ppos, ctx->d_pnrm, ctx->d_pwi, ctx->d_ppow, ctx->d_pdepth,
+                 ctx->d_ppos2, ctx->d_pnrm2, ctx->d_pwi2, ctx->d_ppow2, ctx->d_pdepth2,
                  ctx->recs.rec0, ctx->recs.rec1, ctx->recs.rec2, ctx->recs.rec3, ctx->recs.pack,
                  ctx->sort.keys_a,
                  ctx->sort.vals_a, ctx->sort.keys_b, ctx->sort.vals_b, ctx->sort.hist,
                  ctx->d_cell_start, ctx->d_hdr, ctx->d_bounds, ctx->d_cell,
                  ctx->o_gather_r, ctx->o_stat, ctx->o_crit, ctx->o_flux, ctx->o_flags, ctx->o_rad,
-                 ctx->o_acc, ctx->snap_cnt, ctx->snap_sum, ctx->snap_sq, ctx->d_counters,
+                 ctx->o_acc, ctx->o_tested, ctx->o_rejected, ctx->o_t64,
+                 ctx->snap_cnt, ctx->snap_sum, ctx->snap_sq, ctx->d_counters,
                  ctx->d_iter_tr, ctx->d_work, ctx->d_rmax_bits, ctx->d_crit, ctx->d_scratch};
   for (void *p : dev)
     if (p) cudaFree(p);
@@ -401,6 +422,12 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
                   T.hp_map, T.nonempty};
   for (void *p : tdev)
     if (p) cudaFree(p);
+  if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->ev_copied[i]) cudaEventDestroy(ctx->ev_copied[i]);
+    if (ctx->ev_free[i]) cudaEventDestroy(ctx->ev_free[i]);
+  }
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   for (auto &pr : ctx->ev_k)
     for (cudaEvent_t e : pr)
       if (e) cudaEventDestroy(e);
@@ -416,6 +443,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
 
 int fppm_gpu_synchronize(fppm_gpu_ctx *ctx) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (ctx->cstream) FPPM_CUDA_OK(cudaStreamSynchronize(ctx->cstream));
   FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
   return FPPM_OK;
 }
@@ -560,31 +588,51 @@ int fppm_gpu_max_radius(fppm_gpu_ctx *ctx, double *r_max) {
 }
 
 // ------------------------------------------------------------------ photons + grid
-static void use_staging(fppm_gpu_ctx *ctx) {
-  ctx->in_pos = ctx->d_ppos;
-  ctx->in_nrm = ctx->d_pnrm;
-  ctx->in_wi = ctx->d_pwi;
-  ctx->in_pow = ctx->d_ppow;
-  ctx->in_depth = ctx->d_pdepth;
+static void use_staging(fppm_gpu_ctx *ctx, int set = 0) {
+  ctx->stage_cur = set;
+  ctx->in_pos = set ? ctx->d_ppos2 : ctx->d_ppos;
+  ctx->in_nrm = set ? ctx->d_pnrm2 : ctx->d_pnrm;
+  ctx->in_wi = set ? ctx->d_pwi2 : ctx->d_pwi;
+  ctx->in_pow = set ? ctx->d_ppow2 : ctx->d_ppow;
+  ctx->in_depth = set ? ctx->d_pdepth2 : ctx->d_pdepth;
 }
 
+// Host uploads go to the staging set not holding the current photons, on the
+// copy stream: the copy waits only until the grid build that last read that
+// set has consumed it (ev_free), and the next grid build waits for the copy
+// (ev_copied).  With pinned host memory the call returns immediately.
 static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cudaMemcpyKind kind) {
   if (!ctx || !p) return FPPM_ERR_INVALID_ARGUMENT;
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (n && (!p->pos || !p->normal || !p->wi || !p->power || !p->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
-  cudaStream_t s = ctx->stream;
+  const int set = ctx->stage_cur ^ 1;
+  if (!ctx->cstream) {
+    FPPM_CUDA_OK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_copied[i], cudaEventDisableTiming));
+      FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_free[i], cudaEventDisableTiming));
+    }
+  }
+  cudaStream_t s = ctx->cstream;
+  // the set must not be overwritten while an enqueued grid build still reads it,
+  // nor while earlier work on the context stream (e.g. generation) writes it
+  if (ctx->free_recorded[set]) FPPM_CUDA_OK(cudaStreamWaitEvent(s, ctx->ev_free[set], 0));
+  else FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
   const size_t b3 = sizeof(float) * 3 * n;
   if (n) {
-    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_ppos, p->pos, b3, kind, s));
-    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_pnrm, p->normal, b3, kind, s));
-    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_pwi, p->wi, b3, kind, s));
-    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_ppow, p->power, b3, kind, s));
-    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_pdepth, p->depth, sizeof(uint32_t) * n, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(set ? ctx->d_ppos2 : ctx->d_ppos, p->pos, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(set ? ctx->d_pnrm2 : ctx->d_pnrm, p->normal, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(set ? ctx->d_pwi2 : ctx->d_pwi, p->wi, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(set ? ctx->d_ppow2 : ctx->d_ppow, p->power, b3, kind, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(set ? ctx->d_pdepth2 : ctx->d_pdepth, p->depth, sizeof(uint32_t) * n,
+                                 kind, s));
   }
+  FPPM_CUDA_OK(cudaEventRecord(ctx->ev_copied[set], s));
+  ctx->stage_pending = set;
   ctx->N = n;
   ctx->grid_valid = false;
-  use_staging(ctx);
+  use_staging(ctx, set);
   return FPPM_OK;
 }
 
@@ -599,6 +647,7 @@ int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (n && (!dev->pos || !dev->normal || !dev->wi || !dev->power || !dev->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
+  ctx->stage_pending = -1;  // an unconsumed upload is superseded
   ctx->in_pos = dev->pos;
   ctx->in_nrm = dev->normal;
   ctx->in_wi = dev->wi;
@@ -615,6 +664,8 @@ int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed
   if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2)
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
+  if (ctx->stage_pending == 0) FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[0], 0));
+  ctx->stage_pending = -1;
   launch_generate_photons(ctx->stream, workload, seed, iteration, begin, n, ctx->d_ppos, ctx->d_pnrm,
                           ctx->d_pwi, ctx->d_ppow, ctx->d_pdepth, ctx->sms);
   FPPM_CUDA_OK(cudaGetLastError());
@@ -644,6 +695,8 @@ int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi
                          uint32_t *depth) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   if (!ctx->in_pos) use_staging(ctx);
+  if (ctx->stage_pending >= 0)
+    FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[ctx->stage_pending], 0));
   const size_t b3 = sizeof(float) * 3 * ctx->N;
   int rc;
   if ((rc = copy_out(ctx, pos, ctx->in_pos, b3))) return rc;
@@ -671,6 +724,11 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
   FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_bounds, ctx->h_bounds_init, sizeof(long long) * 6,
                                cudaMemcpyHostToDevice, s));
   if (!ctx->in_pos) use_staging(ctx);
+  const int reading = ctx->stage_pending >= 0 ? ctx->stage_pending : -1;
+  if (reading >= 0) {
+    FPPM_CUDA_OK(cudaStreamWaitEvent(s, ctx->ev_copied[reading], 0));
+    ctx->stage_pending = -1;
+  }
   launch_cell_bounds(s, ctx->in_pos, ctx->N, ctx->d_cell, S_req, ctx->d_bounds, ctx->sms);
   launch_grid_header(s, ctx->d_bounds, ctx->d_cell, ctx->N, ctx->cfg.max_cells, S_req, ctx->d_hdr);
   FPPM_CUDA_OK(cudaGetLastError());
@@ -696,6 +754,11 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
   launch_permute(s, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,
                  ctx->in_depth, ctx->recs, gather_variant(ctx) == 4, ctx->sms);
   FPPM_CUDA_OK(cudaGetLastError());
+  if (ctx->cstream && ctx->in_pos == (ctx->stage_cur ? ctx->d_ppos2 : ctx->d_ppos)) {
+    // the staging set is consumed: a later upload may overwrite it
+    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_free[ctx->stage_cur], s));
+    ctx->free_recorded[ctx->stage_cur] = true;
+  }
   ctx->grid_valid = true;
   return FPPM_OK;
 }
