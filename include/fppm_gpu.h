@@ -91,6 +91,13 @@ typedef struct fppm_gpu_config {
   void *stream;       /* cudaStream_t to order work on; NULL -> own stream */
   int32_t gather_kernel; /* 0 auto (= 4); 1 warp per hit point; 2 tiled; 3 lanes = hit points;
                             4 fine-cell tiled (default) */
+  /* VCM+ merge stage (integrator.cpp:595-627): every gathered photon value is
+   * weighted by mis_weight_merge (path.cpp:103-111) with the tested radius;
+   * needs fppm_gpu_set_hitpoint_mis / fppm_gpu_set_photon_mis; runs on the
+   * warp kernel (gather_kernel 0 or 1) */
+  int32_t vcm_plus;
+  int32_t mis_n_vm;   /* MisContext::n_vm (light paths per iteration, integrator.cpp:133) */
+  double mis_beta;    /* MisContext::beta (MIS power) */
 } fppm_gpu_config;
 
 typedef struct fppm_gpu_ctx fppm_gpu_ctx;
@@ -232,6 +239,15 @@ int fppm_gpu_set_samples_per_iteration(fppm_gpu_ctx *ctx, uint64_t samples_per_i
  * (outputs asynchronous as for fppm_gpu_gather_test). */
 int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration,
                            fppm_gpu_iter_out *out);
+
+/* ---- VCM+ merge stage inputs (host arrays) ---- */
+/* Eye-vertex MIS partials per hit point (PathVertex::mis d_vcm, d_vm). */
+int fppm_gpu_set_hitpoint_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const double *d_vm, uint32_t n);
+/* Light-vertex MIS partials and roulette survival per photon (LightVertex::mis
+ * d_vcm, d_vm and ::cont, path.hpp:76-89), in the order of the photons passed
+ * to fppm_gpu_set_photons; used by the next grid build. */
+int fppm_gpu_set_photon_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const double *d_vm,
+                            const double *cont, uint32_t n);
 
 /* Cumulative counters of this context: [accepted, candidates, exact, ambiguous]. */
 int fppm_gpu_counters(fppm_gpu_ctx *ctx, uint64_t out[4]);

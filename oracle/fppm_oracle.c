@@ -427,7 +427,39 @@ struct orc_session {
   region_t *reg;
   uint64_t *stat_count;
   double *stat_sum, *stat_sum_sq;
+  double *eye_d_vcm, *eye_d_vm;                           /* VCM+ (per hit point) */
+  const double *ph_d_vcm, *ph_d_vm, *ph_cont;             /* VCM+ (per photon) */
 };
+
+/* path.cpp:11-13 */
+static double mis_pow(double beta, double x) { return beta == 1.0 ? x : pow(x, beta); }
+
+/* path.cpp:103-111 with vc_factor (path.cpp:22-24) of eta_vm = n_vm pi r^2
+ * (integrator.cpp:503, evaluated left to right) */
+double orc_mis_weight_merge(int n_vm, double beta, double r, double eye_d_vcm, double eye_d_vm,
+                            double light_d_vcm, double light_d_vm, double bsdf_fwd_pdf_w,
+                            double bsdf_rev_pdf_w) {
+  const double eta_vm = (double)n_vm * kPi * r * r;
+  const double vcf = eta_vm > 0.0 ? mis_pow(beta, 1.0 / eta_vm) : 0.0;
+  const double w_light = light_d_vcm * vcf + light_d_vm * mis_pow(beta, bsdf_fwd_pdf_w);
+  const double w_camera = eye_d_vcm * vcf + eye_d_vm * mis_pow(beta, bsdf_rev_pdf_w);
+  return 1.0 / (w_light + 1.0 + w_camera);
+}
+
+void orc_session_set_eye_mis(orc_session *s, const double *d_vcm, const double *d_vm) {
+  for (size_t h = 0; h < s->H; ++h) {
+    s->eye_d_vcm[h] = d_vcm ? d_vcm[h] : 0.0;
+    s->eye_d_vm[h] = d_vm ? d_vm[h] : 0.0;
+  }
+}
+
+void orc_session_set_photon_mis(orc_session *s, const double *d_vcm, const double *d_vm,
+                                const double *cont, size_t n) {
+  (void)n;
+  s->ph_d_vcm = d_vcm;
+  s->ph_d_vm = d_vm;
+  s->ph_cont = cont;
+}
 
 orc_session *orc_session_create(const orc_config *cfg, size_t H,
                                 const double *pos, const double *nrm,
@@ -467,6 +499,8 @@ orc_session *orc_session_create(const orc_config *cfg, size_t H,
   s->stat_sum = (double *)calloc(cg * (H ? H : 1), sizeof(double));
   s->stat_sum_sq = (double *)calloc(cg * (H ? H : 1), sizeof(double));
   s->reg = (region_t *)calloc(H ? H : 1, sizeof(region_t));
+  s->eye_d_vcm = (double *)calloc(H ? H : 1, sizeof(double));
+  s->eye_d_vm = (double *)calloc(H ? H : 1, sizeof(double));
   for (size_t h = 0; h < H; ++h) {
     s->reg[h].radius = r0;
     s->reg[h].initial_radius = r0;
@@ -483,6 +517,7 @@ void orc_session_free(orc_session *s) {
   free(s->pos); free(s->nrm); free(s->wo); free(s->thr); free(s->alb);
   free(s->eye_depth); free(s->gathered);
   free(s->stat_count); free(s->stat_sum); free(s->stat_sum_sq); free(s->reg);
+  free(s->eye_d_vcm); free(s->eye_d_vm);
   free(s);
 }
 
@@ -504,6 +539,8 @@ typedef struct {
   double sum[3];
   uint64_t accepted;
   int err;
+  /* VCM+: eye cos_o, continuation probability and MIS partials */
+  double cos_o, cont, e_vcm, e_vm;
 } gather_ctx;
 
 static void gather_cb(uint32_t id, void *user) {
@@ -523,8 +560,21 @@ static void gather_cb(uint32_t id, void *user) {
   const double wi[3] = {g->pwi[3 * id], g->pwi[3 * id + 1], g->pwi[3 * id + 2]};
   const double cos_i = dot3(wi, g->reg->n);
   const double *k = cos_i <= 0.0 ? g->Kzero : g->K;
-  const double val[3] = {k[0] * (double)g->ppow[3 * id], k[1] * (double)g->ppow[3 * id + 1],
-                         k[2] * (double)g->ppow[3 * id + 2]};
+  double val[3] = {k[0] * (double)g->ppow[3 * id], k[1] * (double)g->ppow[3 * id + 1],
+                   k[2] * (double)g->ppow[3 * id + 2]};
+  if (cfg->vcm_plus) {
+    /* integrator.cpp:612-616: f, pf, pr of Bsdf::eval (bsdf.cpp:53-63, pdfs
+     * zero when the value is black), merge weight, val = thr * f * p.thr * w */
+    const int black = g->cos_o <= 0.0 || cos_i <= 0.0;
+    const double pf = black ? 0.0 : (cos_i > 0 ? cos_i * kInvPi : 0.0);
+    const double pr = black ? 0.0 : (g->cos_o > 0 ? g->cos_o * kInvPi : 0.0);
+    const double w = orc_mis_weight_merge(cfg->mis_n_vm, cfg->mis_beta, g->r, g->e_vcm, g->e_vm,
+                                          g->s->ph_d_vcm[id], g->s->ph_d_vm[id], pf * g->cont,
+                                          pr * g->s->ph_cont[id]);
+    val[0] = val[0] * w;
+    val[1] = val[1] * w;
+    val[2] = val[2] * w;
+  }
   g->sum[0] += val[0]; g->sum[1] += val[1]; g->sum[2] += val[2];
   g->accepted++;
   /* GatherRegion::accumulate (gather.cpp:59-67) */
@@ -583,6 +633,17 @@ static void process_hit(worker_t *w, size_t slot) {
     g.r = r; g.r2 = r * r;
     const double *thr = s->thr + 3 * h, *alb = s->alb + 3 * h;
     const double cos_o = dot3(s->wo + 3 * h, reg->n); /* bsdf.cpp:34 */
+    g.cos_o = cos_o;
+    {
+      /* bsdf.cpp:42-51 (Lambertian): min(1, albedo.max_component()),
+       * std::max / std::min semantics (vec.hpp:73) */
+      const double *a = s->alb + 3 * h;
+      const double m1 = a[1] < a[2] ? a[2] : a[1];
+      const double amax = a[0] < m1 ? m1 : a[0];
+      g.cont = amax < 1.0 ? amax : 1.0;
+    }
+    g.e_vcm = s->eye_d_vcm[h];
+    g.e_vm = s->eye_d_vm[h];
     for (int c = 0; c < 3; ++c) {
       const double f = cos_o <= 0.0 ? 0.0 : alb[c] * kInvPi; /* bsdf.cpp:58,63 */
       g.K[c] = thr[c] * f;                                  /* integrator.cpp:448 */

@@ -46,6 +46,7 @@ class Config(C.Structure):
         ("initial_radius", C.c_double), ("samples_per_iteration", C.c_uint64),
         ("max_depth", C.c_uint32), ("normal_guard_cos", C.c_double),
         ("threads", C.c_int), ("alpha_chi2", C.c_double), ("policy", C.c_int),
+        ("vcm_plus", C.c_int), ("mis_n_vm", C.c_int), ("mis_beta", C.c_double),
     ]
 
 
@@ -114,6 +115,11 @@ class Oracle:
         self._sc = fn("session_create", C.c_void_p, [C.POINTER(Config), C.c_size_t, _dp, _dp, _dp, _dp, _dp, _u32p, _u8p, _ip])
         self._sf = fn("session_free", None, [C.c_void_p])
         self._smr = fn("session_max_radius", C.c_double, [C.c_void_p])
+        self._seye = fn("session_set_eye_mis", None, [C.c_void_p, _dp, _dp])
+        self._sphm = fn("session_set_photon_mis", None, [C.c_void_p, _dp, _dp, _dp, C.c_size_t])
+        self._mwm = fn("mis_weight_merge", C.c_double, [C.c_int, C.c_double, C.c_double, C.c_double,
+                                                        C.c_double, C.c_double, C.c_double,
+                                                        C.c_double, C.c_double])
         if kind == "port":
             self._si = fn("session_iterate", C.c_int, [C.c_void_p, C.c_uint64, _fp, _fp, _fp, _fp, _u32p, C.c_size_t, C.c_double, _u32p, C.c_size_t, C.POINTER(IterOut)])
             self._gen = fn("gen_photons", None, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _fp, _fp, _fp, _fp, _u32p])
@@ -158,6 +164,9 @@ class Oracle:
 
     def reg_lower_gamma(self, a, x):
         return self._call(self._lg, a, x)
+
+    def mis_weight_merge(self, n_vm, beta, r, e_vcm, e_vm, l_vcm, l_vm, fwd, rev):
+        return self._mwm(n_vm, beta, r, e_vcm, e_vm, l_vcm, l_vm, fwd, rev)
 
     def f_statistic(self, count, s, q, m):
         s = np.ascontiguousarray(s, np.float64)
@@ -244,7 +253,7 @@ class _Session:
                         override_decision=0, k=0.7, alpha=0.75, r_min_base=0.0,
                         initial_radius=0.02, samples_per_iteration=1, max_depth=10,
                         normal_guard_cos=0.86602540378443865, threads=1, alpha_chi2=0.01,
-                        policy=0)
+                        policy=0, vcm_plus=0, mis_n_vm=0, mis_beta=1.0)
         defaults.update(cfg)
         for k_, v in defaults.items():
             setattr(c, k_, v)
@@ -269,6 +278,17 @@ class _Session:
 
     def max_radius(self):
         return self.o._smr(self.h)
+
+    def set_eye_mis(self, d_vcm, d_vm):
+        """VCM+: eye-vertex MIS partials per hit point."""
+        self._eye = [np.ascontiguousarray(d_vcm, np.float64), np.ascontiguousarray(d_vm, np.float64)]
+        self.o._seye(self.h, *[_ptr(a, _dp) for a in self._eye])
+
+    def set_photon_mis(self, d_vcm, d_vm, cont):
+        """VCM+: light-vertex MIS partials + survival per photon (used by the
+        next iterate; arrays are kept alive here)."""
+        self._pm = [np.ascontiguousarray(a, np.float64) for a in (d_vcm, d_vm, cont)]
+        self.o._sphm(self.h, *[_ptr(a, _dp) for a in self._pm], len(self._pm[0]))
 
     def iterate(self, iteration, ph, cell=0.0, subset=None):
         n = self.H if subset is None else len(subset)

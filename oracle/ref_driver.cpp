@@ -191,6 +191,9 @@ struct RefConfig { // identical layout to orc_config (fppm_oracle.h)
   int threads;
   double alpha_chi2;
   int policy;  // 0 end_iteration, 1 chi2_end_iteration, 2 schedule_end_iteration
+  int vcm_plus;
+  int mis_n_vm;
+  double mis_beta;
 };
 
 struct RefIterOut { // identical layout to orc_iter_out
@@ -219,6 +222,8 @@ struct RefSession {
   std::vector<Material> mat;
   std::vector<uint32_t> eye_depth;
   std::vector<uint8_t> gathered;
+  std::vector<MisPartials> eye_mis;            // VCM+ (PathVertex::mis)
+  const double *ph_d_vcm = nullptr, *ph_d_vm = nullptr, *ph_cont = nullptr;  // VCM+
 };
 
 void* ref_session_create(const RefConfig* cfg, size_t H, const double* pos,
@@ -251,6 +256,7 @@ void* ref_session_create(const RefConfig* cfg, size_t H, const double* pos,
       s->eye_depth.push_back(eye_depth[h]);
       s->gathered.push_back(gathered ? gathered[h] : 1);
     }
+    s->eye_mis.assign(H, MisPartials{});
     return s;
   } catch (const std::invalid_argument&) {
     if (err) *err = 1;
@@ -259,6 +265,34 @@ void* ref_session_create(const RefConfig* cfg, size_t H, const double* pos,
 }
 
 void ref_session_free(void* s) { delete static_cast<RefSession*>(s); }
+
+void ref_session_set_eye_mis(void* sp, const double* d_vcm, const double* d_vm) {
+  auto* s = static_cast<RefSession*>(sp);
+  for (size_t h = 0; h < s->eye_mis.size(); ++h) {
+    s->eye_mis[h].d_vcm = d_vcm ? d_vcm[h] : 0.0;
+    s->eye_mis[h].d_vm = d_vm ? d_vm[h] : 0.0;
+  }
+}
+
+void ref_session_set_photon_mis(void* sp, const double* d_vcm, const double* d_vm, const double* cont,
+                                size_t) {
+  auto* s = static_cast<RefSession*>(sp);
+  s->ph_d_vcm = d_vcm;
+  s->ph_d_vm = d_vm;
+  s->ph_cont = cont;
+}
+
+double ref_mis_weight_merge(int n_vm, double beta, double r, double eye_d_vcm, double eye_d_vm,
+                            double light_d_vcm, double light_d_vm, double fwd, double rev) {
+  MisContext ctx{1, n_vm, beta, 0.0};
+  ctx.eta_vm = ctx.n_vm * kPi * r * r;  // integrator.cpp:503
+  MisPartials e, l;
+  e.d_vcm = eye_d_vcm;
+  e.d_vm = eye_d_vm;
+  l.d_vcm = light_d_vcm;
+  l.d_vm = light_d_vm;
+  return mis_weight_merge(ctx, e, l, fwd, rev);
+}
 
 double ref_session_max_radius(void* sp) {
   auto* s = static_cast<RefSession*>(sp);
@@ -291,6 +325,11 @@ int ref_session_iterate(void* sp, uint64_t iteration, const float* ppos,
     v.throughput = {ppow[3 * i], ppow[3 * i + 1], ppow[3 * i + 2]};
     v.path_index = static_cast<uint32_t>(i);
     v.depth = pdepth[i];
+    if (cfg.vcm_plus && s->ph_d_vcm) {
+      v.mis.d_vcm = s->ph_d_vcm[i];
+      v.mis.d_vm = s->ph_d_vm[i];
+      v.cont = s->ph_cont[i];
+    }
   }
   PhotonGrid grid;
   try {
@@ -331,10 +370,17 @@ int ref_session_iterate(void* sp, uint64_t iteration, const float* ppos,
             if (dot(p.shading_normal, normal) < cfg.normal_guard_cos) continue;
             const UnifiedPoint y = map_to_unified(center, p.position, frame);
             if (y.u * y.u + y.v * y.v > r2) continue;
-            // callback (:445-451)
+            // callback (:445-451); VCM+ merge callback (:609-616)
             double pf = 0, pr = 0;
             const Rgb f = bsdf.eval(p.wi, pf, pr);
-            const Rgb val = throughput * f * p.throughput;
+            Rgb val = throughput * f * p.throughput;
+            if (cfg.vcm_plus) {
+              MisContext ctx{1, cfg.mis_n_vm, cfg.mis_beta, 0.0};
+              ctx.eta_vm = ctx.n_vm * kPi * r * r;  // :503
+              const double w = mis_weight_merge(ctx, s->eye_mis[h], p.mis,
+                                                pf * bsdf.continuation_prob(), pr * p.cont);
+              val = throughput * f * p.throughput * w;
+            }
             sum += val;
             region->accumulate({y, val});
             ++accepted;

@@ -82,6 +82,7 @@ class Config(C.Structure):
         ("max_depth", C.c_uint32), ("normal_guard_cos", C.c_double),
         ("max_hitpoints", C.c_uint32), ("max_photons", C.c_uint32), ("max_cells", C.c_uint32),
         ("device", C.c_int32), ("stream", C.c_void_p), ("gather_kernel", C.c_int32),
+        ("vcm_plus", C.c_int32), ("mis_n_vm", C.c_int32), ("mis_beta", C.c_double),
     ]
 
 
@@ -153,6 +154,8 @@ _SIGS = [
     ("fppm_gpu_kernel_launches", C.c_uint64, []),
     ("fppm_gpu_gather_kernel_ms", C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.POINTER(C.c_uint32)]),
     ("fppm_gpu_counters", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("fppm_gpu_set_hitpoint_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    ("fppm_gpu_set_photon_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     ("fppm_gpu_schedule_radius", C.c_double, [C.c_double, C.c_double, C.c_uint64]),
     ("fppm_gpu_f_quantile", C.c_double, [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int)]),
     ("fppm_gpu_chi2_quantile", C.c_double, [C.c_double, C.c_double, C.POINTER(C.c_int)]),

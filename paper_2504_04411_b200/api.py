@@ -93,7 +93,8 @@ class FppmContext:
                  k: float = 0.7, alpha: float = 0.75, r_min_base: Optional[float] = None,
                  max_depth: int = 10, normal_guard_cos: float = NORMAL_GUARD_COS,
                  max_hitpoints: int = 1, max_photons: int = 1, max_cells: int = 0,
-                 device: int = 0, stream: Optional[int] = None, gather_kernel: str = "auto"):
+                 device: int = 0, stream: Optional[int] = None, gather_kernel: str = "auto",
+                 vcm_plus: bool = False, mis_n_vm: int = 0, mis_beta: float = 1.0):
         self._lib = N.lib()
         cfg = N.Config()
         cfg.n_annuli, cfg.n_sectors = n_annuli, n_sectors
@@ -111,6 +112,7 @@ class FppmContext:
         cfg.device = device
         cfg.stream = stream
         cfg.gather_kernel = {"auto": 0, "warp": 1, "tile": 2, "lanes": 3, "fine": 4}[gather_kernel]
+        cfg.vcm_plus, cfg.mis_n_vm, cfg.mis_beta = int(bool(vcm_plus)), int(mis_n_vm), float(mis_beta)
         self.config = cfg
         self.G = n_annuli * n_sectors
         self.C = cfg.channels
@@ -199,6 +201,19 @@ class FppmContext:
         if not dev:
             self.synchronize()  # host arrays may be pageable temporaries
         self.H = n
+
+    def set_hitpoint_mis(self, d_vcm, d_vm):
+        """VCM+: eye-vertex MIS partials per hit point."""
+        a = [_host(d_vcm, np.float64), _host(d_vm, np.float64)]
+        self._check(self._lib.fppm_gpu_set_hitpoint_mis(self._h, a[0].ctypes.data, a[1].ctypes.data,
+                                                        len(a[0])))
+
+    def set_photon_mis(self, d_vcm, d_vm, cont):
+        """VCM+: light-vertex MIS partials and survival per photon (photon order)."""
+        a = [_host(x, np.float64) for x in (d_vcm, d_vm, cont)]
+        self._check(self._lib.fppm_gpu_set_photon_mis(self._h, a[0].ctypes.data, a[1].ctypes.data,
+                                                      a[2].ctypes.data, len(a[0])))
+        self.synchronize()  # host arrays may be pageable temporaries
 
     def generate_raster_hitpoints(self, W: int):
         self._check(self._lib.fppm_gpu_generate_raster_hitpoints(self._h, W))

@@ -49,6 +49,12 @@ struct fppm_gpu_ctx {
   const float *in_pos = nullptr, *in_nrm = nullptr, *in_wi = nullptr, *in_pow = nullptr;
   const uint32_t *in_depth = nullptr;
 
+  // VCM+ merge stage inputs
+  double2 *d_eye_mis = nullptr;                                   // [H] {d_vcm, d_vm}
+  double *d_pmis_in[3] = {nullptr, nullptr, nullptr};             // [N] photon order
+  double *d_pmis[3] = {nullptr, nullptr, nullptr};                // [N] sorted order
+  bool pmis_set = false;
+
   // grid
   fppm_b200::PhotonRecs recs{};
   fppm_b200::SortScratch sort{};
@@ -119,6 +125,7 @@ static cudaError_t dalloc(T **p, size_t count) {
 
 // gather kernel variant: 1 warp per hit point, 2 tiled, 3 lanes, 4 fine (default)
 static int gather_variant(const fppm_gpu_ctx *ctx) {
+  if (ctx->cfg.vcm_plus) return 1;  // the merge weights run on the warp kernel
   if (ctx->cfg.gather_kernel == 0) return fine_supported(ctx->G, ctx->C) ? 4 : 2;
   return ctx->cfg.gather_kernel;
 }
@@ -309,6 +316,8 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   if (c.channels != FPPM_CHANNELS_LUMINANCE && c.channels != FPPM_CHANNELS_RGB) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy < FPPM_POLICY_FTEST || c.policy > FPPM_POLICY_SCHEDULE) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.gather_kernel < 0 || c.gather_kernel > 4) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.vcm_plus && (c.gather_kernel > 1 || c.mis_n_vm < 0 || !(c.mis_beta > 0.0)))
+    return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy == FPPM_POLICY_FTEST && c.override_decision == FPPM_OVERRIDE_NONE &&
       !(c.alpha_f > 0.0 && c.alpha_f < 1.0)) return FPPM_ERR_INVALID_ARGUMENT;  // stat_tests.cpp:88
   int ndev = 0;
@@ -369,6 +378,14 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->tile.sort.hist, radix_hist_entries((uint32_t)Hc)));
   A(dalloc(&ctx->tile.hp_map, 3 * Hc));
   A(dalloc(reinterpret_cast<char **>(&ctx->tile.fprep), fine_prep_bytes() * Hc));
+  if (c.vcm_plus) {
+    A(dalloc(&ctx->d_eye_mis, Hc));
+    A(cudaMemset(ctx->d_eye_mis, 0, sizeof(double2) * Hc));
+    for (int i = 0; i < 3; ++i) {
+      A(dalloc(&ctx->d_pmis_in[i], Nc));
+      A(dalloc(&ctx->d_pmis[i], Nc));
+    }
+  }
   A(dalloc(reinterpret_cast<char **>(&ctx->tile.fhot), fine_hot_bytes() * Hc));
   A(dalloc(&ctx->tile.nonempty, 1));
   A(cudaMallocHost(&ctx->h_total, 2 * sizeof(uint32_t)));
@@ -423,6 +440,11 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   for (void *p : tdev)
     if (p) cudaFree(p);
   if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
+  if (ctx->d_eye_mis) cudaFree(ctx->d_eye_mis);
+  for (int i = 0; i < 3; ++i) {
+    if (ctx->d_pmis_in[i]) cudaFree(ctx->d_pmis_in[i]);
+    if (ctx->d_pmis[i]) cudaFree(ctx->d_pmis[i]);
+  }
   for (int i = 0; i < 2; ++i) {
     if (ctx->ev_copied[i]) cudaEventDestroy(ctx->ev_copied[i]);
     if (ctx->ev_free[i]) cudaEventDestroy(ctx->ev_free[i]);
@@ -753,6 +775,9 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
   launch_cell_start(s, ctx->d_skeys, ctx->N, ctx->d_hdr, ctx->d_cell_start, g.ncells, ctx->sms);
   launch_permute(s, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,
                  ctx->in_depth, ctx->recs, gather_variant(ctx) == 4, ctx->sms);
+  if (ctx->cfg.vcm_plus)
+    launch_permute_f64x3(s, ctx->d_order, ctx->N, ctx->d_pmis_in[0], ctx->d_pmis_in[1], ctx->d_pmis_in[2],
+                         ctx->d_pmis[0], ctx->d_pmis[1], ctx->d_pmis[2], ctx->sms);
   FPPM_CUDA_OK(cudaGetLastError());
   if (ctx->cstream && ctx->in_pos == (ctx->stage_cur ? ctx->d_ppos2 : ctx->d_ppos)) {
     // the staging set is consumed: a later upload may overwrite it
@@ -952,9 +977,15 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
   A.o_flux = ctx->o_flux; A.o_flags = ctx->o_flags; A.o_radiance = ctx->o_rad;
   A.o_accepted = ctx->o_acc;
   if (snap) { A.snap_cnt = ctx->snap_cnt; A.snap_sum = ctx->snap_sum; A.snap_sq = ctx->snap_sq; }
+  A.vcm = ctx->cfg.vcm_plus;
+  A.mis_n_vm = ctx->cfg.mis_n_vm;
+  A.mis_beta = ctx->cfg.mis_beta;
+  A.eye_mis = ctx->d_eye_mis;
+  A.p_vcm = ctx->d_pmis[0]; A.p_vm = ctx->d_pmis[1]; A.p_cont = ctx->d_pmis[2];
+  A.wo = ctx->d_wo; A.alb = ctx->d_alb;
   A.counters = ctx->d_counters; A.iter_tr = ctx->d_iter_tr; A.work = ctx->d_work;
   A.rmax_bits = ctx->d_rmax_bits;
-  if (ctx->H && ctx->cfg.gather_kernel == 1) {
+  if (ctx->H && gather_variant(ctx) == 1) {
     if ((rc = kernel_event(ctx, 0))) return rc;
     FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
     if ((rc = kernel_event(ctx, 1))) return rc;
@@ -1137,6 +1168,33 @@ int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_
 }
 
 uint64_t fppm_gpu_kernel_launches(void) { return g_kernel_launches.load(); }
+
+int fppm_gpu_set_hitpoint_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const double *d_vm, uint32_t n) {
+  if (!ctx || (n && (!d_vcm || !d_vm))) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->cfg.vcm_plus) return fail(ctx, FPPM_ERR_STATE, "MIS partials need vcm_plus");
+  if (n != ctx->H) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "one MIS pair per hit point");
+  std::vector<double2> v(n);
+  for (uint32_t h = 0; h < n; ++h) v[h] = make_double2(d_vcm[h], d_vm[h]);
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_eye_mis, v.data(), sizeof(double2) * n, cudaMemcpyHostToDevice,
+                               ctx->stream));
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  return FPPM_OK;
+}
+
+int fppm_gpu_set_photon_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const double *d_vm, const double *cont,
+                            uint32_t n) {
+  if (!ctx || (n && (!d_vcm || !d_vm || !cont))) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->cfg.vcm_plus) return fail(ctx, FPPM_ERR_STATE, "MIS partials need vcm_plus");
+  if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
+  const double *src[3] = {d_vcm, d_vm, cont};
+  for (int i = 0; i < 3; ++i)
+    if (n)
+      FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_pmis_in[i], src[i], sizeof(double) * n, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+  ctx->pmis_set = true;
+  ctx->grid_valid = false;
+  return FPPM_OK;
+}
 
 int fppm_gpu_counters(fppm_gpu_ctx *ctx, uint64_t out[4]) {
   if (!ctx || !out) return FPPM_ERR_INVALID_ARGUMENT;

@@ -45,6 +45,19 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
     }
     double p0 = 0.0, p1 = 0.0, p2 = 0.0;
 
+    // VCM+ eye Bsdf terms: cos_o (bsdf.cpp:34) and continuation probability
+    // (bsdf.cpp:42-51, std::max / std::min semantics)
+    double v_cos_o = 0.0, v_cont = 0.0, v_vcm = 0.0, v_vm = 0.0;
+    if (A.vcm) {
+      const double3 wo = A.wo[h], al = A.alb[h];
+      v_cos_o = edot(wo.x, wo.y, wo.z, Hs.nx, Hs.ny, Hs.nz);
+      const double m1 = al.y < al.z ? al.z : al.y;
+      const double amax = al.x < m1 ? m1 : al.x;
+      v_cont = amax < 1.0 ? amax : 1.0;
+      const double2 em = A.eye_mis[h];
+      v_vcm = em.x;
+      v_vm = em.y;
+    }
     if (gathered && grid.n > 0) {
       const long long ix = (long long)floor(dm(Hs.cx, grid.inv)) - grid.ix0;
       const long long iy = (long long)floor(dm(Hs.cy, grid.inv)) - grid.iy0;
@@ -92,6 +105,32 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
         if (!flush_pair(F, Hs, a, b, c2, A.guard, sector, cos_pos, my_exact, my_amb)) continue;
         ++my_acc;
         const float4 c3 = __ldg(&A.rec3[i]);
+        if (A.vcm) {
+          // merge callback (integrator.cpp:609-616): f and the pdfs of
+          // Bsdf::eval (bsdf.cpp:53-63), merge weight, val = thr * f * p.thr * w
+          const double ci = edot((double)b.w, (double)c2.x, (double)c2.y, Hs.nx, Hs.ny, Hs.nz);
+          const bool black = v_cos_o <= 0.0 || ci <= 0.0;
+          const double pf = black ? 0.0 : (ci > 0.0 ? dm(ci, kInvPi) : 0.0);
+          const double prv = black ? 0.0 : (v_cos_o > 0.0 ? dm(v_cos_o, kInvPi) : 0.0);
+          const double w = mis_weight_merge_dev(A.mis_n_vm, A.mis_beta, Hs.r, v_vcm, v_vm, A.p_vcm[i],
+                                                A.p_vm[i], dm(pf, v_cont), dm(prv, A.p_cont[i]));
+          const double k0 = ci <= 0.0 ? dm(Hs.K0, 0.0) : Hs.K0, k1 = ci <= 0.0 ? dm(Hs.K1, 0.0) : Hs.K1,
+                       k2 = ci <= 0.0 ? dm(Hs.K2, 0.0) : Hs.K2;
+          const double v0 = dm(dm(k0, (double)c2.z), w), v1 = dm(dm(k1, (double)c2.w), w),
+                       v2 = dm(dm(k2, (double)c3.x), w);
+          p0 += v0; p1 += v1; p2 += v2;
+#pragma unroll
+          for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
+          if constexpr (CH == 1) {
+            const double v = elum(v0, v1, v2);
+            acc_pred<GMAX>(sm[0], sq[0], sector, v, v * v);
+          } else {
+            acc_pred<GMAX>(sm[0], sq[0], sector, v0, v0 * v0);
+            acc_pred<GMAX>(sm[1], sq[1], sector, v1, v1 * v1);
+            acc_pred<GMAX>(sm[2], sq[2], sector, v2, v2 * v2);
+          }
+          continue;
+        }
         const double pr = cos_pos ? (double)c2.z : 0.0, pg = cos_pos ? (double)c2.w : 0.0,
                      pb_ = cos_pos ? (double)c3.x : 0.0;
         p0 += pr; p1 += pg; p2 += pb_;

@@ -52,6 +52,13 @@ struct GatherArgs {
   uint32_t *o_accepted;
   unsigned long long *snap_cnt;
   double *snap_sum, *snap_sq;
+  // VCM+ merge stage (warp kernel): MIS merge weight per pair
+  int vcm;
+  int mis_n_vm;
+  double mis_beta;
+  const double2 *eye_mis;                      // per hit point {d_vcm, d_vm}
+  const double *p_vcm, *p_vm, *p_cont;         // per photon, sorted order
+  const double3 *wo, *alb;                     // eye Bsdf (cos_o, continuation prob)
   // counters
   unsigned long long *counters;  // cumulative [accepted, candidates, exact, ambiguous]
   unsigned int *iter_tr;         // this launch [tested, rejected]
@@ -199,6 +206,8 @@ void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridH
                        uint32_t *keys, uint32_t *vals, int sms);
 void launch_pack_fine(cudaStream_t s, const float *pos, const float *nrm, const float *wi, const float *pw,
                       const uint32_t *depth, uint32_t n, float4 *pack, int sms);
+void launch_permute_f64x3(cudaStream_t s, const uint32_t *order, uint32_t n, const double *a,
+                          const double *b, const double *c, double *oa, double *ob, double *oc, int sms);
 void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const GridHeader *hdr,
                        uint32_t *start, unsigned long long ncells, int sms);
 void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const float *pos,

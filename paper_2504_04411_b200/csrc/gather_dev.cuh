@@ -333,6 +333,23 @@ static __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
   return x;
 }
 
+// ---------------------------------------------------------------- VCM+ merge weight
+// path.cpp:11-13
+static __device__ __forceinline__ double mis_pow_dev(double beta, double x) {
+  return beta == 1.0 ? x : pow(x, beta);
+}
+// path.cpp:103-111 with vc_factor (path.cpp:22-24) of eta_vm = n_vm pi r^2
+// (integrator.cpp:503), in the reference's operation order without FMA.
+static __device__ __forceinline__ double mis_weight_merge_dev(int n_vm, double beta, double r, double e_vcm,
+                                                              double e_vm, double l_vcm, double l_vm,
+                                                              double fwd, double rev) {
+  const double eta = dm(dm(dm((double)n_vm, kPi), r), r);
+  const double vcf = eta > 0.0 ? mis_pow_dev(beta, dd(1.0, eta)) : 0.0;
+  const double w_light = da(dm(l_vcm, vcf), dm(l_vm, mis_pow_dev(beta, fwd)));
+  const double w_camera = da(dm(e_vcm, vcf), dm(e_vm, mis_pow_dev(beta, rev)));
+  return dd(1.0, da(da(w_light, 1.0), w_camera));
+}
+
 // ---------------------------------------------------------------- end_iteration
 // f_statistic (stat_tests.cpp:12-44) with the reference's operation order.
 static __device__ double f_statistic_dev(const double *sum, const double *sq, int n, uint64_t m) {
@@ -440,7 +457,10 @@ static __device__ __forceinline__ void finalize_hit(const GatherArgs &A, uint32_
   uint32_t t = A.t[h];
   const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
   const double3 K = A.K[h];
-  const double fl0 = dm(K.x, p0), fl1 = dm(K.y, p1), fl2 = dm(K.z, p2);
+  // FPPM: p = sum of photon power over accepted pairs (flux = K p); VCM+:
+  // p = sum of the weighted values themselves (integrator.cpp:617)
+  const double fl0 = A.vcm ? p0 : dm(K.x, p0), fl1 = A.vcm ? p1 : dm(K.y, p1),
+               fl2 = A.vcm ? p2 : dm(K.z, p2);
   double r_new = r;
   double stat = 0.0, critical = 0.0;
   uint8_t flags = 0;

@@ -494,6 +494,25 @@ void launch_pack_fine(cudaStream_t s, const float *pos, const float *nrm, const 
   note_launches(1);
 }
 
+// VCM+ per-photon MIS data into sorted order
+__global__ void k_permute_f64x3(const uint32_t *__restrict__ order, uint32_t n, const double *__restrict__ a,
+                                const double *__restrict__ b, const double *__restrict__ c,
+                                double *__restrict__ oa, double *__restrict__ ob, double *__restrict__ oc) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t j = order[i];
+    oa[i] = a[j];
+    ob[i] = b[j];
+    oc[i] = c[j];
+  }
+}
+
+void launch_permute_f64x3(cudaStream_t s, const uint32_t *order, uint32_t n, const double *a,
+                          const double *b, const double *c, double *oa, double *ob, double *oc, int sms) {
+  if (n == 0) return;
+  k_permute_f64x3<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, a, b, c, oa, ob, oc);
+  note_launches(1);
+}
+
 void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridHeader *hdr,
                        uint32_t *keys, uint32_t *vals, int sms) {
   if (n == 0) return;

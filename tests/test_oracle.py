@@ -203,3 +203,41 @@ def test_thread_count_invariance(port):
         for k in a:
             if k != "times":
                 assert np.array_equal(a[k], b[k]), k
+
+
+def test_mis_weight_merge_matches_reference(port, ref):
+    """path.cpp:103-111 merge weight with eta_vm = n_vm pi r^2 (integrator.cpp:503)."""
+    rng = np.random.default_rng(5)
+    for beta in (1.0, 2.0):
+        for _ in range(300):
+            scale = rng.choice([0.0, 1e-3, 1.0, 1e3], 4)
+            args = (int(rng.integers(0, 1 << 22)), beta, float(rng.random() * 0.05),
+                    *map(float, rng.random(4) * scale), float(rng.random()), float(rng.random()))
+            a, b = port.mis_weight_merge(*args), ref.mis_weight_merge(*args)
+            assert a == b or (np.isnan(a) and np.isnan(b)), args
+
+
+@pytest.mark.parametrize("beta", [1.0, 2.0])
+def test_port_matches_reference_vcm_plus(port, ref, beta):
+    """VCM+ merge stage: photon values weighted by the MIS merge weight of the
+    tested radius (integrator.cpp:595-627); canonical raster + C2 photons with
+    random MIS partials, bit-identical to the reference build."""
+    W, N = 24, 1 << 13
+    hp = port.gen_raster_hitpoints(W)
+    cfg = dict(n_annuli=2, n_sectors=4, alpha_f=0.01, initial_radius=0.04, r_min_base=4e-5,
+               samples_per_iteration=N, threads=4, vcm_plus=1, mis_n_vm=N, mis_beta=beta)
+    sp, sr = port.session(cfg, hp), ref.session(cfg, hp)
+    rng = np.random.default_rng(9)
+    ev, em = rng.random(W * W) * 2, rng.random(W * W)
+    sp.set_eye_mis(ev, em)
+    sr.set_eye_mis(ev, em)
+    for it in range(1, 4):
+        ph = port.gen_photons(2, 0x5EED, it, 0, N)
+        pv, pm, pc = rng.random(N) * 3, rng.random(N), rng.random(N)
+        sp.set_photon_mis(pv, pm, pc)
+        sr.set_photon_mis(pv, pm, pc)
+        a, b = sp.iterate(it, ph), sr.iterate(it, ph)
+        assert a["accepted"].sum() > 0
+        for k in a:
+            if k != "times":
+                assert np.array_equal(a[k], b[k]), k
