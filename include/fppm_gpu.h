@@ -240,6 +240,40 @@ int fppm_gpu_set_samples_per_iteration(fppm_gpu_ctx *ctx, uint64_t samples_per_i
 int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration,
                            fppm_gpu_iter_out *out);
 
+/* ---- photon emission and tracing (integrator.cpp:230-265, path.cpp:388-449) ---- */
+/* Analytic scene (Scene, scene.hpp): spheres and quads, Lambertian / mirror /
+ * dielectric materials, area emitters on primitives.  Host arrays. */
+#define FPPM_MATERIAL_LAMBERTIAN 0
+#define FPPM_MATERIAL_MIRROR 1
+#define FPPM_MATERIAL_DIELECTRIC 2
+#define FPPM_SHAPE_SPHERE 0
+#define FPPM_SHAPE_QUAD 1
+typedef struct fppm_scene {
+  uint32_t n_materials;
+  const int32_t *material_kind;  /* FPPM_MATERIAL_* */
+  const double *material_rgb;    /* [n][3] albedo / reflectance / tint */
+  const double *material_ior;    /* [n] (dielectric) */
+  uint32_t n_primitives;
+  const int32_t *shape_kind;     /* FPPM_SHAPE_* */
+  const double *shape;           /* [n][9] sphere: center xyz, radius; quad: corner, e1, e2 */
+  const int32_t *shape_material; /* [n] */
+  uint32_t n_emitters;           /* area emitters */
+  const int32_t *emitter_shape;  /* [n] primitive the emitter lives on */
+  const double *emitter_radiance;/* [n][3] */
+} fppm_scene;
+int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *scene);
+/* Light phase of one iteration: traces light paths j = 0..n_paths-1 with
+ * RngStream(seed, iteration, j, kLightStream = 0) to light depth max_depth - 1
+ * and stages every non-delta deposit, in path order, as the photons of the
+ * next grid build (with VCM+ MIS partials when vcm_plus; eta_vm uses
+ * mis_radius, or the max live radius when mis_radius <= 0).  *n_photons
+ * receives the deposit count (synchronizes). */
+int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t n_paths,
+                           uint32_t max_depth, double mis_radius, uint32_t *n_photons);
+/* Copies the staged photons' VCM partials (d_vcm, d_vm, cont; photon order)
+ * to host arrays of n_photons doubles each (vcm_plus contexts only). */
+int fppm_gpu_get_photon_mis(fppm_gpu_ctx *ctx, double *d_vcm, double *d_vm, double *cont);
+
 /* ---- VCM+ merge stage inputs (host arrays) ---- */
 /* Eye-vertex MIS partials per hit point (PathVertex::mis d_vcm, d_vm). */
 int fppm_gpu_set_hitpoint_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const double *d_vm, uint32_t n);

@@ -133,6 +133,13 @@ class Oracle:
             self._si = fn("session_iterate", C.c_int, [C.c_void_p, C.c_uint64, _fp, _fp, _fp, _fp, _u32p, C.c_size_t, C.c_double, _u32p, C.c_size_t, C.POINTER(IterOut), _dp, _dp])
             self._anova = fn("anova_f_test", None, [_u64p, _dp, _dp, C.c_int, C.c_uint64, C.c_double, _dp, _ip])
             self._hw = fn("hardware_threads", C.c_uint, [])
+            self._scn = fn("scene_create", C.c_void_p, [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                        C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                        C.c_uint32, C.c_void_p, C.c_void_p])
+            self._scnf = fn("scene_free", None, [C.c_void_p])
+            self._trace = fn("trace_photons", C.c_size_t, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                                           C.c_uint32, C.c_uint32, C.c_int, C.c_double,
+                                                           C.c_double, C.c_int, C.c_size_t] + [C.c_void_p] * 7)
 
     # ---------------------------------------------------------- scalars
     def _call(self, f, *a):
@@ -197,6 +204,11 @@ class Oracle:
         return _Session(self, cfg, hit)
 
     # ---------------------------------------------------------- generators (port only)
+    def scene(self, arrays: dict):
+        if self.kind != "reference":
+            raise NotImplementedError("photon tracing is checked against the reference build only")
+        return _Scene(self, arrays)
+
     def gen_photons(self, workload, seed, iteration, begin, count):
         pos = np.zeros((count, 3), np.float32); nrm = np.zeros((count, 3), np.float32)
         wi = np.zeros((count, 3), np.float32); pw = np.zeros((count, 3), np.float32)
@@ -212,6 +224,34 @@ class Oracle:
         self._ghp(W, *[_ptr(a[k], _dp) for k in ("pos", "nrm", "wo", "thr", "alb")],
                   _ptr(a["eye_depth"], _u32p))
         return a
+
+
+class _Scene:
+    """The reference's own Scene + build_accel + trace_light_subpath (oracle/_ref)."""
+
+    def __init__(self, o, arrays):
+        self.o = o
+        a = self.a = {k: np.ascontiguousarray(v) for k, v in arrays.items()}
+        self.h = o._scn(len(a["material_kind"]), a["material_kind"].ctypes.data, a["material_rgb"].ctypes.data,
+                        a["material_ior"].ctypes.data, len(a["shape_kind"]), a["shape_kind"].ctypes.data,
+                        a["shape"].ctypes.data, a["shape_material"].ctypes.data, len(a["emitter_shape"]),
+                        a["emitter_shape"].ctypes.data, a["emitter_radiance"].ctypes.data)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o._scnf(self.h)
+            self.h = None
+
+    def trace(self, seed, iteration, n_paths, max_depth, n_vm=0, beta=1.0, eta_vm=0.0, threads=0, begin=0):
+        """light_phase's flattened vertices (fp64) for paths [begin, begin + n_paths)."""
+        end = begin + n_paths
+        n = self.o._trace(self.h, seed, iteration, begin, end, max_depth, n_vm, beta, eta_vm, threads, 0,
+                          *([None] * 7))
+        out = dict(pos=np.zeros((n, 3)), nrm=np.zeros((n, 3)), wi=np.zeros((n, 3)), pow=np.zeros((n, 3)),
+                   depth=np.zeros(n, np.uint32), path=np.zeros(n, np.uint32), mis=np.zeros((n, 3)))
+        self.o._trace(self.h, seed, iteration, begin, end, max_depth, n_vm, beta, eta_vm, threads, n,
+                      *[out[k].ctypes.data for k in ("pos", "nrm", "wi", "pow", "depth", "path", "mis")])
+        return out
 
 
 class _Grid:

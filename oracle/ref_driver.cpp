@@ -35,6 +35,8 @@
 #include "fppm/bsdf.hpp"
 #include "fppm/frame.hpp"
 #include "fppm/gather.hpp"
+#include "fppm/path.hpp"
+#include "fppm/scene.hpp"
 #include "fppm/sampling.hpp"
 #include "fppm/special_functions.hpp"
 #include "fppm/stat_tests.hpp"
@@ -431,6 +433,106 @@ int ref_session_iterate(void* sp, uint64_t iteration, const float* ppos,
   if (grid_seconds) *grid_seconds = std::chrono::duration<double>(t1 - t0).count();
   if (gather_seconds) *gather_seconds = std::chrono::duration<double>(t2 - t1).count();
   return failure;
+}
+
+// ---- light phase (Renderer::light_phase, integrator.cpp:230-265) ----------
+// Scene arrays mirror fppm_scene (include/fppm_gpu.h): materials kind 0
+// lambertian / 1 mirror / 2 dielectric with one rgb (albedo / reflectance /
+// tint) and ior; shapes kind 0 sphere (center, radius) / 1 quad (corner, e1,
+// e2) packed in 9 doubles; area emitters (shape, radiance).
+struct RefScene {
+  Scene scene;
+};
+
+void* ref_scene_create(uint32_t nm, const int32_t* mkind, const double* mrgb, const double* mior, uint32_t np,
+                       const int32_t* skind, const double* shape, const int32_t* smat, uint32_t ne,
+                       const int32_t* eshape, const double* erad) {
+  auto* rs = new RefScene;
+  Scene& sc = rs->scene;
+  for (uint32_t i = 0; i < nm; ++i) {
+    Material m;
+    const Rgb c{mrgb[3 * i], mrgb[3 * i + 1], mrgb[3 * i + 2]};
+    m.kind = mkind[i] == 0 ? MaterialKind::lambertian
+                           : (mkind[i] == 1 ? MaterialKind::mirror : MaterialKind::dielectric);
+    m.albedo = c;
+    m.reflectance = c;
+    m.tint = c;
+    m.ior = mior[i];
+    sc.materials.push_back(m);
+  }
+  for (uint32_t i = 0; i < np; ++i) {
+    Primitive p;
+    const double* q = shape + 9 * i;
+    if (skind[i] == 0) {
+      p.kind = ShapeKind::sphere;
+      p.sphere.center = {q[0], q[1], q[2]};
+      p.sphere.radius = q[3];
+    } else {
+      p.kind = ShapeKind::quad;
+      p.quad.corner = {q[0], q[1], q[2]};
+      p.quad.e1 = {q[3], q[4], q[5]};
+      p.quad.e2 = {q[6], q[7], q[8]};
+    }
+    p.material = smat[i];
+    sc.primitives.push_back(p);
+  }
+  for (uint32_t i = 0; i < ne; ++i) {
+    Emitter e;
+    e.kind = EmitterKind::area;
+    e.primitive = eshape[i];
+    e.radiance = Rgb{erad[3 * i], erad[3 * i + 1], erad[3 * i + 2]};
+    sc.primitives[static_cast<std::size_t>(eshape[i])].emitter = static_cast<int>(i);
+    sc.emitters.push_back(e);
+  }
+  build_accel(sc);
+  return rs;
+}
+
+void ref_scene_free(void* s) { delete static_cast<RefScene*>(s); }
+
+// Traces light paths [begin, end) of `iteration` with RngStream(seed,
+// iteration, j, kLightStream = 0) and light_depth = max_depth - 1, then
+// flattens the vertices in path order.  Writes up to `cap` vertices (fp64
+// pos/nrm/wi/pow [.][3], depth, path index, mis [.][3] = d_vcm, d_vm, cont)
+// and returns the total count (call again with a larger cap if it exceeds).
+size_t ref_trace_photons(void* sp, uint64_t seed, uint64_t iteration, uint32_t begin, uint32_t end,
+                         uint32_t max_depth, int n_vm, double beta, double eta_vm, int threads, size_t cap,
+                         double* pos, double* nrm, double* wi, double* pw, uint32_t* depth, uint32_t* path,
+                         double* mis) {
+  const Scene& sc = static_cast<RefScene*>(sp)->scene;
+  MisContext ctx;
+  ctx.n_vm = n_vm;
+  ctx.beta = beta;
+  ctx.eta_vm = eta_vm;
+  const uint32_t light_depth = max_depth > 0 ? max_depth - 1 : 0;
+  std::vector<LightPath> paths(end - begin);
+  parallel_ranges(threads, paths.size(), [&](std::size_t b, std::size_t e) {
+    for (std::size_t k = b; k < e; ++k) {
+      const std::size_t j = begin + k;
+      RngStream rng(seed, iteration, j, 0 /* kLightStream */);
+      paths[k] = trace_light_subpath(sc, ctx, static_cast<std::uint32_t>(j), light_depth, rng);
+    }
+  });
+  size_t n = 0;
+  for (const LightPath& p : paths)
+    for (const LightVertex& v : p.vertices) {
+      if (n < cap && pos) {
+        const double a[4][3] = {{v.position.x, v.position.y, v.position.z},
+                                {v.shading_normal.x, v.shading_normal.y, v.shading_normal.z},
+                                {v.wi.x, v.wi.y, v.wi.z},
+                                {v.throughput.r, v.throughput.g, v.throughput.b}};
+        double* dst[4] = {pos, nrm, wi, pw};
+        for (int f = 0; f < 4; ++f)
+          for (int c = 0; c < 3; ++c) dst[f][3 * n + c] = a[f][c];
+        depth[n] = v.depth;
+        path[n] = v.path_index;
+        mis[3 * n] = v.mis.d_vcm;
+        mis[3 * n + 1] = v.mis.d_vm;
+        mis[3 * n + 2] = v.cont;
+      }
+      ++n;
+    }
+  return n;
 }
 
 unsigned ref_hardware_threads() { return std::thread::hardware_concurrency(); }

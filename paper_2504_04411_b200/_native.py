@@ -156,6 +156,10 @@ _SIGS = [
     ("fppm_gpu_counters", C.c_int, [C.c_void_p, C.c_void_p]),
     ("fppm_gpu_set_hitpoint_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     ("fppm_gpu_set_photon_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    ("fppm_gpu_set_scene", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("fppm_gpu_trace_photons", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_double,
+                                         C.POINTER(C.c_uint32)]),
+    ("fppm_gpu_get_photon_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fppm_gpu_schedule_radius", C.c_double, [C.c_double, C.c_double, C.c_uint64]),
     ("fppm_gpu_f_quantile", C.c_double, [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int)]),
     ("fppm_gpu_chi2_quantile", C.c_double, [C.c_double, C.c_double, C.POINTER(C.c_int)]),

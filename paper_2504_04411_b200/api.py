@@ -269,6 +269,31 @@ class FppmContext:
         self._check(self._lib.fppm_gpu_generate_photons(self._h, workload, seed, iteration, begin, n))
         self.N = n
 
+    def set_scene(self, scene):
+        """Upload an analytic scene (paper_2504_04411_b200.scene.Scene)."""
+        from .scene import to_struct
+        st, keep = to_struct(scene)
+        self._check(self._lib.fppm_gpu_set_scene(self._h, C.byref(st)))
+        del keep
+
+    def trace_photons(self, seed: int, iteration: int, n_paths: int, max_depth: int,
+                      mis_radius: float = 0.0) -> int:
+        """Renderer::light_phase (integrator.cpp:230-265) on the device: traces
+        n_paths light sub-paths and stages their non-delta vertices, in path
+        order, as the photons of the next grid build.  Returns the count."""
+        n = C.c_uint32()
+        self._check(self._lib.fppm_gpu_trace_photons(self._h, seed, iteration, n_paths, max_depth,
+                                                     mis_radius, C.byref(n)))
+        self.N = n.value
+        return n.value
+
+    def get_photon_mis(self) -> dict:
+        n = self.N
+        o = dict(d_vcm=np.zeros(n), d_vm=np.zeros(n), cont=np.zeros(n))
+        self._check(self._lib.fppm_gpu_get_photon_mis(self._h, o["d_vcm"].ctypes.data, o["d_vm"].ctypes.data,
+                                                      o["cont"].ctypes.data))
+        return o
+
     def get_photons(self) -> dict:
         n = self.N
         o = dict(pos=np.zeros((n, 3), np.float32), nrm=np.zeros((n, 3), np.float32),

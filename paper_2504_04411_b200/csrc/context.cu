@@ -49,6 +49,15 @@ struct fppm_gpu_ctx {
   const float *in_pos = nullptr, *in_nrm = nullptr, *in_wi = nullptr, *in_pow = nullptr;
   const uint32_t *in_depth = nullptr;
 
+  // light phase: scene on the device + per-path deposit slots
+  fppm_b200::TraceScene scene{};
+  void *scene_mem[8] = {};
+  bool has_scene = false;
+  float *t_pos = nullptr, *t_nrm = nullptr, *t_wi = nullptr, *t_pow = nullptr;
+  uint32_t *t_depth = nullptr, *t_count = nullptr, *t_base = nullptr, *t_scan = nullptr;
+  double *t_mis = nullptr;
+  unsigned long long t_slot_cap = 0, t_path_cap = 0;
+
   // VCM+ merge stage inputs
   double2 *d_eye_mis = nullptr;                                   // [H] {d_vcm, d_vm}
   double *d_pmis_in[3] = {nullptr, nullptr, nullptr};             // [N] photon order
@@ -283,6 +292,22 @@ static int copy_iter_out(fppm_gpu_ctx *ctx, fppm_gpu_iter_out *out, bool with_ga
 
 using namespace fppm_b200;
 
+#define UPLOAD_OK(x)                                                       \
+  do {                                                                     \
+    cudaError_t e_ = (x);                                                  \
+    if (e_ != cudaSuccess) return fail(ctx, FPPM_ERR_CUDA, cudaGetErrorString(e_)); \
+  } while (0)
+template <typename T>
+static int upload(fppm_gpu_ctx *ctx, void *&slot, const T *src, size_t n) {
+  if (slot) cudaFree(slot);
+  slot = nullptr;
+  UPLOAD_OK(cudaMalloc(&slot, sizeof(T) * (n ? n : 1)));
+  if (n) UPLOAD_OK(cudaMemcpy(slot, src, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return FPPM_OK;
+}
+
+#undef UPLOAD_OK
+
 extern "C" {
 
 int fppm_gpu_abi_version(void) { return FPPM_GPU_ABI_VERSION; }
@@ -441,6 +466,14 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
   if (ctx->d_eye_mis) cudaFree(ctx->d_eye_mis);
+  for (void *p : ctx->scene_mem)
+    if (p) cudaFree(p);
+  {
+    void *tp[] = {ctx->t_pos, ctx->t_nrm, ctx->t_wi, ctx->t_pow, ctx->t_depth, ctx->t_count, ctx->t_base,
+                  ctx->t_scan, ctx->t_mis};
+    for (void *p : tp)
+      if (p) cudaFree(p);
+  }
   for (int i = 0; i < 3; ++i) {
     if (ctx->d_pmis_in[i]) cudaFree(ctx->d_pmis_in[i]);
     if (ctx->d_pmis[i]) cudaFree(ctx->d_pmis[i]);
@@ -1168,6 +1201,137 @@ int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_
 }
 
 uint64_t fppm_gpu_kernel_launches(void) { return g_kernel_launches.load(); }
+
+int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *sc) {
+  if (!ctx || !sc) return FPPM_ERR_INVALID_ARGUMENT;
+  const uint32_t nm = sc->n_materials, np = sc->n_primitives, ne = sc->n_emitters;
+  if ((nm && (!sc->material_kind || !sc->material_rgb || !sc->material_ior)) ||
+      (np && (!sc->shape_kind || !sc->shape || !sc->shape_material)) ||
+      (ne && (!sc->emitter_shape || !sc->emitter_radiance)))
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null scene array");
+  for (uint32_t i = 0; i < nm; ++i)
+    if (sc->material_kind[i] < 0 || sc->material_kind[i] > 2)
+      return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unsupported material kind");
+  for (uint32_t i = 0; i < np; ++i)
+    if (sc->shape_kind[i] < 0 || sc->shape_kind[i] > 1 || sc->shape_material[i] < 0 ||
+        (uint32_t)sc->shape_material[i] >= nm)
+      return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "bad primitive");
+  for (uint32_t i = 0; i < ne; ++i)
+    if (sc->emitter_shape[i] < 0 || (uint32_t)sc->emitter_shape[i] >= np)
+      return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "bad emitter primitive");
+  int rc;
+  if ((rc = upload(ctx, ctx->scene_mem[0], sc->material_kind, nm)) ||
+      (rc = upload(ctx, ctx->scene_mem[1], sc->material_rgb, 3 * (size_t)nm)) ||
+      (rc = upload(ctx, ctx->scene_mem[2], sc->material_ior, nm)) ||
+      (rc = upload(ctx, ctx->scene_mem[3], sc->shape_kind, np)) ||
+      (rc = upload(ctx, ctx->scene_mem[4], sc->shape, 9 * (size_t)np)) ||
+      (rc = upload(ctx, ctx->scene_mem[5], sc->shape_material, np)) ||
+      (rc = upload(ctx, ctx->scene_mem[6], sc->emitter_shape, ne)) ||
+      (rc = upload(ctx, ctx->scene_mem[7], sc->emitter_radiance, 3 * (size_t)ne)))
+    return rc;
+  fppm_b200::TraceScene &t = ctx->scene;
+  t.n_mat = (int)nm;
+  t.n_prim = (int)np;
+  t.n_emit = (int)ne;
+  t.mat_kind = static_cast<const int *>(ctx->scene_mem[0]);
+  t.mat_rgb = static_cast<const double *>(ctx->scene_mem[1]);
+  t.mat_ior = static_cast<const double *>(ctx->scene_mem[2]);
+  t.prim_kind = static_cast<const int *>(ctx->scene_mem[3]);
+  t.prim = static_cast<const double *>(ctx->scene_mem[4]);
+  t.prim_mat = static_cast<const int *>(ctx->scene_mem[5]);
+  t.emit_prim = static_cast<const int *>(ctx->scene_mem[6]);
+  t.emit_rad = static_cast<const double *>(ctx->scene_mem[7]);
+  ctx->has_scene = true;
+  return FPPM_OK;
+}
+
+int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t n_paths,
+                           uint32_t max_depth, double mis_radius, uint32_t *n_photons) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->has_scene) return fail(ctx, FPPM_ERR_STATE, "trace_photons before set_scene");
+  cudaStream_t s = ctx->stream;
+  const uint32_t depth = max_depth > 0 ? max_depth - 1 : 0;  // light_phase: max_depth - 1
+  const unsigned long long slots = (unsigned long long)n_paths * depth;
+  if (slots > ctx->t_slot_cap) {
+    void *tp[] = {ctx->t_pos, ctx->t_nrm, ctx->t_wi, ctx->t_pow, ctx->t_depth, ctx->t_mis};
+    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    for (void *p : tp)
+      if (p) cudaFree(p);
+    const unsigned long long cap = std::max<unsigned long long>(slots, 1024);
+    FPPM_CUDA_OK(dalloc(&ctx->t_pos, 3 * cap)); FPPM_CUDA_OK(dalloc(&ctx->t_nrm, 3 * cap));
+    FPPM_CUDA_OK(dalloc(&ctx->t_wi, 3 * cap)); FPPM_CUDA_OK(dalloc(&ctx->t_pow, 3 * cap));
+    FPPM_CUDA_OK(dalloc(&ctx->t_depth, cap));
+    ctx->t_mis = nullptr;
+    if (ctx->cfg.vcm_plus) FPPM_CUDA_OK(dalloc(&ctx->t_mis, 3 * cap));
+    ctx->t_slot_cap = cap;
+  }
+  if ((unsigned long long)n_paths + 1 > ctx->t_path_cap) {
+    void *tp[] = {ctx->t_count, ctx->t_base, ctx->t_scan};
+    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    for (void *p : tp)
+      if (p) cudaFree(p);
+    const unsigned long long cap = std::max<unsigned long long>(2ull * (n_paths + 1), 4096);
+    FPPM_CUDA_OK(dalloc(&ctx->t_count, cap));
+    FPPM_CUDA_OK(dalloc(&ctx->t_base, cap));
+    FPPM_CUDA_OK(dalloc(&ctx->t_scan, cap / 4096 + 8));
+    ctx->t_path_cap = cap;
+  }
+  double eta = 0.0;
+  if (ctx->cfg.vcm_plus) {
+    double r = mis_radius;
+    if (!(r > 0.0)) {
+      int rc = fppm_gpu_max_radius(ctx, &r);
+      if (rc) return rc;
+    }
+    eta = (double)ctx->cfg.mis_n_vm * 3.141592653589793 * r * r;  // integrator.cpp:171-174
+  }
+  fppm_b200::TraceArgs T;
+  T.sc = ctx->scene;
+  T.seed = seed;
+  T.iteration = iteration;
+  T.n_paths = n_paths;
+  T.light_depth = depth;
+  T.n_vm = ctx->cfg.mis_n_vm;
+  T.beta = ctx->cfg.mis_beta > 0.0 ? ctx->cfg.mis_beta : 1.0;
+  T.eta_vm = eta;
+  T.v_pos = ctx->t_pos; T.v_nrm = ctx->t_nrm; T.v_wi = ctx->t_wi; T.v_pow = ctx->t_pow;
+  T.v_depth = ctx->t_depth;
+  T.v_mis = ctx->cfg.vcm_plus ? ctx->t_mis : nullptr;
+  T.count = ctx->t_count;
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->t_count + n_paths, 0, sizeof(uint32_t), s));
+  FPPM_CUDA_OK(launch_trace(s, T, ctx->sms));
+  FPPM_CUDA_OK(launch_exclusive_scan(s, ctx->t_count, n_paths + 1, ctx->t_scan, ctx->t_base));
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, ctx->t_base + n_paths, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               s));
+  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  const uint32_t total = ctx->h_total[0];
+  if (total > ctx->cfg.max_photons)
+    return fail(ctx, FPPM_ERR_CAPACITY, "traced deposits exceed max_photons");
+  // the deposits become the staged photons (set 0) of the next grid build
+  if (ctx->stage_pending == 0 && ctx->ev_copied[0])
+    FPPM_CUDA_OK(cudaStreamWaitEvent(s, ctx->ev_copied[0], 0));
+  ctx->stage_pending = -1;
+  FPPM_CUDA_OK(launch_trace_compact(s, T, ctx->t_base, ctx->d_ppos, ctx->d_pnrm, ctx->d_pwi, ctx->d_ppow,
+                                    ctx->d_pdepth, ctx->cfg.vcm_plus ? ctx->d_pmis_in[0] : nullptr,
+                                    ctx->d_pmis_in[1], ctx->d_pmis_in[2], ctx->sms));
+  ctx->N = total;
+  ctx->grid_valid = false;
+  use_staging(ctx);
+  if (n_photons) *n_photons = total;
+  return FPPM_OK;
+}
+
+int fppm_gpu_get_photon_mis(fppm_gpu_ctx *ctx, double *d_vcm, double *d_vm, double *cont) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->cfg.vcm_plus || !ctx->d_pmis_in[0]) return fail(ctx, FPPM_ERR_STATE, "context is not vcm_plus");
+  double *dst[3] = {d_vcm, d_vm, cont};
+  for (int i = 0; i < 3; ++i)
+    if (dst[i] && ctx->N)
+      FPPM_CUDA_OK(cudaMemcpyAsync(dst[i], ctx->d_pmis_in[i], sizeof(double) * ctx->N, cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  return FPPM_OK;
+}
 
 int fppm_gpu_set_hitpoint_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const double *d_vm, uint32_t n) {
   if (!ctx || (n && (!d_vcm || !d_vm))) return FPPM_ERR_INVALID_ARGUMENT;

@@ -218,6 +218,34 @@ void launch_query_ball(cudaStream_t s, const double *centers, const double *radi
                        const uint32_t *order, unsigned long long *counts,
                        const unsigned long long *offsets, uint32_t *out, int fill);
 
+// trace.cu (light phase on analytic geometry)
+struct TraceScene {
+  int n_mat, n_prim, n_emit;
+  const int *mat_kind;      // FPPM_MATERIAL_*
+  const double *mat_rgb;    // [n][3]
+  const double *mat_ior;
+  const int *prim_kind;     // FPPM_SHAPE_*
+  const double *prim;       // [n][9]
+  const int *prim_mat;
+  const int *emit_prim;
+  const double *emit_rad;   // [n][3]
+};
+struct TraceArgs {
+  TraceScene sc;
+  unsigned long long seed, iteration;
+  uint32_t n_paths, light_depth;
+  int n_vm;
+  double beta, eta_vm;
+  float *v_pos, *v_nrm, *v_wi, *v_pow;  // per path slots [n_paths][light_depth][3]
+  uint32_t *v_depth;
+  double *v_mis;                        // [.][3] d_vcm, d_vm, cont (nullable)
+  uint32_t *count;                      // [n_paths]
+};
+cudaError_t launch_trace(cudaStream_t s, const TraceArgs &A, int sms);
+cudaError_t launch_trace_compact(cudaStream_t s, const TraceArgs &A, const uint32_t *base, float *pos,
+                                 float *nrm, float *wi, float *pw, uint32_t *depth, double *mv, double *mm,
+                                 double *mc, int sms);
+
 // generate.cu
 void launch_generate_photons(cudaStream_t s, int workload, uint64_t seed, uint64_t iteration,
                              uint64_t begin, uint32_t n, float *pos, float *nrm, float *wi,
