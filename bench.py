@@ -45,6 +45,8 @@ def parse():
                    help="gather kernel variant (A/B)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-trace", action="store_true", help="skip the light-phase (photons traced/s) leg")
+    p.add_argument("--cpu-trace-paths", type=int, default=1 << 20)
     p.add_argument("--cpu-stride", type=int, default=0,
                    help="hit-point stride of the CPU sample (0 = auto)")
     return p.parse_args()
@@ -200,7 +202,78 @@ def run_reference_arm(args, wl, rank):
           "config": workload_config(wl),
           "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                            "sample": sample},
-          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+          "trace": reference_trace(threads, args)})
+
+
+def reference_trace(threads, args):
+    if args.no_trace:
+        return None
+    try:
+        paths = args.cpu_trace_paths
+        dep, secs = cpu_trace_run(paths, threads)
+        return {"photons_traced_per_s": dep / secs, "light_paths_per_s": paths / secs, "cores": threads,
+                "kind": "reference", "sample": f"{paths} light paths of iteration 1 (of {TRACE_PATHS})",
+                "config": trace_config()}
+    except Exception as e:
+        return {"unavailable": f"reference tracer failed: {e}"}
+
+
+# ---------------------------------------------------------------- light phase
+TRACE_PATHS = 1 << 23      # BASELINE configs[2]: 8M photons (light paths) per iteration
+TRACE_MAX_DEPTH = 8        # maximum path length 8
+
+
+def trace_config():
+    return {"workload": "c3 light phase (BASELINE configs[2]): caustic box (scene.caustic_box), "
+                        f"{TRACE_PATHS} light paths per iteration, max_depth {TRACE_MAX_DEPTH}",
+            "roulette": "from depth 5 (reference kRouletteDepth, path.hpp:156)"}
+
+
+def cpu_trace_run(paths, threads, iteration=1):
+    """Reference light phase (oracle/_ref: Scene + BVH + trace_light_subpath)
+    on `paths` light paths with `threads` host threads.  (deposits, seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle
+    from paper_2504_04411_b200.scene import caustic_box
+    sc = Oracle("reference").scene(caustic_box().arrays())
+    t0 = time.perf_counter()
+    out = sc.trace(0x5EED, iteration, paths, TRACE_MAX_DEPTH, threads=threads)
+    return len(out["depth"]), time.perf_counter() - t0
+
+
+def run_trace_bench(args, local_rank, steps, warmup):
+    """photons traced/s: fppm_gpu_trace_photons (emission + tracing + path-order
+    compaction into the staging buffers of the next grid build), timed with
+    CUDA events on the context stream."""
+    import torch
+    from paper_2504_04411_b200 import FppmContext
+    from paper_2504_04411_b200.scene import caustic_box
+    ctx = FppmContext(initial_radius=0.01, samples_per_iteration=TRACE_PATHS, max_hitpoints=1,
+                      max_photons=4 * TRACE_PATHS, device=local_rank)
+    ctx.set_scene(caustic_box())
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    for it in range(1, warmup + 1):
+        ctx.trace_photons(0x5EED, it, TRACE_PATHS, TRACE_MAX_DEPTH)
+    torch.cuda.synchronize()
+    l0 = FppmContext.kernel_launches()
+    ms, dep = [], 0
+    for it in range(warmup + 1, warmup + steps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dep += ctx.trace_photons(0x5EED, it, TRACE_PATHS, TRACE_MAX_DEPTH)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    launches = FppmContext.kernel_launches() - l0
+    ctx.close()
+    secs = sum(ms) / 1e3
+    return {"photons_traced_per_s": dep / secs, "light_paths_per_s": TRACE_PATHS * steps / secs,
+            "ms_per_iteration": 1e3 * secs / steps, "deposits_per_iteration": dep / steps,
+            "gpu_launches": launches, "steps": steps,
+            "timing": "CUDA events around fppm_gpu_trace_photons on the context stream",
+            "config": trace_config()}
 
 
 def workload_config(wl, **extra):
@@ -353,6 +426,12 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    trace = None
+    if not args.no_trace:
+        trace = run_trace_bench(args, local_rank, max(args.steps, 1), max(args.warmup, 1))
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            trace["cpu_baseline"] = reference_trace(os.cpu_count() or 1, args)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -389,6 +468,8 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
+        if trace:
+            line["trace"] = trace
         emit(line)
     ctx.close()
 
