@@ -51,7 +51,8 @@ struct fppm_gpu_ctx {
 
   // light phase: scene on the device + per-path deposit slots
   fppm_b200::TraceScene scene{};
-  void *scene_mem[8] = {};
+  void *scene_mem[9] = {};  // [8]: per-primitive constants (k_scene_prep)
+  uint32_t *t_ctr = nullptr;
   bool has_scene = false;
   float *t_pos = nullptr, *t_nrm = nullptr, *t_wi = nullptr, *t_pow = nullptr;
   uint32_t *t_depth = nullptr, *t_count = nullptr, *t_base = nullptr, *t_scan = nullptr;
@@ -470,7 +471,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   {
     void *tp[] = {ctx->t_pos, ctx->t_nrm, ctx->t_wi, ctx->t_pow, ctx->t_depth, ctx->t_count, ctx->t_base,
-                  ctx->t_scan, ctx->t_mis};
+                  ctx->t_scan, ctx->t_mis, ctx->t_ctr};
     for (void *p : tp)
       if (p) cudaFree(p);
   }
@@ -1212,6 +1213,8 @@ int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *sc) {
   for (uint32_t i = 0; i < nm; ++i)
     if (sc->material_kind[i] < 0 || sc->material_kind[i] > 2)
       return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unsupported material kind");
+  if (np > (uint32_t)fppm_b200::trace_max_prims())
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "scene has more primitives than the tracer supports");
   for (uint32_t i = 0; i < np; ++i)
     if (sc->shape_kind[i] < 0 || sc->shape_kind[i] > 1 || sc->shape_material[i] < 0 ||
         (uint32_t)sc->shape_material[i] >= nm)
@@ -1241,6 +1244,11 @@ int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *sc) {
   t.prim_mat = static_cast<const int *>(ctx->scene_mem[5]);
   t.emit_prim = static_cast<const int *>(ctx->scene_mem[6]);
   t.emit_rad = static_cast<const double *>(ctx->scene_mem[7]);
+  if (ctx->scene_mem[8]) cudaFree(ctx->scene_mem[8]);
+  ctx->scene_mem[8] = nullptr;
+  FPPM_CUDA_OK(cudaMalloc(&ctx->scene_mem[8], fppm_b200::trace_prep_bytes((int)np)));
+  FPPM_CUDA_OK(fppm_b200::launch_scene_prep(ctx->stream, t, ctx->scene_mem[8]));
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
   ctx->has_scene = true;
   return FPPM_OK;
 }
@@ -1299,7 +1307,9 @@ int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration,
   T.v_mis = ctx->cfg.vcm_plus ? ctx->t_mis : nullptr;
   T.count = ctx->t_count;
   FPPM_CUDA_OK(cudaMemsetAsync(ctx->t_count + n_paths, 0, sizeof(uint32_t), s));
-  FPPM_CUDA_OK(launch_trace(s, T, ctx->sms));
+  if (!ctx->t_ctr) FPPM_CUDA_OK(dalloc(&ctx->t_ctr, 1));
+  T.path_counter = ctx->t_ctr;
+  FPPM_CUDA_OK(launch_trace(s, T, ctx->scene_mem[8], ctx->sms));
   FPPM_CUDA_OK(launch_exclusive_scan(s, ctx->t_count, n_paths + 1, ctx->t_scan, ctx->t_base));
   FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, ctx->t_base + n_paths, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                s));

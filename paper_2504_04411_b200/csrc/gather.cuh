@@ -240,8 +240,12 @@ struct TraceArgs {
   uint32_t *v_depth;
   double *v_mis;                        // [.][3] d_vcm, d_vm, cont (nullable)
   uint32_t *count;                      // [n_paths]
+  uint32_t *path_counter;               // work queue (reset by launch_trace)
 };
-cudaError_t launch_trace(cudaStream_t s, const TraceArgs &A, int sms);
+size_t trace_prep_bytes(int n_prim);
+int trace_max_prims();
+cudaError_t launch_scene_prep(cudaStream_t s, const TraceScene &sc, void *prep);
+cudaError_t launch_trace(cudaStream_t s, const TraceArgs &A, const void *prep, int sms);
 cudaError_t launch_trace_compact(cudaStream_t s, const TraceArgs &A, const uint32_t *base, float *pos,
                                  float *nrm, float *wi, float *pw, uint32_t *depth, double *mv, double *mm,
                                  double *mc, int sms);

@@ -39,6 +39,7 @@ __device__ __forceinline__ DVec normalize(DVec a) { return divs(a, __dsqrt_rn(do
 // rng.hpp RngStream
 struct Rng {
   unsigned long long s;
+  Rng() = default;
   __device__ static unsigned long long mix(unsigned long long z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
@@ -96,13 +97,55 @@ struct Mis {
 };
 __device__ __forceinline__ double mpow(double beta, double x) { return beta == 1.0 ? x : pow(x, beta); }
 
+// Per-primitive constants hoisted out of the hit tests: every value is the
+// same IEEE expression the reference evaluates per call (cross(e1, e2), the
+// Gram entries, r * r, 1 / r, 1 / area), so hoisting changes no bit.
+struct PrimD {
+  int kind, mat;
+  double c[3], e1[3], e2[3];
+  double n[3];   // quad: cross(e1, e2)
+  double on[3];  // quad: normalize(cross(e1, e2))
+  double a11, a12, a22, det;
+  double r, r2, inv_r;
+  double inv_area;  // 1 / primitive_area (scene_geometry.cpp:320-338)
+};
+constexpr int kMaxTracePrims = 96;
+
+__global__ void k_scene_prep(const TraceScene sc, PrimD *out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sc.n_prim) return;
+  const double *p = sc.prim + 9 * (size_t)i;
+  PrimD d;
+  d.kind = sc.prim_kind[i];
+  d.mat = sc.prim_mat[i];
+  for (int k = 0; k < 3; ++k) {
+    d.c[k] = p[k];
+    d.e1[k] = p[3 + k];
+    d.e2[k] = p[6 + k];
+  }
+  d.r = p[3];
+  d.r2 = dm(p[3], p[3]);
+  d.inv_r = dd(1.0, p[3]);
+  const DVec e1 = dv(p[3], p[4], p[5]), e2 = dv(p[6], p[7], p[8]);
+  const DVec n = cross(e1, e2);
+  d.n[0] = n.x; d.n[1] = n.y; d.n[2] = n.z;
+  const DVec on = normalize(n);
+  d.on[0] = on.x; d.on[1] = on.y; d.on[2] = on.z;
+  d.a11 = dot(e1, e1);
+  d.a12 = dot(e1, e2);
+  d.a22 = dot(e2, e2);
+  d.det = ds(dm(d.a11, d.a22), dm(d.a12, d.a12));
+  const double area = d.kind == 0 ? dm(dm(dm(4.0, kPi), p[3]), p[3]) : __dsqrt_rn(dot(n, n));
+  d.inv_area = dd(1.0, area);
+  out[i] = d;
+}
+
 // intersect_sphere (scene_geometry.cpp:11-26)
-__device__ __forceinline__ bool hit_sphere(const double *p, DVec o, DVec d, double tmin, double tmax,
+__device__ __forceinline__ bool hit_sphere(const PrimD &p, DVec o, DVec d, double tmin, double tmax,
                                            double &t) {
-  const DVec c = dv(p[0], p[1], p[2]);
-  const DVec oc = sub(o, c);
+  const DVec oc = sub(o, dv(p.c[0], p.c[1], p.c[2]));
   const double b = dot(oc, d);
-  const double cc = ds(dot(oc, oc), dm(p[3], p[3]));
+  const double cc = ds(dot(oc, oc), p.r2);
   const double disc = ds(dm(b, b), cc);
   if (disc < 0.0) return false;
   const double sq = __dsqrt_rn(disc);
@@ -119,21 +162,20 @@ __device__ __forceinline__ bool hit_sphere(const double *p, DVec o, DVec d, doub
 }
 
 // intersect_quad (scene_geometry.cpp:28-45)
-__device__ __forceinline__ bool hit_quad(const double *p, DVec o, DVec d, double tmin, double tmax,
+__device__ __forceinline__ bool hit_quad(const PrimD &p, DVec o, DVec d, double tmin, double tmax,
                                          double &t) {
-  const DVec corner = dv(p[0], p[1], p[2]), e1 = dv(p[3], p[4], p[5]), e2 = dv(p[6], p[7], p[8]);
-  const DVec n = cross(e1, e2);
+  const DVec n = dv(p.n[0], p.n[1], p.n[2]);
   const double denom = dot(d, n);
   if (denom == 0.0) return false;
+  const DVec corner = dv(p.c[0], p.c[1], p.c[2]);
   const double tt = dd(dot(sub(corner, o), n), denom);
   if (tt <= tmin || tt >= tmax) return false;
+  const DVec e1 = dv(p.e1[0], p.e1[1], p.e1[2]), e2 = dv(p.e2[0], p.e2[1], p.e2[2]);
   const DVec rel = sub(add(o, mul(d, tt)), corner);
-  const double a11 = dot(e1, e1), a12 = dot(e1, e2), a22 = dot(e2, e2);
   const double b1 = dot(rel, e1), b2 = dot(rel, e2);
-  const double det = ds(dm(a11, a22), dm(a12, a12));
-  if (det == 0.0) return false;
-  const double u = dd(ds(dm(b1, a22), dm(b2, a12)), det);
-  const double v = dd(ds(dm(b2, a11), dm(b1, a12)), det);
+  if (p.det == 0.0) return false;
+  const double u = dd(ds(dm(b1, p.a22), dm(b2, p.a12)), p.det);
+  const double v = dd(ds(dm(b2, p.a11), dm(b1, p.a12)), p.det);
   if (u < 0.0 || u > 1.0 || v < 0.0 || v > 1.0) return false;
   t = tt;
   return true;
@@ -141,47 +183,41 @@ __device__ __forceinline__ bool hit_quad(const double *p, DVec o, DVec d, double
 
 struct HitD {
   double t;
-  DVec point, gn, sn;
+  DVec point, sn;
   bool front;
   int mat;
 };
 
-// intersect + fill_hit (scene_geometry.cpp:186-224, 263-315), closest hit
-// over all primitives in declaration order.
-__device__ bool intersect(const TraceScene &sc, DVec o, DVec d, HitD &h) {
+// intersect + fill_hit (scene_geometry.cpp:186-224, 263-315): closest hit
+// over all primitives in declaration order (strict '<' keeps the first of
+// equal distances; the reference's BVH visits leaves in a fixed order, so a
+// tie between two primitives at bit-identical t is the only case that could
+// pick differently).
+__device__ __forceinline__ bool intersect(const PrimD *P, int np, DVec o, DVec d, HitD &h) {
   double tbest = 1e300;
   int best = -1;
-  for (int i = 0; i < sc.n_prim; ++i) {
-    const double *p = sc.prim + 9 * (size_t)i;
+  for (int i = 0; i < np; ++i) {
     double t;
-    const bool ok = sc.prim_kind[i] == 0 ? hit_sphere(p, o, d, 1e-6, tbest, t)
-                                         : hit_quad(p, o, d, 1e-6, tbest, t);
+    const bool ok = P[i].kind == 0 ? hit_sphere(P[i], o, d, 1e-6, tbest, t) : hit_quad(P[i], o, d, 1e-6, tbest, t);
     if (ok && t < tbest) {
       tbest = t;
       best = i;
     }
   }
   if (best < 0) return false;
-  const double *p = sc.prim + 9 * (size_t)best;
+  const PrimD &p = P[best];
   h.t = tbest;
   h.point = add(o, mul(d, tbest));
-  h.mat = sc.prim_mat[best];
+  h.mat = p.mat;
   DVec outward;
-  if (sc.prim_kind[best] == 0)
-    outward = mul(sub(h.point, dv(p[0], p[1], p[2])), dd(1.0, p[3]));
+  if (p.kind == 0)
+    outward = mul(sub(h.point, dv(p.c[0], p.c[1], p.c[2])), p.inv_r);
   else
-    outward = normalize(cross(dv(p[3], p[4], p[5]), dv(p[6], p[7], p[8])));
+    outward = dv(p.on[0], p.on[1], p.on[2]);
   h.front = dot(d, outward) < 0.0;
-  h.gn = h.front ? outward : neg(outward);
-  h.sn = dot(outward, h.gn) < 0.0 ? neg(outward) : outward;
+  const DVec gn = h.front ? outward : neg(outward);
+  h.sn = dot(outward, gn) < 0.0 ? neg(outward) : outward;
   return true;
-}
-
-__device__ __forceinline__ double prim_area(const TraceScene &sc, int i) {
-  const double *p = sc.prim + 9 * (size_t)i;
-  if (sc.prim_kind[i] == 0) return dm(dm(dm(4.0, kPi), p[3]), p[3]);
-  const DVec c = cross(dv(p[3], p[4], p[5]), dv(p[6], p[7], p[8]));
-  return __dsqrt_rn(dot(c, c));
 }
 
 // bsdf.cpp:41-51 (min(1, max component))
@@ -192,211 +228,315 @@ __device__ __forceinline__ double cont_prob(const TraceScene &sc, int m) {
   return mx < 1.0 ? mx : 1.0;
 }
 
-__global__ void __launch_bounds__(128) k_trace_paths(const TraceArgs A) {
+struct PathState {
+  Rng rng;
+  DVec o, dir;
+  double t0, t1, t2;
+  Mis mis;
+  uint32_t depth, nv, j;
+};
+
+// Emission (trace_light_subpath prologue, path.cpp:392-407; sample_emission
+// area branch, path.cpp:180-195, 222-236).  False: the path deposits nothing.
+__device__ __forceinline__ bool start_path(const TraceArgs &A, const PrimD *P, PathState &s, uint32_t j,
+                                           double vcf) {
   const TraceScene &sc = A.sc;
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < A.n_paths; j += gridDim.x * blockDim.x) {
-    uint32_t nv = 0;
-    Rng rng(A.seed, A.iteration, j, 0ull /* kLightStream */);
-    const size_t slot = (size_t)j * A.light_depth;
-    if (sc.n_emit > 0) {
-      // emitter pick (path.cpp:392-397)
-      const int n = sc.n_emit;
-      int pick = (int)dm(rng.next(), (double)n);
-      if (pick > n - 1) pick = n - 1;
-      const double pick_prob = dd(1.0, (double)n);
-      // area emission (path.cpp:180-195, 222-236)
-      const int pi = sc.emit_prim[pick];
-      const double *p = sc.prim + 9 * (size_t)pi;
-      DVec pos, nrm;
-      if (sc.prim_kind[pi] == 1) {
-        const double u = rng.next(), v = rng.next();
-        pos = add(add(dv(p[0], p[1], p[2]), mul(dv(p[3], p[4], p[5]), u)), mul(dv(p[6], p[7], p[8]), v));
-        nrm = normalize(cross(dv(p[3], p[4], p[5]), dv(p[6], p[7], p[8])));
-      } else {
-        // f(rng.next_double(), rng.next_double()): the reference build (g++)
-        // evaluates call arguments right to left, so the first draw is u2
-        const double u2 = rng.next(), u1 = rng.next();
-        const DVec dd_ = sample_uniform_sphere(u1, u2);
-        pos = add(dv(p[0], p[1], p[2]), mul(dd_, p[3]));
-        nrm = dd_;
+  s.rng = Rng(A.seed, A.iteration, j, 0ull /* kLightStream */);
+  s.j = j;
+  s.nv = 0;
+  s.depth = 1;
+  if (sc.n_emit <= 0 || A.light_depth == 0) return false;  // no loop iteration (path.cpp:409)
+  const int n = sc.n_emit;
+  int pick = (int)dm(s.rng.next(), (double)n);
+  if (pick > n - 1) pick = n - 1;
+  const double pick_prob = dd(1.0, (double)n);
+  const int pi = sc.emit_prim[pick];
+  const PrimD &p = P[pi];
+  DVec pos, nrm;
+  if (p.kind == 1) {
+    const double u = s.rng.next(), v = s.rng.next();
+    pos = add(add(dv(p.c[0], p.c[1], p.c[2]), mul(dv(p.e1[0], p.e1[1], p.e1[2]), u)),
+              mul(dv(p.e2[0], p.e2[1], p.e2[2]), v));
+    nrm = dv(p.on[0], p.on[1], p.on[2]);
+  } else {
+    // f(rng.next_double(), rng.next_double()): the reference build (g++)
+    // evaluates call arguments right to left, so the first draw is u2
+    const double u2 = s.rng.next(), u1 = s.rng.next();
+    const DVec dd_ = sample_uniform_sphere(u1, u2);
+    pos = add(dv(p.c[0], p.c[1], p.c[2]), mul(dd_, p.r));
+    nrm = dd_;
+  }
+  const double pdf_a = p.inv_area;
+  const Frame fr = make_frame(nrm);
+  const double u2 = s.rng.next(), u1 = s.rng.next();  // right-to-left arguments (see above)
+  const DVec local = sample_cosine_hemisphere(u1, u2);
+  s.dir = to_world(fr, local);
+  const double cos_at_light = local.z;
+  const double emission_pdf = dm(pdf_a, cos_pdf(local.z));
+  const double *rad = sc.emit_rad + 3 * (size_t)pick;
+  const double wscale = dd(kPi, pdf_a);
+  s.t0 = dm(rad[0], wscale);
+  s.t1 = dm(rad[1], wscale);
+  s.t2 = dm(rad[2], wscale);
+  if (emission_pdf <= 0.0 || (s.t0 == 0 && s.t1 == 0 && s.t2 == 0)) return false;
+  // mis_light_origin (path.cpp:28-36)
+  const double ep = dm(emission_pdf, pick_prob), dp = dm(pdf_a, pick_prob);
+  s.mis.d_vcm = mpow(A.beta, dd(dp, ep));
+  s.mis.d_vc = mpow(A.beta, dd(cos_at_light, ep));
+  s.mis.d_vm = dm(s.mis.d_vc, vcf);
+  s.t0 = dd(s.t0, pick_prob);
+  s.t1 = dd(s.t1, pick_prob);
+  s.t2 = dd(s.t2, pick_prob);
+  s.o = pos;
+  return true;
+}
+
+// One segment of trace_light_subpath's loop (path.cpp:409-447).  False: the
+// path ended.
+__device__ __forceinline__ bool bounce(const TraceArgs &A, const PrimD *P, int np, PathState &s, double vcf,
+                                       double vmf) {
+  const TraceScene &sc = A.sc;
+  HitD h;
+  if (!intersect(P, np, s.o, s.dir, h)) return false;
+  const DVec wi = neg(s.dir);
+  const double cos_in = fabs(dot(h.sn, wi));
+  if (cos_in == 0.0) return false;
+  {  // mis_arrive (path.cpp:45-50)
+    const double inv_cos = dd(1.0, mpow(A.beta, cos_in));
+    s.mis.d_vcm = dm(s.mis.d_vcm, dm(mpow(A.beta, dm(h.t, h.t)), inv_cos));
+    s.mis.d_vc = dm(s.mis.d_vc, inv_cos);
+    s.mis.d_vm = dm(s.mis.d_vm, inv_cos);
+  }
+  const int mk = sc.mat_kind[h.mat];
+  const double cont = cont_prob(sc, h.mat);
+  const double cos_o = dot(wi, h.sn);  // Bsdf ctor (bsdf.cpp:34)
+  if (mk == 0) {  // non-delta: deposit (path.cpp:414-428)
+    const size_t slot = (size_t)s.j * A.light_depth + s.nv;
+    const size_t o3 = 3 * slot;
+    A.v_pos[o3] = (float)h.point.x; A.v_pos[o3 + 1] = (float)h.point.y; A.v_pos[o3 + 2] = (float)h.point.z;
+    A.v_nrm[o3] = (float)h.sn.x; A.v_nrm[o3 + 1] = (float)h.sn.y; A.v_nrm[o3 + 2] = (float)h.sn.z;
+    A.v_wi[o3] = (float)wi.x; A.v_wi[o3 + 1] = (float)wi.y; A.v_wi[o3 + 2] = (float)wi.z;
+    A.v_pow[o3] = (float)s.t0; A.v_pow[o3 + 1] = (float)s.t1; A.v_pow[o3 + 2] = (float)s.t2;
+    A.v_depth[slot] = s.depth;
+    if (A.v_mis) {
+      A.v_mis[o3] = s.mis.d_vcm;
+      A.v_mis[o3 + 1] = s.mis.d_vm;
+      A.v_mis[o3 + 2] = cont;
+    }
+    ++s.nv;
+  }
+  if (s.depth == A.light_depth) return false;
+  // bsdf.sample (bsdf.cpp:94-182)
+  DVec ndir;
+  double s_cos, s_pdf, s_rev;
+  bool s_delta;
+  const double *rgb = sc.mat_rgb + 3 * (size_t)h.mat;
+  if (mk == 2) {  // dielectric (bsdf.cpp:147-180)
+    const double eta = h.front ? sc.mat_ior[h.mat] : dd(1.0, sc.mat_ior[h.mat]);
+    const double ci = cos_o;
+    if (ci <= 0.0) return false;
+    const double sin2_t = dd(ds(1.0, dm(ci, ci)), dm(eta, eta));
+    double frs;
+    if (sin2_t >= 1.0) {
+      frs = 1.0;
+    } else {
+      const double ct = __dsqrt_rn(ds(1.0, sin2_t));
+      const double rs = dd(ds(ci, dm(eta, ct)), da(ci, dm(eta, ct)));
+      const double rp = dd(ds(dm(eta, ci), ct), da(dm(eta, ci), ct));
+      frs = dm(0.5, da(dm(rs, rs), dm(rp, rp)));
+    }
+    s_delta = true;
+    if (s.rng.next() < frs) {
+      ndir = reflect(wi, h.sn);
+      s_cos = dot(ndir, h.sn);
+      s_pdf = frs;
+      s_rev = frs;
+    } else {
+      const double x = ds(1.0, sin2_t);
+      const double ct = __dsqrt_rn(x > 0.0 ? x : 0.0);
+      ndir = normalize(add(mul(wi, dd(-1.0, eta)), mul(h.sn, ds(dd(ci, eta), ct))));
+      s_cos = ct;
+      s_pdf = ds(1.0, frs);
+      s_rev = ds(1.0, frs);
+    }
+  } else {
+    if (cos_o <= 0.0) return false;
+    if (mk == 0) {  // lambertian
+      const Frame sf = make_frame(h.sn);
+      const double a2 = s.rng.next(), a1 = s.rng.next();  // right-to-left arguments
+      const DVec l = sample_cosine_hemisphere(a1, a2);
+      ndir = to_world(sf, l);
+      s_cos = l.z;
+      if (s_cos <= 0.0) return false;
+      s_pdf = cos_pdf(s_cos);
+      s_rev = cos_pdf(cos_o);
+      s_delta = false;
+    } else {  // mirror
+      ndir = reflect(wi, h.sn);
+      s_cos = dot(ndir, h.sn);
+      s_pdf = 1.0;
+      s_rev = 1.0;
+      s_delta = true;
+    }
+  }
+  const double w0 = rgb[0], w1 = rgb[1], w2 = rgb[2];
+  if (s_pdf <= 0.0 || (w0 == 0 && w1 == 0 && w2 == 0)) return false;
+  double q = 1.0;
+  if (s.depth >= 5) {  // kRouletteDepth (path.hpp:156)
+    q = cont;
+    if (s.rng.next() >= q) return false;
+  }
+  {  // mis_scatter (path.cpp:52-76)
+    const double pf = dm(s_pdf, cont), pr = dm(s_rev, cont);
+    if (s_delta) {
+      const double f = mpow(A.beta, dd(dm(s_cos, pr), pf));
+      s.mis.d_vcm = 0.0;
+      s.mis.d_vc = dm(s.mis.d_vc, f);
+      s.mis.d_vm = dm(s.mis.d_vm, f);
+    } else {
+      const double ratio = mpow(A.beta, dd(s_cos, pf));
+      const double rev = mpow(A.beta, pr);
+      const double d_vc = dm(ratio, da(da(dm(s.mis.d_vc, rev), s.mis.d_vcm), vmf));
+      const double d_vm = dm(ratio, da(da(dm(s.mis.d_vm, rev), dm(s.mis.d_vcm, vcf)), 1.0));
+      s.mis.d_vc = d_vc;
+      s.mis.d_vm = d_vm;
+      s.mis.d_vcm = mpow(A.beta, dd(1.0, pf));
+    }
+  }
+  s.t0 = dd(dm(s.t0, w0), q);
+  s.t1 = dd(dm(s.t1, w1), q);
+  s.t2 = dd(dm(s.t2, w2), q);
+  s.o = h.point;
+  s.dir = ndir;
+  ++s.depth;
+  return true;
+}
+
+// Persistent warps with path regeneration: a lane whose path ended takes the
+// next path id from a warp-local chunk (refilled by one atomic per kTraceChunk
+// paths), so lanes stay busy instead of idling until the warp's longest path
+// ends.  Output slots are indexed by path id, so the processing order does
+// not change the flattened photon order.
+constexpr uint32_t kTraceChunk = 64;
+
+#ifndef FPPM_TRACE_MINB
+#define FPPM_TRACE_MINB 3
+#endif
+__global__ void __launch_bounds__(256, FPPM_TRACE_MINB) k_trace_paths(const TraceArgs A, const PrimD *__restrict__ prims) {
+  __shared__ PrimD P[kMaxTracePrims];
+  const int np = A.sc.n_prim;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) P[i] = prims[i];
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  const double vcf = A.eta_vm > 0.0 ? mpow(A.beta, dd(1.0, A.eta_vm)) : 0.0;  // vc_factor (path.cpp:22-24)
+  const double vmf = A.eta_vm > 0.0 ? mpow(A.beta, A.eta_vm) : 0.0;           // vm_factor (path.cpp:19-21)
+  uint32_t q_next = 0, q_end = 0;  // warp-uniform chunk of path ids
+  bool alive = false, done = false;
+  PathState st;
+  for (;;) {
+    unsigned need = __ballot_sync(~0u, !alive && !done);
+    while (need) {
+      if (q_next >= q_end) {
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(A.path_counter, kTraceChunk);
+        b = __shfl_sync(~0u, b, 0);
+        q_next = b < A.n_paths ? b : A.n_paths;
+        q_end = b + kTraceChunk < A.n_paths ? b + kTraceChunk : A.n_paths;
+        if (q_next >= q_end) {  // no paths left
+          if (!alive) done = true;
+          break;
+        }
       }
-      const double pdf_a = dd(1.0, prim_area(sc, pi));
-      const Frame fr = make_frame(nrm);
-      const double u2 = rng.next(), u1 = rng.next();  // right-to-left arguments (see above)
-      const DVec local = sample_cosine_hemisphere(u1, u2);
-      DVec dir = to_world(fr, local);
-      const double cos_at_light = local.z;
-      const double emission_pdf = dm(pdf_a, cos_pdf(local.z));
-      const double *rad = sc.emit_rad + 3 * (size_t)pick;
-      const double wscale = dd(kPi, pdf_a);
-      double t0 = dm(rad[0], wscale), t1 = dm(rad[1], wscale), t2 = dm(rad[2], wscale);
-      const bool black = t0 == 0 && t1 == 0 && t2 == 0;
-      if (!(emission_pdf <= 0.0) && !black) {
-        // mis_light_origin (path.cpp:28-36)
-        const double ep = dm(emission_pdf, pick_prob), dp = dm(pdf_a, pick_prob);
-        const double vcf = A.eta_vm > 0.0 ? mpow(A.beta, dd(1.0, A.eta_vm)) : 0.0;
-        const double vmf = A.eta_vm > 0.0 ? mpow(A.beta, A.eta_vm) : 0.0;
-        Mis mis;
-        mis.d_vcm = mpow(A.beta, dd(dp, ep));
-        mis.d_vc = mpow(A.beta, dd(cos_at_light, ep));
-        mis.d_vm = dm(mis.d_vc, vcf);
-        t0 = dd(t0, pick_prob);
-        t1 = dd(t1, pick_prob);
-        t2 = dd(t2, pick_prob);
-        DVec o = pos;
-        for (uint32_t depth = 1; depth <= A.light_depth; ++depth) {
-          HitD h;
-          if (!intersect(sc, o, dir, h)) break;
-          const DVec wi = neg(dir);
-          const double cos_in = fabs(dot(h.sn, wi));
-          if (cos_in == 0.0) break;
-          // mis_arrive (path.cpp:45-50)
-          {
-            const double inv_cos = dd(1.0, mpow(A.beta, cos_in));
-            mis.d_vcm = dm(mis.d_vcm, dm(mpow(A.beta, dm(h.t, h.t)), inv_cos));
-            mis.d_vc = dm(mis.d_vc, inv_cos);
-            mis.d_vm = dm(mis.d_vm, inv_cos);
-          }
-          const int mk = sc.mat_kind[h.mat];
-          const double cont = cont_prob(sc, h.mat);
-          const double cos_o = dot(wi, h.sn);  // Bsdf ctor (bsdf.cpp:34)
-          if (mk == 0) {  // non-delta: deposit (path.cpp:414-428)
-            const size_t o3 = 3 * (slot + nv);
-            A.v_pos[o3] = (float)h.point.x; A.v_pos[o3 + 1] = (float)h.point.y; A.v_pos[o3 + 2] = (float)h.point.z;
-            A.v_nrm[o3] = (float)h.sn.x; A.v_nrm[o3 + 1] = (float)h.sn.y; A.v_nrm[o3 + 2] = (float)h.sn.z;
-            A.v_wi[o3] = (float)wi.x; A.v_wi[o3 + 1] = (float)wi.y; A.v_wi[o3 + 2] = (float)wi.z;
-            A.v_pow[o3] = (float)t0; A.v_pow[o3 + 1] = (float)t1; A.v_pow[o3 + 2] = (float)t2;
-            A.v_depth[slot + nv] = depth;
-            if (A.v_mis) {
-              A.v_mis[o3] = mis.d_vcm;
-              A.v_mis[o3 + 1] = mis.d_vm;
-              A.v_mis[o3 + 2] = cont;
-            }
-            ++nv;
-          }
-          if (depth == A.light_depth) break;
-          // bsdf.sample (bsdf.cpp:94-182)
-          DVec ndir;
-          double s_cos, s_pdf, s_rev, w0, w1, w2;
-          bool s_delta;
-          const double *rgb = sc.mat_rgb + 3 * (size_t)h.mat;
-          if (mk == 2) {  // dielectric (bsdf.cpp:147-180)
-            const double eta = h.front ? sc.mat_ior[h.mat] : dd(1.0, sc.mat_ior[h.mat]);
-            const double ci = cos_o;
-            if (ci <= 0.0) break;
-            const double sin2_t = dd(ds(1.0, dm(ci, ci)), dm(eta, eta));
-            double frs;
-            if (sin2_t >= 1.0) {
-              frs = 1.0;
-            } else {
-              const double ct = __dsqrt_rn(ds(1.0, sin2_t));
-              const double rs = dd(ds(ci, dm(eta, ct)), da(ci, dm(eta, ct)));
-              const double rp = dd(ds(dm(eta, ci), ct), da(dm(eta, ci), ct));
-              frs = dm(0.5, da(dm(rs, rs), dm(rp, rp)));
-            }
-            s_delta = true;
-            if (rng.next() < frs) {
-              ndir = reflect(wi, h.sn);
-              s_cos = dot(ndir, h.sn);
-              s_pdf = frs;
-              s_rev = frs;
-            } else {
-              const double s2 = dd(ds(1.0, dm(ci, ci)), dm(eta, eta));
-              const double x = ds(1.0, s2);
-              const double ct = __dsqrt_rn(x > 0.0 ? x : 0.0);
-              ndir = normalize(add(mul(wi, dd(-1.0, eta)), mul(h.sn, ds(dd(ci, eta), ct))));
-              s_cos = ct;
-              s_pdf = ds(1.0, frs);
-              s_rev = ds(1.0, frs);
-            }
-            w0 = rgb[0]; w1 = rgb[1]; w2 = rgb[2];
-          } else {
-            if (cos_o <= 0.0) break;
-            if (mk == 0) {  // lambertian
-              const Frame sf = make_frame(h.sn);
-              const double a2 = rng.next(), a1 = rng.next();  // right-to-left arguments
-              const DVec l = sample_cosine_hemisphere(a1, a2);
-              ndir = to_world(sf, l);
-              s_cos = l.z;
-              if (s_cos <= 0.0) break;
-              s_pdf = cos_pdf(s_cos);
-              s_rev = cos_pdf(cos_o);
-              s_delta = false;
-            } else {  // mirror
-              ndir = reflect(wi, h.sn);
-              s_cos = dot(ndir, h.sn);
-              s_pdf = 1.0;
-              s_rev = 1.0;
-              s_delta = true;
-            }
-            w0 = rgb[0]; w1 = rgb[1]; w2 = rgb[2];
-          }
-          if (s_pdf <= 0.0 || (w0 == 0 && w1 == 0 && w2 == 0)) break;
-          double q = 1.0;
-          if (depth >= 5) {  // kRouletteDepth (path.hpp:156)
-            q = cont;
-            if (rng.next() >= q) break;
-          }
-          // mis_scatter (path.cpp:52-76)
-          {
-            const double pf = dm(s_pdf, cont), pr = dm(s_rev, cont);
-            if (s_delta) {
-              const double f = mpow(A.beta, dd(dm(s_cos, pr), pf));
-              mis.d_vcm = 0.0;
-              mis.d_vc = dm(mis.d_vc, f);
-              mis.d_vm = dm(mis.d_vm, f);
-            } else {
-              const double ratio = mpow(A.beta, dd(s_cos, pf));
-              const double rev = mpow(A.beta, pr);
-              const double d_vc = dm(ratio, da(da(dm(mis.d_vc, rev), mis.d_vcm), vmf));
-              const double d_vm = dm(ratio, da(da(dm(mis.d_vm, rev), dm(mis.d_vcm, vcf)), 1.0));
-              mis.d_vc = d_vc;
-              mis.d_vm = d_vm;
-              mis.d_vcm = mpow(A.beta, dd(1.0, pf));
-            }
-          }
-          t0 = dd(dm(t0, w0), q);
-          t1 = dd(dm(t1, w1), q);
-          t2 = dd(dm(t2, w2), q);
-          o = h.point;
-          dir = ndir;
+      const uint32_t avail = q_end - q_next;
+      const uint32_t rank = __popc(need & ((1u << lane) - 1u));
+      if (((need >> lane) & 1u) && rank < avail) {
+        const uint32_t j = q_next + rank;
+        alive = start_path(A, P, st, j, vcf);
+        if (!alive) A.count[j] = 0;
+      }
+      const uint32_t took = __popc(need) < avail ? __popc(need) : avail;
+      q_next += took;
+      need = __ballot_sync(~0u, !alive && !done);
+    }
+    if (__all_sync(~0u, done)) break;
+    if (alive && !bounce(A, P, np, st, vcf, vmf)) {
+      A.count[st.j] = st.nv;
+      alive = false;
+    }
+  }
+}
+
+// Flatten the per-path slots in path order (light_phase, integrator.cpp:
+// 250-258).  One warp per 32 consecutive paths: their outputs form one
+// contiguous range, copied lane-per-photon with the owning path found by a
+// shuffle binary search over the warp's exclusive offsets.
+__global__ void __launch_bounds__(256) k_trace_compact(const TraceArgs A, const uint32_t *__restrict__ base,
+                                                       float *pos, float *nrm, float *wi, float *pw,
+                                                       uint32_t *depth, double *mis_vcm, double *mis_vm,
+                                                       double *mis_cont) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * 32u < A.n_paths; w += nwarps) {
+    const uint32_t p = w * 32u + lane;
+    const uint32_t cnt = p < A.n_paths ? A.count[p] : 0u;
+    const uint32_t b = p < A.n_paths ? base[p] : 0xffffffffu;
+    const uint32_t start = __shfl_sync(~0u, b, 0);
+    const uint32_t total = __reduce_add_sync(~0u, cnt);
+    const uint32_t rel = b - start;  // lanes past n_paths: huge, never selected
+    for (uint32_t o0 = 0; o0 < total; o0 += 32) {
+      const uint32_t o = o0 + lane;
+      uint32_t L = 0, rv = 0;  // rel of lane 0 is 0
+#pragma unroll
+      for (uint32_t step = 16; step; step >>= 1) {
+        const uint32_t v = __shfl_sync(~0u, rel, L + step);
+        if (v <= o) {
+          L += step;
+          rv = v;
+        }
+      }
+      if (o < total) {
+        const uint32_t k = o - rv;
+        const size_t s = (size_t)(w * 32u + L) * A.light_depth + k;
+        const size_t s3 = 3 * s, d3 = 3 * (size_t)(start + o);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          pos[d3 + c] = A.v_pos[s3 + c];
+          nrm[d3 + c] = A.v_nrm[s3 + c];
+          wi[d3 + c] = A.v_wi[s3 + c];
+          pw[d3 + c] = A.v_pow[s3 + c];
+        }
+        depth[start + o] = A.v_depth[s];
+        if (mis_vcm) {
+          mis_vcm[start + o] = A.v_mis[s3];
+          mis_vm[start + o] = A.v_mis[s3 + 1];
+          mis_cont[start + o] = A.v_mis[s3 + 2];
         }
       }
     }
-    A.count[j] = nv;
   }
 }
 
-// flatten the per-path slots in path order (light_phase, integrator.cpp:250-258)
-__global__ void k_trace_compact(const TraceArgs A, const uint32_t *__restrict__ base, float *pos, float *nrm,
-                                float *wi, float *pw, uint32_t *depth, double *mis_vcm, double *mis_vm,
-                                double *mis_cont) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < A.n_paths; j += gridDim.x * blockDim.x) {
-    const uint32_t n = A.count[j], b = base[j];
-    const size_t slot = (size_t)j * A.light_depth;
-    for (uint32_t k = 0; k < n; ++k) {
-      const size_t s3 = 3 * (slot + k), d3 = 3 * (size_t)(b + k);
-      for (int c = 0; c < 3; ++c) {
-        pos[d3 + c] = A.v_pos[s3 + c];
-        nrm[d3 + c] = A.v_nrm[s3 + c];
-        wi[d3 + c] = A.v_wi[s3 + c];
-        pw[d3 + c] = A.v_pow[s3 + c];
-      }
-      depth[b + k] = A.v_depth[slot + k];
-      if (mis_vcm) {
-        mis_vcm[b + k] = A.v_mis[s3];
-        mis_vm[b + k] = A.v_mis[s3 + 1];
-        mis_cont[b + k] = A.v_mis[s3 + 2];
-      }
-    }
-  }
+size_t trace_prep_bytes(int n_prim) { return sizeof(PrimD) * (size_t)(n_prim > 0 ? n_prim : 1); }
+int trace_max_prims() { return kMaxTracePrims; }
+
+cudaError_t launch_scene_prep(cudaStream_t s, const TraceScene &sc, void *prep) {
+  if (sc.n_prim <= 0) return cudaSuccess;
+  k_scene_prep<<<(sc.n_prim + 63) / 64, 64, 0, s>>>(sc, static_cast<PrimD *>(prep));
+  note_launches(1);
+  return cudaGetLastError();
 }
 
-cudaError_t launch_trace(cudaStream_t s, const TraceArgs &A, int sms) {
+cudaError_t launch_trace(cudaStream_t s, const TraceArgs &A, const void *prep, int sms) {
   if (A.n_paths == 0) return cudaSuccess;
-  unsigned blocks = (A.n_paths + 127) / 128;
-  if (blocks > (unsigned)sms * 16) blocks = sms * 16;
-  k_trace_paths<<<blocks, 128, 0, s>>>(A);
+  cudaError_t e = cudaMemsetAsync(A.path_counter, 0, sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace_paths, 256, 0);
+  if (e != cudaSuccess) return e;
+  unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1);
+  const unsigned need = (A.n_paths + 255) / 256;
+  if (blocks > need) blocks = need;
+  k_trace_paths<<<blocks, 256, 0, s>>>(A, static_cast<const PrimD *>(prep));
   note_launches(1);
   return cudaGetLastError();
 }
@@ -406,7 +546,7 @@ cudaError_t launch_trace_compact(cudaStream_t s, const TraceArgs &A, const uint3
                                  double *mc, int sms) {
   if (A.n_paths == 0) return cudaSuccess;
   unsigned blocks = (A.n_paths + 255) / 256;
-  if (blocks > (unsigned)sms * 16) blocks = sms * 16;
+  if (blocks > (unsigned)sms * 8) blocks = sms * 8;
   k_trace_compact<<<blocks, 256, 0, s>>>(A, base, pos, nrm, wi, pw, depth, mv, mm, mc);
   note_launches(1);
   return cudaGetLastError();
