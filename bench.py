@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-trace", action="store_true", help="skip the light-phase (photons traced/s) leg")
+    p.add_argument("--dist-mode", default="auto", choices=["auto", "a", "b"],
+                   help="multi-GPU decomposition (distributed.py); auto = measure both in warm-up")
     p.add_argument("--cpu-trace-paths", type=int, default=1 << 20)
     p.add_argument("--cpu-stride", type=int, default=0,
                    help="hit-point stride of the CPU sample (0 = auto)")
@@ -286,80 +288,176 @@ def workload_config(wl, **extra):
 
 
 # ---------------------------------------------------------------- GPU arm
+class Arm:
+    """One decomposition of the iteration over `world` ranks (distributed.py).
+
+    mode "a": this rank's raster-row band of hit points; photon shares
+              all-gathered (NCCL) so every rank builds the full grid.
+    mode "b": every hit point on every rank; the local photon share only,
+              gathered into partial-sum rows, reduce-scattered to the owners,
+              owners test, radii all-gathered.
+    With world == 1 both are the plain single-GPU iteration (b through the
+    deltas API)."""
+
+    def __init__(self, mode, wl, args, rank, world, local_rank, dev):
+        import torch
+        from paper_2504_04411_b200 import FppmContext
+        self.mode, self.wl, self.rank, self.world, self.dev = mode, wl, rank, world, dev
+        W = wl.raster
+        if mode == "a":
+            r0, r1 = raster_rows(W, rank, world)
+        else:
+            r0, r1 = 0, W
+        self.H = (r1 - r0) * W
+        self.ctx = FppmContext(**wl.context_kwargs(max_hitpoints=self.H, max_photons=wl.photons,
+                                                   device=local_rank, gather_kernel=args.kernel))
+        pos, nrm = hitpoints_for_rows(W, r0, r1)
+        self.ctx.set_hitpoints(pos, nrm)
+        self.stream = torch.cuda.ExternalStream(self.ctx.stream, device=dev)
+        self.n_local = wl.photons * (rank + 1) // world - wl.photons * rank // world
+        self.begin = wl.photons * rank // world
+        self.full = None
+        if mode == "a" and world > 1:
+            self.full = {k: torch.empty((wl.photons,) + shape, dtype=dt, device=dev)
+                         for k, dt, shape in PHOTON_LAYOUT}
+        if mode == "b":
+            from paper_2504_04411_b200.distributed import owner_slice
+            self.h0, self.n_own = owner_slice(self.H, rank, world)
+            self.rows = torch.zeros((self.H, self.ctx.delta_stride), dtype=torch.float64, device=dev)
+            self.radius = self.ctx.radius_tensor()
+
+    def photons(self, src, n):
+        from paper_2504_04411_b200 import _native as N
+        return N.Photons(*[src[k].data_ptr() for k, _, _ in PHOTON_LAYOUT])
+
+    def step(self, it, b, host_out=None):
+        """One iteration on photon share `b` (device tensors, this rank's
+        share); `host_out`: optional IterOut pointer for this rank's results."""
+        import torch
+        import torch.distributed as dist
+        from paper_2504_04411_b200 import _native as N
+        ctx, world = self.ctx, self.world
+        if self.mode == "a":
+            src = b
+            if world > 1:
+                with torch.cuda.stream(self.stream):
+                    for k in self.full:
+                        dist.all_gather_into_tensor(self.full[k], b[k])
+                src = self.full
+            N.check(ctx._lib.fppm_gpu_set_photons_device(ctx._h, self.photons(src, 0),
+                                                         self.wl.photons), ctx._h)
+            if world > 1:
+                rl = torch.tensor([ctx.max_radius()], dtype=torch.float64, device=self.dev)
+                dist.all_reduce(rl, op=dist.ReduceOp.MAX)
+                cell = float(rl.item())  # integrator.cpp:159-161 over all ranks
+            else:
+                cell = 0.0  # device-side max live radius
+            ctx.build_grid(cell)
+            N.check(ctx._lib.fppm_gpu_gather_test(ctx._h, it, host_out, None), ctx._h)
+            return
+        self._step_b(it, b, host_out)
+
+    def _step_b(self, it, b, host_out):
+        import torch
+        from paper_2504_04411_b200 import _native as N
+        from paper_2504_04411_b200.distributed import allgather_owner_values, reduce_scatter_rows
+        ctx, world = self.ctx, self.world
+        N.check(ctx._lib.fppm_gpu_set_photons_device(ctx._h, self.photons(b, 0), self.n_local), ctx._h)
+        ctx.build_grid(0.0)  # radii are replicated: the local max is the global r_max
+        with torch.cuda.stream(self.stream):
+            ctx.gather_deltas(it, self.rows)
+            mine = reduce_scatter_rows(self.rows, world)
+            N.check(ctx._lib.fppm_gpu_apply_deltas(ctx._h, it, self.h0, self.n_own, mine.data_ptr(),
+                                                   host_out, None), ctx._h)
+            if world > 1:
+                self.radius.copy_(allgather_owner_values(self.radius[self.h0:self.h0 + self.n_own],
+                                                         self.H, world))
+
+    def close(self):
+        self.ctx.close()
+
+
+PHOTON_LAYOUT = None
+
+
+def _photon_layout():
+    import torch
+    return (("photon_pos", torch.float32, (3,)), ("photon_normal", torch.float32, (3,)),
+            ("photon_wi", torch.float32, (3,)), ("photon_power", torch.float32, (3,)),
+            ("photon_depth", torch.int32, ()))
+
+
 def run_gpu_arm(args, wl, rank, world, local_rank):
-    import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2504_04411_b200 import FppmContext
     from paper_2504_04411_b200 import _native as N
+    global PHOTON_LAYOUT
+    PHOTON_LAYOUT = _photon_layout()
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    W = wl.raster
-    r0, r1 = raster_rows(W, rank, world)
-    H = (r1 - r0) * W
+    total_steps = args.warmup + args.steps
     n_local = wl.photons * (rank + 1) // world - wl.photons * rank // world
     begin = wl.photons * rank // world
-    ctx = FppmContext(**wl.context_kwargs(max_hitpoints=H, max_photons=wl.photons,
-                                          device=local_rank, gather_kernel=args.kernel))
-    pos, nrm = hitpoints_for_rows(W, r0, r1)
-    ctx.set_hitpoints(pos, nrm)
-    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
-    total_steps = args.warmup + args.steps
 
     # ---- per-iteration photon shares, resident in HBM before timing
+    gen_ctx = FppmContext(initial_radius=wl.initial_radius, samples_per_iteration=wl.photons,
+                          max_hitpoints=1, max_photons=1, device=local_rank)
+
     def gen_batch(it):
-        out = {}
-        for key, dt, width in (("photon_pos", torch.float32, 3), ("photon_normal", torch.float32, 3),
-                               ("photon_wi", torch.float32, 3), ("photon_power", torch.float32, 3),
-                               ("photon_depth", torch.int32, 1)):
-            out[key] = torch.empty((n_local, width) if width > 1 else (n_local,), dtype=dt,
-                                   device=dev)
-        ph = N.Photons(*[out[k].data_ptr() for k in ("photon_pos", "photon_normal", "photon_wi",
-                                                      "photon_power", "photon_depth")])
+        out = {k: torch.empty((n_local,) + shape, dtype=dt, device=dev) for k, dt, shape in PHOTON_LAYOUT}
+        ph = N.Photons(*[out[k].data_ptr() for k, _, _ in PHOTON_LAYOUT])
         torch.cuda.synchronize()
-        N.check(ctx._lib.fppm_gpu_generate_photons_to(ctx._h, wl.generator, wl.seed, it, begin,
-                                                      n_local, ph), ctx._h)
-        ctx.synchronize()
+        N.check(gen_ctx._lib.fppm_gpu_generate_photons_to(gen_ctx._h, wl.generator, wl.seed, it, begin,
+                                                          n_local, ph), gen_ctx._h)
+        gen_ctx.synchronize()
         return out
 
     batches = [gen_batch(it) for it in range(1, total_steps + 1)]
-    full = None
-    if world > 1:
-        full = {k: torch.empty((wl.photons,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-                for k, t in batches[0].items()}
+    gen_ctx.close()
     torch.cuda.synchronize()
 
-    gather_ms = []
-
-    def step(it, b, timed):
-        src = b
-        if world > 1:
-            with torch.cuda.stream(stream):
-                for k in full:
-                    dist.all_gather_into_tensor(full[k], b[k])
-            src = full
-        ph = N.Photons(*[src[k].data_ptr() for k in ("photon_pos", "photon_normal", "photon_wi",
-                                                      "photon_power", "photon_depth")])
-        N.check(ctx._lib.fppm_gpu_set_photons_device(ctx._h, ph, wl.photons), ctx._h)
-        if world > 1:
-            rl = torch.tensor([ctx.max_radius()], dtype=torch.float64, device=dev)
-            dist.all_reduce(rl, op=dist.ReduceOp.MAX)
-            cell = float(rl.item())  # integrator.cpp:159-161 over all ranks
+    # ---- decomposition: fixed by --dist-mode, or chosen by measurement over
+    # the warm-up iterations (BASELINE: all-gather vs reduce-scatter)
+    modes = [args.dist_mode] if args.dist_mode != "auto" else (["a", "b"] if world > 1 else ["a"])
+    choice = {}
+    arm = None
+    for mode in modes:
+        cand = Arm(mode, wl, args, rank, world, local_rank, dev)
+        for s in range(args.warmup):
+            cand.step(s + 1, batches[s])
+        torch.cuda.synchronize()
+        if len(modes) > 1:
+            # time one more warm-up-style iteration (max over ranks), then rewind
+            cand.ctx.reset_regions()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            t0.record(cand.stream)
+            for s in range(args.warmup):
+                cand.step(s + 1, batches[s])
+            t1.record(cand.stream)
+            torch.cuda.synchronize()
+            ms = torch.tensor([t0.elapsed_time(t1) / max(args.warmup, 1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            choice[mode] = float(ms.item())
+        if arm is None or (len(modes) > 1 and choice[mode] < choice[arm.mode]):
+            if arm is not None:
+                arm.close()
+            arm = cand
         else:
-            cell = 0.0  # device-side max live radius
-        ctx.build_grid(cell)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        ctx.gather_test(it, outputs=False, summary=False)
-        e1.record(stream)
-        if timed:
-            gather_ms.append((e0, e1))
+            cand.close()
+    ctx, H, stream = arm.ctx, arm.H, arm.stream
+    if len(modes) > 1:
+        # replay the warm-up on the chosen arm so the timed iterations continue it
+        ctx.reset_regions()
+        for s in range(args.warmup):
+            arm.step(s + 1, batches[s])
+        torch.cuda.synchronize()
 
-    for s in range(args.warmup):
-        step(s + 1, batches[s], False)
-    torch.cuda.synchronize()
     ctx.gather_kernel_ms()  # drop the warm-up launches
     if world > 1:
         dist.barrier()
@@ -374,7 +472,7 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     for s in range(args.warmup, total_steps):
-        step(s + 1, batches[s], True)
+        arm.step(s + 1, batches[s])
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -383,7 +481,6 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
     launches = FppmContext.kernel_launches() - l0
     c1 = ctx.counters()
     elapsed_ms = t_start.elapsed_time(t_end)
-    call_ms = [a.elapsed_time(b) for a, b in gather_ms]  # whole gather_test call
     g_ms = ctx.gather_kernel_ms()  # the dominant kernel alone (events in the library)
     q_local = c1["accepted"] - c0["accepted"]
     stats = torch.tensor([elapsed_ms, float(q_local), float(launches)], dtype=torch.float64, device=dev)
@@ -397,7 +494,7 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
         q_total = float(q_local)
     value = q_total / (elapsed_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (k_gather_test), rank 0
+    # ---- roofline of the dominant kernel (the gather), rank 0
     G, C = wl.groups, 1
     gather_avg_s = statistics.mean(g_ms) / 1e3
     alg_bytes = 16.0 * q_local / args.steps + (64 + 48 * G * C) * H
@@ -408,7 +505,7 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
     # ---- end to end through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(ctx, wl, batches, args, world, rank, dev, stream, H)
+        e2e = run_e2e(arm, batches, args, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -433,6 +530,15 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
             trace["cpu_baseline"] = reference_trace(os.cpu_count() or 1, args)
 
     if rank == 0:
+        if world == 1:
+            par = "1 GPU"
+        elif arm.mode == "a":
+            par = (f"option A over {world} GPUs: hit points sharded by raster rows; photon shares "
+                   "all-gathered (NCCL) each step; every rank builds the full grid")
+        else:
+            par = (f"option B over {world} GPUs: every rank gathers its own photon share for all "
+                   "hit points; partial-sum rows reduce-scattered (NCCL) to the owners, radii "
+                   "all-gathered")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
@@ -440,8 +546,8 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (canonical PCG32 inputs generated on device, DESIGN.md §3)",
             "config": workload_config(
-                wl, parallelism=f"hit points sharded by raster rows over {world} GPU(s); photon "
-                                "shares all-gathered (NCCL) each step" if world > 1 else "1 GPU",
+                wl, parallelism=par,
+                decomposition={"mode": arm.mode, "measured_ms_per_iteration": choice or None},
                 l2=f"inputs larger than L2: fresh {wl.photons * 52 / 1e6:.0f} MB photon batch "
                    "per step (+256 MB sorted records)" if wl.photons * 52 > 126e6 else
                    "photon batch smaller than L2 (not flushed)",
@@ -455,7 +561,6 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
                          "avg_launch_ms": gather_avg_s * 1e3, "launch_ms": [round(x, 3) for x in g_ms],
                          "timing": "CUDA events around the kernel launch on the context stream "
                                    "(fppm_gpu_gather_kernel_ms)",
-                         "gather_call_ms": statistics.mean(call_ms),
                          "share_of_step": gather_avg_s * 1e3 / (elapsed_ms / args.steps),
                          "peak_source": peak_src, "traffic_source": traffic_wl},
             "gpu_launches": launches,
@@ -471,62 +576,49 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
         if trace:
             line["trace"] = trace
         emit(line)
-    ctx.close()
+    arm.close()
 
 
-def run_e2e(ctx, wl, batches, args, world, rank, dev, stream, H):
+def run_e2e(arm, batches, args, dev):
     """Same metric through the C-ABI host path: per step the photon share is
     copied from pinned host memory (fppm_gpu_set_photons) and the per-hit-point
-    radius, radiance and decision are read back (fppm_gpu_gather_test out)."""
+    radius, radiance and decision of this rank's hit points are read back."""
     import ctypes as C
-    import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2504_04411_b200 import _native as N
-
+    ctx, wl, world, H = arm.ctx, arm.wl, arm.world, arm.H
     pinned = []
     for b in batches:
         hb = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for k, t in b.items()}
         for k in b:
             hb[k].copy_(b[k])
         pinned.append(hb)
-    if world > 1:
-        # each rank uploads its share; the exchange stays on the device (NCCL)
-        full = {k: torch.empty((wl.photons,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-                for k, t in batches[0].items()}
-        local = {k: torch.empty_like(t) for k, t in batches[0].items()}
-    out_r = torch.empty(H, dtype=torch.float64, pin_memory=True)
-    out_rad = torch.empty((H, 3), dtype=torch.float32, pin_memory=True)
-    out_rej = torch.empty(H, dtype=torch.uint8, pin_memory=True)
+    n_out = H if arm.mode == "a" else arm.n_own
+    out_r = torch.empty(max(n_out, 1), dtype=torch.float64, pin_memory=True)
+    out_rad = torch.empty((max(n_out, 1), 3), dtype=torch.float32, pin_memory=True)
+    out_rej = torch.empty(max(n_out, 1), dtype=torch.uint8, pin_memory=True)
     io = N.IterOut()
     io.radius = out_r.data_ptr()
     io.radiance = out_rad.data_ptr()
     io.rejected = out_rej.data_ptr()
+    local = {k: torch.empty_like(t) for k, t in batches[0].items()}
     torch.cuda.synchronize()
     ctx.reset_regions()
     n_local = next(iter(pinned[0].values())).shape[0]
     h2d = sum(t.numel() * t.element_size() for t in pinned[0].values())
-    d2h = H * (8 + 12 + 1)
+    d2h = n_out * (8 + 12 + 1)
 
     def one(it, hb):
-        if world == 1:
-            ph = N.Photons(*[hb[k].data_ptr() for k in ("photon_pos", "photon_normal", "photon_wi",
-                                                         "photon_power", "photon_depth")])
+        if world == 1 and arm.mode == "a":
+            ph = N.Photons(*[hb[k].data_ptr() for k, _, _ in PHOTON_LAYOUT])
             N.check(ctx._lib.fppm_gpu_set_photons(ctx._h, ph, n_local), ctx._h)
             N.check(ctx._lib.fppm_gpu_iterate(ctx._h, it, C.byref(io), None), ctx._h)
-        else:
-            with torch.cuda.stream(stream):
-                for k in local:
-                    local[k].copy_(hb[k], non_blocking=True)
-                    dist.all_gather_into_tensor(full[k], local[k])
-            ph = N.Photons(*[full[k].data_ptr() for k in ("photon_pos", "photon_normal",
-                                                           "photon_wi", "photon_power",
-                                                           "photon_depth")])
-            N.check(ctx._lib.fppm_gpu_set_photons_device(ctx._h, ph, wl.photons), ctx._h)
-            rl = torch.tensor([ctx.max_radius()], dtype=torch.float64, device=dev)
-            dist.all_reduce(rl, op=dist.ReduceOp.MAX)
-            ctx.build_grid(float(rl.item()))
-            N.check(ctx._lib.fppm_gpu_gather_test(ctx._h, it, C.byref(io), None), ctx._h)
+            return
+        with torch.cuda.stream(arm.stream):
+            for k in local:
+                local[k].copy_(hb[k], non_blocking=True)
+        arm.step(it, local, C.byref(io))
 
     for s in range(args.warmup):
         one(s + 1, pinned[s])
@@ -549,9 +641,10 @@ def run_e2e(ctx, wl, batches, args, world, rank, dev, stream, H):
         secs, q = float(tm.item()), float(qs.item())
     else:
         secs = t1 - t0
+    path = ("fppm_gpu_set_photons (pinned host) + fppm_gpu_iterate with host outputs" if world == 1 and
+            arm.mode == "a" else f"pinned host share -> device, option {arm.mode.upper()} step with host outputs")
     return {"value": q / secs, "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * secs / args.steps,
-            "path": "fppm_gpu_set_photons (pinned host) + fppm_gpu_iterate with host outputs"}
+            "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * secs / args.steps, "path": path}
 
 
 def main():

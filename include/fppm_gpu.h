@@ -229,6 +229,25 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration,
 int fppm_gpu_iterate(fppm_gpu_ctx *ctx, uint64_t iteration,
                      fppm_gpu_iter_out *out, fppm_gpu_summary *summary);
 
+/* ---- multi-GPU, photon-sharded decomposition (SURVEY.md 8(e) option B) ----
+ * Each rank builds the grid of its own photon share and gathers for ALL hit
+ * points, producing per-hit-point partial sums instead of the end-of-iteration
+ * update; the rows are summed across ranks (ncclReduceScatter) and each owner
+ * pools its slice and runs the policy.  A row is fppm_gpu_delta_stride(ctx)
+ * doubles: [count G | sum C*G | sum_sq C*G | power 3] (G = n_a*n_s, C =
+ * channels; counts are exact integers in fp64).  Afterwards the owners'
+ * radii are all-gathered into every rank's radius array
+ * (fppm_gpu_device_view_get) so the next gather sees them. */
+uint32_t fppm_gpu_delta_stride(const fppm_gpu_ctx *ctx);
+/* Gather against the grid built last into d_rows (device, [H][stride]);
+ * region state is unchanged. */
+int fppm_gpu_gather_deltas(fppm_gpu_ctx *ctx, uint64_t iteration, double *d_rows);
+/* Pools d_rows (device, [n][stride], summed over ranks) into regions
+ * [h0, h0 + n) and runs the end-of-iteration policy; `out` arrays hold n
+ * entries (the slice), asynchronous as for fppm_gpu_gather_test. */
+int fppm_gpu_apply_deltas(fppm_gpu_ctx *ctx, uint64_t iteration, uint32_t h0, uint32_t n,
+                          const double *d_rows, fppm_gpu_iter_out *out, fppm_gpu_summary *summary);
+
 /* ---- GatherRegion primitives on explicit samples (gather.cpp:59-67, 90-144) ---- */
 /* Adds samples (region index, plane coords y, RGB value) to pooled stats. */
 int fppm_gpu_accumulate(fppm_gpu_ctx *ctx, const uint32_t *region, const double *y,

@@ -160,6 +160,10 @@ _SIGS = [
     ("fppm_gpu_trace_photons", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_double,
                                          C.POINTER(C.c_uint32)]),
     ("fppm_gpu_get_photon_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("fppm_gpu_delta_stride", C.c_uint32, [C.c_void_p]),
+    ("fppm_gpu_gather_deltas", C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p]),
+    ("fppm_gpu_apply_deltas", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
+                                        C.POINTER(IterOut), C.POINTER(Summary)]),
     ("fppm_gpu_schedule_radius", C.c_double, [C.c_double, C.c_double, C.c_uint64]),
     ("fppm_gpu_f_quantile", C.c_double, [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int)]),
     ("fppm_gpu_chi2_quantile", C.c_double, [C.c_double, C.c_double, C.POINTER(C.c_int)]),

@@ -114,6 +114,7 @@ class FppmContext:
         cfg.gather_kernel = {"auto": 0, "warp": 1, "tile": 2, "lanes": 3, "fine": 4}[gather_kernel]
         cfg.vcm_plus, cfg.mis_n_vm, cfg.mis_beta = int(bool(vcm_plus)), int(mis_n_vm), float(mis_beta)
         self.config = cfg
+        self.device = device
         self.G = n_annuli * n_sectors
         self.C = cfg.channels
         self._h = C.c_void_p()
@@ -333,10 +334,10 @@ class FppmContext:
         return [idx[offsets[q]:offsets[q + 1]].copy() for q in range(nq)]
 
     # ------------------------------------------------------------ hot path
-    def _out(self, outputs: bool, stats: bool, gather: bool):
+    def _out(self, outputs: bool, stats: bool, gather: bool, n: Optional[int] = None):
         if not outputs and not stats:
             return None, None
-        H, CG = self.H, self.G * self.C
+        H, CG = (self.H if n is None else n), self.G * self.C
         o = {}
         if outputs:
             o.update(radius=np.zeros(H), gather_radius=np.zeros(H), t=np.zeros(H, np.uint64),
@@ -372,6 +373,59 @@ class FppmContext:
                                                C.byref(sm) if sm is not None else None))
         if o is not None:
             self.synchronize()  # outputs are written asynchronously
+        return o, (sm.as_dict() if sm is not None else None)
+
+    # ---------------------------------------- multi-GPU option B (photon-sharded)
+    @property
+    def delta_stride(self) -> int:
+        return int(self._lib.fppm_gpu_delta_stride(self._h))
+
+    def _stream_handoff(self, rows, to_ctx: bool):
+        """Order the context stream after torch's current stream (to_ctx) or
+        the other way round, without a host synchronization."""
+        if not _is_device(rows):
+            return
+        import torch
+        ctx_stream = torch.cuda.ExternalStream(self.stream, device=rows.device)
+        cur = torch.cuda.current_stream(rows.device)
+        src, dst = (cur, ctx_stream) if to_ctx else (ctx_stream, cur)
+        ev = torch.cuda.Event()
+        ev.record(src)
+        dst.wait_event(ev)
+
+    def radius_tensor(self):
+        """torch view (no copy) of the context's live radii [H] fp64 on the
+        device: the all-gather of option B writes into it."""
+        import torch
+
+        class _View:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+        v = self.device_view()
+        return torch.as_tensor(_View(v["radius"], self.H), device=f"cuda:{self.device}")
+
+    def gather_deltas(self, iteration: int, rows):
+        """Partial sums of this context's photons for every hit point into the
+        device tensor ``rows`` ([H, delta_stride] fp64); no state change.
+        Stream-ordered with torch's current stream on both sides."""
+        self._stream_handoff(rows, True)
+        self._check(self._lib.fppm_gpu_gather_deltas(self._h, iteration, _ptr(rows)))
+        self._stream_handoff(rows, False)
+
+    def apply_deltas(self, iteration: int, h0: int, rows, outputs: bool = True, stats: bool = False,
+                     summary: bool = False):
+        """Pool rows (device [n, delta_stride], summed over ranks) into regions
+        [h0, h0 + n) and run the end-of-iteration policy; outputs cover the slice."""
+        n = int(rows.shape[0])
+        o, io = self._out(outputs, stats, True, n=n)
+        self._stream_handoff(rows, True)
+        sm = N.Summary() if summary else None
+        self._check(self._lib.fppm_gpu_apply_deltas(self._h, iteration, h0, n, _ptr(rows),
+                                                    C.byref(io) if io is not None else None,
+                                                    C.byref(sm) if sm is not None else None))
+        if o is not None:
+            self.synchronize()
         return o, (sm.as_dict() if sm is not None else None)
 
     def accumulate(self, region, y, value):

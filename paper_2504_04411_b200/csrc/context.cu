@@ -255,9 +255,10 @@ __global__ void k_unpack_outputs(const uint8_t *__restrict__ flags, const uint32
   }
 }
 
-static int copy_iter_out(fppm_gpu_ctx *ctx, fppm_gpu_iter_out *out, bool with_gather) {
+static int copy_iter_out(fppm_gpu_ctx *ctx, fppm_gpu_iter_out *out, bool with_gather, size_t h0 = 0,
+                         size_t n = ~size_t(0)) {
   if (!out) return FPPM_OK;
-  const size_t H = ctx->H, CG = (size_t)ctx->G * ctx->C;
+  const size_t H = std::min<size_t>(ctx->H - h0, n), CG = (size_t)ctx->G * ctx->C;
   int rc;
   if (!ctx->o_tested) {
     const size_t Hc = std::max<uint32_t>(ctx->cfg.max_hitpoints, 1);
@@ -267,25 +268,25 @@ static int copy_iter_out(fppm_gpu_ctx *ctx, fppm_gpu_iter_out *out, bool with_ga
   }
   if (H && (out->tested || out->rejected || out->t)) {
     k_unpack_outputs<<<(unsigned)std::min<size_t>((H + 255) / 256, 1024), 256, 0, ctx->stream>>>(
-        ctx->o_flags, ctx->d_t, (uint32_t)H, ctx->o_tested, ctx->o_rejected, ctx->o_t64);
+        ctx->o_flags + h0, ctx->d_t + h0, (uint32_t)H, ctx->o_tested + h0, ctx->o_rejected + h0, ctx->o_t64 + h0);
     fppm_b200::note_launches(1);
     FPPM_CUDA_OK(cudaGetLastError());
   }
-  if ((rc = copy_out(ctx, out->radius, ctx->d_radius, sizeof(double) * H))) return rc;
-  if ((rc = copy_out(ctx, out->gather_radius, ctx->o_gather_r, sizeof(double) * H))) return rc;
-  if ((rc = copy_out(ctx, out->tested, ctx->o_tested, H))) return rc;
-  if ((rc = copy_out(ctx, out->rejected, ctx->o_rejected, H))) return rc;
-  if ((rc = copy_out(ctx, out->t, ctx->o_t64, sizeof(uint64_t) * H))) return rc;
-  if ((rc = copy_out(ctx, out->statistic, ctx->o_stat, sizeof(double) * H))) return rc;
-  if ((rc = copy_out(ctx, out->critical, ctx->o_crit, sizeof(double) * H))) return rc;
+  if ((rc = copy_out(ctx, out->radius, ctx->d_radius + h0, sizeof(double) * H))) return rc;
+  if ((rc = copy_out(ctx, out->gather_radius, ctx->o_gather_r + h0, sizeof(double) * H))) return rc;
+  if ((rc = copy_out(ctx, out->tested, ctx->o_tested + h0, H))) return rc;
+  if ((rc = copy_out(ctx, out->rejected, ctx->o_rejected + h0, H))) return rc;
+  if ((rc = copy_out(ctx, out->t, ctx->o_t64 + h0, sizeof(uint64_t) * H))) return rc;
+  if ((rc = copy_out(ctx, out->statistic, ctx->o_stat + h0, sizeof(double) * H))) return rc;
+  if ((rc = copy_out(ctx, out->critical, ctx->o_crit + h0, sizeof(double) * H))) return rc;
   if (with_gather) {
-    if ((rc = copy_out(ctx, out->flux, ctx->o_flux, sizeof(double) * 3 * H))) return rc;
-    if ((rc = copy_out(ctx, out->radiance, ctx->o_rad, sizeof(float) * 3 * H))) return rc;
-    if ((rc = copy_out(ctx, out->accepted, ctx->o_acc, sizeof(uint32_t) * H))) return rc;
+    if ((rc = copy_out(ctx, out->flux, ctx->o_flux + 3 * h0, sizeof(double) * 3 * H))) return rc;
+    if ((rc = copy_out(ctx, out->radiance, ctx->o_rad + 3 * h0, sizeof(float) * 3 * H))) return rc;
+    if ((rc = copy_out(ctx, out->accepted, ctx->o_acc + h0, sizeof(uint32_t) * H))) return rc;
   }
-  if ((rc = copy_out(ctx, out->stat_count, ctx->snap_cnt, sizeof(unsigned long long) * CG * H))) return rc;
-  if ((rc = copy_out(ctx, out->stat_sum, ctx->snap_sum, sizeof(double) * CG * H))) return rc;
-  if ((rc = copy_out(ctx, out->stat_sum_sq, ctx->snap_sq, sizeof(double) * CG * H))) return rc;
+  if ((rc = copy_out(ctx, out->stat_count, ctx->snap_cnt + CG * h0, sizeof(unsigned long long) * CG * H))) return rc;
+  if ((rc = copy_out(ctx, out->stat_sum, ctx->snap_sum + CG * h0, sizeof(double) * CG * H))) return rc;
+  if ((rc = copy_out(ctx, out->stat_sum_sq, ctx->snap_sq + CG * h0, sizeof(double) * CG * H))) return rc;
   return FPPM_OK;
 }
 
@@ -978,8 +979,71 @@ int fppm_gpu_gather_kernel_ms(fppm_gpu_ctx *ctx, float *out, uint32_t max, uint3
   return FPPM_OK;
 }
 
+static void fill_gather_args(fppm_gpu_ctx *ctx, uint64_t iteration, GatherArgs &A) {
+  std::memset(&A, 0, sizeof(A));
+  A.pos = ctx->d_pos; A.nrm = ctx->d_nrm; A.K = ctx->d_K;
+  A.eye_depth = ctx->d_eye; A.gathered = ctx->d_gathered;
+  A.radius = ctx->d_radius; A.t = ctx->d_t;
+  A.st_cnt = ctx->d_st_cnt; A.st_sum = ctx->d_st_sum; A.st_sq = ctx->d_st_sq;
+  A.H = ctx->H;
+  A.rec0 = ctx->recs.rec0; A.rec1 = ctx->recs.rec1; A.rec2 = ctx->recs.rec2; A.rec3 = ctx->recs.rec3;
+  A.cell_start = ctx->d_cell_start; A.grid = ctx->d_hdr;
+  A.na = ctx->cfg.n_annuli; A.ns = ctx->cfg.n_sectors;
+  A.max_depth = ctx->cfg.max_depth; A.guard = ctx->cfg.normal_guard_cos;
+  A.end = end_params(ctx, iteration);
+  A.o_gather_r = ctx->o_gather_r; A.o_stat = ctx->o_stat; A.o_crit = ctx->o_crit;
+  A.o_flux = ctx->o_flux; A.o_flags = ctx->o_flags; A.o_radiance = ctx->o_rad;
+  A.o_accepted = ctx->o_acc;
+  A.vcm = ctx->cfg.vcm_plus;
+  A.mis_n_vm = ctx->cfg.mis_n_vm;
+  A.mis_beta = ctx->cfg.mis_beta;
+  A.eye_mis = ctx->d_eye_mis;
+  A.p_vcm = ctx->d_pmis[0]; A.p_vm = ctx->d_pmis[1]; A.p_cont = ctx->d_pmis[2];
+  A.wo = ctx->d_wo; A.alb = ctx->d_alb;
+  A.counters = ctx->d_counters; A.iter_tr = ctx->d_iter_tr; A.work = ctx->d_work;
+  A.rmax_bits = ctx->d_rmax_bits;
+}
+
+static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *out,
+                       fppm_gpu_summary *summary, double *delta);
+
 int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *out,
                          fppm_gpu_summary *summary) {
+  return gather_impl(ctx, iteration, out, summary, nullptr);
+}
+
+uint32_t fppm_gpu_delta_stride(const fppm_gpu_ctx *ctx) {
+  return ctx ? (uint32_t)(ctx->G + 2 * ctx->G * ctx->C + 3) : 0u;
+}
+
+int fppm_gpu_gather_deltas(fppm_gpu_ctx *ctx, uint64_t iteration, double *d_rows) {
+  if (!ctx || (!d_rows && ctx->H)) return FPPM_ERR_INVALID_ARGUMENT;
+  return gather_impl(ctx, iteration, nullptr, nullptr, d_rows);
+}
+
+int fppm_gpu_apply_deltas(fppm_gpu_ctx *ctx, uint64_t iteration, uint32_t h0, uint32_t n,
+                          const double *d_rows, fppm_gpu_iter_out *out, fppm_gpu_summary *summary) {
+  if (!ctx || (n && !d_rows)) return FPPM_ERR_INVALID_ARGUMENT;
+  if ((uint64_t)h0 + n > ctx->H) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "apply range exceeds hit points");
+  int rc = ensure_crit(ctx, ctx->end_calls + 2);
+  if (rc) return rc;
+  const bool snap = out && (out->stat_count || out->stat_sum || out->stat_sum_sq);
+  if (snap && (rc = ensure_snapshots(ctx))) return rc;
+  cudaStream_t s = ctx->stream;
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_iter_tr, 0, 2 * sizeof(unsigned int), s));
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_rmax_bits, 0, sizeof(unsigned long long), s));
+  GatherArgs A;
+  fill_gather_args(ctx, iteration, A);
+  if (snap) { A.snap_cnt = ctx->snap_cnt; A.snap_sum = ctx->snap_sum; A.snap_sq = ctx->snap_sq; }
+  FPPM_CUDA_OK(launch_apply_deltas(s, A, ctx->C, h0, n, d_rows));
+  ctx->end_calls++;
+  if (out && (rc = copy_iter_out(ctx, out, true, h0, n))) return rc;
+  if (summary && (rc = fill_summary(ctx, summary))) return rc;
+  return FPPM_OK;
+}
+
+static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *out,
+                       fppm_gpu_summary *summary, double *delta) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "gather before build_grid");
   const bool dbg = std::getenv("FPPM_DEBUG") != nullptr;
@@ -996,29 +1060,9 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
   FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_iter_tr, 0, 2 * sizeof(unsigned int), s));
   FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_rmax_bits, 0, sizeof(unsigned long long), s));
   GatherArgs A;
-  std::memset(&A, 0, sizeof(A));
-  A.pos = ctx->d_pos; A.nrm = ctx->d_nrm; A.K = ctx->d_K;
-  A.eye_depth = ctx->d_eye; A.gathered = ctx->d_gathered;
-  A.radius = ctx->d_radius; A.t = ctx->d_t;
-  A.st_cnt = ctx->d_st_cnt; A.st_sum = ctx->d_st_sum; A.st_sq = ctx->d_st_sq;
-  A.H = ctx->H;
-  A.rec0 = ctx->recs.rec0; A.rec1 = ctx->recs.rec1; A.rec2 = ctx->recs.rec2; A.rec3 = ctx->recs.rec3;
-  A.cell_start = ctx->d_cell_start; A.grid = ctx->d_hdr;
-  A.na = ctx->cfg.n_annuli; A.ns = ctx->cfg.n_sectors;
-  A.max_depth = ctx->cfg.max_depth; A.guard = ctx->cfg.normal_guard_cos;
-  A.end = end_params(ctx, iteration);
-  A.o_gather_r = ctx->o_gather_r; A.o_stat = ctx->o_stat; A.o_crit = ctx->o_crit;
-  A.o_flux = ctx->o_flux; A.o_flags = ctx->o_flags; A.o_radiance = ctx->o_rad;
-  A.o_accepted = ctx->o_acc;
+  fill_gather_args(ctx, iteration, A);
   if (snap) { A.snap_cnt = ctx->snap_cnt; A.snap_sum = ctx->snap_sum; A.snap_sq = ctx->snap_sq; }
-  A.vcm = ctx->cfg.vcm_plus;
-  A.mis_n_vm = ctx->cfg.mis_n_vm;
-  A.mis_beta = ctx->cfg.mis_beta;
-  A.eye_mis = ctx->d_eye_mis;
-  A.p_vcm = ctx->d_pmis[0]; A.p_vm = ctx->d_pmis[1]; A.p_cont = ctx->d_pmis[2];
-  A.wo = ctx->d_wo; A.alb = ctx->d_alb;
-  A.counters = ctx->d_counters; A.iter_tr = ctx->d_iter_tr; A.work = ctx->d_work;
-  A.rmax_bits = ctx->d_rmax_bits;
+  A.delta_out = delta;
   if (ctx->H && gather_variant(ctx) == 1) {
     if ((rc = kernel_event(ctx, 0))) return rc;
     FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
@@ -1128,6 +1172,7 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_ou
     }
     FPPM_CUDA_OK(launch_tile_finalize(s, A, T, ctx->C, ctx->sms));
   }
+  if (delta) return FPPM_OK;  // option B: pooled and tested by the owner (apply_deltas)
   ctx->end_calls++;
   if (out && (rc = copy_iter_out(ctx, out, true))) return rc;
   if (summary && (rc = fill_summary(ctx, summary))) return rc;

@@ -318,6 +318,69 @@ cudaError_t launch_gather_test(cudaStream_t s, const GatherArgs &A, int C, int s
   return launch_one<32, 3>(s, A, sms);
 }
 
+// Owner side of option B: rows summed over all ranks' photon shares are
+// pooled exactly like a local gather's sums (finalize_hit).
+template <int GMAX, int CH>
+__global__ void __launch_bounds__(128) k_apply_deltas(const GatherArgs A, uint32_t h0, uint32_t n,
+                                                      const double *__restrict__ delta) {
+  const int G = A.na * A.ns, CG = G * CH;
+  unsigned int my_tested = 0, my_rejected = 0;
+  double my_rmax = 0.0;
+  unsigned long long my_acc = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double *d = delta + (size_t)i * (size_t)(G + 2 * CG + 3);
+    uint32_t cnt[GMAX];
+    double sm[CH][GMAX], sq[CH][GMAX];
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      cnt[g] = g < G ? (uint32_t)d[g] : 0u;
+      my_acc += cnt[g];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        sm[c][g] = g < G ? d[G + c * G + g] : 0.0;
+        sq[c][g] = g < G ? d[G + CG + c * G + g] : 0.0;
+      }
+    }
+    finalize_hit<GMAX, CH>(A, h0 + i, cnt, sm, sq, d[G + 2 * CG], d[G + 2 * CG + 1], d[G + 2 * CG + 2],
+                           my_tested, my_rejected, my_rmax);
+  }
+  for (int o = 16; o; o >>= 1) {
+    my_tested += __shfl_xor_sync(~0u, my_tested, o);
+    my_rejected += __shfl_xor_sync(~0u, my_rejected, o);
+    my_rmax = fmax(my_rmax, __shfl_xor_sync(~0u, my_rmax, o));
+    my_acc += __shfl_xor_sync(~0u, my_acc, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(A.iter_tr, my_tested);
+    atomicAdd(A.iter_tr + 1, my_rejected);
+    atomicMax(A.rmax_bits, (unsigned long long)__double_as_longlong(my_rmax));
+  }
+}
+
+template <int GMAX, int CH>
+static cudaError_t launch_apply(cudaStream_t s, const GatherArgs &A, uint32_t h0, uint32_t n,
+                                const double *delta) {
+  const unsigned blocks = (unsigned)std::min<uint32_t>((n + 127) / 128, 4096u);
+  k_apply_deltas<GMAX, CH><<<blocks, 128, 0, s>>>(A, h0, n, delta);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_deltas(cudaStream_t s, const GatherArgs &A, int C, uint32_t h0, uint32_t n,
+                                const double *delta) {
+  if (n == 0) return cudaSuccess;
+  const int G = A.na * A.ns;
+  if (C == 1) {
+    if (G <= 4) return launch_apply<4, 1>(s, A, h0, n, delta);
+    if (G <= 8) return launch_apply<8, 1>(s, A, h0, n, delta);
+    if (G <= 16) return launch_apply<16, 1>(s, A, h0, n, delta);
+    return launch_apply<32, 1>(s, A, h0, n, delta);
+  }
+  if (G <= 4) return launch_apply<4, 3>(s, A, h0, n, delta);
+  if (G <= 8) return launch_apply<8, 3>(s, A, h0, n, delta);
+  return launch_apply<32, 3>(s, A, h0, n, delta);
+}
+
 cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2 *y,
                            const double *value, uint32_t n, const double *radius, uint32_t H, int na,
                            int ns, int C, int *sectors, int *err, unsigned long long *st_cnt,

@@ -59,6 +59,10 @@ struct GatherArgs {
   const double2 *eye_mis;                      // per hit point {d_vcm, d_vm}
   const double *p_vcm, *p_vm, *p_cont;         // per photon, sorted order
   const double3 *wo, *alb;                     // eye Bsdf (cos_o, continuation prob)
+  // multi-GPU option B: per-hit-point partial sums of this launch's photons
+  // (row [count G | sum C*G | sum_sq C*G | power 3], fp64) instead of the
+  // end-of-iteration update; pooled on the owner by launch_apply_deltas
+  double *delta_out;
   // counters
   unsigned long long *counters;  // cumulative [accepted, candidates, exact, ambiguous]
   unsigned int *iter_tr;         // this launch [tested, rejected]
@@ -191,6 +195,10 @@ cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2
                            int na, int ns, int C, int *sectors, int *err,
                            unsigned long long *st_cnt, double *st_sum, double *st_sq, int phase);
 cudaError_t launch_end_iteration(cudaStream_t s, const EndArgs &A);
+// pools summed option-B rows into regions [h0, h0 + n) and runs the
+// end-of-iteration policy (finalize_hit)
+cudaError_t launch_apply_deltas(cudaStream_t s, const GatherArgs &A, int C, uint32_t h0, uint32_t n,
+                                const double *delta);
 cudaError_t launch_hit_weights(cudaStream_t s, const double3 *nrm, const double3 *wo,
                                const double3 *thr, const double3 *alb, uint32_t H, double3 *K);
 

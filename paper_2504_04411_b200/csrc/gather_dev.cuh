@@ -452,6 +452,24 @@ static __device__ __forceinline__ void finalize_hit(const GatherArgs &A, uint32_
                                                  double &rmax) {
   const int G = A.na * A.ns;
   const int CG = G * CH;
+  if (A.delta_out) {  // option B: hand the partial sums to the owner
+    double *d = A.delta_out + (size_t)h * (size_t)(G + 2 * CG + 3);
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g)
+      if (g < G) d[g] = (double)cnt[g];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+      for (int g = 0; g < GMAX; ++g)
+        if (g < G) {
+          d[G + c * G + g] = sm[c][g];
+          d[G + CG + c * G + g] = sq[c][g];
+        }
+    d[G + 2 * CG] = p0;
+    d[G + 2 * CG + 1] = p1;
+    d[G + 2 * CG + 2] = p2;
+    return;
+  }
   const size_t base = (size_t)h * CG;
   const double r = A.radius[h];
   uint32_t t = A.t[h];

@@ -88,3 +88,48 @@ def test_partitions_cover_exactly():
         shares = [photon_share(1 << 22, r, world) for r in range(world)]
         assert sum(c for _, c in shares) == 1 << 22
         assert all(s[0] + s[1] == t[0] for s, t in zip(shares, shares[1:]))
+
+
+def _worker_b(rank, world, port, outdir):
+    """Option B plumbing: reduce-scatter of partial-sum rows to owners and the
+    all-gather of owner values, over gloo."""
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    from paper_2504_04411_b200.distributed import (allgather_owner_values, owner_slice,
+                                                   reduce_scatter_rows)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    H, stride = 37, 5
+    rows = torch.arange(H * stride, dtype=torch.float64).reshape(H, stride) * (rank + 1)
+    mine = reduce_scatter_rows(rows, world)
+    h0, n = owner_slice(H, rank, world)
+    full = allgather_owner_values(mine[:n, 0].clone(), H, world)
+    np.save(os.path.join(outdir, f"b{rank}.npy"), {"mine": mine[:n].numpy(), "full": full.numpy(),
+                                                    "h0": h0}, allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_option_b_row_exchange(tmp_path, world):
+    import torch.multiprocessing as mp
+    mp.spawn(_worker_b, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    H, stride = 37, 5
+    base = np.arange(H * stride, dtype=np.float64).reshape(H, stride)
+    total = base * sum(r + 1 for r in range(world))
+    for r in range(world):
+        d = np.load(tmp_path / f"b{r}.npy", allow_pickle=True).item()
+        n = len(d["mine"])
+        assert np.array_equal(d["mine"], total[d["h0"]:d["h0"] + n])
+        assert np.array_equal(d["full"], total[:, 0])
+
+
+def test_owner_slices_cover_exactly():
+    from paper_2504_04411_b200.distributed import owner_slice
+    for H in (1, 7, 37, 512 * 512):
+        for world in (1, 2, 3, 8):
+            s = [owner_slice(H, r, world) for r in range(world)]
+            assert s[0][0] == 0 and sum(n for _, n in s) == H
+            assert all(a[0] + a[1] == b[0] for a, b in zip(s, s[1:]))
