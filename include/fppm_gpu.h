@@ -289,6 +289,30 @@ int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *scene);
  * receives the deposit count (synchronizes). */
 int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t n_paths,
                            uint32_t max_depth, double mis_radius, uint32_t *n_photons);
+/* ---- eye pass and film (integrator.cpp:407-474, film.cpp:21-50) ---- */
+typedef struct fppm_camera {   /* Camera (scene.hpp:75-82) */
+  double position[3];
+  double look_at[3];
+  double up[3];
+  double vfov_deg;
+  int32_t width, height;
+} fppm_camera;
+/* Pinhole camera; width * height <= max_hitpoints.  Clears the film. */
+int fppm_gpu_set_camera(fppm_gpu_ctx *ctx, const fppm_camera *camera);
+/* Renderer::pixel_pm's camera walk for every pixel (RngStream(seed, iteration,
+ * px, kEyeStream)): jittered ray, emitted radiance along the specular chain,
+ * and the first non-delta hit as the pixel's hit point (move_to + eye Bsdf;
+ * gathered = 0 when the walk ends without one).  Replaces set_hitpoints. */
+int fppm_gpu_trace_eye(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration);
+/* Copies the current hit points (fppm_hitpoints layout; any field may be
+ * NULL) and, after trace_eye, the per-pixel emitted radiance [n][3]. */
+int fppm_gpu_get_hitpoints(fppm_gpu_ctx *ctx, fppm_hitpoints *out, double *emitted);
+/* Film::add_iteration of this iteration's estimate: emitted + flux / (pi r^2 J)
+ * of the gather_test / iterate that followed trace_eye. */
+int fppm_gpu_film_add(fppm_gpu_ctx *ctx);
+/* Film::image(): per-pixel mean over the added iterations ([npix][3] host). */
+int fppm_gpu_film_mean(fppm_gpu_ctx *ctx, double *rgb, uint64_t *iterations);
+
 /* Copies the staged photons' VCM partials (d_vcm, d_vm, cont; photon order)
  * to host arrays of n_photons doubles each (vcm_plus contexts only). */
 int fppm_gpu_get_photon_mis(fppm_gpu_ctx *ctx, double *d_vcm, double *d_vm, double *cont);

@@ -512,6 +512,21 @@ orc_session *orc_session_create(const orc_config *cfg, size_t H,
   return s;
 }
 
+/* move_to with new hit points (integrator.cpp:433-440): the eye pass of every
+ * iteration moves each region's center; radius, t and stats stay. */
+void orc_session_set_hitpoints(orc_session *s, const double *pos, const double *nrm, const double *wo,
+                               const double *thr, const double *alb, const uint32_t *eye_depth,
+                               const uint8_t *gathered) {
+  const size_t H = s->H;
+  memcpy(s->pos, pos, sizeof(double) * 3 * H);
+  memcpy(s->nrm, nrm, sizeof(double) * 3 * H);
+  memcpy(s->wo, wo, sizeof(double) * 3 * H);
+  memcpy(s->thr, thr, sizeof(double) * 3 * H);
+  memcpy(s->alb, alb, sizeof(double) * 3 * H);
+  memcpy(s->eye_depth, eye_depth, sizeof(uint32_t) * H);
+  if (gathered) memcpy(s->gathered, gathered, H); else memset(s->gathered, 1, H);
+}
+
 void orc_session_free(orc_session *s) {
   if (!s) return;
   free(s->pos); free(s->nrm); free(s->wo); free(s->thr); free(s->alb);

@@ -116,6 +116,7 @@ class Oracle:
         self._sf = fn("session_free", None, [C.c_void_p])
         self._smr = fn("session_max_radius", C.c_double, [C.c_void_p])
         self._seye = fn("session_set_eye_mis", None, [C.c_void_p, _dp, _dp])
+        self._shp = fn("session_set_hitpoints", None, [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _u32p, _u8p])
         self._sphm = fn("session_set_photon_mis", None, [C.c_void_p, _dp, _dp, _dp, C.c_size_t])
         self._mwm = fn("mis_weight_merge", C.c_double, [C.c_int, C.c_double, C.c_double, C.c_double,
                                                         C.c_double, C.c_double, C.c_double,
@@ -137,6 +138,13 @@ class Oracle:
                                                         C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
                                                         C.c_uint32, C.c_void_p, C.c_void_p])
             self._scnf = fn("scene_free", None, [C.c_void_p])
+            self._eye = fn("eye_pass", None, [C.c_void_p, _dp, C.c_double, C.c_int, C.c_int, C.c_uint64,
+                                              C.c_uint64, C.c_uint32] + [C.c_void_p] * 8)
+            self._render = fn("render_fppm", C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, C.c_int,
+                                                       C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64,
+                                                       C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
+                                                       C.c_void_p, C.c_void_p, _dp])
+            self._brad = fn("bounding_radius", C.c_double, [C.c_void_p])
             self._trace = fn("trace_photons", C.c_size_t, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
                                                            C.c_uint32, C.c_uint32, C.c_int, C.c_double,
                                                            C.c_double, C.c_int, C.c_size_t] + [C.c_void_p] * 7)
@@ -254,6 +262,44 @@ class _Scene:
         return out
 
 
+def _cam9(cam):
+    return np.ascontiguousarray(np.concatenate([cam.position, cam.look_at, cam.up]).astype(np.float64))
+
+
+def _scene_eye(self, cam, seed, iteration, max_depth):
+    """pixel_pm's camera walk per pixel (hit points + emitted radiance)."""
+    n = cam.width * cam.height
+    out = dict(pos=np.zeros((n, 3)), nrm=np.zeros((n, 3)), wo=np.zeros((n, 3)), thr=np.zeros((n, 3)),
+               alb=np.zeros((n, 3)), eye_depth=np.zeros(n, np.uint32), gathered=np.zeros(n, np.uint8),
+               emitted=np.zeros((n, 3)))
+    c9 = _cam9(cam)
+    self.o._eye(self.h, c9.ctypes.data_as(_dp), cam.vfov_deg, cam.width, cam.height, seed, iteration, max_depth,
+                *[out[k].ctypes.data for k in ("pos", "nrm", "wo", "thr", "alb", "eye_depth", "gathered",
+                                                "emitted")])
+    return out
+
+
+def _scene_render(self, cam, seed, iterations, max_depth, light_paths, r0_frac=0.002, n_annuli=2, n_sectors=6,
+                  alpha_f=0.01, threads=0):
+    """The reference's render() with Algorithm::fppm: (film mean, last radii, seconds)."""
+    n = cam.width * cam.height
+    film = np.zeros((n, 3))
+    radius = np.zeros(n)
+    secs = C.c_double()
+    c9 = _cam9(cam)
+    rc = self.o._render(self.h, c9.ctypes.data_as(_dp), cam.vfov_deg, cam.width, cam.height, seed, iterations,
+                        max_depth, light_paths, r0_frac, n_annuli, n_sectors, alpha_f, threads,
+                        film.ctypes.data, radius.ctypes.data, C.byref(secs))
+    if rc:
+        raise OracleError("reference render failed")
+    return film, radius, secs.value
+
+
+_Scene.eye_pass = _scene_eye
+_Scene.render_fppm = _scene_render
+_Scene.bounding_radius = lambda self: self.o._brad(self.h)
+
+
 class _Grid:
     def __init__(self, o, h, n):
         self.o, self.h, self.n = o, h, n
@@ -318,6 +364,17 @@ class _Session:
 
     def max_radius(self):
         return self.o._smr(self.h)
+
+    def set_hitpoints(self, hit):
+        """move_to for every region (new eye-pass hit points; state kept)."""
+        kp = {k: np.ascontiguousarray(hit[k], np.float64) for k in ("pos", "nrm", "wo", "thr", "alb")}
+        kp["eye_depth"] = np.ascontiguousarray(hit["eye_depth"], np.uint32)
+        g = hit.get("gathered")
+        kp["gathered"] = None if g is None else np.ascontiguousarray(g, np.uint8)
+        assert len(kp["pos"]) == self.H
+        self._keep = kp
+        self.o._shp(self.h, *[_ptr(kp[k], _dp) for k in ("pos", "nrm", "wo", "thr", "alb")],
+                    _ptr(kp["eye_depth"], _u32p), _ptr(kp["gathered"], _u8p))
 
     def set_eye_mis(self, d_vcm, d_vm):
         """VCM+: eye-vertex MIS partials per hit point."""

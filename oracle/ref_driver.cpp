@@ -37,6 +37,8 @@
 #include "fppm/gather.hpp"
 #include "fppm/path.hpp"
 #include "fppm/scene.hpp"
+#include "fppm/integrator.hpp"
+#include "fppm/film.hpp"
 #include "fppm/sampling.hpp"
 #include "fppm/special_functions.hpp"
 #include "fppm/stat_tests.hpp"
@@ -267,6 +269,21 @@ void* ref_session_create(const RefConfig* cfg, size_t H, const double* pos,
 }
 
 void ref_session_free(void* s) { delete static_cast<RefSession*>(s); }
+
+void ref_session_set_hitpoints(void* sp, const double* pos, const double* nrm, const double* wo,
+                               const double* thr, const double* alb, const uint32_t* eye_depth,
+                               const uint8_t* gathered) {
+  auto* s = static_cast<RefSession*>(sp);
+  for (size_t h = 0; h < s->pos.size(); ++h) {
+    s->pos[h] = {pos[3 * h], pos[3 * h + 1], pos[3 * h + 2]};
+    s->nrm[h] = {nrm[3 * h], nrm[3 * h + 1], nrm[3 * h + 2]};
+    s->wo[h] = {wo[3 * h], wo[3 * h + 1], wo[3 * h + 2]};
+    s->thr[h] = {thr[3 * h], thr[3 * h + 1], thr[3 * h + 2]};
+    s->mat[h].albedo = Rgb{alb[3 * h], alb[3 * h + 1], alb[3 * h + 2]};
+    s->eye_depth[h] = eye_depth[h];
+    s->gathered[h] = gathered ? gathered[h] : 1;
+  }
+}
 
 void ref_session_set_eye_mis(void* sp, const double* d_vcm, const double* d_vm) {
   auto* s = static_cast<RefSession*>(sp);
@@ -534,6 +551,122 @@ size_t ref_trace_photons(void* sp, uint64_t seed, uint64_t iteration, uint32_t b
     }
   return n;
 }
+
+// ---- eye pass + full render ------------------------------------------------
+static Camera make_cam(const double* c9, double vfov, int w, int h) {
+  Camera cam;
+  cam.position = {c9[0], c9[1], c9[2]};
+  cam.look_at = {c9[3], c9[4], c9[5]};
+  cam.up = {c9[6], c9[7], c9[8]};
+  cam.vfov_deg = vfov;
+  cam.width = w;
+  cam.height = h;
+  return cam;
+}
+
+// Renderer::pixel_pm's camera walk (integrator.cpp:407-474) up to the gather,
+// restated on the reference's public pieces (the Renderer is private):
+// make_camera_frame / make_camera_ray, intersect, Bsdf, RngStream with
+// kEyeStream = 1.  Per pixel: hit point (pos, shading normal, wo, throughput,
+// albedo, eye depth, gathered) and the emitted radiance collected on the way.
+void ref_eye_pass(void* sp, const double* cam9, double vfov, int w, int h, uint64_t seed, uint64_t iteration,
+                  uint32_t max_depth, double* pos, double* nrm, double* wo_out, double* thr, double* alb,
+                  uint32_t* eye_depth, uint8_t* gathered, double* emitted) {
+  const Scene& scene = static_cast<RefScene*>(sp)->scene;
+  const CameraFrame cam = make_camera_frame(make_cam(cam9, vfov, w, h));
+  const std::size_t npix = static_cast<std::size_t>(w) * h;
+  for (std::size_t px = 0; px < npix; ++px) {
+    RngStream rng(seed, iteration, px, 1 /* kEyeStream */);
+    const double sx = static_cast<double>(px % cam.width) + rng.next_double();
+    const double sy = static_cast<double>(px / cam.width) + rng.next_double();
+    Ray ray = make_camera_ray(cam, sx, sy);
+    Rgb throughput{1.0, 1.0, 1.0};
+    Rgb out;
+    gathered[px] = 0;
+    eye_depth[px] = 0;
+    for (int k = 0; k < 3; ++k) pos[3 * px + k] = nrm[3 * px + k] = wo_out[3 * px + k] = thr[3 * px + k] = alb[3 * px + k] = 0.0;
+    nrm[3 * px + 2] = wo_out[3 * px + 2] = 1.0;
+    for (std::uint32_t depth = 1; depth <= max_depth; ++depth) {
+      const auto hit = intersect(scene, ray);
+      if (!hit) break;
+      const Vec3 wo = -ray.dir;
+      if (hit->emitter >= 0 && hit->front_face)
+        out += throughput * scene.emitters[static_cast<std::size_t>(hit->emitter)].radiance;
+      const Material& mat = scene.materials[static_cast<std::size_t>(hit->material)];
+      const Bsdf bsdf(mat, hit->shading_normal, wo, hit->front_face);
+      if (!bsdf.is_delta_only()) {
+        const double p3[5][3] = {{hit->point.x, hit->point.y, hit->point.z},
+                                 {hit->shading_normal.x, hit->shading_normal.y, hit->shading_normal.z},
+                                 {wo.x, wo.y, wo.z},
+                                 {throughput.r, throughput.g, throughput.b},
+                                 {mat.albedo.r, mat.albedo.g, mat.albedo.b}};
+        double* dst[5] = {pos, nrm, wo_out, thr, alb};
+        for (int f = 0; f < 5; ++f)
+          for (int k = 0; k < 3; ++k) dst[f][3 * px + k] = p3[f][k];
+        eye_depth[px] = depth;
+        gathered[px] = 1;
+        break;
+      }
+      if (depth == max_depth) break;
+      const auto s = bsdf.sample(rng);
+      if (!s || s->pdf_w <= 0.0 || s->weight.is_black()) break;
+      double q = 1.0;
+      if (depth >= kRouletteDepth) {
+        q = bsdf.continuation_prob();
+        if (rng.next_double() >= q) break;
+      }
+      throughput = throughput * s->weight / q;
+      ray = Ray{hit->point, s->dir};
+    }
+    emitted[3 * px] = out.r;
+    emitted[3 * px + 1] = out.g;
+    emitted[3 * px + 2] = out.b;
+  }
+}
+
+// The reference's own render() (integrator.cpp:669-...) with the FPPM
+// algorithm: film mean [npix][3] and the last iteration's radii [npix].
+int ref_render_fppm(void* sp, const double* cam9, double vfov, int w, int h, uint64_t seed, uint64_t iterations,
+                    uint32_t max_depth, uint64_t light_paths, double r0_frac, int na, int ns, double alpha_f,
+                    int threads, double* film_mean, double* radius, double* seconds) {
+  RefScene* rs = static_cast<RefScene*>(sp);
+  Scene scene = rs->scene;
+  scene.has_camera = true;
+  scene.camera = make_cam(cam9, vfov, w, h);
+  IntegratorConfig cfg;
+  cfg.algorithm = Algorithm::fppm;
+  cfg.iterations = iterations;
+  cfg.seed = seed;
+  cfg.max_depth = max_depth;
+  cfg.threads = threads;
+  cfg.r0_frac = r0_frac;
+  cfg.light_paths = light_paths;
+  cfg.test.n_annuli = na;
+  cfg.test.n_sectors = ns;
+  cfg.test.alpha_f = alpha_f;
+  try {
+    const auto t0 = std::chrono::steady_clock::now();
+    RenderResult res = render(scene, cfg);
+    if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const Image img = res.film.image();
+    for (std::size_t i = 0; i < img.pixels.size(); ++i) {
+      film_mean[3 * i] = img.pixels[i].r;
+      film_mean[3 * i + 1] = img.pixels[i].g;
+      film_mean[3 * i + 2] = img.pixels[i].b;
+    }
+    if (radius && !res.reports.empty()) {
+      const auto& r = res.reports.back().radius;
+      for (std::size_t i = 0; i < r.size(); ++i) radius[i] = r[i];
+    }
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return 0;
+}
+
+// bounding_radius (scene_geometry.cpp:341-362): the initial radius is
+// r0_frac times this (integrator.cpp:121).
+double ref_bounding_radius(void* sp) { return bounding_radius(static_cast<RefScene*>(sp)->scene); }
 
 unsigned ref_hardware_threads() { return std::thread::hardware_concurrency(); }
 

@@ -121,6 +121,11 @@ class DeviceView(C.Structure):
                 ("photon_depth", C.c_void_p), ("radius", C.c_void_p), ("counters", C.c_void_p)]
 
 
+class CameraStruct(C.Structure):
+    _fields_ = [("position", C.c_double * 3), ("look_at", C.c_double * 3), ("up", C.c_double * 3),
+                ("vfov_deg", C.c_double), ("width", C.c_int32), ("height", C.c_int32)]
+
+
 # (name, restype, argtypes)
 _SIGS = [
     ("fppm_gpu_abi_version", C.c_int, []),
@@ -160,6 +165,11 @@ _SIGS = [
     ("fppm_gpu_trace_photons", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_double,
                                          C.POINTER(C.c_uint32)]),
     ("fppm_gpu_get_photon_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("fppm_gpu_set_camera", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("fppm_gpu_trace_eye", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64]),
+    ("fppm_gpu_film_add", C.c_int, [C.c_void_p]),
+    ("fppm_gpu_get_hitpoints", C.c_int, [C.c_void_p, C.POINTER(HitPoints), C.c_void_p]),
+    ("fppm_gpu_film_mean", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
     ("fppm_gpu_delta_stride", C.c_uint32, [C.c_void_p]),
     ("fppm_gpu_gather_deltas", C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p]),
     ("fppm_gpu_apply_deltas", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,

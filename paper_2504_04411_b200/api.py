@@ -288,6 +288,54 @@ class FppmContext:
         self.N = n.value
         return n.value
 
+    def set_camera(self, camera):
+        """Pinhole camera (scene.Camera); clears the film."""
+        from .scene import Camera  # noqa: F401
+        c = N.CameraStruct((C.c_double * 3)(*camera.position), (C.c_double * 3)(*camera.look_at),
+                           (C.c_double * 3)(*camera.up), float(camera.vfov_deg), int(camera.width),
+                           int(camera.height))
+        self._check(self._lib.fppm_gpu_set_camera(self._h, C.byref(c)))
+        self.camera = camera
+
+    def trace_eye(self, seed: int, iteration: int):
+        """pixel_pm's camera walk (integrator.cpp:407-474): one hit point per
+        pixel (gathered = 0 where the walk found no rough surface)."""
+        self._check(self._lib.fppm_gpu_trace_eye(self._h, seed, iteration))
+        self.H = self.camera.width * self.camera.height
+
+    def get_hitpoints(self, emitted: bool = False) -> dict:
+        H = self.H
+        o = dict(pos=np.zeros((H, 3)), nrm=np.zeros((H, 3)), wo=np.zeros((H, 3)), thr=np.zeros((H, 3)),
+                 alb=np.zeros((H, 3)), eye_depth=np.zeros(H, np.uint32), gathered=np.zeros(H, np.uint8))
+        hp = N.HitPoints(*[o[k].ctypes.data for k in ("pos", "nrm", "wo", "thr", "alb", "eye_depth",
+                                                       "gathered")])
+        em = np.zeros((H, 3)) if emitted else None
+        self._check(self._lib.fppm_gpu_get_hitpoints(self._h, C.byref(hp), _ptr(em)))
+        if emitted:
+            o["emitted"] = em
+        return o
+
+    def film_add(self):
+        self._check(self._lib.fppm_gpu_film_add(self._h))
+
+    def film_mean(self):
+        """(image [height, width, 3] fp64, iterations)."""
+        n = self.camera.width * self.camera.height
+        out = np.zeros((n, 3))
+        it = C.c_uint64()
+        self._check(self._lib.fppm_gpu_film_mean(self._h, out.ctypes.data, C.byref(it)))
+        return out.reshape(self.camera.height, self.camera.width, 3), it.value
+
+    def render_iteration(self, seed: int, iteration: int, light_paths: int, max_depth: Optional[int] = None,
+                         outputs: bool = False, stats: bool = False):
+        """One full FPPM iteration of Renderer::step on the device: light
+        phase, eye pass, grid + gather + F-test, film."""
+        self.trace_photons(seed, iteration, light_paths, max_depth or self.config.max_depth)
+        self.trace_eye(seed, iteration)
+        o, sm = self.iterate(iteration, outputs=outputs, stats=stats, summary=outputs or stats)
+        self.film_add()
+        return o, sm
+
     def get_photon_mis(self) -> dict:
         n = self.N
         o = dict(d_vcm=np.zeros(n), d_vm=np.zeros(n), cont=np.zeros(n))

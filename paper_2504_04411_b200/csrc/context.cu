@@ -50,6 +50,10 @@ struct fppm_gpu_ctx {
   const uint32_t *in_depth = nullptr;
 
   // light phase: scene on the device + per-path deposit slots
+  fppm_b200::CamD cam{};
+  bool has_camera = false;
+  double3 *d_emit = nullptr, *d_film = nullptr;  // per pixel: emitted radiance, film sum
+  uint64_t film_iters = 0;
   fppm_b200::TraceScene scene{};
   void *scene_mem[9] = {};  // [8]: per-primitive constants (k_scene_prep)
   uint32_t *t_ctr = nullptr;
@@ -468,6 +472,8 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
   if (ctx->d_eye_mis) cudaFree(ctx->d_eye_mis);
+  if (ctx->d_emit) cudaFree(ctx->d_emit);
+  if (ctx->d_film) cudaFree(ctx->d_film);
   for (void *p : ctx->scene_mem)
     if (p) cudaFree(p);
   {
@@ -1373,6 +1379,115 @@ int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration,
   ctx->grid_valid = false;
   use_staging(ctx);
   if (n_photons) *n_photons = total;
+  return FPPM_OK;
+}
+
+// make_camera_frame (path.cpp:122-133) on the host: glibc tan, no FMA, as
+// the reference build.
+static void vnorm(double v[3]) {
+  const double l = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  v[0] = v[0] / l;
+  v[1] = v[1] / l;
+  v[2] = v[2] / l;
+}
+static void vcross(const double a[3], const double b[3], double o[3]) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+int fppm_gpu_set_camera(fppm_gpu_ctx *ctx, const fppm_camera *c) {
+  if (!ctx || !c) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c->width < 1 || c->height < 1) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "camera resolution must be >= 1");
+  const uint64_t npix = (uint64_t)c->width * (uint64_t)c->height;
+  if (npix > ctx->cfg.max_hitpoints) return fail(ctx, FPPM_ERR_CAPACITY, "camera pixels exceed max_hitpoints");
+  CamD &k = ctx->cam;
+  for (int i = 0; i < 3; ++i) {
+    k.pos[i] = c->position[i];
+    k.fwd[i] = c->look_at[i] - c->position[i];
+  }
+  vnorm(k.fwd);
+  vcross(k.fwd, c->up, k.right);
+  vnorm(k.right);
+  vcross(k.right, k.fwd, k.up);
+  k.width = c->width;
+  k.height = c->height;
+  const double half_fov = 0.5 * c->vfov_deg * 3.141592653589793 / 180.0;
+  k.plane_dist = (c->height * 0.5) / std::tan(half_fov);
+  if (!ctx->d_emit) {
+    const size_t n = std::max<uint32_t>(ctx->cfg.max_hitpoints, 1);
+    FPPM_CUDA_OK(dalloc(&ctx->d_emit, n));
+    FPPM_CUDA_OK(dalloc(&ctx->d_film, n));
+  }
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_film, 0, sizeof(double3) * npix, ctx->stream));
+  ctx->film_iters = 0;
+  ctx->has_camera = true;
+  return FPPM_OK;
+}
+
+int fppm_gpu_trace_eye(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->has_scene || !ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "trace_eye needs set_scene and set_camera");
+  EyeArgs E;
+  E.sc = ctx->scene;
+  E.cam = ctx->cam;
+  E.seed = seed;
+  E.iteration = iteration;
+  E.max_depth = ctx->cfg.max_depth;
+  E.npix = (uint32_t)((uint64_t)ctx->cam.width * ctx->cam.height);
+  E.pos = ctx->d_pos; E.nrm = ctx->d_nrm; E.wo = ctx->d_wo; E.thr = ctx->d_thr; E.alb = ctx->d_alb;
+  E.emitted = ctx->d_emit;
+  E.eye_depth = ctx->d_eye;
+  E.gathered = ctx->d_gathered;
+  FPPM_CUDA_OK(launch_trace_eye(ctx->stream, E, ctx->scene_mem[8], ctx->sms));
+  return finish_hitpoints(ctx, E.npix, true);
+}
+
+int fppm_gpu_get_hitpoints(fppm_gpu_ctx *ctx, fppm_hitpoints *o, double *emitted) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  const size_t H = ctx->H, b3 = sizeof(double3) * H;
+  int rc;
+  if (o) {
+    if ((rc = copy_out(ctx, const_cast<double *>(o->pos), ctx->d_pos, b3))) return rc;
+    if ((rc = copy_out(ctx, const_cast<double *>(o->normal), ctx->d_nrm, b3))) return rc;
+    if ((rc = copy_out(ctx, const_cast<double *>(o->wo), ctx->d_wo, b3))) return rc;
+    if ((rc = copy_out(ctx, const_cast<double *>(o->throughput), ctx->d_thr, b3))) return rc;
+    if ((rc = copy_out(ctx, const_cast<double *>(o->albedo), ctx->d_alb, b3))) return rc;
+    if ((rc = copy_out(ctx, const_cast<uint32_t *>(o->eye_depth), ctx->d_eye, sizeof(uint32_t) * H))) return rc;
+    if ((rc = copy_out(ctx, const_cast<uint8_t *>(o->gathered), ctx->d_gathered, H))) return rc;
+  }
+  if (emitted) {
+    if (!ctx->d_emit) return fail(ctx, FPPM_ERR_STATE, "no eye pass yet");
+    if ((rc = copy_out(ctx, emitted, ctx->d_emit, b3))) return rc;
+  }
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  return FPPM_OK;
+}
+
+int fppm_gpu_film_add(fppm_gpu_ctx *ctx) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "film_add before set_camera");
+  const uint32_t npix = (uint32_t)((uint64_t)ctx->cam.width * ctx->cam.height);
+  if (npix != ctx->H) return fail(ctx, FPPM_ERR_STATE, "film_add: hit points are not the camera's pixels");
+  FPPM_CUDA_OK(launch_film(ctx->stream, 0, npix, ctx->d_emit, ctx->d_gathered, ctx->o_flux, ctx->o_gather_r,
+                           (double)ctx->cfg.samples_per_iteration, ctx->d_film, nullptr, ctx->sms));
+  ctx->film_iters++;
+  return FPPM_OK;
+}
+
+int fppm_gpu_film_mean(fppm_gpu_ctx *ctx, double *rgb, uint64_t *iterations) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "film_mean before set_camera");
+  const uint32_t npix = (uint32_t)((uint64_t)ctx->cam.width * ctx->cam.height);
+  if (iterations) *iterations = ctx->film_iters;
+  if (!rgb) return FPPM_OK;
+  const size_t bytes = sizeof(double) * 3 * (size_t)npix;
+  FPPM_CUDA_OK(ensure_scratch(ctx, bytes + 64));
+  double *d = static_cast<double *>(ctx->d_scratch);
+  FPPM_CUDA_OK(launch_film(ctx->stream, 1, npix, nullptr, nullptr, nullptr, nullptr, (double)ctx->film_iters,
+                           ctx->d_film, d, ctx->sms));
+  FPPM_CUDA_OK(cudaMemcpyAsync(rgb, d, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
   return FPPM_OK;
 }
 

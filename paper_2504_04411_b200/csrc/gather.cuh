@@ -250,6 +250,25 @@ struct TraceArgs {
   uint32_t *count;                      // [n_paths]
   uint32_t *path_counter;               // work queue (reset by launch_trace)
 };
+struct CamD {  // CameraFrame (path.hpp:93-98), built on the host (make_camera_frame)
+  double pos[3], fwd[3], right[3], up[3];
+  double plane_dist;
+  int width, height;
+};
+struct EyeArgs {
+  TraceScene sc;
+  CamD cam;
+  unsigned long long seed, iteration;
+  uint32_t max_depth, npix;
+  double3 *pos, *nrm, *wo, *thr, *alb, *emitted;
+  uint32_t *eye_depth;
+  uint8_t *gathered;
+};
+cudaError_t launch_trace_eye(cudaStream_t s, const EyeArgs &E, const void *prep, int sms);
+// op 0: film += estimate (J = samples per iteration); op 1: mean_out = film / J (J = iterations)
+cudaError_t launch_film(cudaStream_t s, int op, uint32_t npix, const double3 *emitted, const uint8_t *gathered,
+                        const double *flux, const double *gather_r, double J, double3 *film, double *mean_out,
+                        int sms);
 size_t trace_prep_bytes(int n_prim);
 int trace_max_prims();
 cudaError_t launch_scene_prep(cudaStream_t s, const TraceScene &sc, void *prep);

@@ -101,7 +101,7 @@ __device__ __forceinline__ double mpow(double beta, double x) { return beta == 1
 // same IEEE expression the reference evaluates per call (cross(e1, e2), the
 // Gram entries, r * r, 1 / r, 1 / area), so hoisting changes no bit.
 struct PrimD {
-  int kind, mat;
+  int kind, mat, emitter, pad;  // emitter: area emitter on this primitive, -1 if none
   double c[3], e1[3], e2[3];
   double n[3];   // quad: cross(e1, e2)
   double on[3];  // quad: normalize(cross(e1, e2))
@@ -118,6 +118,10 @@ __global__ void k_scene_prep(const TraceScene sc, PrimD *out) {
   PrimD d;
   d.kind = sc.prim_kind[i];
   d.mat = sc.prim_mat[i];
+  d.emitter = -1;
+  d.pad = 0;
+  for (int e = 0; e < sc.n_emit; ++e)
+    if (sc.emit_prim[e] == i) d.emitter = e;
   for (int k = 0; k < 3; ++k) {
     d.c[k] = p[k];
     d.e1[k] = p[3 + k];
@@ -185,7 +189,7 @@ struct HitD {
   double t;
   DVec point, sn;
   bool front;
-  int mat;
+  int mat, prim;
 };
 
 // intersect + fill_hit (scene_geometry.cpp:186-224, 263-315): closest hit
@@ -209,6 +213,7 @@ __device__ __forceinline__ bool intersect(const PrimD *P, int np, DVec o, DVec d
   h.t = tbest;
   h.point = add(o, mul(d, tbest));
   h.mat = p.mat;
+  h.prim = best;
   DVec outward;
   if (p.kind == 0)
     outward = mul(sub(h.point, dv(p.c[0], p.c[1], p.c[2])), p.inv_r);
@@ -514,6 +519,173 @@ __global__ void __launch_bounds__(256) k_trace_compact(const TraceArgs A, const 
       }
     }
   }
+}
+
+// ---------------------------------------------------------------- eye pass
+// Renderer::pixel_pm's camera walk (integrator.cpp:407-474) up to the gather:
+// jittered pinhole ray (make_camera_ray, path.cpp:135-142) with
+// RngStream(seed, iteration, px, kEyeStream = 1), emitted radiance of
+// front-facing emitter hits, delta bounces (mirror / dielectric) with Russian
+// roulette from depth 5, and the first non-delta hit becomes the pixel's hit
+// point (GatherRegion::move_to, eye Bsdf, eye depth).
+__global__ void __launch_bounds__(128) k_trace_eye(const EyeArgs E, const PrimD *__restrict__ prims) {
+  __shared__ PrimD P[kMaxTracePrims];
+  const TraceScene &sc = E.sc;
+  const int np = sc.n_prim;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) P[i] = prims[i];
+  __syncthreads();
+  const CamD &cam = E.cam;
+  for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < E.npix; px += gridDim.x * blockDim.x) {
+    Rng rng(E.seed, E.iteration, px, 1ull /* kEyeStream */);
+    const double sx = da((double)(px % (uint32_t)cam.width), rng.next());
+    const double sy = da((double)(px / (uint32_t)cam.width), rng.next());
+    DVec dir = normalize(add(add(mul(dv(cam.fwd[0], cam.fwd[1], cam.fwd[2]), cam.plane_dist),
+                                 mul(dv(cam.right[0], cam.right[1], cam.right[2]),
+                                     ds(sx, dm(0.5, (double)cam.width)))),
+                             mul(dv(cam.up[0], cam.up[1], cam.up[2]), ds(dm(0.5, (double)cam.height), sy))));
+    DVec o = dv(cam.pos[0], cam.pos[1], cam.pos[2]);
+    double t0 = 1.0, t1 = 1.0, t2 = 1.0;
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+    uint8_t gathered = 0;
+    uint32_t eye_depth = 0;
+    HitD hp{};
+    DVec hwo = dv(0, 0, 0);
+    for (uint32_t depth = 1; depth <= E.max_depth; ++depth) {
+      HitD h;
+      if (!intersect(P, np, o, dir, h)) break;
+      const DVec wo = neg(dir);
+      const int em = P[h.prim].emitter;
+      if (em >= 0 && h.front) {  // out += throughput * radiance
+        const double *L = sc.emit_rad + 3 * (size_t)em;
+        e0 = da(e0, dm(t0, L[0]));
+        e1 = da(e1, dm(t1, L[1]));
+        e2 = da(e2, dm(t2, L[2]));
+      }
+      const int mk = sc.mat_kind[h.mat];
+      if (mk == 0) {  // first rough surface: gather here
+        hp = h;
+        hwo = wo;
+        eye_depth = depth;
+        gathered = 1;
+        break;
+      }
+      if (depth == E.max_depth) break;
+      const double cos_o = dot(wo, h.sn);
+      DVec ndir;
+      double pdf;
+      if (mk == 2) {  // sample_dielectric (bsdf.cpp:147-180)
+        const double eta = h.front ? sc.mat_ior[h.mat] : dd(1.0, sc.mat_ior[h.mat]);
+        const double ci = cos_o;
+        if (ci <= 0.0) break;
+        const double sin2_t = dd(ds(1.0, dm(ci, ci)), dm(eta, eta));
+        double frs;
+        if (sin2_t >= 1.0) {
+          frs = 1.0;
+        } else {
+          const double ct = __dsqrt_rn(ds(1.0, sin2_t));
+          const double rs = dd(ds(ci, dm(eta, ct)), da(ci, dm(eta, ct)));
+          const double rp = dd(ds(dm(eta, ci), ct), da(dm(eta, ci), ct));
+          frs = dm(0.5, da(dm(rs, rs), dm(rp, rp)));
+        }
+        if (rng.next() < frs) {
+          ndir = reflect(wo, h.sn);
+          pdf = frs;
+        } else {
+          const double x = ds(1.0, sin2_t);
+          const double ct = __dsqrt_rn(x > 0.0 ? x : 0.0);
+          ndir = normalize(add(mul(wo, dd(-1.0, eta)), mul(h.sn, ds(dd(ci, eta), ct))));
+          pdf = ds(1.0, frs);
+        }
+      } else {  // mirror (bsdf.cpp:108-116)
+        if (cos_o <= 0.0) break;
+        ndir = reflect(wo, h.sn);
+        pdf = 1.0;
+      }
+      const double *w = sc.mat_rgb + 3 * (size_t)h.mat;
+      if (pdf <= 0.0 || (w[0] == 0 && w[1] == 0 && w[2] == 0)) break;
+      double q = 1.0;
+      if (depth >= 5) {  // kRouletteDepth
+        q = cont_prob(sc, h.mat);
+        if (rng.next() >= q) break;
+      }
+      t0 = dd(dm(t0, w[0]), q);
+      t1 = dd(dm(t1, w[1]), q);
+      t2 = dd(dm(t2, w[2]), q);
+      o = h.point;
+      dir = ndir;
+    }
+    E.emitted[px] = make_double3(e0, e1, e2);
+    E.gathered[px] = gathered;
+    E.eye_depth[px] = eye_depth;
+    if (gathered) {
+      const double *a = sc.mat_rgb + 3 * (size_t)hp.mat;
+      E.pos[px] = make_double3(hp.point.x, hp.point.y, hp.point.z);
+      E.nrm[px] = make_double3(hp.sn.x, hp.sn.y, hp.sn.z);
+      E.wo[px] = make_double3(hwo.x, hwo.y, hwo.z);
+      E.thr[px] = make_double3(t0, t1, t2);
+      E.alb[px] = make_double3(a[0], a[1], a[2]);
+    } else {
+      E.pos[px] = make_double3(0, 0, 0);
+      E.nrm[px] = make_double3(0, 0, 1);
+      E.wo[px] = make_double3(0, 0, 1);
+      E.thr[px] = make_double3(0, 0, 0);
+      E.alb[px] = make_double3(0, 0, 0);
+    }
+  }
+}
+
+// Film::add_iteration (film.cpp:21-26) of the pixel estimate
+// out = emitted + sum / (pi r^2 J) (integrator.cpp:452-455).
+__global__ void k_film_add(uint32_t npix, const double3 *__restrict__ emitted, const uint8_t *__restrict__ gathered,
+                           const double *__restrict__ flux, const double *__restrict__ gather_r, double J,
+                           double3 *__restrict__ film) {
+  for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < npix; px += gridDim.x * blockDim.x) {
+    double3 est = emitted[px];
+    if (gathered[px]) {
+      const double r = gather_r[px];
+      const double denom = dm(dm(dm(kPi, r), r), J);
+      est.x = da(est.x, dd(flux[3 * (size_t)px], denom));
+      est.y = da(est.y, dd(flux[3 * (size_t)px + 1], denom));
+      est.z = da(est.z, dd(flux[3 * (size_t)px + 2], denom));
+    }
+    double3 f = film[px];
+    f.x = da(f.x, est.x);
+    f.y = da(f.y, est.y);
+    f.z = da(f.z, est.z);
+    film[px] = f;
+  }
+}
+
+__global__ void k_film_mean(uint32_t npix, const double3 *__restrict__ film, double iters, double *__restrict__ out) {
+  for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < npix; px += gridDim.x * blockDim.x) {
+    const double3 f = film[px];
+    out[3 * (size_t)px] = iters > 0 ? dd(f.x, iters) : 0.0;
+    out[3 * (size_t)px + 1] = iters > 0 ? dd(f.y, iters) : 0.0;
+    out[3 * (size_t)px + 2] = iters > 0 ? dd(f.z, iters) : 0.0;
+  }
+}
+
+cudaError_t launch_trace_eye(cudaStream_t s, const EyeArgs &E, const void *prep, int sms) {
+  if (E.npix == 0) return cudaSuccess;
+  unsigned blocks = (E.npix + 127) / 128;
+  if (blocks > (unsigned)sms * 16) blocks = sms * 16;
+  k_trace_eye<<<blocks, 128, 0, s>>>(E, static_cast<const PrimD *>(prep));
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_film(cudaStream_t s, int op, uint32_t npix, const double3 *emitted, const uint8_t *gathered,
+                        const double *flux, const double *gather_r, double J, double3 *film, double *mean_out,
+                        int sms) {
+  if (npix == 0) return cudaSuccess;
+  unsigned blocks = (npix + 255) / 256;
+  if (blocks > (unsigned)sms * 8) blocks = sms * 8;
+  if (op == 0)
+    k_film_add<<<blocks, 256, 0, s>>>(npix, emitted, gathered, flux, gather_r, J, film);
+  else
+    k_film_mean<<<blocks, 256, 0, s>>>(npix, film, J, mean_out);
+  note_launches(1);
+  return cudaGetLastError();
 }
 
 size_t trace_prep_bytes(int n_prim) { return sizeof(PrimD) * (size_t)(n_prim > 0 ? n_prim : 1); }

@@ -69,6 +69,51 @@ class Scene:
         )
 
 
+@dataclass
+class Camera:
+    """Pinhole camera (Camera, scene.hpp:75-82)."""
+    position: tuple = (0.0, 0.0, 0.0)
+    look_at: tuple = (0.0, 0.0, -1.0)
+    up: tuple = (0.0, 1.0, 0.0)
+    vfov_deg: float = 45.0
+    width: int = 1
+    height: int = 1
+
+
+def caustic_box_camera(res: int = 1024) -> Camera:
+    """BASELINE configs[2]: res x res pinhole at (0.5, 0.5, -1.4), FOV 40
+    degrees, looking into the room (+z)."""
+    return Camera((0.5, 0.5, -1.4), (0.5, 0.5, 0.0), (0.0, 1.0, 0.0), 40.0, res, res)
+
+
+def bounding_radius(scene: Scene) -> float:
+    """bounding_radius (scene_geometry.cpp:341-362): half the diagonal of the
+    box of all non-emitter primitives (all primitives if there are none); the
+    reference's initial radius is r0_frac (0.002) times this."""
+    emitters = set(scene.emitter_shape)
+    lo = np.full(3, np.inf)
+    hi = np.full(3, -np.inf)
+    for pass_ in range(2):
+        any_ = False
+        for i, (k, p) in enumerate(zip(scene.shape_kind, scene.shape)):
+            if pass_ == 0 and i in emitters:
+                continue
+            any_ = True
+            p = np.asarray(p, np.float64)
+            if k == SPHERE:
+                pts = [p[:3] - p[3], p[:3] + p[3]]
+            else:
+                c, e1, e2 = p[:3], p[3:6], p[6:9]
+                pts = [c, c + e1, c + e2, c + e1 + e2]
+            for q in pts:
+                lo = np.minimum(lo, q)
+                hi = np.maximum(hi, q)
+        if any_:
+            break
+    d = hi - lo
+    return 0.5 * float(np.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]))
+
+
 def caustic_box(light_radiance: float = 15.0) -> Scene:
     """BASELINE.json configs[2] / [3]: an axis-aligned unit room of five
     Lambertian walls (albedo 0.75, red/green side pair, open towards the camera
