@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--workload", default="c2", choices=["c1", "c2"])
-    p.add_argument("--kernel", default="auto", choices=["auto", "fine", "tile", "warp", "lanes"],
+    p.add_argument("--kernel", default="auto", choices=["auto", "fine", "tile", "warp", "lanes", "sparse"],
                    help="gather kernel variant (A/B)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--dist-mode", default="auto", choices=["auto", "a", "b"],
                    help="multi-GPU decomposition (distributed.py); auto = measure both in warm-up")
     p.add_argument("--cpu-trace-paths", type=int, default=1 << 20)
+    p.add_argument("--no-render", action="store_true", help="skip the C3 full-iteration leg")
     p.add_argument("--cpu-stride", type=int, default=0,
                    help="hit-point stride of the CPU sample (0 = auto)")
     return p.parse_args()
@@ -205,7 +206,8 @@ def run_reference_arm(args, wl, rank):
           "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                            "sample": sample},
           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-          "trace": reference_trace(threads, args)})
+          "trace": reference_trace(threads, args),
+          "render": None if args.no_render else reference_render(threads)})
 
 
 def reference_trace(threads, args):
@@ -276,6 +278,66 @@ def run_trace_bench(args, local_rank, steps, warmup):
             "gpu_launches": launches, "steps": steps,
             "timing": "CUDA events around fppm_gpu_trace_photons on the context stream",
             "config": trace_config()}
+
+
+RENDER_RES = 1024          # BASELINE configs[2]: 1024 x 1024 camera
+
+
+def render_config():
+    return {"workload": f"c3 full improved-PPM iteration (BASELINE configs[2]): caustic box, {RENDER_RES}^2 "
+                        f"pinhole, {TRACE_PATHS} light paths, max_depth {TRACE_MAX_DEPTH}",
+            "test": "reference defaults (C3 leaves them open): 2x6 groups, alpha_F 0.01, "
+                    "r1 = 0.002 * bounding radius, luminance channel",
+            "stages": "light phase + eye pass + grid + gather/F-test + film (Renderer::step)"}
+
+
+def run_render_bench(local_rank, steps, warmup):
+    """C3: Renderer::step on the device, timed with CUDA events per iteration."""
+    import torch
+    from paper_2504_04411_b200 import FppmContext
+    from paper_2504_04411_b200.scene import bounding_radius, caustic_box, caustic_box_camera
+    sc, cam = caustic_box(), caustic_box_camera(RENDER_RES)
+    r1 = 0.002 * bounding_radius(sc)
+    ctx = FppmContext(initial_radius=r1, samples_per_iteration=TRACE_PATHS, n_annuli=2, n_sectors=6,
+                      alpha_f=0.01, r_min_base=0.001 * r1, max_depth=TRACE_MAX_DEPTH,
+                      max_hitpoints=RENDER_RES * RENDER_RES, max_photons=4 * TRACE_PATHS, device=local_rank)
+    ctx.set_scene(sc)
+    ctx.set_camera(cam)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    for it in range(1, warmup + 1):
+        ctx.render_iteration(0x5EED, it, TRACE_PATHS)
+    torch.cuda.synchronize()
+    c0 = ctx.counters()["accepted"]
+    ms = []
+    for it in range(warmup + 1, warmup + steps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.render_iteration(0x5EED, it, TRACE_PATHS)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    q = ctx.counters()["accepted"] - c0
+    ctx.close()
+    return {"ms_per_iteration": statistics.mean(ms), "queries_per_s": q / (sum(ms) / 1e3),
+            "steps": steps, "timing": "CUDA events around FppmContext.render_iteration on the context stream",
+            "config": render_config()}
+
+
+def reference_render(threads):
+    """The reference's own render() (oracle/_ref), one C3 iteration."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle
+    from paper_2504_04411_b200.scene import caustic_box, caustic_box_camera
+    try:
+        rs = Oracle("reference").scene(caustic_box().arrays())
+        _, _, secs = rs.render_fppm(caustic_box_camera(RENDER_RES), 0x5EED, 1, TRACE_MAX_DEPTH, TRACE_PATHS,
+                                    r0_frac=0.002, n_annuli=2, n_sectors=6, alpha_f=0.01, threads=threads)
+        return {"ms_per_iteration": 1e3 * secs, "cores": threads, "kind": "reference",
+                "sample": "iteration 1 of the full C3 config through the reference's render() "
+                          "(IterationReport wall time of the whole call)"}
+    except Exception as e:
+        return {"unavailable": f"reference render failed: {e}"}
 
 
 def workload_config(wl, **extra):
@@ -528,6 +590,11 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
         trace = run_trace_bench(args, local_rank, max(args.steps, 1), max(args.warmup, 1))
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             trace["cpu_baseline"] = reference_trace(os.cpu_count() or 1, args)
+    render = None
+    if not args.no_render:
+        render = run_render_bench(local_rank, max(min(args.steps, 5), 1), max(min(args.warmup, 3), 1))
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            render["cpu_baseline"] = reference_render(os.cpu_count() or 1)
 
     if rank == 0:
         if world == 1:
@@ -575,6 +642,8 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
             line["cpu_baseline"] = cpu
         if trace:
             line["trace"] = trace
+        if render:
+            line["render"] = render
         emit(line)
     arm.close()
 

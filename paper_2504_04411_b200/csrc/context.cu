@@ -139,9 +139,16 @@ static cudaError_t dalloc(T **p, size_t count) {
 
 // gather kernel variant: 1 warp per hit point, 2 tiled, 3 lanes, 4 fine (default)
 static int gather_variant(const fppm_gpu_ctx *ctx) {
-  if (ctx->cfg.vcm_plus) return 1;  // the merge weights run on the warp kernel
+  if (ctx->cfg.vcm_plus) return ctx->cfg.gather_kernel == 5 ? 5 : 1;  // merge weights: warp / sparse kernels
   if (ctx->cfg.gather_kernel == 0) return fine_supported(ctx->G, ctx->C) ? 4 : 2;
   return ctx->cfg.gather_kernel;
+}
+
+// The kernel that will gather this grid: auto picks the fine kernel on slab
+// (planar) grids and the thread-per-hit-point kernel on 3D grids (S = 1).
+static int effective_variant(const fppm_gpu_ctx *ctx, uint32_t S) {
+  const int v = gather_variant(ctx);
+  return v == 4 && ctx->cfg.gather_kernel == 0 && S == 1 ? 5 : v;
 }
 
 static cudaError_t ensure_scratch(fppm_gpu_ctx *ctx, size_t bytes) {
@@ -346,8 +353,8 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   if (c.n_annuli * c.n_sectors > 32) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.channels != FPPM_CHANNELS_LUMINANCE && c.channels != FPPM_CHANNELS_RGB) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy < FPPM_POLICY_FTEST || c.policy > FPPM_POLICY_SCHEDULE) return FPPM_ERR_INVALID_ARGUMENT;
-  if (c.gather_kernel < 0 || c.gather_kernel > 4) return FPPM_ERR_INVALID_ARGUMENT;
-  if (c.vcm_plus && (c.gather_kernel > 1 || c.mis_n_vm < 0 || !(c.mis_beta > 0.0)))
+  if (c.gather_kernel < 0 || c.gather_kernel > 5) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.vcm_plus && ((c.gather_kernel > 1 && c.gather_kernel != 5) || c.mis_n_vm < 0 || !(c.mis_beta > 0.0)))
     return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy == FPPM_POLICY_FTEST && c.override_decision == FPPM_OVERRIDE_NONE &&
       !(c.alpha_f > 0.0 && c.alpha_f < 1.0)) return FPPM_ERR_INVALID_ARGUMENT;  // stat_tests.cpp:88
@@ -808,14 +815,15 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
     FPPM_CUDA_OK(cudaMalloc(&ctx->d_cell_start, sizeof(uint32_t) * cap));
     ctx->cell_cap = cap;
   }
+  const bool fine_layout = effective_variant(ctx, g.S) == 4;
   launch_dense_keys(s, ctx->in_pos, ctx->N, ctx->d_hdr, ctx->sort.keys_a, ctx->sort.vals_a, ctx->sms);
-  if (gather_variant(ctx) == 4 && ctx->recs.pack)
+  if (fine_layout && ctx->recs.pack)
     launch_pack_fine(s, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow, ctx->in_depth, ctx->N,
                      ctx->recs.pack, ctx->sms);
   FPPM_CUDA_OK(radix_sort_pairs(s, ctx->sort, ctx->N, g.key_bits, &ctx->d_skeys, &ctx->d_order));
   launch_cell_start(s, ctx->d_skeys, ctx->N, ctx->d_hdr, ctx->d_cell_start, g.ncells, ctx->sms);
   launch_permute(s, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,
-                 ctx->in_depth, ctx->recs, gather_variant(ctx) == 4, ctx->sms);
+                 ctx->in_depth, ctx->recs, fine_layout, ctx->sms);
   if (ctx->cfg.vcm_plus)
     launch_permute_f64x3(s, ctx->d_order, ctx->N, ctx->d_pmis_in[0], ctx->d_pmis_in[1], ctx->d_pmis_in[2],
                          ctx->d_pmis[0], ctx->d_pmis[1], ctx->d_pmis[2], ctx->sms);
@@ -1069,9 +1077,15 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
   fill_gather_args(ctx, iteration, A);
   if (snap) { A.snap_cnt = ctx->snap_cnt; A.snap_sum = ctx->snap_sum; A.snap_sq = ctx->snap_sq; }
   A.delta_out = delta;
-  if (ctx->H && gather_variant(ctx) == 1) {
+  // auto: the fine kernel on slab (planar) grids, the thread-per-hit-point
+  // kernel on 3D grids (S = 1: a few hit points per cell)
+  const int var = effective_variant(ctx, ctx->h_hdr->S);
+  if (ctx->H && (var == 1 || var == 5)) {
     if ((rc = kernel_event(ctx, 0))) return rc;
-    FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
+    if (var == 1)
+      FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
+    else
+      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, ctx->sms));
     if ((rc = kernel_event(ctx, 1))) return rc;
   } else if (ctx->H) {
     // ---- tiled path: bin hit points by home cell, build items, run

@@ -15,6 +15,76 @@
 
 namespace fppm_b200 {
 
+// One candidate of a hit point (photon_map.cpp:65-77 ball, gather_disk
+// filters integrator.cpp:388-402, value :445-451 / VCM+ :607-615, sector and
+// SectorStats::add); shared by the warp-per-hit-point and
+// thread-per-hit-point kernels.
+struct EyeVcm {
+  double cos_o, cont, d_vcm, d_vm;
+};
+
+template <int GMAX, int CH>
+static __device__ __forceinline__ void pair_accumulate(const GatherArgs &A, const HitF &F, const Hit &Hs,
+                                                       uint32_t i, const EyeVcm &E, uint32_t (&cnt)[GMAX],
+                                                       double (&sm)[CH][GMAX], double (&sq)[CH][GMAX],
+                                                       double &p0, double &p1, double &p2, uint32_t &my_acc,
+                                                       uint32_t &my_exact, uint32_t &my_amb) {
+  const double v_cos_o = E.cos_o, v_cont = E.cont, v_vcm = E.d_vcm, v_vm = E.d_vm;
+  const float4 a = __ldg(&A.rec0[i]);
+  if (!test_pair(F, a, A.max_depth)) return;
+  const float4 b = __ldg(&A.rec1[i]);
+  const float4 c2 = __ldg(&A.rec2[i]);
+  int sector;
+  bool cos_pos;
+  if (!flush_pair(F, Hs, a, b, c2, A.guard, sector, cos_pos, my_exact, my_amb)) return;
+  ++my_acc;
+  const float4 c3 = __ldg(&A.rec3[i]);
+  if (A.vcm) {
+    // merge callback (integrator.cpp:609-616): f and the pdfs of
+    // Bsdf::eval (bsdf.cpp:53-63), merge weight, val = thr * f * p.thr * w
+    const double ci = edot((double)b.w, (double)c2.x, (double)c2.y, Hs.nx, Hs.ny, Hs.nz);
+    const bool black = v_cos_o <= 0.0 || ci <= 0.0;
+    const double pf = black ? 0.0 : (ci > 0.0 ? dm(ci, kInvPi) : 0.0);
+    const double prv = black ? 0.0 : (v_cos_o > 0.0 ? dm(v_cos_o, kInvPi) : 0.0);
+    const double w = mis_weight_merge_dev(A.mis_n_vm, A.mis_beta, Hs.r, v_vcm, v_vm, A.p_vcm[i],
+                                          A.p_vm[i], dm(pf, v_cont), dm(prv, A.p_cont[i]));
+    const double k0 = ci <= 0.0 ? dm(Hs.K0, 0.0) : Hs.K0, k1 = ci <= 0.0 ? dm(Hs.K1, 0.0) : Hs.K1,
+                 k2 = ci <= 0.0 ? dm(Hs.K2, 0.0) : Hs.K2;
+    const double v0 = dm(dm(k0, (double)c2.z), w), v1 = dm(dm(k1, (double)c2.w), w),
+                 v2 = dm(dm(k2, (double)c3.x), w);
+    p0 += v0; p1 += v1; p2 += v2;
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
+    if constexpr (CH == 1) {
+      const double v = elum(v0, v1, v2);
+      acc_pred<GMAX>(sm[0], sq[0], sector, v, v * v);
+    } else {
+      acc_pred<GMAX>(sm[0], sq[0], sector, v0, v0 * v0);
+      acc_pred<GMAX>(sm[1], sq[1], sector, v1, v1 * v1);
+      acc_pred<GMAX>(sm[2], sq[2], sector, v2, v2 * v2);
+    }
+    return;
+  }
+  const double pr = cos_pos ? (double)c2.z : 0.0, pg = cos_pos ? (double)c2.w : 0.0,
+               pb_ = cos_pos ? (double)c3.x : 0.0;
+  p0 += pr; p1 += pg; p2 += pb_;
+  if constexpr (CH == 1) {
+    const double v = elum(dm(Hs.K0, pr), dm(Hs.K1, pg), dm(Hs.K2, pb_));
+    const double vv = v * v;
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
+    acc_pred<GMAX>(sm[0], sq[0], sector, v, vv);
+  } else {
+    const double v0 = dm(Hs.K0, pr), v1 = dm(Hs.K1, pg), v2 = dm(Hs.K2, pb_);
+    const double w0 = v0 * v0, w1 = v1 * v1, w2 = v2 * v2;
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
+    acc_pred<GMAX>(sm[0], sq[0], sector, v0, w0);
+    acc_pred<GMAX>(sm[1], sq[1], sector, v1, w1);
+    acc_pred<GMAX>(sm[2], sq[2], sector, v2, w2);
+  }
+}
+
 template <int GMAX, int CH>
 __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs A) {
   const int lane = threadIdx.x & 31;
@@ -58,6 +128,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
       v_vcm = em.x;
       v_vm = em.y;
     }
+    const EyeVcm eye{v_cos_o, v_cont, v_vcm, v_vm};
     if (gathered && grid.n > 0) {
       const long long ix = (long long)floor(dm(Hs.cx, grid.inv)) - grid.ix0;
       const long long iy = (long long)floor(dm(Hs.cy, grid.inv)) - grid.iy0;
@@ -96,59 +167,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
         if (idx >= total) continue;
         const uint32_t i = pb + (idx - pp);
         ++my_cand;
-        const float4 a = __ldg(&A.rec0[i]);
-        if (!test_pair(F, a, A.max_depth)) continue;
-        const float4 b = __ldg(&A.rec1[i]);
-        const float4 c2 = __ldg(&A.rec2[i]);
-        int sector;
-        bool cos_pos;
-        if (!flush_pair(F, Hs, a, b, c2, A.guard, sector, cos_pos, my_exact, my_amb)) continue;
-        ++my_acc;
-        const float4 c3 = __ldg(&A.rec3[i]);
-        if (A.vcm) {
-          // merge callback (integrator.cpp:609-616): f and the pdfs of
-          // Bsdf::eval (bsdf.cpp:53-63), merge weight, val = thr * f * p.thr * w
-          const double ci = edot((double)b.w, (double)c2.x, (double)c2.y, Hs.nx, Hs.ny, Hs.nz);
-          const bool black = v_cos_o <= 0.0 || ci <= 0.0;
-          const double pf = black ? 0.0 : (ci > 0.0 ? dm(ci, kInvPi) : 0.0);
-          const double prv = black ? 0.0 : (v_cos_o > 0.0 ? dm(v_cos_o, kInvPi) : 0.0);
-          const double w = mis_weight_merge_dev(A.mis_n_vm, A.mis_beta, Hs.r, v_vcm, v_vm, A.p_vcm[i],
-                                                A.p_vm[i], dm(pf, v_cont), dm(prv, A.p_cont[i]));
-          const double k0 = ci <= 0.0 ? dm(Hs.K0, 0.0) : Hs.K0, k1 = ci <= 0.0 ? dm(Hs.K1, 0.0) : Hs.K1,
-                       k2 = ci <= 0.0 ? dm(Hs.K2, 0.0) : Hs.K2;
-          const double v0 = dm(dm(k0, (double)c2.z), w), v1 = dm(dm(k1, (double)c2.w), w),
-                       v2 = dm(dm(k2, (double)c3.x), w);
-          p0 += v0; p1 += v1; p2 += v2;
-#pragma unroll
-          for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
-          if constexpr (CH == 1) {
-            const double v = elum(v0, v1, v2);
-            acc_pred<GMAX>(sm[0], sq[0], sector, v, v * v);
-          } else {
-            acc_pred<GMAX>(sm[0], sq[0], sector, v0, v0 * v0);
-            acc_pred<GMAX>(sm[1], sq[1], sector, v1, v1 * v1);
-            acc_pred<GMAX>(sm[2], sq[2], sector, v2, v2 * v2);
-          }
-          continue;
-        }
-        const double pr = cos_pos ? (double)c2.z : 0.0, pg = cos_pos ? (double)c2.w : 0.0,
-                     pb_ = cos_pos ? (double)c3.x : 0.0;
-        p0 += pr; p1 += pg; p2 += pb_;
-        if constexpr (CH == 1) {
-          const double v = elum(dm(Hs.K0, pr), dm(Hs.K1, pg), dm(Hs.K2, pb_));
-          const double vv = v * v;
-#pragma unroll
-          for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
-          acc_pred<GMAX>(sm[0], sq[0], sector, v, vv);
-        } else {
-          const double v0 = dm(Hs.K0, pr), v1 = dm(Hs.K1, pg), v2 = dm(Hs.K2, pb_);
-          const double w0 = v0 * v0, w1 = v1 * v1, w2 = v2 * v2;
-#pragma unroll
-          for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
-          acc_pred<GMAX>(sm[0], sq[0], sector, v0, w0);
-          acc_pred<GMAX>(sm[1], sq[1], sector, v1, w1);
-          acc_pred<GMAX>(sm[2], sq[2], sector, v2, w2);
-        }
+        pair_accumulate<GMAX, CH>(A, F, Hs, i, eye, cnt, sm, sq, p0, p1, p2, my_acc, my_exact, my_amb);
       }
     }
 
@@ -191,6 +210,113 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
     atomicAdd(A.iter_tr + 1, s_tr[1]);
     atomicMax(A.rmax_bits, s_rmax);
   }
+}
+
+// ---------------------------------------------------------------- sparse frames
+// Thread per hit point, for 3D frames with a few hit points per cell (C3's
+// camera hit points on the walls, C5): the per-hit-point fixed cost of the
+// warp kernel (a 5-level warp reduction of 3 G accumulators and a
+// single-lane end-of-iteration) exceeds its ~100 candidates, so here each
+// thread walks its own 9 columns of the 27-cell neighbourhood with the same
+// pair code and runs finalize_hit itself.  Neighbouring threads hold nearby
+// hit points (pixel order), so their photon records share L1/L2 lines.
+template <int GMAX, int CH>
+__global__ void __launch_bounds__(128) k_gather_sparse(const GatherArgs A) {
+  __shared__ Hit s_hit[128];
+  Hit &Hs = s_hit[threadIdx.x];
+  const GridHeader grid = *A.grid;
+  uint32_t my_cand = 0, my_exact = 0, my_amb = 0, my_acc = 0;
+  double my_rmax = 0.0;
+  uint32_t my_tested = 0, my_rejected = 0;
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < A.H; h += gridDim.x * blockDim.x) {
+    make_hit(A, h, Hs);
+    const HitF F = hitf(Hs, A.na, A.ns);
+    const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
+    uint32_t cnt[GMAX];
+    double sm[CH][GMAX], sq[CH][GMAX];
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      cnt[g] = 0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) { sm[c][g] = 0.0; sq[c][g] = 0.0; }
+    }
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    EyeVcm eye{0.0, 0.0, 0.0, 0.0};
+    if (A.vcm) {
+      const double3 wo = A.wo[h], al = A.alb[h];
+      eye.cos_o = edot(wo.x, wo.y, wo.z, Hs.nx, Hs.ny, Hs.nz);
+      const double m1 = al.y < al.z ? al.z : al.y;
+      const double amax = al.x < m1 ? m1 : al.x;
+      eye.cont = amax < 1.0 ? amax : 1.0;
+      const double2 em = A.eye_mis[h];
+      eye.d_vcm = em.x;
+      eye.d_vm = em.y;
+    }
+    if (gathered && grid.n > 0) {
+      const long long ix = (long long)floor(dm(Hs.cx, grid.inv)) - grid.ix0;
+      const long long iy = (long long)floor(dm(Hs.cy, grid.inv)) - grid.iy0;
+      const long long iz = (long long)floor(dm(Hs.cz, grid.inv)) - grid.iz0;
+      const long long z0 = iz - 1 < 0 ? 0 : iz - 1;
+      const long long z1 = iz + 1 >= grid.nz ? grid.nz - 1 : iz + 1;
+      for (int col = 0; col < 9; ++col) {
+        const long long X = ix + col / 3 - 1, Y = iy + col % 3 - 1;
+        if (X < 0 || X >= grid.nx || Y < 0 || Y >= grid.ny || z0 > z1) continue;
+        const unsigned long long k0 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z0);
+        const unsigned long long k1 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z1);
+        const uint32_t beg = __ldg(&A.cell_start[k0]), end = __ldg(&A.cell_start[k1 + 1]);
+        my_cand += end - beg;
+        for (uint32_t i = beg; i < end; ++i)
+          pair_accumulate<GMAX, CH>(A, F, Hs, i, eye, cnt, sm, sq, p0, p1, p2, my_acc, my_exact, my_amb);
+      }
+    }
+    finalize_hit<GMAX, CH>(A, h, cnt, sm, sq, p0, p1, p2, my_tested, my_rejected, my_rmax);
+  }
+  // counters: warp reduce, then one atomic per warp
+  unsigned long long c4[4] = {my_acc, my_cand, my_exact, my_amb};
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c4[k] += __shfl_xor_sync(~0u, c4[k], o);
+    my_tested += __shfl_xor_sync(~0u, my_tested, o);
+    my_rejected += __shfl_xor_sync(~0u, my_rejected, o);
+    my_rmax = fmax(my_rmax, __shfl_xor_sync(~0u, my_rmax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) atomicAdd(&A.counters[k], c4[k]);
+    atomicAdd(A.iter_tr, my_tested);
+    atomicAdd(A.iter_tr + 1, my_rejected);
+    atomicMax(A.rmax_bits, (unsigned long long)__double_as_longlong(my_rmax));
+  }
+}
+
+template <int GMAX, int CH>
+static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, int sms) {
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_sparse<GMAX, CH>, 128, 0);
+  if (e != cudaSuccess) return e;
+  unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1) * 4u;
+  const unsigned need = (A.H + 127) / 128;
+  if (blocks > need) blocks = need;
+  if (blocks == 0) blocks = 1;
+  k_gather_sparse<GMAX, CH><<<blocks, 128, 0, s>>>(A);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, int sms) {
+  const int G = A.na * A.ns;
+  if (C == 1) {
+    if (G <= 4) return launch_sparse_one<4, 1>(s, A, sms);
+    if (G <= 8) return launch_sparse_one<8, 1>(s, A, sms);
+    if (G <= 12) return launch_sparse_one<12, 1>(s, A, sms);
+    if (G <= 16) return launch_sparse_one<16, 1>(s, A, sms);
+    return launch_sparse_one<32, 1>(s, A, sms);
+  }
+  if (G <= 4) return launch_sparse_one<4, 3>(s, A, sms);
+  if (G <= 8) return launch_sparse_one<8, 3>(s, A, sms);
+  if (G <= 12) return launch_sparse_one<12, 3>(s, A, sms);
+  return launch_sparse_one<32, 3>(s, A, sms);
 }
 
 // ---------------------------------------------------------------- explicit samples

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("kernel", ["fine", "warp"])
+@pytest.mark.parametrize("kernel", ["fine", "warp", "sparse"])
 def test_photon_sharded_matches_oracle(port, world, kernel):
     wl = WORKLOADS["c2"].scaled(raster=48, photons=1 << 16)
     H = wl.hitpoints
