@@ -57,6 +57,8 @@ struct fppm_gpu_ctx {
   fppm_b200::TraceScene scene{};
   void *scene_mem[9] = {};  // [8]: per-primitive constants (k_scene_prep)
   uint32_t *t_ctr = nullptr;
+  double *d_rows = nullptr;  // sparse gather: per-hit-point sums before the end of iteration
+  size_t rows_cap = 0;
   bool has_scene = false;
   float *t_pos = nullptr, *t_nrm = nullptr, *t_wi = nullptr, *t_pow = nullptr;
   uint32_t *t_depth = nullptr, *t_count = nullptr, *t_base = nullptr, *t_scan = nullptr;
@@ -397,7 +399,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->d_ppow, Nc * 3)); A(dalloc(&ctx->d_pdepth, Nc));
   A(dalloc(&ctx->recs.rec0, Nc)); A(dalloc(&ctx->recs.rec1, Nc));
   A(dalloc(&ctx->recs.rec2, Nc)); A(dalloc(&ctx->recs.rec3, Nc));
-  if (gather_variant(ctx) == 4) A(dalloc(&ctx->recs.pack, 4 * Nc));
+  A(dalloc(&ctx->recs.pack, 4 * Nc));  // records packed in input order, then permuted whole
   A(dalloc(&ctx->sort.keys_a, Nc)); A(dalloc(&ctx->sort.vals_a, Nc));
   A(dalloc(&ctx->sort.keys_b, Nc)); A(dalloc(&ctx->sort.vals_b, Nc));
   A(dalloc(&ctx->sort.hist, radix_hist_entries((uint32_t)Nc)));
@@ -480,6 +482,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
   if (ctx->d_eye_mis) cudaFree(ctx->d_eye_mis);
   if (ctx->d_emit) cudaFree(ctx->d_emit);
+  if (ctx->d_rows) cudaFree(ctx->d_rows);
   if (ctx->d_film) cudaFree(ctx->d_film);
   for (void *p : ctx->scene_mem)
     if (p) cudaFree(p);
@@ -1082,11 +1085,30 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
   const int var = effective_variant(ctx, ctx->h_hdr->S);
   if (ctx->H && (var == 1 || var == 5)) {
     if ((rc = kernel_event(ctx, 0))) return rc;
-    if (var == 1)
+    if (var == 1) {
       FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
-    else
-      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, ctx->sms));
-    if ((rc = kernel_event(ctx, 1))) return rc;
+      if ((rc = kernel_event(ctx, 1))) return rc;
+    } else {
+      double *rows = delta;
+      if (!rows) {
+        const size_t need = (size_t)ctx->H * fppm_gpu_delta_stride(ctx);
+        if (need > ctx->rows_cap) {
+          if (ctx->d_rows) cudaFree(ctx->d_rows);
+          ctx->d_rows = nullptr;
+          ctx->rows_cap = 0;
+          FPPM_CUDA_OK(dalloc(&ctx->d_rows, need));
+          ctx->rows_cap = need;
+        }
+        rows = ctx->d_rows;
+      }
+      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, rows, ctx->sms));
+      if ((rc = kernel_event(ctx, 1))) return rc;
+      if (!delta) {
+        GatherArgs B = A;
+        B.delta_out = nullptr;
+        FPPM_CUDA_OK(launch_apply_deltas(s, B, ctx->C, 0, ctx->H, rows));
+      }
+    }
   } else if (ctx->H) {
     // ---- tiled path: bin hit points by home cell, build items, run
     TileSched &S = ctx->tile;

@@ -23,66 +23,71 @@ struct EyeVcm {
   double cos_o, cont, d_vcm, d_vm;
 };
 
+// Evaluates one candidate: false when the reference rejects it; otherwise the
+// sector, the statistic values (luminance, or RGB for CH = 3) with their
+// squares, and the flux addends (photon power for FPPM, the weighted value
+// for VCM+).
+template <int CH>
+static __device__ __forceinline__ bool pair_eval(const GatherArgs &A, const HitF &F, const Hit &Hs, uint32_t i,
+                                                 const EyeVcm &E, int &sector, double (&sv)[CH],
+                                                 double (&sw)[CH], double &f0, double &f1, double &f2,
+                                                 uint32_t &my_exact, uint32_t &my_amb) {
+  const float4 a = __ldg(&A.rec0[i]);
+  if (!test_pair(F, a, A.max_depth)) return false;
+  const float4 b = __ldg(&A.rec1[i]);
+  const float4 c2 = __ldg(&A.rec2[i]);
+  bool cos_pos;
+  if (!flush_pair(F, Hs, a, b, c2, A.guard, sector, cos_pos, my_exact, my_amb)) return false;
+  const float4 c3 = __ldg(&A.rec3[i]);
+  double v0, v1, v2;
+  if (A.vcm) {
+    // merge callback (integrator.cpp:609-616): f and the pdfs of
+    // Bsdf::eval (bsdf.cpp:53-63), merge weight, val = thr * f * p.thr * w
+    const double ci = edot((double)b.w, (double)c2.x, (double)c2.y, Hs.nx, Hs.ny, Hs.nz);
+    const bool black = E.cos_o <= 0.0 || ci <= 0.0;
+    const double pf = black ? 0.0 : (ci > 0.0 ? dm(ci, kInvPi) : 0.0);
+    const double prv = black ? 0.0 : (E.cos_o > 0.0 ? dm(E.cos_o, kInvPi) : 0.0);
+    const double w = mis_weight_merge_dev(A.mis_n_vm, A.mis_beta, Hs.r, E.d_vcm, E.d_vm, A.p_vcm[i],
+                                          A.p_vm[i], dm(pf, E.cont), dm(prv, A.p_cont[i]));
+    const double k0 = ci <= 0.0 ? dm(Hs.K0, 0.0) : Hs.K0, k1 = ci <= 0.0 ? dm(Hs.K1, 0.0) : Hs.K1,
+                 k2 = ci <= 0.0 ? dm(Hs.K2, 0.0) : Hs.K2;
+    v0 = dm(dm(k0, (double)c2.z), w);
+    v1 = dm(dm(k1, (double)c2.w), w);
+    v2 = dm(dm(k2, (double)c3.x), w);
+    f0 = v0; f1 = v1; f2 = v2;
+  } else {
+    const double pr = cos_pos ? (double)c2.z : 0.0, pg = cos_pos ? (double)c2.w : 0.0,
+                 pb_ = cos_pos ? (double)c3.x : 0.0;
+    f0 = pr; f1 = pg; f2 = pb_;
+    v0 = dm(Hs.K0, pr);
+    v1 = dm(Hs.K1, pg);
+    v2 = dm(Hs.K2, pb_);
+  }
+  if constexpr (CH == 1) {
+    sv[0] = elum(v0, v1, v2);
+    sw[0] = dm(sv[0], sv[0]);
+  } else {
+    sv[0] = v0; sv[1] = v1; sv[2] = v2;
+    sw[0] = dm(v0, v0); sw[1] = dm(v1, v1); sw[2] = dm(v2, v2);
+  }
+  return true;
+}
+
 template <int GMAX, int CH>
 static __device__ __forceinline__ void pair_accumulate(const GatherArgs &A, const HitF &F, const Hit &Hs,
                                                        uint32_t i, const EyeVcm &E, uint32_t (&cnt)[GMAX],
                                                        double (&sm)[CH][GMAX], double (&sq)[CH][GMAX],
                                                        double &p0, double &p1, double &p2, uint32_t &my_acc,
                                                        uint32_t &my_exact, uint32_t &my_amb) {
-  const double v_cos_o = E.cos_o, v_cont = E.cont, v_vcm = E.d_vcm, v_vm = E.d_vm;
-  const float4 a = __ldg(&A.rec0[i]);
-  if (!test_pair(F, a, A.max_depth)) return;
-  const float4 b = __ldg(&A.rec1[i]);
-  const float4 c2 = __ldg(&A.rec2[i]);
   int sector;
-  bool cos_pos;
-  if (!flush_pair(F, Hs, a, b, c2, A.guard, sector, cos_pos, my_exact, my_amb)) return;
+  double sv[CH], sw[CH], f0, f1, f2;
+  if (!pair_eval<CH>(A, F, Hs, i, E, sector, sv, sw, f0, f1, f2, my_exact, my_amb)) return;
   ++my_acc;
-  const float4 c3 = __ldg(&A.rec3[i]);
-  if (A.vcm) {
-    // merge callback (integrator.cpp:609-616): f and the pdfs of
-    // Bsdf::eval (bsdf.cpp:53-63), merge weight, val = thr * f * p.thr * w
-    const double ci = edot((double)b.w, (double)c2.x, (double)c2.y, Hs.nx, Hs.ny, Hs.nz);
-    const bool black = v_cos_o <= 0.0 || ci <= 0.0;
-    const double pf = black ? 0.0 : (ci > 0.0 ? dm(ci, kInvPi) : 0.0);
-    const double prv = black ? 0.0 : (v_cos_o > 0.0 ? dm(v_cos_o, kInvPi) : 0.0);
-    const double w = mis_weight_merge_dev(A.mis_n_vm, A.mis_beta, Hs.r, v_vcm, v_vm, A.p_vcm[i],
-                                          A.p_vm[i], dm(pf, v_cont), dm(prv, A.p_cont[i]));
-    const double k0 = ci <= 0.0 ? dm(Hs.K0, 0.0) : Hs.K0, k1 = ci <= 0.0 ? dm(Hs.K1, 0.0) : Hs.K1,
-                 k2 = ci <= 0.0 ? dm(Hs.K2, 0.0) : Hs.K2;
-    const double v0 = dm(dm(k0, (double)c2.z), w), v1 = dm(dm(k1, (double)c2.w), w),
-                 v2 = dm(dm(k2, (double)c3.x), w);
-    p0 += v0; p1 += v1; p2 += v2;
+  p0 = da(p0, f0); p1 = da(p1, f1); p2 = da(p2, f2);
 #pragma unroll
-    for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
-    if constexpr (CH == 1) {
-      const double v = elum(v0, v1, v2);
-      acc_pred<GMAX>(sm[0], sq[0], sector, v, v * v);
-    } else {
-      acc_pred<GMAX>(sm[0], sq[0], sector, v0, v0 * v0);
-      acc_pred<GMAX>(sm[1], sq[1], sector, v1, v1 * v1);
-      acc_pred<GMAX>(sm[2], sq[2], sector, v2, v2 * v2);
-    }
-    return;
-  }
-  const double pr = cos_pos ? (double)c2.z : 0.0, pg = cos_pos ? (double)c2.w : 0.0,
-               pb_ = cos_pos ? (double)c3.x : 0.0;
-  p0 += pr; p1 += pg; p2 += pb_;
-  if constexpr (CH == 1) {
-    const double v = elum(dm(Hs.K0, pr), dm(Hs.K1, pg), dm(Hs.K2, pb_));
-    const double vv = v * v;
+  for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
 #pragma unroll
-    for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
-    acc_pred<GMAX>(sm[0], sq[0], sector, v, vv);
-  } else {
-    const double v0 = dm(Hs.K0, pr), v1 = dm(Hs.K1, pg), v2 = dm(Hs.K2, pb_);
-    const double w0 = v0 * v0, w1 = v1 * v1, w2 = v2 * v2;
-#pragma unroll
-    for (int g = 0; g < GMAX; ++g) cnt[g] += sector == g ? 1u : 0u;
-    acc_pred<GMAX>(sm[0], sq[0], sector, v0, w0);
-    acc_pred<GMAX>(sm[1], sq[1], sector, v1, w1);
-    acc_pred<GMAX>(sm[2], sq[2], sector, v2, w2);
-  }
+  for (int c = 0; c < CH; ++c) acc_pred<GMAX>(sm[c], sq[c], sector, sv[c], sw[c]);
 }
 
 template <int GMAX, int CH>
@@ -220,26 +225,31 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
 // thread walks its own 9 columns of the 27-cell neighbourhood with the same
 // pair code and runs finalize_hit itself.  Neighbouring threads hold nearby
 // hit points (pixel order), so their photon records share L1/L2 lines.
+constexpr int kSparseThreads = 128;
+
 template <int GMAX, int CH>
-__global__ void __launch_bounds__(128) k_gather_sparse(const GatherArgs A) {
-  __shared__ Hit s_hit[128];
-  Hit &Hs = s_hit[threadIdx.x];
+__global__ void __launch_bounds__(kSparseThreads) k_gather_sparse(const GatherArgs A, double *__restrict__ rows) {
+  // per thread: its Hit (exact path) and its sector accumulators, indexed
+  // [slot][thread] so a lane's dynamic sector index costs one LDS/STS
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int G = A.na * A.ns, CG = G * CH;
+  const int t = threadIdx.x;
+  Hit *s_hit = reinterpret_cast<Hit *>(s_raw);
+  double *s_sum = reinterpret_cast<double *>(s_hit + kSparseThreads);   // [CG][T]
+  double *s_sq = s_sum + (size_t)CG * kSparseThreads;                     // [CG][T]
+  uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_sq + (size_t)CG * kSparseThreads);  // [G][T]
+  Hit &Hs = s_hit[t];
   const GridHeader grid = *A.grid;
   uint32_t my_cand = 0, my_exact = 0, my_amb = 0, my_acc = 0;
-  double my_rmax = 0.0;
-  uint32_t my_tested = 0, my_rejected = 0;
-  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < A.H; h += gridDim.x * blockDim.x) {
+  for (uint32_t h = blockIdx.x * blockDim.x + t; h < A.H; h += gridDim.x * blockDim.x) {
     make_hit(A, h, Hs);
     const HitF F = hitf(Hs, A.na, A.ns);
     const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
-    uint32_t cnt[GMAX];
-    double sm[CH][GMAX], sq[CH][GMAX];
-#pragma unroll
-    for (int g = 0; g < GMAX; ++g) {
-      cnt[g] = 0;
-#pragma unroll
-      for (int c = 0; c < CH; ++c) { sm[c][g] = 0.0; sq[c][g] = 0.0; }
+    for (int k = 0; k < CG; ++k) {
+      s_sum[k * kSparseThreads + t] = 0.0;
+      s_sq[k * kSparseThreads + t] = 0.0;
     }
+    for (int g = 0; g < G; ++g) s_cnt[g * kSparseThreads + t] = 0u;
     double p0 = 0.0, p1 = 0.0, p2 = 0.0;
     EyeVcm eye{0.0, 0.0, 0.0, 0.0};
     if (A.vcm) {
@@ -258,65 +268,94 @@ __global__ void __launch_bounds__(128) k_gather_sparse(const GatherArgs A) {
       const long long iz = (long long)floor(dm(Hs.cz, grid.inv)) - grid.iz0;
       const long long z0 = iz - 1 < 0 ? 0 : iz - 1;
       const long long z1 = iz + 1 >= grid.nz ? grid.nz - 1 : iz + 1;
+      // the 9 (x, y) columns as one candidate sequence, so a lane's trip
+      // count is its total, not the sum of per-column maxima over the warp
+      uint32_t cb[9], ce[9];
+      uint32_t total = 0;
+#pragma unroll
       for (int col = 0; col < 9; ++col) {
         const long long X = ix + col / 3 - 1, Y = iy + col % 3 - 1;
-        if (X < 0 || X >= grid.nx || Y < 0 || Y >= grid.ny || z0 > z1) continue;
-        const unsigned long long k0 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z0);
-        const unsigned long long k1 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z1);
-        const uint32_t beg = __ldg(&A.cell_start[k0]), end = __ldg(&A.cell_start[k1 + 1]);
-        my_cand += end - beg;
-        for (uint32_t i = beg; i < end; ++i)
-          pair_accumulate<GMAX, CH>(A, F, Hs, i, eye, cnt, sm, sq, p0, p1, p2, my_acc, my_exact, my_amb);
+        cb[col] = ce[col] = 0;
+        if (X >= 0 && X < grid.nx && Y >= 0 && Y < grid.ny && z0 <= z1) {
+          const unsigned long long k0 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z0);
+          const unsigned long long k1 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z1);
+          cb[col] = __ldg(&A.cell_start[k0]);
+          ce[col] = __ldg(&A.cell_start[k1 + 1]);
+        }
+        total += ce[col] - cb[col];
+      }
+      my_cand += total;
+      int col = 0;
+      uint32_t i = cb[0];
+      for (uint32_t n = 0; n < total; ++n, ++i) {
+        while (i >= ce[col]) {
+          ++col;
+          i = cb[col];
+        }
+        int sector;
+        double sv[CH], sw[CH], f0, f1, f2;
+        if (!pair_eval<CH>(A, F, Hs, i, eye, sector, sv, sw, f0, f1, f2, my_exact, my_amb)) continue;
+        ++my_acc;
+        p0 = da(p0, f0); p1 = da(p1, f1); p2 = da(p2, f2);
+        s_cnt[sector * kSparseThreads + t] += 1u;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          double &x = s_sum[(c * G + sector) * kSparseThreads + t];
+          double &y = s_sq[(c * G + sector) * kSparseThreads + t];
+          x = da(x, sv[c]);
+          y = da(y, sw[c]);
+        }
       }
     }
-    finalize_hit<GMAX, CH>(A, h, cnt, sm, sq, p0, p1, p2, my_tested, my_rejected, my_rmax);
+    // option-B row layout [count G | sum C*G | sum_sq C*G | power 3]; the
+    // end of iteration runs in k_apply_deltas (thread per hit point)
+    double *d = rows + (size_t)h * (size_t)(G + 2 * CG + 3);
+    for (int g = 0; g < G; ++g) d[g] = (double)s_cnt[g * kSparseThreads + t];
+    for (int k = 0; k < CG; ++k) {
+      d[G + k] = s_sum[k * kSparseThreads + t];
+      d[G + CG + k] = s_sq[k * kSparseThreads + t];
+    }
+    d[G + 2 * CG] = p0;
+    d[G + 2 * CG + 1] = p1;
+    d[G + 2 * CG + 2] = p2;
   }
-  // counters: warp reduce, then one atomic per warp
   unsigned long long c4[4] = {my_acc, my_cand, my_exact, my_amb};
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
+  for (int o = 16; o; o >>= 1)
 #pragma unroll
     for (int k = 0; k < 4; ++k) c4[k] += __shfl_xor_sync(~0u, c4[k], o);
-    my_tested += __shfl_xor_sync(~0u, my_tested, o);
-    my_rejected += __shfl_xor_sync(~0u, my_rejected, o);
-    my_rmax = fmax(my_rmax, __shfl_xor_sync(~0u, my_rmax, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
+  if ((t & 31) == 0)
 #pragma unroll
     for (int k = 0; k < 4; ++k) atomicAdd(&A.counters[k], c4[k]);
-    atomicAdd(A.iter_tr, my_tested);
-    atomicAdd(A.iter_tr + 1, my_rejected);
-    atomicMax(A.rmax_bits, (unsigned long long)__double_as_longlong(my_rmax));
-  }
+}
+
+size_t sparse_smem_bytes(int G, int C) {
+  return sizeof(Hit) * kSparseThreads + (size_t)kSparseThreads * (16 * (size_t)G * C + 4 * (size_t)G);
 }
 
 template <int GMAX, int CH>
-static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, int sms) {
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_sparse<GMAX, CH>, 128, 0);
+static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, double *rows, int sms) {
+  const int G = A.na * A.ns;
+  const size_t smem = sparse_smem_bytes(G, CH);
+  cudaError_t e = cudaFuncSetAttribute(k_gather_sparse<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
-  unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1) * 4u;
-  const unsigned need = (A.H + 127) / 128;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_sparse<GMAX, CH>, kSparseThreads, smem);
+  if (e != cudaSuccess) return e;
+  unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1) * 8u;
+  const unsigned need = (A.H + kSparseThreads - 1) / kSparseThreads;
   if (blocks > need) blocks = need;
   if (blocks == 0) blocks = 1;
-  k_gather_sparse<GMAX, CH><<<blocks, 128, 0, s>>>(A);
+  k_gather_sparse<GMAX, CH><<<blocks, kSparseThreads, smem, s>>>(A, rows);
   note_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, int sms) {
-  const int G = A.na * A.ns;
-  if (C == 1) {
-    if (G <= 4) return launch_sparse_one<4, 1>(s, A, sms);
-    if (G <= 8) return launch_sparse_one<8, 1>(s, A, sms);
-    if (G <= 12) return launch_sparse_one<12, 1>(s, A, sms);
-    if (G <= 16) return launch_sparse_one<16, 1>(s, A, sms);
-    return launch_sparse_one<32, 1>(s, A, sms);
-  }
-  if (G <= 4) return launch_sparse_one<4, 3>(s, A, sms);
-  if (G <= 8) return launch_sparse_one<8, 3>(s, A, sms);
-  if (G <= 12) return launch_sparse_one<12, 3>(s, A, sms);
-  return launch_sparse_one<32, 3>(s, A, sms);
+cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, double *rows, int sms) {
+  // GMAX only sizes the apply kernel's registers here; one instance per C
+  if (C == 1) return launch_sparse_one<32, 1>(s, A, rows, sms);
+  return launch_sparse_one<32, 3>(s, A, rows, sms);
 }
 
 // ---------------------------------------------------------------- explicit samples

@@ -196,7 +196,10 @@ cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2
                            unsigned long long *st_cnt, double *st_sum, double *st_sq, int phase);
 cudaError_t launch_end_iteration(cudaStream_t s, const EndArgs &A);
 // thread-per-hit-point gather for sparse 3D frames (gather.cu)
-cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, int sms);
+// writes option-B rows [H][G + 2 G C + 3]; the caller pools them
+// (launch_apply_deltas) unless they are the cross-rank partial sums
+cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, double *rows, int sms);
+size_t sparse_smem_bytes(int G, int C);
 // pools summed option-B rows into regions [h0, h0 + n) and runs the
 // end-of-iteration policy (finalize_hit)
 cudaError_t launch_apply_deltas(cudaStream_t s, const GatherArgs &A, int C, uint32_t h0, uint32_t n,

@@ -339,6 +339,42 @@ __global__ void k_cell_start_bsearch(const uint32_t *__restrict__ skeys, uint32_
   }
 }
 
+// Sparse tables, warp-cooperative: a warp owns 256 consecutive cells, finds
+// the window of sorted keys that falls in them with two binary searches, and
+// each lane resolves its cells inside that (small, cached) window; the table
+// writes are coalesced and no thread walks a long empty stretch.
+__global__ void __launch_bounds__(256) k_cell_start_chunked(const uint32_t *__restrict__ skeys, uint32_t n,
+                                                            unsigned long long ncells,
+                                                            uint32_t *__restrict__ start) {
+  constexpr unsigned long long kCells = 256;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  for (unsigned long long w = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+       w * kCells <= ncells; w += nwarps) {
+    const unsigned long long c0 = w * kCells;
+    const unsigned long long c1 = c0 + kCells < ncells + 1 ? c0 + kCells : ncells + 1;
+    uint32_t p = 0;
+    if (lane < 2) {
+      const unsigned long long c = lane == 0 ? c0 : c1;
+      uint32_t lo = 0, hi = n;
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if ((unsigned long long)skeys[mid] < c) lo = mid + 1; else hi = mid;
+      }
+      p = lo;
+    }
+    const uint32_t p0 = __shfl_sync(~0u, p, 0), p1 = __shfl_sync(~0u, p, 1);
+    for (unsigned long long c = c0 + lane; c < c1; c += 32) {
+      uint32_t lo = p0, hi = p1;
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if ((unsigned long long)skeys[mid] < c) lo = mid + 1; else hi = mid;
+      }
+      start[c] = lo;
+    }
+  }
+}
+
 __global__ void k_cell_start_empty(uint32_t *__restrict__ start, unsigned long long ncells) {
   for (unsigned long long c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncells;
        c += gridDim.x * blockDim.x)
@@ -363,6 +399,24 @@ __global__ void __launch_bounds__(256)
     const unsigned long long Lb = (unsigned long long)__double_as_longlong(L);
     rec3[i] = make_float4(pw[o + 2], 0.f, __uint_as_float((uint32_t)Lb),
                           __uint_as_float((uint32_t)(Lb >> 32)));
+  }
+}
+
+// warp / sparse kernel layout, packed in input order (coalesced) so the
+// permute moves whole 64-B records
+__global__ void __launch_bounds__(256)
+    k_pack_std(const float *__restrict__ pos, const float *__restrict__ nrm, const float *__restrict__ wi,
+               const float *__restrict__ pw, const uint32_t *__restrict__ depth, uint32_t n,
+               float4 *__restrict__ pack) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const size_t o = 3 * (size_t)j;
+    float4 *d = pack + 4 * (size_t)j;
+    d[0] = make_float4(pos[o], pos[o + 1], pos[o + 2], __uint_as_float(depth[j]));
+    d[1] = make_float4(nrm[o], nrm[o + 1], nrm[o + 2], wi[o]);
+    d[2] = make_float4(wi[o + 1], wi[o + 2], pw[o], pw[o + 1]);
+    const double L = elum((double)pw[o], (double)pw[o + 1], (double)pw[o + 2]);
+    const unsigned long long Lb = (unsigned long long)__double_as_longlong(L);
+    d[3] = make_float4(pw[o + 2], 0.f, __uint_as_float((uint32_t)Lb), __uint_as_float((uint32_t)(Lb >> 32)));
   }
 }
 
@@ -525,7 +579,8 @@ void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const 
   if (n == 0) {
     k_cell_start_empty<<<1, 32, 0, s>>>(start, ncells);
   } else if (ncells > 4ull * n) {
-    k_cell_start_bsearch<<<cap_blocks(ncells + 1, 256, sms, 16), 256, 0, s>>>(skeys, n, ncells, start);
+    k_cell_start_chunked<<<cap_blocks((ncells + 1 + 255) / 256 * 32, 256, sms, 16), 256, 0, s>>>(skeys, n, ncells,
+                                                                                              start);
   } else {
     k_cell_start<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(skeys, n, hdr, start);
   }
@@ -542,7 +597,12 @@ void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const flo
   else if (fine_layout)
     k_permute_fine<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
                                                                 r.rec0, r.rec1, r.rec2, r.rec3);
-  else
+  else if (r.pack) {
+    k_pack_std<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(pos, nrm, wi, pw, depth, n, r.pack);
+    note_launches(1);
+    k_permute_packed<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, r.pack, r.rec0, r.rec1, r.rec2,
+                                                                  r.rec3);
+  } else
     k_permute<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
                                                            r.rec0, r.rec1, r.rec2, r.rec3);
   note_launches(1);
