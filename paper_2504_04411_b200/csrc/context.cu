@@ -1084,8 +1084,8 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
   // kernel on 3D grids (S = 1: a few hit points per cell)
   const int var = effective_variant(ctx, ctx->h_hdr->S);
   if (ctx->H && (var == 1 || var == 5)) {
-    if ((rc = kernel_event(ctx, 0))) return rc;
     if (var == 1) {
+      if ((rc = kernel_event(ctx, 0))) return rc;
       FPPM_CUDA_OK(launch_gather_test(s, A, ctx->C, ctx->sms));
       if ((rc = kernel_event(ctx, 1))) return rc;
     } else {
@@ -1101,7 +1101,10 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
         }
         rows = ctx->d_rows;
       }
-      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, rows, ctx->sms));
+      const uint32_t *order = nullptr;
+      FPPM_CUDA_OK(hp_cell_order(s, A, ctx->tile, *ctx->h_hdr, ctx->sms, &order));
+      if ((rc = kernel_event(ctx, 0))) return rc;
+      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, order, rows, ctx->sms));
       if ((rc = kernel_event(ctx, 1))) return rc;
       if (!delta) {
         GatherArgs B = A;

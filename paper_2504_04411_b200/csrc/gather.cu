@@ -27,6 +27,12 @@ struct EyeVcm {
 // sector, the statistic values (luminance, or RGB for CH = 3) with their
 // squares, and the flux addends (photon power for FPPM, the weighted value
 // for VCM+).
+template <int CH, class HT>
+static __device__ __forceinline__ bool pair_tail(const GatherArgs &A, const HitF &F, const HT &Hs, uint32_t i,
+                                                 const EyeVcm &E, float4 a, float4 b, float4 c2, float4 c3,
+                                                 int &sector, double (&sv)[CH], double (&sw)[CH], double &f0,
+                                                 double &f1, double &f2, uint32_t &my_exact, uint32_t &my_amb);
+
 template <int CH>
 static __device__ __forceinline__ bool pair_eval(const GatherArgs &A, const HitF &F, const Hit &Hs, uint32_t i,
                                                  const EyeVcm &E, int &sector, double (&sv)[CH],
@@ -36,9 +42,18 @@ static __device__ __forceinline__ bool pair_eval(const GatherArgs &A, const HitF
   if (!test_pair(F, a, A.max_depth)) return false;
   const float4 b = __ldg(&A.rec1[i]);
   const float4 c2 = __ldg(&A.rec2[i]);
+  const float4 c3 = __ldg(&A.rec3[i]);
+  return pair_tail<CH, Hit>(A, F, Hs, i, E, a, b, c2, c3, sector, sv, sw, f0, f1, f2, my_exact, my_amb);
+}
+
+// flush_pair + value of a candidate whose records are loaded
+template <int CH, class HT>
+static __device__ __forceinline__ bool pair_tail(const GatherArgs &A, const HitF &F, const HT &Hs, uint32_t i,
+                                                 const EyeVcm &E, float4 a, float4 b, float4 c2, float4 c3,
+                                                 int &sector, double (&sv)[CH], double (&sw)[CH], double &f0,
+                                                 double &f1, double &f2, uint32_t &my_exact, uint32_t &my_amb) {
   bool cos_pos;
   if (!flush_pair(F, Hs, a, b, c2, A.guard, sector, cos_pos, my_exact, my_amb)) return false;
-  const float4 c3 = __ldg(&A.rec3[i]);
   double v0, v1, v2;
   if (A.vcm) {
     // merge callback (integrator.cpp:609-616): f and the pdfs of
@@ -226,24 +241,42 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
 // pair code and runs finalize_hit itself.  Neighbouring threads hold nearby
 // hit points (pixel order), so their photon records share L1/L2 lines.
 constexpr int kSparseThreads = 128;
+#ifndef FPPM_SPARSE_U
+#define FPPM_SPARSE_U 4
+#endif
+constexpr int kSparseU = FPPM_SPARSE_U;
 
 template <int GMAX, int CH>
-__global__ void __launch_bounds__(kSparseThreads) k_gather_sparse(const GatherArgs A, double *__restrict__ rows) {
+#ifndef FPPM_SPARSE_MINB
+#define FPPM_SPARSE_MINB 4
+#endif
+__global__ void __launch_bounds__(kSparseThreads, FPPM_SPARSE_MINB) k_gather_sparse(const GatherArgs A, const uint32_t *__restrict__ order,
+                                                                   double *__restrict__ rows) {
   // per thread: its Hit (exact path) and its sector accumulators, indexed
   // [slot][thread] so a lane's dynamic sector index costs one LDS/STS
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int G = A.na * A.ns, CG = G * CH;
   const int t = threadIdx.x;
-  Hit *s_hit = reinterpret_cast<Hit *>(s_raw);
+  HitX *s_hit = reinterpret_cast<HitX *>(s_raw);
   double *s_sum = reinterpret_cast<double *>(s_hit + kSparseThreads);   // [CG][T]
   double *s_sq = s_sum + (size_t)CG * kSparseThreads;                     // [CG][T]
   uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_sq + (size_t)CG * kSparseThreads);  // [G][T]
-  Hit &Hs = s_hit[t];
+  HitX &Hs = s_hit[t];
   const GridHeader grid = *A.grid;
   uint32_t my_cand = 0, my_exact = 0, my_amb = 0, my_acc = 0;
-  for (uint32_t h = blockIdx.x * blockDim.x + t; h < A.H; h += gridDim.x * blockDim.x) {
-    make_hit(A, h, Hs);
-    const HitF F = hitf(Hs, A.na, A.ns);
+  for (uint32_t q = blockIdx.x * blockDim.x + t; q < A.H; q += gridDim.x * blockDim.x) {
+    const uint32_t h = order ? order[q] : q;
+    HitF F;
+    {
+      Hit H;
+      make_hit(A, h, H);
+      F = hitf(H, A.na, A.ns);
+      Hs.cx = H.cx; Hs.cy = H.cy; Hs.cz = H.cz;
+      Hs.nx = H.nx; Hs.ny = H.ny; Hs.nz = H.nz;
+      Hs.u = H.u; Hs.v = H.v;
+      Hs.r = H.r; Hs.r2 = H.r2;
+      Hs.K0 = H.K0; Hs.K1 = H.K1; Hs.K2 = H.K2;
+    }
     const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
     for (int k = 0; k < CG; ++k) {
       s_sum[k * kSparseThreads + t] = 0.0;
@@ -268,42 +301,53 @@ __global__ void __launch_bounds__(kSparseThreads) k_gather_sparse(const GatherAr
       const long long iz = (long long)floor(dm(Hs.cz, grid.inv)) - grid.iz0;
       const long long z0 = iz - 1 < 0 ? 0 : iz - 1;
       const long long z1 = iz + 1 >= grid.nz ? grid.nz - 1 : iz + 1;
-      // the 9 (x, y) columns as one candidate sequence, so a lane's trip
-      // count is its total, not the sum of per-column maxima over the warp
-      uint32_t cb[9], ce[9];
-      uint32_t total = 0;
-#pragma unroll
+      // 9 (x, y) columns, each one contiguous z range of the sorted records
+#pragma unroll 1
       for (int col = 0; col < 9; ++col) {
         const long long X = ix + col / 3 - 1, Y = iy + col % 3 - 1;
-        cb[col] = ce[col] = 0;
-        if (X >= 0 && X < grid.nx && Y >= 0 && Y < grid.ny && z0 <= z1) {
-          const unsigned long long k0 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z0);
-          const unsigned long long k1 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z1);
-          cb[col] = __ldg(&A.cell_start[k0]);
-          ce[col] = __ldg(&A.cell_start[k1 + 1]);
-        }
-        total += ce[col] - cb[col];
-      }
-      my_cand += total;
-      int col = 0;
-      uint32_t i = cb[0];
-      for (uint32_t n = 0; n < total; ++n, ++i) {
-        while (i >= ce[col]) {
-          ++col;
-          i = cb[col];
-        }
-        int sector;
-        double sv[CH], sw[CH], f0, f1, f2;
-        if (!pair_eval<CH>(A, F, Hs, i, eye, sector, sv, sw, f0, f1, f2, my_exact, my_amb)) continue;
-        ++my_acc;
-        p0 = da(p0, f0); p1 = da(p1, f1); p2 = da(p2, f2);
-        s_cnt[sector * kSparseThreads + t] += 1u;
+        if (X < 0 || X >= grid.nx || Y < 0 || Y >= grid.ny || z0 > z1) continue;
+        const unsigned long long k0 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z0);
+        const unsigned long long k1 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z1);
+        const uint32_t beg = __ldg(&A.cell_start[k0]), end = __ldg(&A.cell_start[k1 + 1]);
+        my_cand += end - beg;
+        // kSparseU candidates per step: their record loads are issued
+        // together (the loop is latency bound, one chain per thread)
+        for (uint32_t i0 = beg; i0 < end; i0 += kSparseU) {
+          float4 ra[kSparseU], rb[kSparseU], rc[kSparseU], rd[kSparseU];
+          bool live[kSparseU];
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          double &x = s_sum[(c * G + sector) * kSparseThreads + t];
-          double &y = s_sq[(c * G + sector) * kSparseThreads + t];
-          x = da(x, sv[c]);
-          y = da(y, sw[c]);
+          for (int u = 0; u < kSparseU; ++u) {
+            live[u] = i0 + u < end;
+            ra[u] = live[u] ? __ldg(&A.rec0[i0 + u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < kSparseU; ++u) live[u] = live[u] && test_pair(F, ra[u], A.max_depth);
+#pragma unroll
+          for (int u = 0; u < kSparseU; ++u)
+            if (live[u]) {
+              rb[u] = __ldg(&A.rec1[i0 + u]);
+              rc[u] = __ldg(&A.rec2[i0 + u]);
+              rd[u] = __ldg(&A.rec3[i0 + u]);
+            }
+#pragma unroll
+          for (int u = 0; u < kSparseU; ++u) {
+            if (!live[u]) continue;
+            int sector;
+            double sv[CH], sw[CH], f0, f1, f2;
+            if (!pair_tail<CH, HitX>(A, F, Hs, i0 + u, eye, ra[u], rb[u], rc[u], rd[u], sector, sv, sw, f0, f1, f2,
+                               my_exact, my_amb))
+              continue;
+            ++my_acc;
+            p0 = da(p0, f0); p1 = da(p1, f1); p2 = da(p2, f2);
+            s_cnt[sector * kSparseThreads + t] += 1u;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+              double &x = s_sum[(c * G + sector) * kSparseThreads + t];
+              double &y = s_sq[(c * G + sector) * kSparseThreads + t];
+              x = da(x, sv[c]);
+              y = da(y, sw[c]);
+            }
+          }
         }
       }
     }
@@ -330,11 +374,12 @@ __global__ void __launch_bounds__(kSparseThreads) k_gather_sparse(const GatherAr
 }
 
 size_t sparse_smem_bytes(int G, int C) {
-  return sizeof(Hit) * kSparseThreads + (size_t)kSparseThreads * (16 * (size_t)G * C + 4 * (size_t)G);
+  return sizeof(HitX) * kSparseThreads + (size_t)kSparseThreads * (16 * (size_t)G * C + 4 * (size_t)G);
 }
 
 template <int GMAX, int CH>
-static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, double *rows, int sms) {
+static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, double *rows,
+                                     int sms) {
   const int G = A.na * A.ns;
   const size_t smem = sparse_smem_bytes(G, CH);
   cudaError_t e = cudaFuncSetAttribute(k_gather_sparse<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -347,15 +392,16 @@ static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, double
   const unsigned need = (A.H + kSparseThreads - 1) / kSparseThreads;
   if (blocks > need) blocks = need;
   if (blocks == 0) blocks = 1;
-  k_gather_sparse<GMAX, CH><<<blocks, kSparseThreads, smem, s>>>(A, rows);
+  k_gather_sparse<GMAX, CH><<<blocks, kSparseThreads, smem, s>>>(A, order, rows);
   note_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, double *rows, int sms) {
-  // GMAX only sizes the apply kernel's registers here; one instance per C
-  if (C == 1) return launch_sparse_one<32, 1>(s, A, rows, sms);
-  return launch_sparse_one<32, 3>(s, A, rows, sms);
+cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, const uint32_t *order,
+                                 double *rows, int sms) {
+  // the accumulators live in shared memory: one instance per C
+  if (C == 1) return launch_sparse_one<32, 1>(s, A, order, rows, sms);
+  return launch_sparse_one<32, 3>(s, A, order, rows, sms);
 }
 
 // ---------------------------------------------------------------- explicit samples

@@ -198,7 +198,10 @@ cudaError_t launch_end_iteration(cudaStream_t s, const EndArgs &A);
 // thread-per-hit-point gather for sparse 3D frames (gather.cu)
 // writes option-B rows [H][G + 2 G C + 3]; the caller pools them
 // (launch_apply_deltas) unless they are the cross-rank partial sums
-cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, double *rows, int sms);
+cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, const uint32_t *order,
+                                 double *rows, int sms);
+cudaError_t hp_cell_order(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g, int sms,
+                          const uint32_t **order);
 size_t sparse_smem_bytes(int G, int C);
 // pools summed option-B rows into regions [h0, h0 + n) and runs the
 // end-of-iteration policy (finalize_hit)

@@ -65,6 +65,13 @@ struct Hit {
 };
 
 // Register-resident subset used by the candidate loops.
+// fp64 subset of Hit for the exact path and pair values (sparse kernel smem)
+struct HitX {
+  double cx, cy, cz, nx, ny, nz;
+  double3 u, v;
+  double r, r2, K0, K1, K2;
+};
+
 struct HitF {
   float chx, chy, chz, clx, cly, clz;
   float nfx, nfy, nfz, ufx, ufy, ufz, vfx, vfy, vfz;
@@ -122,7 +129,8 @@ static __device__ __forceinline__ HitF hitf(const Hit &H, int na, int ns) {
 
 // Full reference evaluation of one candidate in fp64 (no FMA).
 // Returns true when the photon is accepted; sets sector and cos_pos.
-static __device__ __noinline__ bool exact_pair(const Hit &H, float4 a, float4 b, float4 c2, int na,
+template <class HT>
+static __device__ __noinline__ bool exact_pair(const HT &H, float4 a, float4 b, float4 c2, int na,
                                                int ns, double guard, int &sector, bool &cos_pos,
                                                bool &amb) {
   const double dx = ds((double)a.x, H.cx), dy = ds((double)a.y, H.cy),
@@ -164,7 +172,8 @@ static __device__ __forceinline__ bool test_pair(const HitF &F, float4 a, uint32
 
 // Full decision for a pre-tested candidate: every predicate in fp32 with a
 // rigorous error band; anything inside a band goes to the exact fp64 path.
-static __device__ __forceinline__ bool flush_pair(const HitF &F, const Hit &Hs, float4 a, float4 b,
+template <class HT>
+static __device__ __forceinline__ bool flush_pair(const HitF &F, const HT &Hs, float4 a, float4 b,
                                                   float4 c2, double guard, int &sector,
                                                   bool &cos_pos, uint32_t &n_exact,
                                                   uint32_t &n_amb) {

@@ -608,6 +608,24 @@ static inline unsigned blocks_for(unsigned long long n, int threads, int sms, in
   return (unsigned)(b ? b : 1);
 }
 
+// Hit points sorted by home cell (k_hp_bin keys): the sparse kernel walks
+// them in this order so a warp's hit points share candidate records.
+cudaError_t hp_cell_order(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g, int sms,
+                          const uint32_t **order) {
+  const unsigned long long n_ext =
+      (unsigned long long)(g.nx + 2) * (unsigned long long)(g.ny + 2) * (unsigned long long)(g.nz + 2);
+  if (n_ext + 1 >= 0xffffffffull) return cudaErrorInvalidValue;
+  k_hp_bin<<<blocks_for(A.H, 256, sms, 16), 256, 0, s>>>(A.pos, A.gathered, A.H, A.grid, S.sort.keys_a,
+                                                         S.sort.vals_a);
+  note_launches(1);
+  uint32_t bits = 1;
+  while (bits < 32 && (1ull << bits) < n_ext + 1) ++bits;
+  uint32_t *skeys, *svals;
+  cudaError_t e = radix_sort_pairs(s, S.sort, A.H, bits, &skeys, &svals);
+  *order = svals;
+  return e;
+}
+
 cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S,
                                const GridHeader &g, int sms, uint32_t chunk, uint32_t *nb_out) {
   const unsigned long long n_ext =
