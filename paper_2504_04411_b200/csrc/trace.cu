@@ -172,7 +172,13 @@ __device__ __forceinline__ bool hit_quad(const PrimD &p, DVec o, DVec d, double 
   const double denom = dot(d, n);
   if (denom == 0.0) return false;
   const DVec corner = dv(p.c[0], p.c[1], p.c[2]);
-  const double tt = dd(dot(sub(corner, o), n), denom);
+  const double num = dot(sub(corner, o), n);
+  // Division-free rejections that the IEEE quotient num / denom would also
+  // reject: t <= 0 (opposite signs or num == 0) and t >= tmax when |num|
+  // exceeds tmax |denom| by more than the rounding of both operations.
+  if (num == 0.0 || ((num < 0.0) != (denom < 0.0))) return false;
+  if (fabs(num) > dm(dm(tmax, fabs(denom)), 1.0 + 0x1p-50)) return false;
+  const double tt = dd(num, denom);
   if (tt <= tmin || tt >= tmax) return false;
   const DVec e1 = dv(p.e1[0], p.e1[1], p.e1[2]), e2 = dv(p.e2[0], p.e2[1], p.e2[2]);
   const DVec rel = sub(add(o, mul(d, tt)), corner);

@@ -13,8 +13,8 @@ from scenes import scene3d
 pytestmark = pytest.mark.gpu
 
 
-def _ctx(cfg, hit, H):
-    ctx = FppmContext(initial_radius=cfg["initial_radius"], samples_per_iteration=cfg["samples_per_iteration"],
+def _ctx(cfg, hit, H, kernel="auto"):
+    ctx = FppmContext(gather_kernel=kernel, initial_radius=cfg["initial_radius"], samples_per_iteration=cfg["samples_per_iteration"],
                       n_annuli=cfg["n_annuli"], n_sectors=cfg["n_sectors"], alpha_f=cfg["alpha_f"],
                       r_min_base=cfg["r_min_base"], channels="rgb" if cfg.get("channels", 1) == 3 else "luminance",
                       max_hitpoints=H, max_photons=1 << 17, vcm_plus=True, mis_n_vm=cfg["mis_n_vm"],
@@ -24,14 +24,15 @@ def _ctx(cfg, hit, H):
     return ctx
 
 
+@pytest.mark.parametrize("kernel", ["auto", "sparse"])
 @pytest.mark.parametrize("beta", [1.0, 2.0])
 @pytest.mark.parametrize("channels", [1, 3])
-def test_vcm_canonical_matches_oracle(port, beta, channels):
+def test_vcm_canonical_matches_oracle(port, beta, channels, kernel):
     W, N = 48, 1 << 15
     hit = port.gen_raster_hitpoints(W)
     cfg = dict(n_annuli=2, n_sectors=4, alpha_f=0.01, initial_radius=0.02, r_min_base=2e-5,
                samples_per_iteration=N, threads=8, vcm_plus=1, mis_n_vm=N, mis_beta=beta, channels=channels)
-    ctx = _ctx(cfg, hit, W * W)
+    ctx = _ctx(cfg, hit, W * W, kernel)
     sess = port.session(cfg, hit)
     rng = np.random.default_rng(int(beta * 10) + channels)
     ev, em = rng.random(W * W) * 2, rng.random(W * W)
@@ -49,11 +50,12 @@ def test_vcm_canonical_matches_oracle(port, beta, channels):
         assert want["accepted"].sum() > 0
 
 
-def test_vcm_general_scene_matches_reference(port, ref):
+@pytest.mark.parametrize("kernel", ["auto", "sparse"])
+def test_vcm_general_scene_matches_reference(port, ref, kernel):
     hit, _ = scene3d(4, H=400, N=15000)
     cfg = dict(n_annuli=2, n_sectors=6, alpha_f=0.05, initial_radius=0.03, r_min_base=3e-5,
                samples_per_iteration=15000, threads=4, vcm_plus=1, mis_n_vm=15000, mis_beta=2.0)
-    ctx = _ctx(cfg, hit, 400)
+    ctx = _ctx(cfg, hit, 400, kernel)
     sess = ref.session(cfg, hit)
     rng = np.random.default_rng(3)
     ev, em = rng.random(400) * 2, rng.random(400)
