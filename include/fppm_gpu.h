@@ -62,6 +62,7 @@ typedef enum fppm_status {
 /* canonical synthetic workloads */
 #define FPPM_WORKLOAD_C1 1
 #define FPPM_WORKLOAD_C2 2
+#define FPPM_WORKLOAD_C5 5  /* needs fppm_gpu_c5_setup (same seed) */
 
 typedef struct fppm_gpu_config {
   /* TestConfig (gather.hpp:34-41) */
@@ -229,6 +230,15 @@ int fppm_gpu_gather_test(fppm_gpu_ctx *ctx, uint64_t iteration,
 /* One FPPM iteration: build_grid(max live radius) + gather_test. */
 int fppm_gpu_iterate(fppm_gpu_ctx *ctx, uint64_t iteration,
                      fppm_gpu_iter_out *out, fppm_gpu_summary *summary);
+
+/* ---- C5 synthetic workload (BASELINE configs[4]) ----
+ * Generates the n_hitpoints hit points of the workload (uniform in the unit
+ * cube, uniform random normals), their nearest-neighbour grid and the 64
+ * photon clusters for `seed`; FPPM_WORKLOAD_C5 photons then come from
+ * fppm_gpu_generate_photons(_to).  c5_hitpoints sets hit points
+ * [h0, h0 + n) of that set as the context's hit points (a rank's share). */
+int fppm_gpu_c5_setup(fppm_gpu_ctx *ctx, uint64_t seed, uint32_t n_hitpoints);
+int fppm_gpu_c5_hitpoints(fppm_gpu_ctx *ctx, uint32_t h0, uint32_t n);
 
 /* ---- multi-GPU, photon-sharded decomposition (SURVEY.md 8(e) option B) ----
  * Each rank builds the grid of its own photon share and gathers for ALL hit

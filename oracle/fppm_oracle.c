@@ -975,3 +975,207 @@ void orc_gen_raster_hitpoints(uint32_t W, double *pos, double *nrm, double *wo,
       eye_depth[h] = 1;
     }
 }
+
+
+/* ---------------------------------------------------------------- C5
+ * BASELINE configs[4] workload generator (same draws and operation order as
+ * generate.cu's C5 kernels): hit points uniform in the unit cube with uniform
+ * random normals; photons from 64 Gaussian clusters (sigma 0.01 * 5^u,
+ * Dirichlet(1) weights) + 20 % uniform, rejected (up to 8 attempts) unless
+ * within 0.05 of the tangent plane of the nearest hit point, whose normal is
+ * the deposit normal; wi cosine-distributed about it. */
+#define C5_CLUSTERS 64
+#define C5_ATTEMPTS 8
+
+struct orc_c5 {
+  uint64_t seed;
+  uint32_t H;
+  int G;
+  double cl[5 * C5_CLUSTERS];
+  double *pos, *nrm;
+  uint32_t *start, *items;
+};
+
+static void c5_draws(uint64_t seed, uint64_t iteration, uint64_t kind, uint64_t idx, uint32_t *d, int n) {
+  const uint64_t stream = stream_id(iteration, kind);
+  const uint64_t inc = (stream << 1) | 1u;
+  uint64_t st = pcg_advance(pcg_seed_state(seed, inc), idx * DRAWS_PER_PHOTON, inc);
+  for (int i = 0; i < n; ++i) {
+    d[i] = pcg_output(st);
+    st = st * PCG_MULT + inc;
+  }
+}
+
+static int c5_cell(double x, int G) {
+  const double f = floor(x * (double)G);
+  return f < 0.0 ? 0 : (f > (double)(G - 1) ? G - 1 : (int)f);
+}
+
+orc_c5 *orc_c5_create(uint64_t seed, uint32_t H) {
+  orc_c5 *c = (orc_c5 *)calloc(1, sizeof(orc_c5));
+  c->seed = seed;
+  c->H = H;
+  int G = 1;
+  while ((uint64_t)(G + 1) * (G + 1) * (G + 1) * 2u <= H) ++G;
+  c->G = G;
+  double w[C5_CLUSTERS], total = 0.0;
+  for (int k = 0; k < C5_CLUSTERS; ++k) {
+    uint32_t d[5];
+    c5_draws(seed, 0, 3, (uint64_t)k, d, 5);
+    c->cl[5 * k] = (double)u24(d[0]);
+    c->cl[5 * k + 1] = (double)u24(d[1]);
+    c->cl[5 * k + 2] = (double)u24(d[2]);
+    c->cl[5 * k + 3] = 0.01 * orc_dm_exp((double)u24(d[3]) * 0x1.9c041f7ed8d33p+0);
+    w[k] = -orc_dm_log(uopen(d[4]));
+    total = total + w[k];
+  }
+  double run = 0.0;
+  for (int k = 0; k < C5_CLUSTERS; ++k) {
+    run = run + w[k];
+    c->cl[5 * k + 4] = run / total;
+  }
+  c->pos = (double *)malloc(sizeof(double) * 3 * (H ? H : 1));
+  c->nrm = (double *)malloc(sizeof(double) * 3 * (H ? H : 1));
+  for (uint32_t h = 0; h < H; ++h) {
+    uint32_t d[5];
+    c5_draws(seed, 0, 2, h, d, 5);
+    c->pos[3 * h] = (double)u24(d[0]);
+    c->pos[3 * h + 1] = (double)u24(d[1]);
+    c->pos[3 * h + 2] = (double)u24(d[2]);
+    const double z = 1.0 - 2.0 * (double)u24(d[3]);
+    const double q = 1.0 - z * z;
+    const double r = sqrt(q > 0.0 ? q : 0.0);
+    double sn, cs;
+    orc_dm_sincos2pi((double)u24(d[4]), &sn, &cs);
+    c->nrm[3 * h] = r * cs;
+    c->nrm[3 * h + 1] = r * sn;
+    c->nrm[3 * h + 2] = z;
+  }
+  const size_t nc = (size_t)G * G * G;
+  c->start = (uint32_t *)calloc(nc + 1, sizeof(uint32_t));
+  c->items = (uint32_t *)malloc(sizeof(uint32_t) * (H ? H : 1));
+  uint32_t *cell = (uint32_t *)malloc(sizeof(uint32_t) * (H ? H : 1));
+  for (uint32_t h = 0; h < H; ++h) {
+    cell[h] = ((uint32_t)c5_cell(c->pos[3 * h + 2], G) * (uint32_t)G + (uint32_t)c5_cell(c->pos[3 * h + 1], G)) *
+                  (uint32_t)G + (uint32_t)c5_cell(c->pos[3 * h], G);
+    c->start[cell[h] + 1]++;
+  }
+  for (size_t i = 0; i < nc; ++i) c->start[i + 1] += c->start[i];
+  uint32_t *fill = (uint32_t *)calloc(nc ? nc : 1, sizeof(uint32_t));
+  for (uint32_t h = 0; h < H; ++h) c->items[c->start[cell[h]] + fill[cell[h]]++] = h;
+  free(fill);
+  free(cell);
+  return c;
+}
+
+void orc_c5_free(orc_c5 *c) {
+  if (!c) return;
+  free(c->pos); free(c->nrm); free(c->start); free(c->items);
+  free(c);
+}
+
+static uint32_t c5_nearest(const orc_c5 *C, double px, double py, double pz) {
+  const int G = C->G;
+  const int cx = c5_cell(px, G), cy = c5_cell(py, G), cz = c5_cell(pz, G);
+  const double cs = 1.0 / (double)G;
+  double best = 1e300;
+  uint32_t bi = 0xffffffffu;
+  for (int k = 0; k <= G; ++k) {
+    for (int z = cz - k; z <= cz + k; ++z) {
+      if (z < 0 || z >= G) continue;
+      for (int y = cy - k; y <= cy + k; ++y) {
+        if (y < 0 || y >= G) continue;
+        for (int x = cx - k; x <= cx + k; ++x) {
+          if (x < 0 || x >= G) continue;
+          if (z != cz - k && z != cz + k && y != cy - k && y != cy + k && x != cx - k && x != cx + k) continue;
+          const uint32_t c = ((uint32_t)z * (uint32_t)G + (uint32_t)y) * (uint32_t)G + (uint32_t)x;
+          for (uint32_t e = C->start[c]; e < C->start[c + 1]; ++e) {
+            const uint32_t h = C->items[e];
+            const double dx = px - C->pos[3 * h], dy = py - C->pos[3 * h + 1], dz = pz - C->pos[3 * h + 2];
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 < best || (d2 == best && h < bi)) {
+              best = d2;
+              bi = h;
+            }
+          }
+        }
+      }
+    }
+    const double b = (double)k * cs;
+    if (bi != 0xffffffffu && best <= b * b) break;
+  }
+  return bi;
+}
+
+void orc_c5_hitpoints(const orc_c5 *C, uint32_t h0, uint32_t n, double *pos, double *nrm, double *wo, double *thr,
+                      double *alb, uint32_t *eye_depth) {
+  for (uint32_t i = 0; i < n; ++i) {
+    for (int k = 0; k < 3; ++k) {
+      pos[3 * i + k] = C->pos[3 * (h0 + i) + k];
+      nrm[3 * i + k] = C->nrm[3 * (h0 + i) + k];
+      wo[3 * i + k] = C->nrm[3 * (h0 + i) + k];
+      thr[3 * i + k] = 1.0;
+      alb[3 * i + k] = 1.0;
+    }
+    eye_depth[i] = 1;
+  }
+}
+
+void orc_c5_photons(const orc_c5 *C, uint64_t iteration, uint64_t begin, uint64_t count, float *pos, float *nrm,
+                    float *wi, float *pow_, uint32_t *depth) {
+  for (uint64_t k = 0; k < count; ++k) {
+    const uint64_t j = begin + k;
+    uint32_t d[11];
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    uint32_t hn = 0;
+    for (int a = 0; a < C5_ATTEMPTS; ++a) {
+      c5_draws(C->seed, iteration, a == 0 ? 0u : (uint64_t)(7 + a), j, d, 11);
+      double x, y, z;
+      if (u24(d[0]) < 0.2f) {
+        x = (double)u24(d[2]);
+        y = (double)u24(d[3]);
+        z = (double)u24(d[4]);
+      } else {
+        const double u = (double)u24(d[1]);
+        int c = 0;
+        while (c < C5_CLUSTERS - 1 && !(u < C->cl[5 * c + 4])) ++c;
+        const double *q = C->cl + 5 * c;
+        const double r1 = sqrt(-2.0 * orc_dm_log(uopen(d[2])));
+        const double r2 = sqrt(-2.0 * orc_dm_log(uopen(d[4])));
+        double s1, c1, s2, c2;
+        orc_dm_sincos2pi((double)u24(d[3]), &s1, &c1);
+        orc_dm_sincos2pi((double)u24(d[5]), &s2, &c2);
+        x = q[0] + q[3] * (r1 * c1);
+        y = q[1] + q[3] * (r1 * s1);
+        z = q[2] + q[3] * (r2 * c2);
+      }
+      fx = (float)x;
+      fy = (float)y;
+      fz = (float)z;
+      hn = c5_nearest(C, (double)fx, (double)fy, (double)fz);
+      const double *hp = C->pos + 3 * (size_t)hn, *hv = C->nrm + 3 * (size_t)hn;
+      const double off = ((double)fx - hp[0]) * hv[0] + ((double)fy - hp[1]) * hv[1] + ((double)fz - hp[2]) * hv[2];
+      if (fabs(off) <= 0.05) break;
+    }
+    const double *nv = C->nrm + 3 * (size_t)hn;
+    pos[3 * k] = fx;
+    pos[3 * k + 1] = fy;
+    pos[3 * k + 2] = fz;
+    nrm[3 * k] = (float)nv[0];
+    nrm[3 * k + 1] = (float)nv[1];
+    nrm[3 * k + 2] = (float)nv[2];
+    pow_[3 * k] = u24(d[6]);
+    pow_[3 * k + 1] = u24(d[7]);
+    pow_[3 * k + 2] = u24(d[8]);
+    const double u1 = (double)u24(d[9]);
+    double sn, cs;
+    orc_dm_sincos2pi((double)u24(d[10]), &sn, &cs);
+    const double r = sqrt(u1);
+    const double zz = 1.0 - u1;
+    const double lx = r * cs, ly = r * sn, lz = sqrt(zz < 0.0 ? 0.0 : zz);
+    double fu[3], fv[3];
+    orc_build_frame(nv, fu, fv);
+    for (int i = 0; i < 3; ++i) wi[3 * k + i] = (float)(fu[i] * lx + fv[i] * ly + nv[i] * lz);
+    depth[k] = 1;
+  }
+}

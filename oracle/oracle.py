@@ -130,6 +130,10 @@ class Oracle:
             self._log = fn("dm_log", C.c_double, [C.c_double])
             self._exp = fn("dm_exp", C.c_double, [C.c_double])
             self._fcrit = fn("f_critical", C.c_double, [C.c_int64, C.c_int64, C.c_double])
+            self._c5c = fn("c5_create", C.c_void_p, [C.c_uint64, C.c_uint32])
+            self._c5f = fn("c5_free", None, [C.c_void_p])
+            self._c5h = fn("c5_hitpoints", None, [C.c_void_p, C.c_uint32, C.c_uint32] + [C.c_void_p] * 6)
+            self._c5p = fn("c5_photons", None, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64] + [C.c_void_p] * 5)
         else:
             self._si = fn("session_iterate", C.c_int, [C.c_void_p, C.c_uint64, _fp, _fp, _fp, _fp, _u32p, C.c_size_t, C.c_double, _u32p, C.c_size_t, C.POINTER(IterOut), _dp, _dp])
             self._anova = fn("anova_f_test", None, [_u64p, _dp, _dp, C.c_int, C.c_uint64, C.c_double, _dp, _ip])
@@ -212,6 +216,11 @@ class Oracle:
         return _Session(self, cfg, hit)
 
     # ---------------------------------------------------------- generators (port only)
+    def c5(self, seed, H):
+        if self.kind != "port":
+            raise NotImplementedError("the C5 generator is part of the C restatement")
+        return _C5(self, seed, H)
+
     def scene(self, arrays: dict):
         if self.kind != "reference":
             raise NotImplementedError("photon tracing is checked against the reference build only")
@@ -232,6 +241,35 @@ class Oracle:
         self._ghp(W, *[_ptr(a[k], _dp) for k in ("pos", "nrm", "wo", "thr", "alb")],
                   _ptr(a["eye_depth"], _u32p))
         return a
+
+
+class _C5:
+    """C5 workload generator (oracle restatement of generate.cu's C5 kernels)."""
+
+    def __init__(self, o, seed, H):
+        self.o, self.seed, self.H = o, seed, H
+        self.h = o._c5c(seed, H)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o._c5f(self.h)
+            self.h = None
+
+    def hitpoints(self, h0=0, n=None):
+        n = self.H - h0 if n is None else n
+        out = dict(pos=np.zeros((n, 3)), nrm=np.zeros((n, 3)), wo=np.zeros((n, 3)), thr=np.zeros((n, 3)),
+                   alb=np.zeros((n, 3)), eye_depth=np.zeros(n, np.uint32))
+        self.o._c5h(self.h, h0, n, *[out[k].ctypes.data for k in ("pos", "nrm", "wo", "thr", "alb", "eye_depth")])
+        out["gathered"] = np.ones(n, np.uint8)
+        return out
+
+    def photons(self, iteration, begin, count):
+        out = dict(pos=np.zeros((count, 3), np.float32), nrm=np.zeros((count, 3), np.float32),
+                   wi=np.zeros((count, 3), np.float32), pow=np.zeros((count, 3), np.float32),
+                   depth=np.zeros(count, np.uint32))
+        self.o._c5p(self.h, iteration, begin, count,
+                    *[out[k].ctypes.data for k in ("pos", "nrm", "wi", "pow", "depth")])
+        return out
 
 
 class _Scene:

@@ -165,6 +165,8 @@ _SIGS = [
     ("fppm_gpu_trace_photons", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_double,
                                          C.POINTER(C.c_uint32)]),
     ("fppm_gpu_get_photon_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("fppm_gpu_c5_setup", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
+    ("fppm_gpu_c5_hitpoints", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32]),
     ("fppm_gpu_set_camera", C.c_int, [C.c_void_p, C.c_void_p]),
     ("fppm_gpu_trace_eye", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64]),
     ("fppm_gpu_film_add", C.c_int, [C.c_void_p]),

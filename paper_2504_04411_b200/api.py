@@ -216,6 +216,14 @@ class FppmContext:
                                                       a[2].ctypes.data, len(a[0])))
         self.synchronize()  # host arrays may be pageable temporaries
 
+    def c5_setup(self, seed: int, n_hitpoints: int):
+        """Generate the C5 workload's hit point set, its NN grid and clusters."""
+        self._check(self._lib.fppm_gpu_c5_setup(self._h, seed, n_hitpoints))
+
+    def c5_hitpoints(self, h0: int, n: int):
+        self._check(self._lib.fppm_gpu_c5_hitpoints(self._h, h0, n))
+        self.H = n
+
     def generate_raster_hitpoints(self, W: int):
         self._check(self._lib.fppm_gpu_generate_raster_hitpoints(self._h, W))
         self.H = W * W

@@ -50,6 +50,9 @@ struct fppm_gpu_ctx {
   const uint32_t *in_depth = nullptr;
 
   // light phase: scene on the device + per-path deposit slots
+  // C5 workload: all hit points, their NN grid and the cluster table
+  fppm_b200::C5Args c5{};
+  void *c5_mem[8] = {};
   fppm_b200::CamD cam{};
   bool has_camera = false;
   double3 *d_emit = nullptr, *d_film = nullptr;  // per pixel: emitted radiance, film sum
@@ -483,6 +486,8 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   if (ctx->d_eye_mis) cudaFree(ctx->d_eye_mis);
   if (ctx->d_emit) cudaFree(ctx->d_emit);
   if (ctx->d_rows) cudaFree(ctx->d_rows);
+  for (void *p : ctx->c5_mem)
+    if (p) cudaFree(p);
   if (ctx->d_film) cudaFree(ctx->d_film);
   for (void *p : ctx->scene_mem)
     if (p) cudaFree(p);
@@ -580,6 +585,53 @@ int fppm_gpu_generate_raster_hitpoints(fppm_gpu_ctx *ctx, uint32_t W) {
                           ctx->d_eye, ctx->d_gathered, ctx->sms);
   FPPM_CUDA_OK(cudaGetLastError());
   return finish_hitpoints(ctx, (uint32_t)n, true);
+}
+
+int fppm_gpu_c5_setup(fppm_gpu_ctx *ctx, uint64_t seed, uint32_t n_hitpoints) {
+  if (!ctx || n_hitpoints == 0) return FPPM_ERR_INVALID_ARGUMENT;
+  for (void *&p : ctx->c5_mem) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  int G = 1;  // NN grid: about 2 hit points per cell
+  while ((unsigned long long)(G + 1) * (G + 1) * (G + 1) * 2ull <= n_hitpoints) ++G;
+  const unsigned long long nc = (unsigned long long)G * G * G;
+  const size_t H = n_hitpoints;
+  const size_t sizes[8] = {sizeof(double) * 5 * kC5Clusters, sizeof(double3) * H, sizeof(double3) * H,
+                           sizeof(uint32_t) * (nc + 1), sizeof(uint32_t) * H, sizeof(uint32_t) * (nc + 2),
+                           sizeof(uint32_t) * nc, sizeof(uint32_t) * H};
+  for (int i = 0; i < 8; ++i) FPPM_CUDA_OK(cudaMalloc(&ctx->c5_mem[i], sizes[i]));
+  uint32_t *scan_tmp = nullptr;
+  FPPM_CUDA_OK(dalloc(&scan_tmp, (nc + 1) / 4096 + 8));
+  C5Args &C = ctx->c5;
+  C.seed = seed;
+  C.H = n_hitpoints;
+  C.G = G;
+  C.clusters = static_cast<double *>(ctx->c5_mem[0]);
+  C.pos = static_cast<double3 *>(ctx->c5_mem[1]);
+  C.nrm = static_cast<double3 *>(ctx->c5_mem[2]);
+  C.start = static_cast<uint32_t *>(ctx->c5_mem[5]);
+  C.items = static_cast<uint32_t *>(ctx->c5_mem[7]);
+  cudaError_t e = launch_c5_setup(ctx->stream, seed, n_hitpoints, G, static_cast<double *>(ctx->c5_mem[0]),
+                                  static_cast<double3 *>(ctx->c5_mem[1]), static_cast<double3 *>(ctx->c5_mem[2]),
+                                  static_cast<uint32_t *>(ctx->c5_mem[3]), static_cast<uint32_t *>(ctx->c5_mem[4]),
+                                  static_cast<uint32_t *>(ctx->c5_mem[5]), static_cast<uint32_t *>(ctx->c5_mem[6]),
+                                  static_cast<uint32_t *>(ctx->c5_mem[7]), scan_tmp, ctx->sms);
+  cudaError_t e2 = cudaStreamSynchronize(ctx->stream);
+  cudaFree(scan_tmp);
+  FPPM_CUDA_OK(e);
+  FPPM_CUDA_OK(e2);
+  return FPPM_OK;
+}
+
+int fppm_gpu_c5_hitpoints(fppm_gpu_ctx *ctx, uint32_t h0, uint32_t n) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->c5.pos) return fail(ctx, FPPM_ERR_STATE, "c5_hitpoints before c5_setup");
+  if ((uint64_t)h0 + n > ctx->c5.H) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "hit point range exceeds C5 set");
+  if (n > ctx->cfg.max_hitpoints) return fail(ctx, FPPM_ERR_CAPACITY, "hit points exceed max_hitpoints");
+  FPPM_CUDA_OK(launch_c5_set_hitpoints(ctx->stream, ctx->c5, h0, n, ctx->d_pos, ctx->d_nrm, ctx->d_wo, ctx->d_thr,
+                                       ctx->d_alb, ctx->d_eye, ctx->d_gathered, ctx->sms));
+  return finish_hitpoints(ctx, n, true);
 }
 
 int fppm_gpu_reset_regions(fppm_gpu_ctx *ctx) {
@@ -734,13 +786,20 @@ int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint
 int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed, uint64_t iteration,
                               uint64_t begin, uint32_t n) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
-  if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2)
+  if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2 && workload != FPPM_WORKLOAD_C5)
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
+  if (workload == FPPM_WORKLOAD_C5 && !ctx->c5.pos) return fail(ctx, FPPM_ERR_STATE, "C5 photons before c5_setup");
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (ctx->stage_pending == 0) FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[0], 0));
   ctx->stage_pending = -1;
-  launch_generate_photons(ctx->stream, workload, seed, iteration, begin, n, ctx->d_ppos, ctx->d_pnrm,
-                          ctx->d_pwi, ctx->d_ppow, ctx->d_pdepth, ctx->sms);
+  if (workload == FPPM_WORKLOAD_C5) {
+    if (seed != ctx->c5.seed) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "C5 seed differs from c5_setup");
+    FPPM_CUDA_OK(launch_c5_photons(ctx->stream, ctx->c5, iteration, begin, n, ctx->d_ppos, ctx->d_pnrm, ctx->d_pwi,
+                                   ctx->d_ppow, ctx->d_pdepth, ctx->sms));
+  } else {
+    launch_generate_photons(ctx->stream, workload, seed, iteration, begin, n, ctx->d_ppos, ctx->d_pnrm,
+                            ctx->d_pwi, ctx->d_ppow, ctx->d_pdepth, ctx->sms);
+  }
   FPPM_CUDA_OK(cudaGetLastError());
   ctx->N = n;
   ctx->grid_valid = false;
@@ -752,10 +811,18 @@ int fppm_gpu_generate_photons_to(fppm_gpu_ctx *ctx, int32_t workload, uint64_t s
                                  uint64_t iteration, uint64_t begin, uint32_t n,
                                  const fppm_photons *d) {
   if (!ctx || !d) return FPPM_ERR_INVALID_ARGUMENT;
-  if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2)
+  if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2 && workload != FPPM_WORKLOAD_C5)
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
   if (n && (!d->pos || !d->normal || !d->wi || !d->power || !d->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
+  if (workload == FPPM_WORKLOAD_C5) {
+    if (!ctx->c5.pos) return fail(ctx, FPPM_ERR_STATE, "C5 photons before c5_setup");
+    if (seed != ctx->c5.seed) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "C5 seed differs from c5_setup");
+    FPPM_CUDA_OK(launch_c5_photons(ctx->stream, ctx->c5, iteration, begin, n, const_cast<float *>(d->pos),
+                                   const_cast<float *>(d->normal), const_cast<float *>(d->wi),
+                                   const_cast<float *>(d->power), const_cast<uint32_t *>(d->depth), ctx->sms));
+    return FPPM_OK;
+  }
   launch_generate_photons(ctx->stream, workload, seed, iteration, begin, n,
                           const_cast<float *>(d->pos), const_cast<float *>(d->normal),
                           const_cast<float *>(d->wi), const_cast<float *>(d->power),

@@ -286,6 +286,25 @@ cudaError_t launch_trace_compact(cudaStream_t s, const TraceArgs &A, const uint3
                                  double *mc, int sms);
 
 // generate.cu
+// C5 workload (generate.cu)
+constexpr int kC5Clusters = 64;
+constexpr int kC5Attempts = 8;
+struct C5Args {
+  uint64_t seed;
+  uint32_t H;
+  int G;                       // NN grid: G^3 cells over the unit cube
+  const double *clusters;      // [64][5] center xyz, sigma, cumulative weight
+  const double3 *pos, *nrm;    // all H hit points
+  const uint32_t *start, *items;
+};
+cudaError_t launch_c5_setup(cudaStream_t s, uint64_t seed, uint32_t H, int G, double *clusters, double3 *pos,
+                            double3 *nrm, uint32_t *cnt, uint32_t *cell_of, uint32_t *start, uint32_t *fill,
+                            uint32_t *items, uint32_t *scan_tmp, int sms);
+cudaError_t launch_c5_photons(cudaStream_t s, const C5Args &C, uint64_t iteration, uint64_t begin, uint32_t n,
+                              float *pos, float *nrm, float *wi, float *pw, uint32_t *depth, int sms);
+cudaError_t launch_c5_set_hitpoints(cudaStream_t s, const C5Args &C, uint32_t h0, uint32_t n, double3 *pos,
+                                    double3 *nrm, double3 *wo, double3 *thr, double3 *alb, uint32_t *eye_depth,
+                                    uint8_t *gathered, int sms);
 void launch_generate_photons(cudaStream_t s, int workload, uint64_t seed, uint64_t iteration,
                              uint64_t begin, uint32_t n, float *pos, float *nrm, float *wi,
                              float *pw, uint32_t *depth, int sms);

@@ -9,6 +9,9 @@ a reference parameter open, the choice is recorded here and in DESIGN.md:
   wi cosine-distributed about +z;
 * r_min_base = 0.001 r_1 (integrator.cpp:125-126), k = 0.7, alpha = 0.75,
   max_depth 10, normal guard cos 30 deg (integrator.cpp:47).
+* C5: hit points uniform in the unit cube with uniform random normals (raster
+  = 4096 only fixes H = 4096^2); photons from the generator in generate.cu
+  (clusters + background, nearest-hit-point tangent-plane restriction).
 """
 from __future__ import annotations
 
@@ -46,6 +49,15 @@ class Workload:
         kw.update(over)
         return kw
 
+    def set_hitpoints(self, ctx, h0: int = 0, n: int | None = None):
+        """The workload's hit points [h0, h0 + n) on a context (C1/C2: the
+        raster, all of it; C5: a share of the generated set)."""
+        if self.generator == 5:
+            ctx.c5_setup(self.seed, self.hitpoints)
+            ctx.c5_hitpoints(h0, self.hitpoints - h0 if n is None else n)
+        else:
+            ctx.generate_raster_hitpoints(self.raster)
+
     def scaled(self, raster: int, photons: int, name: str | None = None) -> "Workload":
         """Same density law at a smaller size (parity tests)."""
         from dataclasses import replace
@@ -60,4 +72,8 @@ C1 = Workload("c1_uniform_plane", generator=1, raster=256, photons=1 << 20,
 C2 = Workload("c2_step_blob", generator=2, raster=512, photons=1 << 22,
               initial_radius=0.01, n_annuli=2, n_sectors=4, alpha_f=0.01, iterations=64)
 
-WORKLOADS = {"c1": C1, "c2": C2}
+# BASELINE configs[4]: scaling stress gather, 3D (hit points in the unit cube)
+C5 = Workload("c5_clusters_3d", generator=5, raster=4096, photons=1 << 27,
+              initial_radius=0.005, n_annuli=2, n_sectors=4, alpha_f=0.05, iterations=32)
+
+WORKLOADS = {"c1": C1, "c2": C2, "c5": C5}

@@ -13,7 +13,10 @@ def test_workloads_match_baseline_configs():
     assert (C1.n_annuli, C1.n_sectors, C1.alpha_f, C1.iterations) == (1, 4, 0.05, 16)
     assert (C2.raster, C2.photons, C2.initial_radius) == (512, 1 << 22, 0.01)
     assert (C2.n_annuli * C2.n_sectors, C2.alpha_f, C2.iterations) == (8, 0.01, 64)
-    assert set(WORKLOADS) == {"c1", "c2"}
+    assert set(WORKLOADS) == {"c1", "c2", "c5"}
+    C5 = WORKLOADS["c5"]
+    assert (C5.hitpoints, C5.photons, C5.initial_radius) == (1 << 24, 1 << 27, 0.005)   # 16M x 128M
+    assert (C5.n_annuli * C5.n_sectors, C5.alpha_f, C5.iterations) == (8, 0.05, 32)
     kw = C2.context_kwargs()
     assert kw["r_min_base"] == 0.001 * C2.initial_radius  # integrator.cpp:125-126
     assert kw["samples_per_iteration"] == C2.photons
