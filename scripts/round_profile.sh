@@ -10,3 +10,6 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 STEPS=${STEPS:-2} bash scripts/launches.sh > gpurun_out/launches.txt 2>&1; echo "launches rc=$?"
 bash scripts/ncu_fine.sh > gpurun_out/ncu_fine.txt 2>&1; echo "ncu rc=$?"
+# C3 full-iteration launch list (light phase + eye pass + grid + sparse gather + film)
+timeout 600 python scripts/render_bench.py --steps 2 > gpurun_out/render_plain.txt 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/render_launches.csv python scripts/render_bench.py --steps 2 > /dev/null 2>&1; echo "render launches rc=$?"
