@@ -17,6 +17,7 @@ Output: one JSON line on rank 0 (contract in the task statement).
 from __future__ import annotations
 
 import argparse
+import functools
 import gc
 import json
 import os
@@ -381,7 +382,7 @@ class Arm:
         self.full = None
         if mode == "a" and world > 1:
             self.full = {k: torch.empty((wl.photons,) + shape, dtype=dt, device=dev)
-                         for k, dt, shape in PHOTON_LAYOUT}
+                         for k, dt, shape in photon_layout()}
         if mode == "b":
             from paper_2504_04411_b200.distributed import owner_slice
             self.h0, self.n_own = owner_slice(self.H, rank, world)
@@ -390,7 +391,7 @@ class Arm:
 
     def photons(self, src, n):
         from paper_2504_04411_b200 import _native as N
-        return N.Photons(*[src[k].data_ptr() for k, _, _ in PHOTON_LAYOUT])
+        return N.Photons(*[src[k].data_ptr() for k, _, _ in photon_layout()])
 
     def step(self, it, b, host_out=None):
         """One iteration on photon share `b` (device tensors, this rank's
@@ -439,10 +440,9 @@ class Arm:
         self.ctx.close()
 
 
-PHOTON_LAYOUT = None
-
-
-def _photon_layout():
+@functools.lru_cache(maxsize=None)
+def photon_layout():
+    """(name, dtype, per-photon shape) of the fppm_photons SoA fields."""
     import torch
     return (("photon_pos", torch.float32, (3,)), ("photon_normal", torch.float32, (3,)),
             ("photon_wi", torch.float32, (3,)), ("photon_power", torch.float32, (3,)),
@@ -454,9 +454,6 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
     import torch.distributed as dist
     from paper_2504_04411_b200 import FppmContext
     from paper_2504_04411_b200 import _native as N
-    global PHOTON_LAYOUT
-    PHOTON_LAYOUT = _photon_layout()
-
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     total_steps = args.warmup + args.steps
@@ -468,8 +465,8 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
                           max_hitpoints=1, max_photons=1, device=local_rank)
 
     def gen_batch(it):
-        out = {k: torch.empty((n_local,) + shape, dtype=dt, device=dev) for k, dt, shape in PHOTON_LAYOUT}
-        ph = N.Photons(*[out[k].data_ptr() for k, _, _ in PHOTON_LAYOUT])
+        out = {k: torch.empty((n_local,) + shape, dtype=dt, device=dev) for k, dt, shape in photon_layout()}
+        ph = N.Photons(*[out[k].data_ptr() for k, _, _ in photon_layout()])
         torch.cuda.synchronize()
         N.check(gen_ctx._lib.fppm_gpu_generate_photons_to(gen_ctx._h, wl.generator, wl.seed, it, begin,
                                                           n_local, ph), gen_ctx._h)
@@ -680,7 +677,7 @@ def run_e2e(arm, batches, args, dev):
 
     def one(it, hb):
         if world == 1 and arm.mode == "a":
-            ph = N.Photons(*[hb[k].data_ptr() for k, _, _ in PHOTON_LAYOUT])
+            ph = N.Photons(*[hb[k].data_ptr() for k, _, _ in photon_layout()])
             N.check(ctx._lib.fppm_gpu_set_photons(ctx._h, ph, n_local), ctx._h)
             N.check(ctx._lib.fppm_gpu_iterate(ctx._h, it, C.byref(io), None), ctx._h)
             return

@@ -43,8 +43,6 @@ constexpr int kFWarps = FPPM_FINE_WARPS;
 constexpr int kFThreads = kFWarps * kWarp;
 constexpr int kFWave = 32;      // hit points per wave (= kWave of the partial layout)
 constexpr int kFExact = 128;    // deferred exact pairs per warp (<= 31 + 64 pending)
-constexpr int kFMaxFrag = kFWave + kFWarps;
-constexpr uint32_t kFNone = 0xffffffffu;
 
 __device__ __forceinline__ float4 lds128_f(uint32_t addr) {
   float4 v;

@@ -267,7 +267,6 @@ __host__ __device__ constexpr size_t tile_dyn_smem_bytes() {
 }
 
 constexpr uint32_t kNoEntry = 0xffffffffu;
-constexpr uint32_t kExactCode = 0xffu;
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;

@@ -325,20 +325,6 @@ __global__ void k_cell_start(const uint32_t *__restrict__ skeys, uint32_t n,
   }
 }
 
-// Sparse bounding boxes (ncells >> n): one thread per cell, lower_bound.
-__global__ void k_cell_start_bsearch(const uint32_t *__restrict__ skeys, uint32_t n,
-                                     unsigned long long ncells, uint32_t *__restrict__ start) {
-  for (unsigned long long c = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
-       c <= ncells; c += (unsigned long long)gridDim.x * blockDim.x) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-      const uint32_t mid = lo + (hi - lo) / 2;
-      if ((unsigned long long)skeys[mid] < c) lo = mid + 1; else hi = mid;
-    }
-    start[c] = lo;
-  }
-}
-
 // Sparse tables, warp-cooperative: a warp owns 256 consecutive cells, finds
 // the window of sorted keys that falls in them with two binary searches, and
 // each lane resolves its cells inside that (small, cached) window; the table

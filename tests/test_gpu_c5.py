@@ -44,3 +44,17 @@ def test_c5_iterations_match_oracle(port, kernel):
         want = sess.iterate(it, c.photons(it, 0, wl.photons))
         compare_iteration(got, want)
         assert summary["accepted"] == int(want["accepted"].sum()) > 0
+
+
+def test_c5_api_errors():
+    from paper_2504_04411_b200 import InvalidArgument, StateError
+    ctx = FppmContext(initial_radius=0.04, samples_per_iteration=100, max_hitpoints=64, max_photons=100)
+    with pytest.raises(StateError):
+        ctx.generate_photons(5, 1, 1, 10)   # before c5_setup
+    with pytest.raises(StateError):
+        ctx.c5_hitpoints(0, 10)
+    ctx.c5_setup(1, 100)
+    with pytest.raises(InvalidArgument):
+        ctx.c5_hitpoints(90, 20)            # beyond the generated set
+    with pytest.raises(InvalidArgument):
+        ctx.generate_photons(5, 2, 1, 10)   # seed differs from the setup

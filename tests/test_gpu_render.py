@@ -98,3 +98,21 @@ def test_film_matches_reference_render(ref):
     assert bad.sum() <= max(2, npix // 200)
     rad = ctx.regions()["radius"]
     assert (rad == radius).mean() >= 0.99
+
+
+def test_render_api_errors():
+    from paper_2504_04411_b200 import InvalidArgument, StateError, CapacityError
+    ctx = _ctx(64, 1000, 0.002)
+    with pytest.raises(StateError):
+        ctx.film_add()                      # no camera
+    with pytest.raises(CapacityError):
+        ctx.set_camera(Camera((0, 0, 0), (0, 0, 1), (0, 1, 0), 40.0, 16, 16))   # 256 px > 64
+    ctx.set_camera(Camera((0, 0, 0), (0, 0, 1), (0, 1, 0), 40.0, 8, 8))
+    with pytest.raises(StateError):
+        ctx.trace_eye(1, 1)                 # no scene
+    with pytest.raises(InvalidArgument):
+        ctx.set_camera(Camera((0, 0, 0), (0, 0, 1), (0, 1, 0), 40.0, 0, 8))
+    ctx.set_scene(caustic_box())
+    ctx.trace_eye(1, 1)
+    img, n = ctx.film_mean()
+    assert n == 0 and not img.any()         # Film::mean with no iterations is black
