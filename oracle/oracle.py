@@ -149,6 +149,8 @@ class Oracle:
                                                        C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
                                                        C.c_void_p, C.c_void_p, _dp])
             self._brad = fn("bounding_radius", C.c_double, [C.c_void_p])
+            self._sparse = fn("scene_parse", C.c_void_p, [C.c_char_p, C.c_char_p, C.c_size_t])
+            self._sexport = fn("scene_export", None, [C.c_void_p] + [C.c_void_p] * 10)
             self._trace = fn("trace_photons", C.c_size_t, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
                                                            C.c_uint32, C.c_uint32, C.c_int, C.c_double,
                                                            C.c_double, C.c_int, C.c_size_t] + [C.c_void_p] * 7)
@@ -220,6 +222,48 @@ class Oracle:
         if self.kind != "port":
             raise NotImplementedError("the C5 generator is part of the C restatement")
         return _C5(self, seed, H)
+
+    def parse_scene_error(self, text: str):
+        """The reference parser's ParseError message for `text` ('' when it
+        parses).  Runs in a child interpreter that loads only ctypes: in a
+        process that has imported numpy, a ParseError unwinding out of
+        parse_scene crashes (reproduced only under Python + numpy; C++ hosts
+        catch it normally)."""
+        import subprocess
+        import sys
+        code = ("import ctypes as C, sys\n"
+                f"L = C.CDLL({LIB_REF!r})\n"
+                "f = L.ref_scene_parse; f.restype = C.c_void_p\n"
+                "f.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]\n"
+                "b = C.create_string_buffer(1024)\n"
+                "h = f(sys.stdin.buffer.read(), b, 1024)\n"
+                "sys.stdout.write('' if h else b.value.decode())\n")
+        r = subprocess.run([sys.executable, "-c", code], input=text.encode(), capture_output=True, check=True)
+        return r.stdout.decode()
+
+    def parse_scene(self, text: str):
+        """The reference's parse_scene: (arrays, camera 12-vector or None), or
+        raises OracleError with the reference's ParseError message."""
+        msg = self.parse_scene_error(text)
+        if msg:
+            raise OracleError(msg)
+        err = C.create_string_buffer(512)
+        h = self._sparse(text.encode(), err, 512)
+        if not h:
+            raise OracleError(err.value.decode())
+        sc = _Scene.__new__(_Scene)
+        sc.o, sc.h, sc.a = self, h, None
+        cnt = np.zeros(4, np.int32)
+        self._sexport(h, cnt.ctypes.data, *([None] * 9))
+        nm, npr, ne, hc = (int(x) for x in cnt)
+        a = dict(material_kind=np.zeros(nm, np.int32), material_rgb=np.zeros((nm, 3)), material_ior=np.zeros(nm),
+                 shape_kind=np.zeros(npr, np.int32), shape=np.zeros((npr, 9)), shape_material=np.zeros(npr, np.int32),
+                 emitter_shape=np.zeros(ne, np.int32), emitter_radiance=np.zeros((ne, 3)))
+        cam = np.zeros(12)
+        self._sexport(h, cnt.ctypes.data, *[a[k].ctypes.data for k in (
+            "material_kind", "material_rgb", "material_ior", "shape_kind", "shape", "shape_material",
+            "emitter_shape", "emitter_radiance")], cam.ctypes.data)
+        return a, (cam if hc else None)
 
     def scene(self, arrays: dict):
         if self.kind != "reference":

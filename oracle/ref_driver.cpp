@@ -507,6 +507,72 @@ void* ref_scene_create(uint32_t nm, const int32_t* mkind, const double* mrgb, co
 
 void ref_scene_free(void* s) { delete static_cast<RefScene*>(s); }
 
+// The reference's own parser (scene_parse.cpp parse_scene): a RefScene, or
+// nullptr with the ParseError message in `err` (cap bytes).
+void* ref_scene_parse(const char* text, char* err, size_t cap) {
+  try {
+    auto* rs = new RefScene;
+    rs->scene = parse_scene(text, "", "<scene>");
+    return rs;
+  } catch (const std::exception& e) {
+    if (err && cap) {
+      std::strncpy(err, e.what(), cap - 1);
+      err[cap - 1] = 0;
+    }
+  }
+  return nullptr;
+}
+
+// counts: [materials, primitives, emitters, has_camera]; then the arrays in
+// the fppm_scene layout (NULL to query counts only) and the camera
+// (pos, look, up, vfov, width, height).
+void ref_scene_export(void* sp, int* counts, int* mkind, double* mrgb, double* mior, int* skind, double* shape,
+                      int* smat, int* eshape, double* erad, double* cam) {
+  const Scene& sc = static_cast<RefScene*>(sp)->scene;
+  counts[0] = (int)sc.materials.size();
+  counts[1] = (int)sc.primitives.size();
+  counts[2] = (int)sc.emitters.size();
+  counts[3] = sc.has_camera ? 1 : 0;
+  if (!mkind) return;
+  for (size_t i = 0; i < sc.materials.size(); ++i) {
+    const Material& m = sc.materials[i];
+    const Rgb c = m.kind == MaterialKind::lambertian ? m.albedo
+                  : m.kind == MaterialKind::mirror   ? m.reflectance
+                                                     : m.tint;
+    mkind[i] = m.kind == MaterialKind::lambertian ? 0 : m.kind == MaterialKind::mirror ? 1
+               : m.kind == MaterialKind::dielectric ? 2 : 3;
+    mrgb[3 * i] = c.r; mrgb[3 * i + 1] = c.g; mrgb[3 * i + 2] = c.b;
+    mior[i] = m.ior;
+  }
+  for (size_t i = 0; i < sc.primitives.size(); ++i) {
+    const Primitive& p = sc.primitives[i];
+    double* q = shape + 9 * i;
+    for (int k = 0; k < 9; ++k) q[k] = 0.0;
+    if (p.kind == ShapeKind::sphere) {
+      skind[i] = 0;
+      q[0] = p.sphere.center.x; q[1] = p.sphere.center.y; q[2] = p.sphere.center.z; q[3] = p.sphere.radius;
+    } else {
+      skind[i] = p.kind == ShapeKind::quad ? 1 : 2;
+      q[0] = p.quad.corner.x; q[1] = p.quad.corner.y; q[2] = p.quad.corner.z;
+      q[3] = p.quad.e1.x; q[4] = p.quad.e1.y; q[5] = p.quad.e1.z;
+      q[6] = p.quad.e2.x; q[7] = p.quad.e2.y; q[8] = p.quad.e2.z;
+    }
+    smat[i] = p.material;
+  }
+  for (size_t i = 0; i < sc.emitters.size(); ++i) {
+    eshape[i] = sc.emitters[i].primitive;
+    erad[3 * i] = sc.emitters[i].radiance.r;
+    erad[3 * i + 1] = sc.emitters[i].radiance.g;
+    erad[3 * i + 2] = sc.emitters[i].radiance.b;
+  }
+  if (sc.has_camera && cam) {
+    const Camera& c = sc.camera;
+    const double v[12] = {c.position.x, c.position.y, c.position.z, c.look_at.x, c.look_at.y, c.look_at.z,
+                          c.up.x, c.up.y, c.up.z, c.vfov_deg, (double)c.width, (double)c.height};
+    for (int k = 0; k < 12; ++k) cam[k] = v[k];
+  }
+}
+
 // Traces light paths [begin, end) of `iteration` with RngStream(seed,
 // iteration, j, kLightStream = 0) and light_depth = max_depth - 1, then
 // flattens the vertices in path order.  Writes up to `cap` vertices (fp64

@@ -448,12 +448,16 @@ static __device__ __forceinline__ void fine_accumulate(const HitV &K, bool acc, 
                                                        double &p2) {
   const bool on = acc && cos_pos;
   const double pr = (double)pw.x, pg = (double)pw.y, pb = (double)pw.z;
+#if FPPM_EXPERIMENT != 3
   if (on) {  // predicated: flux sums (integrator.cpp:449)
     p0 += pr;
     p1 += pg;
     p2 += pb;
   }
+#endif
+#if FPPM_EXPERIMENT != 4
   if (acc) pk_add<GMAX>(cnt, sector);
+#endif
   if constexpr (CH == 1) {
     double v;
     if constexpr (GRAY) {

@@ -116,3 +116,43 @@ def test_render_api_errors():
     ctx.trace_eye(1, 1)
     img, n = ctx.film_mean()
     assert n == 0 and not img.any()         # Film::mean with no iterations is black
+
+
+SCENE_TEXT = """camera pos=(0,0.1,-0.9) look=(0,-0.1,1) up=(0,1,0) fov=70 res=40x30
+material white lambertian albedo=(0.7,0.7,0.7)
+material red lambertian albedo=(0.6,0.12,0.1)
+material green lambertian albedo=(0.12,0.5,0.1)
+material chrome mirror refl=(0.9,0.9,0.9)
+material glass dielectric ior=1.5 tint=(0.98,0.96,0.94)
+quad corner=(-1,-1,-1) e1=(0,0,2) e2=(2,0,0) material=white
+quad corner=(-1,1,-1) e1=(2,0,0) e2=(0,0,2) material=white
+quad corner=(-1,-1,1) e1=(0,2,0) e2=(2,0,0) material=white
+quad corner=(-1,-1,-1) e1=(0,2,0) e2=(0,0,2) material=red
+quad corner=(1,-1,-1) e1=(0,0,2) e2=(0,2,0) material=green
+quad corner=(-0.3,0.99,-0.3) e1=(0.6,0,0) e2=(0,0,0.6) material=white emit=(12,9,6)
+sphere center=(-0.4,-0.6,0.3) radius=0.34 material=chrome
+sphere center=(0.45,-0.62,-0.1) radius=0.3 material=glass
+"""
+
+
+def test_scene_text_render_matches_reference(ref):
+    """A scene in the reference's text format (chromatic light -> the RGB test
+    channels the reference auto-detects), rendered on the device and by the
+    reference's render()."""
+    from paper_2504_04411_b200.scene_text import parse_scene
+    sc, cam = parse_scene(SCENE_TEXT)
+    npix, J, iters = cam.width * cam.height, 20000, 3
+    r1 = 0.002 * bounding_radius(sc)
+    ctx = _ctx(npix, J, r1, channels="rgb")
+    ctx.set_scene(sc)
+    ctx.set_camera(cam)
+    for it in range(1, iters + 1):
+        ctx.render_iteration(5, it, J, 8)
+    img, _ = ctx.film_mean()
+    film, radius, _ = ref.scene(sc.arrays()).render_fppm(cam, 5, iters, 8, J, r0_frac=0.002, n_annuli=2,
+                                                         n_sectors=6, alpha_f=0.01, threads=8)
+    got = img.reshape(-1, 3)
+    rel = np.abs(got - film) / np.maximum(np.abs(film), 1e-30)
+    bad = (rel > 1e-5).any(-1) & (np.abs(got - film) > 1e-12).any(-1)
+    assert bad.sum() <= max(2, npix // 200), bad.sum()
+    assert (ctx.regions()["radius"] == radius).mean() >= 0.99
