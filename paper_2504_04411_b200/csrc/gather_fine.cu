@@ -112,23 +112,62 @@ static __device__ __forceinline__ void piece_keys(const GridHeader &g, const FBo
 static __device__ __forceinline__ int piece_count(const GridHeader &g, const FBox &u) {
   return g.S > 1 ? u.x1 - u.x0 + 1 : (u.x1 - u.x0 + 1) * (u.y1 - u.y0 + 1);
 }
-// Run j of hit-point box b inside union u: key range and the piece holding it.
-static __device__ __forceinline__ int run_keys(const GridHeader &g, const FBox &u, const FBox &b, int j,
-                                               unsigned long long &k0, unsigned long long &k1) {
-  if (g.S > 1) {
-    const long long x = b.x0 + j;
-    k0 = fid(g, x, b.y0, 0);
-    k1 = fid(g, x, b.y1, g.nz - 1);
-    return (int)(x - u.x0);
-  }
-  const int nyb = b.y1 - b.y0 + 1, nyu = u.y1 - u.y0 + 1;
-  const long long x = b.x0 + j / nyb, y = b.y0 + j % nyb;
-  k0 = fid(g, x, y, b.z0);
-  k1 = fid(g, x, y, b.z1);
-  return (int)((x - u.x0) * nyu + (y - u.y0));
-}
 static __device__ __forceinline__ int run_count(const GridHeader &g, const FBox &b) {
   return g.S > 1 ? b.x1 - b.x0 + 1 : (b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1);
+}
+
+// Distance from c to the fine slab [X / inv, (X + 1) / inv) of one axis,
+// shortened by `slack` (never negative).  Photons stored in fine cell X
+// satisfy floor(x * inv) = X in fp64; slack covers that rounding.
+static __device__ __forceinline__ double slab_gap(double c, long long X, double inv, double slack) {
+  const double lo = (double)X / inv, hi = (double)(X + 1) / inv;
+  const double d = c < lo ? lo - c : (c > hi ? c - hi : 0.0);
+  return d > slack ? d - slack : 0.0;
+}
+
+// Run j of box b clipped to the chord of the ball (c, m) (m: fine_box's
+// margin radius).  A photon accepted by the reference ball test lies within
+// m of c in the plane of the two outer axes, so in column x (slab layout)
+// only the rows |y - c.y| <= sqrt(m^2 - gap_x^2) can hold it, and in an
+// (x, y) column (reference layout) only |z - c.z| <= sqrt(m^2 - gap_xy^2).
+// The bounds are widened by `slack` (>> fp64 rounding) and mapped through the
+// same monotone floor(v * inv) as the photons' own cells, so no accepted
+// photon is ever cut.  Returns false when the run is empty.
+static __device__ __forceinline__ bool run_keys_clipped(const GridHeader &g, const FBox &b, int j, double cx,
+                                                        double cy, double cz, double m,
+                                                        unsigned long long &k0, unsigned long long &k1) {
+  const double cm = fmax(fabs(cx), fmax(fabs(cy), fabs(cz)));
+  const double slack = 1e-6 / g.inv + m * 1e-7 + cm * 1e-12;
+  const double m2 = m * m;
+  if (g.S > 1) {
+    const long long x = b.x0 + j;
+    const double gx = slab_gap(cx, x + g.ix0, g.inv, slack);
+    const double h2 = m2 - gx * gx;
+    if (!(h2 >= 0.0)) return false;
+    const double hy = sqrt(h2) + slack;
+    long long y0 = (long long)floor(dm(ds(cy, hy), g.inv)) - g.iy0;
+    long long y1 = (long long)floor(dm(da(cy, hy), g.inv)) - g.iy0;
+    if (y0 < b.y0) y0 = b.y0;
+    if (y1 > b.y1) y1 = b.y1;
+    if (y0 > y1) return false;
+    k0 = fid(g, x, y0, 0);
+    k1 = fid(g, x, y1, g.nz - 1);
+    return true;
+  }
+  const int nyb = b.y1 - b.y0 + 1;
+  const long long x = b.x0 + j / nyb, y = b.y0 + j % nyb;
+  const double gx = slab_gap(cx, x + g.ix0, g.inv, slack), gy = slab_gap(cy, y + g.iy0, g.inv, slack);
+  const double h2 = m2 - gx * gx - gy * gy;
+  if (!(h2 >= 0.0)) return false;
+  const double hz = sqrt(h2) + slack;
+  long long z0 = (long long)floor(dm(ds(cz, hz), g.inv)) - g.iz0;
+  long long z1 = (long long)floor(dm(da(cz, hz), g.inv)) - g.iz0;
+  if (z0 < b.z0) z0 = b.z0;
+  if (z1 > b.z1) z1 = b.z1;
+  if (z0 > z1) return false;
+  k0 = fid(g, x, y, z0);
+  k1 = fid(g, x, y, z1);
+  return true;
 }
 
 struct __align__(16) FinePrep {
@@ -167,14 +206,14 @@ __global__ void k_fine_prep(const GatherArgs A, const uint32_t *__restrict__ hp_
     P.bx0 = b.x0; P.bx1 = b.x1; P.by0 = b.y0; P.by1 = b.y1; P.bz0 = b.z0; P.bz1 = b.z1;
     P.nruns = (uint32_t)nr;
     P.pad = 0;
-    const FBox none = {0, 0, 0, 0, 0, 0};
+    // runs clipped to the ball's chord (same margin radius as fine_box)
+    const double cm = fmax(fabs(P.h.cx), fmax(fabs(P.h.cy), fabs(P.h.cz)));
+    const double m = da(da(P.h.r, dm(P.h.r, 1e-9)), dm(cm, 4e-16));
     for (int j = 0; j < kFMaxPieces; ++j) {
       uint2 r = make_uint2(0u, 0u);
-      if (j < nr) {
-        unsigned long long k0, k1;
-        (void)run_keys(g, none, b, j, k0, k1);
+      unsigned long long k0, k1;
+      if (j < nr && run_keys_clipped(g, b, j, P.h.cx, P.h.cy, P.h.cz, m, k0, k1))
         r = make_uint2(A.cell_start[k0], A.cell_start[k1 + 1]);
-      }
       P.run[j] = r;
     }
     prep[i] = P;
