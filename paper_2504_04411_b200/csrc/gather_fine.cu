@@ -27,6 +27,8 @@
 // per-warp list and decided on the exact fp64 path (exact_pair, gather_dev.cuh)
 // outside the hot loop.  Partials and k_tile_finalize are shared with the
 // tiled kernel.
+#include <climits>
+
 #include "common.cuh"
 #include "gather.cuh"
 #include "gather_dev.cuh"
@@ -277,121 +279,141 @@ __global__ void k_fine_bin(const double3 *__restrict__ pos, const uint8_t *__res
   }
 }
 
-// Union box of one wave (false when no member has candidates).
-static __device__ bool wave_union(const GatherArgs &A, const GridHeader &g, const uint32_t *hp_order,
-                                  uint32_t b0, uint32_t n, FBox &u) {
-  bool any = false;
-  for (uint32_t j = 0; j < n; ++j) {
-    const uint32_t h = hp_order[b0 + j];
-    const double3 c = A.pos[h];
-    FBox b;
-    if (!fine_box(g, c.x, c.y, c.z, A.radius[h], b)) continue;
-    if (!any) {
-      u = b;
-      any = true;
-    } else {
-      u.x0 = min(u.x0, b.x0); u.x1 = max(u.x1, b.x1);
-      u.y0 = min(u.y0, b.y0); u.y1 = max(u.y1, b.y1);
-      u.z0 = min(u.z0, b.z0); u.z1 = max(u.z1, b.z1);
+// One wave of a bucket, evaluated by a full warp (lane j = member j): union of
+// the members' fine boxes (from k_fine_prep), its pieces' key ranges (lane p
+// = piece p), candidate total and whether every member takes the planar path.
+struct WaveInfo {
+  FBox u;
+  int np;          // pieces (0: no member has candidates)
+  uint32_t T;      // staged candidates (union size)
+  uint32_t src;    // lane p: first sorted record of piece p
+  uint32_t pre;    // lane p: exclusive offset of piece p
+  bool planar;
+};
+static __device__ __forceinline__ WaveInfo wave_info(const GatherArgs &A, const GridHeader &g,
+                                                     const FinePrep *__restrict__ prep,
+                                                     const FineHot *__restrict__ hot, uint32_t b0, uint32_t n,
+                                                     bool real) {
+  const int lane = threadIdx.x & 31;
+  WaveInfo W;
+  bool valid = false, pl = true;
+  int x0 = INT_MAX, x1 = INT_MIN, y0 = INT_MAX, y1 = INT_MIN, z0 = INT_MAX, z1 = INT_MIN;
+  if ((uint32_t)lane < n) {
+    const FinePrep &P = prep[b0 + lane];
+    valid = real && P.nruns > 0;
+    if (valid) {
+      x0 = P.bx0; x1 = P.bx1; y0 = P.by0; y1 = P.by1; z0 = P.bz0; z1 = P.bz1;
     }
+    pl = hot[b0 + lane].planar != 0u;
   }
-  return any;
+  W.planar = __all_sync(kFull, pl);
+  W.u.x0 = __reduce_min_sync(kFull, x0); W.u.x1 = __reduce_max_sync(kFull, x1);
+  W.u.y0 = __reduce_min_sync(kFull, y0); W.u.y1 = __reduce_max_sync(kFull, y1);
+  W.u.z0 = __reduce_min_sync(kFull, z0); W.u.z1 = __reduce_max_sync(kFull, z1);
+  W.np = __any_sync(kFull, valid) ? piece_count(g, W.u) : 0;
+  uint32_t c = 0;
+  W.src = 0;
+  if (lane < W.np) {
+    unsigned long long k0, k1;
+    piece_keys(g, W.u, lane, k0, k1);
+    W.src = A.cell_start[k0];
+    c = A.cell_start[k1 + 1] - W.src;
+  }
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  W.pre = incl - c;
+  W.T = __shfl_sync(kFull, incl, 31);
+  if (W.np == 0) W.u = FBox{0, -1, 0, -1, 0, -1};
+  return W;
 }
 
-// per bucket: items (runs of <= kFSub windows of ceil(union / chunk)) and
-// partial rows (items x wave size)
-// window capacity of a wave: 48-B records when every member takes the planar
-// path (rec3 is then read from global memory on the exact path only)
-static __device__ __forceinline__ bool wave_planar(const FineHot *hot, uint32_t b0, uint32_t n) {
-  for (uint32_t j = 0; j < n; ++j)
-    if (!hot[b0 + j].planar) return false;
-  return true;
-}
-
+// per bucket (one warp each): items (runs of <= kFSub windows of
+// ceil(union / chunk)) and partial rows (items x wave size)
 __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
-                             const uint32_t *__restrict__ hp_order, const FineHot *__restrict__ hot,
+                             const FinePrep *__restrict__ prep, const FineHot *__restrict__ hot,
                              uint32_t *__restrict__ items, uint32_t *__restrict__ prows, uint32_t cap64,
                              uint32_t cap48, uint32_t *__restrict__ nonempty) {
   const GridHeader g = *A.grid;
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b <= nb; b += nw) {
     const uint32_t h0 = b < nb ? hp_start[b] : 0u;
     const uint32_t nhp = b < nb ? hp_start[b + 1] - h0 : 0u;
     uint32_t it = 0, pr = 0;
-    if (nhp) atomicAdd(nonempty, 1u);
+    if (nhp && lane == 0) atomicAdd(nonempty, 1u);
     for (uint32_t w = 0; w * kFWave < nhp; ++w) {
       const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
-      FBox u;
-      uint32_t T = 0;
-      if (b + 1 < nb && wave_union(A, g, hp_order, h0 + w * kFWave, n, u)) {
-        const int np = piece_count(g, u);
-        for (int p = 0; p < np; ++p) {
-          unsigned long long k0, k1;
-          piece_keys(g, u, p, k0, k1);
-          T += A.cell_start[k1 + 1] - A.cell_start[k0];
-        }
-      }
-      const uint32_t chunk = wave_planar(hot, h0 + w * kFWave, n) ? cap48 : cap64;
-      const uint32_t nwin = T == 0 ? 1u : (T + chunk - 1) / chunk;
+      const WaveInfo W = wave_info(A, g, prep, hot, h0 + w * kFWave, n, b + 1 < nb);
+      const uint32_t chunk = W.planar ? cap48 : cap64;
+      const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
       it += nsub;
       pr += nsub * n;
     }
-    items[b] = it;
-    prows[b] = pr;
+    if (lane == 0) {
+      items[b] = it;
+      prows[b] = pr;
+    }
   }
 }
 
 __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
-                            const uint32_t *__restrict__ hp_order, const FineHot *__restrict__ hot,
-                            const uint32_t *__restrict__ item_base,
+                            const uint32_t *__restrict__ hp_order, const FinePrep *__restrict__ prep,
+                            const FineHot *__restrict__ hot, const uint32_t *__restrict__ item_base,
                             const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
                             uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48) {
+  constexpr int kWarps = 4;  // 128 threads
+  constexpr int kWords = (int)(sizeof(FineDesc) / 4);
+  __shared__ __align__(16) uint32_t s_d[kWarps][kWords];
   const GridHeader g = *A.grid;
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  FineDesc &d = *reinterpret_cast<FineDesc *>(&s_d[wl][0]);
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += nw) {
     const uint32_t h0 = hp_start[b], nhp = hp_start[b + 1] - h0;
     uint32_t item = item_base[b], prow = prow_base[b];
     for (uint32_t w = 0; w * kFWave < nhp; ++w) {
       const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
-      FineDesc d;
-      d.hp_lo = h0 + w * kFWave;
-      d.hp_n = n;
-      FBox u = {0, -1, 0, -1, 0, -1};
-      uint32_t T = 0;
-      int np = 0;
-      if (b + 1 < nb && wave_union(A, g, hp_order, d.hp_lo, n, u)) {
-        np = piece_count(g, u);
-        for (int p = 0; p < np; ++p) {
-          unsigned long long k0, k1;
-          piece_keys(g, u, p, k0, k1);
-          d.src[p] = A.cell_start[k0];
-          d.pre[p] = T;
-          T += A.cell_start[k1 + 1] - d.src[p];
-        }
-      }
-      for (int p = np; p < kFMaxPieces; ++p) {
-        d.src[p] = 0;
-        d.pre[p] = T;
-      }
-      d.pre[kFMaxPieces] = T;
-      d.npieces = (uint32_t)np;
-      const bool planar = wave_planar(hot, d.hp_lo, n);
-      const uint32_t chunk = planar ? cap48 : cap64;
-      d.pad0 = planar ? 1u : 0u;  // flags: bit0 = 48-B records (no rec3 staged)
-      d.ux0 = u.x0; d.ux1 = u.x1; d.uy0 = u.y0; d.uy1 = u.y1; d.uz0 = u.z0; d.uz1 = u.z1;
-      const uint32_t nwin = T == 0 ? 1u : (T + chunk - 1) / chunk;
+      const uint32_t lo = h0 + w * kFWave;
+      const WaveInfo W = wave_info(A, g, prep, hot, lo, n, b + 1 < nb);
+      const uint32_t chunk = W.planar ? cap48 : cap64;
+      const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
-      d.nwin = nwin;
-      for (uint32_t j = 0; j < n; ++j) {
-        const uint32_t h = hp_order[d.hp_lo + j];
-        hp_map[3 * (size_t)h] = prow + j;  // finalize: rows prow + j + sub * n
+      __syncwarp();
+      if (lane < kFMaxPieces) {
+        d.src[lane] = lane < W.np ? W.src : 0u;
+        d.pre[lane] = lane < W.np ? W.pre : W.T;
+      }
+      if (lane == 0) {
+        d.hp_lo = lo;
+        d.hp_n = n;
+        d.nwin = nwin;
+        d.npieces = (uint32_t)W.np;
+        d.pre[kFMaxPieces] = W.T;
+        d.pad0 = W.planar ? 1u : 0u;  // flags: bit0 = 48-B records (no rec3 staged)
+        d.ux0 = W.u.x0; d.ux1 = W.u.x1; d.uy0 = W.u.y0; d.uy1 = W.u.y1; d.uz0 = W.u.z0; d.uz1 = W.u.z1;
+      }
+      if ((uint32_t)lane < n) {
+        const uint32_t h = hp_order[lo + lane];
+        hp_map[3 * (size_t)h] = prow + lane;  // finalize: rows prow + j + sub * n
         hp_map[3 * (size_t)h + 1] = nsub;
         hp_map[3 * (size_t)h + 2] = n;
       }
+      __syncwarp();
       for (uint32_t sb = 0; sb < nsub; ++sb, ++item) {
-        d.c0 = sb * kFSub;
-        d.c1 = min(nwin, d.c0 + kFSub);
-        d.pbase = prow + sb * n;
-        desc[item] = d;
+        if (lane == 0) {
+          d.c0 = sb * kFSub;
+          d.c1 = min(nwin, d.c0 + kFSub);
+          d.pbase = prow + sb * n;
+        }
+        __syncwarp();
+        uint32_t *dst = reinterpret_cast<uint32_t *>(desc + item);
+        for (int k = lane; k < kWords; k += 32) dst[k] = s_d[wl][k];
+        __syncwarp();
       }
       prow += nsub * n;
     }
@@ -1018,9 +1040,9 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   k_fine_prep<<<fblocks(A.H, 128, sms, 8), 128, 0, s>>>(A, S.hp_order, static_cast<FinePrep *>(S.fprep),
                                                         static_cast<FineHot *>(S.fhot));
   note_launches(1);
-  k_fine_items<<<fblocks(nb + 1, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order,
-                                                             static_cast<const FineHot *>(S.fhot), S.items,
-                                                             S.chunks, cap64, cap48, S.nonempty);
+  k_fine_items<<<fblocks((unsigned long long)(nb + 1) * 32, 128, sms, 16), 128, 0, s>>>(
+      A, S.hp_start, nb, static_cast<const FinePrep *>(S.fprep), static_cast<const FineHot *>(S.fhot), S.items,
+      S.chunks, cap64, cap48, S.nonempty);
   note_launches(1);
   e = launch_exclusive_scan(s, S.items, nb + 1, S.scan_tmp, S.item_base);
   if (e != cudaSuccess) return e;
@@ -1029,9 +1051,9 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
 
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
                                 uint32_t cap64, uint32_t cap48) {
-  k_fine_desc<<<fblocks(nb, 128, sms, 16), 128, 0, s>>>(A, S.hp_start, nb, S.hp_order,
-                                                        static_cast<const FineHot *>(S.fhot), S.item_base,
-                                                        S.pbase, S.fdesc, S.hp_map, cap64, cap48);
+  k_fine_desc<<<fblocks((unsigned long long)nb * 32, 128, sms, 16), 128, 0, s>>>(
+      A, S.hp_start, nb, S.hp_order, static_cast<const FinePrep *>(S.fprep), static_cast<const FineHot *>(S.fhot),
+      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48);
   note_launches(1);
   return cudaGetLastError();
 }
