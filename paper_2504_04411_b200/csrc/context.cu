@@ -420,7 +420,6 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->tile.sort.keys_b, Hc)); A(dalloc(&ctx->tile.sort.vals_b, Hc));
   A(dalloc(&ctx->tile.sort.hist, radix_hist_entries((uint32_t)Hc)));
   A(dalloc(&ctx->tile.hp_map, 3 * Hc));
-  A(dalloc(reinterpret_cast<char **>(&ctx->tile.fprep), fine_prep_bytes() * Hc));
   if (c.vcm_plus) {
     A(dalloc(&ctx->d_eye_mis, Hc));
     A(cudaMemset(ctx->d_eye_mis, 0, sizeof(double2) * Hc));
@@ -430,6 +429,8 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
     }
   }
   A(dalloc(reinterpret_cast<char **>(&ctx->tile.fhot), fine_hot_bytes() * Hc));
+  A(dalloc(&ctx->tile.fbox, Hc));
+  A(dalloc(reinterpret_cast<char **>(&ctx->tile.fhit), fine_hit_bytes() * Hc));
   A(dalloc(&ctx->tile.nonempty, 1));
   A(cudaMallocHost(&ctx->h_total, 2 * sizeof(uint32_t)));
   if (e != cudaSuccess) {
@@ -478,7 +479,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
-                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.fdesc, T.fprep, T.fhot, T.pbase, T.partials,
+                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.fdesc, T.fhot, T.fbox, T.fhit, T.pbase, T.partials,
                   T.hp_map, T.nonempty};
   for (void *p : tdev)
     if (p) cudaFree(p);
@@ -1262,8 +1263,8 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48));
       FineArgs F;
       F.desc = S.fdesc;
-      F.prep = static_cast<const FinePrep *>(S.fprep);
       F.hot = static_cast<const FineHot *>(S.fhot);
+      F.hits = static_cast<const Hit *>(S.fhit);
       F.hp_order = S.hp_order;
       F.partials = S.partials;
       F.hp_map = S.hp_map;

@@ -127,12 +127,12 @@ struct alignas(16) FineDesc {  // one per (home cell, wave, run of <= kFSub wind
 };
 static_assert(sizeof(FineDesc) % 16 == 0 && sizeof(FineDesc) / 4 <= 256, "FineDesc layout");
 
-struct FinePrep;  // gather_fine.cu (per hit point state in wave order)
 struct FineHot;   // compact per hit point state staged per item
+struct Hit;       // gather_dev.cuh
 struct FineArgs {
   const FineDesc *desc;
-  const FinePrep *prep;
   const FineHot *hot;
+  const Hit *hits;  // full per-hit-point state (exact path), wave order
   const uint32_t *hp_order;
   double *partials;
   const uint32_t *hp_map;
@@ -142,8 +142,9 @@ struct FineArgs {
 struct TileSched {
   FineDesc *fdesc = nullptr;
   unsigned long long fdesc_cap = 0;
-  void *fprep = nullptr;  // FinePrep[H]
   void *fhot = nullptr;   // FineHot[H]
+  int4 *fbox = nullptr;   // [H] (bx1, bz0, bz1, -): the rest of a hit point's fine box (wave unions)
+  void *fhit = nullptr;   // Hit[H]: full state for the exact path, wave order
   uint32_t *pbase = nullptr;  // [nb + 1] partial rows per bucket, scanned
   SortScratch sort;     // hit-point keys (capacity H)
   uint32_t *hp_order;   // alias of the sorted values
@@ -186,8 +187,8 @@ cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &
                                 uint32_t cap64, uint32_t cap48);
 size_t fine_acc_doubles(int G, int C);
 cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms);
-size_t fine_prep_bytes();
 size_t fine_hot_bytes();
+size_t fine_hit_bytes();
 
 cudaError_t launch_gather_test(cudaStream_t s, const GatherArgs &A, int C, int sms);
 cudaError_t launch_samples(cudaStream_t s, const uint32_t *region, const double2 *y,

@@ -118,11 +118,11 @@ static __device__ __forceinline__ int run_count(const GridHeader &g, const FBox 
   return g.S > 1 ? b.x1 - b.x0 + 1 : (b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1);
 }
 
-// Distance from c to the fine slab [X / inv, (X + 1) / inv) of one axis,
+// Distance from c to the fine slab [X f, (X + 1) f) of one axis (f = 1 / inv),
 // shortened by `slack` (never negative).  Photons stored in fine cell X
 // satisfy floor(x * inv) = X in fp64; slack covers that rounding.
-static __device__ __forceinline__ double slab_gap(double c, long long X, double inv, double slack) {
-  const double lo = (double)X / inv, hi = (double)(X + 1) / inv;
+static __device__ __forceinline__ double slab_gap(double c, long long X, double f, double slack) {
+  const double lo = (double)X * f, hi = (double)(X + 1) * f;  // f = 1 / inv (rounding << slack)
   const double d = c < lo ? lo - c : (c > hi ? c - hi : 0.0);
   return d > slack ? d - slack : 0.0;
 }
@@ -139,11 +139,12 @@ static __device__ __forceinline__ bool run_keys_clipped(const GridHeader &g, con
                                                         double cy, double cz, double m,
                                                         unsigned long long &k0, unsigned long long &k1) {
   const double cm = fmax(fabs(cx), fmax(fabs(cy), fabs(cz)));
-  const double slack = 1e-6 / g.inv + m * 1e-7 + cm * 1e-12;
+  const double f = 1.0 / g.inv;
+  const double slack = 1e-6 * f + m * 1e-7 + cm * 1e-12;
   const double m2 = m * m;
   if (g.S > 1) {
     const long long x = b.x0 + j;
-    const double gx = slab_gap(cx, x + g.ix0, g.inv, slack);
+    const double gx = slab_gap(cx, x + g.ix0, f, slack);
     const double h2 = m2 - gx * gx;
     if (!(h2 >= 0.0)) return false;
     const double hy = sqrt(h2) + slack;
@@ -158,7 +159,7 @@ static __device__ __forceinline__ bool run_keys_clipped(const GridHeader &g, con
   }
   const int nyb = b.y1 - b.y0 + 1;
   const long long x = b.x0 + j / nyb, y = b.y0 + j % nyb;
-  const double gx = slab_gap(cx, x + g.ix0, g.inv, slack), gy = slab_gap(cy, y + g.iy0, g.inv, slack);
+  const double gx = slab_gap(cx, x + g.ix0, f, slack), gy = slab_gap(cy, y + g.iy0, f, slack);
   const double h2 = m2 - gx * gx - gy * gy;
   if (!(h2 >= 0.0)) return false;
   const double hz = sqrt(h2) + slack;
@@ -172,68 +173,55 @@ static __device__ __forceinline__ bool run_keys_clipped(const GridHeader &g, con
   return true;
 }
 
-struct __align__(16) FinePrep {
-  Hit h;
-  int32_t bx0, bx1, by0, by1, bz0, bz1;  // fine box (fine_box)
-  uint32_t nruns, pad;
-  uint2 run[kFMaxPieces];  // sorted-record range [begin, end) of each run
-};
-static_assert(sizeof(FinePrep) % 16 == 0, "FinePrep must be a multiple of 16 B (TMA)");
-
 // Compact per-hit-point state staged in shared memory per item (the full
-// Hit stays in global memory for the exact path).
+// Hit state stays in global memory for the exact path).
 struct alignas(16) FineHot {
   HitF F;
   double K0, K1, K2;
   uint32_t planar, gray;
-  int32_t bx0, by0, by1;
+  int32_t bx0, by0, by1;  // fine box (fine_box); bx1, bz0, bz1 in the fbox array
   uint32_t nruns;
-  uint2 run[kFMaxPieces];
+  uint2 run[kFMaxPieces];  // sorted-record range [begin, end) of each run (clipped to the chord)
 };
 static_assert(sizeof(FineHot) % 16 == 0, "FineHot must be a multiple of 16 B (TMA)");
 
 // Per hit point, once per gather, in wave order (position in hp_order): the
-// full Hit state, its fine box and the sorted-record range of each run.
+// staged state, its fine box and the sorted-record range of each run.
 __global__ void k_fine_prep(const GatherArgs A, const uint32_t *__restrict__ hp_order,
-                            FinePrep *__restrict__ prep, FineHot *__restrict__ hot) {
+                            FineHot *__restrict__ hot, int4 *__restrict__ fbox, Hit *__restrict__ hits) {
   const GridHeader g = *A.grid;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.H; i += gridDim.x * blockDim.x) {
     const uint32_t h = hp_order[i];
-    FinePrep P;
-    make_hit(A, h, P.h);
+    Hit P;
+    make_hit(A, h, P);
     FBox b = {0, -1, 0, -1, 0, -1};
     const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
-    const bool ok = gathered && fine_box(g, P.h.cx, P.h.cy, P.h.cz, P.h.r, b);
+    const bool ok = gathered && fine_box(g, P.cx, P.cy, P.cz, P.r, b);
     const int nr = ok ? run_count(g, b) : 0;
-    P.bx0 = b.x0; P.bx1 = b.x1; P.by0 = b.y0; P.by1 = b.y1; P.bz0 = b.z0; P.bz1 = b.z1;
-    P.nruns = (uint32_t)nr;
-    P.pad = 0;
+    FineHot Q;
+    Q.F = hitf(P, A.na, A.ns);
+    Q.K0 = P.K0;
+    Q.K1 = P.K1;
+    Q.K2 = P.K2;
+    // n = +z, fp32-exact center, 4 bins: the planar fast path (gather_dev.cuh)
+    Q.planar = (P.fast && P.nx == 0.0 && P.ny == 0.0 && P.nz == 1.0 && A.ns == 4 &&
+                P.clx == 0.0f && P.cly == 0.0f && P.clz == 0.0f) ? 1u : 0u;
+    Q.gray = P.gray ? 1u : 0u;
+    Q.bx0 = b.x0; Q.by0 = b.y0; Q.by1 = b.y1;
+    fbox[i] = make_int4(b.x1, b.z0, b.z1, 0);
+    Q.nruns = (uint32_t)nr;
     // runs clipped to the ball's chord (same margin radius as fine_box)
-    const double cm = fmax(fabs(P.h.cx), fmax(fabs(P.h.cy), fabs(P.h.cz)));
-    const double m = da(da(P.h.r, dm(P.h.r, 1e-9)), dm(cm, 4e-16));
+    const double cm = fmax(fabs(P.cx), fmax(fabs(P.cy), fabs(P.cz)));
+    const double m = da(da(P.r, dm(P.r, 1e-9)), dm(cm, 4e-16));
     for (int j = 0; j < kFMaxPieces; ++j) {
       uint2 r = make_uint2(0u, 0u);
       unsigned long long k0, k1;
-      if (j < nr && run_keys_clipped(g, b, j, P.h.cx, P.h.cy, P.h.cz, m, k0, k1))
+      if (j < nr && run_keys_clipped(g, b, j, P.cx, P.cy, P.cz, m, k0, k1))
         r = make_uint2(A.cell_start[k0], A.cell_start[k1 + 1]);
-      P.run[j] = r;
+      Q.run[j] = r;
     }
-    prep[i] = P;
-    FineHot Q;
-    Q.F = hitf(P.h, A.na, A.ns);
-    Q.K0 = P.h.K0;
-    Q.K1 = P.h.K1;
-    Q.K2 = P.h.K2;
-    // n = +z, fp32-exact center, 4 bins: the planar fast path (gather_dev.cuh)
-    Q.planar = (P.h.fast && P.h.nx == 0.0 && P.h.ny == 0.0 && P.h.nz == 1.0 && A.ns == 4 &&
-                P.h.clx == 0.0f && P.h.cly == 0.0f && P.h.clz == 0.0f) ? 1u : 0u;
-    Q.gray = P.h.gray ? 1u : 0u;
-    Q.bx0 = b.x0;
-    Q.by0 = b.y0;
-    Q.by1 = b.y1;
-    Q.nruns = (uint32_t)nr;
-    for (int j = 0; j < kFMaxPieces; ++j) Q.run[j] = P.run[j];
     hot[i] = Q;
+    hits[i] = P;
   }
 }
 
@@ -291,20 +279,21 @@ struct WaveInfo {
   bool planar;
 };
 static __device__ __forceinline__ WaveInfo wave_info(const GatherArgs &A, const GridHeader &g,
-                                                     const FinePrep *__restrict__ prep,
-                                                     const FineHot *__restrict__ hot, uint32_t b0, uint32_t n,
+                                                     const FineHot *__restrict__ hot,
+                                                     const int4 *__restrict__ fbox, uint32_t b0, uint32_t n,
                                                      bool real) {
   const int lane = threadIdx.x & 31;
   WaveInfo W;
   bool valid = false, pl = true;
   int x0 = INT_MAX, x1 = INT_MIN, y0 = INT_MAX, y1 = INT_MIN, z0 = INT_MAX, z1 = INT_MIN;
   if ((uint32_t)lane < n) {
-    const FinePrep &P = prep[b0 + lane];
+    const FineHot &P = hot[b0 + lane];
     valid = real && P.nruns > 0;
     if (valid) {
-      x0 = P.bx0; x1 = P.bx1; y0 = P.by0; y1 = P.by1; z0 = P.bz0; z1 = P.bz1;
+      const int4 B = fbox[b0 + lane];
+      x0 = P.bx0; x1 = B.x; y0 = P.by0; y1 = P.by1; z0 = B.y; z1 = B.z;
     }
-    pl = hot[b0 + lane].planar != 0u;
+    pl = P.planar != 0u;
   }
   W.planar = __all_sync(kFull, pl);
   W.u.x0 = __reduce_min_sync(kFull, x0); W.u.x1 = __reduce_max_sync(kFull, x1);
@@ -334,7 +323,7 @@ static __device__ __forceinline__ WaveInfo wave_info(const GatherArgs &A, const 
 // per bucket (one warp each): items (runs of <= kFSub windows of
 // ceil(union / chunk)) and partial rows (items x wave size)
 __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
-                             const FinePrep *__restrict__ prep, const FineHot *__restrict__ hot,
+                             const FineHot *__restrict__ hot, const int4 *__restrict__ fbox,
                              uint32_t *__restrict__ items, uint32_t *__restrict__ prows, uint32_t cap64,
                              uint32_t cap48, uint32_t *__restrict__ nonempty) {
   const GridHeader g = *A.grid;
@@ -347,7 +336,7 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
     if (nhp && lane == 0) atomicAdd(nonempty, 1u);
     for (uint32_t w = 0; w * kFWave < nhp; ++w) {
       const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
-      const WaveInfo W = wave_info(A, g, prep, hot, h0 + w * kFWave, n, b + 1 < nb);
+      const WaveInfo W = wave_info(A, g, hot, fbox, h0 + w * kFWave, n, b + 1 < nb);
       const uint32_t chunk = W.planar ? cap48 : cap64;
       const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
@@ -362,8 +351,8 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
 }
 
 __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
-                            const uint32_t *__restrict__ hp_order, const FinePrep *__restrict__ prep,
-                            const FineHot *__restrict__ hot, const uint32_t *__restrict__ item_base,
+                            const uint32_t *__restrict__ hp_order, const FineHot *__restrict__ hot,
+                            const int4 *__restrict__ fbox, const uint32_t *__restrict__ item_base,
                             const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
                             uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48) {
   constexpr int kWarps = 4;  // 128 threads
@@ -379,7 +368,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
     for (uint32_t w = 0; w * kFWave < nhp; ++w) {
       const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
       const uint32_t lo = h0 + w * kFWave;
-      const WaveInfo W = wave_info(A, g, prep, hot, lo, n, b + 1 < nb);
+      const WaveInfo W = wave_info(A, g, hot, fbox, lo, n, b + 1 < nb);
       const uint32_t chunk = W.planar ? cap48 : cap64;
       const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
@@ -886,7 +875,7 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
             }
           }
           if (!__any_sync(kFull, rl != 0)) continue;
-          const Hit &Hs = T.prep[s_desc.hp_lo + k].h;  // full state: exact path only
+          const Hit &Hs = T.hits[s_desc.hp_lo + k];  // full state: exact path only
           PackedCounts<GMAX> cnt;
 #pragma unroll
           for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
@@ -1037,11 +1026,11 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   e = launch_bucket_start(s, skeys, A.H, nb, S.hp_start, sms);
   if (e != cudaSuccess) return e;
   // per hit point state in wave order (needed by the window sizing below)
-  k_fine_prep<<<fblocks(A.H, 128, sms, 8), 128, 0, s>>>(A, S.hp_order, static_cast<FinePrep *>(S.fprep),
-                                                        static_cast<FineHot *>(S.fhot));
+  k_fine_prep<<<fblocks(A.H, 128, sms, 8), 128, 0, s>>>(A, S.hp_order, static_cast<FineHot *>(S.fhot),
+                                                        S.fbox, static_cast<Hit *>(S.fhit));
   note_launches(1);
   k_fine_items<<<fblocks((unsigned long long)(nb + 1) * 32, 128, sms, 16), 128, 0, s>>>(
-      A, S.hp_start, nb, static_cast<const FinePrep *>(S.fprep), static_cast<const FineHot *>(S.fhot), S.items,
+      A, S.hp_start, nb, static_cast<const FineHot *>(S.fhot), S.fbox, S.items,
       S.chunks, cap64, cap48, S.nonempty);
   note_launches(1);
   e = launch_exclusive_scan(s, S.items, nb + 1, S.scan_tmp, S.item_base);
@@ -1052,7 +1041,7 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
                                 uint32_t cap64, uint32_t cap48) {
   k_fine_desc<<<fblocks((unsigned long long)nb * 32, 128, sms, 16), 128, 0, s>>>(
-      A, S.hp_start, nb, S.hp_order, static_cast<const FinePrep *>(S.fprep), static_cast<const FineHot *>(S.fhot),
+      A, S.hp_start, nb, S.hp_order, static_cast<const FineHot *>(S.fhot), S.fbox,
       S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48);
   note_launches(1);
   return cudaGetLastError();
@@ -1074,8 +1063,8 @@ static cudaError_t launch_fine_t(cudaStream_t s, const GatherArgs &A, const Fine
   return cudaGetLastError();
 }
 
-size_t fine_prep_bytes() { return sizeof(FinePrep); }
 size_t fine_hot_bytes() { return sizeof(FineHot); }
+size_t fine_hit_bytes() { return sizeof(Hit); }
 
 cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms) {
   const int G = A.na * A.ns;

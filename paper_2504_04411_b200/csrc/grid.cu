@@ -169,13 +169,32 @@ __global__ void __launch_bounds__(256)
     k_permute_packed(const uint32_t *__restrict__ order, uint32_t n, const float4 *__restrict__ pack,
                      float4 *__restrict__ rec0, float4 *__restrict__ rec1, float4 *__restrict__ rec2,
                      float4 *__restrict__ rec3) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const float4 *src = pack + 4 * (size_t)order[i];
-    const float4 q0 = src[0], q1 = src[1], q2 = src[2], q3 = src[3];
-    rec0[i] = q0;
-    rec1[i] = q1;
-    rec2[i] = q2;
-    rec3[i] = q3;
+  // U records per thread per round, all loads issued before the stores
+  // (random 64-B record reads: latency bound without the extra parallelism)
+  constexpr uint32_t U = 4;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    uint32_t o[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) o[u] = i0 + u * stride < n ? __ldg(&order[i0 + u * stride]) : 0u;
+    float4 q[U][4];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const float4 *src = pack + 4 * (size_t)o[u];
+      if (i0 + u * stride < n) {
+        q[u][0] = __ldg(&src[0]); q[u][1] = __ldg(&src[1]); q[u][2] = __ldg(&src[2]); q[u][3] = __ldg(&src[3]);
+      }
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const uint32_t i = i0 + u * stride;
+      if (i < n) {
+        __stcs(&rec0[i], q[u][0]);
+        __stcs(&rec1[i], q[u][1]);
+        __stcs(&rec2[i], q[u][2]);
+        __stcs(&rec3[i], q[u][3]);
+      }
+    }
   }
 }
 
