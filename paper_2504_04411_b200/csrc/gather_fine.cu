@@ -187,10 +187,29 @@ static_assert(sizeof(FineHot) % 16 == 0, "FineHot must be a multiple of 16 B (TM
 
 // Per hit point, once per gather, in wave order (position in hp_order): the
 // staged state, its fine box and the sorted-record range of each run.
-__global__ void k_fine_prep(const GatherArgs A, const uint32_t *__restrict__ hp_order,
-                            FineHot *__restrict__ hot, int4 *__restrict__ fbox, Hit *__restrict__ hits) {
+// Tiles of kPrepThreads hit points: the per-thread structs are assembled in
+// shared memory and written out as contiguous 16-B vectors (coalesced).
+constexpr int kPrepThreads = 128;
+constexpr size_t kPrepSmem = (size_t)kPrepThreads * (sizeof(FineHot) + sizeof(Hit));
+static_assert(sizeof(Hit) % 16 == 0, "Hit must be a multiple of 16 B");
+
+static __device__ __forceinline__ void copy_out16(const void *src, void *dst, uint32_t bytes) {
+  const int4 *s = static_cast<const int4 *>(src);
+  int4 *d = static_cast<int4 *>(dst);
+  for (uint32_t k = threadIdx.x; k < bytes / 16; k += blockDim.x) d[k] = s[k];
+}
+
+__global__ void __launch_bounds__(kPrepThreads)
+    k_fine_prep(const GatherArgs A, const uint32_t *__restrict__ hp_order, FineHot *__restrict__ hot,
+                int4 *__restrict__ fbox, Hit *__restrict__ hits) {
+  extern __shared__ __align__(16) unsigned char prep_smem[];
+  FineHot *s_hot = reinterpret_cast<FineHot *>(prep_smem);
+  Hit *s_hit = reinterpret_cast<Hit *>(prep_smem + (size_t)kPrepThreads * sizeof(FineHot));
   const GridHeader g = *A.grid;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.H; i += gridDim.x * blockDim.x) {
+  for (uint32_t t0 = blockIdx.x * kPrepThreads; t0 < A.H; t0 += gridDim.x * kPrepThreads) {
+    const uint32_t i = t0 + threadIdx.x;
+    const uint32_t nt = min((uint32_t)kPrepThreads, A.H - t0);
+    if (i < A.H) {
     const uint32_t h = hp_order[i];
     Hit P;
     make_hit(A, h, P);
@@ -220,8 +239,13 @@ __global__ void k_fine_prep(const GatherArgs A, const uint32_t *__restrict__ hp_
         r = make_uint2(A.cell_start[k0], A.cell_start[k1 + 1]);
       Q.run[j] = r;
     }
-    hot[i] = Q;
-    hits[i] = P;
+    s_hot[threadIdx.x] = Q;
+    s_hit[threadIdx.x] = P;
+    }
+    __syncthreads();
+    copy_out16(s_hot, hot + t0, nt * (uint32_t)sizeof(FineHot));
+    copy_out16(s_hit, hits + t0, nt * (uint32_t)sizeof(Hit));
+    __syncthreads();
   }
 }
 
@@ -1026,7 +1050,10 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   e = launch_bucket_start(s, skeys, A.H, nb, S.hp_start, sms);
   if (e != cudaSuccess) return e;
   // per hit point state in wave order (needed by the window sizing below)
-  k_fine_prep<<<fblocks(A.H, 128, sms, 8), 128, 0, s>>>(A, S.hp_order, static_cast<FineHot *>(S.fhot),
+  e = cudaFuncSetAttribute(k_fine_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem);
+  if (e != cudaSuccess) return e;
+  k_fine_prep<<<fblocks(A.H, kPrepThreads, sms, 8), kPrepThreads, kPrepSmem, s>>>(
+      A, S.hp_order, static_cast<FineHot *>(S.fhot),
                                                         S.fbox, static_cast<Hit *>(S.fhit));
   note_launches(1);
   k_fine_items<<<fblocks((unsigned long long)(nb + 1) * 32, 128, sms, 16), 128, 0, s>>>(
