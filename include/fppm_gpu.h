@@ -321,6 +321,20 @@ int fppm_gpu_get_hitpoints(fppm_gpu_ctx *ctx, fppm_hitpoints *out, double *emitt
 /* Film::add_iteration of this iteration's estimate: emitted + flux / (pi r^2 J)
  * of the gather_test / iterate that followed trace_eye. */
 int fppm_gpu_film_add(fppm_gpu_ctx *ctx);
+/* One whole VCM+ iteration (Renderer::step with Algorithm::vcm_plus,
+ * integrator.cpp:150-228, 236-301, 492-653) on the device: light sub-paths
+ * (light_paths = J = samples_per_iteration, depth max_depth - 1, eta_vm of
+ * the max live radius) and their camera splats; eye sub-paths with MIS
+ * partials, emitter hits, next-event estimation and connections to light
+ * sub-path px % J; kernel estimation at every rough eye vertex (the first one
+ * accumulates into the pixel's region and is F-tested, the others only add
+ * their merge sums); the estimate is added to the film.  Replaces the hit
+ * points with the pixels' primary vertices.  Needs a vcm_plus context with
+ * max_depth <= 16, set_scene and set_camera.  *n_photons (nullable) receives
+ * the light-vertex count.
+ * Replaces: Renderer::step for vcm_plus (integrator.cpp:150-228). */
+int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t light_paths,
+                        uint32_t max_depth, uint32_t *n_photons);
 /* Film::image(): per-pixel mean over the added iterations ([npix][3] host). */
 int fppm_gpu_film_mean(fppm_gpu_ctx *ctx, double *rgb, uint64_t *iterations);
 

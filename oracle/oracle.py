@@ -148,6 +148,10 @@ class Oracle:
                                                        C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64,
                                                        C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
                                                        C.c_void_p, C.c_void_p, _dp])
+            self._render_vcm = fn("render_vcm_plus", C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, C.c_int,
+                                                               C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64,
+                                                               C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
+                                                               C.c_void_p, C.c_void_p, _dp])
             self._brad = fn("bounding_radius", C.c_double, [C.c_void_p])
             self._sparse = fn("scene_parse", C.c_void_p, [C.c_char_p, C.c_char_p, C.c_size_t])
             self._sexport = fn("scene_export", None, [C.c_void_p] + [C.c_void_p] * 10)
@@ -362,14 +366,16 @@ def _scene_eye(self, cam, seed, iteration, max_depth):
 
 
 def _scene_render(self, cam, seed, iterations, max_depth, light_paths, r0_frac=0.002, n_annuli=2, n_sectors=6,
-                  alpha_f=0.01, threads=0):
-    """The reference's render() with Algorithm::fppm: (film mean, last radii, seconds)."""
+                  alpha_f=0.01, threads=0, algorithm="fppm"):
+    """The reference's render() with Algorithm::fppm (or vcm_plus): (film mean,
+    last radii, seconds)."""
     n = cam.width * cam.height
     film = np.zeros((n, 3))
     radius = np.zeros(n)
     secs = C.c_double()
     c9 = _cam9(cam)
-    rc = self.o._render(self.h, c9.ctypes.data_as(_dp), cam.vfov_deg, cam.width, cam.height, seed, iterations,
+    fn = {"fppm": self.o._render, "vcm_plus": self.o._render_vcm}[algorithm]
+    rc = fn(self.h, c9.ctypes.data_as(_dp), cam.vfov_deg, cam.width, cam.height, seed, iterations,
                         max_depth, light_paths, r0_frac, n_annuli, n_sectors, alpha_f, threads,
                         film.ctypes.data, radius.ctypes.data, C.byref(secs))
     if rc:
@@ -379,6 +385,7 @@ def _scene_render(self, cam, seed, iterations, max_depth, light_paths, r0_frac=0
 
 _Scene.eye_pass = _scene_eye
 _Scene.render_fppm = _scene_render
+_Scene.render_vcm_plus = lambda self, *a, **k: _scene_render(self, *a, algorithm="vcm_plus", **k)
 _Scene.bounding_radius = lambda self: self.o._brad(self.h)
 
 

@@ -692,15 +692,15 @@ void ref_eye_pass(void* sp, const double* cam9, double vfov, int w, int h, uint6
 
 // The reference's own render() (integrator.cpp:669-...) with the FPPM
 // algorithm: film mean [npix][3] and the last iteration's radii [npix].
-int ref_render_fppm(void* sp, const double* cam9, double vfov, int w, int h, uint64_t seed, uint64_t iterations,
-                    uint32_t max_depth, uint64_t light_paths, double r0_frac, int na, int ns, double alpha_f,
-                    int threads, double* film_mean, double* radius, double* seconds) {
+static int render_algo(Algorithm algo, void* sp, const double* cam9, double vfov, int w, int h, uint64_t seed,
+                       uint64_t iterations, uint32_t max_depth, uint64_t light_paths, double r0_frac, int na, int ns,
+                       double alpha_f, int threads, double* film_mean, double* radius, double* seconds) {
   RefScene* rs = static_cast<RefScene*>(sp);
   Scene scene = rs->scene;
   scene.has_camera = true;
   scene.camera = make_cam(cam9, vfov, w, h);
   IntegratorConfig cfg;
-  cfg.algorithm = Algorithm::fppm;
+  cfg.algorithm = algo;
   cfg.iterations = iterations;
   cfg.seed = seed;
   cfg.max_depth = max_depth;
@@ -728,6 +728,21 @@ int ref_render_fppm(void* sp, const double* cam9, double vfov, int w, int h, uin
     return 1;
   }
   return 0;
+}
+
+int ref_render_fppm(void* sp, const double* cam9, double vfov, int w, int h, uint64_t seed, uint64_t iterations,
+                    uint32_t max_depth, uint64_t light_paths, double r0_frac, int na, int ns, double alpha_f,
+                    int threads, double* film_mean, double* radius, double* seconds) {
+  return render_algo(Algorithm::fppm, sp, cam9, vfov, w, h, seed, iterations, max_depth, light_paths, r0_frac, na,
+                     ns, alpha_f, threads, film_mean, radius, seconds);
+}
+
+// The same with Algorithm::vcm_plus (bidirectional, tested per-pixel radii).
+int ref_render_vcm_plus(void* sp, const double* cam9, double vfov, int w, int h, uint64_t seed,
+                        uint64_t iterations, uint32_t max_depth, uint64_t light_paths, double r0_frac, int na,
+                        int ns, double alpha_f, int threads, double* film_mean, double* radius, double* seconds) {
+  return render_algo(Algorithm::vcm_plus, sp, cam9, vfov, w, h, seed, iterations, max_depth, light_paths, r0_frac,
+                     na, ns, alpha_f, threads, film_mean, radius, seconds);
 }
 
 // bounding_radius (scene_geometry.cpp:341-362): the initial radius is

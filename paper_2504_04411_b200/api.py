@@ -344,6 +344,18 @@ class FppmContext:
         self.film_add()
         return o, sm
 
+    def render_vcm_iteration(self, seed: int, iteration: int, light_paths: int, max_depth: Optional[int] = None):
+        """One whole VCM+ iteration of Renderer::step (Algorithm::vcm_plus) on the
+        device: light sub-paths + camera splats, eye sub-paths with emitter
+        hits, next-event estimation and connections, merges at every rough eye
+        vertex (the primary one tested per pixel), film
+        (fppm_gpu_render_vcm)."""
+        n = C.c_uint32()
+        self._check(self._lib.fppm_gpu_render_vcm(self._h, seed, iteration, light_paths,
+                                                  max_depth or self.config.max_depth, C.byref(n)))
+        self.N = n.value
+        self.H = self.camera.width * self.camera.height
+
     def get_photon_mis(self) -> dict:
         n = self.N
         o = dict(d_vcm=np.zeros(n), d_vm=np.zeros(n), cont=np.zeros(n))

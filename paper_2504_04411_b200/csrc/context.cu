@@ -67,6 +67,20 @@ struct fppm_gpu_ctx {
   uint32_t *t_depth = nullptr, *t_count = nullptr, *t_base = nullptr, *t_scan = nullptr;
   double *t_mis = nullptr;
   unsigned long long t_slot_cap = 0, t_path_cap = 0;
+  // VCM+ bidirectional remainder: fp64 light vertices in the trace slots,
+  // splats, secondary merge vertices and their delta rows
+  bool bidir_trace = false;
+  double last_eta_light = 0.0;
+  double *b_pos = nullptr, *b_sn = nullptr, *b_wi = nullptr, *b_thr = nullptr, *b_mis = nullptr;
+  int *b_mat = nullptr;
+  unsigned long long b_slot_cap = 0;
+  double3 *d_splat = nullptr;
+  double3 *q_pos = nullptr, *q_nrm = nullptr, *q_wo = nullptr, *q_thr = nullptr, *q_alb = nullptr, *q_K = nullptr;
+  uint32_t *q_eye = nullptr;
+  uint8_t *q_gathered = nullptr;
+  double *q_radius = nullptr, *q_rows = nullptr;
+  double2 *q_mis = nullptr;
+  unsigned long long q_cap = 0, q_rows_cap = 0;
 
   // VCM+ merge stage inputs
   double2 *d_eye_mis = nullptr;                                   // [H] {d_vcm, d_vm}
@@ -486,6 +500,13 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
   if (ctx->d_eye_mis) cudaFree(ctx->d_eye_mis);
   if (ctx->d_emit) cudaFree(ctx->d_emit);
+  {
+    void *bq[] = {ctx->b_pos, ctx->b_sn, ctx->b_wi, ctx->b_thr, ctx->b_mis, ctx->b_mat, ctx->d_splat,
+                  ctx->q_pos, ctx->q_nrm, ctx->q_wo, ctx->q_thr, ctx->q_alb, ctx->q_K, ctx->q_eye,
+                  ctx->q_gathered, ctx->q_radius, ctx->q_rows, ctx->q_mis};
+    for (void *p : bq)
+      if (p) cudaFree(p);
+  }
   if (ctx->d_rows) cudaFree(ctx->d_rows);
   for (void *p : ctx->c5_mem)
     if (p) cudaFree(p);
@@ -1464,6 +1485,24 @@ int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration,
   T.v_depth = ctx->t_depth;
   T.v_mis = ctx->cfg.vcm_plus ? ctx->t_mis : nullptr;
   T.count = ctx->t_count;
+  T.b_pos = T.b_sn = T.b_wi = T.b_thr = T.b_mis = nullptr;
+  T.b_mat = nullptr;
+  ctx->last_eta_light = eta;
+  if (ctx->bidir_trace) {
+    if (slots > ctx->b_slot_cap) {
+      void *bp[] = {ctx->b_pos, ctx->b_sn, ctx->b_wi, ctx->b_thr, ctx->b_mis, ctx->b_mat};
+      FPPM_CUDA_OK(cudaStreamSynchronize(s));
+      for (void *p : bp)
+        if (p) cudaFree(p);
+      const unsigned long long cap = std::max<unsigned long long>(slots, 1024);
+      FPPM_CUDA_OK(dalloc(&ctx->b_pos, 3 * cap)); FPPM_CUDA_OK(dalloc(&ctx->b_sn, 3 * cap));
+      FPPM_CUDA_OK(dalloc(&ctx->b_wi, 3 * cap)); FPPM_CUDA_OK(dalloc(&ctx->b_thr, 3 * cap));
+      FPPM_CUDA_OK(dalloc(&ctx->b_mis, 3 * cap)); FPPM_CUDA_OK(dalloc(&ctx->b_mat, cap));
+      ctx->b_slot_cap = cap;
+    }
+    T.b_pos = ctx->b_pos; T.b_sn = ctx->b_sn; T.b_wi = ctx->b_wi; T.b_thr = ctx->b_thr;
+    T.b_mis = ctx->b_mis; T.b_mat = ctx->b_mat;
+  }
   FPPM_CUDA_OK(cudaMemsetAsync(ctx->t_count + n_paths, 0, sizeof(uint32_t), s));
   if (!ctx->t_ctr) FPPM_CUDA_OK(dalloc(&ctx->t_ctr, 1));
   T.path_counter = ctx->t_ctr;
@@ -1548,6 +1587,115 @@ int fppm_gpu_trace_eye(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration) {
   E.gathered = ctx->d_gathered;
   FPPM_CUDA_OK(launch_trace_eye(ctx->stream, E, ctx->scene_mem[8], ctx->sms));
   return finish_hitpoints(ctx, E.npix, true);
+}
+
+
+// ------------------------------------------------------------------ VCM+ render
+// One Renderer::step for vcm_plus (integrator.cpp:150-228, 492-653): light
+// sub-paths with fp64 light vertices and their camera splats, eye sub-paths
+// (emitter hits, next-event estimation, connections to light sub-path
+// px % J), the primary rough vertex of every pixel gathered + tested as its
+// region, the other rough vertices gathered as merge queries, film.
+int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t light_paths,
+                        uint32_t max_depth, uint32_t *n_photons) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->cfg.vcm_plus) return fail(ctx, FPPM_ERR_STATE, "render_vcm needs a vcm_plus context");
+  if (!ctx->has_scene || !ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "render_vcm needs set_scene and set_camera");
+  if (max_depth < 1 || max_depth > kMaxBidirDepth)
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "render_vcm: max_depth must be in [1, 16]");
+  if (light_paths == 0) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "render_vcm: light_paths must be >= 1");
+  if ((uint64_t)light_paths != ctx->cfg.samples_per_iteration)
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "render_vcm: light_paths must equal samples_per_iteration (J)");
+  if (max_depth != ctx->cfg.max_depth)
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "render_vcm: max_depth must equal the context's max_depth");
+  cudaStream_t s = ctx->stream;
+  const uint32_t npix = (uint32_t)((uint64_t)ctx->cam.width * ctx->cam.height);
+  const uint32_t nq = max_depth > 1 ? max_depth - 1 : 1;
+  const unsigned long long nqt = (unsigned long long)npix * nq;
+  const uint32_t stride = (uint32_t)(ctx->G + 2 * ctx->G * ctx->C + 3);
+  if (nqt > 0xffffffffull) return fail(ctx, FPPM_ERR_CAPACITY, "render_vcm: too many merge vertices");
+  if (nqt > ctx->q_cap) {
+    void *qp[] = {ctx->q_pos, ctx->q_nrm, ctx->q_wo, ctx->q_thr, ctx->q_alb, ctx->q_K, ctx->q_eye,
+                  ctx->q_gathered, ctx->q_radius, ctx->q_mis, ctx->d_splat};
+    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    for (void *p : qp)
+      if (p) cudaFree(p);
+    FPPM_CUDA_OK(dalloc(&ctx->q_pos, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_nrm, nqt));
+    FPPM_CUDA_OK(dalloc(&ctx->q_wo, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_thr, nqt));
+    FPPM_CUDA_OK(dalloc(&ctx->q_alb, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_K, nqt));
+    FPPM_CUDA_OK(dalloc(&ctx->q_eye, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_gathered, nqt));
+    FPPM_CUDA_OK(dalloc(&ctx->q_radius, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_mis, nqt));
+    FPPM_CUDA_OK(dalloc(&ctx->d_splat, std::max<uint32_t>(npix, 1)));
+    ctx->q_cap = nqt;
+  }
+  if (nqt * stride > ctx->q_rows_cap) {
+    if (ctx->q_rows) cudaFree(ctx->q_rows);
+    ctx->q_rows = nullptr;
+    FPPM_CUDA_OK(dalloc(&ctx->q_rows, nqt * stride));
+    ctx->q_rows_cap = nqt * stride;
+  }
+  // the pixels are the regions (integrator.cpp:136-137): fresh regions on a new frame size
+  if (ctx->H != npix) {
+    ctx->H = npix;
+    if (int rc0 = fppm_gpu_reset_regions(ctx)) return rc0;
+  }
+  // light phase with fp64 light vertices (r_max of the live radii, integrator.cpp:159-175)
+  ctx->bidir_trace = true;
+  int rc = fppm_gpu_trace_photons(ctx, seed, iteration, light_paths, max_depth, 0.0, n_photons);
+  ctx->bidir_trace = false;
+  if (rc) return rc;
+  BidirArgs B;
+  std::memset(&B, 0, sizeof(B));
+  B.sc = ctx->scene;
+  B.cam = ctx->cam;
+  B.seed = seed;
+  B.iteration = iteration;
+  B.max_depth = max_depth;
+  B.npix = npix;
+  B.n_paths = light_paths;
+  B.light_depth = max_depth - 1;
+  B.n_vm = ctx->cfg.mis_n_vm;
+  B.beta = ctx->cfg.mis_beta > 0.0 ? ctx->cfg.mis_beta : 1.0;
+  B.eta_light = ctx->last_eta_light;
+  B.radius = ctx->d_radius;
+  B.l_pos = ctx->b_pos; B.l_sn = ctx->b_sn; B.l_wi = ctx->b_wi; B.l_thr = ctx->b_thr; B.l_mis = ctx->b_mis;
+  B.l_mat = ctx->b_mat; B.l_depth = ctx->t_depth; B.l_count = ctx->t_count;
+  B.direct = ctx->d_emit;
+  B.pos = ctx->d_pos; B.nrm = ctx->d_nrm; B.wo = ctx->d_wo; B.thr = ctx->d_thr; B.alb = ctx->d_alb;
+  B.eye_depth = ctx->d_eye; B.gathered = ctx->d_gathered; B.eye_mis = ctx->d_eye_mis;
+  B.q_pos = ctx->q_pos; B.q_nrm = ctx->q_nrm; B.q_wo = ctx->q_wo; B.q_thr = ctx->q_thr; B.q_alb = ctx->q_alb;
+  B.q_eye = ctx->q_eye; B.q_gathered = ctx->q_gathered; B.q_radius = ctx->q_radius; B.q_mis = ctx->q_mis;
+  B.splat = ctx->d_splat;
+  if (light_paths > 0 && B.light_depth > 0) {
+    FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_splat, 0, sizeof(double3) * npix, s));
+    FPPM_CUDA_OK(launch_light_splat(s, B, ctx->scene_mem[8], ctx->sms));
+  } else {
+    FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_splat, 0, sizeof(double3) * npix, s));
+    B.l_count = ctx->t_count;
+  }
+  FPPM_CUDA_OK(launch_eye_bidir(s, B, ctx->scene_mem[8], ctx->sms));
+  if ((rc = finish_hitpoints(ctx, npix, true))) return rc;
+  FPPM_CUDA_OK(launch_hit_weights(s, ctx->q_nrm, ctx->q_wo, ctx->q_thr, ctx->q_alb, (uint32_t)nqt, ctx->q_K));
+  // primary vertices: grid (cell = r_max) + VCM+ gather / F-test of the regions
+  if ((rc = fppm_gpu_iterate(ctx, iteration, nullptr, nullptr))) return rc;
+  // secondary vertices: merge queries with the pixel's radius, delta rows
+  GatherArgs Q;
+  fill_gather_args(ctx, iteration, Q);
+  Q.pos = ctx->q_pos; Q.nrm = ctx->q_nrm; Q.K = ctx->q_K; Q.eye_depth = ctx->q_eye; Q.gathered = ctx->q_gathered;
+  Q.radius = ctx->q_radius; Q.wo = ctx->q_wo; Q.alb = ctx->q_alb; Q.eye_mis = ctx->q_mis;
+  Q.H = (uint32_t)nqt;
+  Q.delta_out = ctx->q_rows;
+  Q.o_gather_r = Q.o_stat = Q.o_crit = Q.o_flux = nullptr;
+  Q.o_flags = nullptr;
+  Q.o_radiance = nullptr;
+  Q.o_accepted = nullptr;
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned int), s));
+  FPPM_CUDA_OK(launch_gather_test(s, Q, ctx->C, ctx->sms));
+  FPPM_CUDA_OK(launch_film_vcm(s, npix, nq, ctx->d_emit, ctx->d_gathered, ctx->o_flux, ctx->o_gather_r,
+                               ctx->q_rows, stride, ctx->q_gathered, ctx->q_radius, ctx->d_splat,
+                               (double)light_paths, ctx->d_film, ctx->sms));
+  ctx->film_iters++;
+  return FPPM_OK;
 }
 
 int fppm_gpu_get_hitpoints(fppm_gpu_ctx *ctx, fppm_hitpoints *o, double *emitted) {

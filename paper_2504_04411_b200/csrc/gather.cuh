@@ -258,6 +258,10 @@ struct TraceArgs {
   double *v_mis;                        // [.][3] d_vcm, d_vm, cont (nullable)
   uint32_t *count;                      // [n_paths]
   uint32_t *path_counter;               // work queue (reset by launch_trace)
+  // bidirectional (VCM+) light vertices in fp64, same slots (nullable):
+  // LightVertex position, shading normal, wi, throughput, {d_vcm, d_vc, d_vm}
+  double *b_pos, *b_sn, *b_wi, *b_thr, *b_mis;
+  int *b_mat;
 };
 struct CamD {  // CameraFrame (path.hpp:93-98), built on the host (make_camera_frame)
   double pos[3], fwd[3], right[3], up[3];
@@ -274,6 +278,45 @@ struct EyeArgs {
   uint8_t *gathered;
 };
 cudaError_t launch_trace_eye(cudaStream_t s, const EyeArgs &E, const void *prep, int sms);
+
+// VCM+ bidirectional remainder (trace.cu): eye sub-paths with MIS partials,
+// emitter hits, next-event estimation, connections to the pixel's light
+// sub-path, merge vertices for the gathers; light-vertex splats to the camera.
+constexpr uint32_t kMaxBidirDepth = 16;
+struct BidirArgs {
+  TraceScene sc;
+  CamD cam;
+  unsigned long long seed, iteration;
+  uint32_t max_depth, npix, n_paths, light_depth;
+  int n_vm;
+  double beta, eta_light;          // light sub-paths' eta_vm (r_max; integrator.cpp:171-174)
+  const double *radius;            // [npix] region radius before this iteration's update
+  // light vertices (TraceArgs::b_*), per-path counts
+  const double *l_pos, *l_sn, *l_wi, *l_thr, *l_mis;
+  const int *l_mat;
+  const uint32_t *l_depth;  // TraceArgs::v_depth slots (LightVertex::depth)
+  const uint32_t *l_count;
+  // outputs: direct estimate per pixel, primary merge vertex (the region's
+  // hit point), secondary merge vertices [npix][max_depth - 1]
+  double3 *direct;
+  double3 *pos, *nrm, *wo, *thr, *alb;
+  uint32_t *eye_depth;
+  uint8_t *gathered;
+  double2 *eye_mis;
+  double3 *q_pos, *q_nrm, *q_wo, *q_thr, *q_alb;
+  uint32_t *q_eye;
+  uint8_t *q_gathered;
+  double *q_radius;
+  double2 *q_mis;
+  double3 *splat;  // light-to-camera splats (atomic adds)
+};
+cudaError_t launch_eye_bidir(cudaStream_t s, const BidirArgs &B, const void *prep, int sms);
+cudaError_t launch_light_splat(cudaStream_t s, const BidirArgs &B, const void *prep, int sms);
+// film for VCM+: est = direct + (flux + secondary merge sums) / (pi r^2 J) + splats
+cudaError_t launch_film_vcm(cudaStream_t s, uint32_t npix, uint32_t nq_per_px, const double3 *direct,
+                            const uint8_t *gathered, const double *flux, const double *gather_r,
+                            const double *q_rows, uint32_t q_stride, const uint8_t *q_gathered,
+                            const double *q_radius, const double3 *splat, double J, double3 *film, int sms);
 // op 0: film += estimate (J = samples per iteration); op 1: mean_out = film / J (J = iterations)
 cudaError_t launch_film(cudaStream_t s, int op, uint32_t npix, const double3 *emitted, const uint8_t *gathered,
                         const double *flux, const double *gather_r, double J, double3 *film, double *mean_out,

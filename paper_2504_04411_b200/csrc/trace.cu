@@ -302,6 +302,64 @@ __device__ __forceinline__ bool start_path(const TraceArgs &A, const PrimD *P, P
   return true;
 }
 
+// Bsdf::sample (bsdf.cpp:94-182) for the analytic materials: Lambertian
+// (cosine lobe), mirror, dielectric (Fresnel pick).  wi is the Bsdf's stored
+// direction (toward the previous vertex), cos_o = dot(wi, sn).  False: no
+// sample (the path ends).
+__device__ __forceinline__ bool bsdf_sample(const TraceScene &sc, int mk, int mat, DVec sn, DVec wi, bool front,
+                                            double cos_o, Rng &rng, DVec &ndir, double &s_cos, double &s_pdf,
+                                            double &s_rev, bool &s_delta) {
+  if (mk == 2) {  // dielectric (bsdf.cpp:147-180)
+    const double eta = front ? sc.mat_ior[mat] : dd(1.0, sc.mat_ior[mat]);
+    const double ci = cos_o;
+    if (ci <= 0.0) return false;
+    const double sin2_t = dd(ds(1.0, dm(ci, ci)), dm(eta, eta));
+    double frs;
+    if (sin2_t >= 1.0) {
+      frs = 1.0;
+    } else {
+      const double ct = __dsqrt_rn(ds(1.0, sin2_t));
+      const double rs = dd(ds(ci, dm(eta, ct)), da(ci, dm(eta, ct)));
+      const double rp = dd(ds(dm(eta, ci), ct), da(dm(eta, ci), ct));
+      frs = dm(0.5, da(dm(rs, rs), dm(rp, rp)));
+    }
+    s_delta = true;
+    if (rng.next() < frs) {
+      ndir = reflect(wi, sn);
+      s_cos = dot(ndir, sn);
+      s_pdf = frs;
+      s_rev = frs;
+    } else {
+      const double x = ds(1.0, sin2_t);
+      const double ct = __dsqrt_rn(x > 0.0 ? x : 0.0);
+      ndir = normalize(add(mul(wi, dd(-1.0, eta)), mul(sn, ds(dd(ci, eta), ct))));
+      s_cos = ct;
+      s_pdf = ds(1.0, frs);
+      s_rev = ds(1.0, frs);
+    }
+  } else {
+    if (cos_o <= 0.0) return false;
+    if (mk == 0) {  // lambertian
+      const Frame sf = make_frame(sn);
+      const double a2 = rng.next(), a1 = rng.next();  // right-to-left arguments
+      const DVec l = sample_cosine_hemisphere(a1, a2);
+      ndir = to_world(sf, l);
+      s_cos = l.z;
+      if (s_cos <= 0.0) return false;
+      s_pdf = cos_pdf(s_cos);
+      s_rev = cos_pdf(cos_o);
+      s_delta = false;
+    } else {  // mirror
+      ndir = reflect(wi, sn);
+      s_cos = dot(ndir, sn);
+      s_pdf = 1.0;
+      s_rev = 1.0;
+      s_delta = true;
+    }
+  }
+  return true;
+}
+
 // One segment of trace_light_subpath's loop (path.cpp:409-447).  False: the
 // path ended.
 __device__ __forceinline__ bool bounce(const TraceArgs &A, const PrimD *P, int np, PathState &s, double vcf,
@@ -334,6 +392,14 @@ __device__ __forceinline__ bool bounce(const TraceArgs &A, const PrimD *P, int n
       A.v_mis[o3 + 1] = s.mis.d_vm;
       A.v_mis[o3 + 2] = cont;
     }
+    if (A.b_pos) {  // fp64 LightVertex for connections and camera splats
+      A.b_pos[o3] = h.point.x; A.b_pos[o3 + 1] = h.point.y; A.b_pos[o3 + 2] = h.point.z;
+      A.b_sn[o3] = h.sn.x; A.b_sn[o3 + 1] = h.sn.y; A.b_sn[o3 + 2] = h.sn.z;
+      A.b_wi[o3] = wi.x; A.b_wi[o3 + 1] = wi.y; A.b_wi[o3 + 2] = wi.z;
+      A.b_thr[o3] = s.t0; A.b_thr[o3 + 1] = s.t1; A.b_thr[o3 + 2] = s.t2;
+      A.b_mis[o3] = s.mis.d_vcm; A.b_mis[o3 + 1] = s.mis.d_vc; A.b_mis[o3 + 2] = s.mis.d_vm;
+      A.b_mat[slot] = h.mat;
+    }
     ++s.nv;
   }
   if (s.depth == A.light_depth) return false;
@@ -342,54 +408,8 @@ __device__ __forceinline__ bool bounce(const TraceArgs &A, const PrimD *P, int n
   double s_cos, s_pdf, s_rev;
   bool s_delta;
   const double *rgb = sc.mat_rgb + 3 * (size_t)h.mat;
-  if (mk == 2) {  // dielectric (bsdf.cpp:147-180)
-    const double eta = h.front ? sc.mat_ior[h.mat] : dd(1.0, sc.mat_ior[h.mat]);
-    const double ci = cos_o;
-    if (ci <= 0.0) return false;
-    const double sin2_t = dd(ds(1.0, dm(ci, ci)), dm(eta, eta));
-    double frs;
-    if (sin2_t >= 1.0) {
-      frs = 1.0;
-    } else {
-      const double ct = __dsqrt_rn(ds(1.0, sin2_t));
-      const double rs = dd(ds(ci, dm(eta, ct)), da(ci, dm(eta, ct)));
-      const double rp = dd(ds(dm(eta, ci), ct), da(dm(eta, ci), ct));
-      frs = dm(0.5, da(dm(rs, rs), dm(rp, rp)));
-    }
-    s_delta = true;
-    if (s.rng.next() < frs) {
-      ndir = reflect(wi, h.sn);
-      s_cos = dot(ndir, h.sn);
-      s_pdf = frs;
-      s_rev = frs;
-    } else {
-      const double x = ds(1.0, sin2_t);
-      const double ct = __dsqrt_rn(x > 0.0 ? x : 0.0);
-      ndir = normalize(add(mul(wi, dd(-1.0, eta)), mul(h.sn, ds(dd(ci, eta), ct))));
-      s_cos = ct;
-      s_pdf = ds(1.0, frs);
-      s_rev = ds(1.0, frs);
-    }
-  } else {
-    if (cos_o <= 0.0) return false;
-    if (mk == 0) {  // lambertian
-      const Frame sf = make_frame(h.sn);
-      const double a2 = s.rng.next(), a1 = s.rng.next();  // right-to-left arguments
-      const DVec l = sample_cosine_hemisphere(a1, a2);
-      ndir = to_world(sf, l);
-      s_cos = l.z;
-      if (s_cos <= 0.0) return false;
-      s_pdf = cos_pdf(s_cos);
-      s_rev = cos_pdf(cos_o);
-      s_delta = false;
-    } else {  // mirror
-      ndir = reflect(wi, h.sn);
-      s_cos = dot(ndir, h.sn);
-      s_pdf = 1.0;
-      s_rev = 1.0;
-      s_delta = true;
-    }
-  }
+  if (!bsdf_sample(sc, mk, h.mat, h.sn, wi, h.front, cos_o, s.rng, ndir, s_cos, s_pdf, s_rev, s_delta))
+    return false;
   const double w0 = rgb[0], w1 = rgb[1], w2 = rgb[2];
   if (s_pdf <= 0.0 || (w0 == 0 && w1 == 0 && w2 == 0)) return false;
   double q = 1.0;
@@ -690,6 +710,465 @@ cudaError_t launch_film(cudaStream_t s, int op, uint32_t npix, const double3 *em
     k_film_add<<<blocks, 256, 0, s>>>(npix, emitted, gathered, flux, gather_r, J, film);
   else
     k_film_mean<<<blocks, 256, 0, s>>>(npix, film, J, mean_out);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------- VCM+ bidirectional remainder
+// Renderer::pixel_bidir (integrator.cpp:492-653) for vcm_plus and the light
+// sub-paths' camera connections (light_phase / camera_connect,
+// integrator.cpp:236-301), restated in fp64 without FMA in the reference's
+// operation order.  The merges themselves run on the gather kernels: the
+// primary rough vertex becomes the pixel's region hit point (tested,
+// integrator.cpp:596-602), the others are merge queries gathered without a
+// region (the same kernel in delta-row mode).
+
+// any hit in (tmin, tmax): occluded (scene_geometry.cpp:308-318)
+__device__ __forceinline__ bool occluded(const PrimD *P, int np, DVec a, DVec b) {
+  const DVec d = sub(b, a);
+  const double dist = __dsqrt_rn(dot(d, d));
+  if (dist == 0.0) return false;
+  const DVec dir = mul(d, dd(1.0, dist));
+  const double tmin = dm(1e-6, dist), tmax = dm(ds(1.0, 1e-6), dist);  // kShadowEps (scene.hpp:121)
+  for (int i = 0; i < np; ++i) {
+    double t;
+    const bool ok = P[i].kind == 0 ? hit_sphere(P[i], a, dir, tmin, tmax, t) : hit_quad(P[i], a, dir, tmin, tmax, t);
+    if (ok) return true;
+  }
+  return false;
+}
+
+// Lambertian Bsdf::eval (bsdf.cpp:53-63): f = albedo / pi when cos_o > 0 and
+// cos_i > 0, with the forward / reverse cosine pdfs; black otherwise (mirror
+// and dielectric have no non-delta lobe).
+struct Eval {
+  double f0, f1, f2, pf, pr;
+  bool black;
+};
+__device__ __forceinline__ Eval bsdf_eval(const TraceScene &sc, int mat, DVec sn, double cos_o, DVec wi) {
+  Eval e{0, 0, 0, 0, 0, true};
+  const double cos_i = dot(wi, sn);
+  if (cos_o <= 0.0 || cos_i <= 0.0) return e;
+  if (sc.mat_kind[mat] != 0) return e;
+  const double *a = sc.mat_rgb + 3 * (size_t)mat;
+  e.pf = cos_pdf(cos_i);
+  e.pr = cos_pdf(cos_o);
+  e.f0 = dm(a[0], kInvPi);
+  e.f1 = dm(a[1], kInvPi);
+  e.f2 = dm(a[2], kInvPi);
+  e.black = e.f0 == 0 && e.f1 == 0 && e.f2 == 0;
+  return e;
+}
+
+struct MisC {  // MisContext (path.hpp:30-36) with the factors hoisted
+  double beta, vmf, vcf;
+};
+__device__ __forceinline__ MisC mis_ctx(double beta, double eta) {
+  MisC c;
+  c.beta = beta;
+  c.vmf = eta > 0.0 ? mpow(beta, eta) : 0.0;           // vm_factor (path.cpp:19-21)
+  c.vcf = eta > 0.0 ? mpow(beta, dd(1.0, eta)) : 0.0;  // vc_factor (path.cpp:22-24)
+  return c;
+}
+
+// Eye vertex of trace_eye_subpath (path.cpp:337-386)
+struct EyeV {
+  DVec pos, sn, gn, wo;
+  double t0, t1, t2;
+  Mis mis;
+  int mat, emitter;
+  uint32_t depth;
+  bool delta, front;
+};
+
+__global__ void __launch_bounds__(128) k_eye_bidir(const BidirArgs B, const PrimD *__restrict__ prims) {
+  __shared__ PrimD P[kMaxTracePrims];
+  const TraceScene &sc = B.sc;
+  const int np = sc.n_prim;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) P[i] = prims[i];
+  __syncthreads();
+  const CamD &cam = B.cam;
+  const DVec fwd = dv(cam.fwd[0], cam.fwd[1], cam.fwd[2]);
+  const uint32_t nq = B.max_depth > 1 ? B.max_depth - 1 : 1;
+  const int n_emit = sc.n_emit;
+  const double pick_prob = n_emit ? dd(1.0, (double)n_emit) : 0.0;
+  EyeV V[kMaxBidirDepth];
+  for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < B.npix; px += gridDim.x * blockDim.x) {
+    Rng rng(B.seed, B.iteration, px, 1ull /* kEyeStream */);
+    const double r = B.radius[px];
+    const double eta = dm(dm(dm((double)B.n_vm, kPi), r), r);  // n_vm * kPi * r * r (integrator.cpp:503)
+    const MisC ctx = mis_ctx(B.beta, eta);
+    const double sx = da((double)(px % (uint32_t)cam.width), rng.next());
+    const double sy = da((double)(px / (uint32_t)cam.width), rng.next());
+    DVec dir = normalize(add(add(mul(fwd, cam.plane_dist),
+                                 mul(dv(cam.right[0], cam.right[1], cam.right[2]),
+                                     ds(sx, dm(0.5, (double)cam.width)))),
+                             mul(dv(cam.up[0], cam.up[1], cam.up[2]), ds(dm(0.5, (double)cam.height), sy))));
+    DVec o = dv(cam.pos[0], cam.pos[1], cam.pos[2]);
+    // ---- trace_eye_subpath (path.cpp:331-386)
+    Mis mis;
+    {  // mis_camera_origin (path.cpp:38-43) with camera_pdf_w (path.cpp:144-148)
+      const double ct = dot(dir, fwd);
+      const double cpdf = ct <= 0.0 ? 0.0 : dd(dm(cam.plane_dist, cam.plane_dist), dm(dm(ct, ct), ct));
+      mis.d_vcm = mpow(B.beta, dd((double)B.n_paths, cpdf));
+      mis.d_vc = 0.0;
+      mis.d_vm = 0.0;
+    }
+    double t0 = 1.0, t1 = 1.0, t2 = 1.0;
+    uint32_t nv = 0;
+    for (uint32_t depth = 1; depth <= B.max_depth; ++depth) {
+      HitD h;
+      if (!intersect(P, np, o, dir, h)) break;
+      const DVec wo = neg(dir);
+      const double cos_in = fabs(dot(h.sn, wo));
+      if (cos_in == 0.0) break;
+      {  // mis_arrive
+        const double inv_cos = dd(1.0, mpow(B.beta, cos_in));
+        mis.d_vcm = dm(mis.d_vcm, dm(mpow(B.beta, dm(h.t, h.t)), inv_cos));
+        mis.d_vc = dm(mis.d_vc, inv_cos);
+        mis.d_vm = dm(mis.d_vm, inv_cos);
+      }
+      const int mk = sc.mat_kind[h.mat];
+      EyeV &v = V[nv++];
+      v.pos = h.point;
+      v.sn = h.sn;
+      {  // fill_hit's geometric normal (gn = front ? outward : -outward)
+        const PrimD &pp = P[h.prim];
+        const DVec outward = pp.kind == 0 ? mul(sub(h.point, dv(pp.c[0], pp.c[1], pp.c[2])), pp.inv_r)
+                                          : dv(pp.on[0], pp.on[1], pp.on[2]);
+        v.gn = h.front ? outward : neg(outward);
+      }
+      v.wo = wo;
+      v.t0 = t0; v.t1 = t1; v.t2 = t2;
+      v.mat = h.mat;
+      v.emitter = P[h.prim].emitter;
+      v.delta = mk != 0;
+      v.front = h.front;
+      v.depth = depth;
+      v.mis = mis;
+      if (depth == B.max_depth) break;
+      const double cos_o = dot(wo, h.sn);
+      DVec ndir;
+      double s_cos, s_pdf, s_rev;
+      bool s_delta;
+      if (!bsdf_sample(sc, mk, h.mat, h.sn, wo, h.front, cos_o, rng, ndir, s_cos, s_pdf, s_rev, s_delta)) break;
+      const double *w = sc.mat_rgb + 3 * (size_t)h.mat;
+      if (s_pdf <= 0.0 || (w[0] == 0 && w[1] == 0 && w[2] == 0)) break;
+      double q = 1.0;
+      const double cont = cont_prob(sc, h.mat);
+      if (depth >= 5) {  // kRouletteDepth
+        q = cont;
+        if (rng.next() >= q) break;
+      }
+      {  // mis_scatter with pdfs x continuation (path.cpp:52-76, 374-380)
+        const double pf = dm(s_pdf, cont), pr = dm(s_rev, cont);
+        if (s_delta) {
+          const double f = mpow(B.beta, dd(dm(s_cos, pr), pf));
+          mis.d_vcm = 0.0;
+          mis.d_vc = dm(mis.d_vc, f);
+          mis.d_vm = dm(mis.d_vm, f);
+        } else {
+          const double ratio = mpow(B.beta, dd(s_cos, pf));
+          const double rev = mpow(B.beta, pr);
+          const double d_vc = dm(ratio, da(da(dm(mis.d_vc, rev), mis.d_vcm), ctx.vmf));
+          const double d_vm = dm(ratio, da(da(dm(mis.d_vm, rev), dm(mis.d_vcm, ctx.vcf)), 1.0));
+          mis.d_vc = d_vc;
+          mis.d_vm = d_vm;
+          mis.d_vcm = mpow(B.beta, dd(1.0, pf));
+        }
+      }
+      t0 = dd(dm(t0, w[0]), q);
+      t1 = dd(dm(t1, w[1]), q);
+      t2 = dd(dm(t2, w[2]), q);
+      o = h.point;
+      dir = ndir;
+    }
+    // ---- pixel_bidir's vertex loop (integrator.cpp:519-625)
+    double o0 = 0.0, o1 = 0.0, o2 = 0.0;
+    const uint32_t lp = px % B.n_paths;
+    const size_t lbase = (size_t)lp * B.light_depth;
+    const uint32_t lcount = B.l_count[lp];
+    bool primary_seen = false;
+    uint32_t nsec = 0;
+    B.gathered[px] = 0;
+    for (uint32_t k = 0; k < nv; ++k) {
+      const EyeV &v = V[k];
+      if (v.emitter >= 0 && v.front) {  // emitted radiance (integrator.cpp:520-531)
+        double w = 1.0;
+        if (v.depth > 1) {
+          // emitter_hit_pdfs (path.cpp:320-329): area emitters, cos_exit = dot(n, -ray_dir)
+          const double cos_exit = dot(v.gn, v.wo);
+          if (cos_exit <= 0.0) {
+            w = 0.0;
+          } else {
+            const double dpa = P[sc.emit_prim[v.emitter]].inv_area;
+            const double epdf = dm(dpa, cos_pdf(cos_exit));
+            const double a = dm(pick_prob, dpa), e = dm(pick_prob, epdf);
+            // mis_weight_emitter_hit (path.cpp:78-83)
+            const double wc = da(dm(mpow(B.beta, a), v.mis.d_vcm), dm(mpow(B.beta, e), v.mis.d_vc));
+            w = dd(1.0, da(1.0, wc));
+          }
+        }
+        const double *L = sc.emit_rad + 3 * (size_t)v.emitter;
+        o0 = da(o0, dm(dm(v.t0, L[0]), w));
+        o1 = da(o1, dm(dm(v.t1, L[1]), w));
+        o2 = da(o2, dm(dm(v.t2, L[2]), w));
+      }
+      if (v.delta) continue;
+      const double cos_o = dot(v.wo, v.sn);  // Bsdf ctor (bsdf.cpp:34)
+      const double cont = cont_prob(sc, v.mat);
+      // ---- next-event estimation (integrator.cpp:537-561)
+      if (n_emit && v.depth + 1 <= B.max_depth) {
+        int pick = (int)dm(rng.next(), (double)n_emit);
+        if (pick > n_emit - 1) pick = n_emit - 1;
+        // sample_direct, area emitters (path.cpp:262-277) via sample_area_point (path.cpp:172-189)
+        const PrimD &ep = P[sc.emit_prim[pick]];
+        DVec apos, anrm;
+        if (ep.kind == 1) {
+          const double u = rng.next(), w2 = rng.next();
+          apos = add(add(dv(ep.c[0], ep.c[1], ep.c[2]), mul(dv(ep.e1[0], ep.e1[1], ep.e1[2]), u)),
+                     mul(dv(ep.e2[0], ep.e2[1], ep.e2[2]), w2));
+          anrm = dv(ep.on[0], ep.on[1], ep.on[2]);
+        } else {
+          const double u2 = rng.next(), u1 = rng.next();  // right-to-left arguments
+          const DVec d_ = sample_uniform_sphere(u1, u2);
+          apos = add(dv(ep.c[0], ep.c[1], ep.c[2]), mul(d_, ep.r));
+          anrm = d_;
+        }
+        const double pdf_a = ep.inv_area;
+        const DVec lv = sub(apos, v.pos);
+        const double dist2 = dot(lv, lv);
+        if (dist2 != 0.0) {
+          const double dist = __dsqrt_rn(dist2);
+          const DVec to_light = mul(lv, dd(1.0, dist));
+          const double cos_at_light = dot(anrm, neg(to_light));
+          const double *Le = sc.emit_rad + 3 * (size_t)pick;
+          if (cos_at_light > 0.0 && !(Le[0] == 0 && Le[1] == 0 && Le[2] == 0)) {
+            const double direct_pdf_w = dd(dm(pdf_a, dist2), cos_at_light);
+            const double emission_pdf = dm(pdf_a, cos_pdf(cos_at_light));
+            const Eval f = bsdf_eval(sc, v.mat, v.sn, cos_o, to_light);
+            const double cos_v = fabs(dot(v.sn, to_light));
+            if (!f.black && cos_v > 0.0 && !occluded(P, np, v.pos, add(v.pos, mul(to_light, dist)))) {
+              // mis_weight_nee (path.cpp:85-95), delta_light = false
+              const double dpw = dm(pick_prob, direct_pdf_w), epw = dm(pick_prob, emission_pdf);
+              const double w_light = mpow(B.beta, dd(dm(f.pf, cont), dpw));
+              const double w_camera =
+                  dm(mpow(B.beta, dd(dm(epw, cos_v), dm(dpw, cos_at_light))),
+                     da(da(ctx.vmf, v.mis.d_vcm), dm(v.mis.d_vc, mpow(B.beta, dm(f.pr, cont)))));
+              const double w = dd(1.0, da(da(w_light, 1.0), w_camera));
+              const double sc_ = dd(dm(w, cos_v), dpw);
+              o0 = da(o0, dm(dm(dm(v.t0, f.f0), Le[0]), sc_));
+              o1 = da(o1, dm(dm(dm(v.t1, f.f1), Le[1]), sc_));
+              o2 = da(o2, dm(dm(dm(v.t2, f.f2), Le[2]), sc_));
+            }
+          }
+        }
+      }
+      // ---- connections to light sub-path px % J (integrator.cpp:563-588)
+      for (uint32_t li = 0; li < lcount; ++li) {
+        const size_t sl = lbase + li, s3 = 3 * sl;
+        if (v.depth + B.l_depth[sl] + 1 > B.max_depth) continue;
+        const DVec lpos = dv(B.l_pos[s3], B.l_pos[s3 + 1], B.l_pos[s3 + 2]);
+        DVec d = sub(lpos, v.pos);
+        const double d2 = dot(d, d);
+        if (d2 == 0.0) continue;
+        const double dist = __dsqrt_rn(d2);
+        d = divs(d, dist);
+        const Eval fe = bsdf_eval(sc, v.mat, v.sn, cos_o, d);
+        if (fe.black) continue;
+        const DVec lsn = dv(B.l_sn[s3], B.l_sn[s3 + 1], B.l_sn[s3 + 2]);
+        const DVec lwi = dv(B.l_wi[s3], B.l_wi[s3 + 1], B.l_wi[s3 + 2]);
+        const int lmat = B.l_mat[sl];
+        const Eval fl = bsdf_eval(sc, lmat, lsn, dot(lwi, lsn), neg(d));
+        if (fl.black) continue;
+        if (occluded(P, np, v.pos, lpos)) continue;
+        const double lcont = cont_prob(sc, lmat);
+        const double cos_e = fabs(dot(v.sn, d)), cos_l = fabs(dot(lsn, d));
+        // mis_weight_connect (path.cpp:97-108)
+        const double efa = dd(dm(dm(fe.pf, cont), cos_l), d2), erw = dm(fe.pr, cont);
+        const double lfa = dd(dm(dm(fl.pf, lcont), cos_e), d2), lrw = dm(fl.pr, lcont);
+        const double w_light = dm(mpow(B.beta, efa), da(da(ctx.vmf, B.l_mis[s3]), dm(B.l_mis[s3 + 1], mpow(B.beta, lrw))));
+        const double w_camera = dm(mpow(B.beta, lfa), da(da(ctx.vmf, v.mis.d_vcm), dm(v.mis.d_vc, mpow(B.beta, erw))));
+        const double w = dd(1.0, da(da(w_light, 1.0), w_camera));
+        const double g = dd(dm(dm(w, cos_e), cos_l), d2);
+        o0 = da(o0, dm(dm(dm(dm(v.t0, fe.f0), fl.f0), B.l_thr[s3]), g));
+        o1 = da(o1, dm(dm(dm(dm(v.t1, fe.f1), fl.f1), B.l_thr[s3 + 1]), g));
+        o2 = da(o2, dm(dm(dm(dm(v.t2, fe.f2), fl.f2), B.l_thr[s3 + 2]), g));
+      }
+      // ---- merge vertex (integrator.cpp:590-623)
+      const bool primary = !primary_seen;
+      primary_seen = true;
+      const double *alb = sc.mat_rgb + 3 * (size_t)v.mat;
+      if (primary) {
+        B.pos[px] = make_double3(v.pos.x, v.pos.y, v.pos.z);
+        B.nrm[px] = make_double3(v.sn.x, v.sn.y, v.sn.z);
+        B.wo[px] = make_double3(v.wo.x, v.wo.y, v.wo.z);
+        B.thr[px] = make_double3(v.t0, v.t1, v.t2);
+        B.alb[px] = make_double3(alb[0], alb[1], alb[2]);
+        B.eye_depth[px] = v.depth;
+        B.eye_mis[px] = make_double2(v.mis.d_vcm, v.mis.d_vm);
+        B.gathered[px] = 1;
+      } else if (nsec < nq) {
+        const size_t q = (size_t)px * nq + nsec++;
+        B.q_pos[q] = make_double3(v.pos.x, v.pos.y, v.pos.z);
+        B.q_nrm[q] = make_double3(v.sn.x, v.sn.y, v.sn.z);
+        B.q_wo[q] = make_double3(v.wo.x, v.wo.y, v.wo.z);
+        B.q_thr[q] = make_double3(v.t0, v.t1, v.t2);
+        B.q_alb[q] = make_double3(alb[0], alb[1], alb[2]);
+        B.q_eye[q] = v.depth;
+        B.q_mis[q] = make_double2(v.mis.d_vcm, v.mis.d_vm);
+        B.q_radius[q] = r;
+        B.q_gathered[q] = 1;
+      }
+    }
+    for (uint32_t k = nsec; k < nq; ++k) B.q_gathered[(size_t)px * nq + k] = 0;
+    if (!primary_seen) {  // the region holds (integrator.cpp:627-631); placeholders
+      B.pos[px] = make_double3(0, 0, 0);
+      B.nrm[px] = make_double3(0, 0, 1);
+      B.wo[px] = make_double3(0, 0, 1);
+      B.thr[px] = make_double3(0, 0, 0);
+      B.alb[px] = make_double3(0, 0, 0);
+      B.eye_depth[px] = 0;
+      B.eye_mis[px] = make_double2(0.0, 0.0);
+    }
+    B.direct[px] = make_double3(o0, o1, o2);
+  }
+}
+
+
+// camera_connect (integrator.cpp:270-301) for every light vertex with
+// depth + 1 <= max_depth: project_to_camera (path.cpp:150-170), the light
+// vertex's Bsdf toward the camera, visibility, mis_weight_camera_connect
+// (path.cpp:119-126) with the light sub-paths' context; the splat goes to the
+// pixel the vertex projects to (fp64 atomics: the reference adds the splats
+// serially in path order, so sums agree to rounding).
+__global__ void __launch_bounds__(128) k_light_splat(const BidirArgs B, const PrimD *__restrict__ prims) {
+  __shared__ PrimD P[kMaxTracePrims];
+  const TraceScene &sc = B.sc;
+  const int np = sc.n_prim;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) P[i] = prims[i];
+  __syncthreads();
+  const CamD &cam = B.cam;
+  const DVec cpos = dv(cam.pos[0], cam.pos[1], cam.pos[2]), fwd = dv(cam.fwd[0], cam.fwd[1], cam.fwd[2]);
+  const DVec right = dv(cam.right[0], cam.right[1], cam.right[2]), up = dv(cam.up[0], cam.up[1], cam.up[2]);
+  const MisC ctx = mis_ctx(B.beta, B.eta_light);
+  const double n_paths = (double)B.n_paths;
+  const size_t nslots = (size_t)B.n_paths * B.light_depth;
+  for (size_t sl = blockIdx.x * (size_t)blockDim.x + threadIdx.x; sl < nslots; sl += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t j = (uint32_t)(sl / B.light_depth), k = (uint32_t)(sl % B.light_depth);
+    if (k >= B.l_count[j]) continue;
+    if (B.l_depth[sl] + 1 > B.max_depth) continue;
+    const size_t s3 = 3 * sl;
+    const DVec p = dv(B.l_pos[s3], B.l_pos[s3 + 1], B.l_pos[s3 + 2]);
+    // project_to_camera
+    const DVec vv = sub(p, cpos);
+    const double dist = __dsqrt_rn(dot(vv, vv));
+    if (dist == 0.0) continue;
+    const DVec d = mul(vv, dd(1.0, dist));
+    const double ct = dot(d, fwd);
+    if (ct <= 1e-9) continue;
+    const DVec on_plane = mul(d, dd(cam.plane_dist, ct));
+    const double sx = da(dm(0.5, (double)cam.width), dot(on_plane, right));
+    const double sy = ds(dm(0.5, (double)cam.height), dot(on_plane, up));
+    if (sx < 0.0 || sx >= (double)cam.width || sy < 0.0 || sy >= (double)cam.height) continue;
+    const DVec to_cam = neg(d);
+    const double pdf_w = dd(dm(cam.plane_dist, cam.plane_dist), dm(dm(ct, ct), ct));
+    const DVec sn = dv(B.l_sn[s3], B.l_sn[s3 + 1], B.l_sn[s3 + 2]);
+    const DVec wi = dv(B.l_wi[s3], B.l_wi[s3 + 1], B.l_wi[s3 + 2]);
+    const int mat = B.l_mat[sl];
+    const Eval f = bsdf_eval(sc, mat, sn, dot(wi, sn), to_cam);
+    if (f.black) continue;
+    if (occluded(P, np, p, cpos)) continue;
+    const double cos_v = fabs(dot(sn, to_cam));
+    const double dist2 = dm(dist, dist);
+    const double cam_pdf_a = dd(dm(pdf_w, cos_v), dist2);
+    const double rev = dm(f.pr, cont_prob(sc, mat));
+    const double w_light = dm(mpow(B.beta, dd(cam_pdf_a, n_paths)),
+                              da(da(ctx.vmf, B.l_mis[s3]), dm(B.l_mis[s3 + 1], mpow(B.beta, rev))));
+    const double w = dd(1.0, da(w_light, 1.0));
+    const double g = dd(dm(dm(w, pdf_w), cos_v), dm(dist2, n_paths));
+    const double v0 = dm(dm(B.l_thr[s3], f.f0), g), v1 = dm(dm(B.l_thr[s3 + 1], f.f1), g),
+                 v2 = dm(dm(B.l_thr[s3 + 2], f.f2), g);
+    if (v0 == 0 && v1 == 0 && v2 == 0) continue;
+    int x = (int)sx, y = (int)sy;
+    x = x < 0 ? 0 : (x > cam.width - 1 ? cam.width - 1 : x);
+    y = y < 0 ? 0 : (y > cam.height - 1 ? cam.height - 1 : y);
+    double *o = reinterpret_cast<double *>(B.splat + (size_t)y * (uint32_t)cam.width + (uint32_t)x);
+    atomicAdd(o, v0);
+    atomicAdd(o + 1, v1);
+    atomicAdd(o + 2, v2);
+  }
+}
+
+// Film::add_iteration of the VCM+ estimate: out = direct + sum_k merge_k *
+// vm_norm in vertex order (vm_norm = 1 / (pi r^2 J), integrator.cpp:505-506,
+// 620) + the splats (integrator.cpp:205-211).
+__global__ void k_film_vcm(uint32_t npix, uint32_t nq, const double3 *__restrict__ direct,
+                           const uint8_t *__restrict__ gathered, const double *__restrict__ flux,
+                           const double *__restrict__ gather_r, const double *__restrict__ q_rows, uint32_t q_stride,
+                           const uint8_t *__restrict__ q_gathered, const double *__restrict__ q_radius,
+                           const double3 *__restrict__ splat, double J, double3 *__restrict__ film) {
+  for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < npix; px += gridDim.x * blockDim.x) {
+    double3 est = direct[px];
+    if (gathered[px]) {
+      const double r = gather_r[px];
+      const double vn = dd(1.0, dm(dm(dm(kPi, r), r), J));
+      est.x = da(est.x, dm(flux[3 * (size_t)px], vn));
+      est.y = da(est.y, dm(flux[3 * (size_t)px + 1], vn));
+      est.z = da(est.z, dm(flux[3 * (size_t)px + 2], vn));
+    }
+    for (uint32_t k = 0; k < nq; ++k) {
+      const size_t q = (size_t)px * nq + k;
+      if (!q_gathered[q]) break;
+      const double r = q_radius[q];
+      const double vn = dd(1.0, dm(dm(dm(kPi, r), r), J));
+      const double *row = q_rows + q * q_stride + (q_stride - 3);
+      est.x = da(est.x, dm(row[0], vn));
+      est.y = da(est.y, dm(row[1], vn));
+      est.z = da(est.z, dm(row[2], vn));
+    }
+    const double3 sp = splat[px];
+    est.x = da(est.x, sp.x);
+    est.y = da(est.y, sp.y);
+    est.z = da(est.z, sp.z);
+    double3 f = film[px];
+    f.x = da(f.x, est.x);
+    f.y = da(f.y, est.y);
+    f.z = da(f.z, est.z);
+    film[px] = f;
+  }
+}
+
+cudaError_t launch_eye_bidir(cudaStream_t s, const BidirArgs &B, const void *prep, int sms) {
+  if (B.npix == 0) return cudaSuccess;
+  if (B.max_depth > kMaxBidirDepth) return cudaErrorInvalidValue;
+  unsigned blocks = (B.npix + 127) / 128;
+  if (blocks > (unsigned)sms * 16) blocks = sms * 16;
+  k_eye_bidir<<<blocks, 128, 0, s>>>(B, static_cast<const PrimD *>(prep));
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_light_splat(cudaStream_t s, const BidirArgs &B, const void *prep, int sms) {
+  const unsigned long long n = (unsigned long long)B.n_paths * B.light_depth;
+  if (n == 0) return cudaSuccess;
+  unsigned long long blocks = (n + 127) / 128;
+  if (blocks > (unsigned long long)sms * 16) blocks = (unsigned long long)sms * 16;
+  k_light_splat<<<(unsigned)blocks, 128, 0, s>>>(B, static_cast<const PrimD *>(prep));
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_film_vcm(cudaStream_t s, uint32_t npix, uint32_t nq_per_px, const double3 *direct,
+                            const uint8_t *gathered, const double *flux, const double *gather_r,
+                            const double *q_rows, uint32_t q_stride, const uint8_t *q_gathered,
+                            const double *q_radius, const double3 *splat, double J, double3 *film, int sms) {
+  if (npix == 0) return cudaSuccess;
+  unsigned blocks = (npix + 255) / 256;
+  if (blocks > (unsigned)sms * 8) blocks = sms * 8;
+  k_film_vcm<<<blocks, 256, 0, s>>>(npix, nq_per_px, direct, gathered, flux, gather_r, q_rows, q_stride,
+                                    q_gathered, q_radius, splat, J, film);
   note_launches(1);
   return cudaGetLastError();
 }
