@@ -208,7 +208,8 @@ def run_reference_arm(args, wl, rank):
                            "sample": sample},
           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
           "trace": reference_trace(threads, args),
-          "render": None if args.no_render else reference_render(threads)})
+          "render": None if args.no_render else reference_render(threads),
+          "vcm": None if args.no_render else reference_vcm(threads)})
 
 
 def reference_trace(threads, args):
@@ -336,6 +337,71 @@ def reference_render(threads):
                                     r0_frac=0.002, n_annuli=2, n_sectors=6, alpha_f=0.01, threads=threads)
         return {"ms_per_iteration": 1e3 * secs, "cores": threads, "kind": "reference",
                 "sample": "iteration 1 of the full C3 config through the reference's render() "
+                          "(IterationReport wall time of the whole call)"}
+    except Exception as e:
+        return {"unavailable": f"reference render failed: {e}"}
+
+
+VCM_PATHS = 1 << 20       # BASELINE configs[3]: 1M light sub-paths per iteration
+
+
+def vcm_config():
+    return {"workload": f"c4 full VCM+ iteration (BASELINE configs[3]): caustic box, {RENDER_RES}^2 pinhole, "
+                        f"{VCM_PATHS} light sub-paths, max_depth {TRACE_MAX_DEPTH}",
+            "test": "4 sectors (1x4), alpha_F 0.05, r1 = 0.002 * bounding radius, luminance channel",
+            "stages": "light sub-paths + camera splats + eye sub-paths (emitter hits, NEE, connections) + grid + "
+                      "merges at every rough eye vertex (primary F-tested) + film (Renderer::step, vcm_plus)"}
+
+
+def run_vcm_bench(local_rank, steps, warmup):
+    """C4: Renderer::step with vcm_plus on the device (fppm_gpu_render_vcm),
+    timed with CUDA events per iteration."""
+    import torch
+    from paper_2504_04411_b200 import FppmContext
+    from paper_2504_04411_b200.scene import bounding_radius, caustic_box, caustic_box_camera
+    sc, cam = caustic_box(), caustic_box_camera(RENDER_RES)
+    r1 = 0.002 * bounding_radius(sc)
+    ctx = FppmContext(initial_radius=r1, samples_per_iteration=VCM_PATHS, n_annuli=1, n_sectors=4,
+                      alpha_f=0.05, r_min_base=0.001 * r1, max_depth=TRACE_MAX_DEPTH,
+                      max_hitpoints=RENDER_RES * RENDER_RES, max_photons=8 * VCM_PATHS, device=local_rank,
+                      vcm_plus=True, mis_n_vm=VCM_PATHS)
+    ctx.set_scene(sc)
+    ctx.set_camera(cam)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    for it in range(1, warmup + 1):
+        ctx.render_vcm_iteration(0x5EED, it, VCM_PATHS)
+    torch.cuda.synchronize()
+    c0 = ctx.counters()["accepted"]
+    l0 = FppmContext.kernel_launches()
+    ms = []
+    for it in range(warmup + 1, warmup + steps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.render_vcm_iteration(0x5EED, it, VCM_PATHS)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    q = ctx.counters()["accepted"] - c0
+    launches = FppmContext.kernel_launches() - l0
+    ctx.close()
+    return {"ms_per_iteration": statistics.mean(ms), "merge_queries_per_s": q / (sum(ms) / 1e3),
+            "gpu_launches": launches, "steps": steps,
+            "timing": "CUDA events around FppmContext.render_vcm_iteration on the context stream",
+            "config": vcm_config()}
+
+
+def reference_vcm(threads):
+    """The reference's own render() with vcm_plus (oracle/_ref), one C4 iteration."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle
+    from paper_2504_04411_b200.scene import caustic_box, caustic_box_camera
+    try:
+        rs = Oracle("reference").scene(caustic_box().arrays())
+        _, _, secs = rs.render_vcm_plus(caustic_box_camera(RENDER_RES), 0x5EED, 1, TRACE_MAX_DEPTH, VCM_PATHS,
+                                        r0_frac=0.002, n_annuli=1, n_sectors=4, alpha_f=0.05, threads=threads)
+        return {"ms_per_iteration": 1e3 * secs, "cores": threads, "kind": "reference",
+                "sample": "iteration 1 of the full C4 config through the reference's render() with vcm_plus "
                           "(IterationReport wall time of the whole call)"}
     except Exception as e:
         return {"unavailable": f"reference render failed: {e}"}
@@ -587,11 +653,13 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
         trace = run_trace_bench(args, local_rank, max(args.steps, 1), max(args.warmup, 1))
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             trace["cpu_baseline"] = reference_trace(os.cpu_count() or 1, args)
-    render = None
+    render = vcm = None
     if not args.no_render:
         render = run_render_bench(local_rank, max(min(args.steps, 5), 1), max(min(args.warmup, 3), 1))
+        vcm = run_vcm_bench(local_rank, max(min(args.steps, 5), 1), max(min(args.warmup, 3), 1))
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             render["cpu_baseline"] = reference_render(os.cpu_count() or 1)
+            vcm["cpu_baseline"] = reference_vcm(os.cpu_count() or 1)
 
     if rank == 0:
         if world == 1:
@@ -641,6 +709,8 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
             line["trace"] = trace
         if render:
             line["render"] = render
+        if vcm:
+            line["vcm"] = vcm
         emit(line)
     arm.close()
 
