@@ -158,7 +158,8 @@ static cudaError_t dalloc(T **p, size_t count) {
 
 // gather kernel variant: 1 warp per hit point, 2 tiled, 3 lanes, 4 fine (default)
 static int gather_variant(const fppm_gpu_ctx *ctx) {
-  if (ctx->cfg.vcm_plus) return ctx->cfg.gather_kernel == 5 ? 5 : 1;  // merge weights: warp / sparse kernels
+  // merge weights: the thread-per-hit-point kernel (auto) or the warp kernel
+  if (ctx->cfg.vcm_plus) return ctx->cfg.gather_kernel == 1 ? 1 : 5;
   if (ctx->cfg.gather_kernel == 0) return fine_supported(ctx->G, ctx->C) ? 4 : 2;
   return ctx->cfg.gather_kernel;
 }
@@ -1689,8 +1690,12 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
   Q.o_flags = nullptr;
   Q.o_radiance = nullptr;
   Q.o_accepted = nullptr;
-  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned int), s));
-  FPPM_CUDA_OK(launch_gather_test(s, Q, ctx->C, ctx->sms));
+  if (gather_variant(ctx) == 1) {
+    FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned int), s));
+    FPPM_CUDA_OK(launch_gather_test(s, Q, ctx->C, ctx->sms));
+  } else {  // thread per merge vertex, in (pixel, vertex) order
+    FPPM_CUDA_OK(launch_gather_sparse(s, Q, ctx->C, nullptr, ctx->q_rows, ctx->sms));
+  }
   FPPM_CUDA_OK(launch_film_vcm(s, npix, nq, ctx->d_emit, ctx->d_gathered, ctx->o_flux, ctx->o_gather_r,
                                ctx->q_rows, stride, ctx->q_gathered, ctx->q_radius, ctx->d_splat,
                                (double)light_paths, ctx->d_film, ctx->sms));

@@ -24,7 +24,7 @@ def _ctx(cfg, hit, H, kernel="auto"):
     return ctx
 
 
-@pytest.mark.parametrize("kernel", ["auto", "sparse"])
+@pytest.mark.parametrize("kernel", ["auto", "warp"])
 @pytest.mark.parametrize("beta", [1.0, 2.0])
 @pytest.mark.parametrize("channels", [1, 3])
 def test_vcm_canonical_matches_oracle(port, beta, channels, kernel):
@@ -50,7 +50,7 @@ def test_vcm_canonical_matches_oracle(port, beta, channels, kernel):
         assert want["accepted"].sum() > 0
 
 
-@pytest.mark.parametrize("kernel", ["auto", "sparse"])
+@pytest.mark.parametrize("kernel", ["auto", "warp"])
 def test_vcm_general_scene_matches_reference(port, ref, kernel):
     hit, _ = scene3d(4, H=400, N=15000)
     cfg = dict(n_annuli=2, n_sectors=6, alpha_f=0.05, initial_radius=0.03, r_min_base=3e-5,

@@ -34,12 +34,15 @@ def _compare(got, want, label):
     return bad
 
 
-@pytest.mark.parametrize("res,J,iters", [(24, 5000, 3), (32, 20000, 2)])
-def test_vcm_film_matches_reference_render(ref, res, J, iters):
+@pytest.mark.parametrize("res,J,iters,kernel", [(24, 5000, 3, "auto"), (24, 5000, 3, "warp"),
+                                               (32, 20000, 2, "auto")])
+def test_vcm_film_matches_reference_render(ref, res, J, iters, kernel):
+    """kernel: the merges on the thread-per-vertex kernel (auto) or the warp
+    kernel."""
     sc, cam = caustic_box(), caustic_box_camera(res)
     npix = cam.width * cam.height
     r1 = 0.002 * bounding_radius(sc)
-    ctx = _vcm_ctx(npix, J, r1)
+    ctx = _vcm_ctx(npix, J, r1, gather_kernel=kernel)
     ctx.set_scene(sc)
     ctx.set_camera(cam)
     for it in range(1, iters + 1):
@@ -50,7 +53,7 @@ def test_vcm_film_matches_reference_render(ref, res, J, iters):
     rs = ref.scene(sc.arrays())
     film, radius, _ = rs.render_vcm_plus(cam, 17, iters, 8, J, r0_frac=0.002, n_annuli=2, n_sectors=6,
                                          alpha_f=0.01, threads=8)
-    bad = _compare(img.reshape(-1, 3), film, f"vcm+ {res}^2 J={J}")
+    bad = _compare(img.reshape(-1, 3), film, f"vcm+ {res}^2 J={J} {kernel}")
     assert bad.sum() <= max(2, npix // 100)
     rad = ctx.regions()["radius"]
     assert (rad == radius).mean() >= 0.99
