@@ -13,3 +13,6 @@ bash scripts/ncu_fine.sh > gpurun_out/ncu_fine.txt 2>&1; echo "ncu rc=$?"
 # C3 full-iteration launch list (light phase + eye pass + grid + sparse gather + film)
 timeout 600 python scripts/render_bench.py --steps 2 > gpurun_out/render_plain.txt 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/render_launches.csv python scripts/render_bench.py --steps 2 > /dev/null 2>&1; echo "render launches rc=$?"
+# C4 full VCM+ iteration launch list
+timeout 600 python scripts/vcm_profile.py > gpurun_out/vcm_plain.txt 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/vcm_launches.csv python scripts/vcm_profile.py > /dev/null 2>&1; echo "vcm launches rc=$?"
