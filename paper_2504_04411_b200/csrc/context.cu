@@ -81,6 +81,7 @@ struct fppm_gpu_ctx {
   double *q_radius = nullptr, *q_rows = nullptr;
   double2 *q_mis = nullptr;
   unsigned long long q_cap = 0, q_rows_cap = 0;
+  fppm_b200::SortScratch q_sort{};  // home-cell order of the merge queries
 
   // VCM+ merge stage inputs
   double2 *d_eye_mis = nullptr;                                   // [H] {d_vcm, d_vm}
@@ -503,6 +504,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   if (ctx->d_emit) cudaFree(ctx->d_emit);
   {
     void *bq[] = {ctx->b_pos, ctx->b_sn, ctx->b_wi, ctx->b_thr, ctx->b_mis, ctx->b_mat, ctx->d_splat,
+                  ctx->q_sort.keys_a, ctx->q_sort.vals_a, ctx->q_sort.keys_b, ctx->q_sort.vals_b, ctx->q_sort.hist,
                   ctx->q_pos, ctx->q_nrm, ctx->q_wo, ctx->q_thr, ctx->q_alb, ctx->q_K, ctx->q_eye,
                   ctx->q_gathered, ctx->q_radius, ctx->q_rows, ctx->q_mis};
     for (void *p : bq)
@@ -1617,7 +1619,8 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
   if (nqt > 0xffffffffull) return fail(ctx, FPPM_ERR_CAPACITY, "render_vcm: too many merge vertices");
   if (nqt > ctx->q_cap) {
     void *qp[] = {ctx->q_pos, ctx->q_nrm, ctx->q_wo, ctx->q_thr, ctx->q_alb, ctx->q_K, ctx->q_eye,
-                  ctx->q_gathered, ctx->q_radius, ctx->q_mis, ctx->d_splat};
+                  ctx->q_gathered, ctx->q_radius, ctx->q_mis, ctx->d_splat, ctx->q_sort.keys_a,
+                  ctx->q_sort.vals_a, ctx->q_sort.keys_b, ctx->q_sort.vals_b, ctx->q_sort.hist};
     FPPM_CUDA_OK(cudaStreamSynchronize(s));
     for (void *p : qp)
       if (p) cudaFree(p);
@@ -1627,6 +1630,9 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
     FPPM_CUDA_OK(dalloc(&ctx->q_eye, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_gathered, nqt));
     FPPM_CUDA_OK(dalloc(&ctx->q_radius, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_mis, nqt));
     FPPM_CUDA_OK(dalloc(&ctx->d_splat, std::max<uint32_t>(npix, 1)));
+    FPPM_CUDA_OK(dalloc(&ctx->q_sort.keys_a, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_sort.vals_a, nqt));
+    FPPM_CUDA_OK(dalloc(&ctx->q_sort.keys_b, nqt)); FPPM_CUDA_OK(dalloc(&ctx->q_sort.vals_b, nqt));
+    FPPM_CUDA_OK(dalloc(&ctx->q_sort.hist, radix_hist_entries((uint32_t)nqt)));
     ctx->q_cap = nqt;
   }
   if (nqt * stride > ctx->q_rows_cap) {
@@ -1693,8 +1699,12 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
   if (gather_variant(ctx) == 1) {
     FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned int), s));
     FPPM_CUDA_OK(launch_gather_test(s, Q, ctx->C, ctx->sms));
-  } else {  // thread per merge vertex, in (pixel, vertex) order
-    FPPM_CUDA_OK(launch_gather_sparse(s, Q, ctx->C, nullptr, ctx->q_rows, ctx->sms));
+  } else {  // thread per merge vertex, visited in home-cell order (neighbours share records in L1)
+    TileSched qs;
+    qs.sort = ctx->q_sort;
+    const uint32_t *order = nullptr;
+    FPPM_CUDA_OK(hp_cell_order(s, Q, qs, *ctx->h_hdr, ctx->sms, &order));
+    FPPM_CUDA_OK(launch_gather_sparse(s, Q, ctx->C, order, ctx->q_rows, ctx->sms));
   }
   FPPM_CUDA_OK(launch_film_vcm(s, npix, nq, ctx->d_emit, ctx->d_gathered, ctx->o_flux, ctx->o_gather_r,
                                ctx->q_rows, stride, ctx->q_gathered, ctx->q_radius, ctx->d_splat,
