@@ -241,3 +241,19 @@ def test_port_matches_reference_vcm_plus(port, ref, beta):
         for k in a:
             if k != "times":
                 assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("algorithm", ["fppm", "vcm_plus"])
+def test_reference_render_thread_invariance(ref, algorithm):
+    """The reference's own render() -- the checker of the device's C3 / C4
+    renders (tests/test_gpu_render.py, tests/test_gpu_vcm_render.py) -- is
+    deterministic across thread counts (test_integrator.cpp:267-293), so its
+    film is a fixed target for a given seed."""
+    from paper_2504_04411_b200.scene import caustic_box, caustic_box_camera
+    rs = ref.scene(caustic_box().arrays())
+    cam = caustic_box_camera(8)
+    render = rs.render_fppm if algorithm == "fppm" else rs.render_vcm_plus
+    f1, r1, _ = render(cam, 3, 2, 8, 4000, r0_frac=0.01, n_annuli=1, n_sectors=4, alpha_f=0.05, threads=1)
+    f4, r4, _ = render(cam, 3, 2, 8, 4000, r0_frac=0.01, n_annuli=1, n_sectors=4, alpha_f=0.05, threads=4)
+    assert np.isfinite(f1).all() and f1.mean() > 0
+    assert np.array_equal(f1, f4) and np.array_equal(r1, r4)
