@@ -15,7 +15,8 @@ import numpy as np
 import pytest
 
 from paper_2504_04411_b200 import FppmContext, InvalidArgument, StateError
-from paper_2504_04411_b200.scene import bounding_radius, caustic_box, caustic_box_camera
+from paper_2504_04411_b200.scene import (Camera, bounding_radius, caustic_box, caustic_box_camera, mixed_box,
+                                        two_lights_sphere_emitter)
 
 pytestmark = pytest.mark.gpu
 
@@ -80,3 +81,29 @@ def test_vcm_render_api_errors():
     ctx.render_vcm_iteration(1, 1, 100, 8)
     img, n = ctx.film_mean()
     assert n == 1 and np.isfinite(img).all()
+
+
+MIXED_CAM = Camera((0.0, 0.1, -0.9), (0.0, -0.1, 1.0), (0.0, 1.0, 0.0), 70.0, 24, 16)
+TWO_CAM = Camera((0.0, 1.0, -3.0), (0.0, 0.4, 0.0), (0.0, 1.0, 0.0), 50.0, 20, 16)
+
+
+@pytest.mark.parametrize("which", ["mixed", "two_lights"])
+def test_vcm_other_scenes_match_reference_render(ref, which):
+    """Every material path on the eye side (mirror / glass chains, emitter hits
+    at depth > 1 with their MIS weight), a chromatic light (the reference
+    auto-detects RGB test channels), and two emitters incl. a sphere light
+    (emitter pick, sphere sampling in next-event estimation)."""
+    sc, cam = (mixed_box(), MIXED_CAM) if which == "mixed" else (two_lights_sphere_emitter(), TWO_CAM)
+    npix, J, iters = cam.width * cam.height, 8000, 2
+    r1 = 0.002 * bounding_radius(sc)
+    ctx = _vcm_ctx(npix, J, r1, channels="rgb" if which == "mixed" else "luminance")
+    ctx.set_scene(sc)
+    ctx.set_camera(cam)
+    for it in range(1, iters + 1):
+        ctx.render_vcm_iteration(29, it, J, 8)
+    img, _ = ctx.film_mean()
+    film, radius, _ = ref.scene(sc.arrays()).render_vcm_plus(cam, 29, iters, 8, J, r0_frac=0.002, n_annuli=2,
+                                                             n_sectors=6, alpha_f=0.01, threads=8)
+    bad = _compare(img.reshape(-1, 3), film, f"vcm+ {which}")
+    assert bad.sum() <= max(2, npix // 100)
+    assert (ctx.regions()["radius"] == radius).mean() >= 0.99
