@@ -745,10 +745,13 @@ def run_e2e(arm, batches, args, dev):
     h2d = sum(t.numel() * t.element_size() for t in pinned[0].values())
     d2h = n_out * (8 + 12 + 1)
 
-    def one(it, hb):
+    def one(it, hb, nxt=None):
         if world == 1 and arm.mode == "a":
             ph = N.Photons(*[hb[k].data_ptr() for k, _, _ in photon_layout()])
             N.check(ctx._lib.fppm_gpu_set_photons(ctx._h, ph, n_local), ctx._h)
+            if nxt is not None:  # the next step's upload overlaps this iteration
+                pn = N.Photons(*[nxt[k].data_ptr() for k, _, _ in photon_layout()])
+                N.check(ctx._lib.fppm_gpu_prefetch_photons(ctx._h, pn, n_local), ctx._h)
             N.check(ctx._lib.fppm_gpu_iterate(ctx._h, it, C.byref(io), None), ctx._h)
             return
         with torch.cuda.stream(arm.stream):
@@ -763,8 +766,9 @@ def run_e2e(arm, batches, args, dev):
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for s in range(args.warmup, args.warmup + args.steps):
-        one(s + 1, pinned[s])
+    end = args.warmup + args.steps
+    for s in range(args.warmup, end):  # every step's upload is inside the timed region
+        one(s + 1, pinned[s], pinned[s + 1] if s + 1 < end else None)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     q = float(ctx.counters()["accepted"] - c0)
@@ -777,7 +781,9 @@ def run_e2e(arm, batches, args, dev):
         secs, q = float(tm.item()), float(qs.item())
     else:
         secs = t1 - t0
-    path = ("fppm_gpu_set_photons (pinned host) + fppm_gpu_iterate with host outputs" if world == 1 and
+    path = ("fppm_gpu_set_photons (pinned host; step i+1's upload issued by fppm_gpu_prefetch_photons before "
+            "step i's fppm_gpu_iterate, so it overlaps that iteration) + fppm_gpu_iterate with host outputs"
+            if world == 1 and
             arm.mode == "a" else f"pinned host share -> device, option {arm.mode.upper()} step with host outputs")
     return {"value": q / secs, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * secs / args.steps, "path": path}

@@ -192,6 +192,12 @@ int fppm_gpu_max_radius(fppm_gpu_ctx *ctx, double *r_max);
 
 /* ---- photons + grid (PhotonGrid) ---- */
 int fppm_gpu_set_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n);
+/* Pipelining extension (no reference counterpart): uploads the NEXT batch
+ * into the free staging set on the copy stream while the current iteration
+ * runs, without changing the current photons.  A later fppm_gpu_set_photons
+ * with the same five host arrays and n adopts it without a copy (the arrays
+ * must not change in between); any other photon call discards it. */
+int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n);
 int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint32_t n);
 /* Canonical synthetic photons [begin, begin+n) of (seed, iteration). */
 int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed,

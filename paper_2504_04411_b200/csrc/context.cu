@@ -43,6 +43,11 @@ struct fppm_gpu_ctx {
   cudaEvent_t ev_copied[2] = {}, ev_free[2] = {};
   int stage_cur = 0;       // staging set the current photons live in
   int stage_pending = -1;  // set whose upload the next grid build must wait for
+  // fppm_gpu_prefetch_photons: an upload of the NEXT batch into the free set,
+  // adopted without a copy by a set_photons call with the same arrays
+  int pf_set = -1;
+  fppm_photons pf_src{};
+  uint32_t pf_n = 0;
   bool free_recorded[2] = {false, false};
   // photons the next grid build reads: the staging buffers, or caller-owned
   // device buffers registered by fppm_gpu_set_photons_device (zero copy)
@@ -751,12 +756,57 @@ static void use_staging(fppm_gpu_ctx *ctx, int set = 0) {
 // copy stream: the copy waits only until the grid build that last read that
 // set has consumed it (ev_free), and the next grid build waits for the copy
 // (ev_copied).  With pinned host memory the call returns immediately.
+static bool same_photons(const fppm_photons &a, const fppm_photons &b) {
+  return a.pos == b.pos && a.normal == b.normal && a.wi == b.wi && a.power == b.power && a.depth == b.depth;
+}
+
+// upload n photons into staging set `set` on the copy stream (ev_copied[set])
+static int upload_set(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cudaMemcpyKind kind, int set);
+
 static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cudaMemcpyKind kind) {
   if (!ctx || !p) return FPPM_ERR_INVALID_ARGUMENT;
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (n && (!p->pos || !p->normal || !p->wi || !p->power || !p->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
+  if (kind == cudaMemcpyHostToDevice && ctx->pf_set >= 0 && ctx->pf_n == n && same_photons(ctx->pf_src, *p)) {
+    // adopt the prefetched upload (already enqueued on the copy stream)
+    const int set = ctx->pf_set;
+    ctx->pf_set = -1;
+    ctx->stage_pending = set;
+    ctx->N = n;
+    ctx->grid_valid = false;
+    use_staging(ctx, set);
+    return FPPM_OK;
+  }
+  ctx->pf_set = -1;  // a different batch supersedes the prefetch
   const int set = ctx->stage_cur ^ 1;
+  int rc = upload_set(ctx, p, n, kind, set);
+  if (rc) return rc;
+  ctx->stage_pending = set;
+  ctx->N = n;
+  ctx->grid_valid = false;
+  use_staging(ctx, set);
+  return FPPM_OK;
+}
+
+// Next batch into the staging set not holding the current photons, while the
+// current iteration runs; set_photons with the same arrays then adopts it.
+int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n) {
+  if (!ctx || !host) return FPPM_ERR_INVALID_ARGUMENT;
+  if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
+  if (n && (!host->pos || !host->normal || !host->wi || !host->power || !host->depth))
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
+  const int set = ctx->stage_cur ^ 1;
+  if (ctx->stage_pending == set) return fail(ctx, FPPM_ERR_STATE, "prefetch while the staged batch is unconsumed");
+  int rc = upload_set(ctx, host, n, cudaMemcpyHostToDevice, set);
+  if (rc) return rc;
+  ctx->pf_set = set;
+  ctx->pf_src = *host;
+  ctx->pf_n = n;
+  return FPPM_OK;
+}
+
+static int upload_set(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cudaMemcpyKind kind, int set) {
   if (!ctx->cstream) {
     FPPM_CUDA_OK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
@@ -779,10 +829,6 @@ static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cud
                                  kind, s));
   }
   FPPM_CUDA_OK(cudaEventRecord(ctx->ev_copied[set], s));
-  ctx->stage_pending = set;
-  ctx->N = n;
-  ctx->grid_valid = false;
-  use_staging(ctx, set);
   return FPPM_OK;
 }
 
@@ -798,6 +844,7 @@ int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint
   if (n && (!dev->pos || !dev->normal || !dev->wi || !dev->power || !dev->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
   ctx->stage_pending = -1;  // an unconsumed upload is superseded
+  ctx->pf_set = -1;
   ctx->in_pos = dev->pos;
   ctx->in_nrm = dev->normal;
   ctx->in_wi = dev->wi;
@@ -815,8 +862,10 @@ int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
   if (workload == FPPM_WORKLOAD_C5 && !ctx->c5.pos) return fail(ctx, FPPM_ERR_STATE, "C5 photons before c5_setup");
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
-  if (ctx->stage_pending == 0) FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[0], 0));
+  if (ctx->stage_pending == 0 || ctx->pf_set == 0)
+    FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[0], 0));
   ctx->stage_pending = -1;
+  ctx->pf_set = -1;  // set 0 is rewritten
   if (workload == FPPM_WORKLOAD_C5) {
     if (seed != ctx->c5.seed) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "C5 seed differs from c5_setup");
     FPPM_CUDA_OK(launch_c5_photons(ctx->stream, ctx->c5, iteration, begin, n, ctx->d_ppos, ctx->d_pnrm, ctx->d_pwi,
@@ -1518,9 +1567,10 @@ int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration,
   if (total > ctx->cfg.max_photons)
     return fail(ctx, FPPM_ERR_CAPACITY, "traced deposits exceed max_photons");
   // the deposits become the staged photons (set 0) of the next grid build
-  if (ctx->stage_pending == 0 && ctx->ev_copied[0])
+  if ((ctx->stage_pending == 0 || ctx->pf_set == 0) && ctx->ev_copied[0])
     FPPM_CUDA_OK(cudaStreamWaitEvent(s, ctx->ev_copied[0], 0));
   ctx->stage_pending = -1;
+  ctx->pf_set = -1;  // set 0 is rewritten
   FPPM_CUDA_OK(launch_trace_compact(s, T, ctx->t_base, ctx->d_ppos, ctx->d_pnrm, ctx->d_pwi, ctx->d_ppow,
                                     ctx->d_pdepth, ctx->cfg.vcm_plus ? ctx->d_pmis_in[0] : nullptr,
                                     ctx->d_pmis_in[1], ctx->d_pmis_in[2], ctx->sms));

@@ -1,0 +1,63 @@
+"""fppm_gpu_prefetch_photons: the next batch's upload overlaps the current
+iteration; adopting it gives exactly the results of a plain set_photons, and
+any other photon call discards it."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2504_04411_b200 import FppmContext, WORKLOADS
+from paper_2504_04411_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+def _batch(seed, it, n, generator=2):
+    from oracle import Oracle
+    ph = Oracle("port").gen_photons(generator, seed, it, 0, n)
+    keys = ("pos", "nrm", "wi", "pow", "depth")
+    return {k: np.ascontiguousarray(ph[k], dtype=np.uint32 if k == "depth" else np.float32) for k in keys}
+
+
+def _ph(b):
+    return N.Photons(*[b[k].ctypes.data for k in ("pos", "nrm", "wi", "pow", "depth")])
+
+
+def _run(prefetch):
+    wl = WORKLOADS["c2"].scaled(raster=64, photons=1 << 15)
+    ctx = FppmContext(**wl.context_kwargs())
+    ctx.generate_raster_hitpoints(wl.raster)
+    batches = [_batch(wl.seed, it, wl.photons, wl.generator) for it in range(1, 5)]
+    outs = []
+    for i, b in enumerate(batches):
+        N.check(ctx._lib.fppm_gpu_set_photons(ctx._h, C.byref(_ph(b)), wl.photons), ctx._h)
+        if prefetch and i + 1 < len(batches):
+            N.check(ctx._lib.fppm_gpu_prefetch_photons(ctx._h, C.byref(_ph(batches[i + 1])), wl.photons), ctx._h)
+        ctx.N = wl.photons
+        got, _ = ctx.iterate(i + 1, stats=True)
+        outs.append(got)
+    ctx.close()
+    return outs
+
+
+def test_prefetch_matches_plain_uploads():
+    a, b = _run(False), _run(True)
+    for x, y in zip(a, b):
+        for k in x:
+            assert np.array_equal(np.asarray(x[k]), np.asarray(y[k])), k
+
+
+def test_prefetch_superseded():
+    wl = WORKLOADS["c2"].scaled(raster=32, photons=1 << 12)
+    ctx = FppmContext(**wl.context_kwargs())
+    ctx.generate_raster_hitpoints(wl.raster)
+    b1, b2 = _batch(wl.seed, 1, wl.photons, wl.generator), _batch(wl.seed, 2, wl.photons, wl.generator)
+    N.check(ctx._lib.fppm_gpu_set_photons(ctx._h, C.byref(_ph(b1)), wl.photons), ctx._h)
+    N.check(ctx._lib.fppm_gpu_prefetch_photons(ctx._h, C.byref(_ph(b2)), wl.photons), ctx._h)
+    ctx.generate_photons(wl.generator, wl.seed, 3, wl.photons)   # discards the prefetch
+    got, _ = ctx.iterate(1)
+    ref = FppmContext(**wl.context_kwargs())
+    ref.generate_raster_hitpoints(wl.raster)
+    ref.generate_photons(wl.generator, wl.seed, 3, wl.photons)
+    want, _ = ref.iterate(1)
+    assert np.array_equal(got["accepted"], want["accepted"])
