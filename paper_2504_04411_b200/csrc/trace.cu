@@ -782,7 +782,10 @@ struct EyeV {
   bool delta, front;
 };
 
-__global__ void __launch_bounds__(128) k_eye_bidir(const BidirArgs B, const PrimD *__restrict__ prims) {
+#ifndef FPPM_EYE_MINB
+#define FPPM_EYE_MINB 8
+#endif
+__global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_bidir(const BidirArgs B, const PrimD *__restrict__ prims) {
   __shared__ PrimD P[kMaxTracePrims];
   const TraceScene &sc = B.sc;
   const int np = sc.n_prim;
