@@ -1,4 +1,5 @@
 // Throughput probe: warp-instructions per SM per cycle for a few ops the
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/micro/pipes scripts/micro/pipes.cu
 // gather's inner loop uses (F2F.F64.F32, DADD, DFMA, FFMA, integer-only f32->f64).
 #include <cstdio>
 #include <cstdint>
