@@ -200,9 +200,11 @@ __global__ void __launch_bounds__(256)
 
 // ------------------------------------------------------------------ radix sort
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kTile = kSortThreads * kSortItems;  // 4096 keys per tile
-constexpr int kRadixMax = 256;
+constexpr int kSortItems = 12;
+constexpr int kTile = kSortThreads * kSortItems;  // 3072 keys per tile
+constexpr int kRadixBits = 9;                     // digits of up to 9 bits: 18-bit keys in 2 passes
+constexpr int kRadixMax = 1 << kRadixBits;
+static_assert(kRadixMax == 2 * kSortThreads, "two digits per thread in the tile scans");
 
 __global__ void __launch_bounds__(kSortThreads)
     k_radix_upsweep(const uint32_t *__restrict__ keys, uint32_t n, int shift, uint32_t mask,
@@ -295,19 +297,25 @@ __global__ void __launch_bounds__(kSortThreads)
     rank[it] = before + __popc(peers & lt_mask);
   }
   __syncthreads();
-  uint32_t total = 0;
-  if (threadIdx.x < kRadixMax) {
+  // thread t owns digits 2t, 2t + 1: per-warp prefixes (warp order = index
+  // order), global bases, and the tile's digit starts
+  uint32_t tot2[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const uint32_t d = 2 * threadIdx.x + j;
+    uint32_t total = 0;
     for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_wcnt[w][threadIdx.x];
-      s_wcnt[w][threadIdx.x] = total;
+      const uint32_t c = s_wcnt[w][d];
+      s_wcnt[w][d] = total;
       total += c;
     }
-    s_gbase[threadIdx.x] = threadIdx.x <= mask ? hist_scan[threadIdx.x * tiles + blockIdx.x] : 0u;
+    tot2[j] = total;
+    s_gbase[d] = d <= mask ? hist_scan[d * tiles + blockIdx.x] : 0u;
   }
   uint32_t tile_total;
-  const uint32_t start = block_exclusive_scan_256(threadIdx.x < kRadixMax ? total : 0u, s_warp,
-                                                  &tile_total);
-  if (threadIdx.x < kRadixMax) s_dstart[threadIdx.x] = start;
+  const uint32_t start = block_exclusive_scan_256(tot2[0] + tot2[1], s_warp, &tile_total);
+  s_dstart[2 * threadIdx.x] = start;
+  s_dstart[2 * threadIdx.x + 1] = start + tot2[0];
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
@@ -510,7 +518,7 @@ cudaError_t radix_sort_pairs(cudaStream_t s, SortScratch &sc, uint32_t n, uint32
   uint32_t *ki = sc.keys_a, *vi = sc.vals_a, *ko = sc.keys_b, *vo = sc.vals_b;
   if (n > 1) {
     const uint32_t tiles = (n + kTile - 1) / kTile;
-    const uint32_t passes = (bits + 7) / 8;
+    const uint32_t passes = (bits + kRadixBits - 1) / kRadixBits;
     const uint32_t width = (bits + passes - 1) / passes;
     uint32_t *totals = sc.hist + (size_t)kRadixMax * tiles;
     for (uint32_t p = 0; p < passes; ++p) {
