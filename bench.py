@@ -51,8 +51,6 @@ def parse():
                    help="multi-GPU decomposition (distributed.py); auto = measure both in warm-up")
     p.add_argument("--cpu-trace-paths", type=int, default=1 << 20)
     p.add_argument("--no-render", action="store_true", help="skip the C3 full-iteration leg")
-    p.add_argument("--cpu-stride", type=int, default=0,
-                   help="hit-point stride of the CPU sample (0 = auto)")
     return p.parse_args()
 
 
@@ -153,54 +151,79 @@ def emit(line):
 
 
 # ---------------------------------------------------------------- CPU reference
-def cpu_reference_run(wl, steps, warmup, stride, threads, first_iteration=1):
-    """Reference CPU path (oracle/_ref) on a hit-point sample; per step the
-    full photon grid is built and every `stride`-th hit point is gathered and
-    tested.  Returns per-step extrapolated (queries, seconds)."""
+def cpu_sample(wl, n=None, seed=0xC0FFEE):
+    """Seeded random hit-point sample (sorted): no raster aliasing.  1/64 of
+    the frame for C2, 1/16 for C1."""
     import numpy as np
+    n = n or wl.hitpoints // (64 if wl.hitpoints >= 1 << 18 else 16)
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(wl.hitpoints, n, replace=False)).astype(np.uint32)
+
+
+def cpu_reference_run(wl, first, last, threads, sample=None):
+    """The reference's own CPU path (oracle/_ref: PhotonGrid + GatherRegion,
+    compiled unmodified) on a hit-point sample, iterations 1..last; per
+    iteration the FULL photon grid is built (serial std::sort,
+    photon_map.cpp:26-51) and every sampled hit point is gathered and tested
+    on `threads` threads (integrator.cpp:52-70).  Iterations < first are the
+    untimed warm-up (they only bring the sampled regions' radii to the state
+    of the timed iterations).  Returns (records of the timed iterations,
+    sample): each record holds the measured grid / gather seconds, the
+    sample's accepted pairs, and the frame estimate (queries and seconds
+    scaled by H / n)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import Oracle
     ref, port = Oracle("reference"), Oracle("port")
+    sub = cpu_sample(wl) if sample is None else sample
     hp = port.gen_raster_hitpoints(wl.raster)
-    sub = np.arange(0, wl.hitpoints, stride, dtype=np.uint32)
-    hp_s = {k: v[sub] for k, v in hp.items()}
     sess = ref.session(dict(n_annuli=wl.n_annuli, n_sectors=wl.n_sectors, alpha_f=wl.alpha_f,
                             initial_radius=wl.initial_radius, r_min_base=0.001 * wl.initial_radius,
                             samples_per_iteration=wl.photons, k=wl.k, alpha=wl.alpha,
-                            threads=threads), hp_s)
+                            threads=threads), {k: v[sub] for k, v in hp.items()})
     scale = wl.hitpoints / len(sub)
     out = []
-    for s in range(warmup + steps):
-        it = first_iteration + s
+    for it in range(1, last + 1):
         ph = port.gen_photons(wl.generator, wl.seed, it, 0, wl.photons)
+        t0 = time.perf_counter()
         r = sess.iterate(it, ph)
+        wall = time.perf_counter() - t0
         grid_s, gather_s = r["times"]
-        if s >= warmup:
-            out.append((float(r["accepted"].sum()) * scale, grid_s + gather_s * scale,
-                        grid_s, gather_s))
-    return out, len(sub)
+        if it >= first:
+            q = float(r["accepted"].sum())
+            out.append({"iteration": it, "grid_s": grid_s, "gather_s": gather_s, "wall_s": wall,
+                        "q_sample": q, "accepted": r["accepted"].copy(),
+                        "q_frame_est": q * scale, "s_frame_est": grid_s + gather_s * scale})
+    return out, sub
+
+
+def cpu_sample_text(wl, sub, threads, first, last):
+    return (f"{wl.name} iterations {first}..{last} (after untimed iterations 1..{first - 1} of the same "
+            f"sample): per iteration the full {wl.photons}-photon grid build (reference PhotonGrid, "
+            f"serial std::sort) + gather/F-test of {len(sub)} of {wl.hitpoints} hit points (seeded random "
+            f"sample) on {threads} threads; value = the frame rate estimated from it (queries and gather "
+            f"time x{wl.hitpoints / len(sub):g}, grid build once), ms_per_step = the measured time")
 
 
 def run_reference_arm(args, wl, rank):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    stride = args.cpu_stride or (64 if wl.name.startswith("c2") else 16)
-    steps = run = None
+    first, last = max(args.warmup, 0) + 1, max(args.warmup, 0) + max(args.steps, 1)
     try:
-        run, nsub = cpu_reference_run(wl, max(args.steps, 1), max(args.warmup, 0), stride, threads)
+        run, sub = cpu_reference_run(wl, first, last, threads)
     except Exception as e:  # the reference arm must still print a line
         emit({"impl": "reference", "unavailable": f"reference CPU run failed: {e}"})
         return
-    q = sum(x[0] for x in run)
-    t = sum(x[1] for x in run)
+    q = sum(x["q_frame_est"] for x in run)
+    t = sum(x["s_frame_est"] for x in run)
     v = q / t
-    sample = (f"{wl.name}: per step the full {wl.photons}-photon grid build (serial std::sort, "
-              f"photon_map.cpp:26-51) + gather/F-test of every {stride}th hit point "
-              f"({nsub} of {wl.hitpoints}) on {threads} threads, queries and gather time "
-              f"extrapolated x{wl.hitpoints / nsub:g} to the full frame")
+    measured = sum(x["grid_s"] + x["gather_s"] for x in run)
+    sample = cpu_sample_text(wl, sub, threads, first, last)
     emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(run),
+          "steps": len(run), "warmup": args.warmup, "ms_per_step": 1e3 * measured / len(run),
+          "frame_ms_per_step_estimate": 1e3 * t / len(run),
+          "sample_queries_per_step": sum(x["q_sample"] for x in run) / len(run),
+          "frame_queries_per_step_estimate": q / len(run),
           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
           "data": "synthetic (canonical PCG32 inputs, DESIGN.md §3)",
           "config": workload_config(wl),
@@ -210,6 +233,23 @@ def run_reference_arm(args, wl, rank):
           "trace": reference_trace(threads, args),
           "render": None if args.no_render else reference_render(threads),
           "vcm": None if args.no_render else reference_vcm(threads)})
+
+
+def gpu_sample_check(wl, last, sub, local_rank, kernel):
+    """The device's per-hit-point accepted counts and frame Q for iterations
+    1..last (a fresh context on the same inputs), for the inline CPU
+    baseline's parity and sample-bias check."""
+    from paper_2504_04411_b200 import FppmContext
+    ctx = FppmContext(**wl.context_kwargs(device=local_rank, gather_kernel=kernel))
+    wl.set_hitpoints(ctx)
+    acc, qf = {}, {}
+    for it in range(1, last + 1):
+        ctx.generate_photons(wl.generator, wl.seed, it, wl.photons)
+        o, sm = ctx.iterate(it)
+        acc[it] = o["accepted"][sub].astype("uint64")
+        qf[it] = sm["accepted"]
+    ctx.close()
+    return acc, qf
 
 
 def reference_trace(threads, args):
@@ -634,16 +674,28 @@ def run_gpu_arm(args, wl, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the reference on the first two timed iterations (same sample, same
+        # state: iterations 1..warmup replayed untimed first)
         try:
-            stride = args.cpu_stride or (64 if wl.name.startswith("c2") else 16)
+            import numpy as np
             threads = os.cpu_count() or 1
-            run, nsub = cpu_reference_run(wl, 1, 0, stride, threads)
-            q, t = run[0][0], run[0][1]
+            first = args.warmup + 1
+            last = first + min(args.steps, 2) - 1
+            run, sub = cpu_reference_run(wl, first, last, threads)
+            acc, qf = gpu_sample_check(wl, last, sub, local_rank, args.kernel)
+            q = sum(x["q_frame_est"] for x in run)
+            t = sum(x["s_frame_est"] for x in run)
             cpu = {"value": q / t, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": (f"iteration 1 of {wl.name}: full {wl.photons}-photon grid build "
-                              f"(reference PhotonGrid, serial sort) {run[0][2]:.2f} s + gather/F-test "
-                              f"of every {stride}th hit point ({nsub} of {wl.hitpoints}) "
-                              f"{run[0][3]:.2f} s on {threads} threads, extrapolated to the frame")}
+                   "sample": cpu_sample_text(wl, sub, threads, first, last),
+                   "measured_ms_per_iteration": 1e3 * sum(x["grid_s"] + x["gather_s"] for x in run) / len(run),
+                   "grid_build_s": [round(x["grid_s"], 4) for x in run],
+                   "sample_gather_s": [round(x["gather_s"], 4) for x in run],
+                   "sample_accepted_equal_to_gpu": all(np.array_equal(x["accepted"], acc[x["iteration"]])
+                                                       for x in run),
+                   "sample_queries": [x["q_sample"] for x in run],
+                   "frame_queries_estimate": [x["q_frame_est"] for x in run],
+                   "frame_queries_gpu": [qf[x["iteration"]] for x in run],
+                   "frame_estimate_over_gpu": [x["q_frame_est"] / qf[x["iteration"]] for x in run]}
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}

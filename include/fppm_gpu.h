@@ -65,7 +65,10 @@ typedef enum fppm_status {
 #define FPPM_WORKLOAD_C5 5  /* needs fppm_gpu_c5_setup (same seed) */
 
 typedef struct fppm_gpu_config {
-  /* TestConfig (gather.hpp:34-41) */
+  /* TestConfig (gather.hpp:34-41).  Deliberate deviation: the reference
+   * accepts any n_annuli * n_sectors >= 2 (gather.cpp:49-50); the device
+   * keeps at most 32 sectors per region and fppm_gpu_create returns
+   * FPPM_ERR_CAPACITY above that (the product is formed in 64 bits). */
   int32_t n_annuli;
   int32_t n_sectors;
   double alpha_f;
@@ -116,7 +119,14 @@ typedef struct fppm_hitpoints {
   const uint8_t *gathered;  /* integrator.cpp:476-488 */
 } fppm_hitpoints;
 
-/* Photons = light vertices (LightVertex, path.hpp:76-89), canonical fp32. */
+/* Photons = light vertices (LightVertex, path.hpp:76-89), canonical fp32.
+ * The reference's LightVertex is fp64: a caller binding real LightVertex
+ * data rounds position, normal and wi to fp32 here, and every predicate
+ * (cell_coord, ball, guard, disk, sector) then runs on the rounded values
+ * widened back to fp64.  Parity with the reference is bit-exact for
+ * fp32-representable inputs (all synthetic workloads); for arbitrary fp64
+ * positions a photon within ~2^-24 relative of a cell, ball, disk or sector
+ * boundary may be classified differently. */
 typedef struct fppm_photons {
   const float *pos;     /* [n][3] */
   const float *normal;  /* [n][3] shading normal at the deposit */

@@ -136,6 +136,7 @@ class Oracle:
             self._c5p = fn("c5_photons", None, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64] + [C.c_void_p] * 5)
         else:
             self._si = fn("session_iterate", C.c_int, [C.c_void_p, C.c_uint64, _fp, _fp, _fp, _fp, _u32p, C.c_size_t, C.c_double, _u32p, C.c_size_t, C.POINTER(IterOut), _dp, _dp])
+            self._si64 = fn("session_iterate_f64", C.c_int, [C.c_void_p, C.c_uint64, _dp, _dp, _dp, _dp, _u32p, C.c_size_t, C.c_double, _u32p, C.c_size_t, C.POINTER(IterOut), _dp, _dp])
             self._anova = fn("anova_f_test", None, [_u64p, _dp, _dp, C.c_int, C.c_uint64, C.c_double, _dp, _ip])
             self._hw = fn("hardware_threads", C.c_uint, [])
             self._scn = fn("scene_create", C.c_void_p, [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -489,18 +490,21 @@ class _Session:
         for k in OUT_FIELDS:
             t = IterOut._fields_[[f[0] for f in IterOut._fields_].index(k)][1]
             setattr(io, k, _ptr(out[k], t))
-        arrs = [np.ascontiguousarray(ph[k], np.float32) for k in ("pos", "nrm", "wi", "pow")]
+        # fp64: the reference tracer's own LightVertex values (reference build only)
+        f64 = ph["pos"].dtype == np.float64 and self.o.kind != "port"
+        ft, pt = (np.float64, _dp) if f64 else (np.float32, _fp)
+        arrs = [np.ascontiguousarray(ph[k], ft) for k in ("pos", "nrm", "wi", "pow")]
         depth = np.ascontiguousarray(ph["depth"], np.uint32)
         sub = None if subset is None else np.ascontiguousarray(subset, np.uint32)
         N = len(depth)
-        args = [self.h, iteration, *[_ptr(a, _fp) for a in arrs], _ptr(depth, _u32p), N,
+        args = [self.h, iteration, *[_ptr(a, pt) for a in arrs], _ptr(depth, _u32p), N,
                 float(cell), _ptr(sub, _u32p), 0 if sub is None else len(sub), C.byref(io)]
         if self.o.kind == "port":
             rc = self.o._si(*args)
             times = None
         else:
             gs, ts = C.c_double(0), C.c_double(0)
-            rc = self.o._si(*args, C.byref(gs), C.byref(ts))
+            rc = (self.o._si64 if f64 else self.o._si)(*args, C.byref(gs), C.byref(ts))
             times = (gs.value, ts.value)
         _raise(rc)
         out["times"] = times

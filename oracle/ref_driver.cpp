@@ -324,11 +324,14 @@ double ref_session_max_radius(void* sp) {
 // double, then gathers + tests every selected hit point exactly as
 // Renderer::pixel_pm does (integrator.cpp:407-490) for a first-hit diffuse
 // gather point.  grid_seconds / gather_seconds receive steady-clock timings.
-int ref_session_iterate(void* sp, uint64_t iteration, const float* ppos,
-                        const float* pnrm, const float* pwi, const float* ppow,
-                        const uint32_t* pdepth, size_t N, double cell_size,
-                        const uint32_t* subset, size_t nsub, RefIterOut* out,
-                        double* grid_seconds, double* gather_seconds) {
+// Photon fields as float (the device's canonical records) or double (the
+// reference tracer's own LightVertex values, for attributing fp32 narrowing).
+}  // extern "C"
+template <typename T>
+static int session_iterate(void* sp, uint64_t iteration, const T* ppos, const T* pnrm, const T* pwi,
+                           const T* ppow, const uint32_t* pdepth, size_t N, double cell_size,
+                           const uint32_t* subset, size_t nsub, RefIterOut* out,
+                           double* grid_seconds, double* gather_seconds) {
   auto* s = static_cast<RefSession*>(sp);
   const RefConfig& cfg = s->cfg;
   double cell = cell_size;
@@ -450,6 +453,23 @@ int ref_session_iterate(void* sp, uint64_t iteration, const float* ppos,
   if (grid_seconds) *grid_seconds = std::chrono::duration<double>(t1 - t0).count();
   if (gather_seconds) *gather_seconds = std::chrono::duration<double>(t2 - t1).count();
   return failure;
+}
+extern "C" {
+
+int ref_session_iterate(void* sp, uint64_t iteration, const float* ppos, const float* pnrm, const float* pwi,
+                        const float* ppow, const uint32_t* pdepth, size_t N, double cell_size,
+                        const uint32_t* subset, size_t nsub, RefIterOut* out, double* grid_seconds,
+                        double* gather_seconds) {
+  return session_iterate<float>(sp, iteration, ppos, pnrm, pwi, ppow, pdepth, N, cell_size, subset, nsub, out,
+                                grid_seconds, gather_seconds);
+}
+
+int ref_session_iterate_f64(void* sp, uint64_t iteration, const double* ppos, const double* pnrm,
+                            const double* pwi, const double* ppow, const uint32_t* pdepth, size_t N,
+                            double cell_size, const uint32_t* subset, size_t nsub, RefIterOut* out,
+                            double* grid_seconds, double* gather_seconds) {
+  return session_iterate<double>(sp, iteration, ppos, pnrm, pwi, ppow, pdepth, N, cell_size, subset, nsub, out,
+                                 grid_seconds, gather_seconds);
 }
 
 // ---- light phase (Renderer::light_phase, integrator.cpp:230-265) ----------

@@ -102,8 +102,12 @@ struct fppm_gpu_ctx {
   unsigned long long cell_cap = 0;
   fppm_b200::GridHeader *d_hdr = nullptr, *h_hdr = nullptr;
   long long *d_bounds = nullptr, *h_bounds_init = nullptr;
-  double *d_cell = nullptr, *h_cell = nullptr;
+  double *d_cell = nullptr, *h_cell = nullptr, *d_cell_chk = nullptr;
   bool grid_valid = false;
+  // the reference throws when a query radius exceeds the cell size
+  // (photon_map.cpp:57-58); checked before the next gather whenever the cell
+  // did not come from the max live radius or radii were raised (set_regions)
+  bool grid_explicit = false, rcheck = false;
 
   // outputs
   double *o_gather_r = nullptr, *o_stat = nullptr, *o_crit = nullptr, *o_flux = nullptr;
@@ -187,13 +191,13 @@ static cudaError_t ensure_scratch(fppm_gpu_ctx *ctx, size_t bytes) {
 }
 
 __global__ void k_max_radius(const double *__restrict__ radius, uint32_t H,
-                             double *__restrict__ out) {
+                             double *__restrict__ out, const uint8_t *__restrict__ gathered = nullptr) {
   __shared__ unsigned long long s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
   double m = 0.0;
   for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x)
-    m = fmax(m, radius[h]);
+    if (gathered == nullptr || gathered[h]) m = fmax(m, radius[h]);
   atomicMax(&s, (unsigned long long)__double_as_longlong(m));
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long *>(out), s);
@@ -375,8 +379,10 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   if (!(c.k > 0 && c.k < 1)) return FPPM_ERR_INVALID_ARGUMENT;
   if (!(c.alpha >= 0.5 && c.alpha < 1)) return FPPM_ERR_INVALID_ARGUMENT;
   if (!(c.r_min_base > 0 && c.r_min_base <= c.initial_radius)) return FPPM_ERR_INVALID_ARGUMENT;
-  if (c.n_annuli < 1 || c.n_sectors < 1 || c.n_annuli * c.n_sectors < 2) return FPPM_ERR_INVALID_ARGUMENT;
-  if (c.n_annuli * c.n_sectors > 32) return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.n_annuli < 1 || c.n_sectors < 1 || (long long)c.n_annuli * c.n_sectors < 2) return FPPM_ERR_INVALID_ARGUMENT;
+  // deliberate deviation: the reference accepts any n_a * n_s >= 2
+  // (gather.cpp:49-50); the device keeps at most 32 sectors per region
+  if ((long long)c.n_annuli * c.n_sectors > 32) return FPPM_ERR_CAPACITY;
   if (c.channels != FPPM_CHANNELS_LUMINANCE && c.channels != FPPM_CHANNELS_RGB) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy < FPPM_POLICY_FTEST || c.policy > FPPM_POLICY_SCHEDULE) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.gather_kernel < 0 || c.gather_kernel > 5) return FPPM_ERR_INVALID_ARGUMENT;
@@ -428,6 +434,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->sort.keys_b, Nc)); A(dalloc(&ctx->sort.vals_b, Nc));
   A(dalloc(&ctx->sort.hist, radix_hist_entries((uint32_t)Nc)));
   A(dalloc(&ctx->d_hdr, 1)); A(dalloc(&ctx->d_bounds, 6)); A(dalloc(&ctx->d_cell, 1));
+  A(dalloc(&ctx->d_cell_chk, 1));
   A(cudaMallocHost(&ctx->h_hdr, sizeof(GridHeader)));
   A(cudaMallocHost(&ctx->h_bounds_init, sizeof(long long) * 6));
   A(cudaMallocHost(&ctx->h_cell, sizeof(double)));
@@ -491,7 +498,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
                  ctx->recs.rec0, ctx->recs.rec1, ctx->recs.rec2, ctx->recs.rec3, ctx->recs.pack,
                  ctx->sort.keys_a,
                  ctx->sort.vals_a, ctx->sort.keys_b, ctx->sort.vals_b, ctx->sort.hist,
-                 ctx->d_cell_start, ctx->d_hdr, ctx->d_bounds, ctx->d_cell,
+                 ctx->d_cell_start, ctx->d_hdr, ctx->d_bounds, ctx->d_cell, ctx->d_cell_chk,
                  ctx->o_gather_r, ctx->o_stat, ctx->o_crit, ctx->o_flux, ctx->o_flags, ctx->o_rad,
                  ctx->o_acc, ctx->o_tested, ctx->o_rejected, ctx->o_t64,
                  ctx->snap_cnt, ctx->snap_sum, ctx->snap_sq, ctx->d_counters,
@@ -576,6 +583,7 @@ static int finish_hitpoints(fppm_gpu_ctx *ctx, uint32_t n, bool has_gathered) {
   FPPM_CUDA_OK(launch_hit_weights(ctx->stream, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb, n, ctx->d_K));
   const bool reset = n != ctx->H;
   ctx->H = n;
+  if (ctx->grid_explicit) ctx->rcheck = true;  // a newly gathered region may exceed the cell
   if (reset) return fppm_gpu_reset_regions(ctx);
   return FPPM_OK;
 }
@@ -700,7 +708,10 @@ int fppm_gpu_set_regions(fppm_gpu_ctx *ctx, const double *radius, const uint64_t
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   const size_t H = ctx->H, CG = (size_t)ctx->G * ctx->C;
   cudaStream_t s = ctx->stream;
-  if (radius) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_radius, radius, sizeof(double) * H, cudaMemcpyHostToDevice, s));
+  if (radius) {
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_radius, radius, sizeof(double) * H, cudaMemcpyHostToDevice, s));
+    ctx->rcheck = true;  // radii may now exceed the built grid's cell
+  }
   if (stat_count) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_st_cnt, stat_count, 8 * H * CG, cudaMemcpyHostToDevice, s));
   if (stat_sum) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_st_sum, stat_sum, 8 * H * CG, cudaMemcpyHostToDevice, s));
   if (stat_sum_sq) FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_st_sq, stat_sum_sq, 8 * H * CG, cudaMemcpyHostToDevice, s));
@@ -720,12 +731,12 @@ int fppm_gpu_set_regions(fppm_gpu_ctx *ctx, const double *radius, const uint64_t
   return FPPM_OK;
 }
 
-static int device_max_radius(fppm_gpu_ctx *ctx, double *dst) {
+static int device_max_radius(fppm_gpu_ctx *ctx, double *dst, const uint8_t *gathered = nullptr) {
   FPPM_CUDA_OK(cudaMemsetAsync(dst, 0, sizeof(double), ctx->stream));
   if (ctx->H) {
     unsigned blocks = (ctx->H + 255) / 256;
     blocks = std::min<unsigned>(blocks, (unsigned)ctx->sms * 4);
-    k_max_radius<<<blocks, 256, 0, ctx->stream>>>(ctx->d_radius, ctx->H, dst);
+    k_max_radius<<<blocks, 256, 0, ctx->stream>>>(ctx->d_radius, ctx->H, dst, gathered);
     note_launches(1);
     FPPM_CUDA_OK(cudaGetLastError());
   }
@@ -862,8 +873,9 @@ int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
   if (workload == FPPM_WORKLOAD_C5 && !ctx->c5.pos) return fail(ctx, FPPM_ERR_STATE, "C5 photons before c5_setup");
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
-  if (ctx->stage_pending == 0 || ctx->pf_set == 0)
-    FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[0], 0));
+  // a superseded upload into set 0 may still run on the copy stream: order
+  // the generator after it (a no-op once the copy has finished)
+  if (ctx->cstream) FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[0], 0));
   ctx->stage_pending = -1;
   ctx->pf_set = -1;  // set 0 is rewritten
   if (workload == FPPM_WORKLOAD_C5) {
@@ -928,6 +940,8 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   cudaStream_t s = ctx->stream;
   ctx->grid_valid = false;
+  ctx->grid_explicit = cell_size > 0.0;
+  ctx->rcheck = ctx->grid_explicit;
   if (cell_size > 0.0) {
     *ctx->h_cell = cell_size;
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_cell, ctx->h_cell, sizeof(double), cudaMemcpyHostToDevice, s));
@@ -1204,6 +1218,16 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
                        fppm_gpu_summary *summary, double *delta) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "gather before build_grid");
+  if (ctx->rcheck && ctx->N > 0) {
+    // photon_map.cpp:57-58: every gathered region's radius must fit the cell
+    int rc0 = device_max_radius(ctx, ctx->d_cell_chk, ctx->d_gathered);
+    if (rc0) return rc0;
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_cell, ctx->d_cell_chk, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_cell > ctx->h_hdr->cell)
+      return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "PhotonGrid: query radius exceeds cell size");
+    ctx->rcheck = false;
+  }
   const bool dbg = std::getenv("FPPM_DEBUG") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };

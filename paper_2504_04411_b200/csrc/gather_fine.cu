@@ -543,8 +543,8 @@ static __device__ __forceinline__ void fine_accumulate(const HitV &K, bool acc, 
     }
     const uint32_t a = slots + (uint32_t)(sector * 32 + lane) * 16u;
     double2 o = lds_f64x2(a);
-    o.x += v;
-    o.y += v * v;
+    o.x = da(o.x, v);          // SectorStats::add: sum += v; sum_sq += v * v
+    o.y = da(o.y, dm(v, v));   // (stat_tests.hpp:18-22), v * v rounded alone
     sts_f64x2(a, o);
   } else {
     const double v[3] = {acc ? (cos_pos ? dm(K.K0, pr) : K.Kz0) : 0.0,
@@ -554,8 +554,8 @@ static __device__ __forceinline__ void fine_accumulate(const HitV &K, bool acc, 
     for (int c = 0; c < 3; ++c) {
       const uint32_t a = slots + (uint32_t)((c * GMAX + sector) * 32 + lane) * 16u;
       double2 o = lds_f64x2(a);
-      o.x += v[c];
-      o.y += v[c] * v[c];
+      o.x = da(o.x, v[c]);
+      o.y = da(o.y, dm(v[c], v[c]));
       sts_f64x2(a, o);
     }
   }

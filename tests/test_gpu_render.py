@@ -73,31 +73,85 @@ def test_render_iterations_match_oracle(port):
     assert n == 4 and img.shape == (48, 48, 3) and np.isfinite(img).all() and img.max() > 0
 
 
-def test_film_matches_reference_render(ref):
-    """The whole FPPM render against the reference's render() (same scene,
-    camera, seed, J, iterations; reference defaults 2x6, alpha_F = 0.01,
-    r1 = 0.002 R_bb)."""
-    sc, cam = caustic_box(), caustic_box_camera(32)
-    npix, J, iters = cam.width * cam.height, 30000, 4
+def _attributed_render(ref, sc, cam, J, iters, seed, channels="luminance"):
+    """The whole FPPM render on the device against the reference's render()
+    (reference defaults 2x6, alpha_F = 0.01, r1 = 0.002 R_bb), with every
+    difference attributed.
+
+    Two reference sessions (oracle/_ref: the reference's own PhotonGrid and
+    GatherRegion) replay each iteration on the reference eye pass: A with the
+    reference tracer's fp64 photons, B with the device's fp32 photons.
+      * A reproduces render() bit for bit (film and radii): the harness is the
+        reference;
+      * the device reproduces B exactly (counts, decisions, radii; fp64 sums
+        to summation order): the device is the reference on its inputs;
+      * the device's photons are the reference's rounded to fp32 (except
+        coordinates within 1e-12 of zero: device vs glibc sin/cos);
+    so every pixel whose radius or film differs structurally from render()
+    must be a pixel where A and B accept a different photon set or decide
+    differently -- a photon whose fp32 rounding crosses a cell, ball, disk,
+    annulus or sector boundary.  Everywhere else the film differs only by the
+    fp32 rounding of photon power: <= 1e-6 relative (measured ~4e-8)."""
+    npix = cam.width * cam.height
     r1 = 0.002 * bounding_radius(sc)
-    ctx = _ctx(npix, J, r1)
+    ctx = _ctx(npix, J, r1, channels=channels)
     ctx.set_scene(sc)
     ctx.set_camera(cam)
+    rs = ref.scene(sc.arrays())
+    cfg = dict(n_annuli=2, n_sectors=6, alpha_f=0.01, initial_radius=r1, r_min_base=0.001 * r1,
+               samples_per_iteration=J, max_depth=8, threads=8, channels=3 if channels == "rgb" else 1)
+    sA = sB = None
+    film_a, film_b = np.zeros((npix, 3)), np.zeros((npix, 3))
+    fp32_px = np.zeros(npix, bool)
     for it in range(1, iters + 1):
-        ctx.render_iteration(21, it, J, 8)
+        got, _ = ctx.render_iteration(seed, it, J, 8, outputs=True, stats=True)
+        hit = ctx.get_hitpoints(emitted=True)
+        eye = rs.eye_pass(cam, seed, it, 8)
+        for k in ("pos", "nrm", "wo", "thr", "alb", "emitted", "gathered", "eye_depth"):
+            assert np.array_equal(hit[k], eye[k]), k
+        ph32 = ctx.get_photons()
+        ph64 = rs.trace(seed, it, J, 8)
+        assert np.array_equal(ph32["depth"], ph64["depth"])
+        for k in ("pos", "nrm", "wi", "pow"):
+            d = ph32[k] != ph64[k].astype(np.float32)
+            assert not (d & (np.abs(ph64[k]) > 1e-12)).any(), k
+        if sA is None:
+            sA, sB = ref.session(cfg, eye), ref.session(cfg, eye)
+        else:
+            sA.set_hitpoints(eye)
+            sB.set_hitpoints(eye)
+        wa, wb = sA.iterate(it, ph64), sB.iterate(it, ph32)
+        compare_iteration(got, wb)
+        fp32_px |= (wa["radius"] != wb["radius"]) | (wa["accepted"] != wb["accepted"]) | \
+            (wa["rejected"] != wb["rejected"]) | (wa["tested"] != wb["tested"])
+        film_a = film_a + (eye["emitted"] + wa["radiance"])   # Film::add_iteration (film.cpp:21-26)
+        film_b = film_b + (eye["emitted"] + wb["radiance"])
+    film, radius, _ = rs.render_fppm(cam, seed, iters, 8, J, r0_frac=0.002, n_annuli=2, n_sectors=6,
+                                     alpha_f=0.01, threads=8)
+    assert np.array_equal(film_a / iters, film), "session A is not the reference render()"
+    assert np.array_equal(wa["radius"], radius)
     img, n = ctx.film_mean()
     assert n == iters
-    rs = ref.scene(sc.arrays())
-    film, radius, _ = rs.render_fppm(cam, 21, iters, 8, J, r0_frac=0.002, n_annuli=2, n_sectors=6,
-                                     alpha_f=0.01, threads=8)
-    got = img.reshape(-1, 3)
-    rel = np.abs(got - film) / np.maximum(np.abs(film), 1e-30)
-    bad = (rel > 1e-5).any(-1) & (np.abs(got - film) > 1e-12).any(-1)
-    print(f"film: {bad.sum()} of {npix} pixels outside 1e-5 relative; max rel "
-          f"{rel[~bad].max() if (~bad).any() else 0:.2e} elsewhere")
-    assert bad.sum() <= max(2, npix // 200)
+    got_film = img.reshape(-1, 3)
+    np.testing.assert_allclose(got_film, film_b / iters, rtol=1e-12, atol=1e-300)
+    rel = (np.abs(got_film - film) / np.maximum(np.abs(film), 1e-300)).max(-1)
+    bad = rel > 1e-6
     rad = ctx.regions()["radius"]
-    assert (rad == radius).mean() >= 0.99
+    unexplained = (bad | (rad != radius)) & ~fp32_px
+    mx = rel[~fp32_px].max() if (~fp32_px).any() else 0.0
+    print(f"film vs render(): {bad.sum()} of {npix} pixels beyond 1e-6 relative, "
+          f"{(rad != radius).sum()} radii differ; fp32 rounding changes the accepted set or a decision at "
+          f"{fp32_px.sum()} pixels; unexplained {unexplained.sum()}; max rel elsewhere {mx:.1e}")
+    assert not unexplained.any(), np.flatnonzero(unexplained)[:10]
+    assert mx <= 1e-6
+    return int(fp32_px.sum())
+
+
+def test_film_matches_reference_render(ref):
+    """The whole FPPM render against the reference's render(), every
+    difference attributed (see _attributed_render)."""
+    sc, cam = caustic_box(), caustic_box_camera(32)
+    _attributed_render(ref, sc, cam, 30000, 4, 21)
 
 
 def test_render_api_errors():
@@ -138,21 +192,7 @@ sphere center=(0.45,-0.62,-0.1) radius=0.3 material=glass
 def test_scene_text_render_matches_reference(ref):
     """A scene in the reference's text format (chromatic light -> the RGB test
     channels the reference auto-detects), rendered on the device and by the
-    reference's render()."""
+    reference's render(), every difference attributed."""
     from paper_2504_04411_b200.scene_text import parse_scene
     sc, cam = parse_scene(SCENE_TEXT)
-    npix, J, iters = cam.width * cam.height, 20000, 3
-    r1 = 0.002 * bounding_radius(sc)
-    ctx = _ctx(npix, J, r1, channels="rgb")
-    ctx.set_scene(sc)
-    ctx.set_camera(cam)
-    for it in range(1, iters + 1):
-        ctx.render_iteration(5, it, J, 8)
-    img, _ = ctx.film_mean()
-    film, radius, _ = ref.scene(sc.arrays()).render_fppm(cam, 5, iters, 8, J, r0_frac=0.002, n_annuli=2,
-                                                         n_sectors=6, alpha_f=0.01, threads=8)
-    got = img.reshape(-1, 3)
-    rel = np.abs(got - film) / np.maximum(np.abs(film), 1e-30)
-    bad = (rel > 1e-5).any(-1) & (np.abs(got - film) > 1e-12).any(-1)
-    assert bad.sum() <= max(2, npix // 200), bad.sum()
-    assert (ctx.regions()["radius"] == radius).mean() >= 0.99
+    _attributed_render(ref, sc, cam, 20000, 3, 5, channels="rgb")
