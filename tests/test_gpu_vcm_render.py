@@ -9,8 +9,9 @@ seed, J and iterations.
 The device restates every step in fp64 without FMA in the reference's
 operation order with the reference's RNG streams; the photons of the merge
 gathers are the canonical fp32 records and device sin/cos differ from glibc
-in the last bits, so the film is compared at the north-star radiance
-tolerance (1e-5 relative) on all but a reported handful of pixels."""
+in the last bits; on these scenes and seeds no rounded photon crosses a
+kernel boundary, so every tested radius is identical and every pixel agrees
+within 1e-6 relative (measured <= 3e-8; the north-star tolerance is 1e-5)."""
 import numpy as np
 import pytest
 
@@ -29,8 +30,8 @@ def _vcm_ctx(npix, J, r1, max_depth=8, **kw):
 
 def _compare(got, want, label):
     rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
-    bad = (rel > 1e-5).any(-1) & (np.abs(got - want) > 1e-12).any(-1)
-    print(f"{label}: {bad.sum()} of {len(want)} pixels outside 1e-5 relative; max rel "
+    bad = (rel > 1e-6).any(-1) & (np.abs(got - want) > 1e-12).any(-1)
+    print(f"{label}: {bad.sum()} of {len(want)} pixels outside 1e-6 relative; max rel "
           f"{rel[~bad].max() if (~bad).any() else 0:.2e} elsewhere; mean got {got.mean():.6g} want {want.mean():.6g}")
     return bad
 
@@ -55,9 +56,12 @@ def test_vcm_film_matches_reference_render(ref, res, J, iters, kernel):
     film, radius, _ = rs.render_vcm_plus(cam, 17, iters, 8, J, r0_frac=0.002, n_annuli=2, n_sectors=6,
                                          alpha_f=0.01, threads=8)
     bad = _compare(img.reshape(-1, 3), film, f"vcm+ {res}^2 J={J} {kernel}")
-    assert bad.sum() <= max(2, npix // 100)
+    # measured: every pixel within 3e-8 and every tested radius identical on
+    # these seeds; a fp32-rounded merge photon on a kernel boundary would show
+    # up here as a radius difference (see test_gpu_render._attributed_render)
+    assert bad.sum() == 0
     rad = ctx.regions()["radius"]
-    assert (rad == radius).mean() >= 0.99
+    assert np.array_equal(rad, radius)
 
 
 def test_vcm_render_api_errors():
@@ -105,5 +109,5 @@ def test_vcm_other_scenes_match_reference_render(ref, which):
     film, radius, _ = ref.scene(sc.arrays()).render_vcm_plus(cam, 29, iters, 8, J, r0_frac=0.002, n_annuli=2,
                                                              n_sectors=6, alpha_f=0.01, threads=8)
     bad = _compare(img.reshape(-1, 3), film, f"vcm+ {which}")
-    assert bad.sum() <= max(2, npix // 100)
-    assert (ctx.regions()["radius"] == radius).mean() >= 0.99
+    assert bad.sum() == 0
+    assert np.array_equal(ctx.regions()["radius"], radius)
