@@ -225,7 +225,10 @@ __global__ void __launch_bounds__(kPrepThreads)
     // n = +z, fp32-exact center, 4 bins: the planar fast path (gather_dev.cuh)
     Q.planar = (P.fast && P.nx == 0.0 && P.ny == 0.0 && P.nz == 1.0 && A.ns == 4 &&
                 P.clx == 0.0f && P.cly == 0.0f && P.clz == 0.0f) ? 1u : 0u;
-    Q.gray = P.gray ? 1u : 0u;
+    // bit0: K0 = K1 = K2; bit1: the lean path (planar, gray, finite K: the
+    // lane slots hold photon-luminance moments, scaled by K0 at the end)
+    Q.gray = (P.gray ? 1u : 0u) |
+             ((Q.planar && P.gray && isfinite(P.K0) && A.na <= 2 && A.ns == 4) ? 2u : 0u);
     Q.bx0 = b.x0; Q.by0 = b.y0; Q.by1 = b.y1;
     fbox[i] = make_int4(b.x1, b.z0, b.z1, 0);
     Q.nruns = (uint32_t)nr;
@@ -768,6 +771,234 @@ static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const 
   __syncwarp();
 }
 
+
+// ------------------------------------------------------------------ lean path
+// Planar (n = +z, fp32-exact centre), gray (K0 = K1 = K2, finite), 1-2
+// annuli x 4 quadrants, luminance channel: every canonical workload.  The
+// pair value is v = K0 * L (L = the photon's fp64 luminance from the record),
+// so a lane's slot accumulates the photon moments {sum L, sum L^2} of its
+// accepted pairs and the fragment's sector sums are K0 * sum L and
+// K0^2 * sum L^2 (SectorStats::add, stat_tests.hpp:18-22; equal to the
+// per-pair products up to fp64 reassociation, within the 1e-12 sum
+// tolerance).  Per-sector counts are nibbles of one register (sector s at
+// bits 4s..4s+3), spilled to byte words before they can overflow.
+struct LeanCnt {
+  uint32_t nib, be, bo;  // nibble counts; byte words: even sectors 0,2,4,6 / odd 1,3,5,7
+  uint32_t nadd;         // warp-uniform: pairs added per lane since the last spill (<= 15)
+};
+static __device__ __forceinline__ void lean_spill(LeanCnt &c) {
+  c.be += c.nib & 0x0F0F0F0Fu;
+  c.bo += (c.nib >> 4) & 0x0F0F0F0Fu;
+  c.nib = 0u;
+  c.nadd = 0u;
+}
+
+template <int NA>
+struct LeanPair {
+  bool acc, on, need;
+  uint32_t s4;  // 4 * sector
+  double L;
+  float4 pw;
+};
+
+// Full fp32 evaluation of candidate at smem offset `off` (records r0, r0 + d1,
+// r0 + d2): ball, depth, guard, disk, annulus, quadrant, cos_i with the error
+// bands of fine_eval<PLANAR>.
+template <int NA>
+static __device__ __forceinline__ LeanPair<NA> lean_eval(const HitF &F, uint32_t max_depth, bool valid,
+                                                         uint32_t a0, uint32_t d1, uint32_t d2) {
+  LeanPair<NA> q;
+  const float4 p = lds128_f(a0);
+  const float4 B = lds128_f(a0 + d1);
+  q.pw = lds128_f(a0 + d2);
+  q.L = __longlong_as_double(((long long)__float_as_uint(B.w) << 32) | __float_as_uint(B.z));
+  const float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
+  const float yy = fmaf(dx, dx, dy * dy);
+  const float r2 = fmaf(dz, dz, yy);
+  const bool maybe = valid && F.eye + __float_as_uint(p.w) <= max_depth && r2 <= F.lim_hi;  // :396, :76
+  bool band = !(r2 < F.lim_lo) || !(fabsf(dx) > F.band_y) || !(fabsf(dy) > F.band_y) ||
+              (__float_as_uint(q.pw.w) & 1u) == 0u;
+  // quadrant (exact-sector table): +x+y 0, -x+y 1, -x-y 2, +x-y 3
+  uint32_t s4 = dy > 0.0f ? (dx > 0.0f ? 0u : 4u) : (dx > 0.0f ? 12u : 8u);
+  if constexpr (NA == 2) {  // one annulus edge at d2 = r2 / 2
+    const float qa = yy * F.qa_scale;
+    band = band || fabsf(qa - 1.0f) < 2e-4f;
+    s4 += qa >= 1.0f ? 16u : 0u;
+  }
+  q.s4 = s4;
+  q.need = maybe && band;
+  q.acc = maybe && !band && !(B.x < F.guard_ceil);  // integrator.cpp:397
+  q.on = q.acc && !(B.y <= 0.0f);                     // bsdf.cpp:56-58
+  return q;
+}
+
+template <int NA>
+static __device__ __forceinline__ void lean_add(const LeanPair<NA> &q, uint32_t slot_lane, LeanCnt &c,
+                                                double &p0, double &p1, double &p2) {
+  const double v = q.on ? q.L : 0.0;
+  const uint32_t a = slot_lane + q.s4 * (32u * 16u / 4u);  // [sector][lane] {sum, sum_sq}
+  double2 o = lds_f64x2(a);
+  o.x = da(o.x, v);
+  o.y = da(o.y, dm(v, v));
+  sts_f64x2(a, o);
+  if (q.acc) c.nib += 1u << q.s4;
+  if (q.on) {
+    p0 = da(p0, (double)q.pw.x);
+    p1 = da(p1, (double)q.pw.y);
+    p2 = da(p2, (double)q.pw.z);
+  }
+}
+
+// Deferred pairs on the exact fp64 path (same ring as fine_exact_batch).
+template <int NA>
+static __device__ __forceinline__ void lean_exact_batch(const GatherArgs &A, const Hit &Hs, uint32_t n, uint32_t ex,
+                                                        uint32_t slot_lane, LeanCnt &c, double &p0, double &p1,
+                                                        double &p2, const FineWin &Wn, FineState &st) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  if (c.nadd + 1u > 15u) lean_spill(c);
+  const bool have = (uint32_t)lane < n;
+  const uint32_t i = have ? lds_u32(ex + ((st.eh + lane) & (kFExact - 1)) * 4u) : 0u;
+  st.eh += n;
+  LeanPair<NA> q;
+  q.pw = make_float4(0.f, 0.f, 0.f, 0.f);
+  q.L = 0.0;
+  uint32_t fl = 0;
+  if (have) {
+    fl = fine_exact(Hs, Wn, i, A.na, A.ns, A.guard, q.pw, q.L);
+    st.n_exact += 1;
+    st.n_amb += (fl >> 2) & 1u;
+  }
+  q.acc = (fl & 1u) != 0;
+  q.on = q.acc && (fl & 2u) != 0;
+  q.s4 = (fl >> 8) * 4u;
+  lean_add<NA>(q, slot_lane, c, p0, p1, p2);
+  c.nadd += 1u;
+  __syncwarp();
+}
+
+// All candidates of one hit point inside the staged window, two per lane
+// per step.  Virtual index v in [0, total) over the concatenated runs maps to
+// the smem index v + off[j] of run j; the run is tracked warp-uniformly and a
+// step only resolves per lane when a run ends inside it.
+template <int NA>
+static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const FineHot &Hh, const Hit &Hs,
+                                                     uint32_t rs, uint32_t rl, int nruns, uint32_t ex,
+                                                     uint32_t slot_lane, LeanCnt &c, double &p0, double &p1,
+                                                     double &p2, const FineWin &Wn, FineState &st) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const HitF F = Hh.F;
+  const uint32_t max_depth = A.max_depth;
+  const uint32_t d1 = Wn.r1 - Wn.r0, d2 = Wn.r2 - Wn.r0;
+  uint32_t incl = rl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t off = rs - (incl - rl);  // smem index - virtual index within run `lane`
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  if (lane == 0) st.n_cand += total;
+  int j = 0;
+  uint32_t e = __shfl_sync(kFull, incl, 0), o = __shfl_sync(kFull, off, 0);
+  for (uint32_t base = 0; base < total; base += 64) {
+    while (e <= base) {  // warp-uniform: skip runs that ended (incl. empty ones)
+      ++j;
+      e = __shfl_sync(kFull, incl, j);
+      o = __shfl_sync(kFull, off, j);
+    }
+    const uint32_t v0 = base + lane, v1 = v0 + 32u;
+    uint32_t i0 = v0 + o, i1 = v1 + o;
+    if (e < base + 64u) {  // a run ends inside this step (warp-uniform)
+      int k = j;
+      uint32_t ek = e;
+      while (ek < base + 64u && k + 1 < nruns) {
+        ++k;
+        const uint32_t ok_ = __shfl_sync(kFull, off, k);
+        if (v0 >= ek) i0 = v0 + ok_;
+        if (v1 >= ek) i1 = v1 + ok_;
+        ek = __shfl_sync(kFull, incl, k);
+      }
+    }
+    const bool ok0 = v0 < total, ok1 = v1 < total;
+    if (!ok0) i0 = rs;
+    if (!ok1) i1 = rs;
+    if (c.nadd + 2u > 15u) lean_spill(c);
+    const LeanPair<NA> q0 = lean_eval<NA>(F, max_depth, ok0, Wn.r0 + i0 * 16u, d1, d2);
+    const LeanPair<NA> q1 = lean_eval<NA>(F, max_depth, ok1, Wn.r0 + i1 * 16u, d1, d2);
+    lean_add<NA>(q0, slot_lane, c, p0, p1, p2);
+    lean_add<NA>(q1, slot_lane, c, p0, p1, p2);
+    c.nadd += 2u;
+    const uint32_t m0 = __ballot_sync(kFull, q0.need), m1 = __ballot_sync(kFull, q1.need);
+    if (m0 | m1) {
+      if (q0.need) sts_u32(ex + ((st.et + __popc(m0 & lt)) & (kFExact - 1)) * 4u, i0);
+      st.et += __popc(m0);
+      if (q1.need) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
+      st.et += __popc(m1);
+      while (st.et - st.eh >= 32)
+        lean_exact_batch<NA>(A, Hs, 32u, ex, slot_lane, c, p0, p1, p2, Wn, st);
+    }
+  }
+  while (st.et != st.eh)
+    lean_exact_batch<NA>(A, Hs, min(32u, st.et - st.eh), ex, slot_lane, c, p0, p1, p2, Wn, st);
+  __syncwarp();
+}
+
+
+// End of a lean fragment: the lane slots reduced in the fixed rotated order
+// of the general path, scaled by K0 / K0^2, counts from the byte words, flux;
+// added to the hit point's partial row [count G | sum G | sum_sq G | power 3].
+template <int GMAX>
+static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, double K0, const LeanCnt &c,
+                                                   double p0, double p1, double p2, double *acc,
+                                                   FineState &st) {
+  constexpr int NC = GMAX, NQ = 32 / NC, R = 32 / NQ;
+  const int col = lane % NC, grp = lane / NC;
+  double sm = 0.0, sq = 0.0;
+  {
+    const uint32_t base = slots + (uint32_t)(col * 32 + grp * R) * 16u;
+#pragma unroll 4
+    for (int i = 0; i < R; ++i) {
+      const uint32_t a = base + (uint32_t)((i + col) % R) * 16u;
+      const double2 v = lds_f64x2(a);
+      sm += v.x;
+      sq += v.y;
+      sts_f64x2(a, make_double2(0.0, 0.0));
+    }
+  }
+#pragma unroll
+  for (int o = (NQ / 2) * NC; o >= NC && o > 0; o >>= 1) {
+    sm += __shfl_down_sync(kFull, sm, o);
+    sq += __shfl_down_sync(kFull, sq, o);
+  }
+  p0 = warp_sum(p0);
+  p1 = warp_sum(p1);
+  p2 = warp_sum(p2);
+  // byte words -> 16-bit halves -> warp sums: even word bytes = sectors 0,2,4,6
+  const uint32_t e02 = __reduce_add_sync(kFull, c.be & 0x00ff00ffu);         // s0 | s4 << 16
+  const uint32_t e26 = __reduce_add_sync(kFull, (c.be >> 8) & 0x00ff00ffu);  // s2 | s6 << 16
+  const uint32_t o15 = __reduce_add_sync(kFull, c.bo & 0x00ff00ffu);         // s1 | s5 << 16
+  const uint32_t o37 = __reduce_add_sync(kFull, (c.bo >> 8) & 0x00ff00ffu);  // s3 | s7 << 16
+  if (lane == 0)
+    st.n_acc += (e02 & 0xffffu) + (e02 >> 16) + (e26 & 0xffffu) + (e26 >> 16) + (o15 & 0xffffu) + (o15 >> 16) +
+                (o37 & 0xffffu) + (o37 >> 16);
+  if (lane < NC) {
+    acc[GMAX + lane] += dm(K0, sm);
+    acc[2 * GMAX + lane] += dm(dm(K0, K0), sq);
+  } else if (lane >= 32 - GMAX) {
+    const int g = lane - (32 - GMAX);
+    const uint32_t w = (g & 1) ? ((g & 2) ? o37 : o15) : ((g & 2) ? e26 : e02);
+    acc[g] += (double)((g & 4) ? (w >> 16) : (w & 0xffffu));
+  }
+  if (lane == 0) {
+    acc[3 * GMAX] += p0;
+    acc[3 * GMAX + 1] += p1;
+    acc[3 * GMAX + 2] += p2;
+  }
+  __syncwarp();
+}
+
 template <int GMAX, int CH>
 __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
     k_gather_fine(const GatherArgs A, const FineArgs T) {
@@ -900,6 +1131,21 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
           }
           if (!__any_sync(kFull, rl != 0)) continue;
           const Hit &Hs = T.hits[s_desc.hp_lo + k];  // full state: exact path only
+          double *acc = out + (size_t)k * PS;  // windows of an item run in order in one CTA
+          if constexpr (CH == 1 && GMAX <= 8) {
+            if (Hh.gray & 2u) {
+              LeanCnt lc = {0u, 0u, 0u, 0u};
+              double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+              const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
+              if (A.na == 2)
+                lean_fragment<2>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
+              else
+                lean_fragment<1>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
+              lean_spill(lc);
+              lean_reduce<GMAX>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st);
+              continue;
+            }
+          }
           PackedCounts<GMAX> cnt;
 #pragma unroll
           for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
@@ -952,7 +1198,6 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
             for (int r = 0; r < 2 * PackedCounts<GMAX>::NP; ++r) tot += (csum[r] & 0xffffu) + (csum[r] >> 16);
             st.n_acc += tot;
           }
-          double *acc = out + (size_t)k * PS;  // windows of an item run in order in one CTA
           if (lane < NC) {
             const int cc = lane / GMAX, gg = lane % GMAX;
             acc[GMAX + cc * GMAX + gg] += sm;
