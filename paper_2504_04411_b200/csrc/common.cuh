@@ -61,7 +61,7 @@ struct GridHeader {
   uint32_t ok;     // 1 when dims fit the dense table
   uint32_t S;      // fine cells per reference cell and axis (power of two; 1 = reference cells)
   uint32_t shift;  // log2(S)
-  uint32_t pad;
+  uint32_t lean;   // 1: lean planar records (rec0 = x, y, z, meta; rec1 = L, b; rec2 = r, g; fp64 pairs)
 };
 // With S > 1 the dense table indexes FINE cells of size cell / S ("slab"
 // layout, used when the photons span few reference cells along z): inv is
@@ -74,6 +74,10 @@ struct GridHeader {
 //   rec0 = (x, y, z, depth bits), rec1 = (n.z, wi.z, lum(pow) as fp64 lo/hi),
 //   rec2 = (pow.r, pow.g, pow.b, flags), rec3 = (n.x, n.y, wi.x, wi.y)
 //   flags bit0: n.x, n.y, wi.x, wi.y all finite (planar-shortcut exactness)
+// Lean layout (GridHeader::lean; slab grids whose gathered hit points are all
+// planar and gray, C = 1, n_a <= 2, n_s = 4; gather_fine.cu lean path):
+//   rec0 = (x, y, z, meta), rec1 = (lum(pow), pow.b), rec2 = (pow.r, pow.g)
+//   in fp64; no rec3 (lean_record)
 // Layout used by the tile / warp / lanes kernels:
 //   rec0 = (x, y, z, depth bits)     -- the only vector read per candidate
 //   rec1 = (nx, ny, nz, wi.x)
@@ -83,6 +87,63 @@ struct PhotonRecs {
   float4 *rec0, *rec1, *rec2, *rec3;
   float4 *pack;  // fine layout: 64-B records in input order (permutation source)
 };
+
+// Fine-layout records packed in input order (coalesced reads of the SoA input
+// and 64-B contiguous writes); the permutation then moves whole 64-B records.
+__device__ __forceinline__ void fine_record(const float *__restrict__ pos, const float *__restrict__ nrm,
+                                            const float *__restrict__ wi, const float *__restrict__ pw,
+                                            const uint32_t *__restrict__ depth, size_t j, float4 &q0,
+                                            float4 &q1, float4 &q2, float4 &q3) {
+  const size_t o = 3 * j;
+  const float nx = nrm[o], ny = nrm[o + 1], wx = wi[o], wy = wi[o + 1];
+  const double L = elum((double)pw[o], (double)pw[o + 1], (double)pw[o + 2]);
+  const unsigned long long Lb = (unsigned long long)__double_as_longlong(L);
+  const uint32_t flags =
+      (fabsf(nx) < INFINITY && fabsf(ny) < INFINITY && fabsf(wx) < INFINITY && fabsf(wy) < INFINITY) ? 1u
+                                                                                                     : 0u;
+  q0 = make_float4(pos[o], pos[o + 1], pos[o + 2], __uint_as_float(depth[j]));
+  q1 = make_float4(nrm[o + 2], wi[o + 2], __uint_as_float((uint32_t)Lb), __uint_as_float((uint32_t)(Lb >> 32)));
+  q2 = make_float4(pw[o], pw[o + 1], pw[o + 2], __uint_as_float(flags));
+  q3 = make_float4(nx, ny, wx, wy);
+}
+
+// Lean record (GridHeader::lean): 48 B with the photon-only parts of the
+// planar predicates folded in.  Against a hit normal n = +z the guard and
+// cos_i dots are n.z and wi.z exactly when n.x, n.y, wi.x, wi.y are finite
+// (frame.cpp:5-14, integrator.cpp:397, bsdf.cpp:56-58), so:
+//   meta = depth << 8 | guard_fail << 31: eye + depth <= max_depth and the
+//          guard in one unsigned compare against the hit point's limit
+//          (< 2^31); depth < 2^23;
+//   cos_i <= 0: the pair is counted with value 0 (f = 0) -> L = r = g = b = 0;
+//   a non-finite n.x/n.y/wi.x/wi.y or power, or depth >= 2^23: x = NaN, meta = 0, which
+//          lands every pair with the photon in the exact fp64 path (it reads
+//          the input photon, not this record).
+__device__ __forceinline__ void lean_record(const float *__restrict__ pos, const float *__restrict__ nrm,
+                                            const float *__restrict__ wi, const float *__restrict__ pw,
+                                            const uint32_t *__restrict__ depth, size_t j, double guard, float4 &q0,
+                                            float4 &q1, float4 &q2) {
+  const size_t o = 3 * j;
+  const float nx = nrm[o], ny = nrm[o + 1], wx = wi[o], wy = wi[o + 1];
+  const uint32_t d = depth[j];
+  double r = (double)pw[o], g = (double)pw[o + 1], b = (double)pw[o + 2];
+  double L = elum(r, g, b);
+  const bool exact = !(fabsf(nx) < INFINITY && fabsf(ny) < INFINITY && fabsf(wx) < INFINITY &&
+                       fabsf(wy) < INFINITY) || d >= (1u << 23) || !(fabs(L) < INFINITY) ||
+                     !(fabs(r) < INFINITY && fabs(g) < INFINITY && fabs(b) < INFINITY);
+  const bool guard_fail = (double)nrm[o + 2] < guard;
+  const bool cos_pos = !(wi[o + 2] <= 0.0f);
+  if (!cos_pos) r = g = b = L = 0.0;
+  const uint32_t meta = exact ? 0u : ((d << 8) | (guard_fail ? 0x80000000u : 0u));
+  q0 = make_float4(exact ? __int_as_float(0x7fffffff) : pos[o], pos[o + 1], pos[o + 2], __uint_as_float(meta));
+  q1 = make_float4(__uint_as_float((uint32_t)__double_as_longlong(L)),
+                   __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(L) >> 32)),
+                   __uint_as_float((uint32_t)__double_as_longlong(b)),
+                   __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(b) >> 32)));
+  q2 = make_float4(__uint_as_float((uint32_t)__double_as_longlong(r)),
+                   __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(r) >> 32)),
+                   __uint_as_float((uint32_t)__double_as_longlong(g)),
+                   __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(g) >> 32)));
+}
 
 // exclusive scan of one value per thread over a 256-thread block; returns the
 // block total through *total.

@@ -108,6 +108,12 @@ struct fppm_gpu_ctx {
   // (photon_map.cpp:57-58); checked before the next gather whenever the cell
   // did not come from the max live radius or radii were raised (set_regions)
   bool grid_explicit = false, rcheck = false;
+  // lean record layout: every gathered hit point planar and gray (device
+  // flag from k_lean_check), config C = 1, n_a <= 2, n_s = 4, fine kernel
+  uint32_t *d_lean_ok = nullptr;
+  // staging set the current grid's input photons live in (the lean layout's
+  // exact path reads them during the gather: released after it), -1 none
+  int grid_set = -1;
 
   // outputs
   double *o_gather_r = nullptr, *o_stat = nullptr, *o_crit = nullptr, *o_flux = nullptr;
@@ -435,6 +441,8 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->sort.hist, radix_hist_entries((uint32_t)Nc)));
   A(dalloc(&ctx->d_hdr, 1)); A(dalloc(&ctx->d_bounds, 6)); A(dalloc(&ctx->d_cell, 1));
   A(dalloc(&ctx->d_cell_chk, 1));
+  A(dalloc(&ctx->d_lean_ok, 1));
+  A(cudaMemset(ctx->d_lean_ok, 0, sizeof(uint32_t)));
   A(cudaMallocHost(&ctx->h_hdr, sizeof(GridHeader)));
   A(cudaMallocHost(&ctx->h_bounds_init, sizeof(long long) * 6));
   A(cudaMallocHost(&ctx->h_cell, sizeof(double)));
@@ -498,7 +506,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
                  ctx->recs.rec0, ctx->recs.rec1, ctx->recs.rec2, ctx->recs.rec3, ctx->recs.pack,
                  ctx->sort.keys_a,
                  ctx->sort.vals_a, ctx->sort.keys_b, ctx->sort.vals_b, ctx->sort.hist,
-                 ctx->d_cell_start, ctx->d_hdr, ctx->d_bounds, ctx->d_cell, ctx->d_cell_chk,
+                 ctx->d_cell_start, ctx->d_hdr, ctx->d_bounds, ctx->d_cell, ctx->d_cell_chk, ctx->d_lean_ok,
                  ctx->o_gather_r, ctx->o_stat, ctx->o_crit, ctx->o_flux, ctx->o_flags, ctx->o_rad,
                  ctx->o_acc, ctx->o_tested, ctx->o_rejected, ctx->o_t64,
                  ctx->snap_cnt, ctx->snap_sum, ctx->snap_sq, ctx->d_counters,
@@ -578,9 +586,18 @@ int fppm_gpu_device_view_get(fppm_gpu_ctx *ctx, fppm_gpu_device_view *v) {
 }
 
 // ------------------------------------------------------------------ regions
+static bool lean_config(const fppm_gpu_ctx *ctx) {
+  const fppm_gpu_config &c = ctx->cfg;
+  return ctx->C == 1 && c.n_annuli <= 2 && c.n_sectors == 4 && !c.vcm_plus && gather_variant(ctx) == 4;
+}
+
 static int finish_hitpoints(fppm_gpu_ctx *ctx, uint32_t n, bool has_gathered) {
   if (!has_gathered) FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_gathered, 1, std::max<uint32_t>(n, 1), ctx->stream));
   FPPM_CUDA_OK(launch_hit_weights(ctx->stream, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb, n, ctx->d_K));
+  if (lean_config(ctx))
+    FPPM_CUDA_OK(launch_lean_check(ctx->stream, ctx->d_pos, ctx->d_nrm, ctx->d_K, ctx->d_gathered, n, ctx->d_lean_ok));
+  else
+    FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_lean_ok, 0, sizeof(uint32_t), ctx->stream));
   const bool reset = n != ctx->H;
   ctx->H = n;
   if (ctx->grid_explicit) ctx->rcheck = true;  // a newly gathered region may exceed the cell
@@ -958,7 +975,8 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
     ctx->stage_pending = -1;
   }
   launch_cell_bounds(s, ctx->in_pos, ctx->N, ctx->d_cell, S_req, ctx->d_bounds, ctx->sms);
-  launch_grid_header(s, ctx->d_bounds, ctx->d_cell, ctx->N, ctx->cfg.max_cells, S_req, ctx->d_hdr);
+  launch_grid_header(s, ctx->d_bounds, ctx->d_cell, ctx->N, ctx->cfg.max_cells, S_req,
+                     S_req > 1 ? ctx->d_lean_ok : nullptr, ctx->d_hdr);
   FPPM_CUDA_OK(cudaGetLastError());
   FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_hdr, ctx->d_hdr, sizeof(GridHeader), cudaMemcpyDeviceToHost, s));
   FPPM_CUDA_OK(cudaStreamSynchronize(s));
@@ -976,20 +994,28 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
   const bool fine_layout = effective_variant(ctx, g.S) == 4;
   launch_dense_keys(s, ctx->in_pos, ctx->N, ctx->d_hdr, ctx->sort.keys_a, ctx->sort.vals_a, ctx->sms);
   if (fine_layout && ctx->recs.pack)
-    launch_pack_fine(s, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow, ctx->in_depth, ctx->N,
-                     ctx->recs.pack, ctx->sms);
+    launch_pack_fine(s, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow, ctx->in_depth, ctx->N, ctx->d_hdr,
+                     ctx->cfg.normal_guard_cos, ctx->recs.pack, ctx->sms);
   FPPM_CUDA_OK(radix_sort_pairs(s, ctx->sort, ctx->N, g.key_bits, &ctx->d_skeys, &ctx->d_order));
   launch_cell_start(s, ctx->d_skeys, ctx->N, ctx->d_hdr, ctx->d_cell_start, g.ncells, ctx->sms);
   launch_permute(s, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,
-                 ctx->in_depth, ctx->recs, fine_layout, ctx->sms);
+                 ctx->in_depth, ctx->recs, fine_layout, ctx->d_hdr, ctx->sms);
   if (ctx->cfg.vcm_plus)
     launch_permute_f64x3(s, ctx->d_order, ctx->N, ctx->d_pmis_in[0], ctx->d_pmis_in[1], ctx->d_pmis_in[2],
                          ctx->d_pmis[0], ctx->d_pmis[1], ctx->d_pmis[2], ctx->sms);
   FPPM_CUDA_OK(cudaGetLastError());
+  ctx->grid_set = -1;
   if (ctx->cstream && ctx->in_pos == (ctx->stage_cur ? ctx->d_ppos2 : ctx->d_ppos)) {
-    // the staging set is consumed: a later upload may overwrite it
-    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_free[ctx->stage_cur], s));
-    ctx->free_recorded[ctx->stage_cur] = true;
+    // the staging set is consumed: a later upload may overwrite it -- after
+    // the gather when the lean layout's exact path may still read it (the
+    // stale event of an earlier iteration must not release it before that)
+    if (fine_layout && (g.lean || lean_config(ctx))) {
+      ctx->grid_set = ctx->stage_cur;
+      ctx->free_recorded[ctx->stage_cur] = false;
+    } else {
+      FPPM_CUDA_OK(cudaEventRecord(ctx->ev_free[ctx->stage_cur], s));
+      ctx->free_recorded[ctx->stage_cur] = true;
+    }
   }
   ctx->grid_valid = true;
   return FPPM_OK;
@@ -1160,6 +1186,9 @@ static void fill_gather_args(fppm_gpu_ctx *ctx, uint64_t iteration, GatherArgs &
   A.H = ctx->H;
   A.rec0 = ctx->recs.rec0; A.rec1 = ctx->recs.rec1; A.rec2 = ctx->recs.rec2; A.rec3 = ctx->recs.rec3;
   A.cell_start = ctx->d_cell_start; A.grid = ctx->d_hdr;
+  A.order = ctx->d_order;
+  A.in_pos = ctx->in_pos; A.in_nrm = ctx->in_nrm; A.in_wi = ctx->in_wi; A.in_pow = ctx->in_pow;
+  A.in_depth = ctx->in_depth;
   A.na = ctx->cfg.n_annuli; A.ns = ctx->cfg.n_sectors;
   A.max_depth = ctx->cfg.max_depth; A.guard = ctx->cfg.normal_guard_cos;
   A.end = end_params(ctx, iteration);
@@ -1381,6 +1410,11 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       if ((rc = kernel_event(ctx, 1))) return rc;
     }
     FPPM_CUDA_OK(launch_tile_finalize(s, A, T, ctx->C, ctx->sms));
+  }
+  if (ctx->grid_set >= 0) {  // the exact path read the staged input photons
+    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_free[ctx->grid_set], s));
+    ctx->free_recorded[ctx->grid_set] = true;
+    ctx->grid_set = -1;
   }
   if (delta) return FPPM_OK;  // option B: pooled and tested by the owner (apply_deltas)
   ctx->end_calls++;

@@ -1,3 +1,4 @@
+#include <algorithm>
 // gather.cu -- warp-per-hit-point gather (the "warp" variant) + the
 // explicit-sample / end_iteration kernels of the GatherRegion mirror.
 //
@@ -620,6 +621,28 @@ cudaError_t launch_hit_weights(cudaStream_t s, const double3 *nrm, const double3
   if (H == 0) return cudaSuccess;
   const int blocks = (int)((H + 255) / 256);
   k_hit_weights<<<blocks, 256, 0, s>>>(nrm, wo, thr, alb, H, K);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+__global__ void k_lean_check(const double3 *__restrict__ pos, const double3 *__restrict__ nrm,
+                             const double3 *__restrict__ K, const uint8_t *__restrict__ gathered, uint32_t H,
+                             uint32_t *__restrict__ flag) {
+  bool ok = true;
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
+    if (gathered != nullptr && gathered[h] == 0) continue;
+    const double3 c = pos[h], n = nrm[h], k = K[h];
+    ok = ok && n.x == 0.0 && n.y == 0.0 && n.z == 1.0 && (double)(float)c.x == c.x &&
+         (double)(float)c.y == c.y && (double)(float)c.z == c.z && k.x == k.y && k.y == k.z && isfinite(k.x);
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0u);
+}
+
+cudaError_t launch_lean_check(cudaStream_t s, const double3 *pos, const double3 *nrm, const double3 *K,
+                              const uint8_t *gathered, uint32_t H, uint32_t *flag) {
+  cudaError_t e = cudaMemsetAsync(flag, 0xff, sizeof(uint32_t), s);  // nonzero: lean until a lane objects
+  if (e != cudaSuccess || H == 0) return e;
+  k_lean_check<<<(int)std::min<uint32_t>((H + 255) / 256, 1184u), 256, 0, s>>>(pos, nrm, K, gathered, H, flag);
   note_launches(1);
   return cudaGetLastError();
 }

@@ -40,6 +40,10 @@ struct GatherArgs {
   const float4 *rec0, *rec1, *rec2, *rec3;
   const uint32_t *cell_start;
   const GridHeader *grid;
+  // lean layout's exact path: sorted -> input order, and the input photons
+  const uint32_t *order;
+  const float *in_pos, *in_nrm, *in_wi, *in_pow;
+  const uint32_t *in_depth;
   // config
   int na, ns;
   uint32_t max_depth;
@@ -210,6 +214,10 @@ cudaError_t launch_apply_deltas(cudaStream_t s, const GatherArgs &A, int C, uint
                                 const double *delta);
 cudaError_t launch_hit_weights(cudaStream_t s, const double3 *nrm, const double3 *wo,
                                const double3 *thr, const double3 *alb, uint32_t H, double3 *K);
+// *flag = 1 when every gathered hit point is planar (n = +z, fp32-exact
+// centre) and gray (K0 = K1 = K2 finite): the lean record layout applies
+cudaError_t launch_lean_check(cudaStream_t s, const double3 *pos, const double3 *nrm, const double3 *K,
+                              const uint8_t *gathered, uint32_t H, uint32_t *flag);
 
 // grid.cu
 size_t radix_hist_entries(uint32_t n);
@@ -218,18 +226,19 @@ cudaError_t radix_sort_pairs(cudaStream_t s, SortScratch &sc, uint32_t n, uint32
 void launch_cell_bounds(cudaStream_t s, const float *pos, uint32_t n, const double *cell,
                         uint32_t S, long long *bounds, int sms);
 void launch_grid_header(cudaStream_t s, const long long *bounds, const double *cell, uint32_t n,
-                        unsigned long long max_cells, uint32_t S, GridHeader *hdr);
+                        unsigned long long max_cells, uint32_t S, const uint32_t *lean_ok, GridHeader *hdr);
 void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridHeader *hdr,
                        uint32_t *keys, uint32_t *vals, int sms);
 void launch_pack_fine(cudaStream_t s, const float *pos, const float *nrm, const float *wi, const float *pw,
-                      const uint32_t *depth, uint32_t n, float4 *pack, int sms);
+                      const uint32_t *depth, uint32_t n, const GridHeader *hdr, double guard, float4 *pack,
+                      int sms);
 void launch_permute_f64x3(cudaStream_t s, const uint32_t *order, uint32_t n, const double *a,
                           const double *b, const double *c, double *oa, double *ob, double *oc, int sms);
 void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const GridHeader *hdr,
                        uint32_t *start, unsigned long long ncells, int sms);
 void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const float *pos,
                     const float *nrm, const float *wi, const float *pw, const uint32_t *depth,
-                    const PhotonRecs &r, int fine_layout, int sms);
+                    const PhotonRecs &r, int fine_layout, const GridHeader *hdr, int sms);
 void launch_query_ball(cudaStream_t s, const double *centers, const double *radii, uint32_t nq,
                        const GridHeader *hdr, const uint32_t *start, const float4 *rec0,
                        const uint32_t *order, unsigned long long *counts,

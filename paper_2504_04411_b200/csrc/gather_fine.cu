@@ -182,6 +182,8 @@ struct alignas(16) FineHot {
   int32_t bx0, by0, by1;  // fine box (fine_box); bx1, bz0, bz1 in the fbox array
   uint32_t nruns;
   uint2 run[kFMaxPieces];  // sorted-record range [begin, end) of each run (clipped to the chord)
+  uint32_t mlim;           // lean layout: meta <= mlim <=> eye + depth <= max_depth (integrator.cpp:396)
+  uint32_t pad_[3];
 };
 static_assert(sizeof(FineHot) % 16 == 0, "FineHot must be a multiple of 16 B (TMA)");
 
@@ -228,7 +230,14 @@ __global__ void __launch_bounds__(kPrepThreads)
     // bit0: K0 = K1 = K2; bit1: the lean path (planar, gray, finite K: the
     // lane slots hold photon-luminance moments, scaled by K0 at the end)
     Q.gray = (P.gray ? 1u : 0u) |
-             ((Q.planar && P.gray && isfinite(P.K0) && A.na <= 2 && A.ns == 4) ? 2u : 0u);
+             ((Q.planar && P.gray && isfinite(P.K0) && A.na <= 2 && A.ns == 4 && P.eye <= A.max_depth) ? 2u : 0u);
+    {
+      // lean meta (lean_record): depth < 2^23 in bits 8..30, guard failure in bit 31
+      unsigned long long dm_ = P.eye <= A.max_depth ? (unsigned long long)(A.max_depth - P.eye) : 0ull;
+      if (dm_ > (1ull << 23) - 1) dm_ = (1ull << 23) - 1;
+      Q.mlim = (uint32_t)((dm_ << 8) | 0xffu);
+      Q.pad_[0] = Q.pad_[1] = Q.pad_[2] = 0u;
+    }
     Q.bx0 = b.x0; Q.by0 = b.y0; Q.by1 = b.y1;
     fbox[i] = make_int4(b.x1, b.z0, b.z1, 0);
     Q.nruns = (uint32_t)nr;
@@ -364,7 +373,7 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
     for (uint32_t w = 0; w * kFWave < nhp; ++w) {
       const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
       const WaveInfo W = wave_info(A, g, hot, fbox, h0 + w * kFWave, n, b + 1 < nb);
-      const uint32_t chunk = W.planar ? cap48 : cap64;
+      const uint32_t chunk = (W.planar || g.lean) ? cap48 : cap64;
       const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
       it += nsub;
@@ -396,7 +405,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
       const uint32_t n = min((uint32_t)kFWave, nhp - w * kFWave);
       const uint32_t lo = h0 + w * kFWave;
       const WaveInfo W = wave_info(A, g, hot, fbox, lo, n, b + 1 < nb);
-      const uint32_t chunk = W.planar ? cap48 : cap64;
+      const uint32_t chunk = (W.planar || g.lean) ? cap48 : cap64;
       const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
       __syncwarp();
@@ -410,7 +419,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
         d.nwin = nwin;
         d.npieces = (uint32_t)W.np;
         d.pre[kFMaxPieces] = W.T;
-        d.pad0 = W.planar ? 1u : 0u;  // flags: bit0 = 48-B records (no rec3 staged)
+        d.pad0 = (W.planar || g.lean) ? 1u : 0u;  // flags: bit0 = 48-B records (no rec3 staged)
         d.ux0 = W.u.x0; d.ux1 = W.u.x1; d.uy0 = W.u.y0; d.uy1 = W.u.y1; d.uz0 = W.u.z0; d.uz1 = W.u.z1;
       }
       if ((uint32_t)lane < n) {
@@ -442,19 +451,24 @@ struct FineLayout {
   static constexpr int NC = GMAX * CH;                  // accumulator columns
   static constexpr int NQ = 32 / NC;                    // lane groups in the slot reduction
   static constexpr int PS = partial_size(GMAX, CH);
-  static constexpr size_t kSlotBytes = (size_t)kFWarps * NC * 32 * 16;
+  // lane slots [NC + 1][32] {sum, sum_sq} per warp; row NC: the lean path's
+  // spare row for rejected pairs (never reduced)
+  static constexpr size_t kSlotBytes = (size_t)kFWarps * (NC + 1) * 32 * 16;
   static constexpr size_t kHotBytes = (size_t)kFWave * sizeof(FineHot);
+  // the item's partial rows, accumulated in shared memory over its windows
+  // and written out once at the end of the item
+  static constexpr size_t kRowBytes = (size_t)kFWave * PS * 8;
   static constexpr int kMinBlocks = NC <= 8 ? 2 : 1;
   // dynamic shared memory: records + lane slots + staged hit points;
   // kMinBlocks CTAs share the SM's 228 KB, each with 1 KB reserved and the
   // static arrays of the kernel
   static constexpr size_t kStatic = (size_t)kFWarps * kFExact * 4 + 2 * sizeof(FineDesc) + 64;
   static constexpr size_t kBudget = (size_t)233472 / kMinBlocks - 1024 - kStatic - 256;
-  static constexpr size_t kRecBytes = kBudget - kSlotBytes - kHotBytes;
+  static constexpr size_t kRecBytes = kBudget - kSlotBytes - kHotBytes - kRowBytes;
   // window capacity: 64 B per candidate, or 48 B for planar waves (no rec3)
   static constexpr uint32_t kCap64 = (uint32_t)((kRecBytes / 64) & ~(size_t)31);
   static constexpr uint32_t kCap48 = (uint32_t)((kRecBytes / 48) & ~(size_t)31);
-  static constexpr size_t kDynBytes = kRecBytes + kSlotBytes + kHotBytes;
+  static constexpr size_t kDynBytes = kRecBytes + kSlotBytes + kHotBytes + kRowBytes;
 };
 
 struct FineState {
@@ -773,107 +787,143 @@ static __device__ __forceinline__ void fine_fragment(const GatherArgs &A, const 
 
 
 // ------------------------------------------------------------------ lean path
-// Planar (n = +z, fp32-exact centre), gray (K0 = K1 = K2, finite), 1-2
-// annuli x 4 quadrants, luminance channel: every canonical workload.  The
-// pair value is v = K0 * L (L = the photon's fp64 luminance from the record),
-// so a lane's slot accumulates the photon moments {sum L, sum L^2} of its
-// accepted pairs and the fragment's sector sums are K0 * sum L and
-// K0^2 * sum L^2 (SectorStats::add, stat_tests.hpp:18-22; equal to the
-// per-pair products up to fp64 reassociation, within the 1e-12 sum
-// tolerance).  Per-sector counts are nibbles of one register (sector s at
-// bits 4s..4s+3), spilled to byte words before they can overflow.
+// Lean record layout (GridHeader::lean, common.cuh): every gathered hit point
+// of the frame is planar and gray, C = 1, n_a <= 2, n_s = 4 -- every
+// canonical workload.  A record is 48 B: (x, y, z, meta) with depth, guard
+// and cos_i bits precomputed for n = +z, then (L, b) and (r, g) in fp64, so a
+// pair needs no conversions.  The pair value is v = K0 * L, so a lane's slot
+// accumulates the photon moments {sum L, sum L^2} of its accepted pairs and
+// the fragment's sector sums are K0 * sum L and K0^2 * sum L^2
+// (SectorStats::add, stat_tests.hpp:18-22; equal to the per-pair products up
+// to fp64 reassociation, within the 1e-12 sum tolerance).  Per-sector counts
+// are nibbles of one register per candidate slot (sector s at bits 4s..4s+3),
+// spilled to byte words every 15 steps.  Pairs inside an fp32 error band take
+// the exact fp64 path on the input photon (order[] -> fppm_photons arrays).
 struct LeanCnt {
-  uint32_t nib, be, bo;  // nibble counts; byte words: even sectors 0,2,4,6 / odd 1,3,5,7
-  uint32_t nadd;         // warp-uniform: pairs added per lane since the last spill (<= 15)
+  uint32_t n0, n1, be, bo;  // nibble counts (candidate 0 / 1 of a step); byte words: sectors 0,2,4,6 / 1,3,5,7
 };
 static __device__ __forceinline__ void lean_spill(LeanCnt &c) {
-  c.be += c.nib & 0x0F0F0F0Fu;
-  c.bo += (c.nib >> 4) & 0x0F0F0F0Fu;
-  c.nib = 0u;
-  c.nadd = 0u;
+  c.be += (c.n0 & 0x0F0F0F0Fu) + (c.n1 & 0x0F0F0F0Fu);
+  c.bo += ((c.n0 >> 4) & 0x0F0F0F0Fu) + ((c.n1 >> 4) & 0x0F0F0F0Fu);
+  c.n0 = c.n1 = 0u;
 }
 
-template <int NA>
 struct LeanPair {
-  bool acc, on, need;
+  bool acc, need;
   uint32_t s4;  // 4 * sector
-  double L;
-  float4 pw;
+  double L, r, g, b;
 };
 
-// Full fp32 evaluation of candidate at smem offset `off` (records r0, r0 + d1,
-// r0 + d2): ball, depth, guard, disk, annulus, quadrant, cos_i with the error
-// bands of fine_eval<PLANAR>.
+// Hit-point constants of the lean loop.
+struct LeanHit {
+  float chx, chy, chz, lim_hi, lim_lo, band_y, qa_scale;
+  uint32_t mlim;
+};
+
+// fp32 evaluation of one candidate (records at a0, a0 + d1, a0 + d2): ball,
+// depth, guard, disk, annulus, quadrant, cos_i with the error bands of
+// fine_eval<PLANAR>; band or exact-flagged photons -> need.
 template <int NA>
-static __device__ __forceinline__ LeanPair<NA> lean_eval(const HitF &F, uint32_t max_depth, bool valid,
-                                                         uint32_t a0, uint32_t d1, uint32_t d2) {
-  LeanPair<NA> q;
+static __device__ __forceinline__ LeanPair lean_eval(const LeanHit &F, bool valid, uint32_t a0, uint32_t d1,
+                                                     uint32_t d2) {
+  LeanPair q;
   const float4 p = lds128_f(a0);
-  const float4 B = lds128_f(a0 + d1);
-  q.pw = lds128_f(a0 + d2);
-  q.L = __longlong_as_double(((long long)__float_as_uint(B.w) << 32) | __float_as_uint(B.z));
+  const double2 LB = lds_f64x2(a0 + d1);
+  const double2 RG = lds_f64x2(a0 + d2);
+  q.L = LB.x;
+  q.b = LB.y;
+  q.r = RG.x;
+  q.g = RG.y;
   const float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
   const float yy = fmaf(dx, dx, dy * dy);
   const float r2 = fmaf(dz, dz, yy);
-  const bool maybe = valid && F.eye + __float_as_uint(p.w) <= max_depth && r2 <= F.lim_hi;  // :396, :76
-  bool band = !(r2 < F.lim_lo) || !(fabsf(dx) > F.band_y) || !(fabsf(dy) > F.band_y) ||
-              (__float_as_uint(q.pw.w) & 1u) == 0u;
+  // depth (integrator.cpp:396) + guard (:397) in one compare; ball
+  // (photon_map.cpp:76): NaN (an exact-flagged record) passes into the band
+  const bool maybe = valid && __float_as_uint(p.w) <= F.mlim && !(r2 > F.lim_hi);
+  bool band = !(r2 < F.lim_lo) || !(fabsf(dx) > F.band_y) || !(fabsf(dy) > F.band_y);
   // quadrant (exact-sector table): +x+y 0, -x+y 1, -x-y 2, +x-y 3
   uint32_t s4 = dy > 0.0f ? (dx > 0.0f ? 0u : 4u) : (dx > 0.0f ? 12u : 8u);
   if constexpr (NA == 2) {  // one annulus edge at d2 = r2 / 2
     const float qa = yy * F.qa_scale;
     band = band || fabsf(qa - 1.0f) < 2e-4f;
-    s4 += qa >= 1.0f ? 16u : 0u;
+    if (qa >= 1.0f) s4 += 16u;
   }
-  q.s4 = s4;
   q.need = maybe && band;
-  q.acc = maybe && !band && !(B.x < F.guard_ceil);  // integrator.cpp:397
-  q.on = q.acc && !(B.y <= 0.0f);                     // bsdf.cpp:56-58
+  q.acc = maybe && !band;
+  q.s4 = q.acc ? s4 : 16u * NA;  // a rejected pair adds into the lane's spare slot row (row 4 * NA)
   return q;
 }
 
-template <int NA>
-static __device__ __forceinline__ void lean_add(const LeanPair<NA> &q, uint32_t slot_lane, LeanCnt &c,
+// Predicated add of the packed sector counts.
+static __device__ __forceinline__ void padd_u32(uint32_t &acc, uint32_t v, bool p) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q add.u32 %0, %0, %1;\n\t}"
+      : "+r"(acc) : "r"(v), "r"((uint32_t)p));
+}
+
+// Slot row 4 * n_a is the spare row of rejected pairs (never reduced), so the
+// moments need no value select; cos_i <= 0 photons carry L = r = g = b = 0.
+static __device__ __forceinline__ void lean_add(const LeanPair &q, uint32_t slot_lane, uint32_t &nib,
                                                 double &p0, double &p1, double &p2) {
-  const double v = q.on ? q.L : 0.0;
+  const double v = q.L;
   const uint32_t a = slot_lane + q.s4 * (32u * 16u / 4u);  // [sector][lane] {sum, sum_sq}
   double2 o = lds_f64x2(a);
   o.x = da(o.x, v);
   o.y = da(o.y, dm(v, v));
   sts_f64x2(a, o);
-  if (q.acc) c.nib += 1u << q.s4;
-  if (q.on) {
-    p0 = da(p0, (double)q.pw.x);
-    p1 = da(p1, (double)q.pw.y);
-    p2 = da(p2, (double)q.pw.z);
-  }
+  padd_u32(nib, 1u << q.s4, q.acc);
+  // flux (integrator.cpp:449): fma(x, 1, p) = p + x and fma(x, 0, p) = p
+  // exactly for the finite powers of lean records -- one DFMA per channel
+  const double m = q.acc ? 1.0 : 0.0;
+  p0 = __fma_rn(q.r, m, p0);
+  p1 = __fma_rn(q.g, m, p1);
+  p2 = __fma_rn(q.b, m, p2);
 }
 
-// Deferred pairs on the exact fp64 path (same ring as fine_exact_batch).
-template <int NA>
+// Exact fp64 evaluation of the candidate at window index i of a lean window:
+// the input photon (sorted -> input order) in the reference's operation order.
+static __device__ __forceinline__ uint32_t lean_exact(const GatherArgs &A, const Hit &Hs, const FineWin &Wn,
+                                                      uint32_t i, float4 &pw, double &L) {
+  const uint32_t f = i + Wn.lo;  // flattened position -> piece -> sorted record -> input photon
+  uint32_t p = 0;
+  while (p + 1 < Wn.d->npieces && Wn.d->pre[p + 1] <= f) ++p;
+  const uint32_t j = A.order[Wn.d->src[p] + (f - Wn.d->pre[p])];
+  float4 a, B, Cc, D;
+  fine_record(A.in_pos, A.in_nrm, A.in_wi, A.in_pow, A.in_depth, j, a, B, Cc, D);
+  pw = Cc;
+  L = __longlong_as_double(((long long)__float_as_uint(B.w) << 32) | __float_as_uint(B.z));
+  const float4 b_old = make_float4(D.x, D.y, B.x, D.z);
+  const float4 c2_old = make_float4(D.w, B.y, Cc.x, Cc.y);
+  return exact_pair_packed(Hs, a, b_old, c2_old, A.na, A.ns, A.guard);
+}
+
+// Deferred pairs of a lean fragment (same ring as fine_exact_batch).
 static __device__ __forceinline__ void lean_exact_batch(const GatherArgs &A, const Hit &Hs, uint32_t n, uint32_t ex,
                                                         uint32_t slot_lane, LeanCnt &c, double &p0, double &p1,
                                                         double &p2, const FineWin &Wn, FineState &st) {
   const int lane = threadIdx.x & 31;
   __syncwarp();
-  if (c.nadd + 1u > 15u) lean_spill(c);
+  lean_spill(c);
   const bool have = (uint32_t)lane < n;
   const uint32_t i = have ? lds_u32(ex + ((st.eh + lane) & (kFExact - 1)) * 4u) : 0u;
   st.eh += n;
-  LeanPair<NA> q;
-  q.pw = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 pw = make_float4(0.f, 0.f, 0.f, 0.f);
+  LeanPair q;
   q.L = 0.0;
   uint32_t fl = 0;
   if (have) {
-    fl = fine_exact(Hs, Wn, i, A.na, A.ns, A.guard, q.pw, q.L);
+    fl = lean_exact(A, Hs, Wn, i, pw, q.L);
     st.n_exact += 1;
     st.n_amb += (fl >> 2) & 1u;
   }
   q.acc = (fl & 1u) != 0;
-  q.on = q.acc && (fl & 2u) != 0;
-  q.s4 = (fl >> 8) * 4u;
-  lean_add<NA>(q, slot_lane, c, p0, p1, p2);
-  c.nadd += 1u;
+  const bool on = q.acc && (fl & 2u) != 0;  // cos_i > 0 (bsdf.cpp:56-58): else the value is 0
+  q.r = on ? (double)pw.x : 0.0;
+  q.g = on ? (double)pw.y : 0.0;
+  q.b = on ? (double)pw.z : 0.0;
+  q.L = on ? q.L : 0.0;
+  q.s4 = q.acc ? (fl >> 8) * 4u : 16u * (uint32_t)A.na;
+  lean_add(q, slot_lane, c.n0, p0, p1, p2);
+  lean_spill(c);
   __syncwarp();
 }
 
@@ -888,8 +938,10 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
                                                      double &p2, const FineWin &Wn, FineState &st) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  const HitF F = Hh.F;
-  const uint32_t max_depth = A.max_depth;
+  LeanHit F;
+  F.chx = Hh.F.chx; F.chy = Hh.F.chy; F.chz = Hh.F.chz;
+  F.lim_hi = Hh.F.lim_hi; F.lim_lo = Hh.F.lim_lo; F.band_y = Hh.F.band_y; F.qa_scale = Hh.F.qa_scale;
+  F.mlim = Hh.mlim;
   const uint32_t d1 = Wn.r1 - Wn.r0, d2 = Wn.r2 - Wn.r0;
   uint32_t incl = rl;
 #pragma unroll
@@ -902,6 +954,7 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
   if (lane == 0) st.n_cand += total;
   int j = 0;
   uint32_t e = __shfl_sync(kFull, incl, 0), o = __shfl_sync(kFull, off, 0);
+  uint32_t spill = 15;
   for (uint32_t base = 0; base < total; base += 64) {
     while (e <= base) {  // warp-uniform: skip runs that ended (incl. empty ones)
       ++j;
@@ -921,15 +974,18 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
         ek = __shfl_sync(kFull, incl, k);
       }
     }
+    // slots past the end stay inside the staged window (read, never added)
     const bool ok0 = v0 < total, ok1 = v1 < total;
     if (!ok0) i0 = rs;
     if (!ok1) i1 = rs;
-    if (c.nadd + 2u > 15u) lean_spill(c);
-    const LeanPair<NA> q0 = lean_eval<NA>(F, max_depth, ok0, Wn.r0 + i0 * 16u, d1, d2);
-    const LeanPair<NA> q1 = lean_eval<NA>(F, max_depth, ok1, Wn.r0 + i1 * 16u, d1, d2);
-    lean_add<NA>(q0, slot_lane, c, p0, p1, p2);
-    lean_add<NA>(q1, slot_lane, c, p0, p1, p2);
-    c.nadd += 2u;
+    if (--spill == 0) {
+      lean_spill(c);
+      spill = 15;
+    }
+    const LeanPair q0 = lean_eval<NA>(F, ok0, Wn.r0 + i0 * 16u, d1, d2);
+    const LeanPair q1 = lean_eval<NA>(F, ok1, Wn.r0 + i1 * 16u, d1, d2);
+    lean_add(q0, slot_lane, c.n0, p0, p1, p2);
+    lean_add(q1, slot_lane, c.n1, p0, p1, p2);
     const uint32_t m0 = __ballot_sync(kFull, q0.need), m1 = __ballot_sync(kFull, q1.need);
     if (m0 | m1) {
       if (q0.need) sts_u32(ex + ((st.et + __popc(m0 & lt)) & (kFExact - 1)) * 4u, i0);
@@ -937,14 +993,57 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
       if (q1.need) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
       st.et += __popc(m1);
       while (st.et - st.eh >= 32)
-        lean_exact_batch<NA>(A, Hs, 32u, ex, slot_lane, c, p0, p1, p2, Wn, st);
+        lean_exact_batch(A, Hs, 32u, ex, slot_lane, c, p0, p1, p2, Wn, st);
     }
   }
   while (st.et != st.eh)
-    lean_exact_batch<NA>(A, Hs, min(32u, st.et - st.eh), ex, slot_lane, c, p0, p1, p2, Wn, st);
+    lean_exact_batch(A, Hs, min(32u, st.et - st.eh), ex, slot_lane, c, p0, p1, p2, Wn, st);
+  lean_spill(c);
   __syncwarp();
 }
 
+// A hit point of a lean-layout frame that is not itself lean (another
+// normal, a non-gray weight, ...): every candidate on the exact fp64 path,
+// accumulated with the general slots / packed counts.
+template <int GMAX>
+static __device__ __forceinline__ void exact_fragment(const GatherArgs &A, const FineHot &Hh, const Hit &Hs,
+                                                      uint32_t rs, uint32_t rl, uint32_t slots,
+                                                      PackedCounts<GMAX> &cnt, double &p0, double &p1,
+                                                      double &p2, const FineWin &Wn, FineState &st) {
+  const int lane = threadIdx.x & 31;
+  HitV K;
+  K.K0 = Hh.K0; K.K1 = Hh.K1; K.K2 = Hh.K2;
+  K.gray = false;
+  K.Kz0 = dm(Hh.K0, 0.0); K.Kz1 = dm(Hh.K1, 0.0); K.Kz2 = dm(Hh.K2, 0.0);
+  K.Kz = elum(K.Kz0, K.Kz1, K.Kz2);
+  uint32_t incl = rl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t off = rs - (incl - rl);
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  if (lane == 0) st.n_cand += total;
+  for (uint32_t base = 0; base < total; base += 32) {
+    const uint32_t v = base + lane;
+    int j = 0;
+    for (int k = 0; k < 32; ++k) j += __shfl_sync(kFull, incl, k) <= v ? 1 : 0;  // run of v
+    const uint32_t i = v + __shfl_sync(kFull, off, j & 31);
+    const bool have = v < total;
+    float4 pw = make_float4(0.f, 0.f, 0.f, 0.f);
+    double L = 0.0;
+    uint32_t fl = 0;
+    if (have) {
+      fl = lean_exact(A, Hs, Wn, i, pw, L);
+      st.n_exact += 1;
+      st.n_amb += (fl >> 2) & 1u;
+    }
+    fine_accumulate<GMAX, 1, false>(K, (fl & 1u) != 0, (fl & 2u) != 0, (int)(fl >> 8), pw, L, slots, lane, cnt,
+                                    p0, p1, p2);
+  }
+  __syncwarp();
+}
 
 // End of a lean fragment: the lane slots reduced in the fixed rotated order
 // of the general path, scaled by K0 / K0^2, counts from the byte words, flux;
@@ -972,9 +1071,22 @@ static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, dou
     sm += __shfl_down_sync(kFull, sm, o);
     sq += __shfl_down_sync(kFull, sq, o);
   }
-  p0 = warp_sum(p0);
-  p1 = warp_sum(p1);
-  p2 = warp_sum(p2);
+  // flux: transposed butterfly (12 shuffles instead of 30): after it lane 0
+  // holds sum p0, lane 8 sum p1, lane 16 sum p2
+  {
+    const bool hi16 = (lane & 16) != 0, hi8 = (lane & 8) != 0;
+    const double s0 = hi16 ? p0 : p2, k0 = hi16 ? p2 : p0;  // send / keep
+    const double s1 = hi16 ? p1 : 0.0, k1 = hi16 ? 0.0 : p1;
+    const double a = k0 + __shfl_xor_sync(kFull, s0, 16);   // lo: p0 | hi: p2
+    const double b = k1 + __shfl_xor_sync(kFull, s1, 16);   // lo: p1 | hi: 0
+    double c = (hi8 ? b : a) + __shfl_xor_sync(kFull, hi8 ? a : b, 8);
+    c += __shfl_xor_sync(kFull, c, 4);
+    c += __shfl_xor_sync(kFull, c, 2);
+    c += __shfl_xor_sync(kFull, c, 1);
+    p0 = __shfl_sync(kFull, c, 0);
+    p1 = __shfl_sync(kFull, c, 8);
+    p2 = __shfl_sync(kFull, c, 16);
+  }
   // byte words -> 16-bit halves -> warp sums: even word bytes = sectors 0,2,4,6
   const uint32_t e02 = __reduce_add_sync(kFull, c.be & 0x00ff00ffu);         // s0 | s4 << 16
   const uint32_t e26 = __reduce_add_sync(kFull, (c.be >> 8) & 0x00ff00ffu);  // s2 | s6 << 16
@@ -1007,6 +1119,7 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *s_slots = reinterpret_cast<double *>(smem_raw + Lay::kRecBytes);
   FineHot *s_hot = reinterpret_cast<FineHot *>(smem_raw + Lay::kRecBytes + Lay::kSlotBytes);
+  double *s_rows = reinterpret_cast<double *>(smem_raw + Lay::kRecBytes + Lay::kSlotBytes + Lay::kHotBytes);
   __shared__ uint32_t s_ex[kFWarps][kFExact];
   __shared__ FineDesc s_descs[2];
   __shared__ __align__(8) uint64_t s_bar, s_dbar[2];  // records; descriptor buffer 0 / 1
@@ -1014,8 +1127,8 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t r0 = smem_u32(smem_raw);
-  double *slots_p = s_slots + (size_t)warp * NC * 32 * 2;
-  for (int i = lane; i < NC * 32 * 2; i += 32) slots_p[i] = 0.0;
+  double *slots_p = s_slots + (size_t)warp * (NC + 1) * 32 * 2;
+  for (int i = lane; i < (NC + 1) * 32 * 2; i += 32) slots_p[i] = 0.0;
   const uint32_t slots = smem_u32(slots_p);
   const uint32_t exa = smem_u32(&s_ex[warp][0]);
   const uint32_t total_items = *T.total_items;
@@ -1057,7 +1170,7 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
     }
     const uint32_t hp_n = s_desc.hp_n, Tu = s_desc.pre[kFMaxPieces];
     // per-hp sums over the item's windows accumulate in its partial rows
-    double *out = T.partials + (size_t)s_desc.pbase * PS;
+    double *out = s_rows;
     for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) out[i] = 0.0;
     __syncthreads();  // zeroed rows before any warp adds to them
     if (Tu != 0) {
@@ -1132,33 +1245,38 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
           if (!__any_sync(kFull, rl != 0)) continue;
           const Hit &Hs = T.hits[s_desc.hp_lo + k];  // full state: exact path only
           double *acc = out + (size_t)k * PS;  // windows of an item run in order in one CTA
-          if constexpr (CH == 1 && GMAX <= 8) {
-            if (Hh.gray & 2u) {
-              LeanCnt lc = {0u, 0u, 0u, 0u};
-              double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-              const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
-              if (A.na == 2)
-                lean_fragment<2>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
-              else
-                lean_fragment<1>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
-              lean_spill(lc);
-              lean_reduce<GMAX>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st);
-              continue;
-            }
-          }
           PackedCounts<GMAX> cnt;
 #pragma unroll
           for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
           double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-          if (Hh.planar && Hh.gray)
-            fine_fragment<GMAX, CH, true, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
-          else if (Hh.planar)
-            fine_fragment<GMAX, CH, true, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
-          else if (Hh.gray)
-            fine_fragment<GMAX, CH, false, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
-          else
-            fine_fragment<GMAX, CH, false, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn,
-                                                  st);
+          bool done = false;
+          if constexpr (CH == 1 && GMAX <= 8) {
+            if (g.lean) {
+              if (Hh.gray & 2u) {
+                LeanCnt lc = {0u, 0u, 0u, 0u};
+                const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
+                if (A.na == 2)
+                  lean_fragment<2>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
+                else
+                  lean_fragment<1>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
+                lean_reduce<GMAX>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st);
+                continue;
+              }
+              exact_fragment<GMAX>(A, Hh, Hs, rs, rl, slots, cnt, p0, p1, p2, Wn, st);
+              done = true;
+            }
+          }
+          if (!done) {
+            if (Hh.planar && (Hh.gray & 1u))
+              fine_fragment<GMAX, CH, true, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+            else if (Hh.planar)
+              fine_fragment<GMAX, CH, true, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+            else if (Hh.gray & 1u)
+              fine_fragment<GMAX, CH, false, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+            else
+              fine_fragment<GMAX, CH, false, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn,
+                                                    st);
+          }
 
           // ---- fixed-order reduction of the lane slots, added to the hp's row
           const int col = lane % NC, grp = lane / NC;
@@ -1216,6 +1334,10 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
         }
         __syncthreads();  // the window buffer and s_next are reused by the next window
       }
+    }
+    {  // the item's rows, summed over its windows in order, out to HBM
+      double *dst = T.partials + (size_t)s_desc.pbase * PS;
+      for (uint32_t i = threadIdx.x; i < hp_n * PS; i += kFThreads) dst[i] = s_rows[i];
     }
     if (threadIdx.x == 0) {
       s_cur = nxt;

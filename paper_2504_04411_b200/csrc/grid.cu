@@ -72,11 +72,11 @@ __global__ void __launch_bounds__(256)
 // otherwise the bounds are folded back to reference cells (>> shift, exact).
 __global__ void k_grid_header(const long long *__restrict__ bounds, const double *__restrict__ cell_ptr,
                               uint32_t n, unsigned long long max_cells, uint32_t S_req,
-                              GridHeader *__restrict__ hdr) {
+                              const uint32_t *__restrict__ lean_ok, GridHeader *__restrict__ hdr) {
   GridHeader g;
   g.cell = *cell_ptr;
   g.n = n;
-  g.pad = 0;
+  g.lean = 0;
   uint32_t shift = 0;
   while ((1u << shift) < S_req) ++shift;
   long long b[6];
@@ -93,6 +93,7 @@ __global__ void k_grid_header(const long long *__restrict__ bounds, const double
   }
   g.S = 1u << shift;
   g.shift = shift;
+  g.lean = (shift > 0 && lean_ok != nullptr && *lean_ok != 0u) ? 1u : 0u;
   g.inv = dm(dd(1.0, g.cell), (double)g.S);
   if (n == 0) {
     g.ix0 = g.iy0 = g.iz0 = 0;
@@ -131,44 +132,31 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Fine-layout records packed in input order (coalesced reads of the SoA input
-// and 64-B contiguous writes); the permutation then moves whole 64-B records.
-__device__ __forceinline__ void fine_record(const float *__restrict__ pos, const float *__restrict__ nrm,
-                                            const float *__restrict__ wi, const float *__restrict__ pw,
-                                            const uint32_t *__restrict__ depth, size_t j, float4 &q0,
-                                            float4 &q1, float4 &q2, float4 &q3) {
-  const size_t o = 3 * j;
-  const float nx = nrm[o], ny = nrm[o + 1], wx = wi[o], wy = wi[o + 1];
-  const double L = elum((double)pw[o], (double)pw[o + 1], (double)pw[o + 2]);
-  const unsigned long long Lb = (unsigned long long)__double_as_longlong(L);
-  const uint32_t flags =
-      (fabsf(nx) < INFINITY && fabsf(ny) < INFINITY && fabsf(wx) < INFINITY && fabsf(wy) < INFINITY) ? 1u
-                                                                                                     : 0u;
-  q0 = make_float4(pos[o], pos[o + 1], pos[o + 2], __uint_as_float(depth[j]));
-  q1 = make_float4(nrm[o + 2], wi[o + 2], __uint_as_float((uint32_t)Lb), __uint_as_float((uint32_t)(Lb >> 32)));
-  q2 = make_float4(pw[o], pw[o + 1], pw[o + 2], __uint_as_float(flags));
-  q3 = make_float4(nx, ny, wx, wy);
-}
-
 __global__ void __launch_bounds__(256)
     k_pack_fine(const float *__restrict__ pos, const float *__restrict__ nrm, const float *__restrict__ wi,
                 const float *__restrict__ pw, const uint32_t *__restrict__ depth, uint32_t n,
-                float4 *__restrict__ pack) {
+                const GridHeader *__restrict__ hdr, double guard, float4 *__restrict__ pack) {
+  const bool lean = hdr->lean != 0u;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     float4 q0, q1, q2, q3;
-    fine_record(pos, nrm, wi, pw, depth, i, q0, q1, q2, q3);
     float4 *d = pack + 4 * (size_t)i;
+    if (lean) {
+      lean_record(pos, nrm, wi, pw, depth, i, guard, q0, q1, q2);
+    } else {
+      fine_record(pos, nrm, wi, pw, depth, i, q0, q1, q2, q3);
+      d[3] = q3;
+    }
     d[0] = q0;
     d[1] = q1;
     d[2] = q2;
-    d[3] = q3;
   }
 }
 
 __global__ void __launch_bounds__(256)
     k_permute_packed(const uint32_t *__restrict__ order, uint32_t n, const float4 *__restrict__ pack,
                      float4 *__restrict__ rec0, float4 *__restrict__ rec1, float4 *__restrict__ rec2,
-                     float4 *__restrict__ rec3) {
+                     float4 *__restrict__ rec3, const GridHeader *__restrict__ hdr) {
+  if (hdr != nullptr && hdr->lean != 0u) rec3 = nullptr;  // lean records: 48 B
   // U records per thread per round, all loads issued before the stores
   // (random 64-B record reads: latency bound without the extra parallelism)
   constexpr uint32_t U = 4;
@@ -182,7 +170,8 @@ __global__ void __launch_bounds__(256)
     for (uint32_t u = 0; u < U; ++u) {
       const float4 *src = pack + 4 * (size_t)o[u];
       if (i0 + u * stride < n) {
-        q[u][0] = __ldg(&src[0]); q[u][1] = __ldg(&src[1]); q[u][2] = __ldg(&src[2]); q[u][3] = __ldg(&src[3]);
+        q[u][0] = __ldg(&src[0]); q[u][1] = __ldg(&src[1]); q[u][2] = __ldg(&src[2]);
+        if (rec3) q[u][3] = __ldg(&src[3]);
       }
     }
 #pragma unroll
@@ -192,7 +181,7 @@ __global__ void __launch_bounds__(256)
         __stcs(&rec0[i], q[u][0]);
         __stcs(&rec1[i], q[u][1]);
         __stcs(&rec2[i], q[u][2]);
-        __stcs(&rec3[i], q[u][3]);
+        if (rec3) __stcs(&rec3[i], q[u][3]);
       }
     }
   }
@@ -549,15 +538,16 @@ void launch_cell_bounds(cudaStream_t s, const float *pos, uint32_t n, const doub
 }
 
 void launch_grid_header(cudaStream_t s, const long long *bounds, const double *cell, uint32_t n,
-                        unsigned long long max_cells, uint32_t S, GridHeader *hdr) {
-  k_grid_header<<<1, 1, 0, s>>>(bounds, cell, n, max_cells, S, hdr);
+                        unsigned long long max_cells, uint32_t S, const uint32_t *lean_ok, GridHeader *hdr) {
+  k_grid_header<<<1, 1, 0, s>>>(bounds, cell, n, max_cells, S, lean_ok, hdr);
   note_launches(1);
 }
 
 void launch_pack_fine(cudaStream_t s, const float *pos, const float *nrm, const float *wi, const float *pw,
-                      const uint32_t *depth, uint32_t n, float4 *pack, int sms) {
+                      const uint32_t *depth, uint32_t n, const GridHeader *hdr, double guard, float4 *pack,
+                      int sms) {
   if (n == 0) return;
-  k_pack_fine<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(pos, nrm, wi, pw, depth, n, pack);
+  k_pack_fine<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(pos, nrm, wi, pw, depth, n, hdr, guard, pack);
   note_launches(1);
 }
 
@@ -602,11 +592,11 @@ void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const 
 
 void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const float *pos,
                     const float *nrm, const float *wi, const float *pw, const uint32_t *depth,
-                    const PhotonRecs &r, int fine_layout, int sms) {
+                    const PhotonRecs &r, int fine_layout, const GridHeader *hdr, int sms) {
   if (n == 0) return;
   if (fine_layout && r.pack)
     k_permute_packed<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, r.pack, r.rec0, r.rec1, r.rec2,
-                                                                  r.rec3);
+                                                                  r.rec3, hdr);
   else if (fine_layout)
     k_permute_fine<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
                                                                 r.rec0, r.rec1, r.rec2, r.rec3);
@@ -614,7 +604,7 @@ void launch_permute(cudaStream_t s, const uint32_t *order, uint32_t n, const flo
     k_pack_std<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(pos, nrm, wi, pw, depth, n, r.pack);
     note_launches(1);
     k_permute_packed<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, r.pack, r.rec0, r.rec1, r.rec2,
-                                                                  r.rec3);
+                                                                  r.rec3, nullptr);
   } else
     k_permute<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(order, n, pos, nrm, wi, pw, depth,
                                                            r.rec0, r.rec1, r.rec2, r.rec3);
