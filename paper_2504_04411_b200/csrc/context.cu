@@ -1397,7 +1397,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       F.total_items = S.item_base + nb;
       T.desc = nullptr;
       if ((rc = kernel_event(ctx, 0))) return rc;
-      FPPM_CUDA_OK(launch_gather_fine(s, A, F, ctx->C, ctx->sms));
+      FPPM_CUDA_OK(launch_gather_fine(s, A, F, ctx->C, ctx->sms, g.lean != 0u));
       if ((rc = kernel_event(ctx, 1))) return rc;
     } else {
       FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms, chunk));

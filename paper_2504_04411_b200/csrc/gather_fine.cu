@@ -1004,18 +1004,15 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
 
 // A hit point of a lean-layout frame that is not itself lean (another
 // normal, a non-gray weight, ...): every candidate on the exact fp64 path,
-// accumulated with the general slots / packed counts.
-template <int GMAX>
-static __device__ __forceinline__ void exact_fragment(const GatherArgs &A, const FineHot &Hh, const Hit &Hs,
-                                                      uint32_t rs, uint32_t rl, uint32_t slots,
-                                                      PackedCounts<GMAX> &cnt, double &p0, double &p1,
-                                                      double &p2, const FineWin &Wn, FineState &st) {
+// its full value v = lum(K * pw) accumulated in the lean slots (reduced with
+// scale 1), counts in nibbles.
+template <int NA>
+static __device__ __forceinline__ void exact_fragment_lean(const GatherArgs &A, const FineHot &Hh, const Hit &Hs,
+                                                           uint32_t rs, uint32_t rl, uint32_t slot_lane,
+                                                           LeanCnt &c, double &p0, double &p1, double &p2,
+                                                           const FineWin &Wn, FineState &st) {
   const int lane = threadIdx.x & 31;
-  HitV K;
-  K.K0 = Hh.K0; K.K1 = Hh.K1; K.K2 = Hh.K2;
-  K.gray = false;
-  K.Kz0 = dm(Hh.K0, 0.0); K.Kz1 = dm(Hh.K1, 0.0); K.Kz2 = dm(Hh.K2, 0.0);
-  K.Kz = elum(K.Kz0, K.Kz1, K.Kz2);
+  const double Kz = elum(dm(Hh.K0, 0.0), dm(Hh.K1, 0.0), dm(Hh.K2, 0.0));  // bsdf.cpp:58 (f = 0)
   uint32_t incl = rl;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1025,6 +1022,7 @@ static __device__ __forceinline__ void exact_fragment(const GatherArgs &A, const
   const uint32_t off = rs - (incl - rl);
   const uint32_t total = __shfl_sync(kFull, incl, 31);
   if (lane == 0) st.n_cand += total;
+  uint32_t spill = 15;
   for (uint32_t base = 0; base < total; base += 32) {
     const uint32_t v = base + lane;
     int j = 0;
@@ -1039,9 +1037,21 @@ static __device__ __forceinline__ void exact_fragment(const GatherArgs &A, const
       st.n_exact += 1;
       st.n_amb += (fl >> 2) & 1u;
     }
-    fine_accumulate<GMAX, 1, false>(K, (fl & 1u) != 0, (fl & 2u) != 0, (int)(fl >> 8), pw, L, slots, lane, cnt,
-                                    p0, p1, p2);
+    if (--spill == 0) {
+      lean_spill(c);
+      spill = 15;
+    }
+    LeanPair q;
+    q.acc = (fl & 1u) != 0;
+    const bool on = q.acc && (fl & 2u) != 0;
+    q.L = on ? elum(dm(Hh.K0, (double)pw.x), dm(Hh.K1, (double)pw.y), dm(Hh.K2, (double)pw.z)) : Kz;
+    q.r = on ? (double)pw.x : 0.0;
+    q.g = on ? (double)pw.y : 0.0;
+    q.b = on ? (double)pw.z : 0.0;
+    q.s4 = q.acc ? (fl >> 8) * 4u : 16u * NA;
+    lean_add(q, slot_lane, c.n0, p0, p1, p2);
   }
+  lean_spill(c);
   __syncwarp();
 }
 
@@ -1111,7 +1121,9 @@ static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, dou
   __syncwarp();
 }
 
-template <int GMAX, int CH>
+// LEAN: the lean-layout instantiation (GridHeader::lean): only the lean
+// fragment and its exact fallback are compiled in (register budget).
+template <int GMAX, int CH, bool LEAN>
 __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
     k_gather_fine(const GatherArgs A, const FineArgs T) {
   using Lay = FineLayout<GMAX, CH>;
@@ -1245,38 +1257,31 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
           if (!__any_sync(kFull, rl != 0)) continue;
           const Hit &Hs = T.hits[s_desc.hp_lo + k];  // full state: exact path only
           double *acc = out + (size_t)k * PS;  // windows of an item run in order in one CTA
+          double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+          if constexpr (LEAN) {
+            constexpr int NA = GMAX / 4;
+            LeanCnt lc = {0u, 0u, 0u, 0u};
+            const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
+            if (Hh.gray & 2u) {
+              lean_fragment<NA>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
+              lean_reduce<GMAX>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st);
+            } else {
+              exact_fragment_lean<NA>(A, Hh, Hs, rs, rl, slot_lane, lc, p0, p1, p2, Wn, st);
+              lean_reduce<GMAX>(slots, lane, 1.0, lc, p0, p1, p2, acc, st);
+            }
+            continue;
+          } else {
           PackedCounts<GMAX> cnt;
 #pragma unroll
           for (int r = 0; r < PackedCounts<GMAX>::NP; ++r) cnt.w[r] = 0;
-          double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-          bool done = false;
-          if constexpr (CH == 1 && GMAX <= 8) {
-            if (g.lean) {
-              if (Hh.gray & 2u) {
-                LeanCnt lc = {0u, 0u, 0u, 0u};
-                const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
-                if (A.na == 2)
-                  lean_fragment<2>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
-                else
-                  lean_fragment<1>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
-                lean_reduce<GMAX>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st);
-                continue;
-              }
-              exact_fragment<GMAX>(A, Hh, Hs, rs, rl, slots, cnt, p0, p1, p2, Wn, st);
-              done = true;
-            }
-          }
-          if (!done) {
-            if (Hh.planar && (Hh.gray & 1u))
-              fine_fragment<GMAX, CH, true, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
-            else if (Hh.planar)
-              fine_fragment<GMAX, CH, true, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
-            else if (Hh.gray & 1u)
-              fine_fragment<GMAX, CH, false, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
-            else
-              fine_fragment<GMAX, CH, false, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn,
-                                                    st);
-          }
+          if (Hh.planar && (Hh.gray & 1u))
+            fine_fragment<GMAX, CH, true, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+          else if (Hh.planar)
+            fine_fragment<GMAX, CH, true, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+          else if (Hh.gray & 1u)
+            fine_fragment<GMAX, CH, false, true>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
+          else
+            fine_fragment<GMAX, CH, false, false>(A, Hh, Hs, rs, rl, nr, exa, slots, cnt, p0, p1, p2, Wn, st);
 
           // ---- fixed-order reduction of the lane slots, added to the hp's row
           const int col = lane % NC, grp = lane / NC;
@@ -1331,6 +1336,7 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
             acc[GMAX + 2 * CH * GMAX + 2] += p2;
           }
           __syncwarp();
+          }
         }
         __syncthreads();  // the window buffer and s_next are reused by the next window
       }
@@ -1441,18 +1447,18 @@ cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &
   return cudaGetLastError();
 }
 
-template <int GMAX, int CH>
+template <int GMAX, int CH, bool LEAN>
 static cudaError_t launch_fine_t(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int sms) {
   using Lay = FineLayout<GMAX, CH>;
   const size_t smem = Lay::kDynBytes;
-  cudaError_t e = cudaFuncSetAttribute(k_gather_fine<GMAX, CH>,
+  cudaError_t e = cudaFuncSetAttribute(k_gather_fine<GMAX, CH, LEAN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_fine<GMAX, CH>, kFThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_fine<GMAX, CH, LEAN>, kFThreads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  k_gather_fine<GMAX, CH><<<sms * per_sm, kFThreads, smem, s>>>(A, T);
+  k_gather_fine<GMAX, CH, LEAN><<<sms * per_sm, kFThreads, smem, s>>>(A, T);
   note_launches(1);
   return cudaGetLastError();
 }
@@ -1460,17 +1466,21 @@ static cudaError_t launch_fine_t(cudaStream_t s, const GatherArgs &A, const Fine
 size_t fine_hot_bytes() { return sizeof(FineHot); }
 size_t fine_hit_bytes() { return sizeof(Hit); }
 
-cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms) {
+cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms, bool lean) {
   const int G = A.na * A.ns;
+  if (lean) {  // C = 1, n_s = 4, n_a <= 2 (lean_config)
+    if (C != 1 || A.ns != 4 || A.na > 2) return cudaErrorInvalidValue;
+    return A.na == 1 ? launch_fine_t<4, 1, true>(s, A, T, sms) : launch_fine_t<8, 1, true>(s, A, T, sms);
+  }
   if (C == 1) {
-    if (G <= 4) return launch_fine_t<4, 1>(s, A, T, sms);
-    if (G <= 8) return launch_fine_t<8, 1>(s, A, T, sms);
-    if (G <= 12) return launch_fine_t<12, 1>(s, A, T, sms);
-    if (G <= 16) return launch_fine_t<16, 1>(s, A, T, sms);
+    if (G <= 4) return launch_fine_t<4, 1, false>(s, A, T, sms);
+    if (G <= 8) return launch_fine_t<8, 1, false>(s, A, T, sms);
+    if (G <= 12) return launch_fine_t<12, 1, false>(s, A, T, sms);
+    if (G <= 16) return launch_fine_t<16, 1, false>(s, A, T, sms);
     return cudaErrorInvalidValue;
   }
-  if (G <= 4) return launch_fine_t<4, 3>(s, A, T, sms);
-  if (G <= 8) return launch_fine_t<8, 3>(s, A, T, sms);
+  if (G <= 4) return launch_fine_t<4, 3, false>(s, A, T, sms);
+  if (G <= 8) return launch_fine_t<8, 3, false>(s, A, T, sms);
   return cudaErrorInvalidValue;
 }
 
