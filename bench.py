@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--workload", default="c2", choices=["c1", "c2"])
-    p.add_argument("--kernel", default="auto", choices=["auto", "fine", "tile", "warp", "lanes", "sparse"],
+    p.add_argument("--kernel", default="auto", choices=["auto", "fine", "warp", "3d"],
                    help="gather kernel variant (A/B)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -105,7 +105,7 @@ class ClockSampler:
 
 KERNEL_NAMES = {"auto": "k_gather_fine (gather + accumulate; F-test fused in k_tile_finalize)",
                 "fine": "k_gather_fine (gather + accumulate; F-test fused in k_tile_finalize)",
-                "tile": "k_gather_tiles", "lanes": "k_gather_lanes", "warp": "k_gather_test"}
+                "warp": "k_gather_test", "3d": "k_gather_3d (gather + accumulate; F-test in k_apply_deltas)"}
 
 
 # ---------------------------------------------------------------- helpers

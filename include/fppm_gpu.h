@@ -93,13 +93,14 @@ typedef struct fppm_gpu_config {
   uint32_t max_cells; /* 0 -> 1<<28 dense cells */
   int32_t device;     /* CUDA ordinal */
   void *stream;       /* cudaStream_t to order work on; NULL -> own stream */
-  int32_t gather_kernel; /* 0 auto: 4 on slab (planar) grids, 5 on 3D grids; 1 warp per hit
-                            point; 2 tiled; 3 lanes = hit points; 4 fine-cell tiled;
-                            5 thread per hit point (sparse 3D frames) */
+  int32_t gather_kernel; /* 0 auto: 4 on slab (planar) grids when n_a*n_s*channels <= 24, else 5;
+                            1 warp per hit point over reference cells (cross-check);
+                            4 fine-cell tiled (slab grids; 3D grids use 5);
+                            5 warp per hit point over 3D fine columns (S = 2 or 1) */
   /* VCM+ merge stage (integrator.cpp:595-627): every gathered photon value is
    * weighted by mis_weight_merge (path.cpp:103-111) with the tested radius;
    * needs fppm_gpu_set_hitpoint_mis / fppm_gpu_set_photon_mis; runs on the
-   * warp kernel (gather_kernel 0 or 1) or the sparse kernel (5) */
+   * 3D kernel (gather_kernel 0 or 5) or the warp kernel (1) */
   int32_t vcm_plus;
   int32_t mis_n_vm;   /* MisContext::n_vm (light paths per iteration, integrator.cpp:133) */
   double mis_beta;    /* MisContext::beta (MIS power) */

@@ -111,7 +111,7 @@ class FppmContext:
         cfg.max_hitpoints, cfg.max_photons, cfg.max_cells = max_hitpoints, max_photons, max_cells
         cfg.device = device
         cfg.stream = stream
-        cfg.gather_kernel = {"auto": 0, "warp": 1, "tile": 2, "lanes": 3, "fine": 4, "sparse": 5}[gather_kernel]
+        cfg.gather_kernel = {"auto": 0, "warp": 1, "fine": 4, "3d": 5, "sparse": 5}[gather_kernel]
         cfg.vcm_plus, cfg.mis_n_vm, cfg.mis_beta = int(bool(vcm_plus)), int(mis_n_vm), float(mis_beta)
         self.config = cfg
         self.device = device

@@ -172,19 +172,23 @@ static cudaError_t dalloc(T **p, size_t count) {
   return cudaMalloc(reinterpret_cast<void **>(p), sizeof(T) * count);
 }
 
-// gather kernel variant: 1 warp per hit point, 2 tiled, 3 lanes, 4 fine (default)
+// gather kernel variant: 1 warp per hit point over reference cells (the
+// reference query order; kept selectable as a cross-check), 4 fine (slab
+// grids, the default where G * C <= 24), 5 the 3D warp-per-hit-point kernel
+// over fine columns (every other grid and configuration, VCM+ merges)
 static int gather_variant(const fppm_gpu_ctx *ctx) {
-  // merge weights: the thread-per-hit-point kernel (auto) or the warp kernel
-  if (ctx->cfg.vcm_plus) return ctx->cfg.gather_kernel == 1 ? 1 : 5;
-  if (ctx->cfg.gather_kernel == 0) return fine_supported(ctx->G, ctx->C) ? 4 : 2;
-  return ctx->cfg.gather_kernel;
+  if (ctx->cfg.gather_kernel == 1) return 1;
+  if (ctx->cfg.vcm_plus) return 5;
+  if (ctx->cfg.gather_kernel == 5) return 5;
+  return fine_supported(ctx->G, ctx->C) ? 4 : 5;
 }
 
-// The kernel that will gather this grid: auto picks the fine kernel on slab
-// (planar) grids and the thread-per-hit-point kernel on 3D grids (S = 1).
+// The kernel that will gather this grid: the fine kernel on slab (planar)
+// grids, the 3D kernel on 3D grids (S = 1 or 2).
 static int effective_variant(const fppm_gpu_ctx *ctx, uint32_t S) {
   const int v = gather_variant(ctx);
-  return v == 4 && ctx->cfg.gather_kernel == 0 && S == 1 ? 5 : v;
+  if (v == 4 && S != kFineS) return 5;  // 3D grid (S = 1 or 2): the warp-per-hit-point 3D kernel
+  return v;
 }
 
 static cudaError_t ensure_scratch(fppm_gpu_ctx *ctx, size_t bytes) {
@@ -391,8 +395,10 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   if ((long long)c.n_annuli * c.n_sectors > 32) return FPPM_ERR_CAPACITY;
   if (c.channels != FPPM_CHANNELS_LUMINANCE && c.channels != FPPM_CHANNELS_RGB) return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy < FPPM_POLICY_FTEST || c.policy > FPPM_POLICY_SCHEDULE) return FPPM_ERR_INVALID_ARGUMENT;
-  if (c.gather_kernel < 0 || c.gather_kernel > 5) return FPPM_ERR_INVALID_ARGUMENT;
-  if (c.vcm_plus && ((c.gather_kernel > 1 && c.gather_kernel != 5) || c.mis_n_vm < 0 || !(c.mis_beta > 0.0)))
+  // gather_kernel: 0 auto, 1 warp (reference cells), 4 fine, 5 3D
+  if (c.gather_kernel < 0 || c.gather_kernel > 5 || c.gather_kernel == 2 || c.gather_kernel == 3)
+    return FPPM_ERR_INVALID_ARGUMENT;
+  if (c.vcm_plus && (c.gather_kernel == 4 || c.mis_n_vm < 0 || !(c.mis_beta > 0.0)))
     return FPPM_ERR_INVALID_ARGUMENT;
   if (c.policy == FPPM_POLICY_FTEST && c.override_decision == FPPM_OVERRIDE_NONE &&
       !(c.alpha_f > 0.0 && c.alpha_f < 1.0)) return FPPM_ERR_INVALID_ARGUMENT;  // stat_tests.cpp:88
@@ -515,7 +521,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (p) cudaFree(p);
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
-                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.desc, T.fdesc, T.fhot, T.fbox, T.fhit, T.pbase, T.partials,
+                  T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.fdesc, T.fhot, T.fbox, T.fhit, T.pbase, T.partials,
                   T.hp_map, T.nonempty};
   for (void *p : tdev)
     if (p) cudaFree(p);
@@ -1025,7 +1031,10 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
 // back to reference cells on demand (ensure_reference_cells).
 int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
-  return build_grid_impl(ctx, cell_size, gather_variant(ctx) == 4 ? kFineS : 1u);
+  // the fine kernel asks for slab fine cells (falling back to 3D fine cells
+  // S = 2 or reference cells), the 3D kernel for S = 2 where the table fits
+  const int v = gather_variant(ctx);
+  return build_grid_impl(ctx, cell_size, v == 4 ? kFineS : (v == 5 ? 2u : 1u));
 }
 
 // query_ball / export need the reference-cell table
@@ -1327,49 +1336,32 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       S.bucket_cap = cap;
     }
     uint32_t nb = 0;
-    // kernel choice: the fine-cell tiled kernel is the default (it needs the
-    // fine record layout and supports G*C <= 24); the tiled, lanes and warp
-    // kernels are selectable for A/B runs and as parity cross-checks
-    int variant = gather_variant(ctx);
-    if (variant == 4 && !fine_supported(ctx->G, ctx->C))
-      return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "fine gather supports n_a*n_s*channels <= 24; "
-                                                  "select gather_kernel 1-3");
+    // the fine-cell tiled kernel (slab grids, G * C <= 24)
     uint32_t cap64 = 0, cap48 = 0;
-    if (variant == 4) fine_caps(ctx->G, ctx->C, &cap64, &cap48);
-    const uint32_t chunk = variant == 3 ? (uint32_t)kLaneChunk : (uint32_t)kChunk;
+    fine_caps(ctx->G, ctx->C, &cap64, &cap48);
     FPPM_CUDA_OK(cudaMemsetAsync(S.nonempty, 0, sizeof(uint32_t), s));
-    if (variant == 4)
-      FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, cap64, cap48, &nb));
-    else
-      FPPM_CUDA_OK(tile_schedule_bins(s, A, S, g, ctx->sms, chunk, &nb));
+    FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, cap64, cap48, &nb));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
                                  cudaMemcpyDeviceToHost, s));
-    if (variant == 4)
-      FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total + 1, S.pbase + nb, sizeof(uint32_t),
-                                   cudaMemcpyDeviceToHost, s));
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total + 1, S.pbase + nb, sizeof(uint32_t),
+                                 cudaMemcpyDeviceToHost, s));
     const auto t2 = now();
     FPPM_CUDA_OK(cudaStreamSynchronize(s));
     const auto t3 = now();
     const uint32_t total = ctx->h_total[0];
     if (dbg)
       std::fprintf(stderr, "[fppm] iteration %llu items %u rows %u (caps %llu %llu) crit %.3f sched-issue %.3f sync %.3f ms\n",
-                   (unsigned long long)iteration, total, variant == 4 ? ctx->h_total[1] : total * 32u,
-                   S.item_cap, S.row_cap, ms(t0, t1), ms(t1, t2), ms(t2, t3));
-    // partial rows: fine = one per (hit point, item); tiled = 32 per item
-    const unsigned long long rows =
-        variant == 4 ? (unsigned long long)ctx->h_total[1] : (unsigned long long)total * 32ull;
+                   (unsigned long long)iteration, total, ctx->h_total[1], S.item_cap, S.row_cap, ms(t0, t1),
+                   ms(t1, t2), ms(t2, t3));
+    // partial rows: one per (hit point, item)
+    const unsigned long long rows = (unsigned long long)ctx->h_total[1];
     if (total > S.item_cap) {
-      if (S.desc) cudaFree(S.desc);
       if (S.fdesc) cudaFree(S.fdesc);
-      S.desc = nullptr;
       S.fdesc = nullptr;
       // generous growth: reallocation inside a timed loop costs milliseconds
       const unsigned long long cap =
           std::max<unsigned long long>(2ull * total, (unsigned long long)ctx->H / 8 + 4096);
-      if (variant == 4)
-        FPPM_CUDA_OK(dalloc(&S.fdesc, cap));
-      else
-        FPPM_CUDA_OK(dalloc(&S.desc, cap));
+      FPPM_CUDA_OK(dalloc(&S.fdesc, cap));
       S.item_cap = cap;
     }
     if (rows > S.row_cap) {
@@ -1385,7 +1377,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
     T.partials = S.partials;
     T.hp_map = S.hp_map;
     T.total_items = S.item_base + nb;
-    if (variant == 4) {
+    {
       FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48));
       FineArgs F;
       F.desc = S.fdesc;
@@ -1398,15 +1390,6 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       T.desc = nullptr;
       if ((rc = kernel_event(ctx, 0))) return rc;
       FPPM_CUDA_OK(launch_gather_fine(s, A, F, ctx->C, ctx->sms, g.lean != 0u));
-      if ((rc = kernel_event(ctx, 1))) return rc;
-    } else {
-      FPPM_CUDA_OK(tile_schedule_items(s, A, S, nb, ctx->sms, chunk));
-      T.desc = S.desc;
-      if ((rc = kernel_event(ctx, 0))) return rc;
-      if (variant == 3)
-        FPPM_CUDA_OK(launch_gather_lanes(s, A, T, ctx->C, ctx->sms));
-      else
-        FPPM_CUDA_OK(launch_gather_tiles(s, A, T, ctx->C, ctx->sms));
       if ((rc = kernel_event(ctx, 1))) return rc;
     }
     FPPM_CUDA_OK(launch_tile_finalize(s, A, T, ctx->C, ctx->sms));

@@ -233,58 +233,63 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
   }
 }
 
-// ---------------------------------------------------------------- sparse frames
-// Thread per hit point, for 3D frames with a few hit points per cell (C3's
-// camera hit points on the walls, C5): the per-hit-point fixed cost of the
-// warp kernel (a 5-level warp reduction of 3 G accumulators and a
-// single-lane end-of-iteration) exceeds its ~100 candidates, so here each
-// thread walks its own 9 columns of the 27-cell neighbourhood with the same
-// pair code and runs finalize_hit itself.  Neighbouring threads hold nearby
-// hit points (pixel order), so their photon records share L1/L2 lines.
-constexpr int kSparseThreads = 128;
-#ifndef FPPM_SPARSE_U
-#define FPPM_SPARSE_U 4
-#endif
-constexpr int kSparseU = FPPM_SPARSE_U;
+// ---------------------------------------------------------------- 3D gather
+// Frames whose photons fill a volume (C3 / C4 camera hit points on the walls,
+// the C5 clusters): a warp owns one hit point at a time (hit points visited
+// in cell order, so consecutive warps share cells in L1/L2).  Its candidate
+// runs are the (x, y) columns of its fine box -- S = 2 fine cells when the
+// dense table fits, else reference cells -- clipped to the 27-neighbourhood
+// and to the ball's chord (gather_dev.cuh run_keys_clipped); the lanes walk
+// the concatenated runs one candidate each, reading the sorted records
+// straight from L2 (coalesced within a run).  Three stages per candidate:
+// ball + depth + disk on rec0 (test_pair), the normal guard on rec1 (certain
+// rejections only), then the full banded decision and value (pair_tail,
+// exact fp64 path inside).  Accepted values go to the lane's shared-memory
+// slot [(c * G + sector)][lane] {sum, sum_sq}; counts in 4-bit fields; at
+// the end the slots are reduced in a fixed order into the hit point's
+// option-B row (k_apply_deltas pools it and runs the end of iteration).
+constexpr int kG3Warps = 4;
+constexpr int kG3Threads = kG3Warps * kWarp;
+
+size_t sparse_smem_bytes(int G, int C) {
+  return (size_t)kG3Warps * (sizeof(Hit) + (size_t)(G * C + 1) * 32 * 16);
+}
+
+template <int NW>
+static __device__ __forceinline__ void g3_spill(uint32_t (&nib)[NW], uint32_t (&lo)[NW], uint32_t (&hi)[NW]) {
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    lo[w] += nib[w] & 0x0F0F0F0Fu;         // sectors 8w + 0, 2, 4, 6 in bytes
+    hi[w] += (nib[w] >> 4) & 0x0F0F0F0Fu;  // sectors 8w + 1, 3, 5, 7
+    nib[w] = 0u;
+  }
+}
 
 template <int GMAX, int CH>
-#ifndef FPPM_SPARSE_MINB
-#define FPPM_SPARSE_MINB 4
-#endif
-__global__ void __launch_bounds__(kSparseThreads, FPPM_SPARSE_MINB) k_gather_sparse(const GatherArgs A, const uint32_t *__restrict__ order,
-                                                                   double *__restrict__ rows) {
-  // per thread: its Hit (exact path) and its sector accumulators, indexed
-  // [slot][thread] so a lane's dynamic sector index costs one LDS/STS
+__global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, const uint32_t *__restrict__ order,
+                                                        double *__restrict__ rows) {
+  constexpr int NW = (GMAX + 7) / 8;  // count words (8 sectors of 4 bits each)
   extern __shared__ __align__(16) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = A.na * A.ns, CG = G * CH;
-  const int t = threadIdx.x;
-  HitX *s_hit = reinterpret_cast<HitX *>(s_raw);
-  double *s_sum = reinterpret_cast<double *>(s_hit + kSparseThreads);   // [CG][T]
-  double *s_sq = s_sum + (size_t)CG * kSparseThreads;                     // [CG][T]
-  uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_sq + (size_t)CG * kSparseThreads);  // [G][T]
-  HitX &Hs = s_hit[t];
-  const GridHeader grid = *A.grid;
+  Hit &Hs = reinterpret_cast<Hit *>(s_raw)[warp];
+  double *slot_base = reinterpret_cast<double *>(s_raw + kG3Warps * sizeof(Hit)) + (size_t)warp * (CG + 1) * 64;
+  for (int i = lane; i < (CG + 1) * 64; i += 32) slot_base[i] = 0.0;
+  const uint32_t slots = smem_u32(slot_base);
+  const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
+  const GridHeader g = *A.grid;
   uint32_t my_cand = 0, my_exact = 0, my_amb = 0, my_acc = 0;
-  for (uint32_t q = blockIdx.x * blockDim.x + t; q < A.H; q += gridDim.x * blockDim.x) {
+  for (;;) {
+    uint32_t q = 0;
+    if (lane == 0) q = atomicAdd(A.work, 1u);
+    q = __shfl_sync(kFull, q, 0);
+    if (q >= A.H) break;
     const uint32_t h = order ? order[q] : q;
-    HitF F;
-    {
-      Hit H;
-      make_hit(A, h, H);
-      F = hitf(H, A.na, A.ns);
-      Hs.cx = H.cx; Hs.cy = H.cy; Hs.cz = H.cz;
-      Hs.nx = H.nx; Hs.ny = H.ny; Hs.nz = H.nz;
-      Hs.u = H.u; Hs.v = H.v;
-      Hs.r = H.r; Hs.r2 = H.r2;
-      Hs.K0 = H.K0; Hs.K1 = H.K1; Hs.K2 = H.K2;
-    }
+    __syncwarp();
+    if (lane == 0) make_hit(A, h, Hs);
+    __syncwarp();
+    const HitF F = hitf(Hs, A.na, A.ns);
     const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
-    for (int k = 0; k < CG; ++k) {
-      s_sum[k * kSparseThreads + t] = 0.0;
-      s_sq[k * kSparseThreads + t] = 0.0;
-    }
-    for (int g = 0; g < G; ++g) s_cnt[g * kSparseThreads + t] = 0u;
-    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
     EyeVcm eye{0.0, 0.0, 0.0, 0.0};
     if (A.vcm) {
       const double3 wo = A.wo[h], al = A.alb[h];
@@ -296,113 +301,193 @@ __global__ void __launch_bounds__(kSparseThreads, FPPM_SPARSE_MINB) k_gather_spa
       eye.d_vcm = em.x;
       eye.d_vm = em.y;
     }
-    if (gathered && grid.n > 0) {
-      const long long ix = (long long)floor(dm(Hs.cx, grid.inv)) - grid.ix0;
-      const long long iy = (long long)floor(dm(Hs.cy, grid.inv)) - grid.iy0;
-      const long long iz = (long long)floor(dm(Hs.cz, grid.inv)) - grid.iz0;
-      const long long z0 = iz - 1 < 0 ? 0 : iz - 1;
-      const long long z1 = iz + 1 >= grid.nz ? grid.nz - 1 : iz + 1;
-      // 9 (x, y) columns, each one contiguous z range of the sorted records
-#pragma unroll 1
-      for (int col = 0; col < 9; ++col) {
-        const long long X = ix + col / 3 - 1, Y = iy + col % 3 - 1;
-        if (X < 0 || X >= grid.nx || Y < 0 || Y >= grid.ny || z0 > z1) continue;
-        const unsigned long long k0 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z0);
-        const unsigned long long k1 = (unsigned long long)((X * grid.ny + Y) * grid.nz + z1);
-        const uint32_t beg = __ldg(&A.cell_start[k0]), end = __ldg(&A.cell_start[k1 + 1]);
-        my_cand += end - beg;
-        // kSparseU candidates per step: their record loads are issued
-        // together (the loop is latency bound, one chain per thread)
-        for (uint32_t i0 = beg; i0 < end; i0 += kSparseU) {
-          float4 ra[kSparseU], rb[kSparseU], rc[kSparseU], rd[kSparseU];
-          bool live[kSparseU];
-#pragma unroll
-          for (int u = 0; u < kSparseU; ++u) {
-            live[u] = i0 + u < end;
-            ra[u] = live[u] ? __ldg(&A.rec0[i0 + u]) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int u = 0; u < kSparseU; ++u) live[u] = live[u] && test_pair(F, ra[u], A.max_depth);
-#pragma unroll
-          for (int u = 0; u < kSparseU; ++u)
-            if (live[u]) {
-              rb[u] = __ldg(&A.rec1[i0 + u]);
-              rc[u] = __ldg(&A.rec2[i0 + u]);
-              rd[u] = __ldg(&A.rec3[i0 + u]);
-            }
-#pragma unroll
-          for (int u = 0; u < kSparseU; ++u) {
-            if (!live[u]) continue;
-            int sector;
-            double sv[CH], sw[CH], f0, f1, f2;
-            if (!pair_tail<CH, HitX>(A, F, Hs, i0 + u, eye, ra[u], rb[u], rc[u], rd[u], sector, sv, sw, f0, f1, f2,
-                               my_exact, my_amb))
-              continue;
-            ++my_acc;
-            p0 = da(p0, f0); p1 = da(p1, f1); p2 = da(p2, f2);
-            s_cnt[sector * kSparseThreads + t] += 1u;
-#pragma unroll
-            for (int c = 0; c < CH; ++c) {
-              double &x = s_sum[(c * G + sector) * kSparseThreads + t];
-              double &y = s_sq[(c * G + sector) * kSparseThreads + t];
-              x = da(x, sv[c]);
-              y = da(y, sw[c]);
-            }
-          }
+    // runs: the box's (x, y) columns clipped to the chord (lane j = run j)
+    uint32_t rs = 0, rl = 0;
+    int nruns = 0;
+    {
+      FBox b = {0, -1, 0, -1, 0, -1};
+      if (gathered && fine_box(g, Hs.cx, Hs.cy, Hs.cz, Hs.r, b)) {
+        nruns = run_count(g, b);
+        const double cm = fmax(fabs(Hs.cx), fmax(fabs(Hs.cy), fabs(Hs.cz)));
+        const double m = da(da(Hs.r, dm(Hs.r, 1e-9)), dm(cm, 4e-16));
+        unsigned long long k0, k1;
+        if (lane < nruns && run_keys_clipped(g, b, lane, Hs.cx, Hs.cy, Hs.cz, m, k0, k1)) {
+          rs = __ldg(&A.cell_start[k0]);
+          rl = __ldg(&A.cell_start[k1 + 1]) - rs;
         }
       }
     }
-    // option-B row layout [count G | sum C*G | sum_sq C*G | power 3]; the
-    // end of iteration runs in k_apply_deltas (thread per hit point)
-    double *d = rows + (size_t)h * (size_t)(G + 2 * CG + 3);
-    for (int g = 0; g < G; ++g) d[g] = (double)s_cnt[g * kSparseThreads + t];
-    for (int k = 0; k < CG; ++k) {
-      d[G + k] = s_sum[k * kSparseThreads + t];
-      d[G + CG + k] = s_sq[k * kSparseThreads + t];
+    uint32_t incl = rl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
     }
-    d[G + 2 * CG] = p0;
-    d[G + 2 * CG + 1] = p1;
-    d[G + 2 * CG + 2] = p2;
+    const uint32_t off = rs - (incl - rl);  // sorted index - virtual index within run `lane`
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (lane == 0) my_cand += total;
+    uint32_t nib[NW], lo[NW], hi[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) nib[w] = lo[w] = hi[w] = 0u;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    uint32_t spill = 15;
+    for (uint32_t base = 0; base < total; base += 32) {
+      const uint32_t v = base + lane;
+      // run of v: binary search over the lanes' inclusive ends
+      int j = 0;
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1) {
+        const uint32_t e = __shfl_sync(kFull, incl, (j + st - 1) & 31);
+        if (j + st - 1 < 31 && e <= v) j += st;
+      }
+      if (__shfl_sync(kFull, incl, j & 31) <= v) ++j;
+      const uint32_t i = v + __shfl_sync(kFull, off, j & 31);
+      bool live = v < total;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bb = a, c2 = a, c3 = a;
+      if (live) {
+        a = __ldg(&A.rec0[i]);
+        live = test_pair(F, a, A.max_depth);  // ball (photon_map.cpp:76), depth (:396), disk (:399)
+      }
+      if (live) {
+        bb = __ldg(&A.rec1[i]);
+        // normal guard (integrator.cpp:397): certain rejections only
+        const float gd = fmaf(bb.x, F.nfx, fmaf(bb.y, F.nfy, bb.z * F.nfz));
+        const float gb = 2e-6f * (fabsf(bb.x * F.nfx) + fabsf(bb.y * F.nfy) + fabsf(bb.z * F.nfz)) + 1e-30f;
+        live = !(F.fast && gd < F.guard_f - gb);
+      }
+      int sector = 0;
+      double sv[CH], sw[CH], f0 = 0.0, f1 = 0.0, f2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) sv[c] = sw[c] = 0.0;
+      if (live) {
+        c2 = __ldg(&A.rec2[i]);
+        c3 = __ldg(&A.rec3[i]);
+        live = pair_tail<CH, Hit>(A, F, Hs, i, eye, a, bb, c2, c3, sector, sv, sw, f0, f1, f2, my_exact, my_amb);
+      }
+      if (!live) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) sv[c] = sw[c] = 0.0;
+        f0 = f1 = f2 = 0.0;
+      }
+      if (--spill == 0) {
+        g3_spill<NW>(nib, lo, hi);
+        spill = 15;
+      }
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const uint32_t row = live ? (uint32_t)(c * G + sector) : (uint32_t)CG;  // spare row
+        const uint32_t ad = slot_lane + row * 512u;
+        double2 o;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(o.x), "=d"(o.y) : "r"(ad) : "memory");
+        o.x = da(o.x, sv[c]);
+        o.y = da(o.y, sw[c]);
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ad), "d"(o.x), "d"(o.y) : "memory");
+      }
+      if (live) {
+        ++my_acc;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+          if ((sector >> 3) == w) nib[w] += 1u << ((sector & 7) * 4);
+      }
+      p0 = da(p0, f0);
+      p1 = da(p1, f1);
+      p2 = da(p2, f2);
+    }
+    g3_spill<NW>(nib, lo, hi);
+    // ---- the hit point's option-B row [count G | sum CG | sum_sq CG | power 3]
+    double *d = rows + (size_t)h * (size_t)(G + 2 * CG + 3);
+    // slots: lane (col, grp) sums R rows of column col in a fixed order
+    for (int c0 = 0; c0 < CG; c0 += 32) {
+      const int ncol = min(32, CG - c0);
+      int nq = 1;
+      while (nq * 2 * ncol <= 32) nq *= 2;
+      const int R = 32 / nq;
+      const int col = lane % ncol, grp = lane / ncol;
+      double sm = 0.0, sq = 0.0;
+      if (grp < nq) {
+        const uint32_t bse = slots + (uint32_t)((c0 + col) * 32 + grp * R) * 16u;
+        for (int k = 0; k < R; ++k) {
+          const uint32_t ad = bse + (uint32_t)((k + col) % R) * 16u;
+          double2 o;
+          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(o.x), "=d"(o.y) : "r"(ad) : "memory");
+          sm += o.x;
+          sq += o.y;
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ad), "d"(0.0), "d"(0.0) : "memory");
+        }
+      }
+      for (int o = (nq / 2) * ncol; o >= ncol; o >>= 1) {
+        sm += __shfl_down_sync(kFull, sm, o);
+        sq += __shfl_down_sync(kFull, sq, o);
+      }
+      if (lane < ncol) {
+        d[G + c0 + lane] = sm;
+        d[G + CG + c0 + lane] = sq;
+      }
+    }
+    // counts: byte words -> 16-bit halves -> warp sums
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t e02 = __reduce_add_sync(kFull, lo[w] & 0x00ff00ffu);         // 8w+0 | 8w+4
+      const uint32_t e26 = __reduce_add_sync(kFull, (lo[w] >> 8) & 0x00ff00ffu);  // 8w+2 | 8w+6
+      const uint32_t o15 = __reduce_add_sync(kFull, hi[w] & 0x00ff00ffu);         // 8w+1 | 8w+5
+      const uint32_t o37 = __reduce_add_sync(kFull, (hi[w] >> 8) & 0x00ff00ffu);  // 8w+3 | 8w+7
+      const int s = lane - 8 * w;
+      if (s >= 0 && s < 8 && 8 * w + s < G) {
+        const uint32_t wd = (s & 1) ? ((s & 2) ? o37 : o15) : ((s & 2) ? e26 : e02);
+        d[8 * w + s] = (double)((s & 4) ? (wd >> 16) : (wd & 0xffffu));
+      }
+    }
+    p0 = warp_sum(p0);
+    p1 = warp_sum(p1);
+    p2 = warp_sum(p2);
+    if (lane == 0) {
+      d[G + 2 * CG] = p0;
+      d[G + 2 * CG + 1] = p1;
+      d[G + 2 * CG + 2] = p2;
+    }
+    __syncwarp();
   }
   unsigned long long c4[4] = {my_acc, my_cand, my_exact, my_amb};
 #pragma unroll
   for (int o = 16; o; o >>= 1)
 #pragma unroll
     for (int k = 0; k < 4; ++k) c4[k] += __shfl_xor_sync(~0u, c4[k], o);
-  if ((t & 31) == 0)
+  if (lane == 0)
 #pragma unroll
     for (int k = 0; k < 4; ++k) atomicAdd(&A.counters[k], c4[k]);
 }
 
-size_t sparse_smem_bytes(int G, int C) {
-  return sizeof(HitX) * kSparseThreads + (size_t)kSparseThreads * (16 * (size_t)G * C + 4 * (size_t)G);
-}
-
 template <int GMAX, int CH>
-static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, double *rows,
-                                     int sms) {
+static cudaError_t launch_3d_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, double *rows,
+                                 int sms) {
   const int G = A.na * A.ns;
   const size_t smem = sparse_smem_bytes(G, CH);
-  cudaError_t e = cudaFuncSetAttribute(k_gather_sparse<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_gather_3d<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_sparse<GMAX, CH>, kSparseThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_3d<GMAX, CH>, kG3Threads, smem);
   if (e != cudaSuccess) return e;
-  unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1) * 8u;
-  const unsigned need = (A.H + kSparseThreads - 1) / kSparseThreads;
+  unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1);
+  const unsigned need = (A.H + kG3Warps - 1) / kG3Warps;
   if (blocks > need) blocks = need;
   if (blocks == 0) blocks = 1;
-  k_gather_sparse<GMAX, CH><<<blocks, kSparseThreads, smem, s>>>(A, order, rows);
+  k_gather_3d<GMAX, CH><<<blocks, kG3Threads, smem, s>>>(A, order, rows);
   note_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, const uint32_t *order,
                                  double *rows, int sms) {
-  // the accumulators live in shared memory: one instance per C
-  if (C == 1) return launch_sparse_one<32, 1>(s, A, order, rows, sms);
-  return launch_sparse_one<32, 3>(s, A, order, rows, sms);
+  const int G = A.na * A.ns;
+  if (C == 1) {
+    if (G <= 8) return launch_3d_one<8, 1>(s, A, order, rows, sms);
+    if (G <= 16) return launch_3d_one<16, 1>(s, A, order, rows, sms);
+    return launch_3d_one<32, 1>(s, A, order, rows, sms);
+  }
+  if (G <= 8) return launch_3d_one<8, 3>(s, A, order, rows, sms);
+  if (G <= 16) return launch_3d_one<16, 3>(s, A, order, rows, sms);
+  return launch_3d_one<32, 3>(s, A, order, rows, sms);
 }
 
 // ---------------------------------------------------------------- explicit samples

@@ -88,21 +88,9 @@ struct EndArgs {
   double *snap_sum, *snap_sq;
 };
 
-// ---- tiled gather (gather_tile.cu)
-// candidates staged per item (64 B each: 88 KB of smem, so that two CTAs of
-// the tiled kernel with their queues and fragment partials fit one SM)
-constexpr int kChunk = 1376;
-
-struct ItemDesc {  // 112 B, one per (home cell, hit-point wave, candidate chunk)
-  uint32_t hp_lo, hp_n;      // range in the cell-sorted hit points
-  uint32_t first, nchunks;   // first item of this wave, chunks per wave
-  uint32_t ncand, chunk, npieces, pad;
-  uint32_t src[9], len[9];   // contiguous pieces of the sorted photon records
-  uint32_t pad2[2];
-};
-
+// ---- fine-kernel items (gather_fine.cu) and their pooling (sched.cu)
 struct TileArgs {
-  const ItemDesc *desc;
+  const void *desc;             // unused (fine items carry their own descriptors)
   const uint32_t *hp_order;     // cell-sorted hit point indices
   double *partials;             // [item][32][partial_size] per-item results
   const uint32_t *hp_map;       // per hit point: first item, chunks, wave slot
@@ -155,7 +143,6 @@ struct TileSched {
   uint32_t *hp_start;   // [nb + 1]
   uint32_t *items, *chunks, *item_base;  // [nb + 1]
   uint32_t *scan_tmp;
-  ItemDesc *desc;
   double *partials;
   uint32_t *hp_map;     // [3 H]
   uint32_t *nonempty;   // device counter: buckets holding hit points
@@ -165,16 +152,6 @@ struct TileSched {
 
 __host__ __device__ constexpr int partial_size(int gmax, int ch) { return gmax + 2 * ch * gmax + 3; }
 
-cudaError_t tile_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S,
-                               const GridHeader &g, int sms, uint32_t chunk, uint32_t *nb_out);
-cudaError_t tile_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb,
-                                int sms, uint32_t chunk);
-// lanes kernel (gather_lanes.cu): lanes = hit points of one home cell
-constexpr int kLaneChunk = 2048;  // candidates per item
-cudaError_t launch_gather_lanes(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
-                                int sms);
-cudaError_t launch_gather_tiles(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
-                                int sms);
 cudaError_t launch_tile_finalize(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
                                  int sms);
 size_t tile_partial_doubles(int G, int C);

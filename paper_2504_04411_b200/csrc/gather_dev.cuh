@@ -552,4 +552,129 @@ static __device__ __forceinline__ void finalize_hit(const GatherArgs &A, uint32_
   }
 }
 
+// ---------------------------------------------------------------- fine-cell geometry
+// slab layout: S = kFineS fine cells per reference cell (planar photon sets)
+static __device__ __forceinline__ bool slab_grid(const GridHeader &g) { return g.S == kFineS; }
+
+// (fine boxes, runs clipped to the ball's chord; gather_fine.cu, gather.cu)
+struct FBox {
+  int x0, x1, y0, y1, z0, z1;
+};
+
+// fine-cell range of one axis: the box [c - m, c + m] intersected with the
+// reference 27-neighbourhood of the home cell and the table.
+static __device__ __forceinline__ bool fine_axis(const GridHeader &g, double c, double m,
+                                                 long long o, long long n, int &lo, int &hi) {
+  const double hc = dm(c, g.inv);
+  if (!(fabs(hc) < 4.0e15)) return false;
+  const long long h = (long long)floor(hc);
+  const long long H = h >> g.shift;  // reference cell (floor division by S)
+  long long a = (H - 1) * (long long)g.S, b = (H + 2) * (long long)g.S - 1;
+  const long long a2 = (long long)floor(dm(ds(c, m), g.inv));
+  const long long b2 = (long long)floor(dm(da(c, m), g.inv));
+  a = (a > a2 ? a : a2) - o;
+  b = (b < b2 ? b : b2) - o;
+  if (a < 0) a = 0;
+  if (b > n - 1) b = n - 1;
+  lo = (int)a;
+  hi = (int)b;
+  return a <= b;
+}
+
+// Fine cells that can hold an accepted photon of the ball (c, r): the margin
+// covers the rounding of the fp64 ball test (|p - c| <= r (1 + 2^-50)) and of
+// c +- m.
+static __device__ __forceinline__ bool fine_box(const GridHeader &g, double cx, double cy, double cz,
+                                                double r, FBox &b) {
+  if (g.n == 0) return false;
+  const double cm = fmax(fabs(cx), fmax(fabs(cy), fabs(cz)));
+  const double m = da(da(r, dm(r, 1e-9)), dm(cm, 4e-16));
+  return fine_axis(g, cx, m, g.ix0, g.nx, b.x0, b.x1) && fine_axis(g, cy, m, g.iy0, g.ny, b.y0, b.y1) &&
+         fine_axis(g, cz, m, g.iz0, g.nz, b.z0, b.z1);
+}
+
+static __device__ __forceinline__ unsigned long long fid(const GridHeader &g, long long x, long long y,
+                                                         long long z) {
+  return (unsigned long long)((x * g.ny + y) * g.nz + z);
+}
+
+// Key range of piece p of a union box (slab: one fine row over the union's y
+// range and every z; otherwise one (x, y) column over the union's z range).
+static __device__ __forceinline__ void piece_keys(const GridHeader &g, const FBox &u, int p,
+                                                  unsigned long long &k0, unsigned long long &k1) {
+  if (slab_grid(g)) {
+    const long long x = u.x0 + p;
+    k0 = fid(g, x, u.y0, 0);
+    k1 = fid(g, x, u.y1, g.nz - 1);
+  } else {
+    const int nyu = u.y1 - u.y0 + 1;
+    const long long x = u.x0 + p / nyu, y = u.y0 + p % nyu;
+    k0 = fid(g, x, y, u.z0);
+    k1 = fid(g, x, y, u.z1);
+  }
+}
+static __device__ __forceinline__ int piece_count(const GridHeader &g, const FBox &u) {
+  return slab_grid(g) ? u.x1 - u.x0 + 1 : (u.x1 - u.x0 + 1) * (u.y1 - u.y0 + 1);
+}
+// runs of a box: one fine row per x in the slab layout (S = kFineS, every z
+// of the row), one (x, y) column otherwise (3D grids, S = 1 or 2)
+static __device__ __forceinline__ int run_count(const GridHeader &g, const FBox &b) {
+  return slab_grid(g) ? b.x1 - b.x0 + 1 : (b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1);
+}
+
+// Distance from c to the fine slab [X f, (X + 1) f) of one axis (f = 1 / inv),
+// shortened by `slack` (never negative).  Photons stored in fine cell X
+// satisfy floor(x * inv) = X in fp64; slack covers that rounding.
+static __device__ __forceinline__ double slab_gap(double c, long long X, double f, double slack) {
+  const double lo = (double)X * f, hi = (double)(X + 1) * f;  // f = 1 / inv (rounding << slack)
+  const double d = c < lo ? lo - c : (c > hi ? c - hi : 0.0);
+  return d > slack ? d - slack : 0.0;
+}
+
+// Run j of box b clipped to the chord of the ball (c, m) (m: fine_box's
+// margin radius).  A photon accepted by the reference ball test lies within
+// m of c in the plane of the two outer axes, so in column x (slab layout)
+// only the rows |y - c.y| <= sqrt(m^2 - gap_x^2) can hold it, and in an
+// (x, y) column (reference layout) only |z - c.z| <= sqrt(m^2 - gap_xy^2).
+// The bounds are widened by `slack` (>> fp64 rounding) and mapped through the
+// same monotone floor(v * inv) as the photons' own cells, so no accepted
+// photon is ever cut.  Returns false when the run is empty.
+static __device__ __forceinline__ bool run_keys_clipped(const GridHeader &g, const FBox &b, int j, double cx,
+                                                        double cy, double cz, double m,
+                                                        unsigned long long &k0, unsigned long long &k1) {
+  const double cm = fmax(fabs(cx), fmax(fabs(cy), fabs(cz)));
+  const double f = 1.0 / g.inv;
+  const double slack = 1e-6 * f + m * 1e-7 + cm * 1e-12;
+  const double m2 = m * m;
+  if (slab_grid(g)) {
+    const long long x = b.x0 + j;
+    const double gx = slab_gap(cx, x + g.ix0, f, slack);
+    const double h2 = m2 - gx * gx;
+    if (!(h2 >= 0.0)) return false;
+    const double hy = sqrt(h2) + slack;
+    long long y0 = (long long)floor(dm(ds(cy, hy), g.inv)) - g.iy0;
+    long long y1 = (long long)floor(dm(da(cy, hy), g.inv)) - g.iy0;
+    if (y0 < b.y0) y0 = b.y0;
+    if (y1 > b.y1) y1 = b.y1;
+    if (y0 > y1) return false;
+    k0 = fid(g, x, y0, 0);
+    k1 = fid(g, x, y1, g.nz - 1);
+    return true;
+  }
+  const int nyb = b.y1 - b.y0 + 1;
+  const long long x = b.x0 + j / nyb, y = b.y0 + j % nyb;
+  const double gx = slab_gap(cx, x + g.ix0, f, slack), gy = slab_gap(cy, y + g.iy0, f, slack);
+  const double h2 = m2 - gx * gx - gy * gy;
+  if (!(h2 >= 0.0)) return false;
+  const double hz = sqrt(h2) + slack;
+  long long z0 = (long long)floor(dm(ds(cz, hz), g.inv)) - g.iz0;
+  long long z1 = (long long)floor(dm(da(cz, hz), g.inv)) - g.iz0;
+  if (z0 < b.z0) z0 = b.z0;
+  if (z1 > b.z1) z1 = b.z1;
+  if (z0 > z1) return false;
+  k0 = fid(g, x, y, z0);
+  k1 = fid(g, x, y, z1);
+  return true;
+}
+
 }  // namespace fppm_b200

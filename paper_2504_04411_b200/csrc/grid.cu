@@ -85,8 +85,19 @@ __global__ void k_grid_header(const long long *__restrict__ bounds, const double
     const double fx = (double)(b[3] - b[0] + 1), fy = (double)(b[4] - b[1] + 1),
                  fz = (double)(b[5] - b[2] + 1);
     if (!(fz <= 3.0 * S_req && fx * fy * fz <= (double)max_cells)) {
-      for (int i = 0; i < 6; ++i) b[i] >>= shift;  // floor division by S
-      shift = 0;
+      // not a slab: 3D fine cells (S = 2) when the dense table fits, else
+      // reference cells.  b holds fine coordinates at S_req; floor division
+      // by a power of two is an arithmetic shift.
+      long long r[6];
+      for (int i = 0; i < 6; ++i) r[i] = b[i] >> shift;  // reference cells
+      const double rc = (double)(r[3] - r[0] + 1) * (double)(r[4] - r[1] + 1) * (double)(r[5] - r[2] + 1);
+      if (shift >= 1 && 8.0 * rc <= (double)max_cells) {
+        for (int i = 0; i < 6; ++i) b[i] >>= (shift - 1);
+        shift = 1;
+      } else {
+        for (int i = 0; i < 6; ++i) b[i] = r[i];
+        shift = 0;
+      }
     }
   } else {
     shift = 0;

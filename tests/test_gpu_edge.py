@@ -53,7 +53,7 @@ BASE = dict(n_annuli=2, n_sectors=6, alpha_f=0.05, initial_radius=0.03, r_min_ba
             samples_per_iteration=60000, threads=8)
 
 
-@pytest.mark.parametrize("kernel", ["fine", "tile", "warp", "lanes", "sparse"])
+@pytest.mark.parametrize("kernel", ["fine", "warp", "3d"])
 def test_general_3d_scene(port, kernel):
     hit, _ = scene3d(1)
     ctx, sess = make_pair(port, hit, BASE, kernel)

@@ -23,7 +23,7 @@ def test_generator_bitexact(port, wl_name):
         assert np.array_equal(got[k].view(np.uint32), want[k].view(np.uint32)), k
 
 
-@pytest.mark.parametrize("kernel", ["fine", "tile", "warp", "lanes", "sparse"])
+@pytest.mark.parametrize("kernel", ["fine", "warp", "3d"])
 @pytest.mark.parametrize("wl_name,raster,photons,iters", [
     ("c1", 64, 1 << 16, 4),
     ("c2", 64, 1 << 17, 4),
