@@ -191,6 +191,14 @@ static int effective_variant(const fppm_gpu_ctx *ctx, uint32_t S) {
   return v;
 }
 
+// 3D frames: a warp per hit point pays off once the 27-cell neighbourhood
+// holds tens of photons (C5: ~200); sparser frames (the C3 / C4 camera hit
+// points: ~3) take one thread per hit point
+static bool dense_3d(const GridHeader &g) {
+  const double ref_cells = (double)g.ncells / ((double)g.S * g.S * g.S);
+  return ref_cells > 0.0 && 27.0 * (double)g.n / ref_cells >= 48.0;
+}
+
 static cudaError_t ensure_scratch(fppm_gpu_ctx *ctx, size_t bytes) {
   if (bytes <= ctx->scratch_bytes) return cudaSuccess;
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
@@ -1307,7 +1315,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       const uint32_t *order = nullptr;
       FPPM_CUDA_OK(hp_cell_order(s, A, ctx->tile, *ctx->h_hdr, ctx->sms, &order));
       if ((rc = kernel_event(ctx, 0))) return rc;
-      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, order, rows, ctx->sms));
+      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, order, rows, ctx->sms, dense_3d(*ctx->h_hdr)));
       if ((rc = kernel_event(ctx, 1))) return rc;
       if (!delta) {
         GatherArgs B = A;
@@ -1787,15 +1795,15 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
   Q.o_flags = nullptr;
   Q.o_radiance = nullptr;
   Q.o_accepted = nullptr;
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned int), s));  // both kernels claim by counter
   if (gather_variant(ctx) == 1) {
-    FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned int), s));
     FPPM_CUDA_OK(launch_gather_test(s, Q, ctx->C, ctx->sms));
-  } else {  // thread per merge vertex, visited in home-cell order (neighbours share records in L1)
+  } else {  // 3D kernel, merge vertices visited in home-cell order (neighbours share records in L1/L2)
     TileSched qs;
     qs.sort = ctx->q_sort;
     const uint32_t *order = nullptr;
     FPPM_CUDA_OK(hp_cell_order(s, Q, qs, *ctx->h_hdr, ctx->sms, &order));
-    FPPM_CUDA_OK(launch_gather_sparse(s, Q, ctx->C, order, ctx->q_rows, ctx->sms));
+    FPPM_CUDA_OK(launch_gather_sparse(s, Q, ctx->C, order, ctx->q_rows, ctx->sms, dense_3d(*ctx->h_hdr)));
   }
   FPPM_CUDA_OK(launch_film_vcm(s, npix, nq, ctx->d_emit, ctx->d_gathered, ctx->o_flux, ctx->o_gather_r,
                                ctx->q_rows, stride, ctx->q_gathered, ctx->q_radius, ctx->d_splat,

@@ -233,6 +233,167 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
   }
 }
 
+// ---------------------------------------------------------------- sparse frames
+// Thread per hit point, for sparse 3D frames (C3 / C4 camera hit points on
+// the walls, a few candidates each): a warp's fixed cost per hit point
+// (runs, reductions) would exceed its candidates, so here each thread walks
+// the chord-clipped columns of its own fine box with the same pair code.
+// Neighbouring threads hold nearby hit points (cell order), so their photon
+// records share L1/L2 lines.
+constexpr int kSparseThreads = 128;
+#ifndef FPPM_SPARSE_U
+#define FPPM_SPARSE_U 4
+#endif
+constexpr int kSparseU = FPPM_SPARSE_U;
+
+template <int GMAX, int CH>
+#ifndef FPPM_SPARSE_MINB
+#define FPPM_SPARSE_MINB 4
+#endif
+__global__ void __launch_bounds__(kSparseThreads, FPPM_SPARSE_MINB) k_gather_sparse(const GatherArgs A, const uint32_t *__restrict__ order,
+                                                                   double *__restrict__ rows) {
+  // per thread: its Hit (exact path) and its sector accumulators, indexed
+  // [slot][thread] so a lane's dynamic sector index costs one LDS/STS
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int G = A.na * A.ns, CG = G * CH;
+  const int t = threadIdx.x;
+  HitX *s_hit = reinterpret_cast<HitX *>(s_raw);
+  double *s_sum = reinterpret_cast<double *>(s_hit + kSparseThreads);   // [CG][T]
+  double *s_sq = s_sum + (size_t)CG * kSparseThreads;                     // [CG][T]
+  uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_sq + (size_t)CG * kSparseThreads);  // [G][T]
+  HitX &Hs = s_hit[t];
+  const GridHeader grid = *A.grid;
+  uint32_t my_cand = 0, my_exact = 0, my_amb = 0, my_acc = 0;
+  for (uint32_t q = blockIdx.x * blockDim.x + t; q < A.H; q += gridDim.x * blockDim.x) {
+    const uint32_t h = order ? order[q] : q;
+    HitF F;
+    {
+      Hit H;
+      make_hit(A, h, H);
+      F = hitf(H, A.na, A.ns);
+      Hs.cx = H.cx; Hs.cy = H.cy; Hs.cz = H.cz;
+      Hs.nx = H.nx; Hs.ny = H.ny; Hs.nz = H.nz;
+      Hs.u = H.u; Hs.v = H.v;
+      Hs.r = H.r; Hs.r2 = H.r2;
+      Hs.K0 = H.K0; Hs.K1 = H.K1; Hs.K2 = H.K2;
+    }
+    const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
+    for (int k = 0; k < CG; ++k) {
+      s_sum[k * kSparseThreads + t] = 0.0;
+      s_sq[k * kSparseThreads + t] = 0.0;
+    }
+    for (int g = 0; g < G; ++g) s_cnt[g * kSparseThreads + t] = 0u;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    EyeVcm eye{0.0, 0.0, 0.0, 0.0};
+    if (A.vcm) {
+      const double3 wo = A.wo[h], al = A.alb[h];
+      eye.cos_o = edot(wo.x, wo.y, wo.z, Hs.nx, Hs.ny, Hs.nz);
+      const double m1 = al.y < al.z ? al.z : al.y;
+      const double amax = al.x < m1 ? m1 : al.x;
+      eye.cont = amax < 1.0 ? amax : 1.0;
+      const double2 em = A.eye_mis[h];
+      eye.d_vcm = em.x;
+      eye.d_vm = em.y;
+    }
+    FBox fb = {0, -1, 0, -1, 0, -1};
+    if (gathered && fine_box(grid, Hs.cx, Hs.cy, Hs.cz, Hs.r, fb)) {
+      // the box's columns (27-neighbourhood, chord-clipped: gather_dev.cuh)
+      const int ncol = run_count(grid, fb);
+      const double cm = fmax(fabs(Hs.cx), fmax(fabs(Hs.cy), fabs(Hs.cz)));
+      const double mrad = da(da(Hs.r, dm(Hs.r, 1e-9)), dm(cm, 4e-16));
+#pragma unroll 1
+      for (int col = 0; col < ncol; ++col) {
+        unsigned long long k0, k1;
+        if (!run_keys_clipped(grid, fb, col, Hs.cx, Hs.cy, Hs.cz, mrad, k0, k1)) continue;
+        const uint32_t beg = __ldg(&A.cell_start[k0]), end = __ldg(&A.cell_start[k1 + 1]);
+        my_cand += end - beg;
+        // kSparseU candidates per step: their record loads are issued
+        // together (the loop is latency bound, one chain per thread)
+        for (uint32_t i0 = beg; i0 < end; i0 += kSparseU) {
+          float4 ra[kSparseU], rb[kSparseU], rc[kSparseU], rd[kSparseU];
+          bool live[kSparseU];
+#pragma unroll
+          for (int u = 0; u < kSparseU; ++u) {
+            live[u] = i0 + u < end;
+            ra[u] = live[u] ? __ldg(&A.rec0[i0 + u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < kSparseU; ++u) live[u] = live[u] && test_pair(F, ra[u], A.max_depth);
+#pragma unroll
+          for (int u = 0; u < kSparseU; ++u)
+            if (live[u]) {
+              rb[u] = __ldg(&A.rec1[i0 + u]);
+              rc[u] = __ldg(&A.rec2[i0 + u]);
+              rd[u] = __ldg(&A.rec3[i0 + u]);
+            }
+#pragma unroll
+          for (int u = 0; u < kSparseU; ++u) {
+            if (!live[u]) continue;
+            int sector;
+            double sv[CH], sw[CH], f0, f1, f2;
+            if (!pair_tail<CH, HitX>(A, F, Hs, i0 + u, eye, ra[u], rb[u], rc[u], rd[u], sector, sv, sw, f0, f1, f2,
+                               my_exact, my_amb))
+              continue;
+            ++my_acc;
+            p0 = da(p0, f0); p1 = da(p1, f1); p2 = da(p2, f2);
+            s_cnt[sector * kSparseThreads + t] += 1u;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+              double &x = s_sum[(c * G + sector) * kSparseThreads + t];
+              double &y = s_sq[(c * G + sector) * kSparseThreads + t];
+              x = da(x, sv[c]);
+              y = da(y, sw[c]);
+            }
+          }
+        }
+      }
+    }
+    // option-B row layout [count G | sum C*G | sum_sq C*G | power 3]; the
+    // end of iteration runs in k_apply_deltas (thread per hit point)
+    double *d = rows + (size_t)h * (size_t)(G + 2 * CG + 3);
+    for (int g = 0; g < G; ++g) d[g] = (double)s_cnt[g * kSparseThreads + t];
+    for (int k = 0; k < CG; ++k) {
+      d[G + k] = s_sum[k * kSparseThreads + t];
+      d[G + CG + k] = s_sq[k * kSparseThreads + t];
+    }
+    d[G + 2 * CG] = p0;
+    d[G + 2 * CG + 1] = p1;
+    d[G + 2 * CG + 2] = p2;
+  }
+  unsigned long long c4[4] = {my_acc, my_cand, my_exact, my_amb};
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c4[k] += __shfl_xor_sync(~0u, c4[k], o);
+  if ((t & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) atomicAdd(&A.counters[k], c4[k]);
+}
+
+size_t thread_smem_bytes(int G, int C) {
+  return sizeof(HitX) * kSparseThreads + (size_t)kSparseThreads * (16 * (size_t)G * C + 4 * (size_t)G);
+}
+
+template <int GMAX, int CH>
+static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, double *rows,
+                                     int sms) {
+  const int G = A.na * A.ns;
+  const size_t smem = thread_smem_bytes(G, CH);
+  cudaError_t e = cudaFuncSetAttribute(k_gather_sparse<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_sparse<GMAX, CH>, kSparseThreads, smem);
+  if (e != cudaSuccess) return e;
+  unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1) * 8u;
+  const unsigned need = (A.H + kSparseThreads - 1) / kSparseThreads;
+  if (blocks > need) blocks = need;
+  if (blocks == 0) blocks = 1;
+  k_gather_sparse<GMAX, CH><<<blocks, kSparseThreads, smem, s>>>(A, order, rows);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- 3D gather
 // Frames whose photons fill a volume (C3 / C4 camera hit points on the walls,
 // the C5 clusters): a warp owns one hit point at a time (hit points visited
@@ -255,12 +416,14 @@ size_t sparse_smem_bytes(int G, int C) {
   return (size_t)kG3Warps * (sizeof(Hit) + (size_t)(G * C + 1) * 32 * 16);
 }
 
+// 4-bit counts (sector 8w + k at bits 4k of nib[w]) spilled every 15 steps
+// into 16-bit fields: q[w][k & 3] holds sector 8w + k in half k >> 2
 template <int NW>
-static __device__ __forceinline__ void g3_spill(uint32_t (&nib)[NW], uint32_t (&lo)[NW], uint32_t (&hi)[NW]) {
+static __device__ __forceinline__ void g3_spill(uint32_t (&nib)[NW], uint32_t (&q)[NW][4]) {
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
-    lo[w] += nib[w] & 0x0F0F0F0Fu;         // sectors 8w + 0, 2, 4, 6 in bytes
-    hi[w] += (nib[w] >> 4) & 0x0F0F0F0Fu;  // sectors 8w + 1, 3, 5, 7
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[w][k] += (nib[w] >> (4 * k)) & 0x000F000Fu;
     nib[w] = 0u;
   }
 }
@@ -326,9 +489,13 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
     const uint32_t off = rs - (incl - rl);  // sorted index - virtual index within run `lane`
     const uint32_t total = __shfl_sync(kFull, incl, 31);
     if (lane == 0) my_cand += total;
-    uint32_t nib[NW], lo[NW], hi[NW];
+    uint32_t nib[NW], cq[NW][4];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) nib[w] = lo[w] = hi[w] = 0u;
+    for (int w = 0; w < NW; ++w) {
+      nib[w] = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cq[w][k] = 0u;
+    }
     double p0 = 0.0, p1 = 0.0, p2 = 0.0;
     uint32_t spill = 15;
     for (uint32_t base = 0; base < total; base += 32) {
@@ -370,7 +537,7 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
         f0 = f1 = f2 = 0.0;
       }
       if (--spill == 0) {
-        g3_spill<NW>(nib, lo, hi);
+        g3_spill<NW>(nib, cq);
         spill = 15;
       }
 #pragma unroll
@@ -393,7 +560,7 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
       p1 = da(p1, f1);
       p2 = da(p2, f2);
     }
-    g3_spill<NW>(nib, lo, hi);
+    g3_spill<NW>(nib, cq);
     // ---- the hit point's option-B row [count G | sum CG | sum_sq CG | power 3]
     double *d = rows + (size_t)h * (size_t)(G + 2 * CG + 3);
     // slots: lane (col, grp) sums R rows of column col in a fixed order
@@ -424,19 +591,18 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
         d[G + CG + c0 + lane] = sq;
       }
     }
-    // counts: byte words -> 16-bit halves -> warp sums
+    // counts: 16-bit fields -> warp sums (halves reduced separately)
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const uint32_t e02 = __reduce_add_sync(kFull, lo[w] & 0x00ff00ffu);         // 8w+0 | 8w+4
-      const uint32_t e26 = __reduce_add_sync(kFull, (lo[w] >> 8) & 0x00ff00ffu);  // 8w+2 | 8w+6
-      const uint32_t o15 = __reduce_add_sync(kFull, hi[w] & 0x00ff00ffu);         // 8w+1 | 8w+5
-      const uint32_t o37 = __reduce_add_sync(kFull, (hi[w] >> 8) & 0x00ff00ffu);  // 8w+3 | 8w+7
-      const int s = lane - 8 * w;
-      if (s >= 0 && s < 8 && 8 * w + s < G) {
-        const uint32_t wd = (s & 1) ? ((s & 2) ? o37 : o15) : ((s & 2) ? e26 : e02);
-        d[8 * w + s] = (double)((s & 4) ? (wd >> 16) : (wd & 0xffffu));
+    for (int w = 0; w < NW; ++w)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t c_lo = __reduce_add_sync(kFull, cq[w][k] & 0xffffu);  // sector 8w + k
+        const uint32_t c_hi = __reduce_add_sync(kFull, cq[w][k] >> 16);      // sector 8w + k + 4
+        if (lane == 0) {
+          if (8 * w + k < G) d[8 * w + k] = (double)c_lo;
+          if (8 * w + k + 4 < G) d[8 * w + k + 4] = (double)c_hi;
+        }
       }
-    }
     p0 = warp_sum(p0);
     p1 = warp_sum(p1);
     p2 = warp_sum(p2);
@@ -478,8 +644,10 @@ static cudaError_t launch_3d_one(cudaStream_t s, const GatherArgs &A, const uint
 }
 
 cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, const uint32_t *order,
-                                 double *rows, int sms) {
+                                 double *rows, int sms, bool warp_per_hp) {
   const int G = A.na * A.ns;
+  if (!warp_per_hp)  // few candidates per hit point: one thread each
+    return C == 1 ? launch_sparse_one<32, 1>(s, A, order, rows, sms) : launch_sparse_one<32, 3>(s, A, order, rows, sms);
   if (C == 1) {
     if (G <= 8) return launch_3d_one<8, 1>(s, A, order, rows, sms);
     if (G <= 16) return launch_3d_one<16, 1>(s, A, order, rows, sms);
