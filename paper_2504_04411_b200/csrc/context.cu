@@ -111,6 +111,9 @@ struct fppm_gpu_ctx {
   // lean record layout: every gathered hit point planar and gray (device
   // flag from k_lean_check), config C = 1, n_a <= 2, n_s = 4, fine kernel
   uint32_t *d_lean_ok = nullptr;
+  // 3D kernel staging (k_prep_3d): Hot3 and full Hit per hit point
+  void *hot3 = nullptr, *hot3_hits = nullptr;
+  uint32_t hot3_cap = 0;
   // staging set the current grid's input photons live in (the lean layout's
   // exact path reads them during the gather: released after it), -1 none
   int grid_set = -1;
@@ -197,6 +200,19 @@ static int effective_variant(const fppm_gpu_ctx *ctx, uint32_t S) {
 static bool dense_3d(const GridHeader &g) {
   const double ref_cells = (double)g.ncells / ((double)g.S * g.S * g.S);
   return ref_cells > 0.0 && 27.0 * (double)g.n / ref_cells >= 48.0;
+}
+
+// per-hit-point staging of the 3D kernel (Hot3 + full Hit for the exact path)
+static int ensure_hot3(fppm_gpu_ctx *ctx, uint32_t n) {
+  if (n <= ctx->hot3_cap) return FPPM_OK;
+  if (ctx->hot3) cudaFree(ctx->hot3);
+  if (ctx->hot3_hits) cudaFree(ctx->hot3_hits);
+  ctx->hot3 = ctx->hot3_hits = nullptr;
+  ctx->hot3_cap = 0;
+  FPPM_CUDA_OK(cudaMalloc(&ctx->hot3, hot3_bytes() * std::max<uint32_t>(n, 1)));
+  FPPM_CUDA_OK(cudaMalloc(&ctx->hot3_hits, fine_hit_bytes() * std::max<uint32_t>(n, 1)));
+  ctx->hot3_cap = n;
+  return FPPM_OK;
 }
 
 static cudaError_t ensure_scratch(fppm_gpu_ctx *ctx, size_t bytes) {
@@ -545,6 +561,8 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
       if (p) cudaFree(p);
   }
   if (ctx->d_rows) cudaFree(ctx->d_rows);
+  if (ctx->hot3) cudaFree(ctx->hot3);
+  if (ctx->hot3_hits) cudaFree(ctx->hot3_hits);
   for (void *p : ctx->c5_mem)
     if (p) cudaFree(p);
   if (ctx->d_film) cudaFree(ctx->d_film);
@@ -1315,7 +1333,10 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       const uint32_t *order = nullptr;
       FPPM_CUDA_OK(hp_cell_order(s, A, ctx->tile, *ctx->h_hdr, ctx->sms, &order));
       if ((rc = kernel_event(ctx, 0))) return rc;
-      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, order, rows, ctx->sms, dense_3d(*ctx->h_hdr)));
+      void *hot3 = nullptr;
+      if (dense_3d(*ctx->h_hdr) && (rc = ensure_hot3(ctx, ctx->H))) return rc;
+      if (dense_3d(*ctx->h_hdr)) hot3 = ctx->hot3;
+      FPPM_CUDA_OK(launch_gather_sparse(s, A, ctx->C, order, rows, ctx->sms, hot3, ctx->hot3_hits));
       if ((rc = kernel_event(ctx, 1))) return rc;
       if (!delta) {
         GatherArgs B = A;
@@ -1803,7 +1824,13 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
     qs.sort = ctx->q_sort;
     const uint32_t *order = nullptr;
     FPPM_CUDA_OK(hp_cell_order(s, Q, qs, *ctx->h_hdr, ctx->sms, &order));
-    FPPM_CUDA_OK(launch_gather_sparse(s, Q, ctx->C, order, ctx->q_rows, ctx->sms, dense_3d(*ctx->h_hdr)));
+    void *hot3 = nullptr, *qhits = nullptr;
+    if (dense_3d(*ctx->h_hdr) && (rc = ensure_hot3(ctx, (uint32_t)nqt))) return rc;
+    if (dense_3d(*ctx->h_hdr)) {
+      hot3 = ctx->hot3;
+      qhits = ctx->hot3_hits;
+    }
+    FPPM_CUDA_OK(launch_gather_sparse(s, Q, ctx->C, order, ctx->q_rows, ctx->sms, hot3, qhits));
   }
   FPPM_CUDA_OK(launch_film_vcm(s, npix, nq, ctx->d_emit, ctx->d_gathered, ctx->o_flux, ctx->o_gather_r,
                                ctx->q_rows, stride, ctx->q_gathered, ctx->q_radius, ctx->d_splat,

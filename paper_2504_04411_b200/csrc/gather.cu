@@ -395,26 +395,65 @@ static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, const 
 }
 
 // ---------------------------------------------------------------- 3D gather
-// Frames whose photons fill a volume (C3 / C4 camera hit points on the walls,
-// the C5 clusters): a warp owns one hit point at a time (hit points visited
-// in cell order, so consecutive warps share cells in L1/L2).  Its candidate
-// runs are the (x, y) columns of its fine box -- S = 2 fine cells when the
-// dense table fits, else reference cells -- clipped to the 27-neighbourhood
-// and to the ball's chord (gather_dev.cuh run_keys_clipped); the lanes walk
-// the concatenated runs one candidate each, reading the sorted records
-// straight from L2 (coalesced within a run).  Three stages per candidate:
-// ball + depth + disk on rec0 (test_pair), the normal guard on rec1 (certain
-// rejections only), then the full banded decision and value (pair_tail,
-// exact fp64 path inside).  Accepted values go to the lane's shared-memory
-// slot [(c * G + sector)][lane] {sum, sum_sq}; counts in 4-bit fields; at
-// the end the slots are reduced in a fixed order into the hit point's
-// option-B row (k_apply_deltas pools it and runs the end of iteration).
-constexpr int kG3Warps = 4;
-constexpr int kG3Threads = kG3Warps * kWarp;
+// Dense 3D frames (the C5 clusters: ~100 candidates per hit point): a warp
+// owns one hit point at a time (visited in cell order, so consecutive warps
+// share cells in L1/L2).  k_prep_3d first stages every hit point's state
+// thread-parallel (make_hit, the fp32 predicate constants, the VCM+ eye
+// terms); the warp then computes its runs lane-parallel -- the (x, y)
+// columns of its fine box (S = 2 fine cells where the dense table fits, else
+// reference cells), clipped to the 27-neighbourhood and to the ball's chord
+// (gather_dev.cuh) -- and walks the concatenated runs one candidate per lane,
+// reading the sorted records straight from L2 (coalesced within a run) in
+// three stages: ball + depth + disk on rec0 (test_pair), the normal guard on
+// rec1 (certain rejections only), then the full banded decision and value
+// (pair_tail, exact fp64 path inside).  Accepted values go to the lane's
+// shared-memory slot [(c * G + sector)][lane] {sum, sum_sq} (a spare row for
+// the others), counts in 4-bit fields; the slots are reduced in a fixed order
+// into the hit point's option-B row (k_apply_deltas pools it and runs the end
+// of iteration).
+struct alignas(16) Hot3 {
+  double cx, cy, cz, r;
+  EyeVcm eye;
+  HitF F;
+  uint32_t h, gathered;
+};
 
-size_t sparse_smem_bytes(int G, int C) {
-  return (size_t)kG3Warps * (sizeof(Hit) + (size_t)(G * C + 1) * 32 * 16);
+__global__ void __launch_bounds__(128) k_prep_3d(const GatherArgs A, const uint32_t *__restrict__ order,
+                                               Hot3 *__restrict__ hot, Hit *__restrict__ hits) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < A.H; q += gridDim.x * blockDim.x) {
+    const uint32_t h = order ? order[q] : q;
+    Hit H;
+    make_hit(A, h, H);
+    hits[q] = H;
+    Hot3 o;
+    o.cx = H.cx; o.cy = H.cy; o.cz = H.cz; o.r = H.r;
+    o.F = hitf(H, A.na, A.ns);
+    o.h = h;
+    o.gathered = (A.gathered == nullptr || A.gathered[h] != 0) ? 1u : 0u;
+    o.eye = EyeVcm{0.0, 0.0, 0.0, 0.0};
+    if (A.vcm) {  // bsdf.cpp:42-51 continuation, eye MIS partials
+      const double3 wo = A.wo[h], al = A.alb[h];
+      o.eye.cos_o = edot(wo.x, wo.y, wo.z, H.nx, H.ny, H.nz);
+      const double m1 = al.y < al.z ? al.z : al.y;
+      const double amax = al.x < m1 ? m1 : al.x;
+      o.eye.cont = amax < 1.0 ? amax : 1.0;
+      const double2 em = A.eye_mis[h];
+      o.eye.d_vcm = em.x;
+      o.eye.d_vm = em.y;
+    }
+    hot[q] = o;
+  }
 }
+
+// slot columns padded to a power of two (compile-time reduction shape)
+template <int GMAX, int CH>
+struct G3Lay {
+  static constexpr int NC = GMAX * CH;
+  static constexpr int NCP = NC <= 8 ? 8 : NC <= 16 ? 16 : NC <= 32 ? 32 : NC <= 64 ? 64 : 128;
+  static constexpr int W = NCP <= 32 ? 4 : NCP <= 64 ? 2 : 1;  // warps per CTA (shared memory)
+  static constexpr int NW = (GMAX + 7) / 8;                      // 4-bit count words
+  static constexpr size_t kSmem = (size_t)W * (NCP + 1) * 32 * 16;
+};
 
 // 4-bit counts (sector 8w + k at bits 4k of nib[w]) spilled every 15 steps
 // into 16-bit fields: q[w][k & 3] holds sector 8w + k in half k >> 2
@@ -429,15 +468,16 @@ static __device__ __forceinline__ void g3_spill(uint32_t (&nib)[NW], uint32_t (&
 }
 
 template <int GMAX, int CH>
-__global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, const uint32_t *__restrict__ order,
-                                                        double *__restrict__ rows) {
-  constexpr int NW = (GMAX + 7) / 8;  // count words (8 sectors of 4 bits each)
+__global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
+    k_gather_3d(const GatherArgs A, const Hot3 *__restrict__ hot, const Hit *__restrict__ hits,
+                double *__restrict__ rows) {
+  using L = G3Lay<GMAX, CH>;
+  constexpr int NW = L::NW, NCP = L::NCP;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = A.na * A.ns, CG = G * CH;
-  Hit &Hs = reinterpret_cast<Hit *>(s_raw)[warp];
-  double *slot_base = reinterpret_cast<double *>(s_raw + kG3Warps * sizeof(Hit)) + (size_t)warp * (CG + 1) * 64;
-  for (int i = lane; i < (CG + 1) * 64; i += 32) slot_base[i] = 0.0;
+  double *slot_base = reinterpret_cast<double *>(s_raw) + (size_t)warp * (NCP + 1) * 64;
+  for (int i = lane; i < (NCP + 1) * 64; i += 32) slot_base[i] = 0.0;
   const uint32_t slots = smem_u32(slot_base);
   const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
   const GridHeader g = *A.grid;
@@ -447,34 +487,22 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
     if (lane == 0) q = atomicAdd(A.work, 1u);
     q = __shfl_sync(kFull, q, 0);
     if (q >= A.H) break;
-    const uint32_t h = order ? order[q] : q;
-    __syncwarp();
-    if (lane == 0) make_hit(A, h, Hs);
-    __syncwarp();
-    const HitF F = hitf(Hs, A.na, A.ns);
-    const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
-    EyeVcm eye{0.0, 0.0, 0.0, 0.0};
-    if (A.vcm) {
-      const double3 wo = A.wo[h], al = A.alb[h];
-      eye.cos_o = edot(wo.x, wo.y, wo.z, Hs.nx, Hs.ny, Hs.nz);
-      const double m1 = al.y < al.z ? al.z : al.y;
-      const double amax = al.x < m1 ? m1 : al.x;
-      eye.cont = amax < 1.0 ? amax : 1.0;
-      const double2 em = A.eye_mis[h];
-      eye.d_vcm = em.x;
-      eye.d_vm = em.y;
-    }
+    const Hot3 &Hq = hot[q];
+    const Hit &Hs = hits[q];  // full state: exact path only
+    const HitF F = Hq.F;
+    const EyeVcm eye = Hq.eye;
+    const uint32_t h = Hq.h;
     // runs: the box's (x, y) columns clipped to the chord (lane j = run j)
     uint32_t rs = 0, rl = 0;
-    int nruns = 0;
     {
+      const double cx = Hq.cx, cy = Hq.cy, cz = Hq.cz, r = Hq.r;
       FBox b = {0, -1, 0, -1, 0, -1};
-      if (gathered && fine_box(g, Hs.cx, Hs.cy, Hs.cz, Hs.r, b)) {
-        nruns = run_count(g, b);
-        const double cm = fmax(fabs(Hs.cx), fmax(fabs(Hs.cy), fabs(Hs.cz)));
-        const double m = da(da(Hs.r, dm(Hs.r, 1e-9)), dm(cm, 4e-16));
+      if (Hq.gathered && fine_box(g, cx, cy, cz, r, b)) {
+        const int nruns = run_count(g, b);
+        const double cm = fmax(fabs(cx), fmax(fabs(cy), fabs(cz)));
+        const double m = da(da(r, dm(r, 1e-9)), dm(cm, 4e-16));
         unsigned long long k0, k1;
-        if (lane < nruns && run_keys_clipped(g, b, lane, Hs.cx, Hs.cy, Hs.cz, m, k0, k1)) {
+        if (lane < nruns && run_keys_clipped(g, b, lane, cx, cy, cz, m, k0, k1)) {
           rs = __ldg(&A.cell_start[k0]);
           rl = __ldg(&A.cell_start[k1 + 1]) - rs;
         }
@@ -503,10 +531,8 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
       // run of v: binary search over the lanes' inclusive ends
       int j = 0;
 #pragma unroll
-      for (int st = 16; st > 0; st >>= 1) {
-        const uint32_t e = __shfl_sync(kFull, incl, (j + st - 1) & 31);
-        if (j + st - 1 < 31 && e <= v) j += st;
-      }
+      for (int st = 16; st > 0; st >>= 1)
+        if (__shfl_sync(kFull, incl, j + st - 1) <= v) j += st;
       if (__shfl_sync(kFull, incl, j & 31) <= v) ++j;
       const uint32_t i = v + __shfl_sync(kFull, off, j & 31);
       bool live = v < total;
@@ -542,7 +568,7 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
       }
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
-        const uint32_t row = live ? (uint32_t)(c * G + sector) : (uint32_t)CG;  // spare row
+        const uint32_t row = live ? (uint32_t)(c * G + sector) : (uint32_t)NCP;  // spare row
         const uint32_t ad = slot_lane + row * 512u;
         double2 o;
         asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(o.x), "=d"(o.y) : "r"(ad) : "memory");
@@ -563,30 +589,29 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
     g3_spill<NW>(nib, cq);
     // ---- the hit point's option-B row [count G | sum CG | sum_sq CG | power 3]
     double *d = rows + (size_t)h * (size_t)(G + 2 * CG + 3);
-    // slots: lane (col, grp) sums R rows of column col in a fixed order
-    for (int c0 = 0; c0 < CG; c0 += 32) {
-      const int ncol = min(32, CG - c0);
-      int nq = 1;
-      while (nq * 2 * ncol <= 32) nq *= 2;
-      const int R = 32 / nq;
+    // slots: lane (col, grp) sums R rows of column col in a fixed, rotated order
+#pragma unroll
+    for (int c0 = 0; c0 < NCP; c0 += 32) {
+      constexpr int ncol = NCP < 32 ? NCP : 32;
+      constexpr int nq = 32 / ncol, R = 32 / nq;
       const int col = lane % ncol, grp = lane / ncol;
       double sm = 0.0, sq = 0.0;
-      if (grp < nq) {
-        const uint32_t bse = slots + (uint32_t)((c0 + col) * 32 + grp * R) * 16u;
-        for (int k = 0; k < R; ++k) {
-          const uint32_t ad = bse + (uint32_t)((k + col) % R) * 16u;
-          double2 o;
-          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(o.x), "=d"(o.y) : "r"(ad) : "memory");
-          sm += o.x;
-          sq += o.y;
-          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ad), "d"(0.0), "d"(0.0) : "memory");
-        }
+      const uint32_t bse = slots + (uint32_t)((c0 + col) * 32 + grp * R) * 16u;
+#pragma unroll 4
+      for (int k = 0; k < R; ++k) {
+        const uint32_t ad = bse + (uint32_t)((k + col) % R) * 16u;
+        double2 o;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(o.x), "=d"(o.y) : "r"(ad) : "memory");
+        sm += o.x;
+        sq += o.y;
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ad), "d"(0.0), "d"(0.0) : "memory");
       }
-      for (int o = (nq / 2) * ncol; o >= ncol; o >>= 1) {
+#pragma unroll
+      for (int o = (nq / 2) * ncol; o >= ncol && o > 0; o >>= 1) {
         sm += __shfl_down_sync(kFull, sm, o);
         sq += __shfl_down_sync(kFull, sq, o);
       }
-      if (lane < ncol) {
+      if (lane < ncol && c0 + lane < CG) {
         d[G + c0 + lane] = sm;
         d[G + CG + c0 + lane] = sq;
       }
@@ -603,13 +628,20 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
           if (8 * w + k + 4 < G) d[8 * w + k + 4] = (double)c_hi;
         }
       }
-    p0 = warp_sum(p0);
-    p1 = warp_sum(p1);
-    p2 = warp_sum(p2);
-    if (lane == 0) {
-      d[G + 2 * CG] = p0;
-      d[G + 2 * CG + 1] = p1;
-      d[G + 2 * CG + 2] = p2;
+    // flux: transposed butterfly; lane 0 / 8 / 16 end with p0 / p1 / p2
+    {
+      const bool hi16 = (lane & 16) != 0, hi8 = (lane & 8) != 0;
+      const double s0 = hi16 ? p0 : p2, k0 = hi16 ? p2 : p0;
+      const double s1 = hi16 ? p1 : 0.0, k1 = hi16 ? 0.0 : p1;
+      const double x = k0 + __shfl_xor_sync(kFull, s0, 16);
+      const double y = k1 + __shfl_xor_sync(kFull, s1, 16);
+      double c = (hi8 ? y : x) + __shfl_xor_sync(kFull, hi8 ? x : y, 8);
+      c += __shfl_xor_sync(kFull, c, 4);
+      c += __shfl_xor_sync(kFull, c, 2);
+      c += __shfl_xor_sync(kFull, c, 1);
+      if (lane == 0) d[G + 2 * CG] = c;
+      if (lane == 8) d[G + 2 * CG + 1] = c;
+      if (lane == 16) d[G + 2 * CG + 2] = c;
     }
     __syncwarp();
   }
@@ -623,39 +655,46 @@ __global__ void __launch_bounds__(kG3Threads) k_gather_3d(const GatherArgs A, co
     for (int k = 0; k < 4; ++k) atomicAdd(&A.counters[k], c4[k]);
 }
 
+size_t hot3_bytes() { return sizeof(Hot3); }
+
 template <int GMAX, int CH>
-static cudaError_t launch_3d_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, double *rows,
-                                 int sms) {
-  const int G = A.na * A.ns;
-  const size_t smem = sparse_smem_bytes(G, CH);
+static cudaError_t launch_3d_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, void *hot,
+                                 void *hits, double *rows, int sms) {
+  using L = G3Lay<GMAX, CH>;
+  if (A.H == 0) return cudaSuccess;
+  k_prep_3d<<<(unsigned)std::min<unsigned long long>((A.H + 127) / 128, (unsigned long long)sms * 16), 128, 0, s>>>(
+      A, order, static_cast<Hot3 *>(hot), static_cast<Hit *>(hits));
+  note_launches(1);
+  const size_t smem = L::kSmem;
   cudaError_t e = cudaFuncSetAttribute(k_gather_3d<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_3d<GMAX, CH>, kG3Threads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_3d<GMAX, CH>, L::W * 32, smem);
   if (e != cudaSuccess) return e;
   unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1);
-  const unsigned need = (A.H + kG3Warps - 1) / kG3Warps;
+  const unsigned need = (A.H + L::W - 1) / L::W;
   if (blocks > need) blocks = need;
   if (blocks == 0) blocks = 1;
-  k_gather_3d<GMAX, CH><<<blocks, kG3Threads, smem, s>>>(A, order, rows);
+  k_gather_3d<GMAX, CH><<<blocks, L::W * 32, smem, s>>>(A, static_cast<const Hot3 *>(hot),
+                                                        static_cast<const Hit *>(hits), rows);
   note_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, const uint32_t *order,
-                                 double *rows, int sms, bool warp_per_hp) {
+                                 double *rows, int sms, void *hot3, void *hits) {
   const int G = A.na * A.ns;
-  if (!warp_per_hp)  // few candidates per hit point: one thread each
+  if (hot3 == nullptr)  // few candidates per hit point: one thread each
     return C == 1 ? launch_sparse_one<32, 1>(s, A, order, rows, sms) : launch_sparse_one<32, 3>(s, A, order, rows, sms);
   if (C == 1) {
-    if (G <= 8) return launch_3d_one<8, 1>(s, A, order, rows, sms);
-    if (G <= 16) return launch_3d_one<16, 1>(s, A, order, rows, sms);
-    return launch_3d_one<32, 1>(s, A, order, rows, sms);
+    if (G <= 8) return launch_3d_one<8, 1>(s, A, order, hot3, hits, rows, sms);
+    if (G <= 16) return launch_3d_one<16, 1>(s, A, order, hot3, hits, rows, sms);
+    return launch_3d_one<32, 1>(s, A, order, hot3, hits, rows, sms);
   }
-  if (G <= 8) return launch_3d_one<8, 3>(s, A, order, rows, sms);
-  if (G <= 16) return launch_3d_one<16, 3>(s, A, order, rows, sms);
-  return launch_3d_one<32, 3>(s, A, order, rows, sms);
+  if (G <= 8) return launch_3d_one<8, 3>(s, A, order, hot3, hits, rows, sms);
+  if (G <= 16) return launch_3d_one<16, 3>(s, A, order, hot3, hits, rows, sms);
+  return launch_3d_one<32, 3>(s, A, order, hot3, hits, rows, sms);
 }
 
 // ---------------------------------------------------------------- explicit samples

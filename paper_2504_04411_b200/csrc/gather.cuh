@@ -180,10 +180,13 @@ cudaError_t launch_end_iteration(cudaStream_t s, const EndArgs &A);
 // thread-per-hit-point gather for sparse 3D frames (gather.cu)
 // writes option-B rows [H][G + 2 G C + 3]; the caller pools them
 // (launch_apply_deltas) unless they are the cross-rank partial sums
-// warp_per_hp: k_gather_3d (dense 3D frames, tens of candidates per hit
-// point and more); else k_gather_sparse, one thread per hit point
+// hot3 != NULL: k_prep_3d + k_gather_3d, a warp per hit point (dense 3D
+// frames, tens of candidates per hit point and more; hot3 holds
+// hot3_bytes() and hits fine_hit_bytes() per hit point); else
+// k_gather_sparse, one thread per hit point
 cudaError_t launch_gather_sparse(cudaStream_t s, const GatherArgs &A, int C, const uint32_t *order,
-                                 double *rows, int sms, bool warp_per_hp);
+                                 double *rows, int sms, void *hot3, void *hits);
+size_t hot3_bytes();
 cudaError_t hp_cell_order(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g, int sms,
                           const uint32_t **order);
 size_t sparse_smem_bytes(int G, int C);
