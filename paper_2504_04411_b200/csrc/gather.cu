@@ -412,24 +412,24 @@ static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, const 
 // into the hit point's option-B row (k_apply_deltas pools it and runs the end
 // of iteration).
 struct alignas(16) Hot3 {
-  double cx, cy, cz, r;
   EyeVcm eye;
   HitF F;
-  uint32_t h, gathered;
+  uint32_t h, nruns;  // runs3[q][0 .. nruns): sorted-record [begin, begin + len)
 };
+constexpr int kG3MaxRuns = 32;
 
 __global__ void __launch_bounds__(128) k_prep_3d(const GatherArgs A, const uint32_t *__restrict__ order,
-                                               Hot3 *__restrict__ hot, Hit *__restrict__ hits) {
+                                               Hot3 *__restrict__ hot, Hit *__restrict__ hits,
+                                               uint2 *__restrict__ runs) {
+  const GridHeader g = *A.grid;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < A.H; q += gridDim.x * blockDim.x) {
     const uint32_t h = order ? order[q] : q;
     Hit H;
     make_hit(A, h, H);
     hits[q] = H;
     Hot3 o;
-    o.cx = H.cx; o.cy = H.cy; o.cz = H.cz; o.r = H.r;
     o.F = hitf(H, A.na, A.ns);
     o.h = h;
-    o.gathered = (A.gathered == nullptr || A.gathered[h] != 0) ? 1u : 0u;
     o.eye = EyeVcm{0.0, 0.0, 0.0, 0.0};
     if (A.vcm) {  // bsdf.cpp:42-51 continuation, eye MIS partials
       const double3 wo = A.wo[h], al = A.alb[h];
@@ -441,6 +441,25 @@ __global__ void __launch_bounds__(128) k_prep_3d(const GatherArgs A, const uint3
       o.eye.d_vcm = em.x;
       o.eye.d_vm = em.y;
     }
+    // the box's (x, y) columns clipped to the chord, non-empty ones only
+    uint32_t nr = 0;
+    FBox b = {0, -1, 0, -1, 0, -1};
+    const bool gathered = A.gathered == nullptr || A.gathered[h] != 0;
+    if (gathered && fine_box(g, H.cx, H.cy, H.cz, H.r, b)) {
+      const int n = run_count(g, b);
+      const double cm = fmax(fabs(H.cx), fmax(fabs(H.cy), fabs(H.cz)));
+      const double m = da(da(H.r, dm(H.r, 1e-9)), dm(cm, 4e-16));
+      uint2 *dst = runs + (size_t)q * kG3MaxRuns;
+      for (int j = 0; j < n; ++j) {
+        unsigned long long k0, k1;
+        if (!run_keys_clipped(g, b, j, H.cx, H.cy, H.cz, m, k0, k1)) continue;
+        const uint32_t rb = __ldg(&A.cell_start[k0]), re = __ldg(&A.cell_start[k1 + 1]);
+        // at most 23 columns of a radius-2-fine-cell disk intersect it (S = 2;
+        // 9 at S = 1), so the 32 slots always suffice
+        if (re > rb && nr < (uint32_t)kG3MaxRuns) dst[nr++] = make_uint2(rb, re - rb);
+      }
+    }
+    o.nruns = nr;
     hot[q] = o;
   }
 }
@@ -470,7 +489,7 @@ static __device__ __forceinline__ void g3_spill(uint32_t (&nib)[NW], uint32_t (&
 template <int GMAX, int CH>
 __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
     k_gather_3d(const GatherArgs A, const Hot3 *__restrict__ hot, const Hit *__restrict__ hits,
-                double *__restrict__ rows) {
+                const uint2 *__restrict__ runs, double *__restrict__ rows) {
   using L = G3Lay<GMAX, CH>;
   constexpr int NW = L::NW, NCP = L::NCP;
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -480,7 +499,6 @@ __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
   for (int i = lane; i < (NCP + 1) * 64; i += 32) slot_base[i] = 0.0;
   const uint32_t slots = smem_u32(slot_base);
   const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
-  const GridHeader g = *A.grid;
   uint32_t my_cand = 0, my_exact = 0, my_amb = 0, my_acc = 0;
   for (;;) {
     uint32_t q = 0;
@@ -492,21 +510,12 @@ __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
     const HitF F = Hq.F;
     const EyeVcm eye = Hq.eye;
     const uint32_t h = Hq.h;
-    // runs: the box's (x, y) columns clipped to the chord (lane j = run j)
-    uint32_t rs = 0, rl = 0;
-    {
-      const double cx = Hq.cx, cy = Hq.cy, cz = Hq.cz, r = Hq.r;
-      FBox b = {0, -1, 0, -1, 0, -1};
-      if (Hq.gathered && fine_box(g, cx, cy, cz, r, b)) {
-        const int nruns = run_count(g, b);
-        const double cm = fmax(fabs(cx), fmax(fabs(cy), fabs(cz)));
-        const double m = da(da(r, dm(r, 1e-9)), dm(cm, 4e-16));
-        unsigned long long k0, k1;
-        if (lane < nruns && run_keys_clipped(g, b, lane, cx, cy, cz, m, k0, k1)) {
-          rs = __ldg(&A.cell_start[k0]);
-          rl = __ldg(&A.cell_start[k1 + 1]) - rs;
-        }
-      }
+    const uint32_t nruns = Hq.nruns;
+    uint32_t rs = 0, rl = 0;  // lane j = run j (k_prep_3d)
+    if ((uint32_t)lane < nruns) {
+      const uint2 R = runs[(size_t)q * kG3MaxRuns + lane];
+      rs = R.x;
+      rl = R.y;
     }
     uint32_t incl = rl;
 #pragma unroll
@@ -655,15 +664,18 @@ __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
     for (int k = 0; k < 4; ++k) atomicAdd(&A.counters[k], c4[k]);
 }
 
-size_t hot3_bytes() { return sizeof(Hot3); }
+size_t hot3_bytes() { return sizeof(Hot3) + kG3MaxRuns * sizeof(uint2); }
 
 template <int GMAX, int CH>
 static cudaError_t launch_3d_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, void *hot,
                                  void *hits, double *rows, int sms) {
   using L = G3Lay<GMAX, CH>;
   if (A.H == 0) return cudaSuccess;
+  // one buffer: Hot3[H] then the runs [H][kG3MaxRuns]
+  Hot3 *h3 = static_cast<Hot3 *>(hot);
+  uint2 *runs = reinterpret_cast<uint2 *>(h3 + A.H);
   k_prep_3d<<<(unsigned)std::min<unsigned long long>((A.H + 127) / 128, (unsigned long long)sms * 16), 128, 0, s>>>(
-      A, order, static_cast<Hot3 *>(hot), static_cast<Hit *>(hits));
+      A, order, h3, static_cast<Hit *>(hits), runs);
   note_launches(1);
   const size_t smem = L::kSmem;
   cudaError_t e = cudaFuncSetAttribute(k_gather_3d<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -676,8 +688,7 @@ static cudaError_t launch_3d_one(cudaStream_t s, const GatherArgs &A, const uint
   const unsigned need = (A.H + L::W - 1) / L::W;
   if (blocks > need) blocks = need;
   if (blocks == 0) blocks = 1;
-  k_gather_3d<GMAX, CH><<<blocks, L::W * 32, smem, s>>>(A, static_cast<const Hot3 *>(hot),
-                                                        static_cast<const Hit *>(hits), rows);
+  k_gather_3d<GMAX, CH><<<blocks, L::W * 32, smem, s>>>(A, h3, static_cast<const Hit *>(hits), runs, rows);
   note_launches(1);
   return cudaGetLastError();
 }
