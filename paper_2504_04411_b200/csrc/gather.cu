@@ -419,14 +419,17 @@ struct alignas(16) Hot3 {
 constexpr int kG3MaxRuns = 32;
 
 __global__ void __launch_bounds__(128) k_prep_3d(const GatherArgs A, const uint32_t *__restrict__ order,
-                                               Hot3 *__restrict__ hot, Hit *__restrict__ hits,
+                                               Hot3 *__restrict__ hot, HitX *__restrict__ hits,
                                                uint2 *__restrict__ runs) {
   const GridHeader g = *A.grid;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < A.H; q += gridDim.x * blockDim.x) {
     const uint32_t h = order ? order[q] : q;
     Hit H;
     make_hit(A, h, H);
-    hits[q] = H;
+    HitX X;  // the fp64 subset the exact path and the pair values read
+    X.cx = H.cx; X.cy = H.cy; X.cz = H.cz; X.nx = H.nx; X.ny = H.ny; X.nz = H.nz;
+    X.u = H.u; X.v = H.v; X.r = H.r; X.r2 = H.r2; X.K0 = H.K0; X.K1 = H.K1; X.K2 = H.K2;
+    hits[q] = X;
     Hot3 o;
     o.F = hitf(H, A.na, A.ns);
     o.h = h;
@@ -488,7 +491,7 @@ static __device__ __forceinline__ void g3_spill(uint32_t (&nib)[NW], uint32_t (&
 
 template <int GMAX, int CH>
 __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
-    k_gather_3d(const GatherArgs A, const Hot3 *__restrict__ hot, const Hit *__restrict__ hits,
+    k_gather_3d(const GatherArgs A, const Hot3 *__restrict__ hot, const HitX *__restrict__ hits,
                 const uint2 *__restrict__ runs, double *__restrict__ rows) {
   using L = G3Lay<GMAX, CH>;
   constexpr int NW = L::NW, NCP = L::NCP;
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
     q = __shfl_sync(kFull, q, 0);
     if (q >= A.H) break;
     const Hot3 &Hq = hot[q];
-    const Hit &Hs = hits[q];  // full state: exact path only
+    const HitX &Hs = hits[q];  // fp64 state: exact path and pair values
     const HitF F = Hq.F;
     const EyeVcm eye = Hq.eye;
     const uint32_t h = Hq.h;
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
       if (live) {
         c2 = __ldg(&A.rec2[i]);
         c3 = __ldg(&A.rec3[i]);
-        live = pair_tail<CH, Hit>(A, F, Hs, i, eye, a, bb, c2, c3, sector, sv, sw, f0, f1, f2, my_exact, my_amb);
+        live = pair_tail<CH, HitX>(A, F, Hs, i, eye, a, bb, c2, c3, sector, sv, sw, f0, f1, f2, my_exact, my_amb);
       }
       if (!live) {
 #pragma unroll
@@ -675,7 +678,7 @@ static cudaError_t launch_3d_one(cudaStream_t s, const GatherArgs &A, const uint
   Hot3 *h3 = static_cast<Hot3 *>(hot);
   uint2 *runs = reinterpret_cast<uint2 *>(h3 + A.H);
   k_prep_3d<<<(unsigned)std::min<unsigned long long>((A.H + 127) / 128, (unsigned long long)sms * 16), 128, 0, s>>>(
-      A, order, h3, static_cast<Hit *>(hits), runs);
+      A, order, h3, static_cast<HitX *>(hits), runs);
   note_launches(1);
   const size_t smem = L::kSmem;
   cudaError_t e = cudaFuncSetAttribute(k_gather_3d<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -688,7 +691,7 @@ static cudaError_t launch_3d_one(cudaStream_t s, const GatherArgs &A, const uint
   const unsigned need = (A.H + L::W - 1) / L::W;
   if (blocks > need) blocks = need;
   if (blocks == 0) blocks = 1;
-  k_gather_3d<GMAX, CH><<<blocks, L::W * 32, smem, s>>>(A, h3, static_cast<const Hit *>(hits), runs, rows);
+  k_gather_3d<GMAX, CH><<<blocks, L::W * 32, smem, s>>>(A, h3, static_cast<const HitX *>(hits), runs, rows);
   note_launches(1);
   return cudaGetLastError();
 }

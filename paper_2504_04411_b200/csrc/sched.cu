@@ -8,21 +8,34 @@
 
 namespace fppm_b200 {
 
+// 10-bit coordinate spread to every third bit (Morton order)
+static __device__ __forceinline__ uint32_t spread3(uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+// Hit points keyed by their cell: Morton order when every extended axis fits
+// 10 bits (spatially compact runs of hit points share records in L2), else
+// the dense cell index; key `none` = no candidates (outside / not gathered).
 __global__ void k_hp_bin(const double3 *__restrict__ pos, const uint8_t *__restrict__ gathered,
-                         uint32_t H, const GridHeader *__restrict__ hdr,
+                         uint32_t H, const GridHeader *__restrict__ hdr, uint32_t none, int morton,
                          uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
   const GridHeader g = *hdr;
   const long long ex = g.nx + 2, ey = g.ny + 2, ez = g.nz + 2;
-  const uint32_t n_ext = (uint32_t)(ex * ey * ez);
   for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
-    uint32_t key = n_ext;
+    uint32_t key = none;
     const double3 c = pos[h];
     if (g.n > 0 && (gathered == nullptr || gathered[h])) {
       const long long X = (long long)floor(dm(c.x, g.inv)) - g.ix0 + 1;
       const long long Y = (long long)floor(dm(c.y, g.inv)) - g.iy0 + 1;
       const long long Z = (long long)floor(dm(c.z, g.inv)) - g.iz0 + 1;
       if (X >= 0 && Y >= 0 && Z >= 0 && X < ex && Y < ey && Z < ez)
-        key = (uint32_t)((X * ey + Y) * ez + Z);
+        key = morton ? (spread3((uint32_t)X) << 2) | (spread3((uint32_t)Y) << 1) | spread3((uint32_t)Z)
+                     : (uint32_t)((X * ey + Y) * ez + Z);
     }
     keys[h] = key;
     vals[h] = h;
@@ -164,11 +177,13 @@ cudaError_t hp_cell_order(cudaStream_t s, const GatherArgs &A, TileSched &S, con
   const unsigned long long n_ext =
       (unsigned long long)(g.nx + 2) * (unsigned long long)(g.ny + 2) * (unsigned long long)(g.nz + 2);
   if (n_ext + 1 >= 0xffffffffull) return cudaErrorInvalidValue;
-  k_hp_bin<<<blocks_for(A.H, 256, sms, 16), 256, 0, s>>>(A.pos, A.gathered, A.H, A.grid, S.sort.keys_a,
-                                                         S.sort.vals_a);
+  const bool morton = g.nx + 2 <= 1024 && g.ny + 2 <= 1024 && g.nz + 2 <= 1024;
+  const uint32_t none = morton ? (1u << 30) : (uint32_t)n_ext;
+  k_hp_bin<<<blocks_for(A.H, 256, sms, 16), 256, 0, s>>>(A.pos, A.gathered, A.H, A.grid, none, morton ? 1 : 0,
+                                                         S.sort.keys_a, S.sort.vals_a);
   note_launches(1);
   uint32_t bits = 1;
-  while (bits < 32 && (1ull << bits) < n_ext + 1) ++bits;
+  while (bits < 32 && (1ull << bits) < (unsigned long long)none + 1) ++bits;
   uint32_t *skeys, *svals;
   cudaError_t e = radix_sort_pairs(s, S.sort, A.H, bits, &skeys, &svals);
   *order = svals;
