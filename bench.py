@@ -41,7 +41,8 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    p.add_argument("--workload", default="c2", choices=["c1", "c2", "c5"],
+                   help="c5: BASELINE configs[4] at full size (bench_c5.py)")
     p.add_argument("--kernel", default="auto", choices=["auto", "fine", "warp", "3d"],
                    help="gather kernel variant (A/B)")
     p.add_argument("--no-e2e", action="store_true")
@@ -853,7 +854,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference_arm(args, wl, rank)
+        if args.workload == "c5":
+            import bench_c5
+            bench_c5.run_reference(args, wl, rank, emit, METRIC)
+        else:
+            run_reference_arm(args, wl, rank)
         return
     if world > 1:
         import torch
@@ -861,7 +866,11 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_gpu_arm(args, wl, rank, world, local_rank)
+        if args.workload == "c5":
+            import bench_c5
+            bench_c5.run_gpu(args, wl, rank, world, local_rank, emit, METRIC, ClockSampler, peaks)
+        else:
+            run_gpu_arm(args, wl, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -200,6 +200,14 @@ int fppm_gpu_set_regions(fppm_gpu_ctx *ctx, const double *radius, const uint64_t
                          const uint64_t *stat_count, const double *stat_sum,
                          const double *stat_sum_sq);
 int fppm_gpu_max_radius(fppm_gpu_ctx *ctx, double *r_max);
+/* Multi-GPU plumbing (no host round trip): the max live radius written to
+ * device memory d_r_max (asynchronous, context stream), and a grid build whose
+ * cell is read on the device from d_cell -- e.g. the all-reduce(max) of every
+ * rank's fppm_gpu_max_radius_device (integrator.cpp:159-161).  The cell must
+ * be >= every gathered radius (the reference's r_max is); the next gather
+ * checks it and fails with "query radius exceeds cell size" otherwise. */
+int fppm_gpu_max_radius_device(fppm_gpu_ctx *ctx, double *d_r_max);
+int fppm_gpu_build_grid_device(fppm_gpu_ctx *ctx, const double *d_cell);
 
 /* ---- photons + grid (PhotonGrid) ---- */
 int fppm_gpu_set_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n);

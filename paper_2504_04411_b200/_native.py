@@ -143,6 +143,8 @@ _SIGS = [
     ("fppm_gpu_get_regions", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fppm_gpu_set_regions", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fppm_gpu_max_radius", C.c_int, [C.c_void_p, _dp]),
+    ("fppm_gpu_max_radius_device", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("fppm_gpu_build_grid_device", C.c_int, [C.c_void_p, C.c_void_p]),
     ("fppm_gpu_set_photons", C.c_int, [C.c_void_p, C.POINTER(Photons), C.c_uint32]),
     ("fppm_gpu_set_photons_device", C.c_int, [C.c_void_p, C.POINTER(Photons), C.c_uint32]),
     ("fppm_gpu_prefetch_photons", C.c_int, [C.c_void_p, C.POINTER(Photons), C.c_uint32]),

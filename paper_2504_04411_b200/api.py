@@ -256,6 +256,17 @@ class FppmContext:
         self._check(self._lib.fppm_gpu_max_radius(self._h, C.byref(r)))
         return r.value
 
+    def max_radius_device(self, out) -> None:
+        """Max live radius into device memory (a float64 CUDA tensor of one
+        element), stream-ordered on the context stream, no host sync."""
+        self._check(self._lib.fppm_gpu_max_radius_device(self._h, C.c_void_p(out.data_ptr())))
+
+    def build_grid_device(self, cell) -> None:
+        """Grid whose cell is read on the device from `cell` (float64 CUDA
+        tensor of one element, e.g. the all-reduced max of every rank's
+        max_radius_device)."""
+        self._check(self._lib.fppm_gpu_build_grid_device(self._h, C.c_void_p(cell.data_ptr())))
+
     # ------------------------------------------------------------ photons + grid
     def set_photons(self, pos, normal, wi, power, depth):
         dev = _is_device(pos)

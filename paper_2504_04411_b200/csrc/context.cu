@@ -792,6 +792,11 @@ static int device_max_radius(fppm_gpu_ctx *ctx, double *dst, const uint8_t *gath
   return FPPM_OK;
 }
 
+int fppm_gpu_max_radius_device(fppm_gpu_ctx *ctx, double *d_r_max) {
+  if (!ctx || !d_r_max) return FPPM_ERR_INVALID_ARGUMENT;
+  return device_max_radius(ctx, d_r_max);
+}
+
 int fppm_gpu_max_radius(fppm_gpu_ctx *ctx, double *r_max) {
   if (!ctx || !r_max) return FPPM_ERR_INVALID_ARGUMENT;
   int rc = device_max_radius(ctx, ctx->d_cell);
@@ -985,13 +990,15 @@ int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi
 
 
 // S_req > 1 asks for the fine (slab) table when the photon set allows it.
-static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) {
+static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, const double *d_cell_in = nullptr) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   cudaStream_t s = ctx->stream;
   ctx->grid_valid = false;
-  ctx->grid_explicit = cell_size > 0.0;
+  ctx->grid_explicit = cell_size > 0.0 || d_cell_in != nullptr;
   ctx->rcheck = ctx->grid_explicit;
-  if (cell_size > 0.0) {
+  if (d_cell_in) {
+    FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_cell, d_cell_in, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  } else if (cell_size > 0.0) {
     *ctx->h_cell = cell_size;
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_cell, ctx->h_cell, sizeof(double), cudaMemcpyHostToDevice, s));
   } else {
@@ -1055,6 +1062,16 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req) 
 
 // The fine gather uses the fine (slab) table; query_ball / export_grid switch
 // back to reference cells on demand (ensure_reference_cells).
+static uint32_t requested_S(const fppm_gpu_ctx *ctx) {
+  const int v = gather_variant(ctx);
+  return v == 4 ? kFineS : (v == 5 ? 2u : 1u);
+}
+
+int fppm_gpu_build_grid_device(fppm_gpu_ctx *ctx, const double *d_cell) {
+  if (!ctx || !d_cell) return FPPM_ERR_INVALID_ARGUMENT;
+  return build_grid_impl(ctx, 0.0, requested_S(ctx), d_cell);
+}
+
 int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
   // the fine kernel asks for slab fine cells (falling back to 3D fine cells
