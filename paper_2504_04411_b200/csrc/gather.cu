@@ -453,13 +453,28 @@ __global__ void __launch_bounds__(128) k_prep_3d(const GatherArgs A, const uint3
       const double cm = fmax(fabs(H.cx), fmax(fabs(H.cy), fabs(H.cz)));
       const double m = da(da(H.r, dm(H.r, 1e-9)), dm(cm, 4e-16));
       uint2 *dst = runs + (size_t)q * kG3MaxRuns;
-      for (int j = 0; j < n; ++j) {
-        unsigned long long k0, k1;
-        if (!run_keys_clipped(g, b, j, H.cx, H.cy, H.cz, m, k0, k1)) continue;
-        const uint32_t rb = __ldg(&A.cell_start[k0]), re = __ldg(&A.cell_start[k1 + 1]);
+      // blocks of 12 columns: keys first, then all their table loads in
+      // flight together, then the compaction (the loads are the latency)
+      constexpr int kB = 12;
+      for (int j0 = 0; j0 < n; j0 += kB) {
+        unsigned long long ka[kB], kb[kB];
+        bool ok[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          ok[u] = j0 + u < n && run_keys_clipped(g, b, j0 + u, H.cx, H.cy, H.cz, m, ka[u], kb[u]);
+          if (!ok[u]) ka[u] = kb[u] = 0;
+        }
+        uint32_t rb[kB], re[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          rb[u] = ok[u] ? __ldg(&A.cell_start[ka[u]]) : 0u;
+          re[u] = ok[u] ? __ldg(&A.cell_start[kb[u] + 1]) : 0u;
+        }
         // at most 23 columns of a radius-2-fine-cell disk intersect it (S = 2;
         // 9 at S = 1), so the 32 slots always suffice
-        if (re > rb && nr < (uint32_t)kG3MaxRuns) dst[nr++] = make_uint2(rb, re - rb);
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (re[u] > rb[u] && nr < (uint32_t)kG3MaxRuns) dst[nr++] = make_uint2(rb[u], re[u] - rb[u]);
       }
     }
     o.nruns = nr;

@@ -592,7 +592,9 @@ void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const 
                        uint32_t *start, unsigned long long ncells, int sms) {
   if (n == 0) {
     k_cell_start_empty<<<1, 32, 0, s>>>(start, ncells);
-  } else if (ncells > 4ull * n) {
+  } else if (8ull * ncells > (unsigned long long)n) {
+    // tables with empty stretches (sparse or clustered photons, e.g. C5):
+    // warp-cooperative fill, no thread walks a long gap
     k_cell_start_chunked<<<cap_blocks((ncells + 1 + 255) / 256 * 32, 256, sms, 16), 256, 0, s>>>(skeys, n, ncells,
                                                                                               start);
   } else {

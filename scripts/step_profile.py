@@ -8,7 +8,7 @@ import torch
 from paper_2504_04411_b200 import FppmContext, WORKLOADS
 wl = WORKLOADS[os.environ.get("WL", "c2")]
 ctx = FppmContext(**wl.context_kwargs())
-ctx.generate_raster_hitpoints(wl.raster)
+wl.set_hitpoints(ctx)
 steps = int(os.environ.get("STEPS", "3"))
 for it in range(1, 4):
     ctx.generate_photons(wl.generator, wl.seed, it, wl.photons)
@@ -16,12 +16,18 @@ for it in range(1, 4):
     ctx.gather_test(it, outputs=False, summary=False)
 ctx.synchronize()
 acts = [torch.profiler.ProfilerActivity.CUDA]
+import time
+wall = 0.0
 with torch.profiler.profile(activities=acts) as prof:
     for it in range(4, 4 + steps):
         ctx.generate_photons(wl.generator, wl.seed, it, wl.photons)
+        ctx.synchronize()
+        t0 = time.perf_counter()
         ctx.build_grid(0.0)
         ctx.gather_test(it, outputs=False, summary=False)
-    ctx.synchronize()
+        ctx.synchronize()
+        wall += time.perf_counter() - t0
+print(f"wall per step (grid + gather, host-synchronised): {1e3 * wall / steps:.3f} ms")
 tot = collections.defaultdict(float)
 cnt = collections.Counter()
 for e in prof.events():
