@@ -362,6 +362,11 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
                         uint32_t max_depth, uint32_t *n_photons);
 /* Film::image(): per-pixel mean over the added iterations ([npix][3] host). */
 int fppm_gpu_film_mean(fppm_gpu_ctx *ctx, double *rgb, uint64_t *iterations);
+/* Film::vc_total / vm_total (film.hpp:52-53, add_split film.cpp:28-31): the
+ * per-pixel cumulative luminance delivered by merges (vm) and by everything
+ * else (vc: emitted radiance, next-event estimation, connections, camera
+ * splats) over the added iterations ([npix] host arrays, NULL skips). */
+int fppm_gpu_film_splits(fppm_gpu_ctx *ctx, double *vc, double *vm);
 
 /* Copies the staged photons' VCM partials (d_vcm, d_vm, cont; photon order)
  * to host arrays of n_photons doubles each (vcm_plus contexts only). */

@@ -154,6 +154,19 @@ class Oracle:
                                                                C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
                                                                C.c_void_p, C.c_void_p, _dp])
             self._brad = fn("bounding_radius", C.c_double, [C.c_void_p])
+            self._ser = fn("serialize_scene", C.c_long, [C.c_char_p, C.c_char_p, C.c_size_t])
+            self._wcsv = fn("write_convergence_csv", C.c_int, [C.c_char_p, C.c_size_t] + [C.c_void_p] * 5)
+            self._rcsv = fn("read_convergence_csv", C.c_long, [C.c_char_p, C.c_size_t] + [C.c_void_p] * 5 +
+                            [C.c_char_p, C.c_size_t])
+            self._wpfm = fn("write_pfm", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_void_p])
+            self._mse = fn("mse", C.c_double, [C.c_int, C.c_int, C.c_void_p, C.c_void_p])
+            self._slope = fn("fit_slope", C.c_double, [C.c_size_t, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, _ip])
+            self._faux = fn("film_aux", None, [C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_double, C.c_double] +
+                            [C.c_void_p] * 5)
+            self._render_ex = fn("render_ex", C.c_int, [C.c_void_p, C.c_int, _dp, C.c_double, C.c_int, C.c_int,
+                                                        C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, C.c_double,
+                                                        C.c_int, C.c_int, C.c_double, C.c_int, C.c_double, C.c_int,
+                                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p])
             self._sparse = fn("scene_parse", C.c_void_p, [C.c_char_p, C.c_char_p, C.c_size_t])
             self._sexport = fn("scene_export", None, [C.c_void_p] + [C.c_void_p] * 10)
             self._trace = fn("trace_photons", C.c_size_t, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
@@ -227,6 +240,55 @@ class Oracle:
         if self.kind != "port":
             raise NotImplementedError("the C5 generator is part of the C restatement")
         return _C5(self, seed, H)
+
+    # ---- formats and film outputs (reference build only; tests/test_formats.py)
+    def serialize_scene(self, text: str) -> str:
+        n = self._ser(text.encode(), None, 0)
+        if n < 0:
+            raise OracleError("reference parse_scene failed")
+        buf = C.create_string_buffer(n + 1)
+        self._ser(text.encode(), buf, n + 1)
+        return buf.value.decode()
+
+    def write_convergence_csv(self, path, rows):
+        it = np.ascontiguousarray([r[0] for r in rows], np.uint64)
+        cols = [np.ascontiguousarray([r[k] for r in rows], np.float64) for k in range(1, 5)]
+        if self._wcsv(path.encode(), len(rows), it.ctypes.data, *[c.ctypes.data for c in cols]):
+            raise OracleError("reference write_convergence_csv failed")
+
+    def read_convergence_csv(self, path, cap=4096):
+        it = np.zeros(cap, np.uint64)
+        cols = [np.zeros(cap) for _ in range(4)]
+        err = C.create_string_buffer(512)
+        n = self._rcsv(path.encode(), cap, it.ctypes.data, *[c.ctypes.data for c in cols], err, 512)
+        if n < 0:
+            raise OracleError(err.value.decode())
+        return [(int(it[i]), *[float(c[i]) for c in cols]) for i in range(n)]
+
+    def write_pfm(self, path, img):
+        a = np.ascontiguousarray(img, np.float64)
+        if self._wpfm(path.encode(), a.shape[1], a.shape[0], a.ctypes.data):
+            raise OracleError("reference write_pfm failed")
+
+    def mse(self, a, b):
+        a, b = np.ascontiguousarray(a, np.float64), np.ascontiguousarray(b, np.float64)
+        return self._mse(a.shape[1], a.shape[0], a.ctypes.data, b.ctypes.data)
+
+    def fit_convergence_slope(self, its, m, lo, hi):
+        its, m = np.ascontiguousarray(its, np.uint64), np.ascontiguousarray(m, np.float64)
+        err = C.c_int(0)
+        v = self._slope(len(its), its.ctypes.data, m.ctypes.data, lo, hi, C.byref(err))
+        if err.value:
+            raise OracleError("fit_convergence_slope")
+        return v
+
+    def film_aux(self, mean, vc, vm, radius, r_min, r_1, ref_img):
+        h, w = mean.shape[:2]
+        args = [np.ascontiguousarray(x, np.float64) for x in (mean, vc, vm, radius)]
+        ref_img = np.ascontiguousarray(ref_img, np.float64)
+        outs = [np.zeros((h, w, 3)) for _ in range(4)]
+        self._faux(w, h, *[a.ctypes.data for a in args], r_min, r_1, ref_img.ctypes.data, *[o.ctypes.data for o in outs])
+        return outs
 
     def parse_scene_error(self, text: str):
         """The reference parser's ParseError message for `text` ('' when it
@@ -384,6 +446,24 @@ def _scene_render(self, cam, seed, iterations, max_depth, light_paths, r0_frac=0
     return film, radius, secs.value
 
 
+def _scene_render_ex(self, cam, algorithm, seed, iterations, max_depth, light_paths, r0_frac=0.002, n_annuli=2,
+                     n_sectors=6, alpha_f=0.01, override="none", r_min_base=0.0, threads=0):
+    """render() for fppm / vcm_plus / sppm / vcm / cppm with a test override:
+    (film mean [npix][3], last radii, vc totals, vm totals)."""
+    n = cam.width * cam.height
+    film, radius, vc, vm = np.zeros((n, 3)), np.zeros(n), np.zeros(n), np.zeros(n)
+    algo = {"fppm": 0, "vcm_plus": 1, "sppm": 2, "vcm": 3, "cppm": 4}[algorithm]
+    ov = {"none": 0, "always_reject": 1, "never_reject": 2}[override]
+    c9 = _cam9(cam)
+    rc = self.o._render_ex(self.h, algo, c9.ctypes.data_as(_dp), cam.vfov_deg, cam.width, cam.height, seed,
+                           iterations, max_depth, light_paths, r0_frac, n_annuli, n_sectors, alpha_f, ov,
+                           r_min_base, threads, film.ctypes.data, radius.ctypes.data, vc.ctypes.data, vm.ctypes.data)
+    if rc:
+        raise OracleError("reference render failed")
+    return film, radius, vc, vm
+
+
+_Scene.render_ex = _scene_render_ex
 _Scene.eye_pass = _scene_eye
 _Scene.render_fppm = _scene_render
 _Scene.render_vcm_plus = lambda self, *a, **k: _scene_render(self, *a, algorithm="vcm_plus", **k)

@@ -765,6 +765,159 @@ int ref_render_vcm_plus(void* sp, const double* cam9, double vfov, int w, int h,
                      na, ns, alpha_f, threads, film_mean, radius, seconds);
 }
 
+
+// ---- formats and film outputs (film.cpp, scene_parse.cpp): the reference's
+// own functions for the host-side format tests (tests/test_formats.py)
+long ref_serialize_scene(const char* text, char* out, size_t cap) {
+  try {
+    const Scene sc = parse_scene(text, "", "<scene>");
+    const std::string s = serialize_scene(sc);
+    if (out && cap) {
+      std::strncpy(out, s.c_str(), cap - 1);
+      out[cap - 1] = 0;
+    }
+    return static_cast<long>(s.size());
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+static std::vector<ConvergenceRow> conv_rows(size_t n, const uint64_t* it, const double* sec, const double* m,
+                                             const double* rad, const double* vms) {
+  std::vector<ConvergenceRow> rows(n);
+  for (size_t i = 0; i < n; ++i) rows[i] = ConvergenceRow{it[i], sec[i], m[i], rad[i], vms[i]};
+  return rows;
+}
+
+int ref_write_convergence_csv(const char* path, size_t n, const uint64_t* it, const double* sec, const double* m,
+                              const double* rad, const double* vms) {
+  try {
+    write_convergence_csv(path, conv_rows(n, it, sec, m, rad, vms));
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return 0;
+}
+
+// rows read (<= cap) or -1 with the message in err
+long ref_read_convergence_csv(const char* path, size_t cap, uint64_t* it, double* sec, double* m, double* rad,
+                              double* vms, char* err, size_t errcap) {
+  try {
+    const auto rows = read_convergence_csv(path);
+    for (size_t i = 0; i < rows.size() && i < cap; ++i) {
+      it[i] = rows[i].iteration; sec[i] = rows[i].seconds; m[i] = rows[i].mse;
+      rad[i] = rows[i].mean_radius; vms[i] = rows[i].vm_share;
+    }
+    return static_cast<long>(rows.size());
+  } catch (const std::exception& e) {
+    if (err && errcap) {
+      std::strncpy(err, e.what(), errcap - 1);
+      err[errcap - 1] = 0;
+    }
+    return -1;
+  }
+}
+
+static Image make_image(int w, int h, const double* rgb) {
+  Image img{w, h, {}};
+  img.pixels.resize(static_cast<size_t>(w) * h);
+  for (size_t i = 0; i < img.pixels.size(); ++i) img.pixels[i] = Rgb{rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+  return img;
+}
+
+static void put_image(const Image& img, double* rgb) {
+  for (size_t i = 0; i < img.pixels.size(); ++i) {
+    rgb[3 * i] = img.pixels[i].r; rgb[3 * i + 1] = img.pixels[i].g; rgb[3 * i + 2] = img.pixels[i].b;
+  }
+}
+
+int ref_write_pfm(const char* path, int w, int h, const double* rgb) {
+  try {
+    write_pfm(path, make_image(w, h, rgb));
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return 0;
+}
+
+double ref_mse(int w, int h, const double* a, const double* b) { return mse(make_image(w, h, a), make_image(w, h, b)); }
+
+double ref_fit_slope(size_t n, const uint64_t* it, const double* m, uint64_t lo, uint64_t hi, int* err) {
+  try {
+    *err = 0;
+    return fit_convergence_slope(std::span<const uint64_t>(it, n), std::span<const double>(m, n), lo, hi);
+  } catch (const std::exception&) {
+    *err = 1;
+    return 0.0;
+  }
+}
+
+// A Film holding one iteration `mean`, splits vc / vm and a radius channel:
+// its radius / vc-share / vm-share / squared-error images ([npix][3] each).
+void ref_film_aux(int w, int h, const double* mean, const double* vc, const double* vm, const double* radius,
+                  double r_min, double r_1, const double* ref, double* o_rad, double* o_vcs, double* o_vms,
+                  double* o_sq) {
+  Film film(w, h);
+  const size_t n = static_cast<size_t>(w) * h;
+  std::vector<Rgb> est(n);
+  for (size_t i = 0; i < n; ++i) est[i] = Rgb{mean[3 * i], mean[3 * i + 1], mean[3 * i + 2]};
+  film.add_iteration(est);
+  for (size_t i = 0; i < n; ++i) film.add_split(i, vc[i], vm[i]);
+  film.set_radius_channel(std::span<const double>(radius, n));
+  put_image(film.radius_image(r_min, r_1), o_rad);
+  put_image(film.vc_share_image(), o_vcs);
+  put_image(film.vm_share_image(), o_vms);
+  put_image(film.squared_error_image(make_image(w, h, ref)), o_sq);
+}
+
+// render() for any algorithm (0 fppm, 1 vcm_plus, 2 sppm, 3 vcm, 4 cppm) with
+// the test override and r_min_base, returning the film mean, the last radii
+// and the per-pixel split totals (Film::vc_total / vm_total)
+int ref_render_ex(void* sp, int algo, const double* cam9, double vfov, int w, int h, uint64_t seed,
+                  uint64_t iterations, uint32_t max_depth, uint64_t light_paths, double r0_frac, int na, int ns,
+                  double alpha_f, int override_decision, double r_min_base, int threads, double* film_mean,
+                  double* radius, double* vc, double* vm) {
+  RefScene* rs = static_cast<RefScene*>(sp);
+  Scene scene = rs->scene;
+  scene.has_camera = true;
+  scene.camera = make_cam(cam9, vfov, w, h);
+  IntegratorConfig cfg;
+  const Algorithm algos[] = {Algorithm::fppm, Algorithm::vcm_plus, Algorithm::sppm, Algorithm::vcm,
+                             Algorithm::cppm};
+  cfg.algorithm = algos[algo];
+  cfg.iterations = iterations;
+  cfg.seed = seed;
+  cfg.max_depth = max_depth;
+  cfg.threads = threads;
+  cfg.r0_frac = r0_frac;
+  cfg.light_paths = light_paths;
+  cfg.test.n_annuli = na;
+  cfg.test.n_sectors = ns;
+  cfg.test.alpha_f = alpha_f;
+  cfg.test.override_decision = override_decision == 1   ? TestOverride::always_reject
+                               : override_decision == 2 ? TestOverride::never_reject
+                                                        : TestOverride::none;
+  if (r_min_base > 0) cfg.schedule.r_min_base = r_min_base;
+  try {
+    RenderResult res = render(scene, cfg);
+    const Image img = res.film.image();
+    for (size_t i = 0; i < img.pixels.size(); ++i) {
+      film_mean[3 * i] = img.pixels[i].r;
+      film_mean[3 * i + 1] = img.pixels[i].g;
+      film_mean[3 * i + 2] = img.pixels[i].b;
+      if (vc) vc[i] = res.film.vc_total(i);
+      if (vm) vm[i] = res.film.vm_total(i);
+    }
+    if (radius && !res.reports.empty()) {
+      const auto& r = res.reports.back().radius;
+      for (size_t i = 0; i < r.size(); ++i) radius[i] = r[i];
+    }
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return 0;
+}
+
 // bounding_radius (scene_geometry.cpp:341-362): the initial radius is
 // r0_frac times this (integrator.cpp:121).
 double ref_bounding_radius(void* sp) { return bounding_radius(static_cast<RefScene*>(sp)->scene); }

@@ -176,6 +176,7 @@ _SIGS = [
     ("fppm_gpu_render_vcm", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
     ("fppm_gpu_get_hitpoints", C.c_int, [C.c_void_p, C.POINTER(HitPoints), C.c_void_p]),
     ("fppm_gpu_film_mean", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
+    ("fppm_gpu_film_splits", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fppm_gpu_delta_stride", C.c_uint32, [C.c_void_p]),
     ("fppm_gpu_gather_deltas", C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p]),
     ("fppm_gpu_apply_deltas", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,

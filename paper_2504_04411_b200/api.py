@@ -53,8 +53,22 @@ class TestConfig:
     override_decision: str = "none"
 
 
+# auto_detect at the region level is one channel (GatherRegion, gather.cpp:40);
+# the Renderer resolves it against the scene first (resolve_channels)
 _CHANNELS = {"luminance": N.CHANNELS_LUMINANCE, "auto_detect": N.CHANNELS_LUMINANCE,
              "rgb": N.CHANNELS_RGB}
+
+
+def resolve_channels(channels: str, scene=None) -> str:
+    """Renderer's TestChannels::auto_detect (integrator.cpp:128-130): rgb when
+    the scene has a chromatic emitter, else luminance.  Without a scene the
+    region-level meaning applies (one channel, gather.cpp:40)."""
+    if channels != "auto_detect":
+        return channels
+    if scene is None:
+        return "luminance"
+    from .scene import has_chromatic_emitter
+    return "rgb" if has_chromatic_emitter(scene) else "luminance"
 _OVERRIDE = {"none": N.OVERRIDE_NONE, "always_reject": N.OVERRIDE_ALWAYS_REJECT,
              "never_reject": N.OVERRIDE_NEVER_REJECT}
 _POLICY = {"ftest": N.POLICY_FTEST, "chi2": N.POLICY_CHI2, "schedule": N.POLICY_SCHEDULE}
@@ -94,12 +108,12 @@ class FppmContext:
                  max_depth: int = 10, normal_guard_cos: float = NORMAL_GUARD_COS,
                  max_hitpoints: int = 1, max_photons: int = 1, max_cells: int = 0,
                  device: int = 0, stream: Optional[int] = None, gather_kernel: str = "auto",
-                 vcm_plus: bool = False, mis_n_vm: int = 0, mis_beta: float = 1.0):
+                 vcm_plus: bool = False, mis_n_vm: int = 0, mis_beta: float = 1.0, scene=None):
         self._lib = N.lib()
         cfg = N.Config()
         cfg.n_annuli, cfg.n_sectors = n_annuli, n_sectors
         cfg.alpha_f, cfg.alpha_chi2 = alpha_f, alpha_chi2
-        cfg.channels = _CHANNELS[channels]
+        cfg.channels = _CHANNELS[resolve_channels(channels, scene)]
         cfg.override_decision = _OVERRIDE[override_decision]
         cfg.policy = _POLICY[policy]
         cfg.k, cfg.alpha = k, alpha
@@ -344,6 +358,14 @@ class FppmContext:
         it = C.c_uint64()
         self._check(self._lib.fppm_gpu_film_mean(self._h, out.ctypes.data, C.byref(it)))
         return out.reshape(self.camera.height, self.camera.width, 3), it.value
+
+    def film_splits(self):
+        """(vc, vm): per-pixel cumulative luminance of the non-merge and the
+        merge estimates (Film::vc_total / vm_total), [height, width] each."""
+        n = self.camera.width * self.camera.height
+        vc, vm = np.zeros(n), np.zeros(n)
+        self._check(self._lib.fppm_gpu_film_splits(self._h, vc.ctypes.data, vm.ctypes.data))
+        return vc.reshape(self.camera.height, self.camera.width), vm.reshape(self.camera.height, self.camera.width)
 
     def render_iteration(self, seed: int, iteration: int, light_paths: int, max_depth: Optional[int] = None,
                          outputs: bool = False, stats: bool = False):

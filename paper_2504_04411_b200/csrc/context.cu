@@ -61,6 +61,7 @@ struct fppm_gpu_ctx {
   fppm_b200::CamD cam{};
   bool has_camera = false;
   double3 *d_emit = nullptr, *d_film = nullptr;  // per pixel: emitted radiance, film sum
+  double2 *d_vcvm = nullptr;  // per pixel cumulative {vc, vm} luminance (Film::add_split)
   uint64_t film_iters = 0;
   fppm_b200::TraceScene scene{};
   void *scene_mem[9] = {};  // [8]: per-primitive constants (k_scene_prep)
@@ -566,6 +567,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   for (void *p : ctx->c5_mem)
     if (p) cudaFree(p);
   if (ctx->d_film) cudaFree(ctx->d_film);
+  if (ctx->d_vcvm) cudaFree(ctx->d_vcvm);
   for (void *p : ctx->scene_mem)
     if (p) cudaFree(p);
   {
@@ -1704,8 +1706,10 @@ int fppm_gpu_set_camera(fppm_gpu_ctx *ctx, const fppm_camera *c) {
     const size_t n = std::max<uint32_t>(ctx->cfg.max_hitpoints, 1);
     FPPM_CUDA_OK(dalloc(&ctx->d_emit, n));
     FPPM_CUDA_OK(dalloc(&ctx->d_film, n));
+    FPPM_CUDA_OK(dalloc(&ctx->d_vcvm, n));
   }
   FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_film, 0, sizeof(double3) * npix, ctx->stream));
+  FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_vcvm, 0, sizeof(double2) * npix, ctx->stream));
   ctx->film_iters = 0;
   ctx->has_camera = true;
   return FPPM_OK;
@@ -1851,7 +1855,7 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
   }
   FPPM_CUDA_OK(launch_film_vcm(s, npix, nq, ctx->d_emit, ctx->d_gathered, ctx->o_flux, ctx->o_gather_r,
                                ctx->q_rows, stride, ctx->q_gathered, ctx->q_radius, ctx->d_splat,
-                               (double)light_paths, ctx->d_film, ctx->sms));
+                               (double)light_paths, ctx->d_film, ctx->sms, ctx->d_vcvm));
   ctx->film_iters++;
   return FPPM_OK;
 }
@@ -1883,7 +1887,7 @@ int fppm_gpu_film_add(fppm_gpu_ctx *ctx) {
   const uint32_t npix = (uint32_t)((uint64_t)ctx->cam.width * ctx->cam.height);
   if (npix != ctx->H) return fail(ctx, FPPM_ERR_STATE, "film_add: hit points are not the camera's pixels");
   FPPM_CUDA_OK(launch_film(ctx->stream, 0, npix, ctx->d_emit, ctx->d_gathered, ctx->o_flux, ctx->o_gather_r,
-                           (double)ctx->cfg.samples_per_iteration, ctx->d_film, nullptr, ctx->sms));
+                           (double)ctx->cfg.samples_per_iteration, ctx->d_film, nullptr, ctx->sms, ctx->d_vcvm));
   ctx->film_iters++;
   return FPPM_OK;
 }
@@ -1901,6 +1905,21 @@ int fppm_gpu_film_mean(fppm_gpu_ctx *ctx, double *rgb, uint64_t *iterations) {
                            ctx->d_film, d, ctx->sms));
   FPPM_CUDA_OK(cudaMemcpyAsync(rgb, d, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  return FPPM_OK;
+}
+
+int fppm_gpu_film_splits(fppm_gpu_ctx *ctx, double *vc, double *vm) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (!ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "film_splits before set_camera");
+  const size_t npix = (size_t)ctx->cam.width * ctx->cam.height;
+  std::vector<double2> h(npix);
+  if (npix) FPPM_CUDA_OK(cudaMemcpyAsync(h.data(), ctx->d_vcvm, sizeof(double2) * npix, cudaMemcpyDeviceToHost,
+                                         ctx->stream));
+  FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  for (size_t i = 0; i < npix; ++i) {
+    if (vc) vc[i] = h[i].x;
+    if (vm) vm[i] = h[i].y;
+  }
   return FPPM_OK;
 }
 

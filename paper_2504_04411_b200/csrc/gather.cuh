@@ -307,11 +307,12 @@ cudaError_t launch_light_splat(cudaStream_t s, const BidirArgs &B, const void *p
 cudaError_t launch_film_vcm(cudaStream_t s, uint32_t npix, uint32_t nq_per_px, const double3 *direct,
                             const uint8_t *gathered, const double *flux, const double *gather_r,
                             const double *q_rows, uint32_t q_stride, const uint8_t *q_gathered,
-                            const double *q_radius, const double3 *splat, double J, double3 *film, int sms);
+                            const double *q_radius, const double3 *splat, double J, double3 *film, int sms,
+                            double2 *vcvm);
 // op 0: film += estimate (J = samples per iteration); op 1: mean_out = film / J (J = iterations)
 cudaError_t launch_film(cudaStream_t s, int op, uint32_t npix, const double3 *emitted, const uint8_t *gathered,
                         const double *flux, const double *gather_r, double J, double3 *film, double *mean_out,
-                        int sms);
+                        int sms, double2 *vcvm = nullptr);
 size_t trace_prep_bytes(int n_prim);
 int trace_max_prims();
 cudaError_t launch_scene_prep(cudaStream_t s, const TraceScene &sc, void *prep);

@@ -524,6 +524,18 @@ static __device__ __forceinline__ void finalize_hit(const GatherArgs &A, uint32_
     }
     A.radius[h] = r_new;
     A.t[h] = t;
+  } else if (A.end.policy == FPPM_POLICY_SCHEDULE) {
+    // the global schedule (SPPM / VCM: one radius for every pixel,
+    // integrator.cpp:159-170 radius_now_) moves on whether or not the pixel
+    // gathered
+    r_new = A.end.sched_next;
+    A.radius[h] = r_new;
+    if (A.snap_cnt)
+      for (int i = 0; i < CG; ++i) {
+        A.snap_cnt[base + i] = A.st_cnt[base + i];
+        A.snap_sum[base + i] = A.st_sum[base + i];
+        A.snap_sq[base + i] = A.st_sq[base + i];
+      }
   } else if (A.snap_cnt) {  // no observation: state holds (integrator.cpp:483-488)
     for (int i = 0; i < CG; ++i) {
       A.snap_cnt[base + i] = A.st_cnt[base + i];

@@ -662,17 +662,30 @@ __global__ void __launch_bounds__(128) k_trace_eye(const EyeArgs E, const PrimD 
 
 // Film::add_iteration (film.cpp:21-26) of the pixel estimate
 // out = emitted + sum / (pi r^2 J) (integrator.cpp:452-455).
+// Film::add_iteration + add_split (film.cpp:21-34; integrator.cpp:452-474):
+// vc = luminance of the emitted radiance along the chain, vm = luminance of
+// the kernel estimate c = sum / (pi r^2 J).
 __global__ void k_film_add(uint32_t npix, const double3 *__restrict__ emitted, const uint8_t *__restrict__ gathered,
                            const double *__restrict__ flux, const double *__restrict__ gather_r, double J,
-                           double3 *__restrict__ film) {
+                           double3 *__restrict__ film, double2 *__restrict__ vcvm) {
   for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < npix; px += gridDim.x * blockDim.x) {
     double3 est = emitted[px];
+    double vm = 0.0;
     if (gathered[px]) {
       const double r = gather_r[px];
       const double denom = dm(dm(dm(kPi, r), r), J);
-      est.x = da(est.x, dd(flux[3 * (size_t)px], denom));
-      est.y = da(est.y, dd(flux[3 * (size_t)px + 1], denom));
-      est.z = da(est.z, dd(flux[3 * (size_t)px + 2], denom));
+      const double c0 = dd(flux[3 * (size_t)px], denom), c1 = dd(flux[3 * (size_t)px + 1], denom),
+                   c2 = dd(flux[3 * (size_t)px + 2], denom);
+      vm = elum(c0, c1, c2);
+      est.x = da(est.x, c0);
+      est.y = da(est.y, c1);
+      est.z = da(est.z, c2);
+    }
+    if (vcvm) {
+      double2 v = vcvm[px];
+      v.x = da(v.x, elum(emitted[px].x, emitted[px].y, emitted[px].z));
+      v.y = da(v.y, vm);
+      vcvm[px] = v;
     }
     double3 f = film[px];
     f.x = da(f.x, est.x);
@@ -702,12 +715,12 @@ cudaError_t launch_trace_eye(cudaStream_t s, const EyeArgs &E, const void *prep,
 
 cudaError_t launch_film(cudaStream_t s, int op, uint32_t npix, const double3 *emitted, const uint8_t *gathered,
                         const double *flux, const double *gather_r, double J, double3 *film, double *mean_out,
-                        int sms) {
+                        int sms, double2 *vcvm) {
   if (npix == 0) return cudaSuccess;
   unsigned blocks = (npix + 255) / 256;
   if (blocks > (unsigned)sms * 8) blocks = sms * 8;
   if (op == 0)
-    k_film_add<<<blocks, 256, 0, s>>>(npix, emitted, gathered, flux, gather_r, J, film);
+    k_film_add<<<blocks, 256, 0, s>>>(npix, emitted, gathered, flux, gather_r, J, film, vcvm);
   else
     k_film_mean<<<blocks, 256, 0, s>>>(npix, film, J, mean_out);
   note_launches(1);
@@ -1111,15 +1124,22 @@ __global__ void k_film_vcm(uint32_t npix, uint32_t nq, const double3 *__restrict
                            const uint8_t *__restrict__ gathered, const double *__restrict__ flux,
                            const double *__restrict__ gather_r, const double *__restrict__ q_rows, uint32_t q_stride,
                            const uint8_t *__restrict__ q_gathered, const double *__restrict__ q_radius,
-                           const double3 *__restrict__ splat, double J, double3 *__restrict__ film) {
+                           const double3 *__restrict__ splat, double J, double3 *__restrict__ film,
+                           double2 *__restrict__ vcvm) {
   for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < npix; px += gridDim.x * blockDim.x) {
     double3 est = direct[px];
+    // add_split (integrator.cpp:205-211, 623-624): vm = luminance of the
+    // merges, vc = luminance of everything else (direct + camera splats)
+    double vm = 0.0;
     if (gathered[px]) {
       const double r = gather_r[px];
       const double vn = dd(1.0, dm(dm(dm(kPi, r), r), J));
-      est.x = da(est.x, dm(flux[3 * (size_t)px], vn));
-      est.y = da(est.y, dm(flux[3 * (size_t)px + 1], vn));
-      est.z = da(est.z, dm(flux[3 * (size_t)px + 2], vn));
+      const double c0 = dm(flux[3 * (size_t)px], vn), c1 = dm(flux[3 * (size_t)px + 1], vn),
+                   c2 = dm(flux[3 * (size_t)px + 2], vn);
+      vm = da(vm, elum(c0, c1, c2));
+      est.x = da(est.x, c0);
+      est.y = da(est.y, c1);
+      est.z = da(est.z, c2);
     }
     for (uint32_t k = 0; k < nq; ++k) {
       const size_t q = (size_t)px * nq + k;
@@ -1127,11 +1147,19 @@ __global__ void k_film_vcm(uint32_t npix, uint32_t nq, const double3 *__restrict
       const double r = q_radius[q];
       const double vn = dd(1.0, dm(dm(dm(kPi, r), r), J));
       const double *row = q_rows + q * q_stride + (q_stride - 3);
-      est.x = da(est.x, dm(row[0], vn));
-      est.y = da(est.y, dm(row[1], vn));
-      est.z = da(est.z, dm(row[2], vn));
+      const double c0 = dm(row[0], vn), c1 = dm(row[1], vn), c2 = dm(row[2], vn);
+      vm = da(vm, elum(c0, c1, c2));
+      est.x = da(est.x, c0);
+      est.y = da(est.y, c1);
+      est.z = da(est.z, c2);
     }
     const double3 sp = splat[px];
+    if (vcvm) {
+      double2 v = vcvm[px];
+      v.x = da(v.x, da(elum(direct[px].x, direct[px].y, direct[px].z), elum(sp.x, sp.y, sp.z)));
+      v.y = da(v.y, vm);
+      vcvm[px] = v;
+    }
     est.x = da(est.x, sp.x);
     est.y = da(est.y, sp.y);
     est.z = da(est.z, sp.z);
@@ -1166,12 +1194,13 @@ cudaError_t launch_light_splat(cudaStream_t s, const BidirArgs &B, const void *p
 cudaError_t launch_film_vcm(cudaStream_t s, uint32_t npix, uint32_t nq_per_px, const double3 *direct,
                             const uint8_t *gathered, const double *flux, const double *gather_r,
                             const double *q_rows, uint32_t q_stride, const uint8_t *q_gathered,
-                            const double *q_radius, const double3 *splat, double J, double3 *film, int sms) {
+                            const double *q_radius, const double3 *splat, double J, double3 *film, int sms,
+                            double2 *vcvm) {
   if (npix == 0) return cudaSuccess;
   unsigned blocks = (npix + 255) / 256;
   if (blocks > (unsigned)sms * 8) blocks = sms * 8;
   k_film_vcm<<<blocks, 256, 0, s>>>(npix, nq_per_px, direct, gathered, flux, gather_r, q_rows, q_stride,
-                                    q_gathered, q_radius, splat, J, film);
+                                    q_gathered, q_radius, splat, J, film, vcvm);
   note_launches(1);
   return cudaGetLastError();
 }

@@ -26,13 +26,15 @@ class Scene:
     shape_material: list = field(default_factory=list)
     emitter_shape: list = field(default_factory=list)
     emitter_radiance: list = field(default_factory=list)
+    material_name: list = field(default_factory=list)
 
     # ---- construction (scene_parse.cpp's material / sphere / quad / emit)
-    def material(self, kind: int, rgb=(1.0, 1.0, 1.0), ior: float = 1.5) -> int:
+    def material(self, kind: int, rgb=(1.0, 1.0, 1.0), ior: float = 1.5, name: str = "") -> int:
         if kind not in (LAMBERTIAN, MIRROR, DIELECTRIC):
             raise ValueError(f"unsupported material kind {kind}")
         if kind == DIELECTRIC and not ior > 1.0:
             raise ValueError("ior must exceed 1")
+        self.material_name.append(name or f"m{len(self.material_kind)}")
         self.material_kind.append(kind)
         self.material_rgb.append([float(x) for x in rgb])
         self.material_ior.append(float(ior))
@@ -67,6 +69,62 @@ class Scene:
             emitter_shape=np.asarray(self.emitter_shape, np.int32),
             emitter_radiance=np.asarray(self.emitter_radiance, np.float64).reshape(-1, 3),
         )
+
+
+def schedule_radius_host(base: float, alpha: float, i: int) -> float:
+    """schedule_radius (gather.cpp:11-13) through the library's host table
+    function (glibc pow, like the reference build)."""
+    from .api import schedule_radius
+    return schedule_radius(base, alpha, i)
+
+
+def is_chromatic(c) -> bool:
+    """integrator.cpp:77."""
+    return c[0] != c[1] or c[1] != c[2]
+
+
+def has_chromatic_emitter(scene: Scene) -> bool:
+    """integrator.cpp:79-91 for the area emitters the device supports: the
+    Renderer resolves TestChannels::auto_detect to rgb when this holds
+    (integrator.cpp:128-130)."""
+    return any(is_chromatic(r) for r in scene.emitter_radiance)
+
+
+def _g17(x: float) -> str:
+    return "%.17g" % float(x)
+
+
+def _v3(v) -> str:
+    return "(" + ",".join(_g17(x) for x in v) + ")"
+
+
+def serialize_scene(scene: Scene, camera=None) -> str:
+    """serialize_scene (scene_parse.cpp:441-548): the reference's text form,
+    numbers printed %.17g, one line per camera / material / primitive (with
+    its emitter inline), so parse_scene(serialize_scene(s)) rebuilds s."""
+    out = []
+    if camera is not None:
+        out.append(f"camera pos={_v3(camera.position)} look={_v3(camera.look_at)} up={_v3(camera.up)} "
+                   f"fov={_g17(camera.vfov_deg)} res={int(camera.width)}x{int(camera.height)}\n")
+    names = scene.material_name or [f"m{i}" for i in range(len(scene.material_kind))]
+    for name, kind, rgb, ior in zip(names, scene.material_kind, scene.material_rgb, scene.material_ior):
+        if kind == LAMBERTIAN:
+            out.append(f"material {name} lambertian albedo={_v3(rgb)}\n")
+        elif kind == MIRROR:
+            out.append(f"material {name} mirror refl={_v3(rgb)}\n")
+        else:
+            out.append(f"material {name} dielectric ior={_g17(ior)} tint={_v3(rgb)}\n")
+    emit = dict(zip(scene.emitter_shape, scene.emitter_radiance))
+    for i, (kind, sh, m) in enumerate(zip(scene.shape_kind, scene.shape, scene.shape_material)):
+        if kind == SPHERE:
+            line = f"sphere center={_v3(sh[0:3])} radius={_g17(sh[3])}"
+        else:
+            line = f"quad corner={_v3(sh[0:3])} e1={_v3(sh[3:6])} e2={_v3(sh[6:9])}"
+        line += f" material={names[m]}"
+        if i in emit:
+            line += f" emit={_v3(emit[i])}"
+        out.append(line + "\n")
+    return "".join(out)
 
 
 @dataclass

@@ -226,7 +226,7 @@ def parse_scene(text: str, label: str = "<scene>"):
             else:
                 cur.fail(f"unknown material kind '{kind}'")
             kv.done()
-            materials[name] = scene.material(mk, c, ior)
+            materials[name] = scene.material(mk, c, ior, name=name)
         elif kw in ("sphere", "quad"):
             kv = _Kv(cur)
             if kw == "sphere":
@@ -272,21 +272,5 @@ def load_scene(path: str):
         return parse_scene(f.read(), path)
 
 
-def write_pfm(path: str, image) -> None:
-    """film.cpp:95-115: 'PF', width height, -1.0 (little endian), rows from
-    the bottom of the image up, RGB fp32."""
-    img = np.asarray(image, dtype=np.float64)
-    h, w = img.shape[:2]
-    with open(path, "wb") as f:
-        f.write(f"PF\n{w} {h}\n-1.0\n".encode())
-        f.write(img[::-1].astype("<f4").tobytes())
-
-
-def read_pfm(path: str) -> np.ndarray:
-    with open(path, "rb") as f:
-        assert f.readline().strip() == b"PF"
-        w, h = map(int, f.readline().split())
-        scale = float(f.readline())
-        data = np.frombuffer(f.read(), dtype="<f4" if scale < 0 else ">f4")
-    return data.reshape(h, w, 3)[::-1].astype(np.float64)
-
+# PFM film I/O lives in film.py (film.cpp:95-154); kept importable from here
+from .film import read_pfm, write_pfm  # noqa: E402,F401
