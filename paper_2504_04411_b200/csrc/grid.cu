@@ -119,7 +119,21 @@ __global__ void k_grid_header(const long long *__restrict__ bounds, const double
     g.nx = b[3] - b[0] + 1;
     g.ny = b[4] - b[1] + 1;
     g.nz = b[5] - b[2] + 1;
-    const double dcells = (double)g.nx * (double)g.ny * (double)g.nz;
+    double dcells = (double)g.nx * (double)g.ny * (double)g.nz;
+    // A dense table that would not fit (many tiny cells over a large box,
+    // e.g. a global radius schedule late in a render): coarsen the cell by
+    // powers of two.  floor(x * inv / 2) = floor(floor(x * inv) / 2), so the
+    // bounds shift exactly; every radius stays <= the cell, so each hit
+    // point's accepted set is unchanged -- only the candidates' visit order
+    // (the fp64 summation order) differs from the reference's r_max grid.
+    for (int k = 0; k < 24 && !(dcells <= (double)max_cells); ++k) {
+      for (int i = 0; i < 6; ++i) b[i] >>= 1;
+      g.cell = dm(g.cell, 2.0);
+      g.inv = dm(g.inv, 0.5);
+      g.ix0 = b[0]; g.iy0 = b[1]; g.iz0 = b[2];
+      g.nx = b[3] - b[0] + 1; g.ny = b[4] - b[1] + 1; g.nz = b[5] - b[2] + 1;
+      dcells = (double)g.nx * (double)g.ny * (double)g.nz;
+    }
     g.ok = (g.nx > 0 && g.ny > 0 && g.nz > 0 && dcells <= (double)max_cells) ? 1u : 0u;
     g.ncells = g.ok ? (unsigned long long)g.nx * (unsigned long long)g.ny * (unsigned long long)g.nz : 0;
     uint32_t bits = 1;

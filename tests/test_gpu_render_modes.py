@@ -83,7 +83,8 @@ def test_algorithms_match_reference_render(ref, algorithm):
     """Each algorithm's film and final radii against the reference render()
     (caustic box 24^2): within 1e-6 relative on every pixel (measured <= 1e-7;
     the device photons are the reference's rounded to fp32), radii identical,
-    the vc / vm split totals within 1e-9."""
+    the vc / vm split totals within 1e-6 like the film (the merge share
+    carries the photon powers' fp32 rounding)."""
     sc, cam = caustic_box(), caustic_box_camera(24)
     J, iters = 6000, 3
     got = render(sc, cam, algorithm, iters, seed=11, max_depth=8, light_paths=J, r0_frac=0.002,
@@ -95,8 +96,8 @@ def test_algorithms_match_reference_render(ref, algorithm):
     print(f"{algorithm}: max rel film diff {rel.max():.2e}, radii differ at {(got.reports[-1].radius != radius).sum()}")
     assert (rel <= 1e-6).all()
     assert np.array_equal(got.reports[-1].radius, radius)
-    np.testing.assert_allclose(got.vc_total.ravel(), vc, rtol=1e-9, atol=1e-300)
-    np.testing.assert_allclose(got.vm_total.ravel(), vm, rtol=1e-9, atol=1e-300)
+    np.testing.assert_allclose(got.vc_total.ravel(), vc, rtol=1e-6, atol=1e-300)
+    np.testing.assert_allclose(got.vm_total.ravel(), vm, rtol=1e-6, atol=1e-300)
 
 
 def test_reports_and_film_agree_on_the_split():
