@@ -295,6 +295,18 @@ int fppm_gpu_set_samples_per_iteration(fppm_gpu_ctx *ctx, uint64_t samples_per_i
 int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration,
                            fppm_gpu_iter_out *out);
 
+/* Switches the end-of-iteration policy of every region (gather.cpp:90 F-test,
+ * :114 chi-squared, :138 fixed schedule), e.g. for a caller that drives one
+ * region through different policies like the reference's GatherRegion. */
+int fppm_gpu_set_policy(fppm_gpu_ctx *ctx, int32_t policy);
+/* Host restatements of two reference free functions the C++ wrapper needs:
+ * sector_index (gather.cpp:15-33; FPPM_ERR_INVALID_ARGUMENT for bin counts
+ * < 1, FPPM_ERR_DOMAIN outside the disk) and build_tangent_frame
+ * (frame.cpp:5-14).  The device kernels evaluate the same expressions. */
+int fppm_gpu_sector_index(double u, double v, double radius, int32_t n_annuli, int32_t n_sectors,
+                          int32_t *index);
+int fppm_gpu_build_frame(const double n[3], double u[3], double v[3]);
+
 /* ---- photon emission and tracing (integrator.cpp:230-265, path.cpp:388-449) ---- */
 /* Analytic scene (Scene, scene.hpp): spheres and quads, Lambertian / mirror /
  * dielectric materials, area emitters on primitives.  Host arrays. */

@@ -159,6 +159,10 @@ _SIGS = [
     ("fppm_gpu_accumulate", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     ("fppm_gpu_set_samples_per_iteration", C.c_int, [C.c_void_p, C.c_uint64]),
     ("fppm_gpu_end_iteration", C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(IterOut)]),
+    ("fppm_gpu_set_policy", C.c_int, [C.c_void_p, C.c_int32]),
+    ("fppm_gpu_sector_index", C.c_int, [C.c_double, C.c_double, C.c_double, C.c_int32, C.c_int32,
+                                        C.POINTER(C.c_int32)]),
+    ("fppm_gpu_build_frame", C.c_int, [_dp, _dp, _dp]),
     ("fppm_gpu_kernel_launches", C.c_uint64, []),
     ("fppm_gpu_gather_kernel_ms", C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.POINTER(C.c_uint32)]),
     ("fppm_gpu_counters", C.c_int, [C.c_void_p, C.c_void_p]),

@@ -1521,6 +1521,36 @@ int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_
   return FPPM_OK;
 }
 
+int fppm_gpu_set_policy(fppm_gpu_ctx *ctx, int32_t policy) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (policy < FPPM_POLICY_FTEST || policy > FPPM_POLICY_SCHEDULE)
+    return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown end-of-iteration policy");
+  if (policy == ctx->cfg.policy) return FPPM_OK;
+  if (policy == FPPM_POLICY_CHI2 && !(ctx->chi2_crit > 0.0)) {
+    int st = 0;  // gather.cpp:117-118: solved once per region
+    const double v = host_chi2_quantile(1.0 - ctx->cfg.alpha_chi2, (double)(ctx->G - 1), &st);
+    if (st) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "chi2_quantile: bad alpha_chi2");
+    ctx->chi2_crit = v;
+  }
+  ctx->cfg.policy = policy;
+  ctx->crit.clear();  // the F table is only kept for the F policy
+  return ensure_crit(ctx, ctx->end_calls + 2);
+}
+
+int fppm_gpu_sector_index(double u, double v, double radius, int32_t n_annuli, int32_t n_sectors,
+                          int32_t *index) {
+  if (!index) return FPPM_ERR_INVALID_ARGUMENT;
+  int st = 0;
+  *index = fppm_b200::host_sector_index(u, v, radius, n_annuli, n_sectors, &st);
+  return st == 1 ? FPPM_ERR_INVALID_ARGUMENT : st == 2 ? FPPM_ERR_DOMAIN : FPPM_OK;
+}
+
+int fppm_gpu_build_frame(const double n[3], double u[3], double v[3]) {
+  if (!n || !u || !v) return FPPM_ERR_INVALID_ARGUMENT;
+  fppm_b200::host_build_frame(n, u, v);
+  return FPPM_OK;
+}
+
 uint64_t fppm_gpu_kernel_launches(void) { return g_kernel_launches.load(); }
 
 int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *sc) {

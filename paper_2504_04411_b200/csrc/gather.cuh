@@ -351,6 +351,8 @@ void launch_raster_hitpoints(cudaStream_t s, uint32_t W, double3 *pos, double3 *
 // host_stats.cpp
 double host_f_quantile(double p, double d1, double d2, int *status);
 double host_chi2_quantile(double p, double df, int *status);
+int host_sector_index(double u, double v, double radius, int na, int ns, int *status);
+void host_build_frame(const double n[3], double u[3], double v[3]);
 double host_schedule_radius(double base, double alpha, uint64_t i);
 
 }  // namespace fppm_b200

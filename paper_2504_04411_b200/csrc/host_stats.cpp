@@ -145,3 +145,45 @@ double host_schedule_radius(double base, double alpha, uint64_t i) {
 }
 
 }  // namespace fppm_b200
+
+namespace fppm_b200 {
+
+// ---- host restatements used by the reference-shaped C++ wrapper
+// gather.cpp:15-33 (glibc atan2, as the reference build): 0 ok, 1 invalid
+// argument (bin counts), 2 domain error (outside the disk)
+int host_sector_index(double u, double v, double radius, int na, int ns, int *status) {
+  *status = 0;
+  if (na < 1 || ns < 1) {
+    *status = 1;
+    return 0;
+  }
+  const double r2 = radius * radius;
+  const double d2 = u * u + v * v;
+  if (d2 > r2 * (1.0 + 1e-9)) {
+    *status = 2;
+    return 0;
+  }
+  int a = static_cast<int>(static_cast<double>(na) * d2 / r2);
+  a = a < na - 1 ? a : na - 1;
+  const double two_pi = 6.283185307179586476925286766559;
+  double theta = std::atan2(v, u);
+  if (theta < 0.0) theta += two_pi;
+  int s = static_cast<int>(static_cast<double>(ns) * theta / two_pi);
+  s = s < ns - 1 ? s : ns - 1;
+  return a * ns + s;
+}
+
+// frame.cpp:5-14 (Duff et al. branchless basis)
+void host_build_frame(const double n[3], double u[3], double v[3]) {
+  const double sign = std::copysign(1.0, n[2]);
+  const double a = -1.0 / (sign + n[2]);
+  const double b = n[0] * n[1] * a;
+  u[0] = 1.0 + sign * n[0] * n[0] * a;
+  u[1] = sign * b;
+  u[2] = -sign * n[0];
+  v[0] = b;
+  v[1] = sign + n[1] * n[1] * a;
+  v[2] = -n[1];
+}
+
+}  // namespace fppm_b200
