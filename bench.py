@@ -798,13 +798,19 @@ def run_e2e(arm, batches, args, dev):
     h2d = sum(t.numel() * t.element_size() for t in pinned[0].values())
     d2h = n_out * (8 + 12 + 1)
 
+    token = C.c_uint64(0)
+
     def one(it, hb, nxt=None):
         if world == 1 and arm.mode == "a":
-            ph = N.Photons(*[hb[k].data_ptr() for k, _, _ in photon_layout()])
-            N.check(ctx._lib.fppm_gpu_set_photons(ctx._h, ph, n_local), ctx._h)
+            if token.value:  # this step's batch was prefetched during the previous step
+                N.check(ctx._lib.fppm_gpu_adopt_photons(ctx._h, token.value), ctx._h)
+                token.value = 0
+            else:
+                ph = N.Photons(*[hb[k].data_ptr() for k, _, _ in photon_layout()])
+                N.check(ctx._lib.fppm_gpu_set_photons(ctx._h, ph, n_local), ctx._h)
             if nxt is not None:  # the next step's upload overlaps this iteration
                 pn = N.Photons(*[nxt[k].data_ptr() for k, _, _ in photon_layout()])
-                N.check(ctx._lib.fppm_gpu_prefetch_photons(ctx._h, pn, n_local), ctx._h)
+                N.check(ctx._lib.fppm_gpu_prefetch_photons(ctx._h, pn, n_local, C.byref(token)), ctx._h)
             N.check(ctx._lib.fppm_gpu_iterate(ctx._h, it, C.byref(io), None), ctx._h)
             return
         with torch.cuda.stream(arm.stream):
@@ -834,8 +840,9 @@ def run_e2e(arm, batches, args, dev):
         secs, q = float(tm.item()), float(qs.item())
     else:
         secs = t1 - t0
-    path = ("fppm_gpu_set_photons (pinned host; step i+1's upload issued by fppm_gpu_prefetch_photons before "
-            "step i's fppm_gpu_iterate, so it overlaps that iteration) + fppm_gpu_iterate with host outputs"
+    path = ("pinned host photons -> device through the ABI: step i+1's upload issued by fppm_gpu_prefetch_photons "
+            "before step i's fppm_gpu_iterate (it overlaps that iteration) and adopted by fppm_gpu_adopt_photons; "
+            "the first timed step uploads with fppm_gpu_set_photons; fppm_gpu_iterate with host outputs"
             if world == 1 and
             arm.mode == "a" else f"pinned host share -> device, option {arm.mode.upper()} step with host outputs")
     return {"value": q / secs, "unit": UNIT, "h2d_bytes_per_step": h2d,

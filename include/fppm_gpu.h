@@ -213,10 +213,16 @@ int fppm_gpu_build_grid_device(fppm_gpu_ctx *ctx, const double *d_cell);
 int fppm_gpu_set_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n);
 /* Pipelining extension (no reference counterpart): uploads the NEXT batch
  * into the free staging set on the copy stream while the current iteration
- * runs, without changing the current photons.  A later fppm_gpu_set_photons
- * with the same five host arrays and n adopts it without a copy (the arrays
- * must not change in between); any other photon call discards it. */
-int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n);
+ * runs, without changing the current photons, and returns a token.
+ * fppm_gpu_adopt_photons(token) then makes that batch current without a copy.
+ * Adoption is explicit: fppm_gpu_set_photons always copies (and discards a
+ * pending prefetch).  The host arrays must stay unchanged until adoption;
+ * adopt recomputes a sampled digest (every field of 4096 records spread over
+ * the batch) and returns FPPM_ERR_STATE when they were rewritten, as it does
+ * for a stale or superseded token -- the caller then uploads with
+ * fppm_gpu_set_photons. */
+int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n, uint64_t *token);
+int fppm_gpu_adopt_photons(fppm_gpu_ctx *ctx, uint64_t token);
 int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint32_t n);
 /* Canonical synthetic photons [begin, begin+n) of (seed, iteration). */
 int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed,

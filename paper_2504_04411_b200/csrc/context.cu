@@ -44,10 +44,11 @@ struct fppm_gpu_ctx {
   int stage_cur = 0;       // staging set the current photons live in
   int stage_pending = -1;  // set whose upload the next grid build must wait for
   // fppm_gpu_prefetch_photons: an upload of the NEXT batch into the free set,
-  // adopted without a copy by a set_photons call with the same arrays
+  // made current without a copy by fppm_gpu_adopt_photons(token)
   int pf_set = -1;
   fppm_photons pf_src{};
   uint32_t pf_n = 0;
+  uint64_t pf_digest = 0, pf_token = 0, pf_counter = 0;
   bool free_recorded[2] = {false, false};
   // photons the next grid build reads: the staging buffers, or caller-owned
   // device buffers registered by fppm_gpu_set_photons_device (zero copy)
@@ -823,8 +824,26 @@ static void use_staging(fppm_gpu_ctx *ctx, int set = 0) {
 // copy stream: the copy waits only until the grid build that last read that
 // set has consumed it (ev_free), and the next grid build waits for the copy
 // (ev_copied).  With pinned host memory the call returns immediately.
-static bool same_photons(const fppm_photons &a, const fppm_photons &b) {
-  return a.pos == b.pos && a.normal == b.normal && a.wi == b.wi && a.power == b.power && a.depth == b.depth;
+// Sampled digest of a host photon batch: every field of up to 4096 records
+// spread evenly over the batch (plus the last one).  fppm_gpu_adopt_photons
+// recomputes it to catch arrays rewritten after fppm_gpu_prefetch_photons.
+static uint64_t photon_digest(const fppm_photons &p, uint32_t n) {
+  uint64_t h = 1469598103934665603ull ^ n;
+  auto mix = [&h](const void *src, size_t bytes) {
+    const unsigned char *b = static_cast<const unsigned char *>(src);
+    for (size_t i = 0; i < bytes; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  if (n == 0) return h;
+  const uint32_t m = std::min<uint32_t>(n, 4096u);
+  for (uint32_t k = 0; k <= m; ++k) {
+    const uint32_t i = k == m ? n - 1 : (uint32_t)(((uint64_t)k * n) / m);
+    mix(p.pos + 3 * (size_t)i, 12);
+    mix(p.normal + 3 * (size_t)i, 12);
+    mix(p.wi + 3 * (size_t)i, 12);
+    mix(p.power + 3 * (size_t)i, 12);
+    mix(p.depth + i, 4);
+  }
+  return h;
 }
 
 // upload n photons into staging set `set` on the copy stream (ev_copied[set])
@@ -835,17 +854,7 @@ static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cud
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (n && (!p->pos || !p->normal || !p->wi || !p->power || !p->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
-  if (kind == cudaMemcpyHostToDevice && ctx->pf_set >= 0 && ctx->pf_n == n && same_photons(ctx->pf_src, *p)) {
-    // adopt the prefetched upload (already enqueued on the copy stream)
-    const int set = ctx->pf_set;
-    ctx->pf_set = -1;
-    ctx->stage_pending = set;
-    ctx->N = n;
-    ctx->grid_valid = false;
-    use_staging(ctx, set);
-    return FPPM_OK;
-  }
-  ctx->pf_set = -1;  // a different batch supersedes the prefetch
+  ctx->pf_set = -1;  // any explicit upload supersedes the prefetch
   const int set = ctx->stage_cur ^ 1;
   int rc = upload_set(ctx, p, n, kind, set);
   if (rc) return rc;
@@ -857,19 +866,40 @@ static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cud
 }
 
 // Next batch into the staging set not holding the current photons, while the
-// current iteration runs; set_photons with the same arrays then adopts it.
-int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n) {
-  if (!ctx || !host) return FPPM_ERR_INVALID_ARGUMENT;
+// current iteration runs; fppm_gpu_adopt_photons(token) makes it current.
+int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n, uint64_t *token) {
+  if (!ctx || !host || !token) return FPPM_ERR_INVALID_ARGUMENT;
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (n && (!host->pos || !host->normal || !host->wi || !host->power || !host->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
   const int set = ctx->stage_cur ^ 1;
   if (ctx->stage_pending == set) return fail(ctx, FPPM_ERR_STATE, "prefetch while the staged batch is unconsumed");
+  ctx->pf_set = -1;
+  const uint64_t digest = photon_digest(*host, n);
   int rc = upload_set(ctx, host, n, cudaMemcpyHostToDevice, set);
   if (rc) return rc;
   ctx->pf_set = set;
   ctx->pf_src = *host;
   ctx->pf_n = n;
+  ctx->pf_digest = digest;
+  ctx->pf_token = ++ctx->pf_counter;
+  *token = ctx->pf_token;
+  return FPPM_OK;
+}
+
+int fppm_gpu_adopt_photons(fppm_gpu_ctx *ctx, uint64_t token) {
+  if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if (ctx->pf_set < 0 || token == 0 || token != ctx->pf_token)
+    return fail(ctx, FPPM_ERR_STATE, "no pending prefetch with this token (superseded or already adopted)");
+  const int set = ctx->pf_set;
+  ctx->pf_set = -1;
+  if (photon_digest(ctx->pf_src, ctx->pf_n) != ctx->pf_digest)
+    return fail(ctx, FPPM_ERR_STATE,
+                "prefetched photon arrays changed after fppm_gpu_prefetch_photons; upload them with fppm_gpu_set_photons");
+  ctx->stage_pending = set;
+  ctx->N = ctx->pf_n;
+  ctx->grid_valid = false;
+  use_staging(ctx, set);
   return FPPM_OK;
 }
 
