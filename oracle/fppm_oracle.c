@@ -684,8 +684,9 @@ static void process_hit(worker_t *w, size_t slot) {
    * without observation (integrator.cpp:483-488). */
   int tested = 0, rejected = 0;
   double stat = 0, critical = 0;
-  if (gathered && cfg->policy == 2) {
-    /* schedule_end_iteration (gather.cpp:138-144): fixed SPPM schedule */
+  if (cfg->policy == 2) {
+    /* schedule_end_iteration (gather.cpp:138-144) for every region, gathered
+     * or not: the global SPPM / VCM radius (integrator.cpp:159-164, 213-217) */
     reg->radius = orc_schedule_radius(reg->initial_radius, cfg->alpha, w->iteration + 1);
     ++reg->t;
   } else if (gathered) {

@@ -433,7 +433,10 @@ static int session_iterate(void* sp, uint64_t iteration, const T* ppos, const T*
         }
       }
       RadiusUpdate up;
-      if (gathered) {
+      if (cfg.policy == 2) {
+        // the global schedule moves every region (integrator.cpp:159-164, 213-217)
+        up = region->schedule_end_iteration(iteration);
+      } else if (gathered) {
         // :478-480 (CPPM uses chi2_end_iteration); schedule policy: gather.cpp:138
         up = cfg.policy == 1   ? region->chi2_end_iteration(iteration, cfg.samples_per_iteration)
              : cfg.policy == 2 ? region->schedule_end_iteration(iteration)

@@ -17,6 +17,12 @@ struct fppm_gpu_ctx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // grid records: the fine layout's pack + permute run on gstream, forked
+  // after the grid header / the sort and joined before the next consumer, so
+  // they overlap the sort and the gather's scheduling kernels
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_g_hdr = nullptr, ev_g_sorted = nullptr, ev_g_recs = nullptr;
+  bool recs_pending = false;
   std::string err;
   int G = 0, C = 1;
 
@@ -247,6 +253,18 @@ __global__ void k_fill_regions(double *radius, uint32_t *t, uint32_t H, double r
 }
 
 // grow the F critical table so that every t <= need is covered
+// Orders the context stream after the forked record build (see gstream).
+static int join_recs(fppm_gpu_ctx *ctx) {
+  if (!ctx->recs_pending) return FPPM_OK;
+  ctx->recs_pending = false;
+  FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_g_recs, 0));
+  return FPPM_OK;
+}
+#define JOIN_RECS(ctx)                      \
+  do {                                      \
+    if (int jr_ = join_recs(ctx)) return jr_; \
+  } while (0)
+
 static int ensure_crit(fppm_gpu_ctx *ctx, uint64_t need) {
   const fppm_gpu_config &c = ctx->cfg;
   if (c.policy != FPPM_POLICY_FTEST || c.override_decision != FPPM_OVERRIDE_NONE) {
@@ -530,6 +548,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
 
 int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   if (!ctx) return FPPM_OK;
+  if (ctx->gstream) cudaStreamSynchronize(ctx->gstream);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void *dev[] = {ctx->d_pos, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb, ctx->d_K, ctx->d_eye,
                  ctx->d_gathered, ctx->d_radius, ctx->d_t, ctx->d_st_cnt, ctx->d_st_sum,
@@ -586,6 +605,9 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (ctx->ev_free[i]) cudaEventDestroy(ctx->ev_free[i]);
   }
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  for (cudaEvent_t e : {ctx->ev_g_hdr, ctx->ev_g_sorted, ctx->ev_g_recs})
+    if (e) cudaEventDestroy(e);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   for (auto &pr : ctx->ev_k)
     for (cudaEvent_t e : pr)
       if (e) cudaEventDestroy(e);
@@ -601,15 +623,21 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
 
 int fppm_gpu_synchronize(fppm_gpu_ctx *ctx) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (ctx->cstream) FPPM_CUDA_OK(cudaStreamSynchronize(ctx->cstream));
   FPPM_CUDA_OK(cudaStreamSynchronize(ctx->stream));
   return FPPM_OK;
 }
 
-void *fppm_gpu_stream(fppm_gpu_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+void *fppm_gpu_stream(fppm_gpu_ctx *ctx) {
+  if (!ctx) return nullptr;
+  (void)join_recs(ctx);  // work the caller enqueues follows the record build
+  return (void *)ctx->stream;
+}
 
 int fppm_gpu_device_view_get(fppm_gpu_ctx *ctx, fppm_gpu_device_view *v) {
   if (!ctx || !v) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   v->photon_pos = ctx->d_ppos;
   v->photon_normal = ctx->d_pnrm;
   v->photon_wi = ctx->d_pwi;
@@ -641,6 +669,7 @@ static int finish_hitpoints(fppm_gpu_ctx *ctx, uint32_t n, bool has_gathered) {
 }
 
 static int set_hitpoints(fppm_gpu_ctx *ctx, const fppm_hitpoints *hp, uint32_t n, cudaMemcpyKind kind) {
+  if (ctx) JOIN_RECS(ctx);
   if (!ctx || !hp) return FPPM_ERR_INVALID_ARGUMENT;
   if (n > ctx->cfg.max_hitpoints) return fail(ctx, FPPM_ERR_CAPACITY, "hit points exceed max_hitpoints");
   if (n && (!hp->pos || !hp->normal || !hp->wo || !hp->throughput || !hp->albedo || !hp->eye_depth))
@@ -669,6 +698,7 @@ int fppm_gpu_set_hitpoints_device(fppm_gpu_ctx *ctx, const fppm_hitpoints *dev, 
 
 int fppm_gpu_generate_raster_hitpoints(fppm_gpu_ctx *ctx, uint32_t W) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   const uint64_t n = (uint64_t)W * W;
   if (n > ctx->cfg.max_hitpoints) return fail(ctx, FPPM_ERR_CAPACITY, "raster exceeds max_hitpoints");
   launch_raster_hitpoints(ctx->stream, W, ctx->d_pos, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb,
@@ -679,6 +709,7 @@ int fppm_gpu_generate_raster_hitpoints(fppm_gpu_ctx *ctx, uint32_t W) {
 
 int fppm_gpu_c5_setup(fppm_gpu_ctx *ctx, uint64_t seed, uint32_t n_hitpoints) {
   if (!ctx || n_hitpoints == 0) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   for (void *&p : ctx->c5_mem) {
     if (p) cudaFree(p);
     p = nullptr;
@@ -716,6 +747,7 @@ int fppm_gpu_c5_setup(fppm_gpu_ctx *ctx, uint64_t seed, uint32_t n_hitpoints) {
 
 int fppm_gpu_c5_hitpoints(fppm_gpu_ctx *ctx, uint32_t h0, uint32_t n) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->c5.pos) return fail(ctx, FPPM_ERR_STATE, "c5_hitpoints before c5_setup");
   if ((uint64_t)h0 + n > ctx->c5.H) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "hit point range exceeds C5 set");
   if (n > ctx->cfg.max_hitpoints) return fail(ctx, FPPM_ERR_CAPACITY, "hit points exceed max_hitpoints");
@@ -726,6 +758,7 @@ int fppm_gpu_c5_hitpoints(fppm_gpu_ctx *ctx, uint32_t h0, uint32_t n) {
 
 int fppm_gpu_reset_regions(fppm_gpu_ctx *ctx) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   const size_t H = std::max<uint32_t>(ctx->H, 1), CG = (size_t)ctx->G * ctx->C;
   k_fill_regions<<<(unsigned)((H + 255) / 256), 256, 0, ctx->stream>>>(ctx->d_radius, ctx->d_t, ctx->H,
                                                                      ctx->cfg.initial_radius);
@@ -741,6 +774,7 @@ int fppm_gpu_reset_regions(fppm_gpu_ctx *ctx) {
 int fppm_gpu_get_regions(fppm_gpu_ctx *ctx, double *radius, uint64_t *t, uint64_t *stat_count,
                          double *stat_sum, double *stat_sum_sq) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   const size_t H = ctx->H, CG = (size_t)ctx->G * ctx->C;
   int rc;
   if ((rc = copy_out(ctx, radius, ctx->d_radius, sizeof(double) * H))) return rc;
@@ -758,6 +792,7 @@ int fppm_gpu_set_regions(fppm_gpu_ctx *ctx, const double *radius, const uint64_t
                          const uint64_t *stat_count, const double *stat_sum,
                          const double *stat_sum_sq) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   const size_t H = ctx->H, CG = (size_t)ctx->G * ctx->C;
   cudaStream_t s = ctx->stream;
   if (radius) {
@@ -797,11 +832,13 @@ static int device_max_radius(fppm_gpu_ctx *ctx, double *dst, const uint8_t *gath
 
 int fppm_gpu_max_radius_device(fppm_gpu_ctx *ctx, double *d_r_max) {
   if (!ctx || !d_r_max) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   return device_max_radius(ctx, d_r_max);
 }
 
 int fppm_gpu_max_radius(fppm_gpu_ctx *ctx, double *r_max) {
   if (!ctx || !r_max) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   int rc = device_max_radius(ctx, ctx->d_cell);
   if (rc) return rc;
   FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_cell, ctx->d_cell, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -850,6 +887,7 @@ static uint64_t photon_digest(const fppm_photons &p, uint32_t n) {
 static int upload_set(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cudaMemcpyKind kind, int set);
 
 static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cudaMemcpyKind kind) {
+  if (ctx) JOIN_RECS(ctx);
   if (!ctx || !p) return FPPM_ERR_INVALID_ARGUMENT;
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (n && (!p->pos || !p->normal || !p->wi || !p->power || !p->depth))
@@ -869,6 +907,7 @@ static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cud
 // current iteration runs; fppm_gpu_adopt_photons(token) makes it current.
 int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n, uint64_t *token) {
   if (!ctx || !host || !token) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (n && (!host->pos || !host->normal || !host->wi || !host->power || !host->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
@@ -889,6 +928,7 @@ int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint3
 
 int fppm_gpu_adopt_photons(fppm_gpu_ctx *ctx, uint64_t token) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (ctx->pf_set < 0 || token == 0 || token != ctx->pf_token)
     return fail(ctx, FPPM_ERR_STATE, "no pending prefetch with this token (superseded or already adopted)");
   const int set = ctx->pf_set;
@@ -937,6 +977,7 @@ int fppm_gpu_set_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n
 // must stay valid and unchanged until the next build_grid has been issued.
 int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint32_t n) {
   if (!ctx || !dev) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   if (n && (!dev->pos || !dev->normal || !dev->wi || !dev->power || !dev->depth))
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "null photon array");
@@ -955,6 +996,7 @@ int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint
 int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed, uint64_t iteration,
                               uint64_t begin, uint32_t n) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2 && workload != FPPM_WORKLOAD_C5)
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
   if (workload == FPPM_WORKLOAD_C5 && !ctx->c5.pos) return fail(ctx, FPPM_ERR_STATE, "C5 photons before c5_setup");
@@ -983,6 +1025,7 @@ int fppm_gpu_generate_photons_to(fppm_gpu_ctx *ctx, int32_t workload, uint64_t s
                                  uint64_t iteration, uint64_t begin, uint32_t n,
                                  const fppm_photons *d) {
   if (!ctx || !d) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (workload != FPPM_WORKLOAD_C1 && workload != FPPM_WORKLOAD_C2 && workload != FPPM_WORKLOAD_C5)
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown workload");
   if (n && (!d->pos || !d->normal || !d->wi || !d->power || !d->depth))
@@ -1006,6 +1049,7 @@ int fppm_gpu_generate_photons_to(fppm_gpu_ctx *ctx, int32_t workload, uint64_t s
 int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi, float *power,
                          uint32_t *depth) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->in_pos) use_staging(ctx);
   if (ctx->stage_pending >= 0)
     FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[ctx->stage_pending], 0));
@@ -1024,6 +1068,7 @@ int fppm_gpu_get_photons(fppm_gpu_ctx *ctx, float *pos, float *normal, float *wi
 // S_req > 1 asks for the fine (slab) table when the photon set allows it.
 static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, const double *d_cell_in = nullptr) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   cudaStream_t s = ctx->stream;
   ctx->grid_valid = false;
   ctx->grid_explicit = cell_size > 0.0 || d_cell_in != nullptr;
@@ -1063,13 +1108,31 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, 
     ctx->cell_cap = cap;
   }
   const bool fine_layout = effective_variant(ctx, g.S) == 4;
-  launch_dense_keys(s, ctx->in_pos, ctx->N, ctx->d_hdr, ctx->sort.keys_a, ctx->sort.vals_a, ctx->sms);
-  if (fine_layout && ctx->recs.pack)
-    launch_pack_fine(s, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow, ctx->in_depth, ctx->N, ctx->d_hdr,
+  // the fine layout's 48/64-B records (pack: needs only the header; permute:
+  // needs the sort) are built on gstream, overlapping the key sort here and
+  // the gather's scheduling kernels; the next consumer joins (join_recs)
+  const bool fork = fine_layout && ctx->recs.pack != nullptr && ctx->N > 0;
+  if (fork && !ctx->gstream) {
+    FPPM_CUDA_OK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+    FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_g_hdr, cudaEventDisableTiming));
+    FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_g_sorted, cudaEventDisableTiming));
+    FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_g_recs, cudaEventDisableTiming));
+  }
+  cudaStream_t rs = fork ? ctx->gstream : s;
+  if (fork) {
+    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_g_hdr, s));
+    FPPM_CUDA_OK(cudaStreamWaitEvent(rs, ctx->ev_g_hdr, 0));
+    launch_pack_fine(rs, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow, ctx->in_depth, ctx->N, ctx->d_hdr,
                      ctx->cfg.normal_guard_cos, ctx->recs.pack, ctx->sms);
+  }
+  launch_dense_keys(s, ctx->in_pos, ctx->N, ctx->d_hdr, ctx->sort.keys_a, ctx->sort.vals_a, ctx->sms);
   FPPM_CUDA_OK(radix_sort_pairs(s, ctx->sort, ctx->N, g.key_bits, &ctx->d_skeys, &ctx->d_order));
+  if (fork) {
+    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_g_sorted, s));
+    FPPM_CUDA_OK(cudaStreamWaitEvent(rs, ctx->ev_g_sorted, 0));
+  }
   launch_cell_start(s, ctx->d_skeys, ctx->N, ctx->d_hdr, ctx->d_cell_start, g.ncells, ctx->sms);
-  launch_permute(s, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,
+  launch_permute(rs, ctx->d_order, ctx->N, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow,
                  ctx->in_depth, ctx->recs, fine_layout, ctx->d_hdr, ctx->sms);
   if (ctx->cfg.vcm_plus)
     launch_permute_f64x3(s, ctx->d_order, ctx->N, ctx->d_pmis_in[0], ctx->d_pmis_in[1], ctx->d_pmis_in[2],
@@ -1084,9 +1147,13 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, 
       ctx->grid_set = ctx->stage_cur;
       ctx->free_recorded[ctx->stage_cur] = false;
     } else {
-      FPPM_CUDA_OK(cudaEventRecord(ctx->ev_free[ctx->stage_cur], s));
+      FPPM_CUDA_OK(cudaEventRecord(ctx->ev_free[ctx->stage_cur], rs));  // after pack, dense_keys and the sort
       ctx->free_recorded[ctx->stage_cur] = true;
     }
+  }
+  if (fork) {
+    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_g_recs, rs));
+    ctx->recs_pending = true;
   }
   ctx->grid_valid = true;
   return FPPM_OK;
@@ -1121,6 +1188,7 @@ static int ensure_reference_cells(fppm_gpu_ctx *ctx) {
 int fppm_gpu_export_grid(fppm_gpu_ctx *ctx, uint64_t *keys, uint32_t *begin, uint32_t *end,
                          uint32_t *order, uint64_t *ncells) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "grid not built");
   if (int rc = ensure_reference_cells(ctx)) return rc;
   const uint32_t n = ctx->N;
@@ -1154,6 +1222,7 @@ int fppm_gpu_export_grid(fppm_gpu_ctx *ctx, uint64_t *keys, uint32_t *begin, uin
 int fppm_gpu_query_ball(fppm_gpu_ctx *ctx, const double *centers, const double *radii, uint32_t nq,
                         uint64_t *offsets, uint32_t *indices, uint64_t cap, uint64_t *total) {
   if (!ctx || (nq && (!centers || !radii || !offsets))) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->grid_valid) return fail(ctx, FPPM_ERR_STATE, "grid not built");
   if (int rc = ensure_reference_cells(ctx)) return rc;
   const GridHeader g = *ctx->h_hdr;
@@ -1309,6 +1378,7 @@ int fppm_gpu_gather_deltas(fppm_gpu_ctx *ctx, uint64_t iteration, double *d_rows
 int fppm_gpu_apply_deltas(fppm_gpu_ctx *ctx, uint64_t iteration, uint32_t h0, uint32_t n,
                           const double *d_rows, fppm_gpu_iter_out *out, fppm_gpu_summary *summary) {
   if (!ctx || (n && !d_rows)) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if ((uint64_t)h0 + n > ctx->H) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "apply range exceeds hit points");
   int rc = ensure_crit(ctx, ctx->end_calls + 2);
   if (rc) return rc;
@@ -1361,6 +1431,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
   // auto: the fine kernel on slab (planar) grids, the thread-per-hit-point
   // kernel on 3D grids (S = 1: a few hit points per cell)
   const int var = effective_variant(ctx, ctx->h_hdr->S);
+  if (var != 4 || !ctx->H) JOIN_RECS(ctx);
   if (ctx->H && (var == 1 || var == 5)) {
     if (var == 1) {
       if ((rc = kernel_event(ctx, 0))) return rc;
@@ -1466,6 +1537,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       F.hp_map = S.hp_map;
       F.total_items = S.item_base + nb;
       T.desc = nullptr;
+      JOIN_RECS(ctx);  // the records built on gstream
       if ((rc = kernel_event(ctx, 0))) return rc;
       FPPM_CUDA_OK(launch_gather_fine(s, A, F, ctx->C, ctx->sms, g.lean != 0u));
       if ((rc = kernel_event(ctx, 1))) return rc;
@@ -1494,6 +1566,7 @@ int fppm_gpu_iterate(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *o
 int fppm_gpu_accumulate(fppm_gpu_ctx *ctx, const uint32_t *region, const double *y,
                         const double *value, uint32_t n) {
   if (!ctx || (n && (!region || !y || !value))) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (n == 0) return FPPM_OK;
   const size_t need = (4 + 16 + 24 + 4) * (size_t)n + 64;
   FPPM_CUDA_OK(ensure_scratch(ctx, need));
@@ -1524,6 +1597,7 @@ int fppm_gpu_accumulate(fppm_gpu_ctx *ctx, const uint32_t *region, const double 
 
 int fppm_gpu_set_samples_per_iteration(fppm_gpu_ctx *ctx, uint64_t samples_per_iteration) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (samples_per_iteration == ctx->cfg.samples_per_iteration) return FPPM_OK;
   ctx->cfg.samples_per_iteration = samples_per_iteration;
   ctx->crit.clear();  // F_c depends on m = t * J
@@ -1532,6 +1606,7 @@ int fppm_gpu_set_samples_per_iteration(fppm_gpu_ctx *ctx, uint64_t samples_per_i
 
 int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out *out) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   int rc = ensure_crit(ctx, ctx->end_calls + 2);
   if (rc) return rc;
   const bool snap = out && (out->stat_count || out->stat_sum || out->stat_sum_sq);
@@ -1553,6 +1628,7 @@ int fppm_gpu_end_iteration(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_
 
 int fppm_gpu_set_policy(fppm_gpu_ctx *ctx, int32_t policy) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (policy < FPPM_POLICY_FTEST || policy > FPPM_POLICY_SCHEDULE)
     return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "unknown end-of-iteration policy");
   if (policy == ctx->cfg.policy) return FPPM_OK;
@@ -1585,6 +1661,7 @@ uint64_t fppm_gpu_kernel_launches(void) { return g_kernel_launches.load(); }
 
 int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *sc) {
   if (!ctx || !sc) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   const uint32_t nm = sc->n_materials, np = sc->n_primitives, ne = sc->n_emitters;
   if ((nm && (!sc->material_kind || !sc->material_rgb || !sc->material_ior)) ||
       (np && (!sc->shape_kind || !sc->shape || !sc->shape_material)) ||
@@ -1636,6 +1713,7 @@ int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *sc) {
 int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t n_paths,
                            uint32_t max_depth, double mis_radius, uint32_t *n_photons) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->has_scene) return fail(ctx, FPPM_ERR_STATE, "trace_photons before set_scene");
   cudaStream_t s = ctx->stream;
   const uint32_t depth = max_depth > 0 ? max_depth - 1 : 0;  // light_phase: max_depth - 1
@@ -1746,6 +1824,7 @@ static void vcross(const double a[3], const double b[3], double o[3]) {
 
 int fppm_gpu_set_camera(fppm_gpu_ctx *ctx, const fppm_camera *c) {
   if (!ctx || !c) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (c->width < 1 || c->height < 1) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "camera resolution must be >= 1");
   const uint64_t npix = (uint64_t)c->width * (uint64_t)c->height;
   if (npix > ctx->cfg.max_hitpoints) return fail(ctx, FPPM_ERR_CAPACITY, "camera pixels exceed max_hitpoints");
@@ -1777,6 +1856,7 @@ int fppm_gpu_set_camera(fppm_gpu_ctx *ctx, const fppm_camera *c) {
 
 int fppm_gpu_trace_eye(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->has_scene || !ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "trace_eye needs set_scene and set_camera");
   EyeArgs E;
   E.sc = ctx->scene;
@@ -1803,6 +1883,7 @@ int fppm_gpu_trace_eye(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration) {
 int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t light_paths,
                         uint32_t max_depth, uint32_t *n_photons) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->cfg.vcm_plus) return fail(ctx, FPPM_ERR_STATE, "render_vcm needs a vcm_plus context");
   if (!ctx->has_scene || !ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "render_vcm needs set_scene and set_camera");
   if (max_depth < 1 || max_depth > kMaxBidirDepth)
@@ -1922,6 +2003,7 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
 
 int fppm_gpu_get_hitpoints(fppm_gpu_ctx *ctx, fppm_hitpoints *o, double *emitted) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   const size_t H = ctx->H, b3 = sizeof(double3) * H;
   int rc;
   if (o) {
@@ -1943,6 +2025,7 @@ int fppm_gpu_get_hitpoints(fppm_gpu_ctx *ctx, fppm_hitpoints *o, double *emitted
 
 int fppm_gpu_film_add(fppm_gpu_ctx *ctx) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "film_add before set_camera");
   const uint32_t npix = (uint32_t)((uint64_t)ctx->cam.width * ctx->cam.height);
   if (npix != ctx->H) return fail(ctx, FPPM_ERR_STATE, "film_add: hit points are not the camera's pixels");
@@ -1954,6 +2037,7 @@ int fppm_gpu_film_add(fppm_gpu_ctx *ctx) {
 
 int fppm_gpu_film_mean(fppm_gpu_ctx *ctx, double *rgb, uint64_t *iterations) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "film_mean before set_camera");
   const uint32_t npix = (uint32_t)((uint64_t)ctx->cam.width * ctx->cam.height);
   if (iterations) *iterations = ctx->film_iters;
@@ -1970,6 +2054,7 @@ int fppm_gpu_film_mean(fppm_gpu_ctx *ctx, double *rgb, uint64_t *iterations) {
 
 int fppm_gpu_film_splits(fppm_gpu_ctx *ctx, double *vc, double *vm) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->has_camera) return fail(ctx, FPPM_ERR_STATE, "film_splits before set_camera");
   const size_t npix = (size_t)ctx->cam.width * ctx->cam.height;
   std::vector<double2> h(npix);
@@ -1985,6 +2070,7 @@ int fppm_gpu_film_splits(fppm_gpu_ctx *ctx, double *vc, double *vm) {
 
 int fppm_gpu_get_photon_mis(fppm_gpu_ctx *ctx, double *d_vcm, double *d_vm, double *cont) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->cfg.vcm_plus || !ctx->d_pmis_in[0]) return fail(ctx, FPPM_ERR_STATE, "context is not vcm_plus");
   double *dst[3] = {d_vcm, d_vm, cont};
   for (int i = 0; i < 3; ++i)
@@ -1997,6 +2083,7 @@ int fppm_gpu_get_photon_mis(fppm_gpu_ctx *ctx, double *d_vcm, double *d_vm, doub
 
 int fppm_gpu_set_hitpoint_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const double *d_vm, uint32_t n) {
   if (!ctx || (n && (!d_vcm || !d_vm))) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->cfg.vcm_plus) return fail(ctx, FPPM_ERR_STATE, "MIS partials need vcm_plus");
   if (n != ctx->H) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "one MIS pair per hit point");
   std::vector<double2> v(n);
@@ -2010,6 +2097,7 @@ int fppm_gpu_set_hitpoint_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const doub
 int fppm_gpu_set_photon_mis(fppm_gpu_ctx *ctx, const double *d_vcm, const double *d_vm, const double *cont,
                             uint32_t n) {
   if (!ctx || (n && (!d_vcm || !d_vm || !cont))) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
   if (!ctx->cfg.vcm_plus) return fail(ctx, FPPM_ERR_STATE, "MIS partials need vcm_plus");
   if (n > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
   const double *src[3] = {d_vcm, d_vm, cont};

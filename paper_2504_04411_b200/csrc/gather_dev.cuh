@@ -527,9 +527,10 @@ static __device__ __forceinline__ void finalize_hit(const GatherArgs &A, uint32_
   } else if (A.end.policy == FPPM_POLICY_SCHEDULE) {
     // the global schedule (SPPM / VCM: one radius for every pixel,
     // integrator.cpp:159-170 radius_now_) moves on whether or not the pixel
-    // gathered
+    // gathered: schedule_end_iteration (gather.cpp:138-144) for every region
     r_new = A.end.sched_next;
     A.radius[h] = r_new;
+    A.t[h] = A.t[h] + 1;
     if (A.snap_cnt)
       for (int i = 0; i < CG; ++i) {
         A.snap_cnt[base + i] = A.st_cnt[base + i];
