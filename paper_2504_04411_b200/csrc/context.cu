@@ -95,6 +95,12 @@ struct fppm_gpu_ctx {
   double2 *q_mis = nullptr;
   unsigned long long q_cap = 0, q_rows_cap = 0;
   fppm_b200::SortScratch q_sort{};  // home-cell order of the merge queries
+  // eye sub-paths between the walk and the vertex loop (BidirArgs::vtx_*)
+  double *v_d = nullptr;
+  int4 *v_i = nullptr;
+  uint32_t *v_n = nullptr;
+  unsigned long long *v_rng = nullptr;
+  unsigned long long v_cap = 0;
 
   // VCM+ merge stage inputs
   double2 *d_eye_mis = nullptr;                                   // [H] {d_vcm, d_vm}
@@ -577,7 +583,8 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     void *bq[] = {ctx->b_pos, ctx->b_sn, ctx->b_wi, ctx->b_thr, ctx->b_mis, ctx->b_mat, ctx->d_splat,
                   ctx->q_sort.keys_a, ctx->q_sort.vals_a, ctx->q_sort.keys_b, ctx->q_sort.vals_b, ctx->q_sort.hist,
                   ctx->q_pos, ctx->q_nrm, ctx->q_wo, ctx->q_thr, ctx->q_alb, ctx->q_K, ctx->q_eye,
-                  ctx->q_gathered, ctx->q_radius, ctx->q_rows, ctx->q_mis};
+                  ctx->q_gathered, ctx->q_radius, ctx->q_rows, ctx->q_mis, ctx->v_d, ctx->v_i, ctx->v_n,
+                  ctx->v_rng};
     for (void *p : bq)
       if (p) cudaFree(p);
   }
@@ -1163,7 +1170,9 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, 
 // back to reference cells on demand (ensure_reference_cells).
 static uint32_t requested_S(const fppm_gpu_ctx *ctx) {
   const int v = gather_variant(ctx);
-  return v == 4 ? kFineS : (v == 5 ? 2u : 1u);
+  uint32_t s3 = 2u;
+  if (const char *e = std::getenv("FPPM_3D_S")) s3 = (uint32_t)std::atoi(e) == 1 ? 1u : 2u;  // measurement knob
+  return v == 4 ? kFineS : (v == 5 ? s3 : 1u);
 }
 
 int fppm_gpu_build_grid_device(fppm_gpu_ctx *ctx, const double *d_cell) {
@@ -1176,7 +1185,8 @@ int fppm_gpu_build_grid(fppm_gpu_ctx *ctx, double cell_size) {
   // the fine kernel asks for slab fine cells (falling back to 3D fine cells
   // S = 2 or reference cells), the 3D kernel for S = 2 where the table fits
   const int v = gather_variant(ctx);
-  return build_grid_impl(ctx, cell_size, v == 4 ? kFineS : (v == 5 ? 2u : 1u));
+  (void)v;
+  return build_grid_impl(ctx, cell_size, requested_S(ctx));
 }
 
 // query_ball / export need the reference-cell table
@@ -1917,6 +1927,20 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
     FPPM_CUDA_OK(dalloc(&ctx->q_sort.hist, radix_hist_entries((uint32_t)nqt)));
     ctx->q_cap = nqt;
   }
+  const unsigned long long nvt = (unsigned long long)npix * max_depth;  // eye vertices
+  if (nvt > ctx->v_cap) {
+    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    void *vp[] = {ctx->v_d, ctx->v_i, ctx->v_n, ctx->v_rng};
+    for (void *p : vp)
+      if (p) cudaFree(p);
+    ctx->v_d = nullptr; ctx->v_i = nullptr; ctx->v_n = nullptr; ctx->v_rng = nullptr;
+    ctx->v_cap = 0;
+    FPPM_CUDA_OK(dalloc(&ctx->v_d, 16 * nvt));
+    FPPM_CUDA_OK(dalloc(&ctx->v_i, nvt));
+    FPPM_CUDA_OK(dalloc(&ctx->v_n, std::max<uint32_t>(npix, 1)));
+    FPPM_CUDA_OK(dalloc(&ctx->v_rng, std::max<uint32_t>(npix, 1)));
+    ctx->v_cap = nvt;
+  }
   if (nqt * stride > ctx->q_rows_cap) {
     if (ctx->q_rows) cudaFree(ctx->q_rows);
     ctx->q_rows = nullptr;
@@ -1955,6 +1979,7 @@ int fppm_gpu_render_vcm(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, ui
   B.q_pos = ctx->q_pos; B.q_nrm = ctx->q_nrm; B.q_wo = ctx->q_wo; B.q_thr = ctx->q_thr; B.q_alb = ctx->q_alb;
   B.q_eye = ctx->q_eye; B.q_gathered = ctx->q_gathered; B.q_radius = ctx->q_radius; B.q_mis = ctx->q_mis;
   B.splat = ctx->d_splat;
+  B.vtx_d = ctx->v_d; B.vtx_i = ctx->v_i; B.vtx_n = ctx->v_n; B.vtx_rng = ctx->v_rng;
   if (light_paths > 0 && B.light_depth > 0) {
     FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_splat, 0, sizeof(double3) * npix, s));
     FPPM_CUDA_OK(launch_light_splat(s, B, ctx->scene_mem[8], ctx->sms));

@@ -241,12 +241,11 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather_test(const GatherArgs
 // Neighbouring threads hold nearby hit points (cell order), so their photon
 // records share L1/L2 lines.
 constexpr int kSparseThreads = 128;
-#ifndef FPPM_SPARSE_U
-#define FPPM_SPARSE_U 4
-#endif
-constexpr int kSparseU = FPPM_SPARSE_U;
-
-template <int GMAX, int CH>
+// Candidates per step (U): 4 for the FPPM value, whose record loads then
+// overlap; 1 for the VCM+ value, whose MIS weight makes the unrolled body
+// outgrow the instruction cache (measured on C3 / C4: 3.45 vs 4.04 ms and
+// 2.98 vs 5.23 ms per iteration's gathers).
+template <int GMAX, int CH, int kSparseU>
 #ifndef FPPM_SPARSE_MINB
 #define FPPM_SPARSE_MINB 4
 #endif
@@ -374,24 +373,31 @@ size_t thread_smem_bytes(int G, int C) {
   return sizeof(HitX) * kSparseThreads + (size_t)kSparseThreads * (16 * (size_t)G * C + 4 * (size_t)G);
 }
 
-template <int GMAX, int CH>
-static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, double *rows,
-                                     int sms) {
+template <int GMAX, int CH, int U>
+static cudaError_t launch_sparse_u(cudaStream_t s, const GatherArgs &A, const uint32_t *order, double *rows,
+                                   int sms) {
   const int G = A.na * A.ns;
   const size_t smem = thread_smem_bytes(G, CH);
-  cudaError_t e = cudaFuncSetAttribute(k_gather_sparse<GMAX, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_gather_sparse<GMAX, CH, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_sparse<GMAX, CH>, kSparseThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_sparse<GMAX, CH, U>, kSparseThreads, smem);
   if (e != cudaSuccess) return e;
   unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1) * 8u;
   const unsigned need = (A.H + kSparseThreads - 1) / kSparseThreads;
   if (blocks > need) blocks = need;
   if (blocks == 0) blocks = 1;
-  k_gather_sparse<GMAX, CH><<<blocks, kSparseThreads, smem, s>>>(A, order, rows);
+  k_gather_sparse<GMAX, CH, U><<<blocks, kSparseThreads, smem, s>>>(A, order, rows);
   note_launches(1);
   return cudaGetLastError();
+}
+
+template <int GMAX, int CH>
+static cudaError_t launch_sparse_one(cudaStream_t s, const GatherArgs &A, const uint32_t *order, double *rows,
+                                     int sms) {
+  return A.vcm ? launch_sparse_u<GMAX, CH, 1>(s, A, order, rows, sms)
+               : launch_sparse_u<GMAX, CH, 4>(s, A, order, rows, sms);
 }
 
 // ---------------------------------------------------------------- 3D gather

@@ -300,6 +300,12 @@ struct BidirArgs {
   double *q_radius;
   double2 *q_mis;
   double3 *splat;  // light-to-camera splats (atomic adds)
+  // eye sub-paths between k_eye_walk and k_eye_bidir: [16][max_depth][npix]
+  // fp64 fields, [max_depth][npix] int4, vertex counts, RNG states
+  double *vtx_d;
+  int4 *vtx_i;
+  uint32_t *vtx_n;
+  unsigned long long *vtx_rng;
 };
 cudaError_t launch_eye_bidir(cudaStream_t s, const BidirArgs &B, const void *prep, int sms);
 cudaError_t launch_light_splat(cudaStream_t s, const BidirArgs &B, const void *prep, int sms);

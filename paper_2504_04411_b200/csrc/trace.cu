@@ -785,20 +785,64 @@ __device__ __forceinline__ MisC mis_ctx(double beta, double eta) {
   return c;
 }
 
-// Eye vertex of trace_eye_subpath (path.cpp:337-386)
+// Eye vertex of trace_eye_subpath (path.cpp:337-386), as the vertex loop
+// reads it back (cos_exit = dot(gn, wo) replaces the geometric normal, which
+// is only read for emitter hits, integrator.cpp:520-531).
 struct EyeV {
-  DVec pos, sn, gn, wo;
-  double t0, t1, t2;
+  DVec pos, sn, wo;
+  double t0, t1, t2, cos_exit;
   Mis mis;
   int mat, emitter;
   uint32_t depth;
   bool delta, front;
 };
 
+// The eye sub-paths live in HBM between the walk and the vertex loop:
+// [field][vertex k][pixel] fp64 planes (16 fields) and one int4 plane
+// (mat, emitter, depth, flags), so a warp's accesses at the same k are
+// coalesced; a per-thread vertex array would sit in local memory and
+// (at ~2.6 KB per thread) miss L1 on every access.
+constexpr int kEyeVFields = 16;
+__device__ __forceinline__ size_t eyev_at(const BidirArgs &B, int f, uint32_t k, uint32_t px) {
+  return ((size_t)f * B.max_depth + k) * B.npix + px;
+}
+__device__ __forceinline__ void eyev_store(const BidirArgs &B, uint32_t k, uint32_t px, const EyeV &v) {
+  const double f[kEyeVFields] = {v.pos.x, v.pos.y, v.pos.z, v.sn.x, v.sn.y, v.sn.z, v.wo.x, v.wo.y,
+                                 v.wo.z, v.t0, v.t1, v.t2, v.mis.d_vcm, v.mis.d_vc, v.mis.d_vm, v.cos_exit};
+#pragma unroll
+  for (int i = 0; i < kEyeVFields; ++i) B.vtx_d[eyev_at(B, i, k, px)] = f[i];
+  B.vtx_i[(size_t)k * B.npix + px] =
+      make_int4(v.mat, v.emitter, (int)v.depth, (v.delta ? 1 : 0) | (v.front ? 2 : 0));
+}
+__device__ __forceinline__ EyeV eyev_load(const BidirArgs &B, uint32_t k, uint32_t px) {
+  EyeV v;
+  double f[kEyeVFields];
+#pragma unroll
+  for (int i = 0; i < kEyeVFields; ++i) f[i] = B.vtx_d[eyev_at(B, i, k, px)];
+  v.pos = dv(f[0], f[1], f[2]);
+  v.sn = dv(f[3], f[4], f[5]);
+  v.wo = dv(f[6], f[7], f[8]);
+  v.t0 = f[9]; v.t1 = f[10]; v.t2 = f[11];
+  v.mis.d_vcm = f[12]; v.mis.d_vc = f[13]; v.mis.d_vm = f[14];
+  v.cos_exit = f[15];
+  const int4 q = B.vtx_i[(size_t)k * B.npix + px];
+  v.mat = q.x;
+  v.emitter = q.y;
+  v.depth = (uint32_t)q.z;
+  v.delta = (q.w & 1) != 0;
+  v.front = (q.w & 2) != 0;
+  return v;
+}
+
 #ifndef FPPM_EYE_MINB
-#define FPPM_EYE_MINB 8
+#define FPPM_EYE_MINB 4   // walk: 120 registers, no spills
 #endif
-__global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_bidir(const BidirArgs B, const PrimD *__restrict__ prims) {
+#ifndef FPPM_BIDIR_MINB
+#define FPPM_BIDIR_MINB 3  // vertex loop: 166 registers, no spills
+#endif
+// trace_eye_subpath (path.cpp:331-386) for every pixel: the vertices to HBM,
+// the vertex count and the RNG state the vertex loop continues from.
+__global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_walk(const BidirArgs B, const PrimD *__restrict__ prims) {
   __shared__ PrimD P[kMaxTracePrims];
   const TraceScene &sc = B.sc;
   const int np = sc.n_prim;
@@ -806,10 +850,6 @@ __global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_bidir(const BidirArg
   __syncthreads();
   const CamD &cam = B.cam;
   const DVec fwd = dv(cam.fwd[0], cam.fwd[1], cam.fwd[2]);
-  const uint32_t nq = B.max_depth > 1 ? B.max_depth - 1 : 1;
-  const int n_emit = sc.n_emit;
-  const double pick_prob = n_emit ? dd(1.0, (double)n_emit) : 0.0;
-  EyeV V[kMaxBidirDepth];
   for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < B.npix; px += gridDim.x * blockDim.x) {
     Rng rng(B.seed, B.iteration, px, 1ull /* kEyeStream */);
     const double r = B.radius[px];
@@ -822,7 +862,6 @@ __global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_bidir(const BidirArg
                                      ds(sx, dm(0.5, (double)cam.width)))),
                              mul(dv(cam.up[0], cam.up[1], cam.up[2]), ds(dm(0.5, (double)cam.height), sy))));
     DVec o = dv(cam.pos[0], cam.pos[1], cam.pos[2]);
-    // ---- trace_eye_subpath (path.cpp:331-386)
     Mis mis;
     {  // mis_camera_origin (path.cpp:38-43) with camera_pdf_w (path.cpp:144-148)
       const double ct = dot(dir, fwd);
@@ -846,14 +885,15 @@ __global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_bidir(const BidirArg
         mis.d_vm = dm(mis.d_vm, inv_cos);
       }
       const int mk = sc.mat_kind[h.mat];
-      EyeV &v = V[nv++];
+      EyeV v;
       v.pos = h.point;
       v.sn = h.sn;
       {  // fill_hit's geometric normal (gn = front ? outward : -outward)
         const PrimD &pp = P[h.prim];
         const DVec outward = pp.kind == 0 ? mul(sub(h.point, dv(pp.c[0], pp.c[1], pp.c[2])), pp.inv_r)
                                           : dv(pp.on[0], pp.on[1], pp.on[2]);
-        v.gn = h.front ? outward : neg(outward);
+        const DVec gn = h.front ? outward : neg(outward);
+        v.cos_exit = dot(gn, wo);  // emitter_hit_pdfs' cos_exit (path.cpp:320-329)
       }
       v.wo = wo;
       v.t0 = t0; v.t1 = t1; v.t2 = t2;
@@ -863,6 +903,7 @@ __global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_bidir(const BidirArg
       v.front = h.front;
       v.depth = depth;
       v.mis = mis;
+      eyev_store(B, nv++, px, v);
       if (depth == B.max_depth) break;
       const double cos_o = dot(wo, h.sn);
       DVec ndir;
@@ -900,6 +941,29 @@ __global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_bidir(const BidirArg
       o = h.point;
       dir = ndir;
     }
+    B.vtx_n[px] = nv;
+    B.vtx_rng[px] = rng.s;
+  }
+}
+
+// pixel_bidir's vertex loop (integrator.cpp:519-625) over the stored eye
+// sub-path, continuing the pixel's RNG stream where the walk left it.
+__global__ void __launch_bounds__(128, FPPM_BIDIR_MINB) k_eye_bidir(const BidirArgs B, const PrimD *__restrict__ prims) {
+  __shared__ PrimD P[kMaxTracePrims];
+  const TraceScene &sc = B.sc;
+  const int np = sc.n_prim;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) P[i] = prims[i];
+  __syncthreads();
+  const uint32_t nq = B.max_depth > 1 ? B.max_depth - 1 : 1;
+  const int n_emit = sc.n_emit;
+  const double pick_prob = n_emit ? dd(1.0, (double)n_emit) : 0.0;
+  for (uint32_t px = blockIdx.x * blockDim.x + threadIdx.x; px < B.npix; px += gridDim.x * blockDim.x) {
+    Rng rng;
+    rng.s = B.vtx_rng[px];
+    const uint32_t nv = B.vtx_n[px];
+    const double r = B.radius[px];
+    const double eta = dm(dm(dm((double)B.n_vm, kPi), r), r);  // n_vm * kPi * r * r (integrator.cpp:503)
+    const MisC ctx = mis_ctx(B.beta, eta);
     // ---- pixel_bidir's vertex loop (integrator.cpp:519-625)
     double o0 = 0.0, o1 = 0.0, o2 = 0.0;
     const uint32_t lp = px % B.n_paths;
@@ -909,12 +973,12 @@ __global__ void __launch_bounds__(128, FPPM_EYE_MINB) k_eye_bidir(const BidirArg
     uint32_t nsec = 0;
     B.gathered[px] = 0;
     for (uint32_t k = 0; k < nv; ++k) {
-      const EyeV &v = V[k];
+      const EyeV v = eyev_load(B, k, px);
       if (v.emitter >= 0 && v.front) {  // emitted radiance (integrator.cpp:520-531)
         double w = 1.0;
         if (v.depth > 1) {
           // emitter_hit_pdfs (path.cpp:320-329): area emitters, cos_exit = dot(n, -ray_dir)
-          const double cos_exit = dot(v.gn, v.wo);
+          const double cos_exit = v.cos_exit;
           if (cos_exit <= 0.0) {
             w = 0.0;
           } else {
@@ -1176,8 +1240,9 @@ cudaError_t launch_eye_bidir(cudaStream_t s, const BidirArgs &B, const void *pre
   if (B.max_depth > kMaxBidirDepth) return cudaErrorInvalidValue;
   unsigned blocks = (B.npix + 127) / 128;
   if (blocks > (unsigned)sms * 16) blocks = sms * 16;
+  k_eye_walk<<<blocks, 128, 0, s>>>(B, static_cast<const PrimD *>(prep));
   k_eye_bidir<<<blocks, 128, 0, s>>>(B, static_cast<const PrimD *>(prep));
-  note_launches(1);
+  note_launches(2);
   return cudaGetLastError();
 }
 
