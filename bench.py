@@ -486,10 +486,11 @@ class Arm:
         self.stream = torch.cuda.ExternalStream(self.ctx.stream, device=dev)
         self.n_local = wl.photons * (rank + 1) // world - wl.photons * rank // world
         self.begin = wl.photons * rank // world
-        self.full = None
         if mode == "a" and world > 1:
-            self.full = {k: torch.empty((wl.photons,) + shape, dtype=dt, device=dev)
-                         for k, dt, shape in photon_layout()}
+            from paper_2504_04411_b200.distributed import share_stride
+            self.stride = share_stride(wl.photons, world)
+            self.part_n = [wl.photons * (r + 1) // world - wl.photons * r // world for r in range(world)]
+            self.cell = torch.zeros(1, dtype=torch.float64, device=dev)
         if mode == "b":
             from paper_2504_04411_b200.distributed import owner_slice
             self.h0, self.n_own = owner_slice(self.H, rank, world)
@@ -508,21 +509,22 @@ class Arm:
         from paper_2504_04411_b200 import _native as N
         ctx, world = self.ctx, self.world
         if self.mode == "a":
-            src = b
             if world > 1:
+                # one packed all-gather of the shares; r_max all-reduced on the
+                # device; each rank stages only the photons within r_max of its
+                # band's hit points and builds its grid from the device cell
+                from paper_2504_04411_b200.distributed import allgather_packed, device_cell_size, pack_photons
                 with torch.cuda.stream(self.stream):
-                    for k in self.full:
-                        dist.all_gather_into_tensor(self.full[k], b[k])
-                src = self.full
-            N.check(ctx._lib.fppm_gpu_set_photons_device(ctx._h, self.photons(src, 0),
-                                                         self.wl.photons), ctx._h)
-            if world > 1:
-                rl = torch.tensor([ctx.max_radius()], dtype=torch.float64, device=self.dev)
-                dist.all_reduce(rl, op=dist.ReduceOp.MAX)
-                cell = float(rl.item())  # integrator.cpp:159-161 over all ranks
+                    packed = pack_photons(b["photon_pos"], b["photon_normal"], b["photon_wi"], b["photon_power"],
+                                          b["photon_depth"], self.stride)
+                    full = allgather_packed(packed)
+                device_cell_size(ctx, self.cell)
+                ctx.set_photons_packed(full, self.part_n, margin=self.cell)
+                ctx.build_grid_device(self.cell)
             else:
-                cell = 0.0  # device-side max live radius
-            ctx.build_grid(cell)
+                N.check(ctx._lib.fppm_gpu_set_photons_device(ctx._h, self.photons(b, 0),
+                                                             self.wl.photons), ctx._h)
+                ctx.build_grid(0.0)  # device-side max live radius
             N.check(ctx._lib.fppm_gpu_gather_test(ctx._h, it, host_out, None), ctx._h)
             return
         self._step_b(it, b, host_out)

@@ -224,6 +224,18 @@ int fppm_gpu_set_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n
 int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n, uint64_t *token);
 int fppm_gpu_adopt_photons(fppm_gpu_ctx *ctx, uint64_t token);
 int fppm_gpu_set_photons_device(fppm_gpu_ctx *ctx, const fppm_photons *dev, uint32_t n);
+/* Multi-GPU staging (DESIGN.md §7 option A): `parts` photon shares packed as
+ * [part][13][part_stride] 32-bit words (pos xyz, shading normal xyz, wi xyz,
+ * power rgb as fp32 bits, depth), e.g. the output of ONE all-gather of every
+ * rank's packed share; part p holds part_n[p] photons (host array).  They
+ * are staged in part order, and with d_margin (device double, e.g. the
+ * all-reduced r_max the grid is then built with) only photons inside this
+ * context's hit-point bounding box grown by *d_margin are kept -- no photon
+ * beyond r_max of every local hit point can be gathered, so results are
+ * unchanged while the grid build sorts only the band's photons.
+ * *n_kept receives the staged count (the call synchronizes for it). */
+int fppm_gpu_set_photons_packed(fppm_gpu_ctx *ctx, const void *d_packed, uint32_t parts, uint64_t part_stride,
+                                const uint32_t *part_n, const double *d_margin, uint32_t *n_kept);
 /* Canonical synthetic photons [begin, begin+n) of (seed, iteration). */
 int fppm_gpu_generate_photons(fppm_gpu_ctx *ctx, int32_t workload, uint64_t seed,
                               uint64_t iteration, uint64_t begin, uint32_t n);
@@ -343,6 +355,12 @@ int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *scene);
  * receives the deposit count (synchronizes). */
 int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t n_paths,
                            uint32_t max_depth, double mis_radius, uint32_t *n_photons);
+/* A rank's share of the light phase: paths [path0, path0 + n_paths) of the
+ * iteration (RngStream(seed, iteration, path0 + j, kLightStream)), deposits
+ * in path order; concatenating the shares of all ranks in rank order gives
+ * exactly the single-call photon array. */
+int fppm_gpu_trace_photons_range(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t path0,
+                                 uint32_t n_paths, uint32_t max_depth, double mis_radius, uint32_t *n_photons);
 /* ---- eye pass and film (integrator.cpp:407-474, film.cpp:21-50) ---- */
 typedef struct fppm_camera {   /* Camera (scene.hpp:75-82) */
   double position[3];

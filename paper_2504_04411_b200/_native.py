@@ -147,6 +147,8 @@ _SIGS = [
     ("fppm_gpu_build_grid_device", C.c_int, [C.c_void_p, C.c_void_p]),
     ("fppm_gpu_set_photons", C.c_int, [C.c_void_p, C.POINTER(Photons), C.c_uint32]),
     ("fppm_gpu_set_photons_device", C.c_int, [C.c_void_p, C.POINTER(Photons), C.c_uint32]),
+    ("fppm_gpu_set_photons_packed", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p,
+                                              C.c_void_p, C.POINTER(C.c_uint32)]),
     ("fppm_gpu_prefetch_photons", C.c_int, [C.c_void_p, C.POINTER(Photons), C.c_uint32, _u64p]),
     ("fppm_gpu_adopt_photons", C.c_int, [C.c_void_p, C.c_uint64]),
     ("fppm_gpu_generate_photons", C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32]),
@@ -172,6 +174,8 @@ _SIGS = [
     ("fppm_gpu_set_scene", C.c_int, [C.c_void_p, C.c_void_p]),
     ("fppm_gpu_trace_photons", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_double,
                                          C.POINTER(C.c_uint32)]),
+    ("fppm_gpu_trace_photons_range", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
+                                               C.c_uint32, C.c_double, C.POINTER(C.c_uint32)]),
     ("fppm_gpu_get_photon_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fppm_gpu_c5_setup", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
     ("fppm_gpu_c5_hitpoints", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32]),

@@ -311,13 +311,30 @@ class FppmContext:
         del keep
 
     def trace_photons(self, seed: int, iteration: int, n_paths: int, max_depth: int,
-                      mis_radius: float = 0.0) -> int:
+                      mis_radius: float = 0.0, path0: int = 0) -> int:
         """Renderer::light_phase (integrator.cpp:230-265) on the device: traces
-        n_paths light sub-paths and stages their non-delta vertices, in path
-        order, as the photons of the next grid build.  Returns the count."""
+        light sub-paths [path0, path0 + n_paths) and stages their non-delta
+        vertices, in path order, as the photons of the next grid build.
+        Returns the count."""
         n = C.c_uint32()
-        self._check(self._lib.fppm_gpu_trace_photons(self._h, seed, iteration, n_paths, max_depth,
-                                                     mis_radius, C.byref(n)))
+        self._check(self._lib.fppm_gpu_trace_photons_range(self._h, seed, iteration, path0, n_paths, max_depth,
+                                                           mis_radius, C.byref(n)))
+        self.N = n.value
+        return n.value
+
+    def set_photons_packed(self, packed, part_n, margin=None) -> int:
+        """Stage photon shares packed [parts][13][stride] (a uint32/int32/float32
+        CUDA tensor, e.g. one all-gather of pack_photons() outputs), in part
+        order; with `margin` (float64 CUDA tensor of one element) only the
+        photons within the hit points' box grown by it are kept.  Returns the
+        staged count."""
+        parts = len(part_n)
+        stride = packed.shape[-1]
+        arr = (C.c_uint32 * max(parts, 1))(*part_n)
+        n = C.c_uint32()
+        self._check(self._lib.fppm_gpu_set_photons_packed(
+            self._h, C.c_void_p(packed.data_ptr()), parts, stride, arr,
+            C.c_void_p(margin.data_ptr()) if margin is not None else None, C.byref(n)))
         self.N = n.value
         return n.value
 

@@ -98,6 +98,10 @@ struct fppm_gpu_ctx {
   // eye sub-paths between the walk and the vertex loop (BidirArgs::vtx_*)
   double *v_d = nullptr;
   int4 *v_i = nullptr;
+  // fppm_gpu_set_photons_packed: keep flags, destinations, scan scratch, hit-point box
+  uint32_t *d_keep = nullptr, *d_keep_dst = nullptr, *d_keep_scan = nullptr;
+  unsigned long long keep_cap = 0;
+  double *d_hpbox = nullptr;
   uint32_t *v_n = nullptr;
   unsigned long long *v_rng = nullptr;
   unsigned long long v_cap = 0;
@@ -584,7 +588,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
                   ctx->q_sort.keys_a, ctx->q_sort.vals_a, ctx->q_sort.keys_b, ctx->q_sort.vals_b, ctx->q_sort.hist,
                   ctx->q_pos, ctx->q_nrm, ctx->q_wo, ctx->q_thr, ctx->q_alb, ctx->q_K, ctx->q_eye,
                   ctx->q_gathered, ctx->q_radius, ctx->q_rows, ctx->q_mis, ctx->v_d, ctx->v_i, ctx->v_n,
-                  ctx->v_rng};
+                  ctx->v_rng, ctx->d_keep, ctx->d_keep_dst, ctx->d_keep_scan, ctx->d_hpbox};
     for (void *p : bq)
       if (p) cudaFree(p);
   }
@@ -912,6 +916,56 @@ static int set_photons(fppm_gpu_ctx *ctx, const fppm_photons *p, uint32_t n, cud
 
 // Next batch into the staging set not holding the current photons, while the
 // current iteration runs; fppm_gpu_adopt_photons(token) makes it current.
+int fppm_gpu_set_photons_packed(fppm_gpu_ctx *ctx, const void *d_packed, uint32_t parts, uint64_t part_stride,
+                                const uint32_t *part_n, const double *d_margin, uint32_t *n_kept) {
+  if (!ctx || (parts && (!d_packed || !part_n))) return FPPM_ERR_INVALID_ARGUMENT;
+  JOIN_RECS(ctx);
+  if (parts > (uint32_t)kMaxPackedParts) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "more than 64 packed parts");
+  unsigned long long total = 0;
+  for (uint32_t p = 0; p < parts; ++p) {
+    if (part_n[p] > part_stride) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "part count exceeds the part stride");
+    total += part_n[p];
+  }
+  if (total >= 0xffffffffull) return fail(ctx, FPPM_ERR_CAPACITY, "packed photons exceed 2^32 - 1");
+  cudaStream_t s = ctx->stream;
+  if (total + 1 > ctx->keep_cap) {
+    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    void *kp[] = {ctx->d_keep, ctx->d_keep_dst, ctx->d_keep_scan};
+    for (void *p : kp)
+      if (p) cudaFree(p);
+    ctx->d_keep = ctx->d_keep_dst = ctx->d_keep_scan = nullptr;
+    ctx->keep_cap = 0;
+    const unsigned long long cap = std::max<unsigned long long>(total + 1, 4096);
+    FPPM_CUDA_OK(dalloc(&ctx->d_keep, cap));
+    FPPM_CUDA_OK(dalloc(&ctx->d_keep_dst, cap));
+    FPPM_CUDA_OK(dalloc(&ctx->d_keep_scan, cap / 4096 + 8));
+    ctx->keep_cap = cap;
+  }
+  if (!ctx->d_hpbox) FPPM_CUDA_OK(dalloc(&ctx->d_hpbox, 6));
+  const double *box = nullptr;
+  if (d_margin && ctx->H) {
+    FPPM_CUDA_OK(launch_hp_box(s, reinterpret_cast<const double3 *>(ctx->d_pos), ctx->H, ctx->d_hpbox));
+    box = ctx->d_hpbox;
+  }
+  // staging set 0 is rewritten (as by the light phase): wait for an upload into it
+  if ((ctx->stage_pending == 0 || ctx->pf_set == 0) && ctx->ev_copied[0])
+    FPPM_CUDA_OK(cudaStreamWaitEvent(s, ctx->ev_copied[0], 0));
+  ctx->stage_pending = -1;
+  ctx->pf_set = -1;
+  FPPM_CUDA_OK(launch_cull_packed(s, static_cast<const uint32_t *>(d_packed), part_stride, parts, part_n, box,
+                                  d_margin, ctx->d_keep, ctx->d_keep_dst, ctx->d_keep_scan, ctx->d_ppos,
+                                  ctx->d_pnrm, ctx->d_pwi, ctx->d_ppow, ctx->d_pdepth, ctx->sms));
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, ctx->d_keep_dst + total, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  const uint32_t kept = ctx->h_total[0];
+  if (kept > ctx->cfg.max_photons) return fail(ctx, FPPM_ERR_CAPACITY, "photons exceed max_photons");
+  ctx->N = kept;
+  ctx->grid_valid = false;
+  use_staging(ctx);
+  if (n_kept) *n_kept = kept;
+  return FPPM_OK;
+}
+
 int fppm_gpu_prefetch_photons(fppm_gpu_ctx *ctx, const fppm_photons *host, uint32_t n, uint64_t *token) {
   if (!ctx || !host || !token) return FPPM_ERR_INVALID_ARGUMENT;
   JOIN_RECS(ctx);
@@ -1722,7 +1776,13 @@ int fppm_gpu_set_scene(fppm_gpu_ctx *ctx, const fppm_scene *sc) {
 
 int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t n_paths,
                            uint32_t max_depth, double mis_radius, uint32_t *n_photons) {
+  return fppm_gpu_trace_photons_range(ctx, seed, iteration, 0, n_paths, max_depth, mis_radius, n_photons);
+}
+
+int fppm_gpu_trace_photons_range(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration, uint32_t path0,
+                                 uint32_t n_paths, uint32_t max_depth, double mis_radius, uint32_t *n_photons) {
   if (!ctx) return FPPM_ERR_INVALID_ARGUMENT;
+  if ((uint64_t)path0 + n_paths > 0xffffffffull) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "path range overflows");
   JOIN_RECS(ctx);
   if (!ctx->has_scene) return fail(ctx, FPPM_ERR_STATE, "trace_photons before set_scene");
   cudaStream_t s = ctx->stream;
@@ -1767,6 +1827,7 @@ int fppm_gpu_trace_photons(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iteration,
   T.iteration = iteration;
   T.n_paths = n_paths;
   T.light_depth = depth;
+  T.path0 = path0;
   T.n_vm = ctx->cfg.mis_n_vm;
   T.beta = ctx->cfg.mis_beta > 0.0 ? ctx->cfg.mis_beta : 1.0;
   T.eta_vm = eta;

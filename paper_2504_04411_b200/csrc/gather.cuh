@@ -160,6 +160,13 @@ cudaError_t launch_bucket_start(cudaStream_t s, const uint32_t *skeys, uint32_t 
                                 uint32_t *start, int sms);
 cudaError_t launch_exclusive_scan(cudaStream_t s, const uint32_t *in, uint32_t n, uint32_t *tmp,
                                   uint32_t *out);
+// multi-GPU photon staging (shard.cu)
+constexpr int kMaxPackedParts = 64;
+cudaError_t launch_hp_box(cudaStream_t s, const double3 *pos, uint32_t n, double *box);
+cudaError_t launch_cull_packed(cudaStream_t s, const uint32_t *data, unsigned long long stride, uint32_t parts,
+                               const uint32_t *part_n, const double *box, const double *margin, uint32_t *keep,
+                               uint32_t *dst, uint32_t *scan_tmp, float *pos, float *nrm, float *wi, float *pw,
+                               uint32_t *depth, int sms);
 bool fine_supported(int G, int C);
 void fine_caps(int G, int C, uint32_t *cap64, uint32_t *cap48);
 cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
@@ -242,6 +249,7 @@ struct TraceArgs {
   TraceScene sc;
   unsigned long long seed, iteration;
   uint32_t n_paths, light_depth;
+  uint32_t path0;  // global index of path 0 (a rank's share of the light phase)
   int n_vm;
   double beta, eta_vm;
   float *v_pos, *v_nrm, *v_wi, *v_pow;  // per path slots [n_paths][light_depth][3]

@@ -252,7 +252,7 @@ struct PathState {
 __device__ __forceinline__ bool start_path(const TraceArgs &A, const PrimD *P, PathState &s, uint32_t j,
                                            double vcf) {
   const TraceScene &sc = A.sc;
-  s.rng = Rng(A.seed, A.iteration, j, 0ull /* kLightStream */);
+  s.rng = Rng(A.seed, A.iteration, A.path0 + j, 0ull /* kLightStream */);
   s.j = j;
   s.nv = 0;
   s.depth = 1;

@@ -1,9 +1,11 @@
 """CPU, world_size 2 over gloo: the multi-GPU decomposition reproduces the
 single-process result exactly.
 
-Each rank generates its photon share, the shares are all-gathered in rank
-order, the cell size is all-reduced (max), and each rank gathers + tests its
-own band of raster rows.  The oracle stands in for the per-rank device work
+Each rank generates its photon share, packs it ([13][stride] words), the
+packed shares are all-gathered in rank order (one collective), the cell size
+is all-reduced (max), each rank keeps only the photons within the cell of its
+band's hit-point box (the rule fppm_gpu_set_photons_packed applies on the
+device) and gathers + tests its own band of raster rows.  The oracle stands in for the per-rank device work
 (the decomposition logic, not the kernels, is under test here); the per-rank
 results, stitched by rows, must equal one single-process run bit for bit.
 """
@@ -37,8 +39,8 @@ def _worker(rank, world, port, outdir):
     import torch
     import torch.distributed as dist
     from oracle import Oracle
-    from paper_2504_04411_b200.distributed import (allgather_photons, global_cell_size,
-                                                   photon_share, row_band)
+    from paper_2504_04411_b200.distributed import (allgather_packed, global_cell_size, pack_photons,
+                                                   photon_share, row_band, share_stride, unpack_photons)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     orc = Oracle("port")
     hp = orc.gen_raster_hitpoints(W)
@@ -52,10 +54,20 @@ def _worker(rank, world, port, outdir):
         local = {"pos": torch.from_numpy(part["pos"]), "normal": torch.from_numpy(part["nrm"]),
                  "wi": torch.from_numpy(part["wi"]), "power": torch.from_numpy(part["pow"]),
                  "depth": torch.from_numpy(part["depth"].view(np.int32))}
-        full = allgather_photons(local, N)
+        packed = pack_photons(local["pos"], local["normal"], local["wi"], local["power"], local["depth"],
+                              share_stride(N, world))
+        full = unpack_photons(allgather_packed(packed), [photon_share(N, r, world)[1] for r in range(world)])
         ph = {"pos": full["pos"].numpy(), "nrm": full["normal"].numpy(), "wi": full["wi"].numpy(),
               "pow": full["power"].numpy(), "depth": full["depth"].numpy().view(np.uint32)}
+        assert len(ph["pos"]) == N
         cell = global_cell_size(sess.max_radius())
+        # cull to the band's hit-point box grown by the cell (order kept)
+        lo, hi = mine["pos"].min(0) - cell, mine["pos"].max(0) + cell
+        p64 = ph["pos"].astype(np.float64)
+        keep = np.all((p64 >= lo) & (p64 <= hi), axis=1)
+        ph = {k: v[keep] for k, v in ph.items()}
+        if world > 1:
+            assert keep.sum() < N  # the band needs fewer than all photons
         out = sess.iterate(it, ph, cell=cell)
         results.append({k: v for k, v in out.items() if k != "times"})
     np.save(os.path.join(outdir, f"rank{rank}.npy"), results, allow_pickle=True)
