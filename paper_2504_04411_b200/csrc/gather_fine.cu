@@ -1104,6 +1104,20 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
               bulk_g2s(rec2 + (size_t)dst * 16, A.rec2 + src, n * 16u, &s_bar);
               if (!r48) bulk_g2s(rec3 + (size_t)dst * 16, A.rec3 + src, n * 16u, &s_bar);
             }
+#ifndef FPPM_NO_L2_PREFETCH
+            // the item's next window into L2 while this one is processed
+            if (c + 1 < s_desc.c1) {
+              const uint32_t lo2 = lo + cap, hi2 = min(Tu, lo2 + cap);
+              const uint32_t a2 = max(s_desc.pre[p], lo2), e2 = min(s_desc.pre[p + 1], hi2);
+              if (e2 > a2) {
+                const uint32_t src2 = s_desc.src[p] + (a2 - s_desc.pre[p]), n2 = e2 - a2;
+                bulk_prefetch_l2(A.rec0 + src2, n2 * 16u);
+                bulk_prefetch_l2(A.rec1 + src2, n2 * 16u);
+                bulk_prefetch_l2(A.rec2 + src2, n2 * 16u);
+                if (!r48) bulk_prefetch_l2(A.rec3 + src2, n2 * 16u);
+              }
+            }
+#endif
           }
         }
         mbar_wait(&s_bar, phase);
