@@ -23,6 +23,7 @@ struct fppm_gpu_ctx {
   cudaStream_t gstream = nullptr;
   cudaEvent_t ev_g_hdr = nullptr, ev_g_sorted = nullptr, ev_g_recs = nullptr;
   bool recs_pending = false;
+  unsigned long long hp_version = 0;  // bumped whenever hit points change
   std::string err;
   int G = 0, C = 1;
 
@@ -666,6 +667,7 @@ static bool lean_config(const fppm_gpu_ctx *ctx) {
 }
 
 static int finish_hitpoints(fppm_gpu_ctx *ctx, uint32_t n, bool has_gathered) {
+  ++ctx->hp_version;  // cached hit-point bins are stale
   if (!has_gathered) FPPM_CUDA_OK(cudaMemsetAsync(ctx->d_gathered, 1, std::max<uint32_t>(n, 1), ctx->stream));
   FPPM_CUDA_OK(launch_hit_weights(ctx->stream, ctx->d_nrm, ctx->d_wo, ctx->d_thr, ctx->d_alb, n, ctx->d_K));
   if (lean_config(ctx))
@@ -1547,13 +1549,14 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       FPPM_CUDA_OK(dalloc(&S.pbase, cap + 1));
       FPPM_CUDA_OK(dalloc(&S.scan_tmp, cap / 4096 + 8));
       S.bucket_cap = cap;
+      S.bins_valid = false;
     }
     uint32_t nb = 0;
     // the fine-cell tiled kernel (slab grids, G * C <= 24)
     uint32_t cap64 = 0, cap48 = 0;
     fine_caps(ctx->G, ctx->C, &cap64, &cap48);
     FPPM_CUDA_OK(cudaMemsetAsync(S.nonempty, 0, sizeof(uint32_t), s));
-    FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, cap64, cap48, &nb));
+    FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, cap64, cap48, &nb, ctx->hp_version));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
                                  cudaMemcpyDeviceToHost, s));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total + 1, S.pbase + nb, sizeof(uint32_t),

@@ -148,6 +148,14 @@ struct TileSched {
   uint32_t *nonempty;   // device counter: buckets holding hit points
   unsigned long long bucket_cap, item_cap;
   unsigned long long row_cap = 0;  // partial rows allocated
+  // hit-point bins of the last fine schedule (hp_order, hp_start): reused
+  // while the hit points and the grid geometry they were binned on are
+  // unchanged (a static frame whose r_max holds, e.g. C1 / C2)
+  bool bins_valid = false;
+  unsigned long long bins_version = 0;
+  uint32_t bins_H = 0, bins_nb = 0;
+  double bins_inv = 0.0;
+  long long bins_dims[7] = {0, 0, 0, 0, 0, 0, 0};
 };
 
 __host__ __device__ constexpr int partial_size(int gmax, int ch) { return gmax + 2 * ch * gmax + 3; }
@@ -170,7 +178,8 @@ cudaError_t launch_cull_packed(cudaStream_t s, const uint32_t *data, unsigned lo
 bool fine_supported(int G, int C);
 void fine_caps(int G, int C, uint32_t *cap64, uint32_t *cap48);
 cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
-                               int sms, uint32_t cap64, uint32_t cap48, uint32_t *nb_out);
+                               int sms, uint32_t cap64, uint32_t cap48, uint32_t *nb_out,
+                               unsigned long long hp_version);
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
                                 uint32_t cap64, uint32_t cap48);
 size_t fine_acc_doubles(int G, int C);

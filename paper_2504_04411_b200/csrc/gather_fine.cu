@@ -1297,7 +1297,8 @@ void fine_caps(int G, int C, uint32_t *cap64, uint32_t *cap48) {
 }
 
 cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
-                               int sms, uint32_t cap64, uint32_t cap48, uint32_t *nb_out) {
+                               int sms, uint32_t cap64, uint32_t cap48, uint32_t *nb_out,
+                               unsigned long long hp_version) {
   const long long x0 = g.ix0 >> g.shift, y0 = g.iy0 >> g.shift, z0 = g.iz0 >> g.shift;
   const unsigned long long ex = (unsigned long long)(((g.ix0 + g.nx - 1) >> g.shift) - x0 + 3);
   const unsigned long long ey = (unsigned long long)(((g.iy0 + g.ny - 1) >> g.shift) - y0 + 3);
@@ -1306,17 +1307,31 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   if (n_ext + 1 >= 0xffffffffull) return cudaErrorInvalidValue;
   const uint32_t nb = (uint32_t)n_ext + 1;
   *nb_out = nb;
-  k_fine_bin<<<fblocks(A.H, 256, sms, 16), 256, 0, s>>>(A.pos, A.gathered, A.H, A.grid,
-                                                        S.sort.keys_a, S.sort.vals_a);
-  note_launches(1);
-  uint32_t bits = 1;
-  while (bits < 32 && (1ull << bits) < (unsigned long long)nb) ++bits;
-  uint32_t *skeys, *svals;
-  cudaError_t e = radix_sort_pairs(s, S.sort, A.H, bits, &skeys, &svals);
-  if (e != cudaSuccess) return e;
-  S.hp_order = svals;
-  e = launch_bucket_start(s, skeys, A.H, nb, S.hp_start, sms);
-  if (e != cudaSuccess) return e;
+  const long long dims[7] = {g.ix0, g.iy0, g.iz0, g.nx, g.ny, g.nz, (long long)g.shift};
+  bool same = S.bins_valid && S.bins_version == hp_version && S.bins_H == A.H && S.bins_nb == nb &&
+              S.bins_inv == g.inv;
+  for (int k = 0; k < 7 && same; ++k) same = S.bins_dims[k] == dims[k];
+  cudaError_t e = cudaSuccess;
+  if (!same) {
+    S.bins_valid = false;
+    k_fine_bin<<<fblocks(A.H, 256, sms, 16), 256, 0, s>>>(A.pos, A.gathered, A.H, A.grid,
+                                                          S.sort.keys_a, S.sort.vals_a);
+    note_launches(1);
+    uint32_t bits = 1;
+    while (bits < 32 && (1ull << bits) < (unsigned long long)nb) ++bits;
+    uint32_t *skeys, *svals;
+    e = radix_sort_pairs(s, S.sort, A.H, bits, &skeys, &svals);
+    if (e != cudaSuccess) return e;
+    S.hp_order = svals;
+    e = launch_bucket_start(s, skeys, A.H, nb, S.hp_start, sms);
+    if (e != cudaSuccess) return e;
+    S.bins_valid = true;
+    S.bins_version = hp_version;
+    S.bins_H = A.H;
+    S.bins_nb = nb;
+    S.bins_inv = g.inv;
+    for (int k = 0; k < 7; ++k) S.bins_dims[k] = dims[k];
+  }
   // per hit point state in wave order (needed by the window sizing below)
   e = cudaFuncSetAttribute(k_fine_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem);
   if (e != cudaSuccess) return e;

@@ -174,6 +174,7 @@ static inline unsigned blocks_for(unsigned long long n, int threads, int sms, in
 // them in this order so a warp's hit points share candidate records.
 cudaError_t hp_cell_order(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g, int sms,
                           const uint32_t **order) {
+  S.bins_valid = false;  // the sort scratch is reused here
   const unsigned long long n_ext =
       (unsigned long long)(g.nx + 2) * (unsigned long long)(g.ny + 2) * (unsigned long long)(g.nz + 2);
   if (n_ext + 1 >= 0xffffffffull) return cudaErrorInvalidValue;
