@@ -950,7 +950,7 @@ int fppm_gpu_set_photons_packed(fppm_gpu_ctx *ctx, const void *d_packed, uint32_
     box = ctx->d_hpbox;
   }
   // staging set 0 is rewritten (as by the light phase): wait for an upload into it
-  if ((ctx->stage_pending == 0 || ctx->pf_set == 0) && ctx->ev_copied[0])
+  if (ctx->ev_copied[0])  // any earlier upload into set 0 (a superseded one too)
     FPPM_CUDA_OK(cudaStreamWaitEvent(s, ctx->ev_copied[0], 0));
   ctx->stage_pending = -1;
   ctx->pf_set = -1;
@@ -1553,10 +1553,10 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
     }
     uint32_t nb = 0;
     // the fine-cell tiled kernel (slab grids, G * C <= 24)
-    uint32_t cap64 = 0, cap48 = 0;
-    fine_caps(ctx->G, ctx->C, &cap64, &cap48);
+    uint32_t cap64 = 0, cap48 = 0, fsub = 0;
+    fine_caps(ctx->G, ctx->C, g.lean != 0u, &cap64, &cap48, &fsub);
     FPPM_CUDA_OK(cudaMemsetAsync(S.nonempty, 0, sizeof(uint32_t), s));
-    FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, cap64, cap48, &nb, ctx->hp_version));
+    FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, cap64, cap48, fsub, &nb, ctx->hp_version));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
                                  cudaMemcpyDeviceToHost, s));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total + 1, S.pbase + nb, sizeof(uint32_t),
@@ -1594,7 +1594,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
     T.hp_map = S.hp_map;
     T.total_items = S.item_base + nb;
     {
-      FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48));
+      FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48, fsub));
       FineArgs F;
       F.desc = S.fdesc;
       F.hot = static_cast<const FineHot *>(S.fhot);
@@ -1868,7 +1868,7 @@ int fppm_gpu_trace_photons_range(fppm_gpu_ctx *ctx, uint64_t seed, uint64_t iter
   if (total > ctx->cfg.max_photons)
     return fail(ctx, FPPM_ERR_CAPACITY, "traced deposits exceed max_photons");
   // the deposits become the staged photons (set 0) of the next grid build
-  if ((ctx->stage_pending == 0 || ctx->pf_set == 0) && ctx->ev_copied[0])
+  if (ctx->ev_copied[0])  // any earlier upload into set 0 (a superseded one too)
     FPPM_CUDA_OK(cudaStreamWaitEvent(s, ctx->ev_copied[0], 0));
   ctx->stage_pending = -1;
   ctx->pf_set = -1;  // set 0 is rewritten

@@ -176,12 +176,14 @@ cudaError_t launch_cull_packed(cudaStream_t s, const uint32_t *data, unsigned lo
                                uint32_t *dst, uint32_t *scan_tmp, float *pos, float *nrm, float *wi, float *pw,
                                uint32_t *depth, int sms);
 bool fine_supported(int G, int C);
-void fine_caps(int G, int C, uint32_t *cap64, uint32_t *cap48);
+void fine_caps(int G, int C, bool lean, uint32_t *cap64, uint32_t *cap48, uint32_t *fsub);
+bool ring_enabled();
+int ring_buffers();
 cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
-                               int sms, uint32_t cap64, uint32_t cap48, uint32_t *nb_out,
+                               int sms, uint32_t cap64, uint32_t cap48, uint32_t fsub, uint32_t *nb_out,
                                unsigned long long hp_version);
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
-                                uint32_t cap64, uint32_t cap48);
+                                uint32_t cap64, uint32_t cap48, uint32_t fsub);
 size_t fine_acc_doubles(int G, int C);
 cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms, bool lean);
 size_t fine_hot_bytes();

@@ -28,6 +28,8 @@
 // outside the hot loop.  Partials and k_tile_finalize are shared with the
 // tiled kernel.
 #include <climits>
+#include <type_traits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gather.cuh"
@@ -237,12 +239,12 @@ static __device__ __forceinline__ WaveInfo wave_info(const GatherArgs &A, const 
   return W;
 }
 
-// per bucket (one warp each): items (runs of <= kFSub windows of
+// per bucket (one warp each): items (runs of <= fsub windows of
 // ceil(union / chunk)) and partial rows (items x wave size)
 __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
                              const FineHot *__restrict__ hot, const int4 *__restrict__ fbox,
                              uint32_t *__restrict__ items, uint32_t *__restrict__ prows, uint32_t cap64,
-                             uint32_t cap48, uint32_t *__restrict__ nonempty) {
+                             uint32_t cap48, uint32_t fsub, uint32_t *__restrict__ nonempty) {
   const GridHeader g = *A.grid;
   const int lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -256,7 +258,7 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
       const WaveInfo W = wave_info(A, g, hot, fbox, h0 + w * kFWave, n, b + 1 < nb);
       const uint32_t chunk = (W.planar || g.lean) ? cap48 : cap64;
       const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
-      const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
+      const uint32_t nsub = (nwin + fsub - 1) / fsub;
       it += nsub;
       pr += nsub * n;
     }
@@ -271,7 +273,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
                             const uint32_t *__restrict__ hp_order, const FineHot *__restrict__ hot,
                             const int4 *__restrict__ fbox, const uint32_t *__restrict__ item_base,
                             const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
-                            uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48) {
+                            uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48, uint32_t fsub) {
   constexpr int kWarps = 4;  // 128 threads
   constexpr int kWords = (int)(sizeof(FineDesc) / 4);
   __shared__ __align__(16) uint32_t s_d[kWarps][kWords];
@@ -288,7 +290,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
       const WaveInfo W = wave_info(A, g, hot, fbox, lo, n, b + 1 < nb);
       const uint32_t chunk = (W.planar || g.lean) ? cap48 : cap64;
       const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
-      const uint32_t nsub = (nwin + kFSub - 1) / kFSub;
+      const uint32_t nsub = (nwin + fsub - 1) / fsub;
       __syncwarp();
       if (lane < kFMaxPieces) {
         d.src[lane] = lane < W.np ? W.src : 0u;
@@ -312,8 +314,8 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
       __syncwarp();
       for (uint32_t sb = 0; sb < nsub; ++sb, ++item) {
         if (lane == 0) {
-          d.c0 = sb * kFSub;
-          d.c1 = min(nwin, d.c0 + kFSub);
+          d.c0 = sb * fsub;
+          d.c1 = min(nwin, d.c0 + fsub);
           d.pbase = prow + sb * n;
         }
         __syncwarp();
@@ -752,12 +754,11 @@ static __device__ __forceinline__ void lean_add(const LeanPair &q, uint32_t slot
   o.y = da(o.y, dm(v, v));
   sts_f64x2(a, o);
   padd_u32(nib, 1u << q.s4, q.acc);
-  // flux (integrator.cpp:449): fma(x, 1, p) = p + x and fma(x, 0, p) = p
-  // exactly for the finite powers of lean records -- one DFMA per channel
-  const double m = q.acc ? 1.0 : 0.0;
-  p0 = __fma_rn(q.r, m, p0);
-  p1 = __fma_rn(q.g, m, p1);
-  p2 = __fma_rn(q.b, m, p2);
+  // flux (integrator.cpp:449): predicated fp64 adds
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+      "@q add.rn.f64 %0, %0, %4;\n\t@q add.rn.f64 %1, %1, %5;\n\t@q add.rn.f64 %2, %2, %6;\n\t}"
+      : "+d"(p0), "+d"(p1), "+d"(p2)
+      : "r"((uint32_t)q.acc), "d"(q.r), "d"(q.g), "d"(q.b));
 }
 
 // Exact fp64 evaluation of the candidate at window index i of a lean window:
@@ -836,15 +837,20 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
   int j = 0;
   uint32_t e = __shfl_sync(kFull, incl, 0), o = __shfl_sync(kFull, off, 0);
   uint32_t spill = 15;
-  for (uint32_t base = 0; base < total; base += 64) {
-    while (e <= base) {  // warp-uniform: skip runs that ended (incl. empty ones)
-      ++j;
-      e = __shfl_sync(kFull, incl, j);
-      o = __shfl_sync(kFull, off, j);
-    }
+  // one step: candidates v0 = base + lane and v1 = v0 + 32 (TAIL: the last,
+  // partial step -- slots past the end read the staged window, never added)
+  auto step = [&](uint32_t base, auto tail) {
+    constexpr bool TAIL = decltype(tail)::value;
     const uint32_t v0 = base + lane, v1 = v0 + 32u;
     uint32_t i0 = v0 + o, i1 = v1 + o;
-    if (e < base + 64u) {  // a run ends inside this step (warp-uniform)
+    if (e < base + 64u) {  // a run ends before base + 64 (warp-uniform)
+      while (e <= base) {  // skip runs that ended (incl. empty ones)
+        ++j;
+        e = __shfl_sync(kFull, incl, j);
+        o = __shfl_sync(kFull, off, j);
+      }
+      i0 = v0 + o;
+      i1 = v1 + o;
       int k = j;
       uint32_t ek = e;
       while (ek < base + 64u && k + 1 < nruns) {
@@ -855,10 +861,13 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
         ek = __shfl_sync(kFull, incl, k);
       }
     }
-    // slots past the end stay inside the staged window (read, never added)
-    const bool ok0 = v0 < total, ok1 = v1 < total;
-    if (!ok0) i0 = rs;
-    if (!ok1) i1 = rs;
+    bool ok0 = true, ok1 = true;
+    if constexpr (TAIL) {
+      ok0 = v0 < total;
+      ok1 = v1 < total;
+      if (!ok0) i0 = rs;
+      if (!ok1) i1 = rs;
+    }
     if (--spill == 0) {
       lean_spill(c);
       spill = 15;
@@ -867,8 +876,8 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
     const LeanPair q1 = lean_eval<NA>(F, ok1, Wn.r0 + i1 * 16u, d1, d2);
     lean_add(q0, slot_lane, c.n0, p0, p1, p2);
     lean_add(q1, slot_lane, c.n1, p0, p1, p2);
-    const uint32_t m0 = __ballot_sync(kFull, q0.need), m1 = __ballot_sync(kFull, q1.need);
-    if (m0 | m1) {
+    if (__any_sync(kFull, q0.need || q1.need)) {  // banded pairs (rare) go to the exact ring
+      const uint32_t m0 = __ballot_sync(kFull, q0.need), m1 = __ballot_sync(kFull, q1.need);
       if (q0.need) sts_u32(ex + ((st.et + __popc(m0 & lt)) & (kFExact - 1)) * 4u, i0);
       st.et += __popc(m0);
       if (q1.need) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
@@ -876,7 +885,10 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
       while (st.et - st.eh >= 32)
         lean_exact_batch(A, Hs, 32u, ex, slot_lane, c, p0, p1, p2, Wn, st);
     }
-  }
+  };
+  const uint32_t full = total & ~63u;
+  for (uint32_t base = 0; base < full; base += 64) step(base, std::false_type{});
+  if (full < total) step(full, std::true_type{});
   while (st.et != st.eh)
     lean_exact_batch(A, Hs, min(32u, st.et - st.eh), ex, slot_lane, c, p0, p1, p2, Wn, st);
   lean_spill(c);
@@ -939,7 +951,13 @@ static __device__ __forceinline__ void exact_fragment_lean(const GatherArgs &A, 
 // End of a lean fragment: the lane slots reduced in the fixed rotated order
 // of the general path, scaled by K0 / K0^2, counts from the byte words, flux;
 // added to the hit point's partial row [count G | sum G | sum_sq G | power 3].
-template <int GMAX>
+// STORE: acc is the fragment's own row in HBM (ring kernel: one fragment per
+// (hit point, item)), written instead of accumulated.
+template <bool STORE>
+static __device__ __forceinline__ void row_put(double &d, double v) {
+  if constexpr (STORE) d = v; else d += v;
+}
+template <int GMAX, bool STORE = false>
 static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, double K0, const LeanCnt &c,
                                                    double p0, double p1, double p2, double *acc,
                                                    FineState &st) {
@@ -987,17 +1005,17 @@ static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, dou
     st.n_acc += (e02 & 0xffffu) + (e02 >> 16) + (e26 & 0xffffu) + (e26 >> 16) + (o15 & 0xffffu) + (o15 >> 16) +
                 (o37 & 0xffffu) + (o37 >> 16);
   if (lane < NC) {
-    acc[GMAX + lane] += dm(K0, sm);
-    acc[2 * GMAX + lane] += dm(dm(K0, K0), sq);
+    row_put<STORE>(acc[GMAX + lane], dm(K0, sm));
+    row_put<STORE>(acc[2 * GMAX + lane], dm(dm(K0, K0), sq));
   } else if (lane >= 32 - GMAX) {
     const int g = lane - (32 - GMAX);
     const uint32_t w = (g & 1) ? ((g & 2) ? o37 : o15) : ((g & 2) ? e26 : e02);
-    acc[g] += (double)((g & 4) ? (w >> 16) : (w & 0xffffu));
+    row_put<STORE>(acc[g], (double)((g & 4) ? (w >> 16) : (w & 0xffffu)));
   }
   if (lane == 0) {
-    acc[3 * GMAX] += p0;
-    acc[3 * GMAX + 1] += p1;
-    acc[3 * GMAX + 2] += p2;
+    row_put<STORE>(acc[3 * GMAX], p0);
+    row_put<STORE>(acc[3 * GMAX + 1], p1);
+    row_put<STORE>(acc[3 * GMAX + 2], p2);
   }
   __syncwarp();
 }
@@ -1265,6 +1283,244 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
   }
 }
 
+// ------------------------------------------------------------------ ring kernel
+// k_gather_ring: the lean fine gather with its windows in a ring of NB
+// buffers.  k_gather_fine stages one window per CTA, so every window costs
+// the CTA a barrier (warps wait for the one with the longest hit point) plus
+// the TMA latency of the next window (ncu: 15 % + 6 % of the stall samples).
+// Here one CTA per SM (16 warps) owns NB item buffers; an item is ONE window
+// of a wave (schedule with fsub = 1).  Warps walk the items in sequence
+// (position q in buffer q % NB), claiming hit points of each; the last warp
+// to leave position q refills its buffer with position q + NB while the
+// other buffers are consumed: no CTA-wide barrier, loads overlap the gather.
+// Every buffer keeps one item claimed ahead with its descriptor already
+// prefetched by TMA, so a refill issues its record copies at once.  Each
+// (hit point, item) fragment writes its own partial row to HBM;
+// k_tile_finalize sums a hit point's rows in window order, so the result is
+// deterministic and identical to k_gather_fine's.
+constexpr int kRWarps = 16;
+constexpr int kRThreads = kRWarps * kWarp;
+
+template <int GMAX, int NB>
+struct RingLayout {
+  static constexpr int NC = GMAX;  // lean: C = 1
+  static constexpr int PS = partial_size(GMAX, 1);
+  static constexpr size_t kSlotBytes = (size_t)kRWarps * (NC + 1) * 32 * 16;
+  static constexpr size_t kHotBytes = (size_t)kFWave * sizeof(FineHot);
+  static constexpr size_t kStatic = (size_t)kRWarps * kFExact * 4 + 2 * NB * sizeof(FineDesc) + 64 * NB + 64;
+  static constexpr size_t kBudget = (size_t)233472 - 1024 - kStatic - 256;
+  static constexpr uint32_t kCap =
+      (uint32_t)((((kBudget - kSlotBytes - NB * kHotBytes) / NB) / 48) & ~(size_t)31);
+  static constexpr size_t kBufBytes = (size_t)kCap * 48;  // rec0 | rec1 | rec2, 16 B each
+  static constexpr size_t kDynBytes = NB * kBufBytes + kSlotBytes + NB * kHotBytes;
+};
+
+static __device__ __forceinline__ uint32_t atom_add_smem(uint32_t *p, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return r;
+}
+
+template <int NB>
+struct RingShared {
+  FineDesc desc[NB];   // descriptor of the item in buffer b
+  FineDesc pdesc[NB];  // descriptor of buffer b's next item (TMA prefetch)
+  uint64_t full[NB];   // records + hit points of buffer b landed
+  uint64_t dbar[NB];   // pdesc[b] landed
+  uint32_t item[NB], pitem[NB], next[NB], left[NB], dphase[NB];  // dphase: parity of dbar[b]
+};
+
+// Claim an item for buffer b's next turn and prefetch its descriptor (lane 0).
+template <int NB>
+static __device__ __forceinline__ void ring_preclaim(uint32_t b, const GatherArgs &A, const FineArgs &T,
+                                                     uint32_t total_items, RingShared<NB> &R) {
+  const uint32_t item = atomicAdd(A.work, 1u);
+  R.pitem[b] = item;
+  if (item < total_items) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&R.dbar[b], (uint32_t)sizeof(FineDesc));
+    bulk_g2s(&R.pdesc[b], T.desc + item, (uint32_t)sizeof(FineDesc), &R.dbar[b]);
+  }
+}
+
+// One warp: put buffer b's pre-claimed item into b (descriptor from pdesc,
+// hit points + record pieces by TMA, completing on full[b]), then pre-claim
+// the item for b's following turn.  An item past the end arrives without
+// data: the consumers read R.item and skip it.
+template <int GMAX, int NB>
+static __device__ __forceinline__ void ring_fill(uint32_t b, const GatherArgs &A, const FineArgs &T,
+                                                 uint32_t total_items, RingShared<NB> &R,
+                                                 unsigned char *buf, FineHot *hot) {
+  using Lay = RingLayout<GMAX, NB>;
+  const int lane = threadIdx.x & 31;
+  const uint32_t item = R.pitem[b];
+  if (lane == 0) {
+    R.item[b] = item;
+    R.next[b] = 0;
+    R.left[b] = 0;
+  }
+  if (item < total_items) {
+    mbar_wait(&R.dbar[b], R.dphase[b]);
+    constexpr int kWords = (int)(sizeof(FineDesc) / 4);
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(&R.pdesc[b]);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(&R.desc[b]);
+    for (int k = lane; k < kWords; k += 32) dst[k] = src[k];
+    __syncwarp();
+    const FineDesc &D = R.desc[b];
+    const uint32_t Tu = D.pre[kFMaxPieces];
+    const uint32_t lo = D.c0 * Lay::kCap, hi = min(Tu, lo + Lay::kCap);
+    const uint32_t hot_bytes = D.hp_n * (uint32_t)sizeof(FineHot);
+    if (lane == 0) {
+      R.dphase[b] ^= 1u;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&R.full[b], (hi - lo) * 48u + hot_bytes);
+    }
+    __syncwarp();
+    if (lane == 31) bulk_g2s(hot, T.hot + D.hp_lo, hot_bytes, &R.full[b]);
+    if ((uint32_t)lane < D.npieces) {
+      const uint32_t p = lane;
+      const uint32_t a = max(D.pre[p], lo), e = min(D.pre[p + 1], hi);
+      if (e > a) {
+        const uint32_t sp = D.src[p] + (a - D.pre[p]), dp = a - lo, n = e - a;
+        bulk_g2s(buf + (size_t)dp * 16, A.rec0 + sp, n * 16u, &R.full[b]);
+        bulk_g2s(buf + (size_t)(Lay::kCap + dp) * 16, A.rec1 + sp, n * 16u, &R.full[b]);
+        bulk_g2s(buf + (size_t)(2 * Lay::kCap + dp) * 16, A.rec2 + sp, n * 16u, &R.full[b]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ring_preclaim<NB>(b, A, T, total_items, R);
+  } else {
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(&R.full[b], 0u);  // items past the end stay past the end
+  }
+  __syncwarp();
+}
+
+template <int GMAX, int NB>
+__global__ void __launch_bounds__(kRThreads, 1) k_gather_ring(const GatherArgs A, const FineArgs T) {
+  using Lay = RingLayout<GMAX, NB>;
+  constexpr int NC = Lay::NC, PS = Lay::PS, NA = GMAX / 4;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double *s_slots = reinterpret_cast<double *>(smem_raw + NB * Lay::kBufBytes);
+  FineHot *s_hot = reinterpret_cast<FineHot *>(smem_raw + NB * Lay::kBufBytes + Lay::kSlotBytes);
+  __shared__ uint32_t s_ex[kRWarps][kFExact];
+  __shared__ __align__(16) RingShared<NB> R;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *slots_p = s_slots + (size_t)warp * (NC + 1) * 32 * 2;
+  for (int i = lane; i < (NC + 1) * 32 * 2; i += 32) slots_p[i] = 0.0;
+  const uint32_t slots = smem_u32(slots_p);
+  const uint32_t exa = smem_u32(&s_ex[warp][0]);
+  const uint32_t total_items = *T.total_items;
+  const GridHeader g = *A.grid;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&R.full[b], 1);
+      mbar_init(&R.dbar[b], 1);
+      R.dphase[b] = 0;
+    }
+    fence_mbar_init();
+    for (int b = 0; b < NB; ++b) ring_preclaim<NB>(b, A, T, total_items, R);  // positions 0 .. NB - 1
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int b = 0; b < NB; ++b)
+      ring_fill<GMAX, NB>(b, A, T, total_items, R, smem_raw + b * Lay::kBufBytes, s_hot + b * kFWave);
+  FineState st = {0, 0, 0, 0, 0, 0, 0, 0};
+
+  uint32_t dead = 0;  // consecutive positions past the end
+  for (uint32_t q = 0;; ++q) {
+    const uint32_t b = q % NB;
+    mbar_wait(&R.full[b], (q / NB) & 1u);
+    const uint32_t item = *reinterpret_cast<volatile uint32_t *>(&R.item[b]);
+    if (item < total_items) {
+      dead = 0;
+      const FineDesc &D = R.desc[b];
+      const uint32_t hp_n = D.hp_n, Tu = D.pre[kFMaxPieces];
+      const uint32_t lo = D.c0 * Lay::kCap, hi = min(Tu, lo + Lay::kCap);
+      const uint32_t rb = smem_u32(smem_raw + b * Lay::kBufBytes);
+      FineWin Wn;
+      Wn.r0 = rb;
+      Wn.r1 = rb + Lay::kCap * 16u;
+      Wn.r2 = Wn.r1 + Lay::kCap * 16u;
+      Wn.r3 = 0u;
+      Wn.lo = lo;
+      Wn.d = &D;
+      Wn.grec3 = A.rec3;
+      const FineHot *hot = s_hot + b * kFWave;
+      for (;;) {
+        uint32_t k = 0;
+        if (lane == 0) k = atom_add_smem(&R.next[b], 1u);
+        k = __shfl_sync(kFull, k, 0);
+        if (k >= hp_n) break;
+        const FineHot &Hh = hot[k];
+        const int nr = (int)Hh.nruns;
+        uint32_t rs = 0, rl = 0;
+        if (lane < nr) {
+          int pc;
+          if (slab_grid(g)) {
+            pc = Hh.bx0 + lane - D.ux0;
+          } else {
+            const int nyb = Hh.by1 - Hh.by0 + 1, nyu = D.uy1 - D.uy0 + 1;
+            pc = (Hh.bx0 + lane / nyb - D.ux0) * nyu + (Hh.by0 + lane % nyb - D.uy0);
+          }
+          const uint2 Rr = Hh.run[lane];
+          const uint32_t fa = D.pre[pc] + (Rr.x - D.src[pc]), fb = fa + (Rr.y - Rr.x);
+          const uint32_t ca = max(fa, lo), cb = min(fb, hi);
+          if (cb > ca) {
+            rs = ca - lo;
+            rl = cb - ca;
+          }
+        }
+        double *acc = T.partials + (size_t)(D.pbase + k) * PS;  // this fragment's own row
+        if (!__any_sync(kFull, rl != 0)) {
+          if (lane < PS) acc[lane] = 0.0;
+          continue;
+        }
+        const Hit &Hs = T.hits[D.hp_lo + k];  // full state: exact path only
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+        LeanCnt lc = {0u, 0u, 0u, 0u};
+        const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
+        if (Hh.gray & 2u) {
+          lean_fragment<NA>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
+          lean_reduce<GMAX, true>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st);
+        } else {
+          exact_fragment_lean<NA>(A, Hh, Hs, rs, rl, slot_lane, lc, p0, p1, p2, Wn, st);
+          lean_reduce<GMAX, true>(slots, lane, 1.0, lc, p0, p1, p2, acc, st);
+        }
+      }
+    } else {
+      ++dead;
+    }
+    // leave the position; the last warp out refills its buffer (position q + NB)
+    __syncwarp();
+    uint32_t left = 0;
+    if (lane == 0) left = atom_add_smem(&R.left[b], 1u);
+    left = __shfl_sync(kFull, left, 0);
+    if (left == kRWarps - 1)
+      ring_fill<GMAX, NB>(b, A, T, total_items, R, smem_raw + b * Lay::kBufBytes, s_hot + b * kFWave);
+    // A position's item was claimed when position q - 2 NB was left, and every
+    // claim after one past the end is past the end: after 2 NB dead positions
+    // in a row no later position holds an item.
+    if (dead == 2 * NB) break;
+  }
+
+  __shared__ unsigned long long s_c[4];
+  if (threadIdx.x == 0) s_c[0] = s_c[1] = s_c[2] = s_c[3] = 0;
+  __syncthreads();
+  atomicAdd(&s_c[0], (unsigned long long)st.n_acc);
+  atomicAdd(&s_c[1], (unsigned long long)st.n_cand);
+  atomicAdd(&s_c[2], (unsigned long long)st.n_exact);
+  atomicAdd(&s_c[3], (unsigned long long)st.n_amb);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(&A.counters[0], s_c[0]);
+    atomicAdd(&A.counters[1], s_c[1]);
+    atomicAdd(&A.counters[2], s_c[2]);
+    atomicAdd(&A.counters[3], s_c[3]);
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 static inline unsigned fblocks(unsigned long long n, int threads, int sms, int per_sm) {
   unsigned long long b = (n + threads - 1) / threads;
@@ -1278,12 +1534,20 @@ bool fine_supported(int G, int C) {
   return gmax * C <= 24;
 }
 
-void fine_caps(int G, int C, uint32_t *cap64, uint32_t *cap48) {
+void fine_caps(int G, int C, bool lean, uint32_t *cap64, uint32_t *cap48, uint32_t *fsub) {
 #define FPPM_CAPS(gm, ch) \
   do {                    \
     *cap64 = FineLayout<gm, ch>::kCap64; \
     *cap48 = FineLayout<gm, ch>::kCap48; \
   } while (0)
+  *fsub = kFSub;
+  if (lean && ring_enabled()) {  // k_gather_ring: items of one window, 48-B records
+    const int nb = ring_buffers();
+    if (nb == 3) *cap48 = *cap64 = (G <= 4) ? RingLayout<4, 3>::kCap : RingLayout<8, 3>::kCap;
+    else *cap48 = *cap64 = (G <= 4) ? RingLayout<4, 2>::kCap : RingLayout<8, 2>::kCap;
+    *fsub = 1;
+    return;
+  }
   if (C == 1) {
     if (G <= 4) FPPM_CAPS(4, 1);
     else if (G <= 8) FPPM_CAPS(8, 1);
@@ -1297,7 +1561,7 @@ void fine_caps(int G, int C, uint32_t *cap64, uint32_t *cap48) {
 }
 
 cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
-                               int sms, uint32_t cap64, uint32_t cap48, uint32_t *nb_out,
+                               int sms, uint32_t cap64, uint32_t cap48, uint32_t fsub, uint32_t *nb_out,
                                unsigned long long hp_version) {
   const long long x0 = g.ix0 >> g.shift, y0 = g.iy0 >> g.shift, z0 = g.iz0 >> g.shift;
   const unsigned long long ex = (unsigned long long)(((g.ix0 + g.nx - 1) >> g.shift) - x0 + 3);
@@ -1341,7 +1605,7 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   note_launches(1);
   k_fine_items<<<fblocks((unsigned long long)(nb + 1) * 32, 128, sms, 16), 128, 0, s>>>(
       A, S.hp_start, nb, static_cast<const FineHot *>(S.fhot), S.fbox, S.items,
-      S.chunks, cap64, cap48, S.nonempty);
+      S.chunks, cap64, cap48, fsub, S.nonempty);
   note_launches(1);
   e = launch_exclusive_scan(s, S.items, nb + 1, S.scan_tmp, S.item_base);
   if (e != cudaSuccess) return e;
@@ -1349,10 +1613,10 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
 }
 
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
-                                uint32_t cap64, uint32_t cap48) {
+                                uint32_t cap64, uint32_t cap48, uint32_t fsub) {
   k_fine_desc<<<fblocks((unsigned long long)nb * 32, 128, sms, 16), 128, 0, s>>>(
       A, S.hp_start, nb, S.hp_order, static_cast<const FineHot *>(S.fhot), S.fbox,
-      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48);
+      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48, fsub);
   note_launches(1);
   return cudaGetLastError();
 }
@@ -1376,10 +1640,43 @@ static cudaError_t launch_fine_t(cudaStream_t s, const GatherArgs &A, const Fine
 size_t fine_hot_bytes() { return sizeof(FineHot); }
 size_t fine_hit_bytes() { return sizeof(Hit); }
 
+template <int GMAX, int NB>
+static cudaError_t launch_ring_t(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int sms) {
+  using Lay = RingLayout<GMAX, NB>;
+  const size_t smem = Lay::kDynBytes;
+  cudaError_t e =
+      cudaFuncSetAttribute(k_gather_ring<GMAX, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_gather_ring<GMAX, NB><<<sms, kRThreads, smem, s>>>(A, T);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+// FPPM_RING=0 selects the one-window-per-CTA kernel for lean frames (A/B);
+// FPPM_RING=3 a ring of three buffers
+bool ring_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("FPPM_RING");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+int ring_buffers() {
+  static const int nb = [] {
+    const char *e = std::getenv("FPPM_RING");
+    return (e && e[0] == '3') ? 3 : 2;
+  }();
+  return nb;
+}
+
 cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms, bool lean) {
   const int G = A.na * A.ns;
   if (lean) {  // C = 1, n_s = 4, n_a <= 2 (lean_config)
     if (C != 1 || A.ns != 4 || A.na > 2) return cudaErrorInvalidValue;
+    if (ring_enabled()) {
+      if (ring_buffers() == 3) return A.na == 1 ? launch_ring_t<4, 3>(s, A, T, sms) : launch_ring_t<8, 3>(s, A, T, sms);
+      return A.na == 1 ? launch_ring_t<4, 2>(s, A, T, sms) : launch_ring_t<8, 2>(s, A, T, sms);
+    }
     return A.na == 1 ? launch_fine_t<4, 1, true>(s, A, T, sms) : launch_fine_t<8, 1, true>(s, A, T, sms);
   }
   if (C == 1) {

@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(128) k_tile_finalize(const GatherArgs A, const
   constexpr int PS = partial_size(GMAX, CH);
   double my_rmax = 0.0;
   uint32_t my_tested = 0, my_rejected = 0;
-  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < A.H; h += gridDim.x * blockDim.x) {
+  // wave order: the lanes of a warp read consecutive rows of one wave
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.H; i += gridDim.x * blockDim.x) {
+    const uint32_t h = T.hp_order[i];
     const uint32_t pbase = T.hp_map[3 * (size_t)h], nch = T.hp_map[3 * (size_t)h + 1],
                    stride = T.hp_map[3 * (size_t)h + 2];
     uint32_t cnt[GMAX];

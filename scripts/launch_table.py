@@ -21,3 +21,11 @@ for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
 if len(sys.argv) > 3:
     pat = sys.argv[3]
     print('sequence of', pat, [round(v / 1e6, 3) for n, v in seq if pat in n])
+if len(sys.argv) > 4:
+    # the last iteration: kernels after the second-to-last k_tile_finalize / k_apply_deltas
+    ends = [i for i, (n, v) in enumerate(seq) if 'finalize' in n or 'apply_deltas' in n]
+    if len(ends) >= 2:
+        it = seq[ends[-2] + 1:ends[-1] + 1]
+        print(f"last iteration: {len(it)} launches, {sum(v for _, v in it)/1e3:.1f} us")
+        for n, v in it:
+            print(f"  {v/1e3:8.1f} us  {n}")
