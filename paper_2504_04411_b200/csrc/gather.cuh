@@ -158,7 +158,8 @@ struct TileSched {
   long long bins_dims[7] = {0, 0, 0, 0, 0, 0, 0};
 };
 
-__host__ __device__ constexpr int partial_size(int gmax, int ch) { return gmax + 2 * ch * gmax + 3; }
+// [count G | sum C G | sum_sq C G | power 3], padded to an even count (16-B rows)
+__host__ __device__ constexpr int partial_size(int gmax, int ch) { return (gmax + 2 * ch * gmax + 3 + 1) & ~1; }
 
 cudaError_t launch_tile_finalize(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int C,
                                  int sms);

@@ -66,7 +66,7 @@ struct alignas(16) FineHot {
   uint32_t nruns;
   uint2 run[kFMaxPieces];  // sorted-record range [begin, end) of each run (clipped to the chord)
   uint32_t mlim;           // lean layout: meta <= mlim <=> eye + depth <= max_depth (integrator.cpp:396)
-  uint32_t pad_[3];
+  uint32_t pad_[3];        // ring schedule: row of window 0, first window, end window (k_fine_desc)
 };
 static_assert(sizeof(FineHot) % 16 == 0, "FineHot must be a multiple of 16 B (TMA)");
 
@@ -239,6 +239,48 @@ static __device__ __forceinline__ WaveInfo wave_info(const GatherArgs &A, const 
   return W;
 }
 
+// Ring schedule: the windows [c_first, c_first + nc) of a wave that hold a
+// member's candidates (lane j = member j, W from wave_info): its runs mapped
+// into the union's flattened order (min / max over runs), divided by the
+// window capacity.  nc = 0: no candidates.
+static __device__ __forceinline__ void member_windows(const GridHeader &g, const FineHot *__restrict__ hot,
+                                                      uint32_t b0, uint32_t n, const WaveInfo &W, uint32_t chunk,
+                                                      uint32_t &c_first, uint32_t &nc) {
+  const int lane = threadIdx.x & 31;
+  uint32_t fmin = 0xffffffffu, fmax = 0u;
+  const bool mine = (uint32_t)lane < n;
+  const FineHot *P = mine ? &hot[b0 + lane] : nullptr;
+  const int nr = mine && W.np > 0 ? (int)P->nruns : 0;
+#pragma unroll 1
+  for (int r = 0; r < kFMaxPieces; ++r) {
+    int pc = 0;
+    if (r < nr) {
+      if (slab_grid(g)) {
+        pc = P->bx0 + r - W.u.x0;
+      } else {
+        const int nyb = P->by1 - P->by0 + 1, nyu = W.u.y1 - W.u.y0 + 1;
+        pc = (P->bx0 + r / nyb - W.u.x0) * nyu + (P->by0 + r % nyb - W.u.y0);
+      }
+    }
+    const uint32_t pre = __shfl_sync(kFull, W.pre, pc & 31), src = __shfl_sync(kFull, W.src, pc & 31);
+    if (r < nr) {
+      const uint2 R = P->run[r];
+      if (R.y > R.x) {
+        const uint32_t fa = pre + (R.x - src);
+        fmin = min(fmin, fa);
+        fmax = max(fmax, fa + (R.y - R.x));
+      }
+    }
+  }
+  if (fmin < fmax) {
+    c_first = fmin / chunk;
+    nc = (fmax - 1) / chunk - c_first + 1;
+  } else {
+    c_first = 0;
+    nc = 0;
+  }
+}
+
 // per bucket (one warp each): items (runs of <= fsub windows of
 // ceil(union / chunk)) and partial rows (items x wave size)
 __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
@@ -260,7 +302,13 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
       const uint32_t nwin = W.T == 0 ? 1u : (W.T + chunk - 1) / chunk;
       const uint32_t nsub = (nwin + fsub - 1) / fsub;
       it += nsub;
-      pr += nsub * n;
+      if (fsub == 1) {  // ring: one row per (hit point, window it has candidates in)
+        uint32_t c_first, nc;
+        member_windows(g, hot, h0 + w * kFWave, n, W, chunk, c_first, nc);
+        pr += __reduce_add_sync(kFull, nc);
+      } else {
+        pr += nsub * n;
+      }
     }
     if (lane == 0) {
       items[b] = it;
@@ -270,7 +318,7 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
 }
 
 __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
-                            const uint32_t *__restrict__ hp_order, const FineHot *__restrict__ hot,
+                            const uint32_t *__restrict__ hp_order, FineHot *__restrict__ hot,
                             const int4 *__restrict__ fbox, const uint32_t *__restrict__ item_base,
                             const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
                             uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48, uint32_t fsub) {
@@ -279,7 +327,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
   __shared__ __align__(16) uint32_t s_d[kWarps][kWords];
   const GridHeader g = *A.grid;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  FineDesc &d = *reinterpret_cast<FineDesc *>(&s_d[wl][0]);
+  FineDesc &d = *reinterpret_cast<FineDesc *>(&s_d[wl][0]);  // (d.pbase unused by the ring)
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += nw) {
     const uint32_t h0 = hp_start[b], nhp = hp_start[b + 1] - h0;
@@ -305,7 +353,30 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
         d.pad0 = (W.planar || g.lean) ? 1u : 0u;  // flags: bit0 = 48-B records (no rec3 staged)
         d.ux0 = W.u.x0; d.ux1 = W.u.x1; d.uy0 = W.u.y0; d.uy1 = W.u.y1; d.uz0 = W.u.z0; d.uz1 = W.u.z1;
       }
-      if ((uint32_t)lane < n) {
+      uint32_t rows_used = nsub * n;
+      if (fsub == 1) {
+        // ring: member j's rows are contiguous, one per window of its range;
+        // the fragment of window c writes row pad_[0] + c (FineHot, staged by TMA)
+        uint32_t c_first, nc;
+        member_windows(g, hot, lo, n, W, chunk, c_first, nc);
+        uint32_t incl = nc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t r0 = prow + incl - nc;
+        rows_used = __shfl_sync(kFull, incl, 31);
+        if ((uint32_t)lane < n) {
+          const uint32_t h = hp_order[lo + lane];
+          hp_map[3 * (size_t)h] = r0;  // finalize: rows r0 .. r0 + nc - 1
+          hp_map[3 * (size_t)h + 1] = nc;
+          hp_map[3 * (size_t)h + 2] = 1u;
+          hot[lo + lane].pad_[0] = r0 - c_first;
+          hot[lo + lane].pad_[1] = c_first;
+          hot[lo + lane].pad_[2] = c_first + nc;
+        }
+      } else if ((uint32_t)lane < n) {
         const uint32_t h = hp_order[lo + lane];
         hp_map[3 * (size_t)h] = prow + lane;  // finalize: rows prow + j + sub * n
         hp_map[3 * (size_t)h + 1] = nsub;
@@ -323,7 +394,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
         for (int k = lane; k < kWords; k += 32) dst[k] = s_d[wl][k];
         __syncwarp();
       }
-      prow += nsub * n;
+      prow += rows_used;
     }
   }
 }
@@ -960,7 +1031,7 @@ static __device__ __forceinline__ void row_put(double &d, double v) {
 template <int GMAX, bool STORE = false>
 static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, double K0, const LeanCnt &c,
                                                    double p0, double p1, double p2, double *acc,
-                                                   FineState &st) {
+                                                   FineState &st, size_t fs = 1) {
   constexpr int NC = GMAX, NQ = 32 / NC, R = 32 / NQ;
   const int col = lane % NC, grp = lane / NC;
   double sm = 0.0, sq = 0.0;
@@ -1005,17 +1076,17 @@ static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, dou
     st.n_acc += (e02 & 0xffffu) + (e02 >> 16) + (e26 & 0xffffu) + (e26 >> 16) + (o15 & 0xffffu) + (o15 >> 16) +
                 (o37 & 0xffffu) + (o37 >> 16);
   if (lane < NC) {
-    row_put<STORE>(acc[GMAX + lane], dm(K0, sm));
-    row_put<STORE>(acc[2 * GMAX + lane], dm(dm(K0, K0), sq));
+    row_put<STORE>(acc[(GMAX + lane) * fs], dm(K0, sm));
+    row_put<STORE>(acc[(2 * GMAX + lane) * fs], dm(dm(K0, K0), sq));
   } else if (lane >= 32 - GMAX) {
     const int g = lane - (32 - GMAX);
     const uint32_t w = (g & 1) ? ((g & 2) ? o37 : o15) : ((g & 2) ? e26 : e02);
-    row_put<STORE>(acc[g], (double)((g & 4) ? (w >> 16) : (w & 0xffffu)));
+    row_put<STORE>(acc[g * fs], (double)((g & 4) ? (w >> 16) : (w & 0xffffu)));
   }
   if (lane == 0) {
-    row_put<STORE>(acc[3 * GMAX], p0);
-    row_put<STORE>(acc[3 * GMAX + 1], p1);
-    row_put<STORE>(acc[3 * GMAX + 2], p2);
+    row_put<STORE>(acc[(3 * GMAX) * fs], p0);
+    row_put<STORE>(acc[(3 * GMAX + 1) * fs], p1);
+    row_put<STORE>(acc[(3 * GMAX + 2) * fs], p2);
   }
   __syncwarp();
 }
@@ -1472,7 +1543,13 @@ __global__ void __launch_bounds__(kRThreads, 1) k_gather_ring(const GatherArgs A
             rl = cb - ca;
           }
         }
-        double *acc = T.partials + (size_t)(D.pbase + k) * PS;  // this fragment's own row
+        // this fragment's own row: the hit point's rows are contiguous, one per
+        // window of its range [pad_[1], pad_[2]) (k_fine_desc); a window
+        // outside the range holds none of its candidates and has no row
+        const uint32_t c = D.c0;
+        if (c < Hh.pad_[1] || c >= Hh.pad_[2]) continue;
+        double *acc = T.partials + (size_t)(Hh.pad_[0] + c) * PS;
+        constexpr size_t fs = 1;
         if (!__any_sync(kFull, rl != 0)) {
           if (lane < PS) acc[lane] = 0.0;
           continue;
@@ -1483,10 +1560,10 @@ __global__ void __launch_bounds__(kRThreads, 1) k_gather_ring(const GatherArgs A
         const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
         if (Hh.gray & 2u) {
           lean_fragment<NA>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
-          lean_reduce<GMAX, true>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st);
+          lean_reduce<GMAX, true>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st, fs);
         } else {
           exact_fragment_lean<NA>(A, Hh, Hs, rs, rl, slot_lane, lc, p0, p1, p2, Wn, st);
-          lean_reduce<GMAX, true>(slots, lane, 1.0, lc, p0, p1, p2, acc, st);
+          lean_reduce<GMAX, true>(slots, lane, 1.0, lc, p0, p1, p2, acc, st, fs);
         }
       }
     } else {
@@ -1615,7 +1692,7 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
                                 uint32_t cap64, uint32_t cap48, uint32_t fsub) {
   k_fine_desc<<<fblocks((unsigned long long)nb * 32, 128, sms, 16), 128, 0, s>>>(
-      A, S.hp_start, nb, S.hp_order, static_cast<const FineHot *>(S.fhot), S.fbox,
+      A, S.hp_start, nb, S.hp_order, static_cast<FineHot *>(S.fhot), S.fbox,
       S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48, fsub);
   note_launches(1);
   return cudaGetLastError();

@@ -118,9 +118,7 @@ __global__ void __launch_bounds__(128) k_tile_finalize(const GatherArgs A, const
   constexpr int PS = partial_size(GMAX, CH);
   double my_rmax = 0.0;
   uint32_t my_tested = 0, my_rejected = 0;
-  // wave order: the lanes of a warp read consecutive rows of one wave
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.H; i += gridDim.x * blockDim.x) {
-    const uint32_t h = T.hp_order[i];
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < A.H; h += gridDim.x * blockDim.x) {
     const uint32_t pbase = T.hp_map[3 * (size_t)h], nch = T.hp_map[3 * (size_t)h + 1],
                    stride = T.hp_map[3 * (size_t)h + 2];
     uint32_t cnt[GMAX];
@@ -133,7 +131,15 @@ __global__ void __launch_bounds__(128) k_tile_finalize(const GatherArgs A, const
       for (int c = 0; c < CH; ++c) sm[c][g] = sq[c][g] = 0.0;
     }
     for (uint32_t ch = 0; ch < nch; ++ch) {
-      const double *pp = T.partials + ((size_t)pbase + (size_t)ch * stride) * PS;
+      // 16-B loads of the (even-sized, 16-B aligned) row
+      const double2 *pp2 = reinterpret_cast<const double2 *>(T.partials + ((size_t)pbase + (size_t)ch * stride) * PS);
+      double pp[PS];
+#pragma unroll
+      for (int f = 0; f < PS / 2; ++f) {
+        const double2 v = pp2[f];
+        pp[2 * f] = v.x;
+        pp[2 * f + 1] = v.y;
+      }
 #pragma unroll
       for (int g = 0; g < GMAX; ++g) cnt[g] += (uint32_t)pp[g];
 #pragma unroll
