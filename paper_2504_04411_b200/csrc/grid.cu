@@ -296,12 +296,19 @@ __global__ void __launch_bounds__(kSortThreads)
   const uint32_t tile_base = blockIdx.x * kTile;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t k[kSortItems], v[kSortItems], rank[kSortItems];
+  // all loads issued before the ranking (its warp-synchronous shared-memory
+  // updates would otherwise serialise them)
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
     const uint32_t i = tile_base + (warp * kSortItems + it) * kWarp + lane;
     const bool valid = i < n;
-    k[it] = valid ? keys_in[i] : 0u;
-    v[it] = valid ? vals_in[i] : 0u;
+    k[it] = valid ? __ldcs(&keys_in[i]) : 0u;
+    v[it] = valid ? __ldcs(&vals_in[i]) : 0u;
+  }
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint32_t i = tile_base + (warp * kSortItems + it) * kWarp + lane;
+    const bool valid = i < n;
     const uint32_t d = valid ? ((k[it] >> shift) & mask) : (uint32_t)kRadixMax;
     const uint32_t peers = __match_any_sync(kFull, d);
     const uint32_t before = valid ? s_wcnt[warp][d] : 0u;
@@ -354,51 +361,38 @@ __global__ void __launch_bounds__(kSortThreads)
 
 // ------------------------------------------------------------------ cell table
 // start[c] = first sorted position with dense id >= c, c in [0, ncells].
-__global__ void k_cell_start(const uint32_t *__restrict__ skeys, uint32_t n,
-                             const GridHeader *__restrict__ hdr, uint32_t *__restrict__ start) {
-  const unsigned long long nc = hdr->ncells;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const unsigned long long k = skeys[i];
-    const unsigned long long prev = i == 0 ? 0ull : (unsigned long long)skeys[i - 1] + 1ull;
-    for (unsigned long long c = prev; c <= k; ++c) start[c] = i;
-    if (i == n - 1)
-      for (unsigned long long c = k + 1; c <= nc; ++c) start[c] = n;
-  }
-}
-
-// Sparse tables, warp-cooperative: a warp owns 256 consecutive cells, finds
-// the window of sorted keys that falls in them with two binary searches, and
-// each lane resolves its cells inside that (small, cached) window; the table
-// writes are coalesced and no thread walks a long empty stretch.
-__global__ void __launch_bounds__(256) k_cell_start_chunked(const uint32_t *__restrict__ skeys, uint32_t n,
-                                                            unsigned long long ncells,
-                                                            uint32_t *__restrict__ start) {
-  constexpr unsigned long long kCells = 256;
+// Any table: photon i owns the cells (key[i - 1], key[i]] (start = i) and the
+// last photon also (key[n - 1], ncells] (start = n).  Short gaps are written
+// by their owner lane; long ones (empty stretches of a sparse or clustered
+// photon set) by the whole warp with coalesced stores, so no thread walks a
+// long gap and no binary search is needed.
+__global__ void __launch_bounds__(256) k_cell_start_gaps(const uint32_t *__restrict__ skeys, uint32_t n,
+                                                         unsigned long long ncells, uint32_t *__restrict__ start) {
+  constexpr unsigned long long kShort = 8;
   const int lane = threadIdx.x & 31;
-  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-  for (unsigned long long w = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-       w * kCells <= ncells; w += nwarps) {
-    const unsigned long long c0 = w * kCells;
-    const unsigned long long c1 = c0 + kCells < ncells + 1 ? c0 + kCells : ncells + 1;
-    uint32_t p = 0;
-    if (lane < 2) {
-      const unsigned long long c = lane == 0 ? c0 : c1;
-      uint32_t lo = 0, hi = n;
-      while (lo < hi) {
-        const uint32_t mid = lo + (hi - lo) / 2;
-        if ((unsigned long long)skeys[mid] < c) lo = mid + 1; else hi = mid;
-      }
-      p = lo;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n; base += nwarps * 32) {
+    const uint32_t i = base + lane;
+    const bool valid = i < n;
+    unsigned long long lo = 0, hi = 0;  // cells [lo, hi) get start = i
+    if (valid) {
+      const unsigned long long k = __ldg(&skeys[i]);
+      lo = i == 0 ? 0ull : (unsigned long long)__ldg(&skeys[i - 1]) + 1ull;
+      hi = k + 1;
     }
-    const uint32_t p0 = __shfl_sync(~0u, p, 0), p1 = __shfl_sync(~0u, p, 1);
-    for (unsigned long long c = c0 + lane; c < c1; c += 32) {
-      uint32_t lo = p0, hi = p1;
-      while (lo < hi) {
-        const uint32_t mid = lo + (hi - lo) / 2;
-        if ((unsigned long long)skeys[mid] < c) lo = mid + 1; else hi = mid;
-      }
-      start[c] = lo;
+    if (hi - lo <= kShort)
+      for (unsigned long long c = lo; c < hi; ++c) start[c] = i;
+    uint32_t big = __ballot_sync(kFull, hi - lo > kShort);
+    while (big) {
+      const int j = __ffs(big) - 1;
+      big &= big - 1;
+      const unsigned long long a = __shfl_sync(kFull, lo, j), b = __shfl_sync(kFull, hi, j);
+      for (unsigned long long c = a + lane; c < b; c += 32) start[c] = base + j;
     }
+    // cells after the last photon's
+    const unsigned long long tl = __shfl_sync(kFull, (valid && i == n - 1) ? hi : 0ull, (n - 1 - base) & 31);
+    if (n - 1 >= base && n - 1 < base + 32)
+      for (unsigned long long c = tl + lane; c <= ncells; c += 32) start[c] = n;
   }
 }
 
@@ -606,13 +600,8 @@ void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const 
                        uint32_t *start, unsigned long long ncells, int sms) {
   if (n == 0) {
     k_cell_start_empty<<<1, 32, 0, s>>>(start, ncells);
-  } else if (8ull * ncells > (unsigned long long)n) {
-    // tables with empty stretches (sparse or clustered photons, e.g. C5):
-    // warp-cooperative fill, no thread walks a long gap
-    k_cell_start_chunked<<<cap_blocks((ncells + 1 + 255) / 256 * 32, 256, sms, 16), 256, 0, s>>>(skeys, n, ncells,
-                                                                                              start);
   } else {
-    k_cell_start<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(skeys, n, hdr, start);
+    k_cell_start_gaps<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(skeys, n, ncells, start);
   }
   note_launches(1);
 }
