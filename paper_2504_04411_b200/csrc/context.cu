@@ -217,6 +217,7 @@ static int effective_variant(const fppm_gpu_ctx *ctx, uint32_t S) {
 // holds tens of photons (C5: ~200); sparser frames (the C3 / C4 camera hit
 // points: ~3) take one thread per hit point
 static bool dense_3d(const GridHeader &g) {
+  if (const char *e = std::getenv("FPPM_3D")) return e[0] == '1';  // measurement knob
   const double ref_cells = (double)g.ncells / ((double)g.S * g.S * g.S);
   return ref_cells > 0.0 && 27.0 * (double)g.n / ref_cells >= 48.0;
 }
@@ -517,6 +518,9 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->tile.sort.keys_b, Hc)); A(dalloc(&ctx->tile.sort.vals_b, Hc));
   A(dalloc(&ctx->tile.sort.hist, radix_hist_entries((uint32_t)Hc)));
   A(dalloc(&ctx->tile.hp_map, 3 * Hc));
+  A(dalloc(&ctx->tile.hp_nc, Hc + 1)); A(dalloc(&ctx->tile.hp_rbase, Hc + 1));
+  A(dalloc(&ctx->tile.hp_scan_tmp, Hc / 4096 + 8));
+  A(cudaMemset(ctx->tile.hp_nc, 0, sizeof(uint32_t) * (Hc + 1)));
   if (c.vcm_plus) {
     A(dalloc(&ctx->d_eye_mis, Hc));
     A(cudaMemset(ctx->d_eye_mis, 0, sizeof(double2) * Hc));
@@ -578,7 +582,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
                   T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.fdesc, T.fhot, T.fbox, T.fhit, T.pbase, T.partials,
-                  T.hp_map, T.nonempty};
+                  T.hp_map, T.nonempty, T.hp_nc, T.hp_rbase, T.hp_scan_tmp};
   for (void *p : tdev)
     if (p) cudaFree(p);
   if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
@@ -1593,6 +1597,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
     T.partials = S.partials;
     T.hp_map = S.hp_map;
     T.total_items = S.item_base + nb;
+    T.contig = fsub == 1;
     {
       FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48, fsub));
       FineArgs F;

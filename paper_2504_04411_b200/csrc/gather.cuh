@@ -95,6 +95,7 @@ struct TileArgs {
   double *partials;             // [item][32][partial_size] per-item results
   const uint32_t *hp_map;       // per hit point: first item, chunks, wave slot
   const uint32_t *total_items;  // device scalar
+  bool contig = false;          // ring schedule: each hit point's rows contiguous, in hit-point order
 };
 
 struct SortScratch {
@@ -145,6 +146,7 @@ struct TileSched {
   uint32_t *scan_tmp;
   double *partials;
   uint32_t *hp_map;     // [3 H]
+  uint32_t *hp_nc = nullptr, *hp_rbase = nullptr, *hp_scan_tmp = nullptr;  // ring rows per hit point [H + 1]
   uint32_t *nonempty;   // device counter: buckets holding hit points
   unsigned long long bucket_cap, item_cap;
   unsigned long long row_cap = 0;  // partial rows allocated

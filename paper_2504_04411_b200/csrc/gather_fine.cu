@@ -286,7 +286,8 @@ static __device__ __forceinline__ void member_windows(const GridHeader &g, const
 __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp_start, uint32_t nb,
                              const FineHot *__restrict__ hot, const int4 *__restrict__ fbox,
                              uint32_t *__restrict__ items, uint32_t *__restrict__ prows, uint32_t cap64,
-                             uint32_t cap48, uint32_t fsub, uint32_t *__restrict__ nonempty) {
+                             uint32_t cap48, uint32_t fsub, uint32_t *__restrict__ nonempty,
+                             const uint32_t *__restrict__ hp_order, uint32_t *__restrict__ hp_nc) {
   const GridHeader g = *A.grid;
   const int lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -306,6 +307,7 @@ __global__ void k_fine_items(const GatherArgs A, const uint32_t *__restrict__ hp
         uint32_t c_first, nc;
         member_windows(g, hot, h0 + w * kFWave, n, W, chunk, c_first, nc);
         pr += __reduce_add_sync(kFull, nc);
+        if ((uint32_t)lane < n) hp_nc[hp_order[h0 + w * kFWave + lane]] = nc;  // rows in hit-point order
       } else {
         pr += nsub * n;
       }
@@ -321,7 +323,8 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
                             const uint32_t *__restrict__ hp_order, FineHot *__restrict__ hot,
                             const int4 *__restrict__ fbox, const uint32_t *__restrict__ item_base,
                             const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
-                            uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48, uint32_t fsub) {
+                            uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48, uint32_t fsub,
+                            const uint32_t *__restrict__ hp_rbase) {
   constexpr int kWarps = 4;  // 128 threads
   constexpr int kWords = (int)(sizeof(FineDesc) / 4);
   __shared__ __align__(16) uint32_t s_d[kWarps][kWords];
@@ -355,20 +358,16 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
       }
       uint32_t rows_used = nsub * n;
       if (fsub == 1) {
-        // ring: member j's rows are contiguous, one per window of its range;
-        // the fragment of window c writes row pad_[0] + c (FineHot, staged by TMA)
+        // ring: member j's rows are contiguous, one per window of its range,
+        // allocated in hit-point order (scan of k_fine_items' counts) so the
+        // finalize reads them coalesced; the fragment of window c writes row
+        // pad_[0] + c (FineHot, staged by TMA)
         uint32_t c_first, nc;
         member_windows(g, hot, lo, n, W, chunk, c_first, nc);
-        uint32_t incl = nc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(kFull, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const uint32_t r0 = prow + incl - nc;
-        rows_used = __shfl_sync(kFull, incl, 31);
+        rows_used = __reduce_add_sync(kFull, nc);
         if ((uint32_t)lane < n) {
           const uint32_t h = hp_order[lo + lane];
+          const uint32_t r0 = hp_rbase[h];
           hp_map[3 * (size_t)h] = r0;  // finalize: rows r0 .. r0 + nc - 1
           hp_map[3 * (size_t)h + 1] = nc;
           hp_map[3 * (size_t)h + 2] = 1u;
@@ -1682,10 +1681,16 @@ cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S
   note_launches(1);
   k_fine_items<<<fblocks((unsigned long long)(nb + 1) * 32, 128, sms, 16), 128, 0, s>>>(
       A, S.hp_start, nb, static_cast<const FineHot *>(S.fhot), S.fbox, S.items,
-      S.chunks, cap64, cap48, fsub, S.nonempty);
+      S.chunks, cap64, cap48, fsub, S.nonempty, S.hp_order, S.hp_nc);
   note_launches(1);
   e = launch_exclusive_scan(s, S.items, nb + 1, S.scan_tmp, S.item_base);
   if (e != cudaSuccess) return e;
+  if (fsub == 1) {  // ring rows in hit-point order (hp_nc[H] = 0: rbase[H] = rows)
+    e = cudaMemsetAsync(S.hp_nc + A.H, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    e = launch_exclusive_scan(s, S.hp_nc, A.H + 1, S.hp_scan_tmp, S.hp_rbase);
+    if (e != cudaSuccess) return e;
+  }
   return launch_exclusive_scan(s, S.chunks, nb + 1, S.scan_tmp, S.pbase);
 }
 
@@ -1693,7 +1698,7 @@ cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &
                                 uint32_t cap64, uint32_t cap48, uint32_t fsub) {
   k_fine_desc<<<fblocks((unsigned long long)nb * 32, 128, sms, 16), 128, 0, s>>>(
       A, S.hp_start, nb, S.hp_order, static_cast<FineHot *>(S.fhot), S.fbox,
-      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48, fsub);
+      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48, fsub, S.hp_rbase);
   note_launches(1);
   return cudaGetLastError();
 }

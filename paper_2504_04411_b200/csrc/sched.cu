@@ -69,16 +69,32 @@ __global__ void k_bucket_start_bsearch(const uint32_t *__restrict__ skeys, uint3
 // The 9 (dx, dy) columns of photon-grid cell (ix, iy, iz): each column's three
 // z cells are contiguous in key order.  Returns the candidate count.
 
+// Exclusive scan: tiles of 4096 = 256 threads x 16 consecutive values (one
+// block scan per tile), tile sums scanned by one block, then applied.
 constexpr int kScanTile = 4096;
+constexpr int kScanPer = kScanTile / 256;
+static __device__ __forceinline__ void scan_load16(const uint32_t *__restrict__ in, uint32_t n, uint32_t i0,
+                                                   uint32_t (&v)[kScanPer]) {
+  if (i0 + kScanPer <= n && (i0 & 3u) == 0u) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(in + i0);
+#pragma unroll
+    for (int k = 0; k < kScanPer / 4; ++k) {
+      const uint4 w = q[k];
+      v[4 * k] = w.x; v[4 * k + 1] = w.y; v[4 * k + 2] = w.z; v[4 * k + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) v[k] = i0 + k < n ? in[i0 + k] : 0u;
+  }
+}
 __global__ void __launch_bounds__(256) k_scan_tiles(const uint32_t *__restrict__ in, uint32_t n,
                                                     uint32_t *__restrict__ tile_sum) {
   __shared__ uint32_t s_warp[8];
-  const uint32_t base = blockIdx.x * kScanTile;
+  uint32_t v[kScanPer];
+  scan_load16(in, n, blockIdx.x * kScanTile + threadIdx.x * kScanPer, v);
   uint32_t s = 0;
-  for (int k = 0; k < kScanTile / 256; ++k) {
-    const uint32_t i = base + k * 256 + threadIdx.x;
-    s += i < n ? in[i] : 0u;
-  }
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) s += v[k];
   uint32_t tot;
   (void)block_exclusive_scan_256(s, s_warp, &tot);
   if (threadIdx.x == 0) tile_sum[blockIdx.x] = tot;
@@ -100,18 +116,104 @@ __global__ void __launch_bounds__(256) k_scan_apply(const uint32_t *__restrict__
                                                     const uint32_t *__restrict__ tile_sum,
                                                     uint32_t *__restrict__ out) {
   __shared__ uint32_t s_warp[8];
-  const uint32_t base = blockIdx.x * kScanTile;
-  uint32_t carry = tile_sum[blockIdx.x];
-  for (int k = 0; k < kScanTile / 256; ++k) {
-    const uint32_t i = base + k * 256 + threadIdx.x;
-    const uint32_t v = i < n ? in[i] : 0u;
-    uint32_t tot;
-    const uint32_t ex = block_exclusive_scan_256(v, s_warp, &tot);
-    if (i < n) out[i] = carry + ex;
-    carry += tot;
+  const uint32_t i0 = blockIdx.x * kScanTile + threadIdx.x * kScanPer;
+  uint32_t v[kScanPer];
+  scan_load16(in, n, i0, v);
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) s += v[k];
+  uint32_t tot;
+  uint32_t run = tile_sum[blockIdx.x] + block_exclusive_scan_256(s, s_warp, &tot);
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    if (i0 + k < n) out[i0 + k] = run;
+    run += v[k];
   }
 }
 
+// Ring schedule: a hit point's rows are contiguous and allocated in hit-point
+// order, so the 32 hit points of a warp own one contiguous run of rows.  The
+// warp copies it through shared memory in chunks with coalesced 16-B loads and
+// each lane sums its own rows in order (same order as k_tile_finalize).
+constexpr int kFinChunk = 48;  // rows per warp and chunk
+template <int GMAX, int CH>
+__global__ void __launch_bounds__(128) k_tile_finalize_contig(const GatherArgs A, const TileArgs T) {
+  constexpr int PS = partial_size(GMAX, CH);
+  extern __shared__ __align__(16) double s_fin[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2 *s2 = reinterpret_cast<double2 *>(s_fin + (size_t)warp * kFinChunk * PS);
+  const double *sw = s_fin + (size_t)warp * kFinChunk * PS;
+  const double2 *src2 = reinterpret_cast<const double2 *>(T.partials);
+  double my_rmax = 0.0;
+  uint32_t my_tested = 0, my_rejected = 0;
+  for (uint32_t hb = blockIdx.x * blockDim.x + warp * 32; hb < A.H; hb += gridDim.x * blockDim.x) {
+    const uint32_t h = hb + lane;
+    const bool valid = h < A.H;
+    const uint32_t rb = valid ? T.hp_map[3 * (size_t)h] : 0u, nc = valid ? T.hp_map[3 * (size_t)h + 1] : 0u;
+    const uint32_t r_lo = __shfl_sync(kFull, rb, 0), r_hi = __reduce_max_sync(kFull, valid ? rb + nc : 0u);
+    uint32_t cnt[GMAX];
+    double sm[CH][GMAX], sq[CH][GMAX];
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      cnt[g] = 0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) sm[c][g] = sq[c][g] = 0.0;
+    }
+    for (uint32_t c0 = r_lo; c0 < r_hi; c0 += kFinChunk) {
+      const uint32_t c1 = min(r_hi, c0 + (uint32_t)kFinChunk);
+      const uint32_t nv = (c1 - c0) * (PS / 2);
+      {  // 8 loads in flight per lane
+        const double2 *g2 = src2 + (size_t)c0 * (PS / 2);
+        for (uint32_t k0 = 0; k0 < nv; k0 += 8 * 32) {
+          double2 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t k = k0 + u * 32 + lane;
+            if (k < nv) v[u] = __ldcs(&g2[k]);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t k = k0 + u * 32 + lane;
+            if (k < nv) s2[k] = v[u];
+          }
+        }
+      }
+      __syncwarp();
+      const uint32_t a = max(rb, c0), e = min(rb + nc, c1);
+      for (uint32_t r = a; r < e; ++r) {
+        const double *pp = sw + (size_t)(r - c0) * PS;
+#pragma unroll
+        for (int g = 0; g < GMAX; ++g) cnt[g] += (uint32_t)pp[g];
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+          for (int g = 0; g < GMAX; ++g) {
+            sm[c][g] += pp[GMAX + c * GMAX + g];
+            sq[c][g] += pp[GMAX + CH * GMAX + c * GMAX + g];
+          }
+        p0 += pp[GMAX + 2 * CH * GMAX];
+        p1 += pp[GMAX + 2 * CH * GMAX + 1];
+        p2 += pp[GMAX + 2 * CH * GMAX + 2];
+      }
+      __syncwarp();
+    }
+    if (valid) finalize_hit<GMAX, CH>(A, h, cnt, sm, sq, p0, p1, p2, my_tested, my_rejected, my_rmax);
+  }
+  __shared__ unsigned int s_tr[2];
+  __shared__ unsigned long long s_rmax;
+  if (threadIdx.x == 0) { s_tr[0] = s_tr[1] = 0; s_rmax = 0; }
+  __syncthreads();
+  atomicAdd(&s_tr[0], my_tested);
+  atomicAdd(&s_tr[1], my_rejected);
+  atomicMax(&s_rmax, (unsigned long long)__double_as_longlong(my_rmax));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(A.iter_tr, s_tr[0]);
+    atomicAdd(A.iter_tr + 1, s_tr[1]);
+    atomicMax(A.rmax_bits, s_rmax);
+  }
+}
 
 template <int GMAX, int CH>
 __global__ void __launch_bounds__(128) k_tile_finalize(const GatherArgs A, const TileArgs T) {
@@ -224,7 +326,15 @@ cudaError_t launch_exclusive_scan(cudaStream_t s, const uint32_t *in, uint32_t n
 template <int GMAX, int CH>
 static cudaError_t launch_fin(cudaStream_t s, const GatherArgs &A, const TileArgs &T, int sms) {
   if (A.H == 0) return cudaSuccess;
-  k_tile_finalize<GMAX, CH><<<blocks_for(A.H, 128, sms, 8), 128, 0, s>>>(A, T);
+  if (T.contig) {
+    const size_t smem = (size_t)4 * kFinChunk * partial_size(GMAX, CH) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_tile_finalize_contig<GMAX, CH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_tile_finalize_contig<GMAX, CH><<<blocks_for(A.H, 128, sms, 8), 128, smem, s>>>(A, T);
+  } else {
+    k_tile_finalize<GMAX, CH><<<blocks_for(A.H, 128, sms, 8), 128, 0, s>>>(A, T);
+  }
   note_launches(1);
   return cudaGetLastError();
 }

@@ -38,3 +38,16 @@ T = sum(v for k, v in tot.items() if "k_photons" not in k)
 print(f"per step (excl. photon generation): {T / steps / 1000:.3f} ms")
 for k, v in sorted(tot.items(), key=lambda x: -x[1]):
     print(f"{v / steps:9.1f} us  {cnt[k] // steps:3d}x  {k[:90]}")
+# idle time: the union of kernel intervals against the span of the timed steps
+iv = sorted((e.time_range.start, e.time_range.end) for e in prof.events()
+            if e.device_type == torch.autograd.DeviceType.CUDA and "k_photons" not in e.name)
+if iv:
+    busy, cs, ce = 0.0, iv[0][0], iv[0][1]
+    for a, b in iv[1:]:
+        if a > ce:
+            busy += ce - cs
+            cs, ce = a, b
+        else:
+            ce = max(ce, b)
+    busy += ce - cs
+    print(f"kernel-busy time per step (union of intervals): {busy / steps / 1000:.3f} ms")
