@@ -769,7 +769,7 @@ struct LeanPair {
 
 // Hit-point constants of the lean loop.
 struct LeanHit {
-  float chx, chy, chz, lim_hi, lim_lo, band_y, qa_scale;
+  float chx, chy, chz, lim_hi, lim_lo, band_y, qa_edge, qa_eps;  // annulus edge yy = r2 / 2 and its band
   uint32_t mlim;
 };
 
@@ -796,10 +796,10 @@ static __device__ __forceinline__ LeanPair lean_eval(const LeanHit &F, bool vali
   bool band = !(r2 < F.lim_lo) || !(fabsf(dx) > F.band_y) || !(fabsf(dy) > F.band_y);
   // quadrant (exact-sector table): +x+y 0, -x+y 1, -x-y 2, +x-y 3
   uint32_t s4 = dy > 0.0f ? (dx > 0.0f ? 0u : 4u) : (dx > 0.0f ? 12u : 8u);
-  if constexpr (NA == 2) {  // one annulus edge at d2 = r2 / 2
-    const float qa = yy * F.qa_scale;
-    band = band || fabsf(qa - 1.0f) < 2e-4f;
-    if (qa >= 1.0f) s4 += 16u;
+  if constexpr (NA == 2) {  // one annulus edge at d2 = r2 / 2 (relative band 2e-4)
+    const float de = yy - F.qa_edge;
+    band = band || fabsf(de) < F.qa_eps;
+    if (de >= 0.0f) s4 += 16u;
   }
   q.need = maybe && band;
   q.acc = maybe && !band;
@@ -824,11 +824,13 @@ static __device__ __forceinline__ void lean_add(const LeanPair &q, uint32_t slot
   o.y = da(o.y, dm(v, v));
   sts_f64x2(a, o);
   padd_u32(nib, 1u << q.s4, q.acc);
-  // flux (integrator.cpp:449): predicated fp64 adds
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
-      "@q add.rn.f64 %0, %0, %4;\n\t@q add.rn.f64 %1, %1, %5;\n\t@q add.rn.f64 %2, %2, %6;\n\t}"
-      : "+d"(p0), "+d"(p1), "+d"(p2)
-      : "r"((uint32_t)q.acc), "d"(q.r), "d"(q.g), "d"(q.b));
+  // flux (integrator.cpp:449): fma(x, 1, p) = p + x and fma(x, 0, p) = p
+  // exactly for the finite powers of lean records -- one DFMA per channel
+  // (a predicated add is if-converted by ptxas into DADD + two FSEL)
+  const double m = q.acc ? 1.0 : 0.0;
+  p0 = __fma_rn(q.r, m, p0);
+  p1 = __fma_rn(q.g, m, p1);
+  p2 = __fma_rn(q.b, m, p2);
 }
 
 // Exact fp64 evaluation of the candidate at window index i of a lean window:
@@ -892,7 +894,9 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
   const uint32_t lt = (1u << lane) - 1u;
   LeanHit F;
   F.chx = Hh.F.chx; F.chy = Hh.F.chy; F.chz = Hh.F.chz;
-  F.lim_hi = Hh.F.lim_hi; F.lim_lo = Hh.F.lim_lo; F.band_y = Hh.F.band_y; F.qa_scale = Hh.F.qa_scale;
+  F.lim_hi = Hh.F.lim_hi; F.lim_lo = Hh.F.lim_lo; F.band_y = Hh.F.band_y;
+  F.qa_edge = 1.0f / Hh.F.qa_scale;  // n_a = 2: qa_scale = 2 / r2
+  F.qa_eps = 2e-4f * F.qa_edge;
   F.mlim = Hh.mlim;
   const uint32_t d1 = Wn.r1 - Wn.r0, d2 = Wn.r2 - Wn.r0;
   uint32_t incl = rl;
