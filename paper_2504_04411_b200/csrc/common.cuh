@@ -88,23 +88,68 @@ struct PhotonRecs {
   float4 *pack;  // fine layout: 64-B records in input order (permutation source)
 };
 
+// One input photon (fppm_photons SoA fields).
+struct PhotonIn {
+  float p[3], n[3], w[3], c[3];
+  uint32_t d;
+};
+__device__ __forceinline__ PhotonIn load_photon(const float *__restrict__ pos, const float *__restrict__ nrm,
+                                                const float *__restrict__ wi, const float *__restrict__ pw,
+                                                const uint32_t *__restrict__ depth, size_t j) {
+  PhotonIn P;
+  const size_t o = 3 * j;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    P.p[a] = pos[o + a];
+    P.n[a] = nrm[o + a];
+    P.w[a] = wi[o + a];
+    P.c[a] = pw[o + a];
+  }
+  P.d = depth[j];
+  return P;
+}
+// Photons j .. j + 3 (j % 4 == 0, 16-B aligned arrays) with 16-B loads:
+// three per float[3] array, one for the depths.
+__device__ __forceinline__ void load_photons4(const float *__restrict__ pos, const float *__restrict__ nrm,
+                                              const float *__restrict__ wi, const float *__restrict__ pw,
+                                              const uint32_t *__restrict__ depth, size_t j, PhotonIn (&P)[4]) {
+  const float *src[4] = {pos, nrm, wi, pw};
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const float4 *q = reinterpret_cast<const float4 *>(src[f] + 3 * j);
+    const float4 a = __ldcs(q), b = __ldcs(q + 1), c = __ldcs(q + 2);
+    const float v[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float *dst = f == 0 ? P[k].p : (f == 1 ? P[k].n : (f == 2 ? P[k].w : P[k].c));
+      dst[0] = v[3 * k];
+      dst[1] = v[3 * k + 1];
+      dst[2] = v[3 * k + 2];
+    }
+  }
+  const uint4 d = __ldcs(reinterpret_cast<const uint4 *>(depth + j));
+  P[0].d = d.x; P[1].d = d.y; P[2].d = d.z; P[3].d = d.w;
+}
+
 // Fine-layout records packed in input order (coalesced reads of the SoA input
 // and 64-B contiguous writes); the permutation then moves whole 64-B records.
-__device__ __forceinline__ void fine_record(const float *__restrict__ pos, const float *__restrict__ nrm,
-                                            const float *__restrict__ wi, const float *__restrict__ pw,
-                                            const uint32_t *__restrict__ depth, size_t j, float4 &q0,
-                                            float4 &q1, float4 &q2, float4 &q3) {
-  const size_t o = 3 * j;
-  const float nx = nrm[o], ny = nrm[o + 1], wx = wi[o], wy = wi[o + 1];
-  const double L = elum((double)pw[o], (double)pw[o + 1], (double)pw[o + 2]);
+__device__ __forceinline__ void fine_record(const PhotonIn &P, float4 &q0, float4 &q1, float4 &q2, float4 &q3) {
+  const float nx = P.n[0], ny = P.n[1], wx = P.w[0], wy = P.w[1];
+  const double L = elum((double)P.c[0], (double)P.c[1], (double)P.c[2]);
   const unsigned long long Lb = (unsigned long long)__double_as_longlong(L);
   const uint32_t flags =
       (fabsf(nx) < INFINITY && fabsf(ny) < INFINITY && fabsf(wx) < INFINITY && fabsf(wy) < INFINITY) ? 1u
                                                                                                      : 0u;
-  q0 = make_float4(pos[o], pos[o + 1], pos[o + 2], __uint_as_float(depth[j]));
-  q1 = make_float4(nrm[o + 2], wi[o + 2], __uint_as_float((uint32_t)Lb), __uint_as_float((uint32_t)(Lb >> 32)));
-  q2 = make_float4(pw[o], pw[o + 1], pw[o + 2], __uint_as_float(flags));
+  q0 = make_float4(P.p[0], P.p[1], P.p[2], __uint_as_float(P.d));
+  q1 = make_float4(P.n[2], P.w[2], __uint_as_float((uint32_t)Lb), __uint_as_float((uint32_t)(Lb >> 32)));
+  q2 = make_float4(P.c[0], P.c[1], P.c[2], __uint_as_float(flags));
   q3 = make_float4(nx, ny, wx, wy);
+}
+__device__ __forceinline__ void fine_record(const float *__restrict__ pos, const float *__restrict__ nrm,
+                                            const float *__restrict__ wi, const float *__restrict__ pw,
+                                            const uint32_t *__restrict__ depth, size_t j, float4 &q0,
+                                            float4 &q1, float4 &q2, float4 &q3) {
+  fine_record(load_photon(pos, nrm, wi, pw, depth, j), q0, q1, q2, q3);
 }
 
 // Lean record (GridHeader::lean): 48 B with the photon-only parts of the
@@ -118,23 +163,19 @@ __device__ __forceinline__ void fine_record(const float *__restrict__ pos, const
 //   a non-finite n.x/n.y/wi.x/wi.y or power, or depth >= 2^23: x = NaN, meta = 0, which
 //          lands every pair with the photon in the exact fp64 path (it reads
 //          the input photon, not this record).
-__device__ __forceinline__ void lean_record(const float *__restrict__ pos, const float *__restrict__ nrm,
-                                            const float *__restrict__ wi, const float *__restrict__ pw,
-                                            const uint32_t *__restrict__ depth, size_t j, double guard, float4 &q0,
-                                            float4 &q1, float4 &q2) {
-  const size_t o = 3 * j;
-  const float nx = nrm[o], ny = nrm[o + 1], wx = wi[o], wy = wi[o + 1];
-  const uint32_t d = depth[j];
-  double r = (double)pw[o], g = (double)pw[o + 1], b = (double)pw[o + 2];
+__device__ __forceinline__ void lean_record(const PhotonIn &P, double guard, float4 &q0, float4 &q1, float4 &q2) {
+  const float nx = P.n[0], ny = P.n[1], wx = P.w[0], wy = P.w[1];
+  const uint32_t d = P.d;
+  double r = (double)P.c[0], g = (double)P.c[1], b = (double)P.c[2];
   double L = elum(r, g, b);
   const bool exact = !(fabsf(nx) < INFINITY && fabsf(ny) < INFINITY && fabsf(wx) < INFINITY &&
                        fabsf(wy) < INFINITY) || d >= (1u << 23) || !(fabs(L) < INFINITY) ||
                      !(fabs(r) < INFINITY && fabs(g) < INFINITY && fabs(b) < INFINITY);
-  const bool guard_fail = (double)nrm[o + 2] < guard;
-  const bool cos_pos = !(wi[o + 2] <= 0.0f);
+  const bool guard_fail = (double)P.n[2] < guard;
+  const bool cos_pos = !(P.w[2] <= 0.0f);
   if (!cos_pos) r = g = b = L = 0.0;
   const uint32_t meta = exact ? 0u : ((d << 8) | (guard_fail ? 0x80000000u : 0u));
-  q0 = make_float4(exact ? __int_as_float(0x7fffffff) : pos[o], pos[o + 1], pos[o + 2], __uint_as_float(meta));
+  q0 = make_float4(exact ? __int_as_float(0x7fffffff) : P.p[0], P.p[1], P.p[2], __uint_as_float(meta));
   q1 = make_float4(__uint_as_float((uint32_t)__double_as_longlong(L)),
                    __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(L) >> 32)),
                    __uint_as_float((uint32_t)__double_as_longlong(b)),
@@ -143,6 +184,12 @@ __device__ __forceinline__ void lean_record(const float *__restrict__ pos, const
                    __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(r) >> 32)),
                    __uint_as_float((uint32_t)__double_as_longlong(g)),
                    __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(g) >> 32)));
+}
+__device__ __forceinline__ void lean_record(const float *__restrict__ pos, const float *__restrict__ nrm,
+                                            const float *__restrict__ wi, const float *__restrict__ pw,
+                                            const uint32_t *__restrict__ depth, size_t j, double guard, float4 &q0,
+                                            float4 &q1, float4 &q2) {
+  lean_record(load_photon(pos, nrm, wi, pw, depth, j), guard, q0, q1, q2);
 }
 
 // exclusive scan of one value per thread over a 256-thread block; returns the
