@@ -104,8 +104,8 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-KERNEL_NAMES = {"auto": "k_gather_fine (gather + accumulate; F-test fused in k_tile_finalize)",
-                "fine": "k_gather_fine (gather + accumulate; F-test fused in k_tile_finalize)",
+KERNEL_NAMES = {"auto": "k_gather_ring (lean fine gather, double-buffered windows; F-test fused in k_tile_finalize)",
+                "fine": "k_gather_ring (lean fine gather, double-buffered windows; F-test fused in k_tile_finalize)",
                 "warp": "k_gather_test", "3d": "k_gather_3d (gather + accumulate; F-test in k_apply_deltas)"}
 
 
