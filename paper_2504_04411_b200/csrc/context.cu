@@ -520,6 +520,7 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->tile.hp_map, 3 * Hc));
   A(dalloc(&ctx->tile.hp_nc, Hc + 1)); A(dalloc(&ctx->tile.hp_rbase, Hc + 1));
   A(dalloc(&ctx->tile.hp_scan_tmp, Hc / 4096 + 8));
+  A(dalloc(&ctx->tile.hp_span, Hc));
   A(cudaMemset(ctx->tile.hp_nc, 0, sizeof(uint32_t) * (Hc + 1)));
   if (c.vcm_plus) {
     A(dalloc(&ctx->d_eye_mis, Hc));
@@ -582,7 +583,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
   const TileSched &T = ctx->tile;
   void *tdev[] = {T.sort.keys_a, T.sort.vals_a, T.sort.keys_b, T.sort.vals_b, T.sort.hist,
                   T.hp_start, T.items, T.chunks, T.item_base, T.scan_tmp, T.fdesc, T.fhot, T.fbox, T.fhit, T.pbase, T.partials,
-                  T.hp_map, T.nonempty, T.hp_nc, T.hp_rbase, T.hp_scan_tmp};
+                  T.hp_map, T.nonempty, T.hp_nc, T.hp_rbase, T.hp_scan_tmp, T.hp_span};
   for (void *p : tdev)
     if (p) cudaFree(p);
   if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);

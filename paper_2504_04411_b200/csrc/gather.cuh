@@ -117,6 +117,11 @@ struct alignas(16) FineDesc {  // one per (home cell, wave, run of <= kFSub wind
   int32_t ux0, ux1, uy0, uy1, uz0, uz1;  // union of the wave's fine boxes
   uint32_t src[kFMaxPieces];        // first sorted record of piece p
   uint32_t pre[kFMaxPieces + 1];    // flattened offset of piece p (pre[max] = union size)
+  // ring schedule (one window per item): claim order of the wave's hit points,
+  // largest fragment first; only the nclaim hit points whose window range
+  // holds this window are claimed
+  uint32_t nclaim;
+  uint8_t order[32];
 };
 static_assert(sizeof(FineDesc) % 16 == 0 && sizeof(FineDesc) / 4 <= 256, "FineDesc layout");
 
@@ -147,6 +152,7 @@ struct TileSched {
   double *partials;
   uint32_t *hp_map;     // [3 H]
   uint32_t *hp_nc = nullptr, *hp_rbase = nullptr, *hp_scan_tmp = nullptr;  // ring rows per hit point [H + 1]
+  uint2 *hp_span = nullptr;  // ring: per wave position, the flattened span of the hit point's runs
   uint32_t *nonempty;   // device counter: buckets holding hit points
   unsigned long long bucket_cap, item_cap;
   unsigned long long row_cap = 0;  // partial rows allocated

@@ -245,7 +245,7 @@ static __device__ __forceinline__ WaveInfo wave_info(const GatherArgs &A, const 
 // window capacity.  nc = 0: no candidates.
 static __device__ __forceinline__ void member_windows(const GridHeader &g, const FineHot *__restrict__ hot,
                                                       uint32_t b0, uint32_t n, const WaveInfo &W, uint32_t chunk,
-                                                      uint32_t &c_first, uint32_t &nc) {
+                                                      uint32_t &c_first, uint32_t &nc, uint32_t *span = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t fmin = 0xffffffffu, fmax = 0u;
   const bool mine = (uint32_t)lane < n;
@@ -279,6 +279,24 @@ static __device__ __forceinline__ void member_windows(const GridHeader &g, const
     c_first = 0;
     nc = 0;
   }
+  if (span) {
+    span[0] = fmin;
+    span[1] = fmax;
+  }
+}
+
+// Warp-wide bitonic sort of one key per lane, descending.
+static __device__ __forceinline__ uint32_t warp_sort_desc(uint32_t key) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t other = __shfl_xor_sync(kFull, key, j);
+      const bool lower = (lane & j) == 0, desc = (lane & k) == 0;
+      key = (lower == desc) ? max(key, other) : min(key, other);
+    }
+  return key;
 }
 
 // per bucket (one warp each): items (runs of <= fsub windows of
@@ -324,7 +342,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
                             const int4 *__restrict__ fbox, const uint32_t *__restrict__ item_base,
                             const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
                             uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48, uint32_t fsub,
-                            const uint32_t *__restrict__ hp_rbase) {
+                            const uint32_t *__restrict__ hp_rbase, uint2 *__restrict__ hp_span) {
   constexpr int kWarps = 4;  // 128 threads
   constexpr int kWords = (int)(sizeof(FineDesc) / 4);
   __shared__ __align__(16) uint32_t s_d[kWarps][kWords];
@@ -357,13 +375,15 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
         d.ux0 = W.u.x0; d.ux1 = W.u.x1; d.uy0 = W.u.y0; d.uy1 = W.u.y1; d.uz0 = W.u.z0; d.uz1 = W.u.z1;
       }
       uint32_t rows_used = nsub * n;
+      uint32_t m_span[2] = {0u, 0u};  // ring: this lane's member span (k_fine_order)
       if (fsub == 1) {
         // ring: member j's rows are contiguous, one per window of its range,
         // allocated in hit-point order (scan of k_fine_items' counts) so the
         // finalize reads them coalesced; the fragment of window c writes row
         // pad_[0] + c (FineHot, staged by TMA)
         uint32_t c_first, nc;
-        member_windows(g, hot, lo, n, W, chunk, c_first, nc);
+        member_windows(g, hot, lo, n, W, chunk, c_first, nc, m_span);
+        if ((uint32_t)lane < n) hp_span[lo + lane] = make_uint2(m_span[0], m_span[1]);
         rows_used = __reduce_add_sync(kFull, nc);
         if ((uint32_t)lane < n) {
           const uint32_t h = hp_order[lo + lane];
@@ -388,6 +408,7 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
           d.c1 = min(nwin, d.c0 + fsub);
           d.pbase = prow + sb * n;
         }
+        if (lane == 0) d.nclaim = n;  // ring: claim order filled by k_fine_order
         __syncwarp();
         uint32_t *dst = reinterpret_cast<uint32_t *>(desc + item);
         for (int k = lane; k < kWords; k += 32) dst[k] = s_d[wl][k];
@@ -395,6 +416,39 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
       }
       prow += rows_used;
     }
+  }
+}
+
+// Ring schedule: one warp per item (= one window c of a wave) orders the
+// wave's hit points for claiming: those whose window range holds c, the
+// largest share of the window first (span [first run, last run) of the hit
+// point clipped to the window -- a proxy of its fragment), ties by index.
+// Longest-first claiming shortens the tail of an item, and the buffer is
+// released (refilled) when the last warp leaves it.
+__global__ void __launch_bounds__(128) k_fine_order(FineDesc *__restrict__ desc, const uint32_t *__restrict__ total,
+                                                    const FineHot *__restrict__ hot, const uint2 *__restrict__ hp_span,
+                                                    uint32_t cap) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nitems = *total;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nitems; it += nw) {
+    FineDesc &D = desc[it];
+    const uint32_t hp_lo = D.hp_lo, n = D.hp_n, c = D.c0, T = D.pre[kFMaxPieces];
+    uint32_t key = 0;
+    if ((uint32_t)lane < n) {
+      const FineHot &P = hot[hp_lo + lane];
+      if (c >= P.pad_[1] && c < P.pad_[2]) {
+        const uint2 sp = hp_span[hp_lo + lane];
+        const uint32_t wlo = c * cap, whi = min(T, wlo + cap);
+        const uint32_t sa = max(sp.x, wlo), se = min(sp.y, whi);
+        const uint32_t cnt = se > sa ? se - sa : 0u;
+        key = ((min(cnt, 0x3fffffu) + 1u) << 5) | (31u - (uint32_t)lane);
+      }
+    }
+    const uint32_t sorted = warp_sort_desc(key);
+    const uint32_t ncl = __popc(__ballot_sync(kFull, key != 0u));
+    D.order[lane] = (uint8_t)(31u - (sorted & 31u));
+    if (lane == 0) D.nclaim = ncl;
   }
 }
 
@@ -1522,11 +1576,14 @@ __global__ void __launch_bounds__(kRThreads, 1) k_gather_ring(const GatherArgs A
       Wn.d = &D;
       Wn.grec3 = A.rec3;
       const FineHot *hot = s_hot + b * kFWave;
+      const uint32_t nclaim = D.nclaim;
+      (void)hp_n;
       for (;;) {
-        uint32_t k = 0;
-        if (lane == 0) k = atom_add_smem(&R.next[b], 1u);
-        k = __shfl_sync(kFull, k, 0);
-        if (k >= hp_n) break;
+        uint32_t kc = 0;
+        if (lane == 0) kc = atom_add_smem(&R.next[b], 1u);
+        kc = __shfl_sync(kFull, kc, 0);
+        if (kc >= nclaim) break;
+        const uint32_t k = D.order[kc];  // largest fragment first (k_fine_desc)
         const FineHot &Hh = hot[k];
         const int nr = (int)Hh.nruns;
         uint32_t rs = 0, rl = 0;
@@ -1702,8 +1759,13 @@ cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &
                                 uint32_t cap64, uint32_t cap48, uint32_t fsub) {
   k_fine_desc<<<fblocks((unsigned long long)nb * 32, 128, sms, 16), 128, 0, s>>>(
       A, S.hp_start, nb, S.hp_order, static_cast<FineHot *>(S.fhot), S.fbox,
-      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48, fsub, S.hp_rbase);
+      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48, fsub, S.hp_rbase, S.hp_span);
   note_launches(1);
+  if (fsub == 1) {
+    k_fine_order<<<(unsigned)sms * 8, 128, 0, s>>>(S.fdesc, S.item_base + nb, static_cast<const FineHot *>(S.fhot),
+                                                 S.hp_span, cap48);
+    note_launches(1);
+  }
   return cudaGetLastError();
 }
 
