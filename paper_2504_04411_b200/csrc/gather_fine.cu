@@ -964,13 +964,11 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
   if (lane == 0) st.n_cand += total;
   int j = 0;
   uint32_t e = __shfl_sync(kFull, incl, 0), o = __shfl_sync(kFull, off, 0);
-  uint32_t spill = 15;
-  // one step: candidates v0 = base + lane and v1 = v0 + 32 (TAIL: the last,
-  // partial step -- slots past the end read the staged window, never added)
-  auto step = [&](uint32_t base, auto tail) {
-    constexpr bool TAIL = decltype(tail)::value;
+  // candidates v0 = base + lane and v1 = v0 + 32 of a step -> window indices
+  auto index = [&](uint32_t base, uint32_t &i0, uint32_t &i1) {
     const uint32_t v0 = base + lane, v1 = v0 + 32u;
-    uint32_t i0 = v0 + o, i1 = v1 + o;
+    i0 = v0 + o;
+    i1 = v1 + o;
     if (e < base + 64u) {  // a run ends before base + 64 (warp-uniform)
       while (e <= base) {  // skip runs that ended (incl. empty ones)
         ++j;
@@ -989,34 +987,64 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
         ek = __shfl_sync(kFull, incl, k);
       }
     }
-    bool ok0 = true, ok1 = true;
-    if constexpr (TAIL) {
-      ok0 = v0 < total;
-      ok1 = v1 < total;
-      if (!ok0) i0 = rs;
-      if (!ok1) i1 = rs;
-    }
-    if (--spill == 0) {
-      lean_spill(c);
-      spill = 15;
-    }
+  };
+  // evaluate + accumulate the two candidates; their band flags out
+  auto eval_add = [&](uint32_t i0, uint32_t i1, bool ok0, bool ok1, bool &n0, bool &n1) {
     const LeanPair q0 = lean_eval<NA>(F, ok0, Wn.r0 + i0 * 16u, d1, d2);
     const LeanPair q1 = lean_eval<NA>(F, ok1, Wn.r0 + i1 * 16u, d1, d2);
     lean_add(q0, slot_lane, c.n0, p0, p1, p2);
     lean_add(q1, slot_lane, c.n1, p0, p1, p2);
-    if (__any_sync(kFull, q0.need || q1.need)) {  // banded pairs (rare) go to the exact ring
-      const uint32_t m0 = __ballot_sync(kFull, q0.need), m1 = __ballot_sync(kFull, q1.need);
-      if (q0.need) sts_u32(ex + ((st.et + __popc(m0 & lt)) & (kFExact - 1)) * 4u, i0);
-      st.et += __popc(m0);
-      if (q1.need) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
-      st.et += __popc(m1);
-      while (st.et - st.eh >= 32)
-        lean_exact_batch(A, Hs, 32u, ex, slot_lane, c, p0, p1, p2, Wn, st);
-    }
+    n0 = q0.need;
+    n1 = q1.need;
   };
-  const uint32_t full = total & ~63u;
-  for (uint32_t base = 0; base < full; base += 64) step(base, std::false_type{});
-  if (full < total) step(full, std::true_type{});
+  // banded pairs (rare) go to the exact ring
+  auto push = [&](bool n0, uint32_t i0, bool n1, uint32_t i1) {
+    const uint32_t m0 = __ballot_sync(kFull, n0), m1 = __ballot_sync(kFull, n1);
+    if (n0) sts_u32(ex + ((st.et + __popc(m0 & lt)) & (kFExact - 1)) * 4u, i0);
+    st.et += __popc(m0);
+    if (n1) sts_u32(ex + ((st.et + __popc(m1 & lt)) & (kFExact - 1)) * 4u, i1);
+    st.et += __popc(m1);
+    while (st.et - st.eh >= 32)
+      lean_exact_batch(A, Hs, 32u, ex, slot_lane, c, p0, p1, p2, Wn, st);
+  };
+  // two full steps per iteration: one spill count, one band vote (a nibble
+  // takes <= 2 increments per iteration: spill every 7)
+  const uint32_t full = total & ~63u, full2 = total & ~127u;
+  uint32_t spill = 7;
+  for (uint32_t base = 0; base < full2; base += 128) {
+    uint32_t a0, a1, b0, b1;
+    bool na0, na1, nb0, nb1;
+    index(base, a0, a1);
+    eval_add(a0, a1, true, true, na0, na1);
+    index(base + 64u, b0, b1);
+    eval_add(b0, b1, true, true, nb0, nb1);
+    if (--spill == 0) {
+      lean_spill(c);
+      spill = 7;
+    }
+    if (__any_sync(kFull, na0 || na1 || nb0 || nb1)) {
+      push(na0, a0, na1, a1);
+      push(nb0, b0, nb1, b1);
+    }
+  }
+  lean_spill(c);  // <= 2 more steps below
+  if (full2 < full) {
+    uint32_t a0, a1;
+    bool na0, na1;
+    index(full2, a0, a1);
+    eval_add(a0, a1, true, true, na0, na1);
+    if (__any_sync(kFull, na0 || na1)) push(na0, a0, na1, a1);
+  }
+  if (full < total) {  // the last, partial step: slots past the end read the window, never added
+    uint32_t a0, a1;
+    bool na0, na1;
+    index(full, a0, a1);
+    const bool ok0 = full + lane < total, ok1 = full + 32u + lane < total;
+    if (!ok0) a0 = rs;
+    if (!ok1) a1 = rs;
+    eval_add(a0, a1, ok0, ok1, na0, na1);
+    if (__any_sync(kFull, na0 || na1)) push(na0, a0, na1, a1);
+  }
   while (st.et != st.eh)
     lean_exact_batch(A, Hs, min(32u, st.et - st.eh), ex, slot_lane, c, p0, p1, p2, Wn, st);
   lean_spill(c);
