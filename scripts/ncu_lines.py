@@ -7,7 +7,7 @@ The ncu csv (--page source --csv --print-source sass) lists the kernel's
 instructions in address order; nvdisasm -g of the same cubin gives the
 source line of each instruction offset.  Prints stall samples, warp
 instructions and the top stall reasons per source line, sorted by samples."""
-import collections, csv, re, sys
+import collections, csv, os, re, sys
 
 csv_path, dis_path, func = sys.argv[1], sys.argv[2], sys.argv[3]
 fsub = sys.argv[4] if len(sys.argv) > 4 else ''
@@ -26,7 +26,10 @@ for l in open(dis_path):
         continue
     m = re.search(r'//## File "([^"]+)", line (\d+)', l)
     if m:
-        if 'inlined at' not in l:
+        mi = re.search(r'inlined at "([^"]+)", line (\d+)', l)
+        if mi and os.environ.get('OUTER'):  # attribute helpers (nvdisasm -gi) to their call site
+            cur = (mi.group(1).split('/')[-1], int(mi.group(2)))
+        elif 'inlined at' not in l or os.environ.get('INNER'):
             cur = (m.group(1).split('/')[-1], int(m.group(2)))
         continue
     m = re.match(r'\s*/\*([0-9a-f]+)\*/\s+(.*?);', l)
