@@ -1454,7 +1454,10 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
 // (hit point, item) fragment writes its own partial row to HBM;
 // k_tile_finalize sums a hit point's rows in window order, so the result is
 // deterministic and identical to k_gather_fine's.
-constexpr int kRWarps = 16;
+#ifndef FPPM_RING_WARPS
+#define FPPM_RING_WARPS 16  // warps per CTA (12: 1.47 ms, larger windows but fewer warps)
+#endif
+constexpr int kRWarps = FPPM_RING_WARPS;
 constexpr int kRThreads = kRWarps * kWarp;
 
 template <int GMAX, int NB>
