@@ -22,6 +22,8 @@ struct fppm_gpu_ctx {
   // they overlap the sort and the gather's scheduling kernels
   cudaStream_t gstream = nullptr;
   cudaEvent_t ev_g_hdr = nullptr, ev_g_sorted = nullptr, ev_g_recs = nullptr;
+  cudaEvent_t ev_hdr = nullptr;  // the grid header's copy to the host
+  bool last_fork = false;        // the last build packed records on gstream (speculated for the next)
   bool recs_pending = false;
   unsigned long long hp_version = 0;  // bumped whenever hit points change
   std::string err;
@@ -622,7 +624,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (ctx->ev_free[i]) cudaEventDestroy(ctx->ev_free[i]);
   }
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
-  for (cudaEvent_t e : {ctx->ev_g_hdr, ctx->ev_g_sorted, ctx->ev_g_recs})
+  for (cudaEvent_t e : {ctx->ev_g_hdr, ctx->ev_g_sorted, ctx->ev_g_recs, ctx->ev_hdr})
     if (e) cudaEventDestroy(e);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   for (auto &pr : ctx->ev_k)
@@ -1163,7 +1165,27 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, 
                      S_req > 1 ? ctx->d_lean_ok : nullptr, ctx->d_hdr);
   FPPM_CUDA_OK(cudaGetLastError());
   FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_hdr, ctx->d_hdr, sizeof(GridHeader), cudaMemcpyDeviceToHost, s));
-  FPPM_CUDA_OK(cudaStreamSynchronize(s));
+  if (!ctx->ev_hdr) FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_hdr, cudaEventDisableTiming));
+  FPPM_CUDA_OK(cudaEventRecord(ctx->ev_hdr, s));
+  // Kernels that need only the device-side header are queued before the host
+  // waits for its copy, so the device stays busy over the round trip: the
+  // dense keys, and the record pack when the last build forked it (the
+  // layout decision repeats from build to build).
+  const bool spec = ctx->last_fork && ctx->recs.pack != nullptr && ctx->N > 0;
+  if (spec) {
+    if (!ctx->gstream) {
+      FPPM_CUDA_OK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+      FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_g_hdr, cudaEventDisableTiming));
+      FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_g_sorted, cudaEventDisableTiming));
+      FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_g_recs, cudaEventDisableTiming));
+    }
+    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_g_hdr, s));
+    FPPM_CUDA_OK(cudaStreamWaitEvent(ctx->gstream, ctx->ev_g_hdr, 0));
+    launch_pack_fine(ctx->gstream, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow, ctx->in_depth, ctx->N,
+                     ctx->d_hdr, ctx->cfg.normal_guard_cos, ctx->recs.pack, ctx->sms);
+  }
+  launch_dense_keys(s, ctx->in_pos, ctx->N, ctx->d_hdr, ctx->sort.keys_a, ctx->sort.vals_a, ctx->sms);
+  FPPM_CUDA_OK(cudaEventSynchronize(ctx->ev_hdr));
   const GridHeader g = *ctx->h_hdr;
   if (!(g.cell > 0.0)) return fail(ctx, FPPM_ERR_INVALID_ARGUMENT, "PhotonGrid: cell size must be positive");
   if (!g.ok) return fail(ctx, FPPM_ERR_CAPACITY, "grid bounding box exceeds max_cells dense cells");
@@ -1180,6 +1202,7 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, 
   // needs the sort) are built on gstream, overlapping the key sort here and
   // the gather's scheduling kernels; the next consumer joins (join_recs)
   const bool fork = fine_layout && ctx->recs.pack != nullptr && ctx->N > 0;
+  ctx->last_fork = fork;
   if (fork && !ctx->gstream) {
     FPPM_CUDA_OK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
     FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_g_hdr, cudaEventDisableTiming));
@@ -1187,13 +1210,17 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, 
     FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_g_recs, cudaEventDisableTiming));
   }
   cudaStream_t rs = fork ? ctx->gstream : s;
-  if (fork) {
+  if (fork && !spec) {
     FPPM_CUDA_OK(cudaEventRecord(ctx->ev_g_hdr, s));
     FPPM_CUDA_OK(cudaStreamWaitEvent(rs, ctx->ev_g_hdr, 0));
     launch_pack_fine(rs, ctx->in_pos, ctx->in_nrm, ctx->in_wi, ctx->in_pow, ctx->in_depth, ctx->N, ctx->d_hdr,
                      ctx->cfg.normal_guard_cos, ctx->recs.pack, ctx->sms);
+  } else if (spec && !fork) {
+    // a speculative pack that this layout does not use: nothing else may
+    // write the pack buffer before it has finished
+    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_g_recs, ctx->gstream));
+    FPPM_CUDA_OK(cudaStreamWaitEvent(s, ctx->ev_g_recs, 0));
   }
-  launch_dense_keys(s, ctx->in_pos, ctx->N, ctx->d_hdr, ctx->sort.keys_a, ctx->sort.vals_a, ctx->sms);
   FPPM_CUDA_OK(radix_sort_pairs(s, ctx->sort, ctx->N, g.key_bits, &ctx->d_skeys, &ctx->d_order));
   if (fork) {
     FPPM_CUDA_OK(cudaEventRecord(ctx->ev_g_sorted, s));
