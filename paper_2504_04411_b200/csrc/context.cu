@@ -23,6 +23,7 @@ struct fppm_gpu_ctx {
   cudaStream_t gstream = nullptr;
   cudaEvent_t ev_g_hdr = nullptr, ev_g_sorted = nullptr, ev_g_recs = nullptr;
   cudaEvent_t ev_hdr = nullptr;  // the grid header's copy to the host
+  cudaEvent_t ev_sched = nullptr;  // the fine schedule's totals copied to the host
   bool last_fork = false;        // the last build packed records on gstream (speculated for the next)
   bool recs_pending = false;
   unsigned long long hp_version = 0;  // bumped whenever hit points change
@@ -624,7 +625,7 @@ int fppm_gpu_destroy(fppm_gpu_ctx *ctx) {
     if (ctx->ev_free[i]) cudaEventDestroy(ctx->ev_free[i]);
   }
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
-  for (cudaEvent_t e : {ctx->ev_g_hdr, ctx->ev_g_sorted, ctx->ev_g_recs, ctx->ev_hdr})
+  for (cudaEvent_t e : {ctx->ev_g_hdr, ctx->ev_g_sorted, ctx->ev_g_recs, ctx->ev_hdr, ctx->ev_sched})
     if (e) cudaEventDestroy(e);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   for (auto &pr : ctx->ev_k)
@@ -1593,10 +1594,18 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
                                  cudaMemcpyDeviceToHost, s));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total + 1, S.pbase + nb, sizeof(uint32_t),
                                  cudaMemcpyDeviceToHost, s));
+    // the item descriptors are built speculatively into the current
+    // capacity (k_fine_desc / k_fine_order skip items past it) while the
+    // host waits for the totals; rebuilt below if the capacity was short
+    if (!ctx->ev_sched) FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_sched, cudaEventDisableTiming));
+    FPPM_CUDA_OK(cudaEventRecord(ctx->ev_sched, s));
+    const bool spec_items = S.fdesc != nullptr && S.item_cap > 0;
+    if (spec_items) FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48, fsub));
     const auto t2 = now();
-    FPPM_CUDA_OK(cudaStreamSynchronize(s));
+    FPPM_CUDA_OK(cudaEventSynchronize(ctx->ev_sched));
     const auto t3 = now();
     const uint32_t total = ctx->h_total[0];
+    const bool items_fit = total <= S.item_cap;
     if (dbg)
       std::fprintf(stderr, "[fppm] iteration %llu items %u rows %u (caps %llu %llu) crit %.3f sched-issue %.3f sync %.3f ms\n",
                    (unsigned long long)iteration, total, ctx->h_total[1], S.item_cap, S.row_cap, ms(t0, t1),
@@ -1627,7 +1636,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
     T.total_items = S.item_base + nb;
     T.contig = fsub == 1;
     {
-      FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48, fsub));
+      if (!spec_items || !items_fit) FPPM_CUDA_OK(fine_schedule_items(s, A, S, nb, ctx->sms, cap64, cap48, fsub));
       FineArgs F;
       F.desc = S.fdesc;
       F.hot = static_cast<const FineHot *>(S.fhot);

@@ -342,7 +342,8 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
                             const int4 *__restrict__ fbox, const uint32_t *__restrict__ item_base,
                             const uint32_t *__restrict__ prow_base, FineDesc *__restrict__ desc,
                             uint32_t *__restrict__ hp_map, uint32_t cap64, uint32_t cap48, uint32_t fsub,
-                            const uint32_t *__restrict__ hp_rbase, uint2 *__restrict__ hp_span) {
+                            const uint32_t *__restrict__ hp_rbase, uint2 *__restrict__ hp_span,
+                            unsigned long long item_cap) {
   constexpr int kWarps = 4;  // 128 threads
   constexpr int kWords = (int)(sizeof(FineDesc) / 4);
   __shared__ __align__(16) uint32_t s_d[kWarps][kWords];
@@ -410,8 +411,10 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
         }
         if (lane == 0) d.nclaim = n;  // ring: claim order filled by k_fine_order
         __syncwarp();
-        uint32_t *dst = reinterpret_cast<uint32_t *>(desc + item);
-        for (int k = lane; k < kWords; k += 32) dst[k] = s_d[wl][k];
+        if (item < item_cap) {  // a speculative build skips items past the capacity (the host rebuilds)
+          uint32_t *dst = reinterpret_cast<uint32_t *>(desc + item);
+          for (int k = lane; k < kWords; k += 32) dst[k] = s_d[wl][k];
+        }
         __syncwarp();
       }
       prow += rows_used;
@@ -427,9 +430,9 @@ __global__ void k_fine_desc(const GatherArgs A, const uint32_t *__restrict__ hp_
 // released (refilled) when the last warp leaves it.
 __global__ void __launch_bounds__(128) k_fine_order(FineDesc *__restrict__ desc, const uint32_t *__restrict__ total,
                                                     const FineHot *__restrict__ hot, const uint2 *__restrict__ hp_span,
-                                                    uint32_t cap) {
+                                                    uint32_t cap, unsigned long long item_cap) {
   const int lane = threadIdx.x & 31;
-  const uint32_t nitems = *total;
+  const uint32_t nitems = (uint32_t)min((unsigned long long)*total, item_cap);
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nitems; it += nw) {
     FineDesc &D = desc[it];
@@ -1790,11 +1793,11 @@ cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &
                                 uint32_t cap64, uint32_t cap48, uint32_t fsub) {
   k_fine_desc<<<fblocks((unsigned long long)nb * 32, 128, sms, 16), 128, 0, s>>>(
       A, S.hp_start, nb, S.hp_order, static_cast<FineHot *>(S.fhot), S.fbox,
-      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48, fsub, S.hp_rbase, S.hp_span);
+      S.item_base, S.pbase, S.fdesc, S.hp_map, cap64, cap48, fsub, S.hp_rbase, S.hp_span, S.item_cap);
   note_launches(1);
   if (fsub == 1) {
     k_fine_order<<<(unsigned)sms * 8, 128, 0, s>>>(S.fdesc, S.item_base + nb, static_cast<const FineHot *>(S.fhot),
-                                                 S.hp_span, cap48);
+                                                 S.hp_span, cap48, S.item_cap);
     note_launches(1);
   }
   return cudaGetLastError();
