@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256)
     }
     if (i < n) {
       float4 q0, q1, q2, q3;
-      float4 *d = pack + 4 * (size_t)i;
+      float4 *d = pack + (lean ? 3 : 4) * (size_t)i;  // lean records packed 48 B apart
       if (lean) {
         lean_record(P, guard, q0, q1, q2);
       } else {
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256)
     float4 q[U][4];
 #pragma unroll
     for (uint32_t u = 0; u < U; ++u) {
-      const float4 *src = pack + 4 * (size_t)o[u];
+      const float4 *src = pack + (rec3 ? 4 : 3) * (size_t)o[u];
       if (i0 + u * stride < n) {
         q[u][0] = __ldg(&src[0]); q[u][1] = __ldg(&src[1]); q[u][2] = __ldg(&src[2]);
         if (rec3) q[u][3] = __ldg(&src[3]);
