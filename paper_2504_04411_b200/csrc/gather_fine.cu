@@ -1176,6 +1176,9 @@ static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, dou
     row_put<STORE>(acc[(3 * GMAX + 1) * fs], p1);
     row_put<STORE>(acc[(3 * GMAX + 2) * fs], p2);
   }
+  if constexpr (STORE && partial_size(GMAX, 1) > 3 * GMAX + 3) {
+    if (lane == 1) acc[(3 * GMAX + 3) * fs] = 0.0;  // the pad field: whole sectors written
+  }
   __syncwarp();
 }
 
