@@ -287,17 +287,32 @@ static_assert(kRadixMax == 2 * kSortThreads, "two digits per thread in the tile 
 __global__ void __launch_bounds__(kSortThreads)
     k_radix_upsweep(const uint32_t *__restrict__ keys, uint32_t n, int shift, uint32_t mask,
                     uint32_t *__restrict__ hist /* [digit][tile] */, uint32_t tiles) {
-  __shared__ uint32_t s_h[kRadixMax];
-  for (int d = threadIdx.x; d < kRadixMax; d += blockDim.x) s_h[d] = 0;
+  // per-warp sub-histograms: clustered keys (a photon blob) contend only
+  // within a warp; all loads are issued before the counting
+  constexpr int kWarps = kSortThreads / kWarp;
+  __shared__ uint32_t s_h[kWarps][kRadixMax];
+  for (int d = threadIdx.x; d < kWarps * kRadixMax; d += blockDim.x) (&s_h[0][0])[d] = 0;
   __syncthreads();
   const uint32_t base = blockIdx.x * kTile;
-#pragma unroll 4
+  const int warp = threadIdx.x / kWarp;
+  uint32_t k[kSortItems];
+#pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
     const uint32_t i = base + it * kSortThreads + threadIdx.x;
-    if (i < n) atomicAdd(&s_h[(keys[i] >> shift) & mask], 1u);
+    k[it] = i < n ? __ldcs(&keys[i]) : 0xffffffffu;
+  }
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint32_t i = base + it * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&s_h[warp][(k[it] >> shift) & mask], 1u);
   }
   __syncthreads();
-  for (uint32_t d = threadIdx.x; d <= mask; d += blockDim.x) hist[d * tiles + blockIdx.x] = s_h[d];
+  for (uint32_t d = threadIdx.x; d <= mask; d += blockDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) c += s_h[w][d];
+    hist[d * tiles + blockIdx.x] = c;
+  }
 }
 
 // block d: total of digit d over all tiles
@@ -425,6 +440,18 @@ __global__ void __launch_bounds__(kSortThreads)
 
 // ------------------------------------------------------------------ cell table
 // start[c] = first sorted position with dense id >= c, c in [0, ncells].
+// Dense tables (every gap short): thread per photon writes its own gap.
+__global__ void k_cell_start_dense(const uint32_t *__restrict__ skeys, uint32_t n, unsigned long long ncells,
+                                   uint32_t *__restrict__ start) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long k = skeys[i];
+    const unsigned long long prev = i == 0 ? 0ull : (unsigned long long)skeys[i - 1] + 1ull;
+    for (unsigned long long c = prev; c <= k; ++c) start[c] = i;
+    if (i == n - 1)
+      for (unsigned long long c = k + 1; c <= ncells; ++c) start[c] = n;
+  }
+}
+
 // Any table: photon i owns the cells (key[i - 1], key[i]] (start = i) and the
 // last photon also (key[n - 1], ncells] (start = n).  Short gaps are written
 // by their owner lane; long ones (empty stretches of a sparse or clustered
@@ -664,6 +691,10 @@ void launch_cell_start(cudaStream_t s, const uint32_t *skeys, uint32_t n, const 
                        uint32_t *start, unsigned long long ncells, int sms) {
   if (n == 0) {
     k_cell_start_empty<<<1, 32, 0, s>>>(start, ncells);
+  } else if ((unsigned long long)n >= 4ull * ncells) {
+    // >= 4 photons per cell on average: thread per photon (a long gap at the
+    // end is walked by the last photon, so only for tables this dense)
+    k_cell_start_dense<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(skeys, n, ncells, start);
   } else {
     k_cell_start_gaps<<<cap_blocks(n, 256, sms, 16), 256, 0, s>>>(skeys, n, ncells, start);
   }
