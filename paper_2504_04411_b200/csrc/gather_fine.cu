@@ -981,14 +981,18 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
       i0 = v0 + o;
       i1 = v1 + o;
       int k = j;
-      uint32_t ek = e;
+      uint32_t ek = e, okk = o;
       while (ek < base + 64u && k + 1 < nruns) {
         ++k;
-        const uint32_t ok_ = __shfl_sync(kFull, off, k);
-        if (v0 >= ek) i0 = v0 + ok_;
-        if (v1 >= ek) i1 = v1 + ok_;
+        okk = __shfl_sync(kFull, off, k);
+        if (v0 >= ek) i0 = v0 + okk;
+        if (v1 >= ek) i1 = v1 + okk;
         ek = __shfl_sync(kFull, incl, k);
       }
+      // carry on from the run that holds the step's last slot
+      j = k;
+      e = ek;
+      o = okk;
     }
   };
   // evaluate + accumulate the two candidates; their band flags out
