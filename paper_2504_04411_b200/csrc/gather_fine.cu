@@ -965,8 +965,12 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
   const uint32_t off = rs - (incl - rl);  // smem index - virtual index within run `lane`
   const uint32_t total = __shfl_sync(kFull, incl, 31);
   if (lane == 0) st.n_cand += total;
-  int j = 0;
-  uint32_t e = __shfl_sync(kFull, incl, 0), o = __shfl_sync(kFull, off, 0);
+  // the runs that meet this window are consecutive (the window is a range of
+  // the flattened union): track from the first to the last non-empty one
+  const uint32_t nem = __ballot_sync(kFull, rl != 0u);
+  int j = nem ? __ffs(nem) - 1 : 0;
+  nruns = nem ? 32 - __clz(nem) : 0;
+  uint32_t e = __shfl_sync(kFull, incl, j), o = __shfl_sync(kFull, off, j);
   // candidates v0 = base + lane and v1 = v0 + 32 of a step -> window indices
   auto index = [&](uint32_t base, uint32_t &i0, uint32_t &i1) {
     const uint32_t v0 = base + lane, v1 = v0 + 32u;
