@@ -1021,22 +1021,21 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
   // two full steps per iteration: one spill count, one band vote (a nibble
   // takes <= 2 increments per iteration: spill every 7)
   const uint32_t full = total & ~63u, full2 = total & ~127u;
-  uint32_t spill = 7;
-  for (uint32_t base = 0; base < full2; base += 128) {
-    uint32_t a0, a1, b0, b1;
-    bool na0, na1, nb0, nb1;
-    index(base, a0, a1);
-    eval_add(a0, a1, true, true, na0, na1);
-    index(base + 64u, b0, b1);
-    eval_add(b0, b1, true, true, nb0, nb1);
-    if (--spill == 0) {
-      lean_spill(c);
-      spill = 7;
+  for (uint32_t blk = 0; blk < full2; blk += 7u * 128u) {  // 7 iterations between spills
+    const uint32_t blk_end = min(full2, blk + 7u * 128u);
+    for (uint32_t base = blk; base < blk_end; base += 128) {
+      uint32_t a0, a1, b0, b1;
+      bool na0, na1, nb0, nb1;
+      index(base, a0, a1);
+      eval_add(a0, a1, true, true, na0, na1);
+      index(base + 64u, b0, b1);
+      eval_add(b0, b1, true, true, nb0, nb1);
+      if (__any_sync(kFull, na0 || na1 || nb0 || nb1)) {
+        push(na0, a0, na1, a1);
+        push(nb0, b0, nb1, b1);
+      }
     }
-    if (__any_sync(kFull, na0 || na1 || nb0 || nb1)) {
-      push(na0, a0, na1, a1);
-      push(nb0, b0, nb1, b1);
-    }
+    lean_spill(c);
   }
   lean_spill(c);  // <= 2 more steps below
   if (full2 < full) {
