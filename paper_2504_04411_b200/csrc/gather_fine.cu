@@ -1131,10 +1131,14 @@ static __device__ __forceinline__ void lean_reduce(uint32_t slots, int lane, dou
   const int col = lane % NC, grp = lane / NC;
   double sm = 0.0, sq = 0.0;
   {
-    const uint32_t base = slots + (uint32_t)(col * 32 + grp * R) * 16u;
-#pragma unroll 4
+    // rows visited in an XOR-swizzled fixed order (lanes of different
+    // columns hit different rows at each step: no bank conflicts); the
+    // group's R rows are R * 16-B aligned, so the swizzle is one LOP3 per row
+    static_assert(R == NC && (R & (R - 1)) == 0, "slot groups of R = NC rows, a power of two");
+    const uint32_t base = (slots + (uint32_t)(col * 32 + grp * R) * 16u) | ((uint32_t)col * 16u);
+#pragma unroll
     for (int i = 0; i < R; ++i) {
-      const uint32_t a = base + (uint32_t)((i + col) % R) * 16u;
+      const uint32_t a = base ^ ((uint32_t)i * 16u);
       const double2 v = lds_f64x2(a);
       sm += v.x;
       sq += v.y;
