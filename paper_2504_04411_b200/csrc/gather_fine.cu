@@ -952,7 +952,10 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
   LeanHit F;
   F.chx = Hh.F.chx; F.chy = Hh.F.chy; F.chz = Hh.F.chz;
   F.lim_hi = Hh.F.lim_hi; F.lim_lo = Hh.F.lim_lo; F.band_y = Hh.F.band_y;
-  F.qa_edge = 1.0f / Hh.F.qa_scale;  // n_a = 2: qa_scale = 2 / r2
+  // n_a = 2: the annulus edge yy = r2 / 2, from lim_hi + lim_lo = 2 r2 (up to
+  // an ulp; the 2e-4 band covers it; without the fp32 fast path every pair
+  // is banded by the ball test anyway)
+  F.qa_edge = 0.25f * (Hh.F.lim_hi + Hh.F.lim_lo);
   F.qa_eps = 2e-4f * F.qa_edge;
   F.mlim = Hh.mlim;
   const uint32_t d1 = Wn.r1 - Wn.r0, d2 = Wn.r2 - Wn.r0;
