@@ -838,7 +838,7 @@ __device__ __forceinline__ EyeV eyev_load(const BidirArgs &B, uint32_t k, uint32
 #define FPPM_EYE_MINB 4   // walk: 120 registers, no spills
 #endif
 #ifndef FPPM_BIDIR_MINB
-#define FPPM_BIDIR_MINB 3  // vertex loop: 166 registers, no spills
+#define FPPM_BIDIR_MINB 4  // vertex loop: 128 registers + a small spill beat 166 at 3 CTAs (C4: 2.56 vs 2.64 ms)
 #endif
 // trace_eye_subpath (path.cpp:331-386) for every pixel: the vertices to HBM,
 // the vertex count and the RNG state the vertex loop continues from.
