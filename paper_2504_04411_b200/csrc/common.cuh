@@ -62,6 +62,9 @@ struct GridHeader {
   uint32_t S;      // fine cells per reference cell and axis (power of two; 1 = reference cells)
   uint32_t shift;  // log2(S)
   uint32_t lean;   // 1: lean planar records (rec0 = x, y, z, meta; rec1 = L, b; rec2 = r, g; fp64 pairs)
+                   // 2: flat lean records, 32 B (every photon has z == zflat; flat_record)
+  float zflat;     // lean == 2: the photons' common z
+  uint32_t pad_;
 };
 // With S > 1 the dense table indexes FINE cells of size cell / S ("slab"
 // layout, used when the photons span few reference cells along z): inv is
@@ -190,6 +193,32 @@ __device__ __forceinline__ void lean_record(const float *__restrict__ pos, const
                                             const uint32_t *__restrict__ depth, size_t j, double guard, float4 &q0,
                                             float4 &q1, float4 &q2) {
   lean_record(load_photon(pos, nrm, wi, pw, depth, j), guard, q0, q1, q2);
+}
+
+// Flat lean record (GridHeader::lean == 2): the lean record of a frame whose
+// photons all share one z (bit-identical fp32, k_cell_bounds): z leaves the
+// record (the ball's dz is a per-hit-point constant) and the power stays in
+// the ABI's fp32, widened exactly in the gather:
+//   rec0 = (x, y, meta, pow.r), rec1 = (lum(pow) as fp64 lo/hi, pow.g, pow.b)
+// with meta, the cos_i zeroing and the exact flag (x = NaN) of lean_record.
+__device__ __forceinline__ void flat_record(const PhotonIn &P, double guard, float4 &q0, float4 &q1) {
+  const float nx = P.n[0], ny = P.n[1], wx = P.w[0], wy = P.w[1];
+  const uint32_t d = P.d;
+  float r = P.c[0], g = P.c[1], b = P.c[2];
+  double L = elum((double)r, (double)g, (double)b);
+  const bool exact = !(fabsf(nx) < INFINITY && fabsf(ny) < INFINITY && fabsf(wx) < INFINITY &&
+                       fabsf(wy) < INFINITY) || d >= (1u << 23) || !(fabs(L) < INFINITY) ||
+                     !(fabsf(r) < INFINITY && fabsf(g) < INFINITY && fabsf(b) < INFINITY);
+  const bool guard_fail = (double)P.n[2] < guard;
+  const bool cos_pos = !(P.w[2] <= 0.0f);
+  if (!cos_pos) {
+    r = g = b = 0.0f;
+    L = 0.0;
+  }
+  const uint32_t meta = exact ? 0u : ((d << 8) | (guard_fail ? 0x80000000u : 0u));
+  q0 = make_float4(exact ? __int_as_float(0x7fffffff) : P.p[0], P.p[1], __uint_as_float(meta), r);
+  q1 = make_float4(__uint_as_float((uint32_t)__double_as_longlong(L)),
+                   __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(L) >> 32)), g, b);
 }
 
 // exclusive scan of one value per thread over a 256-thread block; returns the

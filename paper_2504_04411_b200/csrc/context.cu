@@ -504,12 +504,12 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
   A(dalloc(&ctx->sort.keys_a, Nc)); A(dalloc(&ctx->sort.vals_a, Nc));
   A(dalloc(&ctx->sort.keys_b, Nc)); A(dalloc(&ctx->sort.vals_b, Nc));
   A(dalloc(&ctx->sort.hist, radix_hist_entries((uint32_t)Nc)));
-  A(dalloc(&ctx->d_hdr, 1)); A(dalloc(&ctx->d_bounds, 6)); A(dalloc(&ctx->d_cell, 1));
+  A(dalloc(&ctx->d_hdr, 1)); A(dalloc(&ctx->d_bounds, 8)); A(dalloc(&ctx->d_cell, 1));
   A(dalloc(&ctx->d_cell_chk, 1));
   A(dalloc(&ctx->d_lean_ok, 1));
   A(cudaMemset(ctx->d_lean_ok, 0, sizeof(uint32_t)));
   A(cudaMallocHost(&ctx->h_hdr, sizeof(GridHeader)));
-  A(cudaMallocHost(&ctx->h_bounds_init, sizeof(long long) * 6));
+  A(cudaMallocHost(&ctx->h_bounds_init, sizeof(long long) * 8));
   A(cudaMallocHost(&ctx->h_cell, sizeof(double)));
   A(cudaMallocHost(&ctx->h_counters, sizeof(unsigned long long) * 8));
   A(dalloc(&ctx->o_gather_r, Hc)); A(dalloc(&ctx->o_stat, Hc)); A(dalloc(&ctx->o_crit, Hc));
@@ -547,6 +547,8 @@ int fppm_gpu_create(const fppm_gpu_config *config, fppm_gpu_ctx **out) {
     ctx->h_bounds_init[a] = LLONG_MAX;
     ctx->h_bounds_init[3 + a] = LLONG_MIN;
   }
+  ctx->h_bounds_init[6] = LLONG_MAX;  // the photons' z bit patterns (k_cell_bounds)
+  ctx->h_bounds_init[7] = LLONG_MIN;
   cudaMemsetAsync(ctx->d_counters, 0, sizeof(unsigned long long) * 4, ctx->stream);
   if (c.policy == FPPM_POLICY_CHI2) {
     int st = 0;
@@ -1153,7 +1155,7 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, 
     int rc = device_max_radius(ctx, ctx->d_cell);  // integrator.cpp:159-161
     if (rc) return rc;
   }
-  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_bounds, ctx->h_bounds_init, sizeof(long long) * 6,
+  FPPM_CUDA_OK(cudaMemcpyAsync(ctx->d_bounds, ctx->h_bounds_init, sizeof(long long) * 8,
                                cudaMemcpyHostToDevice, s));
   if (!ctx->in_pos) use_staging(ctx);
   const int reading = ctx->stage_pending >= 0 ? ctx->stage_pending : -1;
@@ -1163,7 +1165,7 @@ static int build_grid_impl(fppm_gpu_ctx *ctx, double cell_size, uint32_t S_req, 
   }
   launch_cell_bounds(s, ctx->in_pos, ctx->N, ctx->d_cell, S_req, ctx->d_bounds, ctx->sms);
   launch_grid_header(s, ctx->d_bounds, ctx->d_cell, ctx->N, ctx->cfg.max_cells, S_req,
-                     S_req > 1 ? ctx->d_lean_ok : nullptr, ctx->d_hdr);
+                     S_req > 1 ? ctx->d_lean_ok : nullptr, flat_records_enabled(), ctx->d_hdr);
   FPPM_CUDA_OK(cudaGetLastError());
   FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_hdr, ctx->d_hdr, sizeof(GridHeader), cudaMemcpyDeviceToHost, s));
   if (!ctx->ev_hdr) FPPM_CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_hdr, cudaEventDisableTiming));
@@ -1587,7 +1589,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
     uint32_t nb = 0;
     // the fine-cell tiled kernel (slab grids, G * C <= 24)
     uint32_t cap64 = 0, cap48 = 0, fsub = 0;
-    fine_caps(ctx->G, ctx->C, g.lean != 0u, &cap64, &cap48, &fsub);
+    fine_caps(ctx->G, ctx->C, (int)g.lean, &cap64, &cap48, &fsub);
     FPPM_CUDA_OK(cudaMemsetAsync(S.nonempty, 0, sizeof(uint32_t), s));
     FPPM_CUDA_OK(fine_schedule_bins(s, A, S, g, ctx->sms, cap64, cap48, fsub, &nb, ctx->hp_version));
     FPPM_CUDA_OK(cudaMemcpyAsync(ctx->h_total, S.item_base + nb, sizeof(uint32_t),
@@ -1648,7 +1650,7 @@ static int gather_impl(fppm_gpu_ctx *ctx, uint64_t iteration, fppm_gpu_iter_out 
       T.desc = nullptr;
       JOIN_RECS(ctx);  // the records built on gstream
       if ((rc = kernel_event(ctx, 0))) return rc;
-      FPPM_CUDA_OK(launch_gather_fine(s, A, F, ctx->C, ctx->sms, g.lean != 0u));
+      FPPM_CUDA_OK(launch_gather_fine(s, A, F, ctx->C, ctx->sms, (int)g.lean));
       if ((rc = kernel_event(ctx, 1))) return rc;
     }
     FPPM_CUDA_OK(launch_tile_finalize(s, A, T, ctx->C, ctx->sms));

@@ -185,16 +185,16 @@ cudaError_t launch_cull_packed(cudaStream_t s, const uint32_t *data, unsigned lo
                                uint32_t *dst, uint32_t *scan_tmp, float *pos, float *nrm, float *wi, float *pw,
                                uint32_t *depth, int sms);
 bool fine_supported(int G, int C);
-void fine_caps(int G, int C, bool lean, uint32_t *cap64, uint32_t *cap48, uint32_t *fsub);
+void fine_caps(int G, int C, int lean, uint32_t *cap64, uint32_t *cap48, uint32_t *fsub);  // lean: GridHeader::lean
+bool flat_records_enabled();  // the 32-B flat lean layout may be chosen (ring kernel on, FPPM_FLAT != 0)
 bool ring_enabled();
-int ring_buffers();
 cudaError_t fine_schedule_bins(cudaStream_t s, const GatherArgs &A, TileSched &S, const GridHeader &g,
                                int sms, uint32_t cap64, uint32_t cap48, uint32_t fsub, uint32_t *nb_out,
                                unsigned long long hp_version);
 cudaError_t fine_schedule_items(cudaStream_t s, const GatherArgs &A, TileSched &S, uint32_t nb, int sms,
                                 uint32_t cap64, uint32_t cap48, uint32_t fsub);
 size_t fine_acc_doubles(int G, int C);
-cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms, bool lean);
+cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms, int lean);
 size_t fine_hot_bytes();
 size_t fine_hit_bytes();
 
@@ -235,7 +235,8 @@ cudaError_t radix_sort_pairs(cudaStream_t s, SortScratch &sc, uint32_t n, uint32
 void launch_cell_bounds(cudaStream_t s, const float *pos, uint32_t n, const double *cell,
                         uint32_t S, long long *bounds, int sms);
 void launch_grid_header(cudaStream_t s, const long long *bounds, const double *cell, uint32_t n,
-                        unsigned long long max_cells, uint32_t S, const uint32_t *lean_ok, GridHeader *hdr);
+                        unsigned long long max_cells, uint32_t S, const uint32_t *lean_ok, bool allow_flat,
+                        GridHeader *hdr);
 void launch_dense_keys(cudaStream_t s, const float *pos, uint32_t n, const GridHeader *hdr,
                        uint32_t *keys, uint32_t *vals, int sms);
 void launch_pack_fine(cudaStream_t s, const float *pos, const float *nrm, const float *wi, const float *pw,

@@ -827,29 +827,44 @@ struct LeanPair {
 // Hit-point constants of the lean loop.
 struct LeanHit {
   float chx, chy, chz, lim_hi, lim_lo, band_y, qa_edge, qa_eps;  // annulus edge yy = r2 / 2 and its band
+                                                                 // (FLAT: chz holds dz = zflat - centre z)
   uint32_t mlim;
 };
 
 // fp32 evaluation of one candidate (records at a0, a0 + d1, a0 + d2): ball,
 // depth, guard, disk, annulus, quadrant, cos_i with the error bands of
 // fine_eval<PLANAR>; band or exact-flagged photons -> need.
-template <int NA>
+template <int NA, bool FLAT>
 static __device__ __forceinline__ LeanPair lean_eval(const LeanHit &F, bool valid, uint32_t a0, uint32_t d1,
                                                      uint32_t d2) {
   LeanPair q;
   const float4 p = lds128_f(a0);
-  const double2 LB = lds_f64x2(a0 + d1);
-  const double2 RG = lds_f64x2(a0 + d2);
-  q.L = LB.x;
-  q.b = LB.y;
-  q.r = RG.x;
-  q.g = RG.y;
-  const float dx = p.x - F.chx, dy = p.y - F.chy, dz = p.z - F.chz;
+  float dz;
+  uint32_t meta;
+  if constexpr (FLAT) {  // (x, y, meta, r) | (L, g, b): the power widens exactly
+    const float4 w = lds128_f(a0 + d1);
+    q.L = __hiloint2double(__float_as_int(w.y), __float_as_int(w.x));
+    q.r = (double)p.w;
+    q.g = (double)w.z;
+    q.b = (double)w.w;
+    dz = F.chz;  // zflat - centre z, the same subtraction for every record
+    meta = __float_as_uint(p.z);
+  } else {
+    const double2 LB = lds_f64x2(a0 + d1);
+    const double2 RG = lds_f64x2(a0 + d2);
+    q.L = LB.x;
+    q.b = LB.y;
+    q.r = RG.x;
+    q.g = RG.y;
+    dz = p.z - F.chz;
+    meta = __float_as_uint(p.w);
+  }
+  const float dx = p.x - F.chx, dy = p.y - F.chy;
   const float yy = fmaf(dx, dx, dy * dy);
   const float r2 = fmaf(dz, dz, yy);
   // depth (integrator.cpp:396) + guard (:397) in one compare; ball
   // (photon_map.cpp:76): NaN (an exact-flagged record) passes into the band
-  const bool maybe = valid && __float_as_uint(p.w) <= F.mlim && !(r2 > F.lim_hi);
+  const bool maybe = valid && meta <= F.mlim && !(r2 > F.lim_hi);
   bool band = !(r2 < F.lim_lo) || !(fabsf(dx) > F.band_y) || !(fabsf(dy) > F.band_y);
   // quadrant (exact-sector table): +x+y 0, -x+y 1, -x-y 2, +x-y 3
   uint32_t s4 = dy > 0.0f ? (dx > 0.0f ? 0u : 4u) : (dx > 0.0f ? 12u : 8u);
@@ -942,15 +957,17 @@ static __device__ __forceinline__ void lean_exact_batch(const GatherArgs &A, con
 // per step.  Virtual index v in [0, total) over the concatenated runs maps to
 // the smem index v + off[j] of run j; the run is tracked warp-uniformly and a
 // step only resolves per lane when a run ends inside it.
-template <int NA>
+template <int NA, bool FLAT = false>
 static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const FineHot &Hh, const Hit &Hs,
                                                      uint32_t rs, uint32_t rl, int nruns, uint32_t ex,
                                                      uint32_t slot_lane, LeanCnt &c, double &p0, double &p1,
-                                                     double &p2, const FineWin &Wn, FineState &st) {
+                                                     double &p2, const FineWin &Wn, FineState &st,
+                                                     float zflat = 0.0f) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
   LeanHit F;
   F.chx = Hh.F.chx; F.chy = Hh.F.chy; F.chz = Hh.F.chz;
+  if constexpr (FLAT) F.chz = zflat - Hh.F.chz;
   F.lim_hi = Hh.F.lim_hi; F.lim_lo = Hh.F.lim_lo; F.band_y = Hh.F.band_y;
   // n_a = 2: the annulus edge yy = r2 / 2, from lim_hi + lim_lo = 2 r2 (up to
   // an ulp; the 2e-4 band covers it; without the fp32 fast path every pair
@@ -1004,8 +1021,8 @@ static __device__ __forceinline__ void lean_fragment(const GatherArgs &A, const 
   };
   // evaluate + accumulate the two candidates; their band flags out
   auto eval_add = [&](uint32_t i0, uint32_t i1, bool ok0, bool ok1, bool &n0, bool &n1) {
-    const LeanPair q0 = lean_eval<NA>(F, ok0, Wn.r0 + i0 * 16u, d1, d2);
-    const LeanPair q1 = lean_eval<NA>(F, ok1, Wn.r0 + i1 * 16u, d1, d2);
+    const LeanPair q0 = lean_eval<NA, FLAT>(F, ok0, Wn.r0 + i0 * 16u, d1, d2);
+    const LeanPair q1 = lean_eval<NA, FLAT>(F, ok1, Wn.r0 + i1 * 16u, d1, d2);
     lean_add(q0, slot_lane, c.n0, p0, p1, p2);
     lean_add(q1, slot_lane, c.n1, p0, p1, p2);
     n0 = q0.need;
@@ -1477,11 +1494,15 @@ __global__ void __launch_bounds__(kFThreads, FineLayout<GMAX, CH>::kMinBlocks)
 #ifndef FPPM_RING_WARPS
 #define FPPM_RING_WARPS 16  // warps per CTA (12: 1.47 ms, larger windows but fewer warps)
 #endif
+#ifndef FPPM_RING_CAPDIV
+#define FPPM_RING_CAPDIV 48  // measurement knob: > 48 shrinks the windows (records stay 48 B)
+#endif
 constexpr int kRWarps = FPPM_RING_WARPS;
 constexpr int kRThreads = kRWarps * kWarp;
 
-template <int GMAX, int NB>
+template <int GMAX, int NB, bool FLAT = false>
 struct RingLayout {
+  static constexpr uint32_t kRec = FLAT ? 32u : 48u;  // staged bytes per record
   static constexpr int NC = GMAX;  // lean: C = 1
   static constexpr int PS = partial_size(GMAX, 1);
   static constexpr size_t kSlotBytes = (size_t)kRWarps * (NC + 1) * 32 * 16;
@@ -1489,8 +1510,8 @@ struct RingLayout {
   static constexpr size_t kStatic = (size_t)kRWarps * kFExact * 4 + 2 * NB * sizeof(FineDesc) + 64 * NB + 64;
   static constexpr size_t kBudget = (size_t)233472 - 1024 - kStatic - 256;
   static constexpr uint32_t kCap =
-      (uint32_t)((((kBudget - kSlotBytes - NB * kHotBytes) / NB) / 48) & ~(size_t)31);
-  static constexpr size_t kBufBytes = (size_t)kCap * 48;  // rec0 | rec1 | rec2, 16 B each
+      (uint32_t)((((kBudget - kSlotBytes - NB * kHotBytes) / NB) / (FLAT ? 32 : FPPM_RING_CAPDIV)) & ~(size_t)31);
+  static constexpr size_t kBufBytes = (size_t)kCap * kRec;  // rec0 | rec1 [| rec2], 16 B each
   static constexpr size_t kDynBytes = NB * kBufBytes + kSlotBytes + NB * kHotBytes;
 };
 
@@ -1526,11 +1547,11 @@ static __device__ __forceinline__ void ring_preclaim(uint32_t b, const GatherArg
 // hit points + record pieces by TMA, completing on full[b]), then pre-claim
 // the item for b's following turn.  An item past the end arrives without
 // data: the consumers read R.item and skip it.
-template <int GMAX, int NB>
+template <int GMAX, int NB, bool FLAT>
 static __device__ __forceinline__ void ring_fill(uint32_t b, const GatherArgs &A, const FineArgs &T,
                                                  uint32_t total_items, RingShared<NB> &R,
                                                  unsigned char *buf, FineHot *hot) {
-  using Lay = RingLayout<GMAX, NB>;
+  using Lay = RingLayout<GMAX, NB, FLAT>;
   const int lane = threadIdx.x & 31;
   const uint32_t item = R.pitem[b];
   if (lane == 0) {
@@ -1552,7 +1573,7 @@ static __device__ __forceinline__ void ring_fill(uint32_t b, const GatherArgs &A
     if (lane == 0) {
       R.dphase[b] ^= 1u;
       fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&R.full[b], (hi - lo) * 48u + hot_bytes);
+      mbar_arrive_expect_tx(&R.full[b], (hi - lo) * Lay::kRec + hot_bytes);
     }
     __syncwarp();
     if (lane == 31) bulk_g2s(hot, T.hot + D.hp_lo, hot_bytes, &R.full[b]);
@@ -1563,7 +1584,8 @@ static __device__ __forceinline__ void ring_fill(uint32_t b, const GatherArgs &A
         const uint32_t sp = D.src[p] + (a - D.pre[p]), dp = a - lo, n = e - a;
         bulk_g2s(buf + (size_t)dp * 16, A.rec0 + sp, n * 16u, &R.full[b]);
         bulk_g2s(buf + (size_t)(Lay::kCap + dp) * 16, A.rec1 + sp, n * 16u, &R.full[b]);
-        bulk_g2s(buf + (size_t)(2 * Lay::kCap + dp) * 16, A.rec2 + sp, n * 16u, &R.full[b]);
+        if constexpr (!FLAT)
+          bulk_g2s(buf + (size_t)(2 * Lay::kCap + dp) * 16, A.rec2 + sp, n * 16u, &R.full[b]);
       }
     }
     __syncwarp();
@@ -1575,9 +1597,9 @@ static __device__ __forceinline__ void ring_fill(uint32_t b, const GatherArgs &A
   __syncwarp();
 }
 
-template <int GMAX, int NB>
+template <int GMAX, int NB, bool FLAT>
 __global__ void __launch_bounds__(kRThreads, 1) k_gather_ring(const GatherArgs A, const FineArgs T) {
-  using Lay = RingLayout<GMAX, NB>;
+  using Lay = RingLayout<GMAX, NB, FLAT>;
   constexpr int NC = Lay::NC, PS = Lay::PS, NA = GMAX / 4;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *s_slots = reinterpret_cast<double *>(smem_raw + NB * Lay::kBufBytes);
@@ -1604,7 +1626,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_gather_ring(const GatherArgs A
   __syncthreads();
   if (warp == 0)
     for (int b = 0; b < NB; ++b)
-      ring_fill<GMAX, NB>(b, A, T, total_items, R, smem_raw + b * Lay::kBufBytes, s_hot + b * kFWave);
+      ring_fill<GMAX, NB, FLAT>(b, A, T, total_items, R, smem_raw + b * Lay::kBufBytes, s_hot + b * kFWave);
   FineState st = {0, 0, 0, 0, 0, 0, 0, 0};
 
   uint32_t dead = 0;  // consecutive positions past the end
@@ -1670,7 +1692,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_gather_ring(const GatherArgs A
         LeanCnt lc = {0u, 0u, 0u, 0u};
         const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
         if (Hh.gray & 2u) {
-          lean_fragment<NA>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st);
+          lean_fragment<NA, FLAT>(A, Hh, Hs, rs, rl, nr, exa, slot_lane, lc, p0, p1, p2, Wn, st, g.zflat);
           lean_reduce<GMAX, true>(slots, lane, Hh.K0, lc, p0, p1, p2, acc, st, fs);
         } else {
           exact_fragment_lean<NA>(A, Hh, Hs, rs, rl, slot_lane, lc, p0, p1, p2, Wn, st);
@@ -1686,7 +1708,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_gather_ring(const GatherArgs A
     if (lane == 0) left = atom_add_smem(&R.left[b], 1u);
     left = __shfl_sync(kFull, left, 0);
     if (left == kRWarps - 1)
-      ring_fill<GMAX, NB>(b, A, T, total_items, R, smem_raw + b * Lay::kBufBytes, s_hot + b * kFWave);
+      ring_fill<GMAX, NB, FLAT>(b, A, T, total_items, R, smem_raw + b * Lay::kBufBytes, s_hot + b * kFWave);
     // A position's item was claimed when position q - 2 NB was left, and every
     // claim after one past the end is past the end: after 2 NB dead positions
     // in a row no later position holds an item.
@@ -1722,7 +1744,7 @@ bool fine_supported(int G, int C) {
   return gmax * C <= 24;
 }
 
-void fine_caps(int G, int C, bool lean, uint32_t *cap64, uint32_t *cap48, uint32_t *fsub) {
+void fine_caps(int G, int C, int lean, uint32_t *cap64, uint32_t *cap48, uint32_t *fsub) {
 #define FPPM_CAPS(gm, ch) \
   do {                    \
     *cap64 = FineLayout<gm, ch>::kCap64; \
@@ -1730,8 +1752,7 @@ void fine_caps(int G, int C, bool lean, uint32_t *cap64, uint32_t *cap48, uint32
   } while (0)
   *fsub = kFSub;
   if (lean && ring_enabled()) {  // k_gather_ring: items of one window, 48-B records
-    const int nb = ring_buffers();
-    if (nb == 3) *cap48 = *cap64 = (G <= 4) ? RingLayout<4, 3>::kCap : RingLayout<8, 3>::kCap;
+    if (lean == 2) *cap48 = *cap64 = (G <= 4) ? RingLayout<4, 2, true>::kCap : RingLayout<8, 2, true>::kCap;
     else *cap48 = *cap64 = (G <= 4) ? RingLayout<4, 2>::kCap : RingLayout<8, 2>::kCap;
     *fsub = 1;
     return;
@@ -1839,20 +1860,19 @@ static cudaError_t launch_fine_t(cudaStream_t s, const GatherArgs &A, const Fine
 size_t fine_hot_bytes() { return sizeof(FineHot); }
 size_t fine_hit_bytes() { return sizeof(Hit); }
 
-template <int GMAX, int NB>
+template <int GMAX, int NB, bool FLAT>
 static cudaError_t launch_ring_t(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int sms) {
-  using Lay = RingLayout<GMAX, NB>;
+  using Lay = RingLayout<GMAX, NB, FLAT>;
   const size_t smem = Lay::kDynBytes;
-  cudaError_t e =
-      cudaFuncSetAttribute(k_gather_ring<GMAX, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_gather_ring<GMAX, NB, FLAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
-  k_gather_ring<GMAX, NB><<<sms, kRThreads, smem, s>>>(A, T);
+  k_gather_ring<GMAX, NB, FLAT><<<sms, kRThreads, smem, s>>>(A, T);
   note_launches(1);
   return cudaGetLastError();
 }
 
-// FPPM_RING=0 selects the one-window-per-CTA kernel for lean frames (A/B);
-// FPPM_RING=3 a ring of three buffers
+// FPPM_RING=0 selects the one-window-per-CTA kernel for lean frames (A/B)
 bool ring_enabled() {
   static const bool on = [] {
     const char *e = std::getenv("FPPM_RING");
@@ -1860,22 +1880,25 @@ bool ring_enabled() {
   }();
   return on;
 }
-int ring_buffers() {
-  static const int nb = [] {
-    const char *e = std::getenv("FPPM_RING");
-    return (e && e[0] == '3') ? 3 : 2;
+// FPPM_FLAT=0 keeps 48-B lean records for frames whose photons share one z (A/B)
+bool flat_records_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("FPPM_FLAT");
+    return ring_enabled() && !(e && e[0] == '0');
   }();
-  return nb;
+  return on;
 }
 
-cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms, bool lean) {
+cudaError_t launch_gather_fine(cudaStream_t s, const GatherArgs &A, const FineArgs &T, int C, int sms, int lean) {
   const int G = A.na * A.ns;
   if (lean) {  // C = 1, n_s = 4, n_a <= 2 (lean_config)
     if (C != 1 || A.ns != 4 || A.na > 2) return cudaErrorInvalidValue;
     if (ring_enabled()) {
-      if (ring_buffers() == 3) return A.na == 1 ? launch_ring_t<4, 3>(s, A, T, sms) : launch_ring_t<8, 3>(s, A, T, sms);
-      return A.na == 1 ? launch_ring_t<4, 2>(s, A, T, sms) : launch_ring_t<8, 2>(s, A, T, sms);
+      if (lean == 2)
+        return A.na == 1 ? launch_ring_t<4, 2, true>(s, A, T, sms) : launch_ring_t<8, 2, true>(s, A, T, sms);
+      return A.na == 1 ? launch_ring_t<4, 2, false>(s, A, T, sms) : launch_ring_t<8, 2, false>(s, A, T, sms);
     }
+    if (lean == 2) return cudaErrorInvalidValue;  // flat records are staged by the ring kernel only
     return A.na == 1 ? launch_fine_t<4, 1, true>(s, A, T, sms) : launch_fine_t<8, 1, true>(s, A, T, sms);
   }
   if (C == 1) {

@@ -31,10 +31,13 @@ __device__ __forceinline__ T warp_reduce(T v, Op op) {
 // ------------------------------------------------------------------ bounds
 __global__ void __launch_bounds__(256)
     k_cell_bounds(const float *__restrict__ pos, uint32_t n, const double *__restrict__ cell_ptr,
-                  uint32_t S, long long *__restrict__ bounds /* [6]: min xyz, max xyz */) {
+                  uint32_t S, long long *__restrict__ bounds /* [8]: min xyz, max xyz, z bits min / max */) {
   const double inv = dm(dd(1.0, *cell_ptr), (double)S);  // photon_map.cpp:29, x S exactly
   long long mn[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
   long long mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+  // the photons' z as raw bit patterns (min == max <=> one bit-identical z:
+  // the flat lean layout, common.cuh)
+  uint32_t zlo = 0xffffffffu, zhi = 0u;
   // 4 photons (12 floats) per thread with 16-B loads when aligned; axis of
   // float k of a quad = k % 3
   const uint32_t nq = (reinterpret_cast<uintptr_t>(pos) & 15u) == 0u ? n / 4 : 0;
@@ -47,6 +50,10 @@ __global__ void __launch_bounds__(256)
       const long long cc = (long long)floor(dm((double)v[k], inv));
       mn[k % 3] = min(mn[k % 3], cc);
       mx[k % 3] = max(mx[k % 3], cc);
+      if (k % 3 == 2) {
+        zlo = min(zlo, __float_as_uint(v[k]));
+        zhi = max(zhi, __float_as_uint(v[k]));
+      }
     }
   }
   for (uint32_t i = 4 * nq + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -56,8 +63,12 @@ __global__ void __launch_bounds__(256)
       mn[a] = min(mn[a], c);
       mx[a] = max(mx[a], c);
     }
+    const uint32_t zb = __float_as_uint(pos[3 * (size_t)i + 2]);
+    zlo = min(zlo, zb);
+    zhi = max(zhi, zb);
   }
   __shared__ long long s[6][8];
+  __shared__ uint32_t s_z[2][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -68,7 +79,24 @@ __global__ void __launch_bounds__(256)
       s[3 + a][warp] = wmax;
     }
   }
+  {
+    const uint32_t wlo = warp_reduce(zlo, [](uint32_t x, uint32_t y) { return min(x, y); });
+    const uint32_t whi = warp_reduce(zhi, [](uint32_t x, uint32_t y) { return max(x, y); });
+    if (lane == 0) {
+      s_z[0][warp] = wlo;
+      s_z[1][warp] = whi;
+    }
+  }
   __syncthreads();
+  if (threadIdx.x == 3) {
+    uint32_t blo = 0xffffffffu, bhi = 0u;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      blo = min(blo, s_z[0][w]);
+      bhi = max(bhi, s_z[1][w]);
+    }
+    atomicMin(&bounds[6], (long long)blo);
+    atomicMax(&bounds[7], (long long)bhi);
+  }
   if (threadIdx.x < 3) {
     const int a = threadIdx.x;
     long long bmin = LLONG_MAX, bmax = LLONG_MIN;
@@ -86,11 +114,14 @@ __global__ void __launch_bounds__(256)
 // otherwise the bounds are folded back to reference cells (>> shift, exact).
 __global__ void k_grid_header(const long long *__restrict__ bounds, const double *__restrict__ cell_ptr,
                               uint32_t n, unsigned long long max_cells, uint32_t S_req,
-                              const uint32_t *__restrict__ lean_ok, GridHeader *__restrict__ hdr) {
+                              const uint32_t *__restrict__ lean_ok, int allow_flat,
+                              GridHeader *__restrict__ hdr) {
   GridHeader g;
   g.cell = *cell_ptr;
   g.n = n;
   g.lean = 0;
+  g.zflat = 0.0f;
+  g.pad_ = 0;
   uint32_t shift = 0;
   while ((1u << shift) < S_req) ++shift;
   long long b[6];
@@ -119,6 +150,10 @@ __global__ void k_grid_header(const long long *__restrict__ bounds, const double
   g.S = 1u << shift;
   g.shift = shift;
   g.lean = (shift > 0 && lean_ok != nullptr && *lean_ok != 0u) ? 1u : 0u;
+  if (g.lean != 0u && allow_flat && n > 0 && bounds[6] == bounds[7]) {  // one z: 32-B flat records
+    g.lean = 2u;
+    g.zflat = __uint_as_float((uint32_t)bounds[6]);
+  }
   g.inv = dm(dd(1.0, g.cell), (double)g.S);
   if (n == 0) {
     g.ix0 = g.iy0 = g.iz0 = 0;
@@ -197,7 +232,7 @@ __global__ void __launch_bounds__(256)
                 const GridHeader *__restrict__ hdr, double guard, float4 *__restrict__ pack) {
   __shared__ float4 s_in[4][192];
   __shared__ uint4 s_d[64];
-  const bool lean = hdr->lean != 0u;
+  const bool lean = hdr->lean != 0u, flat = hdr->lean == 2u;
   const bool vec = aligned16(pos) && aligned16(nrm) && aligned16(wi) && aligned16(pw) && aligned16(depth);
   const float *src[4] = {pos, nrm, wi, pw};
   for (uint32_t b0 = blockIdx.x * 256u; b0 < n; b0 += gridDim.x * 256u) {
@@ -227,6 +262,12 @@ __global__ void __launch_bounds__(256)
     }
     if (i < n) {
       float4 q0, q1, q2, q3;
+      if (flat) {  // flat lean records packed 32 B apart
+        flat_record(P, guard, q0, q1);
+        pack[2 * (size_t)i] = q0;
+        pack[2 * (size_t)i + 1] = q1;
+        continue;
+      }
       float4 *d = pack + (lean ? 3 : 4) * (size_t)i;  // lean records packed 48 B apart
       if (lean) {
         lean_record(P, guard, q0, q1, q2);
@@ -246,6 +287,33 @@ __global__ void __launch_bounds__(256)
                      float4 *__restrict__ rec0, float4 *__restrict__ rec1, float4 *__restrict__ rec2,
                      float4 *__restrict__ rec3, const GridHeader *__restrict__ hdr) {
   if (hdr != nullptr && hdr->lean != 0u) rec3 = nullptr;  // lean records: 48 B
+  if (hdr != nullptr && hdr->lean == 2u) {                // flat lean records: 32 B
+    constexpr uint32_t V = 6;
+    const uint32_t st = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += V * st) {
+      uint32_t o[V];
+#pragma unroll
+      for (uint32_t u = 0; u < V; ++u) o[u] = i0 + u * st < n ? __ldg(&order[i0 + u * st]) : 0u;
+      float4 q[V][2];
+#pragma unroll
+      for (uint32_t u = 0; u < V; ++u) {
+        const float4 *src = pack + 2 * (size_t)o[u];
+        if (i0 + u * st < n) {
+          q[u][0] = __ldg(&src[0]);
+          q[u][1] = __ldg(&src[1]);
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < V; ++u) {
+        const uint32_t i = i0 + u * st;
+        if (i < n) {
+          __stcs(&rec0[i], q[u][0]);
+          __stcs(&rec1[i], q[u][1]);
+        }
+      }
+    }
+    return;
+  }
   // U records per thread per round, all loads issued before the stores
   // (random 64-B record reads: latency bound without the extra parallelism)
   constexpr uint32_t U = 4;
@@ -648,8 +716,9 @@ void launch_cell_bounds(cudaStream_t s, const float *pos, uint32_t n, const doub
 }
 
 void launch_grid_header(cudaStream_t s, const long long *bounds, const double *cell, uint32_t n,
-                        unsigned long long max_cells, uint32_t S, const uint32_t *lean_ok, GridHeader *hdr) {
-  k_grid_header<<<1, 1, 0, s>>>(bounds, cell, n, max_cells, S, lean_ok, hdr);
+                        unsigned long long max_cells, uint32_t S, const uint32_t *lean_ok, bool allow_flat,
+                        GridHeader *hdr) {
+  k_grid_header<<<1, 1, 0, s>>>(bounds, cell, n, max_cells, S, lean_ok, allow_flat ? 1 : 0, hdr);
   note_launches(1);
 }
 
