@@ -423,6 +423,11 @@ int fppm_gpu_counters(fppm_gpu_ctx *ctx, uint64_t out[4]);
  * kernel of the gathers issued since the previous call (at most the last 64);
  * waits for them to finish. *n receives the count written to out. */
 int fppm_gpu_gather_kernel_ms(fppm_gpu_ctx *ctx, float *out, uint32_t max, uint32_t *n);
+/* Sorted-record layout of the current grid (bytes staged per photon by the
+ * gather): 64 = general fine records, 48 = lean records (planar gray frames),
+ * 32 = flat lean records (lean, and every photon shares one z), 0 = the grid
+ * is not built or another gather kernel's layout is in use. Diagnostic. */
+int fppm_gpu_record_bytes(const fppm_gpu_ctx *ctx);
 /* Kernel launches issued by this library since load (all contexts). */
 uint64_t fppm_gpu_kernel_launches(void);
 

@@ -167,6 +167,7 @@ _SIGS = [
                                         C.POINTER(C.c_int32)]),
     ("fppm_gpu_build_frame", C.c_int, [_dp, _dp, _dp]),
     ("fppm_gpu_kernel_launches", C.c_uint64, []),
+    ("fppm_gpu_record_bytes", C.c_int, [C.c_void_p]),
     ("fppm_gpu_gather_kernel_ms", C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_uint32, C.POINTER(C.c_uint32)]),
     ("fppm_gpu_counters", C.c_int, [C.c_void_p, C.c_void_p]),
     ("fppm_gpu_set_hitpoint_mis", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),

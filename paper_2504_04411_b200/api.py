@@ -175,6 +175,11 @@ class FppmContext:
     def kernel_launches() -> int:
         return int(N.lib().fppm_gpu_kernel_launches())
 
+    def record_bytes(self) -> int:
+        """Bytes per sorted photon record staged by the fine gather of the
+        current grid: 64 general, 48 lean, 32 flat lean, 0 other kernels."""
+        return int(self._lib.fppm_gpu_record_bytes(self._h))
+
     def gather_kernel_ms(self) -> list:
         """Durations (ms) of the dominant gather kernel of the gathers issued
         since the previous call (CUDA events on the context stream)."""

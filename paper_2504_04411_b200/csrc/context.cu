@@ -1417,6 +1417,12 @@ static int kernel_event(fppm_gpu_ctx *ctx, int which) {
   return FPPM_OK;
 }
 
+int fppm_gpu_record_bytes(const fppm_gpu_ctx *ctx) {
+  if (!ctx || !ctx->grid_valid || !ctx->h_hdr) return 0;
+  if (effective_variant(ctx, ctx->h_hdr->S) != 4) return 0;
+  return ctx->h_hdr->lean == 2u ? 32 : ctx->h_hdr->lean == 1u ? 48 : 64;
+}
+
 int fppm_gpu_gather_kernel_ms(fppm_gpu_ctx *ctx, float *out, uint32_t max, uint32_t *n) {
   if (!ctx || (max && !out)) return FPPM_ERR_INVALID_ARGUMENT;
   const uint32_t cnt = std::min(ctx->ev_count, max);

@@ -52,3 +52,35 @@ def test_iterations_match_reference_build(port, ref):
         got, _ = ctx.iterate(it, stats=True)
         want = sess.iterate(it, port.gen_photons(wl.generator, wl.seed, it, 0, wl.photons))
         compare_iteration(got, want)
+
+
+@pytest.mark.parametrize("z_mode,want_bytes", [
+    ("zero", 32),        # every photon at z = 0: flat lean records
+    ("offset", 32),      # one common non-zero z: flat records, dz != 0 in the ball test
+    ("jitter", 48),      # photons off the plane by different amounts: 48-B lean records
+    ("signed_zero", 48), # +0.0 and -0.0 are different bit patterns: not flat
+])
+def test_lean_record_layouts(port, z_mode, want_bytes):
+    """The lean fine gather stages 32-B records when every photon shares one
+    bit-identical z (common.cuh flat_record) and 48-B records otherwise; both
+    layouts give the oracle's iteration (integrator.cpp:388-402)."""
+    wl = WORKLOADS["c2"].scaled(raster=64, photons=1 << 17)
+    ctx = gpu_context(wl)
+    sess = port.session(oracle_cfg(wl), port.gen_raster_hitpoints(wl.raster))
+    rng = np.random.default_rng(11)
+    for it in range(1, 4):
+        ph = port.gen_photons(wl.generator, wl.seed, it, 0, wl.photons)
+        pos = ph["pos"].copy()
+        if z_mode == "offset":
+            pos[:, 2] = np.float32(0.0015)
+        elif z_mode == "jitter":
+            pos[:, 2] = rng.uniform(-0.004, 0.004, size=pos.shape[0]).astype(np.float32)
+        elif z_mode == "signed_zero":
+            pos[::2, 2] = np.float32(-0.0)
+        ph["pos"] = pos
+        ctx.set_photons(ph["pos"], ph["nrm"], ph["wi"], ph["pow"], ph["depth"])
+        got, summary = ctx.iterate(it, stats=True)
+        assert ctx.record_bytes() == want_bytes
+        want = sess.iterate(it, ph)
+        compare_iteration(got, want)
+        assert summary["accepted"] == int(want["accepted"].sum())
