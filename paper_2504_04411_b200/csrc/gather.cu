@@ -423,6 +423,16 @@ struct alignas(16) Hot3 {
   uint32_t h, nruns;  // runs3[q][0 .. nruns): sorted-record [begin, begin + len)
 };
 constexpr int kG3MaxRuns = 32;
+#ifndef FPPM_G3_BATCH
+#define FPPM_G3_BATCH 2  // 1: 56 / 46 / 41 ms on C5 iterations 1..3, 4: 53 / 40 / 33, 2: 47 / 37 / 32 (8 CTAs per SM)
+#endif
+#ifndef FPPM_G3_MINB
+#define FPPM_G3_MINB 10  // CTAs per SM the register cap aims at (5: 96 registers, 8: 64, 10: 48, 12: 40 and slower)
+#endif
+constexpr int kG3Batch = FPPM_G3_BATCH;  // consecutive hit points per claim
+static __device__ __forceinline__ void prefetch_l1(const void *p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 __global__ void __launch_bounds__(128) k_prep_3d(const GatherArgs A, const uint32_t *__restrict__ order,
                                                Hot3 *__restrict__ hot, HitX *__restrict__ hits,
@@ -496,6 +506,10 @@ struct G3Lay {
   static constexpr int W = NCP <= 32 ? 4 : NCP <= 64 ? 2 : 1;  // warps per CTA (shared memory)
   static constexpr int NW = (GMAX + 7) / 8;                      // 4-bit count words
   static constexpr size_t kSmem = (size_t)W * (NCP + 1) * 32 * 16;
+  // the kernel is latency bound (ncu: 58 % long-scoreboard stalls at 20 warps
+  // per SM): the register cap follows the CTAs per SM shared memory allows
+  static constexpr int kBySmem = (int)((size_t)220 * 1024 / kSmem);
+  static constexpr int kMinBlocks = kBySmem < FPPM_G3_MINB ? (kBySmem < 1 ? 1 : kBySmem) : FPPM_G3_MINB;
 };
 
 // 4-bit counts (sector 8w + k at bits 4k of nib[w]) spilled every 15 steps
@@ -511,7 +525,7 @@ static __device__ __forceinline__ void g3_spill(uint32_t (&nib)[NW], uint32_t (&
 }
 
 template <int GMAX, int CH>
-__global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
+__global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32, G3Lay<GMAX, CH>::kMinBlocks)
     k_gather_3d(const GatherArgs A, const Hot3 *__restrict__ hot, const HitX *__restrict__ hits,
                 const uint2 *__restrict__ runs, double *__restrict__ rows) {
   using L = G3Lay<GMAX, CH>;
@@ -524,11 +538,24 @@ __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
   const uint32_t slots = smem_u32(slot_base);
   const uint32_t slot_lane = slots + (uint32_t)lane * 16u;
   uint32_t my_cand = 0, my_exact = 0, my_amb = 0, my_acc = 0;
-  for (;;) {
-    uint32_t q = 0;
-    if (lane == 0) q = atomicAdd(A.work, 1u);
-    q = __shfl_sync(kFull, q, 0);
-    if (q >= A.H) break;
+  // a warp claims kG3Batch consecutive hit points (neighbours in cell order:
+  // they share their cells' records in L1) and prefetches the next one's
+  // state into L1 while it walks the current one
+  for (uint32_t q = 0, q_end = 0;; ++q) {
+    if (q == q_end) {
+      if (lane == 0) q = atomicAdd(A.work, (uint32_t)kG3Batch);
+      q = __shfl_sync(kFull, q, 0);
+      if (q >= A.H) break;
+      q_end = min(q + (uint32_t)kG3Batch, A.H);
+    }
+    if (q + 1 < q_end) {
+      const char *nh = reinterpret_cast<const char *>(hot + q + 1);
+      const char *nx = reinterpret_cast<const char *>(hits + q + 1);
+      const char *nr = reinterpret_cast<const char *>(runs + (size_t)(q + 1) * kG3MaxRuns);
+      if (lane * 128u < sizeof(Hot3) + 127u) prefetch_l1(nh + lane * 128u);
+      else if (lane >= 8 && (lane - 8) * 128u < sizeof(HitX) + 127u) prefetch_l1(nx + (lane - 8) * 128u);
+      else if (lane >= 16 && lane < 18) prefetch_l1(nr + (lane - 16) * 128u);
+    }
     const Hot3 &Hq = hot[q];
     const HitX &Hs = hits[q];  // fp64 state: exact path and pair values
     const HitF F = Hq.F;
@@ -572,10 +599,10 @@ __global__ void __launch_bounds__(G3Lay<GMAX, CH>::W * 32)
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bb = a, c2 = a, c3 = a;
       if (live) {
         a = __ldg(&A.rec0[i]);
+        bb = __ldg(&A.rec1[i]);  // rec0 and rec1 in flight together (one latency, not two)
         live = test_pair(F, a, A.max_depth);  // ball (photon_map.cpp:76), depth (:396), disk (:399)
       }
       if (live) {
-        bb = __ldg(&A.rec1[i]);
         // normal guard (integrator.cpp:397): certain rejections only
         const float gd = fmaf(bb.x, F.nfx, fmaf(bb.y, F.nfy, bb.z * F.nfz));
         const float gb = 2e-6f * (fabsf(bb.x * F.nfx) + fabsf(bb.y * F.nfy) + fabsf(bb.z * F.nfz)) + 1e-30f;
